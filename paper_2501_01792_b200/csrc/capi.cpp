@@ -1,0 +1,35 @@
+// C-ABI: library-level entry points (error reporting, device info).
+#include <cuda_runtime.h>
+
+#include <string>
+
+#include "capi_util.hpp"
+
+namespace hc {
+namespace {
+thread_local std::string g_last_error;
+}
+void set_last_error(const std::string& msg) { g_last_error = msg; }
+}  // namespace hc
+
+extern "C" {
+
+const char* hc_last_error(void) { return hc::g_last_error.c_str(); }
+
+int hc_abi_version(void) { return 1; }
+
+// Number of visible CUDA devices (0 when no GPU / driver).
+int hc_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+int hc_set_device(int dev) {
+    return hc_guard([&] { HC_CUDA(cudaSetDevice(dev)); });
+}
+
+}  // extern "C"

@@ -1,0 +1,196 @@
+#include "host/model.hpp"
+
+#include <cmath>
+#include <cstring>
+#include <thread>
+
+#include "host/errors.hpp"
+
+namespace hc {
+
+void ModelConfig::validate() {
+    if (ffn_dim == 0) ffn_dim = 4 * hidden_dim;
+    if (num_layers < 1 || hidden_dim < 1 || num_heads < 1 || vocab_size < 1 || tokens_per_block < 1 ||
+        bytes_per_scalar < 1)
+        throw InputError("ModelConfig: all counts must be >= 1");
+    if (hidden_dim % num_heads != 0) throw InputError("ModelConfig: hidden_dim must be divisible by num_heads");
+    if (ffn_dim < hidden_dim) throw InputError("ModelConfig: ffn_dim must be >= hidden_dim");
+}
+
+ModelConfig ModelConfig::preset(const std::string& name) {
+    // public OPT shapes (model.cpp:37-43); vocab 50272, 16-token blocks, fp16 bytes
+    struct P {
+        const char* n;
+        int l, d, h;
+    };
+    static const P table[] = {{"opt-6.7b", 32, 4096, 32},
+                              {"opt-13b", 40, 5120, 40},
+                              {"opt-30b", 48, 7168, 56},
+                              {"opt-66b", 64, 9216, 72}};
+    for (const P& p : table) {
+        if (name == p.n) {
+            ModelConfig c;
+            c.name = name;
+            c.num_layers = p.l;
+            c.hidden_dim = p.d;
+            c.num_heads = p.h;
+            c.ffn_dim = 4 * p.d;
+            c.vocab_size = 50272;
+            return c;
+        }
+    }
+    throw InputError("unknown model preset: " + name);
+}
+
+uint64_t mix_seed(uint64_t seed, uint64_t tag) {
+    SplitMix64 r(seed ^ (0x9e3779b97f4a7c15ULL * (tag + 1)));
+    return r.next();
+}
+
+uint16_t to_bf16(double x) {
+    const float f = static_cast<float>(x);
+    uint32_t u;
+    std::memcpy(&u, &f, 4);
+    if ((u & 0x7f800000u) == 0x7f800000u && (u & 0x007fffffu)) return static_cast<uint16_t>((u >> 16) | 0x40);
+    u += 0x7fffu + ((u >> 16) & 1u);
+    return static_cast<uint16_t>(u >> 16);
+}
+
+double from_bf16(uint16_t b) {
+    const uint32_t u = static_cast<uint32_t>(b) << 16;
+    float f;
+    std::memcpy(&f, &u, 4);
+    return f;
+}
+
+void rescale_factors(const ModelConfig& c, double out[6]) {
+    const double d = c.hidden_dim, f = c.ffn_dim;
+    const double s_attn = 10.0 * std::sqrt(3.0 / d);
+    out[0] = out[1] = out[2] = out[3] = s_attn;
+    out[4] = 10.0 * std::sqrt(3.0 * std::sqrt(2.0) / d);
+    out[5] = 10.0 * std::sqrt(3.0 * std::sqrt(2.0) / f);
+}
+
+LayerOffsets LayerOffsets::of(const ModelConfig& c) {
+    const size_t d = c.hidden_dim, f = c.ffn_dim;
+    LayerOffsets o;
+    o.wqkv = 0;
+    o.wproj = 3 * d * d;
+    o.w1 = o.wproj + d * d;
+    o.w2 = o.w1 + f * d;
+    o.total = o.w2 + d * f;
+    return o;
+}
+
+size_t HostWeights::layer_elems() const { return LayerOffsets::of(config).total; }
+
+namespace {
+
+// Draw a rows x cols U(-0.1, 0.1) matrix from stream `seed` (model.cpp:82-87)
+// and store scale * value transposed into dst[cols x rows] as bf16. The
+// counter-based generator lets threads split the draw sequence.
+void draw_transposed(uint16_t* dst, int rows, int cols, uint64_t seed, double scale) {
+    const size_t n = static_cast<size_t>(rows) * cols;
+    const unsigned hw = std::thread::hardware_concurrency();
+    const int nt = static_cast<int>(std::min<size_t>(hw ? hw : 4, std::max<size_t>(1, n / (1 << 20))));
+    auto work = [&](size_t r0, size_t r1) {
+        for (size_t r = r0; r < r1; ++r) {
+            for (int c = 0; c < cols; ++c) {
+                const size_t i = r * cols + c;
+                const uint64_t z = SplitMix64::mix(seed + (i + 1) * 0x9e3779b97f4a7c15ULL);
+                const double u = static_cast<double>(z >> 11) * 0x1.0p-53;
+                const double v = -0.1 + (0.1 - -0.1) * u;
+                dst[static_cast<size_t>(c) * rows + r] = to_bf16(v * scale);
+            }
+        }
+    };
+    if (nt <= 1) {
+        work(0, rows);
+        return;
+    }
+    std::vector<std::thread> ts;
+    for (int t = 0; t < nt; ++t)
+        ts.emplace_back(work, static_cast<size_t>(rows) * t / nt, static_cast<size_t>(rows) * (t + 1) / nt);
+    for (auto& t : ts) t.join();
+}
+
+// Same draw without transposition (embedding / positional tables).
+void draw_plain(uint16_t* dst, int rows, int cols, uint64_t seed) {
+    const size_t n = static_cast<size_t>(rows) * cols;
+    const unsigned hw = std::thread::hardware_concurrency();
+    const int nt = static_cast<int>(std::min<size_t>(hw ? hw : 4, std::max<size_t>(1, n / (1 << 20))));
+    auto work = [&](size_t i0, size_t i1) {
+        for (size_t i = i0; i < i1; ++i) {
+            const uint64_t z = SplitMix64::mix(seed + (i + 1) * 0x9e3779b97f4a7c15ULL);
+            const double u = static_cast<double>(z >> 11) * 0x1.0p-53;
+            dst[i] = to_bf16(-0.1 + (0.1 - -0.1) * u);
+        }
+    };
+    std::vector<std::thread> ts;
+    for (int t = 0; t < nt; ++t) ts.emplace_back(work, n * t / nt, n * (t + 1) / nt);
+    for (auto& t : ts) t.join();
+}
+
+}  // namespace
+
+HostWeights generate_weights(const ModelConfig& config, uint64_t seed, int max_seq, bool rescale) {
+    ModelConfig c = config;
+    c.validate();
+    if (max_seq < 1) throw InputError("DecoderWeights: max_seq must be >= 1");
+    HostWeights w;
+    w.config = c;
+    w.max_seq = max_seq;
+    const int d = c.hidden_dim, f = c.ffn_dim;
+    w.embedding.resize(static_cast<size_t>(c.vocab_size) * d);
+    w.positional.resize(static_cast<size_t>(max_seq) * d);
+    draw_plain(w.embedding.data(), c.vocab_size, d, mix_seed(seed, 0));
+    draw_plain(w.positional.data(), max_seq, d, mix_seed(seed, 1));
+    double fac[6];
+    rescale_factors(c, fac);
+    if (!rescale)
+        for (double& x : fac) x = 1.0;
+    const LayerOffsets off = LayerOffsets::of(c);
+    w.layers.resize(off.total * c.num_layers);
+    for (int l = 0; l < c.num_layers; ++l) {
+        uint16_t* L = w.layer(l);
+        const uint64_t base = 100 + static_cast<uint64_t>(l) * 8;  // model.cpp:90, 106-113
+        // Wq, Wk, Wv [d x d] -> rows [0,d), [d,2d), [2d,3d) of Wqkv^T
+        for (int k = 0; k < 3; ++k)
+            draw_transposed(L + off.wqkv + static_cast<size_t>(k) * d * d, d, d, mix_seed(seed, base + k), fac[k]);
+        draw_transposed(L + off.wproj, d, d, mix_seed(seed, base + 3), fac[3]);
+        draw_transposed(L + off.w1, d, f, mix_seed(seed, base + 4), fac[4]);
+        draw_transposed(L + off.w2, f, d, mix_seed(seed, base + 5), fac[5]);
+    }
+    return w;
+}
+
+HostWeights weights_from_f64(const ModelConfig& config, int max_seq, const double* emb, const double* pos,
+                             const double* const* layer_tensors) {
+    ModelConfig c = config;
+    c.validate();
+    HostWeights w;
+    w.config = c;
+    w.max_seq = max_seq;
+    const int d = c.hidden_dim, f = c.ffn_dim;
+    w.embedding.resize(static_cast<size_t>(c.vocab_size) * d);
+    w.positional.resize(static_cast<size_t>(max_seq) * d);
+    for (size_t i = 0; i < w.embedding.size(); ++i) w.embedding[i] = to_bf16(emb[i]);
+    for (size_t i = 0; i < w.positional.size(); ++i) w.positional[i] = to_bf16(pos[i]);
+    const LayerOffsets off = LayerOffsets::of(c);
+    w.layers.resize(off.total * c.num_layers);
+    auto put_t = [](uint16_t* dst, const double* src, int rows, int cols) {
+        for (int r = 0; r < rows; ++r)
+            for (int k = 0; k < cols; ++k) dst[static_cast<size_t>(k) * rows + r] = to_bf16(src[static_cast<size_t>(r) * cols + k]);
+    };
+    for (int l = 0; l < c.num_layers; ++l) {
+        uint16_t* L = w.layer(l);
+        const double* const* t = layer_tensors + 6 * l;
+        for (int k = 0; k < 3; ++k) put_t(L + off.wqkv + static_cast<size_t>(k) * d * d, t[k], d, d);
+        put_t(L + off.wproj, t[3], d, d);
+        put_t(L + off.w1, t[4], d, f);
+        put_t(L + off.w2, t[5], f, d);
+    }
+    return w;
+}
+
+}  // namespace hc

@@ -1,0 +1,141 @@
+// Host launcher for the tcgen05 GEMM (gemm.cuh): tensor-map encoding,
+// tile-shape heuristic and template dispatch.
+#include <cudaTypedefs.h>
+
+#include <cstdio>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+
+#include "gemm.cuh"
+#include "kernels.hpp"
+
+namespace hc {
+
+namespace {
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess || !p)
+            throw std::runtime_error("cuTensorMapEncodeTiled entry point unavailable");
+        fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    });
+    return fn;
+}
+
+// 2-D bf16 tensor [rows x cols] with row stride ld (elements); box = box_rows x 64.
+CUtensorMap make_map(const void* ptr, long long rows, long long cols, long long ld, int box_rows) {
+    CUtensorMap m;
+    cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+    cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * 2};
+    cuuint32_t box[2] = {static_cast<cuuint32_t>(gemm::BK), static_cast<cuuint32_t>(box_rows)};
+    cuuint32_t estr[2] = {1, 1};
+    const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims,
+                                   strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS)
+        throw std::runtime_error("cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) +
+                                 "): rows=" + std::to_string(rows) + " cols=" + std::to_string(cols) +
+                                 " ld=" + std::to_string(ld));
+    return m;
+}
+
+template <int BN, int EPI>
+void launch(const GemmCall& c, const gemm::Params& p, cudaStream_t st) {
+    using Cf = gemm::Cfg<BN>;
+    auto kern = gemm::gemm_tn_kernel<BN, EPI>;
+    static bool attr_set = false;  // per instantiation
+    if (!attr_set) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::kSmemBytes);
+        attr_set = true;
+    }
+    const CUtensorMap ta = make_map(c.A, c.a_rows, c.K, c.lda, gemm::BM);
+    const CUtensorMap tb = make_map(c.B, c.N, c.K, c.ldb, BN);
+    const int tiles = p.num_m_tiles * p.num_n_tiles;
+    int grid = tiles < num_sms() ? tiles : num_sms();
+    if (c.max_ctas > 0 && grid > c.max_ctas) grid = c.max_ctas;
+    kern<<<grid, gemm::kThreads, Cf::kSmemBytes, st>>>(ta, tb, p);
+}
+
+template <int BN>
+void dispatch_epi(const GemmCall& c, const gemm::Params& p, cudaStream_t st) {
+    switch (c.epi) {
+        case gemm::kStore: return launch<BN, gemm::kStore>(c, p, st);
+        case gemm::kRelu: return launch<BN, gemm::kRelu>(c, p, st);
+        case gemm::kKvPaged: return launch<BN, gemm::kKvPaged>(c, p, st);
+        case gemm::kF32: return launch<BN, gemm::kF32>(c, p, st);
+    }
+    throw std::invalid_argument("gemm: unknown epilogue");
+}
+
+int pick_bn(int num_m_tiles, int N) {
+    if (num_m_tiles >= 8) return 256;
+    // weight-streaming regime: minimise the per-CTA (A + B) tile bytes
+    const int sms = num_sms();
+    int best = 256;
+    long best_cost = -1;
+    for (int bn : {256, 128, 64, 32}) {
+        const long tiles = static_cast<long>(num_m_tiles) * ((N + bn - 1) / bn);
+        const long per_cta = (tiles + sms - 1) / sms;
+        const long cost = per_cta * (gemm::BM + bn);
+        if (best_cost < 0 || cost < best_cost) {
+            best_cost = cost;
+            best = bn;
+        }
+    }
+    return best;
+}
+
+}  // namespace
+
+int num_sms() {
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = 148;
+    }
+    return n;
+}
+
+void run_gemm(const GemmCall& c, cudaStream_t st) {
+    if (c.M <= 0 || c.N <= 0 || c.K <= 0) return;
+    if (c.N % 16 != 0) throw std::invalid_argument("gemm: N must be a multiple of 16");
+    if ((c.lda * 2) % 16 || (c.ldb * 2) % 16 || (c.K * 2) % 16)
+        throw std::invalid_argument("gemm: row strides must be 16-byte multiples");
+    if (reinterpret_cast<uintptr_t>(c.A) % 16 || reinterpret_cast<uintptr_t>(c.B) % 16)
+        throw std::invalid_argument("gemm: operands must be 16-byte aligned");
+    gemm::Params p{};
+    p.M = c.M;
+    p.N = c.N;
+    p.K = c.K;
+    p.m_tile_rows = c.m_tile_rows;
+    p.num_m_tiles = c.m_tile_rows ? c.num_m_tiles : (c.M + gemm::BM - 1) / gemm::BM;
+    if (p.num_m_tiles <= 0) return;
+    p.out = c.out;
+    p.ldc = c.ldc;
+    p.tpb = c.tpb;
+    p.d = c.d;
+    p.hd = c.hd;
+    p.blk_off = c.blk_off;
+    GemmCall cc = c;
+    if (cc.a_rows <= 0) cc.a_rows = c.M;
+    const int bn = c.bn ? c.bn : pick_bn(p.num_m_tiles, c.N);
+    p.num_n_tiles = (c.N + bn - 1) / bn;
+    switch (bn) {
+        case 32: dispatch_epi<32>(cc, p, st); break;
+        case 64: dispatch_epi<64>(cc, p, st); break;
+        case 128: dispatch_epi<128>(cc, p, st); break;
+        case 256: dispatch_epi<256>(cc, p, st); break;
+        default: throw std::invalid_argument("gemm: bn must be 32/64/128/256");
+    }
+}
+
+}  // namespace hc

@@ -1,0 +1,109 @@
+// Host-side launch API for every CUDA kernel of the hybrid-cache decode path.
+// No torch types; plain device pointers + a stream.
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace hc {
+
+using bf16 = __nv_bfloat16;
+
+// ---------------------------------------------------------------- GEMM ----
+struct GemmCall {
+    int epi = 0;                 // gemm::Epi
+    const bf16* A = nullptr;     // [a_rows x K], row stride lda (elements)
+    long long lda = 0;
+    int a_rows = 0;              // rows addressable by TMA (OOB rows read as 0)
+    const bf16* B = nullptr;     // [N x K] (weights transposed), row stride ldb
+    long long ldb = 0;
+    int M = 0, N = 0, K = 0;     // logical problem (rows >= M are not stored)
+    const int* m_tile_rows = nullptr;  // device array of explicit tile first rows
+    int num_m_tiles = 0;               // used with m_tile_rows
+    void* out = nullptr;
+    long long ldc = 0;
+    int tpb = 0, d = 0, hd = 0, blk_off = 0;  // kKvPaged
+    int bn = 0;                  // 0 = heuristic
+    int max_ctas = 0;            // 0 = all SMs
+};
+void run_gemm(const GemmCall& c, cudaStream_t st);
+int num_sms();
+
+// ----------------------------------------------------------- attention ----
+// Decode attention over the hybrid block table (north-star (3)).
+// For request b: blocks blk_ref[b*max_blocks + i], i < n_blocks[b], each a
+// packed (region << 28 | index) into one of 4 region base pointers; the last
+// block holds ctx_len[b] - (n_blocks[b]-1)*tpb tokens. Block layout:
+// [K|V][head][tpb][hd] bf16. q: [B x d] (row stride ldq), out: [B x d].
+struct AttnCall {
+    const bf16* q = nullptr;
+    long long ldq = 0;
+    bf16* out = nullptr;
+    const int* blk_ref = nullptr;
+    const int* n_blocks = nullptr;
+    const int* ctx_len = nullptr;
+    int max_blocks = 0;
+    const bf16* region[16] = {};
+    int B = 0, H = 0, hd = 0, tpb = 0;
+    float scale = 1.f;
+    // split-K workspace (fp32): [B*H*splits*(hd+2)]; nullptr -> no split
+    float* work = nullptr;
+    int splits = 1;
+};
+void decode_attention(const AttnCall& c, cudaStream_t st);
+int attention_splits(int B, int H, int max_ctx, int tpb);
+
+// Causal prefill attention: qkv [n_req*P x 3d] (Q|K|V per row) for n_req
+// requests of P tokens each; out [n_req*P x d].
+void prefill_attention(const bf16* qkv, bf16* out, int n_req, int P, int H, int hd, float scale,
+                       cudaStream_t st);
+
+// --------------------------------------------------------------- misc ----
+// X[i] = E[ids[i]] + Pos[pos[i]]   (decoder.cpp:65-95), bf16 out
+void embed(const bf16* E, const bf16* Pos, const int* ids, const int* pos, int n, int d, bf16* X,
+           long long ldx, cudaStream_t st);
+
+// Token-slot writes of the new decode token (activation-cache writer / KV
+// append, north-star (1)). Block refs are packed (region << 28 | index) into
+// region[] (device pools, staging buffers, or mapped pinned-host pools).
+// For request b:
+//   act_append: X[b] -> ACT block row slot_tok[b] of dev_ref[b] and of
+//               host_ref[b] (either may be -1 = skip). ACT layout [tpb][d].
+//   kv_append:  K|V columns of qkv[b] -> KV block token slot (layout
+//               [K|V][head][tpb][hd]) of dev_ref[b] / host_ref[b].
+struct AppendCall {
+    const bf16* src = nullptr;      // act: X [B x d]; kv: qkv [B x 3d] (K at +d, V at +2d)
+    long long ld = 0;
+    const int* dev_ref = nullptr;
+    const int* host_ref = nullptr;
+    const int* tok = nullptr;
+    bf16* region[16] = {};
+    int B = 0, d = 0, H = 0, hd = 0, tpb = 0;
+};
+void act_append(const AppendCall& c, cudaStream_t st);
+void kv_append(const AppendCall& c, cudaStream_t st);
+
+// Prefill scatter of whole blocks: block i takes rows [src_row[i],
+// src_row[i] + n_tok[i]) of src and writes them to block dst_ref[i].
+struct BlockScatter {
+    const bf16* src = nullptr;      // act: X rows [d]; kv: qkv rows [3d]
+    long long ld = 0;
+    const int* src_row = nullptr;
+    const int* n_tok = nullptr;
+    const int* dst_ref = nullptr;
+    bf16* region[16] = {};
+    int n_blocks = 0, d = 0, H = 0, hd = 0, tpb = 0;
+};
+void scatter_act_blocks(const BlockScatter& c, cudaStream_t st);
+void scatter_kv_blocks(const BlockScatter& c, cudaStream_t st);
+
+// argmax over each row of fp32 logits [B x V]
+void argmax_rows(const float* logits, int B, int V, int* out, cudaStream_t st);
+
+// fill a bf16 buffer with a deterministic hash pattern in [-a, a]
+void fill_pattern(bf16* dst, size_t n, uint64_t seed, float amp, cudaStream_t st);
+
+inline int pack_ref(int region, int index) { return (region << 28) | index; }
+
+}  // namespace hc

@@ -1,0 +1,199 @@
+// Small HBM-bound kernels of the path: embedding gather, the activation-cache
+// writer / KV append for decode tokens, prefill block scatter, argmax.
+// All move 16-byte vectors; one CTA per row / block.
+#include <cfloat>
+#include <stdexcept>
+
+#include "kernels.hpp"
+#include "ptx.cuh"
+
+namespace hc {
+
+namespace {
+
+__global__ void embed_kernel(const bf16* __restrict__ E, const bf16* __restrict__ Pos, const int* __restrict__ ids,
+                             const int* __restrict__ pos, int d, bf16* __restrict__ X, long long ldx) {
+    const int r = blockIdx.x;
+    const bf16* e = E + static_cast<long long>(ids[r]) * d;
+    const bf16* p = Pos + static_cast<long long>(pos[r]) * d;
+    bf16* x = X + r * ldx;
+    for (int c = threadIdx.x * 8; c < d; c += blockDim.x * 8) {
+        const uint4 a = *reinterpret_cast<const uint4*>(e + c);
+        const uint4 b = *reinterpret_cast<const uint4*>(p + c);
+        const __nv_bfloat162* ha = reinterpret_cast<const __nv_bfloat162*>(&a);
+        const __nv_bfloat162* hb = reinterpret_cast<const __nv_bfloat162*>(&b);
+        uint32_t o[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const float2 fa = __bfloat1622float2(ha[i]), fb = __bfloat1622float2(hb[i]);
+            o[i] = ptx::pack_bf16x2(fa.x + fb.x, fa.y + fb.y);
+        }
+        *reinterpret_cast<uint4*>(x + c) = make_uint4(o[0], o[1], o[2], o[3]);
+    }
+}
+
+__device__ __forceinline__ bf16* ref_ptr(bf16* const* region, int ref, long long block_elems) {
+    return region[ref >> 28] + static_cast<long long>(ref & 0x0FFFFFFF) * block_elems;
+}
+
+// one CTA per request: X row -> ACT block row (device and/or host pool)
+__global__ void act_append_kernel(const AppendCall c) {
+    const int b = blockIdx.x;
+    const int refs[2] = {c.dev_ref ? c.dev_ref[b] : -1, c.host_ref ? c.host_ref[b] : -1};
+    const int t = c.tok[b];
+    const long long block_elems = static_cast<long long>(c.tpb) * c.d;
+    const bf16* src = c.src + b * c.ld;
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        if (refs[k] < 0) continue;
+        bf16* dst = ref_ptr(c.region, refs[k], block_elems) + static_cast<long long>(t) * c.d;
+        for (int x = threadIdx.x * 8; x < c.d; x += blockDim.x * 8)
+            *reinterpret_cast<uint4*>(dst + x) = *reinterpret_cast<const uint4*>(src + x);
+    }
+}
+
+// one CTA per request: K|V of the new token -> its KV block slot
+__global__ void kv_append_kernel(const AppendCall c) {
+    const int b = blockIdx.x;
+    const int refs[2] = {c.dev_ref ? c.dev_ref[b] : -1, c.host_ref ? c.host_ref[b] : -1};
+    const int t = c.tok[b];
+    const long long block_elems = 2LL * c.tpb * c.d;
+    const bf16* src = c.src + b * c.ld + c.d;  // K at +d, V at +2d
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        if (refs[k] < 0) continue;
+        bf16* blk = ref_ptr(c.region, refs[k], block_elems);
+        for (int x = threadIdx.x * 8; x < 2 * c.d; x += blockDim.x * 8) {
+            const int part = x / c.d;
+            const int rem = x - part * c.d;
+            const int h = rem / c.hd;
+            const int cc = rem - h * c.hd;
+            bf16* dst = blk + static_cast<long long>(part) * c.d * c.tpb + static_cast<long long>(h) * c.tpb * c.hd +
+                        t * c.hd + cc;
+            *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(src + x);
+        }
+    }
+}
+
+// one CTA per block
+__global__ void scatter_act_kernel(const BlockScatter c) {
+    const int i = blockIdx.x;
+    const int n = c.n_tok[i];
+    const long long block_elems = static_cast<long long>(c.tpb) * c.d;
+    bf16* blk = ref_ptr(c.region, c.dst_ref[i], block_elems);
+    const bf16* src = c.src + static_cast<long long>(c.src_row[i]) * c.ld;
+    const int per_row = c.d / 8;
+    for (int idx = threadIdx.x; idx < n * per_row; idx += blockDim.x) {
+        const int t = idx / per_row, x = (idx - t * per_row) * 8;
+        *reinterpret_cast<uint4*>(blk + static_cast<long long>(t) * c.d + x) =
+            *reinterpret_cast<const uint4*>(src + t * c.ld + x);
+    }
+}
+
+__global__ void scatter_kv_kernel(const BlockScatter c) {
+    const int i = blockIdx.x;
+    const int n = c.n_tok[i];
+    const long long block_elems = 2LL * c.tpb * c.d;
+    bf16* blk = ref_ptr(c.region, c.dst_ref[i], block_elems);
+    const bf16* src = c.src + static_cast<long long>(c.src_row[i]) * c.ld + c.d;
+    // destination-major walk: consecutive threads write consecutive 16 B of a
+    // head's [tpb][hd] run
+    const int chunks_per_head = c.tpb * c.hd / 8;
+    const int total = 2 * (c.d / c.hd) * chunks_per_head;
+    for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
+        const int ph = idx / chunks_per_head;     // part*H + head
+        const int w = idx - ph * chunks_per_head;
+        const int t = (w * 8) / c.hd;
+        const int cc = (w * 8) - t * c.hd;
+        if (t >= n) continue;
+        const int part = ph / (c.d / c.hd);
+        const int h = ph - part * (c.d / c.hd);
+        const uint4 v = *reinterpret_cast<const uint4*>(src + t * c.ld + part * c.d + h * c.hd + cc);
+        *reinterpret_cast<uint4*>(blk + static_cast<long long>(ph) * c.tpb * c.hd + t * c.hd + cc) = v;
+    }
+}
+
+__global__ void argmax_kernel(const float* __restrict__ logits, int V, int* __restrict__ out) {
+    const int b = blockIdx.x;
+    const float* row = logits + static_cast<long long>(b) * V;
+    float best = -FLT_MAX;
+    int arg = 0;
+    for (int i = threadIdx.x; i < V; i += blockDim.x) {
+        const float v = row[i];
+        if (v > best) {
+            best = v;
+            arg = i;
+        }
+    }
+    __shared__ float sv[32];
+    __shared__ int si[32];
+    for (int o = 16; o >= 1; o >>= 1) {
+        const float ov = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, arg, o);
+        if (ov > best || (ov == best && oi < arg)) {
+            best = ov;
+            arg = oi;
+        }
+    }
+    const int w = threadIdx.x / 32;
+    if (threadIdx.x % 32 == 0) {
+        sv[w] = best;
+        si[w] = arg;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int k = 1; k < static_cast<int>(blockDim.x / 32); ++k)
+            if (sv[k] > best || (sv[k] == best && si[k] < arg)) {
+                best = sv[k];
+                arg = si[k];
+            }
+        out[b] = arg;
+    }
+}
+
+__global__ void fill_pattern_kernel(bf16* dst, size_t n, uint64_t seed, float amp) {
+    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        uint64_t z = seed + (i + 1) * 0x9E3779B97F4A7C15ull;
+        z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+        z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+        z ^= z >> 31;
+        const float u = static_cast<float>(z >> 40) * (1.0f / 16777216.0f);
+        dst[i] = __float2bfloat16(amp * (2.f * u - 1.f));
+    }
+}
+
+}  // namespace
+
+void embed(const bf16* E, const bf16* Pos, const int* ids, const int* pos, int n, int d, bf16* X,
+           long long ldx, cudaStream_t st) {
+    if (n <= 0) return;
+    if (d % 8) throw std::invalid_argument("embed: hidden_dim must be a multiple of 8");
+    embed_kernel<<<n, 128, 0, st>>>(E, Pos, ids, pos, d, X, ldx);
+}
+
+void act_append(const AppendCall& c, cudaStream_t st) {
+    if (c.B > 0) act_append_kernel<<<c.B, 128, 0, st>>>(c);
+}
+
+void kv_append(const AppendCall& c, cudaStream_t st) {
+    if (c.B > 0) kv_append_kernel<<<c.B, 256, 0, st>>>(c);
+}
+
+void scatter_act_blocks(const BlockScatter& c, cudaStream_t st) {
+    if (c.n_blocks > 0) scatter_act_kernel<<<c.n_blocks, 256, 0, st>>>(c);
+}
+
+void scatter_kv_blocks(const BlockScatter& c, cudaStream_t st) {
+    if (c.n_blocks > 0) scatter_kv_kernel<<<c.n_blocks, 256, 0, st>>>(c);
+}
+
+void argmax_rows(const float* logits, int B, int V, int* out, cudaStream_t st) {
+    if (B > 0) argmax_kernel<<<B, 256, 0, st>>>(logits, V, out);
+}
+
+void fill_pattern(bf16* dst, size_t n, uint64_t seed, float amp, cudaStream_t st) {
+    if (n) fill_pattern_kernel<<<4 * num_sms(), 256, 0, st>>>(dst, n, seed, amp);
+}
+
+}  // namespace hc

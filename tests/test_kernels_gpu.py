@@ -1,0 +1,158 @@
+"""Kernel parity on the B200 through the C ABI (fp64 numpy reference on the
+same bf16-rounded inputs). Tolerance: max|got-ref| / max|ref| <= 1e-2 for bf16
+outputs (north_star: 'max relative error <= 1e-2'), 1e-4 for fp32 outputs."""
+import numpy as np
+import pytest
+
+import hybridsim_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+TOL_BF16 = 1e-2
+
+
+def rel(got, ref):
+    return float(np.abs(np.asarray(got, np.float64) - ref).max() / max(np.abs(ref).max(), 1e-30))
+
+
+def rand_bits(rng, shape, scale=1.0):
+    from paper_2501_01792_b200.kernels import f32_to_bf16_bits
+    return f32_to_bf16_bits(rng.uniform(-scale, scale, size=shape))
+
+
+def f64(bits):
+    from paper_2501_01792_b200.kernels import bf16_bits_to_f32
+    return bf16_bits_to_f32(bits).astype(np.float64)
+
+
+@pytest.mark.parametrize("M,N,K,bn", [
+    (128, 128, 64, 0), (128, 256, 128, 256), (64, 768, 768, 0), (300, 512, 320, 128),
+    (130, 96, 200, 32), (128, 7168 // 8, 1024, 64), (1024, 1024, 512, 256), (2048, 512, 7168 // 4, 0),
+])
+def test_gemm_bf16_store(native, M, N, K, bn):
+    from paper_2501_01792_b200.kernels import gemm_bf16
+    rng = np.random.default_rng(M * 7 + N + K)
+    a = rand_bits(rng, (M, K))
+    wt = rand_bits(rng, (N, K), 1.0 / np.sqrt(K))
+    ref = f64(a) @ f64(wt).T
+    got = f64(gemm_bf16(a, wt, 0, bn))
+    assert rel(got, ref) <= TOL_BF16
+
+
+@pytest.mark.parametrize("bn", [32, 64, 128, 256])
+def test_gemm_relu_and_f32(native, bn):
+    from paper_2501_01792_b200.kernels import gemm_bf16
+    rng = np.random.default_rng(bn)
+    M, N, K = 200, 512, 384
+    a = rand_bits(rng, (M, K))
+    wt = rand_bits(rng, (N, K), 1.0 / np.sqrt(K))
+    ref = f64(a) @ f64(wt).T
+    got = f64(gemm_bf16(a, wt, 1, bn))
+    assert rel(got, np.maximum(ref, 0)) <= TOL_BF16
+    assert (got >= 0).all()
+    got32 = gemm_bf16(a, wt, 3, bn).astype(np.float64)
+    assert rel(got32, ref) <= 1e-4
+
+
+@pytest.mark.parametrize("d,heads,nb,tpb", [(256, 2, 20, 16), (768, 12, 9, 16), (1024, 8, 33, 8)])
+def test_recompute_kv_paged(native, d, heads, nb, tpb):
+    """recompute_kv_from_activation (decoder.cpp:123-129) into paged blocks."""
+    from paper_2501_01792_b200.kernels import recompute_kv_paged
+    rng = np.random.default_rng(d + nb)
+    act = rand_bits(rng, (nb, tpb, d))
+    wk = rand_bits(rng, (d, d), 1.0 / np.sqrt(d))   # [in x out] as in the reference
+    wv = rand_bits(rng, (d, d), 1.0 / np.sqrt(d))
+    wkv_t = np.concatenate([wk.T, wv.T], axis=0)      # [2d x d]
+    rows = nb * tpb
+    tiles = np.arange(0, rows, 128, dtype=np.int32)
+    got = f64(recompute_kv_paged(act, wkv_t, heads, tiles))
+    a = f64(act).reshape(rows, d)
+    k, v = O.recompute_kv_from_activation(a, 0, O.DecoderWeights(
+        O.ModelConfig(num_layers=1, hidden_dim=d, num_heads=heads).validate(), 1, None, None,
+        [{"w_k": f64(wk), "w_v": f64(wv)}]))
+    hd = d // heads
+    ref = np.stack([k.reshape(nb, tpb, heads, hd).transpose(0, 2, 1, 3),
+                    v.reshape(nb, tpb, heads, hd).transpose(0, 2, 1, 3)], axis=1)
+    assert got.shape == ref.shape
+    assert rel(got, ref) <= TOL_BF16
+
+
+def test_recompute_kv_paged_tile_subset(native):
+    """Only listed 128-row tiles are recomputed; other blocks stay untouched."""
+    from paper_2501_01792_b200.kernels import recompute_kv_paged
+    rng = np.random.default_rng(5)
+    d, heads, nb, tpb = 256, 2, 32, 16
+    act = rand_bits(rng, (nb, tpb, d))
+    wkv_t = rand_bits(rng, (2 * d, d), 1.0 / 16)
+    got = recompute_kv_paged(act, wkv_t, heads, np.array([256], np.int32))
+    touched = np.abs(f64(got)).reshape(nb, -1).max(axis=1) > 0
+    assert touched[16:24].all() and not touched[:16].any() and not touched[24:].any()
+
+
+def _attention_case(rng, B, H, hd, tpb, ctxs, n0=64, n1=64):
+    d = H * hd
+    q = rand_bits(rng, (B, d))
+    r0 = rand_bits(rng, (n0, 2, H, tpb, hd))
+    r1 = rand_bits(rng, (n1, 2, H, tpb, hd))
+    max_blocks = max((c + tpb - 1) // tpb for c in ctxs)
+    refs = np.full((B, max_blocks), -1, np.int32)
+    nbk = np.zeros(B, np.int32)
+    want = np.zeros((B, d))
+    pools = [f64(r0), f64(r1)]
+    for b, c in enumerate(ctxs):
+        n = (c + tpb - 1) // tpb
+        nbk[b] = n
+        ks, vs = [], []
+        for i in range(n):
+            region = int(rng.integers(0, 2))
+            idx = int(rng.integers(0, (n0, n1)[region]))
+            refs[b, i] = (region << 28) | idx
+            blk = pools[region][idx]                       # [2, H, tpb, hd]
+            ks.append(blk[0].transpose(1, 0, 2).reshape(tpb, d))
+            vs.append(blk[1].transpose(1, 0, 2).reshape(tpb, d))
+        K = np.concatenate(ks)[:c]
+        V = np.concatenate(vs)[:c]
+        want[b] = O.attention_rows(f64(q)[b:b + 1], K, V, [c], H, True)[0]
+    return q, r0, r1, refs, nbk, np.asarray(ctxs, np.int32), want
+
+
+@pytest.mark.parametrize("B,H,hd,tpb,ctxs,splits", [
+    (4, 2, 128, 16, [1, 17, 33, 160], 1),
+    (4, 12, 64, 16, [129, 144, 150, 160], 0),
+    (3, 4, 128, 8, [5, 64, 200], 2),
+    (2, 2, 64, 32, [31, 400], 4),
+    (16, 8, 128, 16, [1152] * 16, 0),
+])
+def test_decode_attention_hybrid_table(native, B, H, hd, tpb, ctxs, splits):
+    from paper_2501_01792_b200.kernels import decode_attention
+    rng = np.random.default_rng(B * 100 + H)
+    q, r0, r1, refs, nbk, cl, want = _attention_case(rng, B, H, hd, tpb, ctxs)
+    got = f64(decode_attention(q, r0, r1, refs, nbk, cl, H, True, splits))
+    assert rel(got, want) <= TOL_BF16
+
+
+def test_decode_attention_single_token_returns_v(native):
+    """test_decoder.cpp:102-107: a one-token context returns that V row."""
+    from paper_2501_01792_b200.kernels import decode_attention
+    rng = np.random.default_rng(1)
+    q, r0, r1, refs, nbk, cl, want = _attention_case(rng, 2, 2, 128, 16, [1, 1])
+    got = decode_attention(q, r0, r1, refs, nbk, cl, 2, True, 1)
+    for b in range(2):
+        idx = refs[b, 0] & 0x0FFFFFFF
+        pool = (r0, r1)[refs[b, 0] >> 28]
+        v = pool[idx, 1, :, 0, :].reshape(-1)
+        assert np.array_equal(got[b], v)
+
+
+@pytest.mark.parametrize("n_req,P,H,hd", [(2, 37, 2, 128), (3, 130, 4, 64), (1, 256, 8, 128)])
+def test_prefill_attention_causal(native, n_req, P, H, hd):
+    from paper_2501_01792_b200.kernels import prefill_attention
+    rng = np.random.default_rng(P)
+    d = H * hd
+    qkv = rand_bits(rng, (n_req * P, 3 * d))
+    got = f64(prefill_attention(qkv, n_req, P, H))
+    x = f64(qkv)
+    for r in range(n_req):
+        sl = slice(r * P, (r + 1) * P)
+        want = O.attention_rows(x[sl, :d], x[sl, d:2 * d], x[sl, 2 * d:], list(range(1, P + 1)), H, True)
+        assert rel(got[sl], want) <= TOL_BF16
