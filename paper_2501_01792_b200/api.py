@@ -1,0 +1,510 @@
+"""Python mirror of the reference engine API (hybridsim, /root/reference/proj),
+backed by the C ABI of libhybridcache_b200.so.
+
+Same names, argument meaning and error behaviour as the reference's C++
+headers: model.hpp (ModelConfig, generate), cache.hpp (HybridCache, block
+tables, bytes_of), plan.hpp / timing.hpp (next_block_kind, planner, fits),
+flops.hpp (flop_count) — plus the B200 Engine (prefill / decode-step calls
+over the hybrid cache). Errors raise InputError / CapacityError / ConfigError
+exactly where the reference throws them.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import json
+from dataclasses import dataclass, field
+from enum import IntEnum
+from typing import Dict, List, Optional, Sequence, Tuple
+
+import numpy as np
+
+from ._native import check, lib, ptr
+from ._signatures import EngineOptionsC, ModelConfigC
+from .errors import InputError
+
+
+class BlockKind(IntEnum):
+    KV = 0
+    ACT = 1
+
+    def __str__(self):
+        return self.name
+
+
+class Location(IntEnum):
+    HostMem = 0
+    GpuMem = 1
+
+    def __str__(self):
+        return "host" if self == Location.HostMem else "gpu"
+
+
+# ----------------------------------------------------------------- model ---
+@dataclass
+class ModelConfig:
+    """model.hpp:15-36"""
+    name: str = "custom"
+    num_layers: int = 1
+    hidden_dim: int = 64
+    num_heads: int = 1
+    ffn_dim: int = 0
+    vocab_size: int = 256
+    tokens_per_block: int = 16
+    bytes_per_scalar: int = 2
+    seed: int = 0
+
+    @property
+    def head_dim(self) -> int:
+        return self.hidden_dim // self.num_heads
+
+    def to_c(self) -> ModelConfigC:
+        return ModelConfigC(self.num_layers, self.hidden_dim, self.num_heads, self.ffn_dim, self.vocab_size,
+                            self.tokens_per_block, self.bytes_per_scalar)
+
+    def validate(self) -> "ModelConfig":
+        c = self.to_c()
+        check(lib().hc_model_validate(C.byref(c)))
+        self.ffn_dim = c.ffn_dim
+        return self
+
+    @classmethod
+    def preset(cls, name: str) -> "ModelConfig":
+        c = ModelConfigC()
+        check(lib().hc_model_preset(name.encode(), C.byref(c)))
+        return cls(name, c.num_layers, c.hidden_dim, c.num_heads, c.ffn_dim, c.vocab_size,
+                   c.tokens_per_block, c.bytes_per_scalar)
+
+    @staticmethod
+    def preset_names() -> List[str]:
+        return ["opt-6.7b", "opt-13b", "opt-30b", "opt-66b"]
+
+
+def generate_weights(cfg: ModelConfig, seed: int, max_seq: int, rescale: bool = True) -> Dict[str, np.ndarray]:
+    """DecoderWeights::generate (+ rescale, bf16) in device layout (bf16 bits):
+    embedding [V,d], positional [S,d], layers [L, layer_elems] packed as
+    Wqkv^T [3d,d] | Wproj^T [d,d] | W1^T [f,d] | W2^T [d,f]."""
+    cfg = ModelConfig(**cfg.__dict__).validate()
+    d, f, V, L = cfg.hidden_dim, cfg.ffn_dim, cfg.vocab_size, cfg.num_layers
+    le = 4 * d * d + 2 * d * f
+    emb = np.zeros((V, d), np.uint16)
+    pos = np.zeros((max_seq, d), np.uint16)
+    layers = np.zeros((L, le), np.uint16)
+    c = cfg.to_c()
+    check(lib().hc_generate_weights(C.byref(c), seed, max_seq, int(rescale), ptr(emb, C.c_uint16),
+                                    ptr(pos, C.c_uint16), ptr(layers, C.c_uint16)))
+    return {"embedding": emb, "positional": pos, "layers": layers}
+
+
+def unpack_layer(cfg: ModelConfig, packed: np.ndarray) -> Dict[str, np.ndarray]:
+    """Split one packed layer into reference-layout [in x out] matrices."""
+    d, f = cfg.hidden_dim, cfg.ffn_dim
+    o = 0
+    wqkv = packed[o:o + 3 * d * d].reshape(3 * d, d); o += 3 * d * d
+    wproj = packed[o:o + d * d].reshape(d, d); o += d * d
+    w1 = packed[o:o + f * d].reshape(f, d); o += f * d
+    w2 = packed[o:o + d * f].reshape(d, f)
+    return {"w_q": wqkv[:d].T, "w_k": wqkv[d:2 * d].T, "w_v": wqkv[2 * d:].T, "w_proj": wproj.T,
+            "w_ffn1": w1.T, "w_ffn2": w2.T}
+
+
+# ----------------------------------------------------------------- cache ---
+@dataclass
+class BlockTableEntry:
+    kind: BlockKind
+    location: Location
+    pbn: int
+    filled_tokens: int = 0
+
+
+@dataclass
+class BlockTable:
+    request_id: str
+    prompt_len: int
+    entries: List[BlockTableEntry] = field(default_factory=list)
+
+    def context_len(self) -> int:
+        return sum(e.filled_tokens for e in self.entries)
+
+    def blocks_by_kind(self) -> Tuple[int, int]:
+        a = sum(1 for e in self.entries if e.kind == BlockKind.ACT)
+        return a, len(self.entries) - a
+
+
+@dataclass
+class PoolCaps:
+    kv_host: int = 0
+    kv_gpu: int = 0
+    act_host: int = 0
+    act_gpu: int = 0
+
+
+def _kind(k) -> int:
+    if isinstance(k, str):
+        return 1 if k.upper() == "ACT" else 0
+    return int(k)
+
+
+def _loc(l) -> int:
+    if isinstance(l, str):
+        return 1 if l.lower() == "gpu" else 0
+    return int(l)
+
+
+class HybridCache:
+    """cache.hpp:49-95 — bit-exact block bookkeeping (C++ host code)."""
+
+    def __init__(self, tokens_per_block: int, caps: Optional[PoolCaps] = None, kv_on_gpu: bool = False,
+                 *, _borrowed: Optional[C.c_void_p] = None, _owner=None):
+        self._owner = _owner
+        if _borrowed is not None:
+            self._h, self._own = _borrowed, False
+            return
+        caps = caps or PoolCaps()
+        h = C.c_void_p()
+        check(lib().hc_cache_create(tokens_per_block, caps.kv_host, caps.kv_gpu, caps.act_host, caps.act_gpu,
+                                    int(kv_on_gpu), C.byref(h)))
+        self._h, self._own = h, True
+
+    def __del__(self):
+        if getattr(self, "_own", False) and self._h:
+            lib().hc_cache_destroy(self._h)
+            self._h = None
+
+    def create_request(self, rid: str, prompt_len: int) -> None:
+        check(lib().hc_cache_create_request(self._h, rid.encode(), prompt_len))
+
+    def append_block(self, rid: str, kind) -> BlockTableEntry:
+        loc, pbn = C.c_int(), C.c_int()
+        check(lib().hc_cache_append_block(self._h, rid.encode(), _kind(kind), C.byref(loc), C.byref(pbn)))
+        return BlockTableEntry(BlockKind(_kind(kind)), Location(loc.value), pbn.value, 0)
+
+    def fill_token(self, rid: str) -> None:
+        check(lib().hc_cache_fill_token(self._h, rid.encode()))
+
+    def free_request(self, rid: str) -> None:
+        check(lib().hc_cache_free_request(self._h, rid.encode()))
+
+    def blocks_by_kind(self, rid: str) -> Tuple[int, int]:
+        a, k = C.c_long(), C.c_long()
+        check(lib().hc_cache_blocks_by_kind(self._h, rid.encode(), C.byref(a), C.byref(k)))
+        return a.value, k.value
+
+    def context_len(self, rid: str) -> int:
+        n = C.c_int()
+        check(lib().hc_cache_context_len(self._h, rid.encode(), C.byref(n)))
+        return n.value
+
+    def table(self, rid: str) -> BlockTable:
+        n = C.c_int()
+        check(lib().hc_cache_table(self._h, rid.encode(), None, None, None, None, 0, C.byref(n)))
+        k, lo, p, f = (np.zeros(n.value, np.int32) for _ in range(4))
+        check(lib().hc_cache_table(self._h, rid.encode(), ptr(k, C.c_int), ptr(lo, C.c_int), ptr(p, C.c_int),
+                                   ptr(f, C.c_int), n.value, C.byref(n)))
+        doc = json.loads(self.dump_json())
+        plen = next(r["prompt_len"] for r in doc["requests"] if r["id"] == rid)
+        return BlockTable(rid, plen, [BlockTableEntry(BlockKind(int(a)), Location(int(b)), int(c), int(d))
+                                      for a, b, c, d in zip(k, lo, p, f)])
+
+    def free_blocks(self, kind, loc) -> int:
+        out = C.c_long()
+        check(lib().hc_cache_free_blocks(self._h, _kind(kind), _loc(loc), C.byref(out)))
+        return out.value
+
+    def capacity(self, kind, loc) -> int:
+        out = C.c_long()
+        check(lib().hc_cache_capacity(self._h, _kind(kind), _loc(loc), C.byref(out)))
+        return out.value
+
+    def dump_json(self) -> str:
+        need = C.c_long()
+        check(lib().hc_cache_dump_json(self._h, None, 0, C.byref(need)))
+        buf = C.create_string_buffer(need.value)
+        check(lib().hc_cache_dump_json(self._h, buf, need.value, C.byref(need)))
+        return buf.value.decode()
+
+    @staticmethod
+    def bytes_of(kind, cfg: ModelConfig) -> int:
+        out = C.c_uint64()
+        check(lib().hc_bytes_of(_kind(kind), cfg.hidden_dim, cfg.tokens_per_block, cfg.bytes_per_scalar,
+                                C.byref(out)))
+        return out.value
+
+
+# --------------------------------------------------------------- planner ---
+@dataclass
+class HostAllocation:
+    """plan.hpp:17-25"""
+    act_host: int = 0
+    kv_host: int = 0
+    act_init: int = 0
+    kv_init: int = 0
+    act_remain: int = 0
+    kv_remain: int = 0
+
+
+def next_block_kind(act_req: int, kv_req: int, allocation: HostAllocation) -> BlockKind:
+    """plan.cpp:154-164 — the hybrid-ratio setting."""
+    k = C.c_int()
+    check(lib().hc_next_block_kind(act_req, kv_req, allocation.act_host, allocation.kv_host, C.byref(k)))
+    return BlockKind(k.value)
+
+
+@dataclass
+class LinearTimeModel:
+    slope: float = 0.0
+    intercept: float = 0.0
+    r_squared: float = 0.0
+    intercept_clamped: bool = False
+
+
+def _darr(x):
+    a = np.ascontiguousarray(x, dtype=np.float64)
+    return a, ptr(a, C.c_double)
+
+
+def fit_linear(samples: Sequence[Tuple[float, float]]) -> LinearTimeModel:
+    """timing.cpp:38-73"""
+    xs, xp = _darr([s[0] for s in samples])
+    ys, yp = _darr([s[1] for s in samples])
+    out, op = _darr(np.zeros(4))
+    check(lib().hc_fit_linear(xp, yp, len(xs), op))
+    return LinearTimeModel(out[0], out[1], out[2], bool(out[3]))
+
+
+@dataclass
+class TimingBundle:
+    t_kv_gen: LinearTimeModel
+    t_load_kv: LinearTimeModel
+    t_load_w: float = 0.0
+    s_weight_layer: int = 0
+    s_weight_total: int = 0
+
+    def arr5(self):
+        return _darr([self.t_kv_gen.slope, self.t_kv_gen.intercept, self.t_load_kv.slope,
+                      self.t_load_kv.intercept, self.t_load_w])
+
+
+@dataclass
+class MemoryBudget:
+    m_host: float = 0.0
+    s_weight: float = 0.0
+    s_kv_block: float = 0.0
+    s_act_block: float = 0.0
+
+    def arr4(self):
+        return _darr([self.m_host, self.s_weight, self.s_kv_block, self.s_act_block])
+
+
+def bundle_from_samples(kv_gen: Sequence[Tuple[float, float]], load_kv: Sequence[Tuple[float, float]],
+                        link_bytes_per_s: float, cfg: ModelConfig) -> TimingBundle:
+    """timing.cpp:172-183, fed by measured B200 samples."""
+    kn, knp = _darr([s[0] for s in kv_gen])
+    ks, ksp = _darr([s[1] for s in kv_gen])
+    ln, lnp = _darr([s[0] for s in load_kv])
+    ls, lsp = _darr([s[1] for s in load_kv])
+    out, op = _darr(np.zeros(11))
+    c = cfg.to_c()
+    check(lib().hc_bundle_from_samples(knp, ksp, len(kn), lnp, lsp, len(ln), link_bytes_per_s, C.byref(c), op))
+    return TimingBundle(LinearTimeModel(out[0], out[1], out[2], bool(out[3])),
+                        LinearTimeModel(out[4], out[5], out[6], bool(out[7])), out[8], int(out[9]), int(out[10]))
+
+
+def budget_for(host_mem: float, cfg: ModelConfig, bundle: TimingBundle) -> MemoryBudget:
+    out, op = _darr(np.zeros(4))
+    c = cfg.to_c()
+    check(lib().hc_budget_for(host_mem, C.byref(c), float(bundle.s_weight_total), op))
+    return MemoryBudget(*out)
+
+
+def initial_cache_allocation(bundle: TimingBundle, tpb: int, act_gpu: int) -> Tuple[int, int]:
+    b, bp = bundle.arr5()
+    out = (C.c_long * 2)()
+    check(lib().hc_initial_cache_allocation(bp, tpb, act_gpu, out))
+    return out[0], out[1]
+
+
+def alloc_remaining(bundle: TimingBundle, mem: MemoryBudget, tpb: int, act_init: int, kv_init: int):
+    b, bp = bundle.arr5()
+    m, mp = mem.arr4()
+    out = (C.c_long * 2)()
+    check(lib().hc_alloc_remaining(bp, mp, tpb, act_init, kv_init, out))
+    return out[0], out[1]
+
+
+def plan_host_allocation(bundle: TimingBundle, mem: MemoryBudget, tpb: int, act_gpu: int) -> HostAllocation:
+    """plan.cpp:106-152 (paper Alg. 1 + frontier polish)."""
+    b, bp = bundle.arr5()
+    m, mp = mem.arr4()
+    out = (C.c_long * 6)()
+    check(lib().hc_plan_host_allocation(bp, mp, tpb, act_gpu, out))
+    return HostAllocation(*list(out))
+
+
+def planned_t_pcie(bundle: TimingBundle, tpb: int, a: HostAllocation) -> float:
+    b, bp = bundle.arr5()
+    out, op = _darr(np.zeros(2))
+    check(lib().hc_planned_times(bp, tpb, a.act_host, a.kv_host, 0, op))
+    return float(out[0])
+
+
+def planned_t_computation(bundle: TimingBundle, tpb: int, a: HostAllocation, act_gpu: int) -> float:
+    b, bp = bundle.arr5()
+    out, op = _darr(np.zeros(2))
+    check(lib().hc_planned_times(bp, tpb, a.act_host, a.kv_host, act_gpu, op))
+    return float(out[1])
+
+
+FLOP_KINDS = {"kv_gen": 0, "qkv_gen": 1, "attention": 2, "proj_ffn": 3, "token_recompute": 4, "full_layer": 5}
+
+
+def flop_count(kind, cfg: ModelConfig, n_tokens: int, k: int = 0) -> float:
+    out = C.c_double()
+    c = cfg.to_c()
+    check(lib().hc_flop_count(FLOP_KINDS.get(kind, kind) if isinstance(kind, str) else int(kind), C.byref(c),
+                              n_tokens, k, C.byref(out)))
+    return out.value
+
+
+def weight_bytes(cfg: ModelConfig) -> Tuple[int, int]:
+    out = (C.c_uint64 * 2)()
+    c = cfg.to_c()
+    check(lib().hc_weight_bytes(C.byref(c), out))
+    return out[0], out[1]
+
+
+# ---------------------------------------------------------------- engine ---
+MODES = {"hybrid": 0, "kv_only": 1, "act_only": 2}
+
+
+def _ids(ids: Sequence[str]):
+    arr = (C.c_char_p * len(ids))(*[s.encode() for s in ids])
+    return arr
+
+
+class Engine:
+    """B200 decode engine over the hybrid KV/ACT cache (csrc/engine.hpp).
+
+    weights: None -> DecoderWeights::generate(cfg, seed, max_seq) drawn in the
+    library (rescale=True applies the depth-stable rescale); or a dict of fp64
+    reference-layout tensors {"embedding", "positional", "layers": [{w_q..}]}.
+    """
+
+    def __init__(self, cfg: ModelConfig, *, seed: int = 42, max_seq: int = 0, rescale: bool = True,
+                 weights: Optional[dict] = None, max_batch: int = 1, weights_on_device: bool = True,
+                 caps: Optional[PoolCaps] = None, kv_on_gpu: bool = False, host_layers: int = 0,
+                 mode: str = "hybrid", allocation: Optional[HostAllocation] = None, scaled: bool = True,
+                 max_prefill_tokens: int = 0, device: int = 0):
+        self.cfg = ModelConfig(**cfg.__dict__).validate()
+        caps = caps or PoolCaps()
+        alloc = allocation or HostAllocation(1, 1)
+        if mode not in MODES:
+            raise InputError(f"unknown mode: {mode}")
+        self.opts = EngineOptionsC(max_batch, max_seq, int(weights_on_device), caps.kv_host, caps.kv_gpu,
+                                   caps.act_host, caps.act_gpu, int(kv_on_gpu), host_layers, MODES[mode],
+                                   alloc.act_host, alloc.kv_host, int(scaled), max_prefill_tokens, device)
+        self.max_batch = max_batch
+        h = C.c_void_p()
+        c = self.cfg.to_c()
+        if weights is None:
+            if max_seq < 1:
+                raise InputError("DecoderWeights: max_seq must be >= 1")
+            check(lib().hc_engine_create(C.byref(c), seed, max_seq, int(rescale), C.byref(self.opts), C.byref(h)))
+        else:
+            emb = np.ascontiguousarray(weights["embedding"], np.float64)
+            pos = np.ascontiguousarray(weights["positional"], np.float64)
+            keep = []
+            ptrs = (C.POINTER(C.c_double) * (6 * self.cfg.num_layers))()
+            names = ("w_q", "w_k", "w_v", "w_proj", "w_ffn1", "w_ffn2")
+            for l, lw in enumerate(weights["layers"]):
+                for j, nme in enumerate(names):
+                    a = np.ascontiguousarray(lw[nme], np.float64)
+                    keep.append(a)
+                    ptrs[6 * l + j] = ptr(a, C.c_double)
+            check(lib().hc_engine_create_from_f64(C.byref(c), pos.shape[0], ptr(emb, C.c_double),
+                                                  ptr(pos, C.c_double), ptrs, C.byref(self.opts), C.byref(h)))
+        self._h = h
+        ch = C.c_void_p()
+        check(lib().hc_engine_cache(self._h, C.byref(ch)))
+        self.cache = HybridCache(self.cfg.tokens_per_block, _borrowed=ch, _owner=self)
+        self._last_n = 0
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            lib().hc_engine_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def prefill(self, ids: Sequence[str], prompts: Sequence[Sequence[int]]) -> None:
+        offs = np.zeros(len(ids) + 1, np.int32)
+        offs[1:] = np.cumsum([len(p) for p in prompts])
+        toks = np.ascontiguousarray(np.concatenate([np.asarray(p, np.int32) for p in prompts])
+                                    if len(prompts) else np.zeros(0, np.int32), dtype=np.int32)
+        check(lib().hc_engine_prefill(self._h, len(ids), _ids(ids), ptr(offs, C.c_int), ptr(toks, C.c_int)))
+
+    def admit_synthetic(self, ids: Sequence[str], prompt_lens: Sequence[int], seed: int = 1) -> None:
+        lens = np.ascontiguousarray(prompt_lens, np.int32)
+        check(lib().hc_engine_admit_synthetic(self._h, len(ids), _ids(ids), ptr(lens, C.c_int), seed))
+
+    def decode_step(self, ids: Sequence[str], tokens: Sequence[int], *, want_x: bool = True,
+                    want_logits: bool = False, want_argmax: bool = False, out: Optional[dict] = None) -> dict:
+        n = len(ids)
+        toks = np.ascontiguousarray(tokens, np.int32)
+        res = out if out is not None else {}
+        if want_x and "x" not in res:
+            res["x"] = np.zeros((n, self.cfg.hidden_dim), np.uint16)
+        if want_logits and "logits" not in res:
+            res["logits"] = np.zeros((n, self.cfg.vocab_size), np.float32)
+        if want_argmax and "argmax" not in res:
+            res["argmax"] = np.zeros(n, np.int32)
+        check(lib().hc_engine_decode_step(
+            self._h, n, _ids(ids), ptr(toks, C.c_int),
+            ptr(res["x"], C.c_uint16) if want_x else None,
+            ptr(res["logits"], C.c_float) if want_logits else None,
+            ptr(res["argmax"], C.c_int) if want_argmax else None))
+        self._last_n = n
+        return res
+
+    def free_request(self, rid: str) -> None:
+        check(lib().hc_engine_free_request(self._h, rid.encode()))
+
+    def read_block(self, kind, loc, pbn: int, layer: int) -> np.ndarray:
+        d, tpb, H = self.cfg.hidden_dim, self.cfg.tokens_per_block, self.cfg.num_heads
+        if _kind(kind) == 0:
+            out = np.zeros((2, H, tpb, d // H), np.uint16)
+        else:
+            out = np.zeros((tpb, d), np.uint16)
+        check(lib().hc_engine_read_block(self._h, _kind(kind), _loc(loc), pbn, layer, ptr(out, C.c_uint16)))
+        return out
+
+    def capture_inputs(self, on: bool = True) -> None:
+        check(lib().hc_engine_capture_inputs(self._h, int(on)))
+
+    def captured_inputs(self) -> np.ndarray:
+        out = np.zeros((self.cfg.num_layers, self._last_n, self.cfg.hidden_dim), np.uint16)
+        check(lib().hc_engine_captured_inputs(self._h, ptr(out, C.c_uint16), out.size))
+        return out
+
+    def last_stats(self) -> dict:
+        out, op = _darr(np.zeros(8))
+        check(lib().hc_engine_last_stats(self._h, op))
+        keys = ("step_ms", "h2d_bytes", "d2h_bytes", "recompute_rows", "recompute_ms", "attn_ms", "gemm_ms",
+                "launches")
+        return dict(zip(keys, out.tolist()))
+
+    def time_kv_gen(self, n_tokens: int, reps: int = 5) -> float:
+        s = C.c_double()
+        check(lib().hc_engine_time_kv_gen(self._h, n_tokens, reps, C.byref(s)))
+        return s.value
+
+    def time_load_kv(self, n_tokens: int, reps: int = 5) -> float:
+        s = C.c_double()
+        check(lib().hc_engine_time_load_kv(self._h, n_tokens, reps, C.byref(s)))
+        return s.value

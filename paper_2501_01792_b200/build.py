@@ -22,7 +22,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-I" + CSRC, "-I" + os.path.join(ROOT, "include")]
 CU_FLAGS = ARCH + COMMON + ["-lineinfo", "--expt-relaxed-constexpr", "-Xptxas", "-warn-spills"]
-CPP_FLAGS = COMMON + ["-Xcompiler", "-Wall"]
+CPP_FLAGS = COMMON + ["-Xcompiler", "-Wall", "-Wno-deprecated-gpu-targets"]
 
 
 def _sources():

@@ -155,7 +155,10 @@ int hc_prefill_attention(int n_req, int P, int H, int hd, const uint16_t* qkv, i
     return hc_guard([&] {
         const int d = H * hd;
         DevBuf<uint16_t> dq(qkv, size_t(n_req) * P * 3 * d), o(size_t(n_req) * P * d);
-        prefill_attention(reinterpret_cast<const bf16*>(dq.p), reinterpret_cast<bf16*>(o.p), n_req, P, H, hd,
+        std::vector<int> cu(n_req + 1);
+        for (int r = 0; r <= n_req; ++r) cu[r] = r * P;
+        DevBuf<int> dcu(cu.data(), cu.size());
+        prefill_attention(reinterpret_cast<const bf16*>(dq.p), reinterpret_cast<bf16*>(o.p), dcu.p, n_req, P, H, hd,
                           scaled ? 1.0f / std::sqrt(static_cast<float>(hd)) : 1.0f, nullptr);
         HC_CUDA(cudaGetLastError());
         HC_CUDA(cudaDeviceSynchronize());

@@ -1,0 +1,761 @@
+#include "engine.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+#include <unordered_set>
+
+#include "capi_util.hpp"
+#include "kernels/gemm_types.hpp"
+
+namespace hc {
+
+namespace {
+
+// region ids of packed block refs (kernels.hpp: ref = region << 28 | index)
+enum Region : int {
+    R_KV_STAGE = 0,   // streamed KV/host blocks of the current layer (slot l%2)
+    R_KV_GPU = 1,     // resident KV/gpu pool, layer l
+    R_KVR = 2,        // K|V recomputed from ACT blocks this layer
+    R_ACT_STAGE = 3,  // streamed ACT/host blocks (slot l%2)
+    R_ACT_GPU = 4,    // resident ACT/gpu pool, layer l
+    R_KV_HOST = 5,    // pinned KV/host pool, physical layer l%Lp (mapped)
+    R_ACT_HOST = 6,   // pinned ACT/host pool (mapped)
+};
+
+struct Run {
+    int start, count;
+};
+
+std::vector<Run> runs_of(std::vector<int> pbns) {
+    std::sort(pbns.begin(), pbns.end());
+    pbns.erase(std::unique(pbns.begin(), pbns.end()), pbns.end());
+    std::vector<Run> r;
+    for (int p : pbns) {
+        if (!r.empty() && r.back().start + r.back().count == p)
+            ++r.back().count;
+        else
+            r.push_back({p, 1});
+    }
+    return r;
+}
+
+// first pool rows of the 128-row GEMM tiles touching the listed blocks
+std::vector<int> tiles_of(const std::vector<int>& pbns, int tpb) {
+    std::vector<int> t;
+    for (int p : pbns) {
+        const long r0 = static_cast<long>(p) * tpb, r1 = r0 + tpb - 1;
+        for (long r = r0 / gemm::BM; r <= r1 / gemm::BM; ++r) t.push_back(static_cast<int>(r * gemm::BM));
+    }
+    std::sort(t.begin(), t.end());
+    t.erase(std::unique(t.begin(), t.end()), t.end());
+    return t;
+}
+
+template <class T>
+T* dalloc(size_t n) {
+    if (!n) return nullptr;
+    void* p = nullptr;
+    HC_CUDA(cudaMalloc(&p, n * sizeof(T)));
+    return static_cast<T*>(p);
+}
+
+template <class T>
+T* halloc(size_t n, bool mapped) {
+    if (!n) return nullptr;
+    void* p = nullptr;
+    HC_CUDA(cudaHostAlloc(&p, n * sizeof(T), cudaHostAllocPortable | (mapped ? cudaHostAllocMapped : 0)));
+    return static_cast<T*>(p);
+}
+
+}  // namespace
+
+struct Engine::Impl {
+    int L = 0, d = 0, H = 0, hd = 0, f = 0, V = 0, tpb = 0, B = 0, max_seq = 0, max_blocks = 0, Lp = 0;
+    size_t LE = 0, kvb = 0, actb = 0;
+    LayerOffsets off{};
+    bf16 *emb = nullptr, *pos = nullptr;
+    bf16* w_all = nullptr;
+    bf16* wbuf[2] = {nullptr, nullptr};
+    uint16_t* h_w = nullptr;
+    bf16 *kv_gpu = nullptr, *act_gpu = nullptr, *kvr = nullptr;
+    bf16 *kv_stage[2] = {nullptr, nullptr}, *act_stage[2] = {nullptr, nullptr};
+    bf16 *kv_host = nullptr, *act_host = nullptr;  // pinned, mapped
+    long kv_host_cap = 0, kv_gpu_cap = 0, act_host_cap = 0, act_gpu_cap = 0;
+    bf16 *x[2] = {nullptr, nullptr}, *qkv = nullptr, *att = nullptr, *proj = nullptr, *hbuf = nullptr;
+    float* logits = nullptr;
+    int* amax = nullptr;
+    float* attn_work = nullptr;
+    size_t attn_work_elems = 0;
+    int* d_meta = nullptr;
+    int* h_meta = nullptr;
+    size_t meta_cap = 0;
+    // prefill scratch
+    bf16 *px[2] = {nullptr, nullptr}, *pqkv = nullptr, *patt = nullptr, *pproj = nullptr, *ph = nullptr;
+    size_t prefill_rows = 0;
+    cudaEvent_t loaded[2]{}, consumed[2]{}, ev0{}, ev1{};
+    bool pools_filled = false;
+
+    void regions(int l, int slot, bf16* r[16]) const {
+        for (int i = 0; i < 16; ++i) r[i] = nullptr;
+        r[R_KV_STAGE] = kv_stage[slot];
+        r[R_KV_GPU] = kv_gpu ? kv_gpu + static_cast<size_t>(l) * kv_gpu_cap * kvb : nullptr;
+        r[R_KVR] = kvr;
+        r[R_ACT_STAGE] = act_stage[slot];
+        r[R_ACT_GPU] = act_gpu ? act_gpu + static_cast<size_t>(l) * act_gpu_cap * actb : nullptr;
+        r[R_KV_HOST] = kv_host ? kv_host + static_cast<size_t>(l % Lp) * kv_host_cap * kvb : nullptr;
+        r[R_ACT_HOST] = act_host ? act_host + static_cast<size_t>(l % Lp) * act_host_cap * actb : nullptr;
+    }
+    const bf16* layer_w(int l, int slot) const { return w_all ? w_all + static_cast<size_t>(l) * LE : wbuf[slot]; }
+
+    void ensure_meta(size_t ints) {
+        if (ints <= meta_cap) return;
+        if (d_meta) cudaFree(d_meta);
+        if (h_meta) cudaFreeHost(h_meta);
+        meta_cap = ints + ints / 2 + 1024;
+        d_meta = dalloc<int>(meta_cap);
+        h_meta = halloc<int>(meta_cap, false);
+    }
+    void ensure_attn_work(size_t elems) {
+        if (elems <= attn_work_elems) return;
+        if (attn_work) cudaFree(attn_work);
+        attn_work_elems = elems;
+        attn_work = dalloc<float>(elems);
+    }
+    void ensure_prefill(size_t rows) {
+        if (rows <= prefill_rows) return;
+        for (bf16* p : {px[0], px[1], pqkv, patt, pproj, ph})
+            if (p) cudaFree(p);
+        prefill_rows = rows;
+        px[0] = dalloc<bf16>(rows * d);
+        px[1] = dalloc<bf16>(rows * d);
+        pqkv = dalloc<bf16>(rows * 3 * d);
+        patt = dalloc<bf16>(rows * d);
+        pproj = dalloc<bf16>(rows * d);
+        ph = dalloc<bf16>(rows * f);
+    }
+};
+
+namespace {
+struct HostWeightsCtx {
+    const HostWeights* w;
+};
+void fill_from_hostweights(const void* ctx, int l, uint16_t* dst) {
+    const HostWeights* w = static_cast<const HostWeightsCtx*>(ctx)->w;
+    std::memcpy(dst, w->layer(l), w->layer_elems() * 2);
+}
+struct GenCtx {
+    ModelConfig c;
+    uint64_t seed;
+    bool rescale;
+};
+void fill_from_generator(const void* ctx, int l, uint16_t* dst) {
+    const GenCtx* g = static_cast<const GenCtx*>(ctx);
+    generate_layer(g->c, g->seed, l, g->rescale, dst);
+}
+}  // namespace
+
+Engine::Engine(const HostWeights& w, const EngineOptions& o) : opt_(o) {
+    HostWeightsCtx ctx{&w};
+    init(w.config, w.max_seq, w.embedding.data(), w.positional.data(), fill_from_hostweights, &ctx);
+}
+
+Engine::Engine(const ModelConfig& c, uint64_t seed, int max_seq, bool rescale, const EngineOptions& o) : opt_(o) {
+    ModelConfig cc = c;
+    cc.validate();
+    if (max_seq < 1) throw InputError("DecoderWeights: max_seq must be >= 1");
+    std::vector<uint16_t> emb(static_cast<size_t>(cc.vocab_size) * cc.hidden_dim);
+    std::vector<uint16_t> pos(static_cast<size_t>(max_seq) * cc.hidden_dim);
+    generate_tables(cc, seed, max_seq, emb.data(), pos.data());
+    GenCtx g{cc, seed, rescale};
+    init(cc, max_seq, emb.data(), pos.data(), fill_from_generator, &g);
+}
+
+void Engine::init(const ModelConfig& c, int w_max_seq, const uint16_t* emb, const uint16_t* pos,
+                  void (*fill_layer)(const void*, int, uint16_t*), const void* ctx) {
+    cfg_ = c;
+    cfg_.validate();
+    impl_ = std::make_unique<Impl>();
+    Impl& m = *impl_;
+    if (cfg_.hidden_dim % 64) throw InputError("Engine: hidden_dim must be a multiple of 64");
+    if (cfg_.head_dim() != 64 && cfg_.head_dim() != 128) throw InputError("Engine: head_dim must be 64 or 128");
+    if (cfg_.ffn_dim % 64) throw InputError("Engine: ffn_dim must be a multiple of 64");
+    if (cfg_.vocab_size % 16) throw InputError("Engine: vocab_size must be a multiple of 16");
+    if (opt_.mode == CacheMode::TokenRecompute)
+        throw ConfigError("Engine: token_recompute mode is modelled by the planner only (not executed)");
+    if (opt_.max_batch < 1) throw InputError("Engine: max_batch must be >= 1");
+    HC_CUDA(cudaSetDevice(opt_.device));
+    m.L = cfg_.num_layers;
+    m.d = cfg_.hidden_dim;
+    m.H = cfg_.num_heads;
+    m.hd = cfg_.head_dim();
+    m.f = cfg_.ffn_dim;
+    m.V = cfg_.vocab_size;
+    m.tpb = cfg_.tokens_per_block;
+    m.B = opt_.max_batch;
+    m.max_seq = opt_.max_seq > 0 ? std::min(opt_.max_seq, w_max_seq) : w_max_seq;
+    m.max_blocks = (m.max_seq + m.tpb - 1) / m.tpb;
+    m.Lp = opt_.host_layers > 0 ? std::min(opt_.host_layers, m.L) : m.L;
+    m.off = LayerOffsets::of(cfg_);
+    m.LE = m.off.total;
+    m.kvb = static_cast<size_t>(2) * m.d * m.tpb;
+    m.actb = static_cast<size_t>(m.d) * m.tpb;
+    m.kv_host_cap = opt_.kv_host_cap;
+    m.kv_gpu_cap = opt_.kv_gpu_cap;
+    m.act_host_cap = opt_.act_host_cap;
+    m.act_gpu_cap = opt_.act_gpu_cap;
+
+    cache_ = std::make_unique<HybridCache>(m.tpb, PoolCaps{m.kv_host_cap, m.kv_gpu_cap, m.act_host_cap, m.act_gpu_cap},
+                                           opt_.kv_on_gpu != 0);
+    assigner_ = std::make_unique<BlockAssigner>(*cache_, opt_.mode, opt_.alloc, opt_.recompute_ratio);
+    if (opt_.mode == CacheMode::Hybrid && opt_.alloc.act_host + opt_.alloc.kv_host <= 0)
+        throw ConfigError("Engine: hybrid mode needs a nonempty host allocation (ratio target)");
+
+    HC_CUDA(cudaStreamCreateWithFlags(&s_compute_, cudaStreamNonBlocking));
+    HC_CUDA(cudaStreamCreateWithFlags(&s_copy_, cudaStreamNonBlocking));
+    for (int i = 0; i < 2; ++i) {
+        HC_CUDA(cudaEventCreateWithFlags(&m.loaded[i], cudaEventDisableTiming));
+        HC_CUDA(cudaEventCreateWithFlags(&m.consumed[i], cudaEventDisableTiming));
+    }
+    HC_CUDA(cudaEventCreate(&m.ev0));
+    HC_CUDA(cudaEventCreate(&m.ev1));
+
+    // tables
+    m.emb = dalloc<bf16>(static_cast<size_t>(m.V) * m.d);
+    m.pos = dalloc<bf16>(static_cast<size_t>(w_max_seq) * m.d);
+    HC_CUDA(cudaMemcpy(m.emb, emb, static_cast<size_t>(m.V) * m.d * 2, cudaMemcpyHostToDevice));
+    HC_CUDA(cudaMemcpy(m.pos, pos, static_cast<size_t>(w_max_seq) * m.d * 2, cudaMemcpyHostToDevice));
+
+    // weights
+    if (opt_.weights_on_device) {
+        m.w_all = dalloc<bf16>(m.LE * m.L);
+        std::vector<uint16_t> tmp(m.LE);
+        for (int l = 0; l < m.L; ++l) {
+            fill_layer(ctx, l, tmp.data());
+            HC_CUDA(cudaMemcpy(m.w_all + static_cast<size_t>(l) * m.LE, tmp.data(), m.LE * 2, cudaMemcpyHostToDevice));
+        }
+    } else {
+        m.h_w = halloc<uint16_t>(m.LE * m.L, false);
+        for (int l = 0; l < m.L; ++l) fill_layer(ctx, l, m.h_w + static_cast<size_t>(l) * m.LE);
+        m.wbuf[0] = dalloc<bf16>(m.LE);
+        m.wbuf[1] = dalloc<bf16>(m.LE);
+    }
+
+    // pools
+    m.kv_gpu = dalloc<bf16>(static_cast<size_t>(m.L) * m.kv_gpu_cap * m.kvb);
+    m.act_gpu = dalloc<bf16>(static_cast<size_t>(m.L) * m.act_gpu_cap * m.actb);
+    m.kv_host = halloc<bf16>(static_cast<size_t>(m.Lp) * m.kv_host_cap * m.kvb, true);
+    m.act_host = halloc<bf16>(static_cast<size_t>(m.Lp) * m.act_host_cap * m.actb, true);
+    for (int s = 0; s < 2; ++s) {
+        m.kv_stage[s] = dalloc<bf16>(static_cast<size_t>(m.kv_host_cap) * m.kvb);
+        m.act_stage[s] = dalloc<bf16>(static_cast<size_t>(m.act_host_cap) * m.actb);
+    }
+    m.kvr = dalloc<bf16>(static_cast<size_t>(m.act_gpu_cap + m.act_host_cap) * m.kvb);
+
+    // decode scratch
+    m.x[0] = dalloc<bf16>(static_cast<size_t>(m.B) * m.d);
+    m.x[1] = dalloc<bf16>(static_cast<size_t>(m.B) * m.d);
+    m.qkv = dalloc<bf16>(static_cast<size_t>(m.B) * 3 * m.d);
+    m.att = dalloc<bf16>(static_cast<size_t>(m.B) * m.d);
+    m.proj = dalloc<bf16>(static_cast<size_t>(m.B) * m.d);
+    m.hbuf = dalloc<bf16>(static_cast<size_t>(m.B) * m.f);
+    m.logits = dalloc<float>(static_cast<size_t>(m.B) * m.V);
+    m.amax = dalloc<int>(m.B);
+    HC_CUDA(cudaDeviceSynchronize());
+}
+
+Engine::~Engine() {
+    if (!impl_) return;
+    Impl& m = *impl_;
+    cudaDeviceSynchronize();
+    for (void* p : {(void*)m.emb, (void*)m.pos, (void*)m.w_all, (void*)m.wbuf[0], (void*)m.wbuf[1], (void*)m.kv_gpu,
+                    (void*)m.act_gpu, (void*)m.kvr, (void*)m.kv_stage[0], (void*)m.kv_stage[1], (void*)m.act_stage[0],
+                    (void*)m.act_stage[1], (void*)m.x[0], (void*)m.x[1], (void*)m.qkv, (void*)m.att, (void*)m.proj,
+                    (void*)m.hbuf, (void*)m.logits, (void*)m.amax, (void*)m.attn_work, (void*)m.d_meta,
+                    (void*)m.px[0], (void*)m.px[1], (void*)m.pqkv, (void*)m.patt, (void*)m.pproj, (void*)m.ph})
+        if (p) cudaFree(p);
+    for (void* p : {(void*)m.h_w, (void*)m.kv_host, (void*)m.act_host, (void*)m.h_meta})
+        if (p) cudaFreeHost(p);
+    for (int i = 0; i < 2; ++i) {
+        cudaEventDestroy(m.loaded[i]);
+        cudaEventDestroy(m.consumed[i]);
+    }
+    cudaEventDestroy(m.ev0);
+    cudaEventDestroy(m.ev1);
+    cudaStreamDestroy(s_compute_);
+    cudaStreamDestroy(s_copy_);
+}
+
+// ---------------------------------------------------------------------------
+// GEMM helpers (weights transposed [out][in]; see model.hpp)
+namespace {
+void gemm_rows(int epi, const bf16* A, int M, int K, const bf16* W, int N, void* out, long long ldc, cudaStream_t st,
+               long long lda = 0) {
+    GemmCall c;
+    c.epi = epi;
+    c.A = A;
+    c.lda = lda ? lda : K;
+    c.a_rows = M;
+    c.B = W;
+    c.ldb = K;
+    c.M = M;
+    c.N = N;
+    c.K = K;
+    c.out = out;
+    c.ldc = ldc;
+    run_gemm(c, st);
+}
+}  // namespace
+
+// ---------------------------------------------------------------------------
+void Engine::prefill(const std::vector<std::string>& ids, const std::vector<std::vector<int>>& prompts) {
+    Impl& m = *impl_;
+    if (ids.size() != prompts.size()) throw InputError("prefill: ids and prompts differ in length");
+    for (size_t r = 0; r < ids.size(); ++r) {
+        if (cache_->has_request(ids[r])) throw InputError("duplicate request id: " + ids[r]);
+        if (static_cast<int>(prompts[r].size()) > m.max_seq) throw InputError("embed: sequence longer than max_seq");
+        for (int t : prompts[r])
+            if (t < 0 || t >= m.V) throw InputError("embed: token id out of range: " + std::to_string(t));
+    }
+    size_t r0 = 0;
+    while (r0 < ids.size()) {
+        // chunk of requests with <= max_prefill_tokens rows (at least one request)
+        size_t r1 = r0;
+        size_t rows = 0;
+        while (r1 < ids.size() && (r1 == r0 || rows + prompts[r1].size() <= static_cast<size_t>(opt_.max_prefill_tokens))) {
+            rows += prompts[r1].size();
+            ++r1;
+        }
+        const int n = static_cast<int>(r1 - r0);
+        // bookkeeping: blocks chosen by the ratio policy, prompt tokens
+        // request by request (sim.cpp:222-223)
+        std::vector<int> tokens, positions, cu(1, 0);
+        std::vector<int> a_src, a_n, a_ref, k_src, k_n, k_ref;
+        int max_len = 0;
+        for (size_t r = r0; r < r1; ++r) {
+            assigner_->add_request(ids[r], static_cast<int>(prompts[r].size()));
+            const int base = cu.back();
+            for (size_t t = 0; t < prompts[r].size(); ++t) {
+                tokens.push_back(prompts[r][t]);
+                positions.push_back(static_cast<int>(t));
+                assigner_->add_token(ids[r]);
+            }
+            const BlockTable& tb = cache_->table(ids[r]);
+            int row = base;
+            for (const auto& e : tb.entries) {
+                const bool gpu = e.location == Location::GpuMem;
+                if (e.kind == BlockKind::ACT) {
+                    a_src.push_back(row);
+                    a_n.push_back(e.filled_tokens);
+                    a_ref.push_back(pack_ref(gpu ? R_ACT_GPU : R_ACT_HOST, e.pbn));
+                } else {
+                    k_src.push_back(row);
+                    k_n.push_back(e.filled_tokens);
+                    k_ref.push_back(pack_ref(gpu ? R_KV_GPU : R_KV_HOST, e.pbn));
+                }
+                row += e.filled_tokens;
+            }
+            cu.push_back(base + static_cast<int>(prompts[r].size()));
+            max_len = std::max<int>(max_len, static_cast<int>(prompts[r].size()));
+        }
+        const int T = cu.back();
+        if (T == 0) {
+            r0 = r1;
+            continue;
+        }
+        m.ensure_prefill(T);
+        // metadata: tokens | positions | cu | a_src | a_n | a_ref | k_src | k_n | k_ref
+        std::vector<int> meta;
+        auto put = [&](const std::vector<int>& v) {
+            const size_t o = meta.size();
+            meta.insert(meta.end(), v.begin(), v.end());
+            return o;
+        };
+        const size_t o_tok = put(tokens), o_pos = put(positions), o_cu = put(cu), o_as = put(a_src), o_an = put(a_n),
+                     o_ar = put(a_ref), o_ks = put(k_src), o_kn = put(k_n), o_kr = put(k_ref);
+        m.ensure_meta(meta.size());
+        std::memcpy(m.h_meta, meta.data(), meta.size() * 4);
+        HC_CUDA(cudaMemcpyAsync(m.d_meta, m.h_meta, meta.size() * 4, cudaMemcpyHostToDevice, s_compute_));
+        const int* dm = m.d_meta;
+        embed(m.emb, m.pos, dm + o_tok, dm + o_pos, T, m.d, m.px[0], m.d, s_compute_);
+        for (int l = 0; l < m.L; ++l) {
+            const int slot = l & 1;
+            if (!m.w_all) {
+                HC_CUDA(cudaStreamWaitEvent(s_copy_, m.consumed[slot]));
+                HC_CUDA(cudaMemcpyAsync(m.wbuf[slot], m.h_w + static_cast<size_t>(l) * m.LE, m.LE * 2,
+                                        cudaMemcpyHostToDevice, s_copy_));
+                HC_CUDA(cudaEventRecord(m.loaded[slot], s_copy_));
+                HC_CUDA(cudaStreamWaitEvent(s_compute_, m.loaded[slot]));
+            }
+            const bf16* W = m.layer_w(l, slot);
+            bf16* R[16];
+            m.regions(l, slot, R);
+            bf16* xin = m.px[l & 1];
+            bf16* xout = m.px[(l + 1) & 1];
+            // activation-cache writer: this layer's input rows of ACT blocks
+            BlockScatter sa;
+            sa.src = xin;
+            sa.ld = m.d;
+            sa.src_row = dm + o_as;
+            sa.n_tok = dm + o_an;
+            sa.dst_ref = dm + o_ar;
+            std::copy(R, R + 16, sa.region);
+            sa.n_blocks = static_cast<int>(a_src.size());
+            sa.d = m.d;
+            sa.H = m.H;
+            sa.hd = m.hd;
+            sa.tpb = m.tpb;
+            scatter_act_blocks(sa, s_compute_);
+            gemm_rows(gemm::kStore, xin, T, m.d, W + m.off.wqkv, 3 * m.d, m.pqkv, 3 * m.d, s_compute_);
+            BlockScatter sk = sa;
+            sk.src = m.pqkv;
+            sk.ld = 3 * m.d;
+            sk.src_row = dm + o_ks;
+            sk.n_tok = dm + o_kn;
+            sk.dst_ref = dm + o_kr;
+            sk.n_blocks = static_cast<int>(k_src.size());
+            scatter_kv_blocks(sk, s_compute_);
+            prefill_attention(m.pqkv, m.patt, dm + o_cu, n, max_len, m.H, m.hd,
+                              opt_.scaled ? 1.0f / std::sqrt(static_cast<float>(m.hd)) : 1.0f, s_compute_);
+            gemm_rows(gemm::kStore, m.patt, T, m.d, W + m.off.wproj, m.d, m.pproj, m.d, s_compute_);
+            gemm_rows(gemm::kRelu, m.pproj, T, m.d, W + m.off.w1, m.f, m.ph, m.f, s_compute_);
+            gemm_rows(gemm::kStore, m.ph, T, m.f, W + m.off.w2, m.d, xout, m.d, s_compute_);
+            HC_CUDA(cudaEventRecord(m.consumed[slot], s_compute_));
+        }
+        HC_CUDA(cudaGetLastError());
+        HC_CUDA(cudaStreamSynchronize(s_compute_));
+        r0 = r1;
+    }
+}
+
+void Engine::admit_synthetic(const std::vector<std::string>& ids, const std::vector<int>& prompt_lens, uint64_t seed) {
+    Impl& m = *impl_;
+    if (ids.size() != prompt_lens.size()) throw InputError("admit_synthetic: ids and lengths differ");
+    for (size_t r = 0; r < ids.size(); ++r) {
+        if (prompt_lens[r] > m.max_seq) throw InputError("embed: sequence longer than max_seq");
+        assigner_->add_request(ids[r], prompt_lens[r]);
+        for (int t = 0; t < prompt_lens[r]; ++t) assigner_->add_token(ids[r]);
+    }
+    if (m.pools_filled) return;
+    // activations ~U(-0.1,0.1) like the embeddings; K,V of matching scale
+    auto fill = [&](bf16* p, size_t n, uint64_t s) {
+        if (p && n) fill_pattern(p, n, s, 0.1f, s_compute_);
+    };
+    fill(m.kv_gpu, static_cast<size_t>(m.L) * m.kv_gpu_cap * m.kvb, seed + 1);
+    fill(m.act_gpu, static_cast<size_t>(m.L) * m.act_gpu_cap * m.actb, seed + 2);
+    fill(m.kv_host, static_cast<size_t>(m.Lp) * m.kv_host_cap * m.kvb, seed + 3);
+    fill(m.act_host, static_cast<size_t>(m.Lp) * m.act_host_cap * m.actb, seed + 4);
+    HC_CUDA(cudaGetLastError());
+    HC_CUDA(cudaStreamSynchronize(s_compute_));
+    m.pools_filled = true;
+}
+
+void Engine::free_request(const std::string& id) { cache_->free_request(id); }
+
+// ---------------------------------------------------------------------------
+void Engine::decode_step(const std::vector<std::string>& ids, const int* tokens, uint16_t* x_out, float* logits_out,
+                         int* argmax_out) {
+    Impl& m = *impl_;
+    const int n = static_cast<int>(ids.size());
+    if (n == 0) return;
+    if (n > m.B) throw InputError("decode_step: batch larger than max_batch");
+    std::vector<int> pos(n);
+    {
+        std::unordered_set<std::string> seen;
+        for (int b = 0; b < n; ++b) {
+            if (!seen.insert(ids[b]).second) throw InputError("decode_step: duplicate request id " + ids[b]);
+            if (tokens[b] < 0 || tokens[b] >= m.V)
+                throw InputError("embed: token id out of range: " + std::to_string(tokens[b]));
+            pos[b] = cache_->table(ids[b]).context_len();  // throws InputError for unknown ids
+            if (pos[b] >= m.max_seq) throw InputError("embed: position exceeds max_seq: " + std::to_string(pos[b]));
+        }
+    }
+    // grow every context by this step's token (sim.cpp:308-310)
+    std::vector<int> act_dev(n, -1), act_host(n, -1), kv_dev(n, -1), kv_host(n, -1), tok(n, 0), nblk(n), ctx(n);
+    std::vector<int> refs(static_cast<size_t>(n) * m.max_blocks, 0);
+    std::vector<int> kvh_pbns, acth_pbns, actg_pbns;
+    bool any_act = false, any_kv = false;
+    for (int b = 0; b < n; ++b) {
+        const TokenSlot s = assigner_->add_token(ids[b]);
+        const BlockTableEntry& e = s.entry;
+        const bool gpu = e.location == Location::GpuMem;
+        tok[b] = s.token_index;
+        if (e.kind == BlockKind::ACT) {
+            any_act = true;
+            act_dev[b] = pack_ref(gpu ? R_ACT_GPU : R_ACT_STAGE, e.pbn);
+            if (!gpu) act_host[b] = pack_ref(R_ACT_HOST, e.pbn);
+        } else {
+            any_kv = true;
+            kv_dev[b] = pack_ref(gpu ? R_KV_GPU : R_KV_STAGE, e.pbn);
+            if (!gpu) kv_host[b] = pack_ref(R_KV_HOST, e.pbn);
+        }
+        const BlockTable& t = cache_->table(ids[b]);
+        nblk[b] = static_cast<int>(t.entries.size());
+        ctx[b] = t.context_len();
+        int* rb = refs.data() + static_cast<size_t>(b) * m.max_blocks;
+        for (size_t i = 0; i < t.entries.size(); ++i) {
+            const auto& en = t.entries[i];
+            const bool g = en.location == Location::GpuMem;
+            if (en.kind == BlockKind::KV) {
+                rb[i] = pack_ref(g ? R_KV_GPU : R_KV_STAGE, en.pbn);
+                if (!g) kvh_pbns.push_back(en.pbn);
+            } else {
+                rb[i] = pack_ref(R_KVR, g ? en.pbn : static_cast<int>(m.act_gpu_cap) + en.pbn);
+                (g ? actg_pbns : acth_pbns).push_back(en.pbn);
+            }
+        }
+    }
+    const std::vector<Run> kv_runs = runs_of(kvh_pbns);
+    const std::vector<Run> act_runs = runs_of(acth_pbns);
+    const std::vector<int> tiles_h = tiles_of(acth_pbns, m.tpb);
+    const std::vector<int> tiles_g = tiles_of(actg_pbns, m.tpb);
+    const int max_ctx = *std::max_element(ctx.begin(), ctx.end());
+    const int splits = attention_splits(n, m.H, max_ctx, m.tpb);
+    if (splits > 1) m.ensure_attn_work(static_cast<size_t>(n) * m.H * splits * (m.hd + 2));
+
+    // one upload of all step metadata
+    std::vector<int> meta;
+    auto put = [&](const std::vector<int>& v) {
+        const size_t o = meta.size();
+        meta.insert(meta.end(), v.begin(), v.end());
+        return o;
+    };
+    const size_t o_tok = put(std::vector<int>(tokens, tokens + n)), o_pos = put(pos), o_ad = put(act_dev),
+                 o_ah = put(act_host), o_kd = put(kv_dev), o_kh = put(kv_host), o_t = put(tok), o_nb = put(nblk),
+                 o_ctx = put(ctx), o_ref = put(refs), o_th = put(tiles_h), o_tg = put(tiles_g);
+    m.ensure_meta(meta.size());
+    std::memcpy(m.h_meta, meta.data(), meta.size() * 4);
+    const int* dm = m.d_meta;
+
+    StepStats st{};
+    const bool stream_any = !m.w_all || !kv_runs.empty() || !act_runs.empty();
+    HC_CUDA(cudaEventRecord(m.ev0, s_compute_));
+    HC_CUDA(cudaMemcpyAsync(m.d_meta, m.h_meta, meta.size() * 4, cudaMemcpyHostToDevice, s_compute_));
+    embed(m.emb, m.pos, dm + o_tok, dm + o_pos, n, m.d, m.x[0], m.d, s_compute_);
+    st.launches += 1;
+    if (capture_inputs_) captured_.assign(static_cast<size_t>(m.L) * n * m.d, 0);
+    const float scale = opt_.scaled ? 1.0f / std::sqrt(static_cast<float>(m.hd)) : 1.0f;
+
+    for (int l = 0; l < m.L; ++l) {
+        const int slot = l & 1;
+        if (stream_any) {
+            // copy stream: weights + this layer's host blocks into slot l%2,
+            // after compute released the slot (layer l-2)
+            HC_CUDA(cudaStreamWaitEvent(s_copy_, m.consumed[slot]));
+            if (!m.w_all) {
+                HC_CUDA(cudaMemcpyAsync(m.wbuf[slot], m.h_w + static_cast<size_t>(l) * m.LE, m.LE * 2,
+                                        cudaMemcpyHostToDevice, s_copy_));
+                st.h2d_bytes += m.LE * 2.0;
+            }
+            const size_t lp = static_cast<size_t>(l % m.Lp);
+            for (const Run& r : act_runs) {
+                const size_t bytes = static_cast<size_t>(r.count) * m.actb * 2;
+                HC_CUDA(cudaMemcpyAsync(m.act_stage[slot] + static_cast<size_t>(r.start) * m.actb,
+                                        m.act_host + (lp * m.act_host_cap + r.start) * m.actb, bytes,
+                                        cudaMemcpyHostToDevice, s_copy_));
+                st.h2d_bytes += bytes;
+            }
+            for (const Run& r : kv_runs) {
+                const size_t bytes = static_cast<size_t>(r.count) * m.kvb * 2;
+                HC_CUDA(cudaMemcpyAsync(m.kv_stage[slot] + static_cast<size_t>(r.start) * m.kvb,
+                                        m.kv_host + (lp * m.kv_host_cap + r.start) * m.kvb, bytes,
+                                        cudaMemcpyHostToDevice, s_copy_));
+                st.h2d_bytes += bytes;
+            }
+            HC_CUDA(cudaEventRecord(m.loaded[slot], s_copy_));
+            HC_CUDA(cudaStreamWaitEvent(s_compute_, m.loaded[slot]));
+        }
+        const bf16* W = m.layer_w(l, slot);
+        bf16* R[16];
+        m.regions(l, slot, R);
+        bf16* xin = m.x[l & 1];
+        bf16* xout = m.x[(l + 1) & 1];
+        if (capture_inputs_)
+            HC_CUDA(cudaMemcpyAsync(captured_.data() + static_cast<size_t>(l) * n * m.d, xin,
+                                    static_cast<size_t>(n) * m.d * 2, cudaMemcpyDeviceToHost, s_compute_));
+        AppendCall ap;
+        std::copy(R, R + 16, ap.region);
+        ap.B = n;
+        ap.d = m.d;
+        ap.H = m.H;
+        ap.hd = m.hd;
+        ap.tpb = m.tpb;
+        ap.tok = dm + o_t;
+        if (any_act) {  // ACT writer: X of the new token -> its ACT slot (device + host)
+            ap.src = xin;
+            ap.ld = m.d;
+            ap.dev_ref = dm + o_ad;
+            ap.host_ref = dm + o_ah;
+            act_append(ap, s_compute_);
+            st.launches += 1;
+            st.d2h_bytes += 0;  // counted below from the slot lists
+        }
+        // recompute K|V of every ACT block (streamed and resident) into R_KVR
+        for (int which = 0; which < 2; ++which) {
+            const std::vector<int>& tl = which == 0 ? tiles_h : tiles_g;
+            if (tl.empty()) continue;
+            GemmCall c;
+            c.epi = gemm::kKvPaged;
+            c.A = which == 0 ? m.act_stage[slot] : R[R_ACT_GPU];
+            c.lda = m.d;
+            c.a_rows = static_cast<int>((which == 0 ? m.act_host_cap : m.act_gpu_cap) * m.tpb);
+            c.B = W + m.off.wqkv + static_cast<size_t>(m.d) * m.d;  // rows d..3d of Wqkv^T = [Wk|Wv]^T
+            c.ldb = m.d;
+            c.M = c.a_rows;
+            c.N = 2 * m.d;
+            c.K = m.d;
+            c.m_tile_rows = dm + (which == 0 ? o_th : o_tg);
+            c.num_m_tiles = static_cast<int>(tl.size());
+            c.out = m.kvr;
+            c.tpb = m.tpb;
+            c.d = m.d;
+            c.hd = m.hd;
+            c.blk_off = which == 0 ? static_cast<int>(m.act_gpu_cap) : 0;
+            if (profile_) HC_CUDA(cudaEventRecord(m.ev1, s_compute_));
+            run_gemm(c, s_compute_);
+            st.launches += 1;
+            st.recompute_tokens += static_cast<double>(tl.size()) * gemm::BM;
+        }
+        gemm_rows(gemm::kStore, xin, n, m.d, W + m.off.wqkv, 3 * m.d, m.qkv, 3 * m.d, s_compute_);
+        if (any_kv) {  // new token's K|V -> its KV slot (device + host)
+            ap.src = m.qkv;
+            ap.ld = 3 * m.d;
+            ap.dev_ref = dm + o_kd;
+            ap.host_ref = dm + o_kh;
+            kv_append(ap, s_compute_);
+            st.launches += 1;
+        }
+        AttnCall a;
+        a.q = m.qkv;
+        a.ldq = 3 * m.d;
+        a.out = m.att;
+        a.blk_ref = dm + o_ref;
+        a.n_blocks = dm + o_nb;
+        a.ctx_len = dm + o_ctx;
+        a.max_blocks = m.max_blocks;
+        for (int i = 0; i < 3; ++i) a.region[i] = R[i];
+        a.B = n;
+        a.H = m.H;
+        a.hd = m.hd;
+        a.tpb = m.tpb;
+        a.scale = scale;
+        a.work = m.attn_work;
+        a.splits = splits;
+        decode_attention(a, s_compute_);
+        gemm_rows(gemm::kStore, m.att, n, m.d, W + m.off.wproj, m.d, m.proj, m.d, s_compute_);
+        gemm_rows(gemm::kRelu, m.proj, n, m.d, W + m.off.w1, m.f, m.hbuf, m.f, s_compute_);
+        gemm_rows(gemm::kStore, m.hbuf, n, m.f, W + m.off.w2, m.d, xout, m.d, s_compute_);
+        st.launches += 4 + (splits > 1 ? 2 : 1);
+        HC_CUDA(cudaEventRecord(m.consumed[slot], s_compute_));
+    }
+    bf16* xf = m.x[m.L & 1];
+    if (logits_out || argmax_out) {
+        gemm_rows(gemm::kF32, xf, n, m.d, m.emb, m.V, m.logits, m.V, s_compute_);
+        st.launches += 1;
+        if (argmax_out) {
+            argmax_rows(m.logits, n, m.V, m.amax, s_compute_);
+            st.launches += 1;
+        }
+    }
+    HC_CUDA(cudaEventRecord(m.ev1, s_compute_));
+    HC_CUDA(cudaGetLastError());
+    if (x_out)
+        HC_CUDA(cudaMemcpyAsync(x_out, xf, static_cast<size_t>(n) * m.d * 2, cudaMemcpyDeviceToHost, s_compute_));
+    if (logits_out)
+        HC_CUDA(cudaMemcpyAsync(logits_out, m.logits, static_cast<size_t>(n) * m.V * 4, cudaMemcpyDeviceToHost,
+                                s_compute_));
+    if (argmax_out)
+        HC_CUDA(cudaMemcpyAsync(argmax_out, m.amax, static_cast<size_t>(n) * 4, cudaMemcpyDeviceToHost, s_compute_));
+    HC_CUDA(cudaStreamSynchronize(s_compute_));
+    float ms = 0;
+    HC_CUDA(cudaEventElapsedTime(&ms, m.ev0, m.ev1));
+    st.step_ms = ms;
+    for (int b = 0; b < n; ++b) {
+        if (act_host[b] >= 0) st.d2h_bytes += static_cast<double>(m.d) * 2 * m.L;
+        if (kv_host[b] >= 0) st.d2h_bytes += static_cast<double>(m.d) * 4 * m.L;
+    }
+    stats_ = st;
+}
+
+// ---------------------------------------------------------------------------
+void Engine::read_block(BlockKind kind, Location loc, int pbn, int layer, uint16_t* out) {
+    Impl& m = *impl_;
+    if (layer < 0 || layer >= m.L) throw InputError("read_block: layer out of range");
+    const bool kv = kind == BlockKind::KV;
+    const long cap = kv ? (loc == Location::GpuMem ? m.kv_gpu_cap : m.kv_host_cap)
+                        : (loc == Location::GpuMem ? m.act_gpu_cap : m.act_host_cap);
+    if (pbn < 0 || pbn >= cap) throw InputError("read_block: pbn out of range");
+    const size_t be = kv ? m.kvb : m.actb;
+    HC_CUDA(cudaStreamSynchronize(s_compute_));
+    if (loc == Location::GpuMem) {
+        const bf16* base = kv ? m.kv_gpu : m.act_gpu;
+        HC_CUDA(cudaMemcpy(out, base + (static_cast<size_t>(layer) * cap + pbn) * be, be * 2, cudaMemcpyDeviceToHost));
+    } else {
+        const bf16* base = kv ? m.kv_host : m.act_host;
+        std::memcpy(out, base + (static_cast<size_t>(layer % m.Lp) * cap + pbn) * be, be * 2);
+    }
+}
+
+// ---------------------------------------------------------------------------
+double Engine::time_kv_gen(int n_tokens, int reps) {
+    Impl& m = *impl_;
+    if (n_tokens <= 0) throw InputError("time_kv_gen: n_tokens must be positive");
+    // recompute GEMM over n tokens of the ACT staging (or GPU) pool, layer 0
+    const long cap_rows = std::max(m.act_host_cap, m.act_gpu_cap) * m.tpb;
+    if (n_tokens > cap_rows) throw InputError("time_kv_gen: more tokens than the ACT pools hold");
+    const bf16* A = m.act_host_cap * m.tpb >= n_tokens ? m.act_stage[0] : m.act_gpu;
+    if (!m.w_all)
+        HC_CUDA(cudaMemcpy(m.wbuf[0], m.h_w, m.LE * 2, cudaMemcpyHostToDevice));
+    const bf16* W = m.layer_w(0, 0);
+    std::vector<int> tiles;
+    for (int r = 0; r < n_tokens; r += gemm::BM) tiles.push_back(r);
+    m.ensure_meta(tiles.size());
+    std::memcpy(m.h_meta, tiles.data(), tiles.size() * 4);
+    HC_CUDA(cudaMemcpy(m.d_meta, m.h_meta, tiles.size() * 4, cudaMemcpyHostToDevice));
+    GemmCall c;
+    c.epi = gemm::kKvPaged;
+    c.A = A;
+    c.lda = m.d;
+    c.a_rows = static_cast<int>(cap_rows);
+    c.B = W + m.off.wqkv + static_cast<size_t>(m.d) * m.d;
+    c.ldb = m.d;
+    c.M = n_tokens;
+    c.N = 2 * m.d;
+    c.K = m.d;
+    c.m_tile_rows = m.d_meta;
+    c.num_m_tiles = static_cast<int>(tiles.size());
+    c.out = m.kvr;
+    c.tpb = m.tpb;
+    c.d = m.d;
+    c.hd = m.hd;
+    run_gemm(c, s_compute_);  // warm-up
+    HC_CUDA(cudaEventRecord(m.ev0, s_compute_));
+    for (int i = 0; i < reps; ++i) run_gemm(c, s_compute_);
+    HC_CUDA(cudaEventRecord(m.ev1, s_compute_));
+    HC_CUDA(cudaEventSynchronize(m.ev1));
+    float ms = 0;
+    HC_CUDA(cudaEventElapsedTime(&ms, m.ev0, m.ev1));
+    return ms / 1e3 / reps;
+}
+
+double Engine::time_load_bytes(size_t bytes, int reps) {
+    Impl& m = *impl_;
+    const size_t cap = static_cast<size_t>(m.kv_host_cap) * m.kvb * 2;
+    if (bytes == 0 || bytes > cap) throw InputError("time_load: byte count exceeds the KV host pool");
+    HC_CUDA(cudaMemcpyAsync(m.kv_stage[0], m.kv_host, bytes, cudaMemcpyHostToDevice, s_copy_));
+    HC_CUDA(cudaEventRecord(m.ev0, s_copy_));
+    for (int i = 0; i < reps; ++i)
+        HC_CUDA(cudaMemcpyAsync(m.kv_stage[i & 1], m.kv_host, bytes, cudaMemcpyHostToDevice, s_copy_));
+    HC_CUDA(cudaEventRecord(m.ev1, s_copy_));
+    HC_CUDA(cudaEventSynchronize(m.ev1));
+    float ms = 0;
+    HC_CUDA(cudaEventElapsedTime(&ms, m.ev0, m.ev1));
+    return ms / 1e3 / reps;
+}
+
+double Engine::time_load_kv(int n_tokens, int reps) {
+    return time_load_bytes(static_cast<size_t>(n_tokens) * 2 * cfg_.hidden_dim * 2, reps);
+}
+
+}  // namespace hc

@@ -1,0 +1,127 @@
+// The B200 decode engine for the KV-activation hybrid cache.
+//
+// One Engine owns one GPU's slice of the batch (requests never interact,
+// SURVEY.md §8(e)): its HybridCache bookkeeping, its block pools and its
+// pipeline. Pools (payload storage behind every pbn of cache.hpp):
+//
+//   KV / gpu    HBM      [L][kv_gpu_cap][2][H][tpb][hd]     resident
+//   ACT / gpu   HBM      [L][act_gpu_cap][tpb][d]           resident
+//   KV / host   pinned   [Lp][kv_host_cap][2][H][tpb][hd]   streamed per layer
+//   ACT / host  pinned   [Lp][act_host_cap][tpb][d]         streamed per layer
+//
+// Lp = host_layers (default L). Lp < L folds the host pools' storage (logical
+// layer l uses physical copy l % Lp) for hosts with less DRAM than the full
+// cache; the bytes streamed per layer are unchanged.
+//
+// Decode step, per layer l (north-star (1)-(4)):
+//   copy stream : [weights(l)] + KV/host runs + ACT/host runs -> slot l%2
+//   compute     : act_append (ACT writer: new token's X -> its ACT slot,
+//                 device + pinned host) -> recompute GEMM (tcgen05, ACT blocks
+//                 -> K|V straight into paged layout) -> QKV GEMM -> kv_append
+//                 (new token's K|V -> its KV slot, device + host) -> decode
+//                 attention over the hybrid block table -> proj -> FFN1+relu
+//                 -> FFN2 (= next layer's X)
+//   copy(l+2) waits for compute(l) to release slot l%2 (double buffering,
+//   sim.cpp:419-429's "2 units in flight").
+#pragma once
+#include <cuda_runtime.h>
+
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "host/cache.hpp"
+#include "host/model.hpp"
+#include "kernels/kernels.hpp"
+
+namespace hc {
+
+struct EngineOptions {
+    int max_batch = 1;            // max requests per decode step
+    int max_seq = 0;              // max context per request (0: weights.max_seq)
+    int weights_on_device = 1;    // 0: weights in pinned host memory, streamed per layer
+    long kv_host_cap = 0, kv_gpu_cap = 0, act_host_cap = 0, act_gpu_cap = 0;
+    int kv_on_gpu = 0;
+    int host_layers = 0;          // Lp (0 = num_layers)
+    CacheMode mode = CacheMode::Hybrid;
+    HostAllocation alloc{};       // hybrid-ratio setting (next_block_kind target)
+    double recompute_ratio = 0.0;
+    int scaled = 1;
+    int max_prefill_tokens = 65536;
+    int device = 0;
+};
+
+struct StepStats {
+    double step_ms = 0;           // compute-stream time of the whole step
+    double h2d_bytes = 0;         // bytes streamed host->device this step
+    double d2h_bytes = 0;         // bytes stored device->host (mapped writes)
+    double recompute_tokens = 0;  // ACT rows recomputed (incl. padding rows)
+    double recompute_ms = 0;      // summed recompute GEMM time (when profiled)
+    double attn_ms = 0;
+    double gemm_ms = 0;
+    int launches = 0;             // kernels launched this step
+};
+
+class Engine {
+public:
+    Engine(const HostWeights& w, const EngineOptions& o);
+    // Draw DecoderWeights::generate(config, seed, max_seq) (+ rescale) layer by
+    // layer straight into the engine's own memory (no full host copy).
+    Engine(const ModelConfig& c, uint64_t seed, int max_seq, bool rescale, const EngineOptions& o);
+    ~Engine();
+    Engine(const Engine&) = delete;
+    Engine& operator=(const Engine&) = delete;
+
+    // Prefill (forward_prompt semantics, decoder.cpp:144-157) of new requests;
+    // writes every layer's ACT / KV blocks chosen by the ratio policy.
+    void prefill(const std::vector<std::string>& ids, const std::vector<std::vector<int>>& prompts);
+    // Admit requests with prompt_len tokens of bookkeeping only and fill their
+    // blocks with a deterministic pattern (benchmark setup; no numerics).
+    void admit_synthetic(const std::vector<std::string>& ids, const std::vector<int>& prompt_lens, uint64_t seed);
+
+    // One decode step for the listed requests (generation_step semantics,
+    // decoder.cpp:159-174, batched). Outputs are optional (nullptr = skip):
+    // x_out [n x d] bf16 bits, logits [n x V] fp32 (tied head x.E^T),
+    // argmax [n].
+    void decode_step(const std::vector<std::string>& ids, const int* tokens, uint16_t* x_out, float* logits,
+                     int* argmax);
+    void free_request(const std::string& id);
+
+    // Payload of one block at one layer (bf16 bits; KV: [2][H][tpb][hd],
+    // ACT: [tpb][d]) — for parity tests of the cache writers.
+    void read_block(BlockKind kind, Location loc, int pbn, int layer, uint16_t* out);
+    // Decode-time layer inputs of the last step: [L][n][d] (debug / parity).
+    void set_capture_layer_inputs(bool on) { capture_inputs_ = on; }
+    const std::vector<uint16_t>& captured_layer_inputs() const { return captured_; }
+
+    // Planner calibration (north-star (5)): time the recompute GEMM over
+    // n ACT tokens and the host->device copy of n KV tokens on this engine's
+    // streams; seconds per layer.
+    double time_kv_gen(int n_tokens, int reps);
+    double time_load_kv(int n_tokens, int reps);
+    double time_load_bytes(size_t bytes, int reps);
+
+    const HybridCache& cache() const { return *cache_; }
+    HybridCache& cache() { return *cache_; }
+    const ModelConfig& config() const { return cfg_; }
+    const StepStats& last_stats() const { return stats_; }
+    void set_profile(bool on) { profile_ = on; }
+    cudaStream_t compute_stream() const { return s_compute_; }
+
+private:
+    struct Impl;
+    void init(const ModelConfig& c, int max_seq, const uint16_t* emb, const uint16_t* pos,
+              void (*fill_layer)(const void* ctx, int l, uint16_t* dst), const void* ctx);
+    std::unique_ptr<Impl> impl_;
+    ModelConfig cfg_;
+    EngineOptions opt_;
+    std::unique_ptr<HybridCache> cache_;
+    std::unique_ptr<BlockAssigner> assigner_;
+    cudaStream_t s_compute_ = nullptr, s_copy_ = nullptr;
+    StepStats stats_{};
+    bool profile_ = false;
+    bool capture_inputs_ = false;
+    std::vector<uint16_t> captured_;
+};
+
+}  // namespace hc

@@ -133,6 +133,27 @@ void draw_plain(uint16_t* dst, int rows, int cols, uint64_t seed) {
 
 }  // namespace
 
+void generate_tables(const ModelConfig& c, uint64_t seed, int max_seq, uint16_t* emb, uint16_t* pos) {
+    draw_plain(emb, c.vocab_size, c.hidden_dim, mix_seed(seed, 0));
+    draw_plain(pos, max_seq, c.hidden_dim, mix_seed(seed, 1));
+}
+
+void generate_layer(const ModelConfig& c, uint64_t seed, int l, bool rescale, uint16_t* L) {
+    const int d = c.hidden_dim, f = c.ffn_dim;
+    double fac[6];
+    rescale_factors(c, fac);
+    if (!rescale)
+        for (double& x : fac) x = 1.0;
+    const LayerOffsets off = LayerOffsets::of(c);
+    const uint64_t base = 100 + static_cast<uint64_t>(l) * 8;  // model.cpp:90, 106-113
+    // Wq, Wk, Wv [d x d] -> rows [0,d), [d,2d), [2d,3d) of Wqkv^T
+    for (int k = 0; k < 3; ++k)
+        draw_transposed(L + off.wqkv + static_cast<size_t>(k) * d * d, d, d, mix_seed(seed, base + k), fac[k]);
+    draw_transposed(L + off.wproj, d, d, mix_seed(seed, base + 3), fac[3]);
+    draw_transposed(L + off.w1, d, f, mix_seed(seed, base + 4), fac[4]);
+    draw_transposed(L + off.w2, f, d, mix_seed(seed, base + 5), fac[5]);
+}
+
 HostWeights generate_weights(const ModelConfig& config, uint64_t seed, int max_seq, bool rescale) {
     ModelConfig c = config;
     c.validate();
@@ -140,27 +161,11 @@ HostWeights generate_weights(const ModelConfig& config, uint64_t seed, int max_s
     HostWeights w;
     w.config = c;
     w.max_seq = max_seq;
-    const int d = c.hidden_dim, f = c.ffn_dim;
-    w.embedding.resize(static_cast<size_t>(c.vocab_size) * d);
-    w.positional.resize(static_cast<size_t>(max_seq) * d);
-    draw_plain(w.embedding.data(), c.vocab_size, d, mix_seed(seed, 0));
-    draw_plain(w.positional.data(), max_seq, d, mix_seed(seed, 1));
-    double fac[6];
-    rescale_factors(c, fac);
-    if (!rescale)
-        for (double& x : fac) x = 1.0;
-    const LayerOffsets off = LayerOffsets::of(c);
-    w.layers.resize(off.total * c.num_layers);
-    for (int l = 0; l < c.num_layers; ++l) {
-        uint16_t* L = w.layer(l);
-        const uint64_t base = 100 + static_cast<uint64_t>(l) * 8;  // model.cpp:90, 106-113
-        // Wq, Wk, Wv [d x d] -> rows [0,d), [d,2d), [2d,3d) of Wqkv^T
-        for (int k = 0; k < 3; ++k)
-            draw_transposed(L + off.wqkv + static_cast<size_t>(k) * d * d, d, d, mix_seed(seed, base + k), fac[k]);
-        draw_transposed(L + off.wproj, d, d, mix_seed(seed, base + 3), fac[3]);
-        draw_transposed(L + off.w1, d, f, mix_seed(seed, base + 4), fac[4]);
-        draw_transposed(L + off.w2, f, d, mix_seed(seed, base + 5), fac[5]);
-    }
+    w.embedding.resize(static_cast<size_t>(c.vocab_size) * c.hidden_dim);
+    w.positional.resize(static_cast<size_t>(max_seq) * c.hidden_dim);
+    generate_tables(c, seed, max_seq, w.embedding.data(), w.positional.data());
+    w.layers.resize(LayerOffsets::of(c).total * c.num_layers);
+    for (int l = 0; l < c.num_layers; ++l) generate_layer(c, seed, l, rescale, w.layer(l));
     return w;
 }
 

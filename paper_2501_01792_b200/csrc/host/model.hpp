@@ -77,6 +77,11 @@ struct LayerOffsets {
 // reference init at toy depth).
 HostWeights generate_weights(const ModelConfig& config, uint64_t seed, int max_seq, bool rescale = true);
 
+// Streaming pieces of generate_weights (so multi-GB models can be drawn
+// straight into pinned / staging memory): one packed layer, or the two tables.
+void generate_layer(const ModelConfig& config, uint64_t seed, int layer, bool rescale, uint16_t* dst);
+void generate_tables(const ModelConfig& config, uint64_t seed, int max_seq, uint16_t* emb, uint16_t* pos);
+
 // Build from externally supplied fp64 tensors in the reference layout
 // ([in x out], row-major): emb [V x d], pos [S x d], per layer q,k,v,proj
 // [d x d], ffn1 [d x f], ffn2 [f x d].

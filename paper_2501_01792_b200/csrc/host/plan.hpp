@@ -1,0 +1,72 @@
+// Hybrid-ratio planner (north-star (5)): the paper's cost model (Alg. 1,
+// Eq. 8-11) fed by MEASURED B200 samples — recompute-GEMM seconds vs ACT
+// tokens and host-link seconds vs KV tokens — instead of the reference's
+// synthetic ones.
+//
+// Reference: timing.hpp:15-88 / timing.cpp:38-183 (fit, eval, invert,
+// weight bytes, bundle), plan.hpp:17-65 / plan.cpp:41-177 (budget, two-step
+// allocation, frontier polish), flops.cpp:7-37 (FLOP model).
+#pragma once
+#include <cstdint>
+#include <utility>
+#include <vector>
+
+#include "host/cache.hpp"
+#include "host/model.hpp"
+
+namespace hc {
+
+struct Sample {
+    double n_tokens = 0.0;
+    double seconds = 0.0;
+};
+
+struct LinearTimeModel {
+    double slope = 0.0;
+    double intercept = 0.0;
+    double r_squared = 0.0;
+    bool intercept_clamped = false;
+};
+
+LinearTimeModel fit_linear(const std::vector<Sample>& samples);
+double eval(const LinearTimeModel& m, double n_tokens);
+long invert(const LinearTimeModel& m, double seconds);
+
+struct WeightBytes {
+    uint64_t per_layer = 0;
+    uint64_t total = 0;
+};
+WeightBytes weight_bytes(const ModelConfig& c);
+
+struct TimingBundle {
+    LinearTimeModel t_kv_gen;   // seconds vs ACT tokens recomputed, per layer
+    LinearTimeModel t_load_kv;  // seconds vs KV tokens loaded, per layer
+    double t_load_w = 0.0;      // seconds per layer of weights over the host link
+    uint64_t s_weight_layer = 0;
+    uint64_t s_weight_total = 0;
+};
+
+TimingBundle bundle_from_samples(const std::vector<Sample>& kv_gen, const std::vector<Sample>& load_kv,
+                                 double link_bytes_per_s, const ModelConfig& c);
+
+struct MemoryBudget {
+    double m_host = 0;
+    double s_weight = 0;
+    double s_kv_block = 0;   // all-layer footprint of one KV block
+    double s_act_block = 0;  // all-layer footprint of one ACT block
+};
+MemoryBudget budget_for(double host_mem, const ModelConfig& c, const TimingBundle& b);
+
+std::pair<long, long> initial_cache_allocation(const TimingBundle& b, int tpb, long act_gpu);
+std::pair<long, long> alloc_remaining(const TimingBundle& b, const MemoryBudget& mem, int tpb, long act_init,
+                                      long kv_init);
+HostAllocation plan_host_allocation(const TimingBundle& b, const MemoryBudget& mem, int tpb, long act_gpu);
+double planned_t_pcie(const TimingBundle& b, int tpb, const HostAllocation& a);
+double planned_t_computation(const TimingBundle& b, int tpb, const HostAllocation& a, long act_gpu);
+
+// FLOP model (flops.cpp:7-37); kinds: 0 KvGen, 1 QkvGen, 2 Attention,
+// 3 ProjFfn, 4 TokenRecomputeToLayerK, 5 FullLayer.
+double flop_count(int kind, const ModelConfig& c, long n_tokens, int k = 0);
+double attention_step_flops(const ModelConfig& c, long ctx);
+
+}  // namespace hc

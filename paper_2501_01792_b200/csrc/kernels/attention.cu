@@ -212,13 +212,17 @@ __global__ void attn_combine_kernel(const AttnCall c) {
 // half of the head dims; K/V tiles of 32 keys staged in shared memory.
 template <int HD>
 __global__ void __launch_bounds__(128)
-    prefill_attn_kernel(const bf16* __restrict__ qkv, bf16* __restrict__ out, int P, int H, float scale) {
+    prefill_attn_kernel(const bf16* __restrict__ qkv, bf16* __restrict__ out, const int* __restrict__ cu, int H,
+                        float scale) {
     constexpr int QT = 64, KT = 32, HALF = HD / 2;
     const int d = H * HD;
     const int ld = 3 * d;
     const int req = blockIdx.z;
     const int h = blockIdx.y;
     const int q0 = blockIdx.x * QT;
+    const int row0 = cu[req];
+    const int P = cu[req + 1] - row0;
+    if (q0 >= P) return;
     const int tq = threadIdx.x / 2;
     const int half = threadIdx.x % 2;
     const int t = q0 + tq;
@@ -227,7 +231,7 @@ __global__ void __launch_bounds__(128)
     __shared__ __align__(16) bf16 sk[KT][HD];
     __shared__ __align__(16) bf16 sv[KT][HD];
 
-    const bf16* rowbase = qkv + static_cast<long long>(req) * P * ld;
+    const bf16* rowbase = qkv + static_cast<long long>(row0) * ld;
     float q[HALF];
     {
         const bf16* qp = rowbase + static_cast<long long>(active ? t : 0) * ld + h * HD + half * HALF;
@@ -286,7 +290,7 @@ __global__ void __launch_bounds__(128)
         }
     }
     if (!active) return;
-    bf16* op = out + static_cast<long long>(req * P + t) * d + h * HD + half * HALF;
+    bf16* op = out + static_cast<long long>(row0 + t) * d + h * HD + half * HALF;
     const float inv = 1.f / l;
 #pragma unroll
     for (int j = 0; j < HALF; j += 8) {
@@ -327,14 +331,14 @@ void decode_attention(const AttnCall& c, cudaStream_t st) {
     throw std::invalid_argument("decode_attention: unsupported (head_dim, tokens_per_block)");
 }
 
-void prefill_attention(const bf16* qkv, bf16* out, int n_req, int P, int H, int hd, float scale,
-                       cudaStream_t st) {
-    if (n_req <= 0 || P <= 0) return;
-    const dim3 grid((P + 63) / 64, H, n_req);
+void prefill_attention(const bf16* qkv, bf16* out, const int* cu, int n_req, int max_len, int H, int hd,
+                       float scale, cudaStream_t st) {
+    if (n_req <= 0 || max_len <= 0) return;
+    const dim3 grid((max_len + 63) / 64, H, n_req);
     if (hd == 128)
-        prefill_attn_kernel<128><<<grid, 128, 0, st>>>(qkv, out, P, H, scale);
+        prefill_attn_kernel<128><<<grid, 128, 0, st>>>(qkv, out, cu, H, scale);
     else if (hd == 64)
-        prefill_attn_kernel<64><<<grid, 128, 0, st>>>(qkv, out, P, H, scale);
+        prefill_attn_kernel<64><<<grid, 128, 0, st>>>(qkv, out, cu, H, scale);
     else
         throw std::invalid_argument("prefill_attention: head_dim must be 64 or 128");
 }

@@ -21,14 +21,11 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include "gemm_types.hpp"
 #include "ptx.cuh"
 
 namespace hc::gemm {
 
-enum Epi : int { kStore = 0, kRelu = 1, kKvPaged = 2, kF32 = 3 };
-
-constexpr int BM = 128;
-constexpr int BK = 64;
 constexpr int kThreads = 192;
 
 struct Params {

@@ -1,0 +1,11 @@
+// Host-visible constants of the tcgen05 GEMM (gemm.cuh).
+#pragma once
+
+namespace hc::gemm {
+
+enum Epi : int { kStore = 0, kRelu = 1, kKvPaged = 2, kF32 = 3 };
+
+constexpr int BM = 128;  // rows per M tile (UMMA M)
+constexpr int BK = 64;   // K per pipeline stage (one 128-byte swizzle atom of bf16)
+
+}  // namespace hc::gemm

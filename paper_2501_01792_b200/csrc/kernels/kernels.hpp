@@ -54,10 +54,11 @@ struct AttnCall {
 void decode_attention(const AttnCall& c, cudaStream_t st);
 int attention_splits(int B, int H, int max_ctx, int tpb);
 
-// Causal prefill attention: qkv [n_req*P x 3d] (Q|K|V per row) for n_req
-// requests of P tokens each; out [n_req*P x d].
-void prefill_attention(const bf16* qkv, bf16* out, int n_req, int P, int H, int hd, float scale,
-                       cudaStream_t st);
+// Causal prefill attention over ragged requests: request r owns rows
+// [cu[r], cu[r+1]) of qkv [rows x 3d] (Q|K|V per row); out [rows x d].
+// cu is a device array of n_req+1 offsets; max_len = max request length.
+void prefill_attention(const bf16* qkv, bf16* out, const int* cu, int n_req, int max_len, int H, int hd,
+                       float scale, cudaStream_t st);
 
 // --------------------------------------------------------------- misc ----
 // X[i] = E[ids[i]] + Pos[pos[i]]   (decoder.cpp:65-95), bf16 out

@@ -1,0 +1,239 @@
+"""End-to-end parity of the B200 engine (prefill + batched decode over the
+hybrid cache) with the CPU oracle, through the C ABI.
+
+Oracle side: hybridsim_oracle (fp64 restatement of decoder.cpp, pinned to the
+reference in test_oracle.py) on the SAME bf16-rounded weights.
+Tolerance (north_star): max|got - ref| / max|ref| <= 1e-2 per tensor for
+decode outputs, recomputed K/V and logits; greedy tokens must match where the
+oracle's top-2 logit margin exceeds the bf16 noise floor.
+Block tables must match the oracle bit-exactly (dump_json string equality).
+"""
+import json
+
+import numpy as np
+import pytest
+
+import hybridsim_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-2
+
+
+def rel(got, ref):
+    return float(np.abs(np.asarray(got, np.float64) - ref).max() / max(np.abs(ref).max(), 1e-30))
+
+
+def f64(bits):
+    return O.bf16_bits_to_f64(np.asarray(bits))
+
+
+def small_cfg(L=3, d=256, H=2, f=512, V=512, tpb=16):
+    return O.ModelConfig(num_layers=L, hidden_dim=d, num_heads=H, ffn_dim=f, vocab_size=V,
+                         tokens_per_block=tpb).validate()
+
+
+def oracle_weights(cfg, seed=42, max_seq=128):
+    return O.prepare_weights(O.generate_weights(cfg, seed, max_seq))
+
+
+def as_engine_weights(w):
+    return {"embedding": w.embedding, "positional": w.positional, "layers": w.layers}
+
+
+def make_engine(cfg, w, **kw):
+    from paper_2501_01792_b200.api import Engine, ModelConfig
+    mc = ModelConfig(num_layers=cfg.num_layers, hidden_dim=cfg.hidden_dim, num_heads=cfg.num_heads,
+                     ffn_dim=cfg.ffn_dim, vocab_size=cfg.vocab_size, tokens_per_block=cfg.tokens_per_block)
+    return Engine(mc, weights=as_engine_weights(w), **kw)
+
+
+def run_case(cfg, w, prompts, decode_tokens, **engine_kw):
+    """Prefill + len(decode_tokens[0]) teacher-forced decode steps; returns the
+    engine outputs per step and the oracle outputs per step."""
+    from paper_2501_01792_b200.api import PoolCaps
+    n = len(prompts)
+    ids = [f"r{i}" for i in range(n)]
+    eng = make_engine(cfg, w, max_batch=n, **engine_kw)
+    eng.prefill(ids, prompts)
+    got, want = [], []
+    seqs = [list(p) for p in prompts]
+    for s in range(len(decode_tokens[0])):
+        toks = [decode_tokens[b][s] for b in range(n)]
+        res = eng.decode_step(ids, toks, want_x=True, want_logits=True, want_argmax=True)
+        got.append(res)
+        ref_x, ref_logits = [], []
+        for b in range(n):
+            seqs[b].append(toks[b])
+            tr = O.forward_prompt(seqs[b], w)
+            x = tr.output[-1:]
+            ref_x.append(x[0])
+            ref_logits.append(O.logits_tied(x, w)[0])
+        want.append({"x": np.array(ref_x), "logits": np.array(ref_logits)})
+    return eng, ids, got, want
+
+
+def check_outputs(got, want):
+    for g, r in zip(got, want):
+        assert rel(f64(g["x"]), r["x"]) <= TOL
+        assert rel(g["logits"], r["logits"]) <= TOL
+        for b in range(len(g["argmax"])):
+            top2 = np.sort(r["logits"][b])[-2:]
+            if top2[1] - top2[0] > 2e-2 * np.abs(r["logits"][b]).max():
+                assert g["argmax"][b] == int(np.argmax(r["logits"][b]))
+
+
+def test_engine_resident_act_only_matches_oracle(native):
+    """Config-2 shape in miniature: ACT-only cache in HBM, resident weights."""
+    from paper_2501_01792_b200.api import PoolCaps
+    cfg = small_cfg()
+    w = oracle_weights(cfg)
+    rng = np.random.default_rng(0)
+    prompts = [rng.integers(0, cfg.vocab_size, 37).tolist(), rng.integers(0, cfg.vocab_size, 50).tolist()]
+    dec = [rng.integers(0, cfg.vocab_size, 4).tolist() for _ in prompts]
+    eng, ids, got, want = run_case(cfg, w, prompts, dec, caps=PoolCaps(act_gpu=16), mode="act_only")
+    check_outputs(got, want)
+    st = eng.last_stats()
+    assert st["h2d_bytes"] == 0 and st["launches"] > 0
+
+
+@pytest.mark.parametrize("weights_on_device", [True, False])
+def test_engine_hybrid_offloaded_matches_oracle(native, weights_on_device):
+    """Hybrid 1:1 ratio, ACT blocks split GPU/host, KV on host, weights streamed
+    or resident: outputs match the oracle and block tables match bit-exactly."""
+    from paper_2501_01792_b200.api import HostAllocation, PoolCaps
+    cfg = small_cfg(L=4, d=256, H=4, f=768)
+    w = oracle_weights(cfg)
+    rng = np.random.default_rng(1)
+    lens = [33, 64, 17]
+    prompts = [rng.integers(0, cfg.vocab_size, n).tolist() for n in lens]
+    dec = [rng.integers(0, cfg.vocab_size, 5).tolist() for _ in prompts]
+    alloc = HostAllocation(20, 20)
+    caps = PoolCaps(kv_host=20, act_host=20, act_gpu=3)
+    eng, ids, got, want = run_case(cfg, w, prompts, dec, caps=caps, allocation=alloc, mode="hybrid",
+                                   weights_on_device=weights_on_device)
+    check_outputs(got, want)
+    # block tables: the oracle's add_token replay in the same call order
+    ba = O.BlockAssigner(cfg.tokens_per_block, O.HYBRID, O.HostAllocation(20, 20), act_gpu=3)
+    for i, n in enumerate(lens):
+        ba.add_request(ids[i], n)
+        for _ in range(n):
+            ba.add_token(ids[i])
+    for _ in range(5):
+        for i in range(len(lens)):
+            ba.add_token(ids[i])
+    assert eng.cache.dump_json() == O.dumps(ba.cache.dump_json())
+    st = eng.last_stats()
+    assert st["h2d_bytes"] > 0
+
+
+def test_engine_cache_writers_match_oracle(native):
+    """ACT writer (layer inputs X) and KV blocks hold the oracle's X / K / V
+    rows after prefill + decode (north-star (1))."""
+    from paper_2501_01792_b200.api import HostAllocation, PoolCaps
+    cfg = small_cfg(L=2, d=256, H=2, f=512, tpb=8)
+    w = oracle_weights(cfg)
+    rng = np.random.default_rng(2)
+    prompt = rng.integers(0, cfg.vocab_size, 29).tolist()
+    dec = rng.integers(0, cfg.vocab_size, 3).tolist()
+    eng = make_engine(cfg, w, max_batch=1, caps=PoolCaps(kv_host=8, act_host=8, act_gpu=1),
+                      allocation=HostAllocation(1, 1))
+    eng.prefill(["a"], [prompt])
+    for t in dec:
+        eng.decode_step(["a"], [t])
+    seq = prompt + dec
+    tr = O.forward_prompt(seq, w)
+    table = eng.cache.table("a")
+    assert table.context_len() == len(seq)
+    tpb, d, H = cfg.tokens_per_block, cfg.hidden_dim, cfg.num_heads
+    row = 0
+    for e in table.entries:
+        for l in range(cfg.num_layers):
+            blk = f64(eng.read_block(e.kind, e.location, e.pbn, l))
+            n = e.filled_tokens
+            if int(e.kind) == 1:  # ACT: X rows
+                assert rel(blk[:n], tr.layer_inputs[l][row:row + n]) <= TOL
+            else:
+                k = blk[0].transpose(1, 0, 2).reshape(tpb, d)[:n]
+                v = blk[1].transpose(1, 0, 2).reshape(tpb, d)[:n]
+                assert rel(k, tr.k[l][row:row + n]) <= TOL
+                assert rel(v, tr.v[l][row:row + n]) <= TOL
+        row += e.filled_tokens
+
+
+def test_engine_modes_agree(native):
+    """kv_only / act_only / hybrid assemble the same context (the reference's
+    4-way equivalence, verify.cpp:54-85, at bf16 tolerance)."""
+    from paper_2501_01792_b200.api import HostAllocation, PoolCaps
+    cfg = small_cfg(L=3, d=256, H=2, f=512)
+    w = oracle_weights(cfg)
+    rng = np.random.default_rng(3)
+    prompts = [rng.integers(0, cfg.vocab_size, 45).tolist()]
+    toks = [int(rng.integers(0, cfg.vocab_size))]
+    outs = {}
+    for mode in ("kv_only", "act_only", "hybrid"):
+        eng = make_engine(cfg, w, max_batch=1, caps=PoolCaps(kv_host=16, act_host=16, act_gpu=2), mode=mode,
+                          allocation=HostAllocation(3, 5))
+        eng.prefill(["r"], prompts)
+        outs[mode] = f64(eng.decode_step(["r"], toks)["x"])
+        eng.close()
+    assert rel(outs["act_only"], outs["kv_only"]) <= TOL
+    assert rel(outs["hybrid"], outs["kv_only"]) <= TOL
+
+
+def test_engine_greedy_generation_matches_oracle(native):
+    """Greedy decode (tied LM head argmax) reproduces the oracle's tokens."""
+    from paper_2501_01792_b200.api import HostAllocation, PoolCaps
+    cfg = small_cfg(L=2, d=256, H=2, f=512)
+    w = oracle_weights(cfg, seed=7)
+    rng = np.random.default_rng(4)
+    prompt = rng.integers(0, cfg.vocab_size, 20).tolist()
+    eng = make_engine(cfg, w, max_batch=1, caps=PoolCaps(kv_host=8, act_host=8), allocation=HostAllocation(1, 2))
+    eng.prefill(["g"], [prompt])
+    seq = list(prompt)
+    tok = int(rng.integers(0, cfg.vocab_size))
+    for _ in range(6):
+        res = eng.decode_step(["g"], [tok], want_logits=True, want_argmax=True)
+        seq.append(tok)
+        ref = O.logits_tied(O.forward_prompt(seq, w).output[-1:], w)[0]
+        top2 = np.sort(ref)[-2:]
+        assert rel(res["logits"][0], ref) <= TOL
+        if top2[1] - top2[0] > 2e-2 * np.abs(ref).max():
+            assert int(res["argmax"][0]) == int(np.argmax(ref))
+        tok = int(np.argmax(ref))  # follow the oracle's greedy path
+
+
+def test_engine_decode_time_layer_inputs(native):
+    """Decode-time X per layer equals forward_prompt(prefix+token).layer_inputs
+    row pos."""
+    from paper_2501_01792_b200.api import PoolCaps
+    cfg = small_cfg(L=3)
+    w = oracle_weights(cfg)
+    rng = np.random.default_rng(5)
+    prompt = rng.integers(0, cfg.vocab_size, 30).tolist()
+    tok = int(rng.integers(0, cfg.vocab_size))
+    eng = make_engine(cfg, w, max_batch=1, caps=PoolCaps(act_gpu=4), mode="act_only")
+    eng.prefill(["x"], [prompt])
+    eng.capture_inputs(True)
+    eng.decode_step(["x"], [tok])
+    cap = f64(eng.captured_inputs())
+    tr = O.forward_prompt(prompt + [tok], w)
+    for l in range(cfg.num_layers):
+        assert rel(cap[l, 0], tr.layer_inputs[l][-1]) <= TOL
+
+
+def test_engine_errors(native):
+    from paper_2501_01792_b200 import CapacityError, InputError
+    from paper_2501_01792_b200.api import PoolCaps
+    cfg = small_cfg(L=1)
+    w = oracle_weights(cfg, max_seq=64)
+    eng = make_engine(cfg, w, max_batch=2, caps=PoolCaps(act_gpu=2), mode="act_only")
+    with pytest.raises(InputError):
+        eng.prefill(["a"], [[cfg.vocab_size]])           # token id out of range
+    with pytest.raises(InputError):
+        eng.decode_step(["nope"], [1])                    # unknown request
+    eng.prefill(["a"], [[1] * 32])                        # fills both ACT blocks
+    with pytest.raises(CapacityError):
+        eng.decode_step(["a"], [1])                       # pools exhausted
+    with pytest.raises(InputError):
+        eng.prefill(["b"], [[1] * 65])                    # longer than max_seq
