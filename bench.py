@@ -1,0 +1,408 @@
+#!/usr/bin/env python
+"""Benchmark: offloaded OPT-30B-shape decode over the KV-activation hybrid
+cache (BASELINE.json configs[2]: weights + hybrid cache in pinned host
+memory, batch 128, prompt 1024, gen 256), generated tokens/s.
+
+A "step" is one decode iteration: all 48 layers for the whole per-GPU batch
+(128 requests), streaming each layer's weights and host KV/ACT blocks over the
+host link, recomputing K/V of the ACT blocks on the tensor cores, attention
+over the hybrid block table, and the new token's cache writes. Multi-GPU:
+batch-partitioned (each rank its own 128 requests, pools and host link; no
+collective on the data path) -> scaling "weak".
+
+    python bench.py [--gpus N --steps K --warmup W] [--ratio R] [--impl reference]
+
+Prints ONE JSON line on rank 0. See DESIGN.md §Measurement for every field.
+"""
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "generated tokens/sec, OPT-30B offloaded, per KV:ACT ratio, at 1/2/4/8 B200"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--model", default="opt-30b")
+    p.add_argument("--batch", type=int, default=128, help="requests per GPU")
+    p.add_argument("--prompt", type=int, default=1024)
+    p.add_argument("--gen", type=int, default=256, help="generation length of the workload (config)")
+    p.add_argument("--ratio", type=float, default=1.0 / 3.0, help="ACT share of context blocks (KV:ACT 2:1)")
+    p.add_argument("--host-gb", type=float, default=0.0, help="pinned host budget per rank (0: auto)")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--layers", type=int, default=0, help="override num_layers (smoke/profiling only)")
+    p.add_argument("--profile-run", action="store_true", help="short run for ncu (no JSON contract)")
+    return p.parse_args()
+
+
+# ---------------------------------------------------------------- helpers ---
+def dist_setup(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch
+        import torch.distributed as td
+        backend = "nccl" if torch.cuda.is_available() else "gloo"
+        if backend == "nccl":
+            torch.cuda.set_device(local)
+        td.init_process_group(backend=backend)
+        dist = td
+    return world, rank, local, dist
+
+
+def barrier(dist):
+    if dist is not None:
+        dist.barrier()
+
+
+def max_over_ranks(dist, x: float) -> float:
+    if dist is None:
+        return x
+    import torch
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def sum_over_ranks(dist, x: float) -> float:
+    if dist is None:
+        return x
+    import torch
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
+def mem_available_bytes() -> float:
+    try:
+        with open("/proc/meminfo") as fh:
+            for line in fh:
+                if line.startswith("MemAvailable:"):
+                    return float(line.split()[1]) * 1024
+    except OSError:
+        pass
+    return 64e9
+
+
+def measured_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            j = json.load(fh)
+        return j.get("hbm_gbs", 6650.0), j.get("bf16_tflops_sustained", 1400.0), j.get("bf16_tflops", 1590.0), "measured"
+    except (OSError, ValueError):
+        return 6650.0, 1400.0, 1590.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=self.f, stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.f.flush()
+        self.f.seek(0)
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.f.read().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        os.unlink(self.f.name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------ CPU baseline ---
+def cpu_reference_sample(cfg, prompt: int, ratio: float, threads: int):
+    """The reference's own CPU path for this workload, bounded: one request,
+    one layer of one decode step at full OPT width — recompute K,V of the
+    request's ACT-cached context tokens (recompute_kv_from_activation,
+    decoder.cpp:123-129) + generation_step of that layer over the full
+    context (decoder.cpp:159-174). tokens/s = 1 / (num_layers * t_sample)."""
+    os.environ["OMP_NUM_THREADS"] = str(threads)
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import ref_lib as R  # noqa: E402  (checker / baseline only)
+    d, H, f, V, tpb = cfg.hidden_dim, cfg.num_heads, cfg.ffn_dim, cfg.vocab_size, cfg.tokens_per_block
+    n_act = int(round(ratio * prompt))
+    if R.available():
+        kind = "reference"
+        rw = R.RefWeights(1, d, H, f, V, tpb, 42, prompt + 2)
+        rng = np.random.default_rng(0)
+        a = rng.uniform(-0.1, 0.1, (max(n_act, 1), d))
+        ck = rng.uniform(-0.1, 0.1, (1, prompt, d))
+        cv = rng.uniform(-0.1, 0.1, (1, prompt, d))
+
+        def run():
+            t0 = time.perf_counter()
+            if n_act:
+                rw.recompute_kv(0, a)
+            rw.generation_step(1, prompt, ck, cv)
+            return time.perf_counter() - t0
+    else:
+        import hybridsim_oracle as O  # noqa: E402
+        kind = "port"
+        rng = np.random.default_rng(0)
+        wl = {n: rng.uniform(-0.1, 0.1, s) for n, s in
+              zip(O.WEIGHT_NAMES, [(d, d)] * 4 + [(d, f), (f, d)])}
+        w = O.DecoderWeights(O.ModelConfig(num_layers=1, hidden_dim=d, num_heads=H, ffn_dim=f,
+                                           vocab_size=V).validate(), prompt + 2,
+                             rng.uniform(-0.1, 0.1, (V, d)), rng.uniform(-0.1, 0.1, (prompt + 2, d)), [wl])
+        a = rng.uniform(-0.1, 0.1, (max(n_act, 1), d))
+        ck = [rng.uniform(-0.1, 0.1, (prompt, d))]
+        cv = [rng.uniform(-0.1, 0.1, (prompt, d))]
+
+        def run():
+            t0 = time.perf_counter()
+            if n_act:
+                O.recompute_kv_from_activation(a, 0, w)
+            O.generation_step(1, prompt, ck, cv, w)
+            return time.perf_counter() - t0
+    return kind, run, (f"1 request x 1 layer of one decode step at {cfg.name} width (d={d}), context {prompt}, "
+                       f"{n_act} ACT-recomputed tokens + generation_step; extrapolated x{cfg.num_layers} layers")
+
+
+def reference_arm(args, cfg, world, rank, dist):
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    kind, run, sample = cpu_reference_sample(cfg, args.prompt, args.ratio, threads)
+    for _ in range(args.warmup):
+        run()
+    ts = [run() for _ in range(args.steps)]
+    t = statistics.mean(ts)
+    v = 1.0 / (cfg.num_layers * t)
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "tokens/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": workload_config(args, cfg, world),
+        "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": threads, "kind": kind, "sample": sample},
+        "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def workload_config(args, cfg, world, extra=None):
+    c = {"workload": f"{cfg.name}-shape offloaded decode (weights + hybrid KV/ACT cache in pinned host memory), "
+                     f"batch {args.batch}/GPU, prompt {args.prompt}, gen {args.gen}",
+         "model": cfg.name, "global_batch": args.batch * world, "seq_len": args.prompt, "gen_len": args.gen,
+         "act_share_r": round(args.ratio, 4),
+         "kv_act_ratio": f"{(1 - args.ratio) / max(args.ratio, 1e-9):.2f}:1" if args.ratio > 0 else "kv_only",
+         "parallelism": f"batch-partitioned x{world} (no collective)",
+         "l2": "inputs larger than L2 (~100+ GB streamed host->HBM per step)"}
+    if extra:
+        c.update(extra)
+    return c
+
+
+# ------------------------------------------------------------------ ours ---
+def our_arm(args, cfg, world, rank, local, dist):
+    from paper_2501_01792_b200 import api, kernels
+    if kernels.device_count() == 0:
+        raise SystemExit("bench needs a CUDA device")
+    hbm_peak, tflops_sust, tflops_burst, peak_src = measured_peaks()
+    B, P, L, d = args.batch, args.prompt, cfg.num_layers, cfg.hidden_dim
+    tpb = cfg.tokens_per_block
+    total_steps = args.warmup + args.steps + 2
+    max_seq = P + total_steps + 1
+    nb = math.ceil((P + total_steps) / tpb)
+    r = args.ratio
+    mode = "kv_only" if r <= 0 else ("act_only" if r >= 1 else "hybrid")
+    act_per = 0 if mode == "kv_only" else (nb if mode == "act_only" else math.ceil(r * nb) + 1)
+    kv_per = 0 if mode == "act_only" else (nb if mode == "kv_only" else math.ceil((1 - r) * nb) + 1)
+    alloc = api.HostAllocation(int(round(r * 1000)), 1000 - int(round(r * 1000)))
+    caps = api.PoolCaps(kv_host=B * kv_per, act_host=B * act_per)
+    kvb = api.HybridCache.bytes_of("KV", cfg)
+    actb = api.HybridCache.bytes_of("ACT", cfg)
+    per_layer_pool = caps.kv_host * kvb + caps.act_host * actb
+    w_layer, _ = api.weight_bytes(cfg)
+    local_world = int(os.environ.get("LOCAL_WORLD_SIZE", str(world)))
+    # pinned host budget: never more than 120 GB or MemAvailable - 48 GB per node
+    # (pinned pages cannot be reclaimed; folding keeps the streamed bytes)
+    budget = args.host_gb * 1e9 if args.host_gb > 0 else min(120e9, mem_available_bytes() - 48e9) / local_world
+    Lw = L if L * w_layer <= 0.55 * budget else max(2, int(0.55 * budget // w_layer))
+    Lp = int(min(L, max(2, (budget - Lw * w_layer) // max(per_layer_pool, 1))))
+    t_setup = time.time()
+    eng = api.Engine(cfg, seed=42, max_seq=max_seq, rescale=True, max_batch=B, weights_on_device=False,
+                     caps=caps, host_layers=Lp, weight_layers=Lw, mode=mode, allocation=alloc, device=local)
+    ids = [f"g{rank}r{i}" for i in range(B)]
+    eng.admit_synthetic(ids, [P] * B, seed=1 + rank)
+    # host-link peak: one large pinned H2D copy on the engine's copy stream
+    n_tok = min(caps.kv_host * tpb, 65536) if caps.kv_host else 0
+    link_gbs = (n_tok * 2 * d * 2) / eng.time_load_kv(n_tok, reps=3) / 1e9 if n_tok else None
+    setup_s = time.time() - t_setup
+
+    rng = np.random.default_rng(rank)
+    tokens = rng.integers(0, cfg.vocab_size, (total_steps, B)).astype(np.int32)
+    out = {"argmax": np.zeros(B, np.int32)}
+    for s in range(args.warmup):
+        eng.decode_step(ids, tokens[s], want_x=False, want_argmax=True, out=out)
+
+    # one profiled (untimed) step: per-kernel split + copy-stream GB/s
+    eng.set_profile(True)
+    eng.decode_step(ids, tokens[args.warmup], want_x=False, want_argmax=True, out=out)
+    prof = eng.last_stats()
+    eng.set_profile(False)
+    act_tokens = sum(e.filled_tokens for rid in ids for e in eng.cache.table(rid).entries
+                     if int(e.kind) == 1)
+
+    clocks = ClockSampler(local)
+    barrier(dist)
+    import torch
+    torch.cuda.synchronize()
+    clocks.start()
+    dev_ms, launches, h2d, d2h = 0.0, 0, 0.0, 0.0
+    t0 = time.perf_counter()
+    for s in range(args.steps):
+        eng.decode_step(ids, tokens[args.warmup + 1 + s], want_x=False, want_argmax=True, out=out)
+        st = eng.last_stats()
+        dev_ms += st["step_ms"]
+        launches += int(st["launches"])
+        h2d += st["h2d_bytes"]
+        d2h += st["d2h_bytes"]
+    wall = time.perf_counter() - t0
+    torch.cuda.synchronize()
+    barrier(dist)
+    clk = clocks.stop()
+
+    dev_s = max_over_ranks(dist, dev_ms / 1e3)
+    wall_s = max_over_ranks(dist, wall)
+    tokens_total = sum_over_ranks(dist, float(B * args.steps))
+    value = tokens_total / dev_s
+    e2e = tokens_total / wall_s
+    ms_per_step = dev_s * 1e3 / args.steps
+
+    # dominant kernel: the recompute GEMM (tcgen05). algorithmic FLOPs/launch
+    # = 4 d^2 x ACT context tokens of the layer (flops.cpp:14), per launch
+    rec_launch_ms = prof["recompute_ms"] / max(prof["recompute_launches"], 1)
+    rec_flops = 4.0 * d * d * act_tokens / max(prof["recompute_launches"] / L, 1)
+    achieved = rec_flops / (rec_launch_ms / 1e3) / 1e12 if rec_launch_ms > 0 else 0.0
+    roof = {"kernel": "gemm_tn_kernel<256,kKvPaged> (ACT->K|V recompute)", "bound": "tensor",
+            "achieved": achieved, "peak": tflops_sust, "unit": "TFLOP/s",
+            "frac": achieved / tflops_sust if tflops_sust else None, "traffic": None,
+            "peak_source": f"{peak_src} bf16_tflops_sustained (MEASURED_PEAKS.json)",
+            "flops_per_launch": rec_flops, "launch_ms": rec_launch_ms}
+    # per-step roofline (north_star): slower of link bytes / link BW, tensor
+    # FLOPs / tensor peak, HBM bytes / HBM BW
+    h2d_step = h2d / args.steps
+    ctx = P + args.warmup + 1 + args.steps // 2
+    tensor_flops = L * (4.0 * d * d * act_tokens + 2.0 * B * (4 * d * d + 2 * d * cfg.ffn_dim))
+    hbm_bytes = L * (B * (ctx + 1) * 2 * d * 2 + act_tokens * 3 * d * 2 + w_layer) + h2d_step
+    t_link = h2d_step / (link_gbs * 1e9) if link_gbs else 0.0
+    t_tensor = tensor_flops / (tflops_sust * 1e12)
+    t_hbm = hbm_bytes / (hbm_peak * 1e9)
+    t_roof = max(t_link, t_tensor, t_hbm)
+    step_roof = {"t_link_ms": t_link * 1e3, "t_tensor_ms": t_tensor * 1e3, "t_hbm_ms": t_hbm * 1e3,
+                 "bound": ["link", "tensor", "hbm"][int(np.argmax([t_link, t_tensor, t_hbm]))],
+                 "roofline_tokens_per_s_per_gpu": B / t_roof if t_roof else None,
+                 "frac": (t_roof * 1e3) / ms_per_step if ms_per_step else None,
+                 "link_peak_gbs": link_gbs, "link_peak_source": "measured: pinned H2D cudaMemcpyAsync on this box",
+                 "achieved_link_gbs": h2d_step / (ms_per_step / 1e3) / 1e9,
+                 "copy_stream_gbs": prof["h2d_bytes"] / (prof["copy_ms"] / 1e3) / 1e9 if prof["copy_ms"] else None,
+                 "profile_split_ms": {"recompute": prof["recompute_ms"], "attention": prof["attn_ms"],
+                                      "qkv_proj_ffn": prof["gemm_ms"], "copy_stream": prof["copy_ms"]}}
+
+    res = None
+    if rank == 0:
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            threads = os.cpu_count() or 1
+            kind, run, sample = cpu_reference_sample(cfg, P, r, threads)
+            run()  # warm
+            t = statistics.mean([run() for _ in range(2)])
+            cpu = {"value": 1.0 / (L * t), "unit": "tokens/s", "cores": threads, "kind": kind, "sample": sample}
+        res = {
+            "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (reference-draw weights rescaled, pattern-filled cache at prompt length)",
+            "config": workload_config(args, cfg, world, {
+                "mode": mode, "host_layers_phys": Lp, "weight_layers_phys": Lw,
+                "host_pool_fold": ("none" if Lp == L and Lw == L else
+                                   f"host storage folded to {Lp} cache / {Lw} weight layer copies "
+                                   "(box DRAM); bytes streamed per layer unchanged"),
+                "kv_host_blocks": caps.kv_host, "act_host_blocks": caps.act_host,
+                "act_context_tokens": act_tokens}),
+            "e2e": {"value": e2e, "unit": "tokens/s", "h2d_bytes_per_step": h2d_step + B * 4,
+                    "d2h_bytes_per_step": d2h / args.steps + B * 4,
+                    "note": "decode_step C-ABI call with host token ids in / argmax out; includes the host-link "
+                            "stream of weights + KV/ACT blocks and the new-token cache stores"},
+            "gpu_launches": launches,
+            "roofline": roof,
+            "step_roofline": step_roof,
+            "cpu_baseline": cpu,
+            "clocks": clk,
+            "setup_s": setup_s,
+        }
+        print(json.dumps(res), flush=True)
+    eng.close()
+    return res
+
+
+def main():
+    args = parse()
+    world, rank, local, dist = dist_setup(args)
+    from paper_2501_01792_b200 import api
+    cfg = api.ModelConfig.preset(args.model)
+    if args.layers:
+        cfg.num_layers = args.layers
+    if args.impl == "reference":
+        reference_arm(args, cfg, world, rank, dist)
+    else:
+        our_arm(args, cfg, world, rank, local, dist)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -120,6 +120,7 @@ typedef struct hc_engine_options {
     int scaled;              /* 1/sqrt(head_dim) attention scale (decoder.hpp:28) */
     int max_prefill_tokens;  /* rows per prefill chunk (0: 65536) */
     int device;
+    int weight_layers;       /* physical pinned weight layers (0 = num_layers) */
 } hc_engine_options;
 
 int hc_engine_create(const hc_model_config* cfg, uint64_t seed, int max_seq, int rescale,
@@ -144,8 +145,11 @@ int hc_engine_read_block(void* engine, int kind, int loc, int pbn, int layer, ui
 int hc_engine_capture_inputs(void* engine, int on);
 /* Decode-time layer inputs of the last step, [L][n][d] bf16 (n = last batch). */
 int hc_engine_captured_inputs(void* engine, uint16_t* out, long count);
-/* out8 = {step_ms, h2d_bytes, d2h_bytes, recompute_rows, recompute_ms, attn_ms, gemm_ms, launches} */
-int hc_engine_last_stats(void* engine, double* out8);
+/* out10 = {step_ms, h2d_bytes, d2h_bytes, recompute_rows, recompute_ms, attn_ms, gemm_ms, launches,
+ *          copy_ms, recompute_launches}; the *_ms splits need hc_engine_set_profile(1). */
+int hc_engine_last_stats(void* engine, double* out10);
+/* Per-kernel CUDA-event timing of the next steps (small overhead). */
+int hc_engine_set_profile(void* engine, int on);
 /* Planner calibration on this engine: seconds per layer. */
 int hc_engine_time_kv_gen(void* engine, int n_tokens, int reps, double* seconds);
 int hc_engine_time_load_kv(void* engine, int n_tokens, int reps, double* seconds);

@@ -22,7 +22,8 @@ class EngineOptionsC(C.Structure):
                 ("kv_host_cap", C.c_long), ("kv_gpu_cap", C.c_long), ("act_host_cap", C.c_long),
                 ("act_gpu_cap", C.c_long), ("kv_on_gpu", C.c_int), ("host_layers", C.c_int),
                 ("mode", C.c_int), ("alloc_act_host", C.c_long), ("alloc_kv_host", C.c_long),
-                ("scaled", C.c_int), ("max_prefill_tokens", C.c_int), ("device", C.c_int)]
+                ("scaled", C.c_int), ("max_prefill_tokens", C.c_int), ("device", C.c_int),
+                ("weight_layers", C.c_int)]
 
 
 cfgp = C.POINTER(ModelConfigC)
@@ -76,6 +77,7 @@ SIGNATURES = {
     "hc_engine_capture_inputs": (i, [vp, i]),
     "hc_engine_captured_inputs": (i, [vp, u16p, l]),
     "hc_engine_last_stats": (i, [vp, dp]),
+    "hc_engine_set_profile": (i, [vp, i]),
     "hc_engine_time_kv_gen": (i, [vp, i, i, dp]),
     "hc_engine_time_load_kv": (i, [vp, i, i, dp]),
     # kernels (host buffers in / out)

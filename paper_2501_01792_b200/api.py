@@ -393,7 +393,7 @@ class Engine:
                  weights: Optional[dict] = None, max_batch: int = 1, weights_on_device: bool = True,
                  caps: Optional[PoolCaps] = None, kv_on_gpu: bool = False, host_layers: int = 0,
                  mode: str = "hybrid", allocation: Optional[HostAllocation] = None, scaled: bool = True,
-                 max_prefill_tokens: int = 0, device: int = 0):
+                 max_prefill_tokens: int = 0, device: int = 0, weight_layers: int = 0):
         self.cfg = ModelConfig(**cfg.__dict__).validate()
         caps = caps or PoolCaps()
         alloc = allocation or HostAllocation(1, 1)
@@ -401,7 +401,8 @@ class Engine:
             raise InputError(f"unknown mode: {mode}")
         self.opts = EngineOptionsC(max_batch, max_seq, int(weights_on_device), caps.kv_host, caps.kv_gpu,
                                    caps.act_host, caps.act_gpu, int(kv_on_gpu), host_layers, MODES[mode],
-                                   alloc.act_host, alloc.kv_host, int(scaled), max_prefill_tokens, device)
+                                   alloc.act_host, alloc.kv_host, int(scaled), max_prefill_tokens, device,
+                                   weight_layers)
         self.max_batch = max_batch
         h = C.c_void_p()
         c = self.cfg.to_c()
@@ -493,11 +494,14 @@ class Engine:
         return out
 
     def last_stats(self) -> dict:
-        out, op = _darr(np.zeros(8))
+        out, op = _darr(np.zeros(10))
         check(lib().hc_engine_last_stats(self._h, op))
         keys = ("step_ms", "h2d_bytes", "d2h_bytes", "recompute_rows", "recompute_ms", "attn_ms", "gemm_ms",
-                "launches")
+                "launches", "copy_ms", "recompute_launches")
         return dict(zip(keys, out.tolist()))
+
+    def set_profile(self, on: bool = True) -> None:
+        check(lib().hc_engine_set_profile(self._h, int(on)))
 
     def time_kv_gen(self, n_tokens: int, reps: int = 5) -> float:
         s = C.c_double()

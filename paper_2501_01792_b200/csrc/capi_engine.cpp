@@ -76,6 +76,7 @@ EngineOptions opts_of(const hc_engine_options* o) {
     e.scaled = o->scaled;
     e.max_prefill_tokens = o->max_prefill_tokens > 0 ? o->max_prefill_tokens : 65536;
     e.device = o->device;
+    e.weight_layers = o->weight_layers;
     return e;
 }
 
@@ -354,10 +355,14 @@ int hc_engine_captured_inputs(void* e, uint16_t* out, long count) {
 int hc_engine_last_stats(void* e, double* o) {
     return hc_guard([&] {
         const StepStats& s = eng(e)->last_stats();
-        const double v[8] = {s.step_ms, s.h2d_bytes, s.d2h_bytes, s.recompute_tokens, s.recompute_ms,
-                             s.attn_ms, s.gemm_ms, static_cast<double>(s.launches)};
+        const double v[10] = {s.step_ms, s.h2d_bytes, s.d2h_bytes, s.recompute_tokens, s.recompute_ms,
+                              s.attn_ms, s.gemm_ms, static_cast<double>(s.launches), s.copy_ms,
+                              static_cast<double>(s.recompute_launches)};
         std::memcpy(o, v, sizeof v);
     });
+}
+int hc_engine_set_profile(void* e, int on) {
+    return hc_guard([&] { eng(e)->set_profile(on != 0); });
 }
 int hc_engine_time_kv_gen(void* e, int n_tokens, int reps, double* seconds) {
     return hc_guard([&] { *seconds = eng(e)->time_kv_gen(n_tokens, reps); });

@@ -72,7 +72,7 @@ T* halloc(size_t n, bool mapped) {
 }  // namespace
 
 struct Engine::Impl {
-    int L = 0, d = 0, H = 0, hd = 0, f = 0, V = 0, tpb = 0, B = 0, max_seq = 0, max_blocks = 0, Lp = 0;
+    int L = 0, d = 0, H = 0, hd = 0, f = 0, V = 0, tpb = 0, B = 0, max_seq = 0, max_blocks = 0, Lp = 0, Lw = 0;
     size_t LE = 0, kvb = 0, actb = 0;
     LayerOffsets off{};
     bf16 *emb = nullptr, *pos = nullptr;
@@ -96,6 +96,32 @@ struct Engine::Impl {
     size_t prefill_rows = 0;
     cudaEvent_t loaded[2]{}, consumed[2]{}, ev0{}, ev1{};
     bool pools_filled = false;
+    // profiling: timing events handed out per step
+    std::vector<cudaEvent_t> pev;
+    size_t pev_used = 0;
+    cudaEvent_t take_event() {
+        if (pev_used == pev.size()) {
+            cudaEvent_t e;
+            HC_CUDA(cudaEventCreate(&e));
+            pev.push_back(e);
+        }
+        return pev[pev_used++];
+    }
+    struct Span {
+        int kind;  // 0 recompute, 1 attention, 2 other gemm, 3 copy
+        cudaEvent_t a, b;
+    };
+    std::vector<Span> spans;
+    void span_begin(bool on, cudaStream_t s, int kind) {
+        if (!on) return;
+        spans.push_back({kind, take_event(), nullptr});
+        HC_CUDA(cudaEventRecord(spans.back().a, s));
+    }
+    void span_end(bool on, cudaStream_t s) {
+        if (!on) return;
+        spans.back().b = take_event();
+        HC_CUDA(cudaEventRecord(spans.back().b, s));
+    }
 
     void regions(int l, int slot, bf16* r[16]) const {
         for (int i = 0; i < 16; ++i) r[i] = nullptr;
@@ -197,6 +223,7 @@ void Engine::init(const ModelConfig& c, int w_max_seq, const uint16_t* emb, cons
     m.max_seq = opt_.max_seq > 0 ? std::min(opt_.max_seq, w_max_seq) : w_max_seq;
     m.max_blocks = (m.max_seq + m.tpb - 1) / m.tpb;
     m.Lp = opt_.host_layers > 0 ? std::min(opt_.host_layers, m.L) : m.L;
+    m.Lw = opt_.weight_layers > 0 ? std::min(opt_.weight_layers, m.L) : m.L;
     m.off = LayerOffsets::of(cfg_);
     m.LE = m.off.total;
     m.kvb = static_cast<size_t>(2) * m.d * m.tpb;
@@ -236,8 +263,8 @@ void Engine::init(const ModelConfig& c, int w_max_seq, const uint16_t* emb, cons
             HC_CUDA(cudaMemcpy(m.w_all + static_cast<size_t>(l) * m.LE, tmp.data(), m.LE * 2, cudaMemcpyHostToDevice));
         }
     } else {
-        m.h_w = halloc<uint16_t>(m.LE * m.L, false);
-        for (int l = 0; l < m.L; ++l) fill_layer(ctx, l, m.h_w + static_cast<size_t>(l) * m.LE);
+        m.h_w = halloc<uint16_t>(m.LE * m.Lw, false);
+        for (int l = 0; l < m.Lw; ++l) fill_layer(ctx, l, m.h_w + static_cast<size_t>(l) * m.LE);
         m.wbuf[0] = dalloc<bf16>(m.LE);
         m.wbuf[1] = dalloc<bf16>(m.LE);
     }
@@ -283,6 +310,7 @@ Engine::~Engine() {
     }
     cudaEventDestroy(m.ev0);
     cudaEventDestroy(m.ev1);
+    for (cudaEvent_t e : m.pev) cudaEventDestroy(e);
     cudaStreamDestroy(s_compute_);
     cudaStreamDestroy(s_copy_);
 }
@@ -383,7 +411,7 @@ void Engine::prefill(const std::vector<std::string>& ids, const std::vector<std:
             const int slot = l & 1;
             if (!m.w_all) {
                 HC_CUDA(cudaStreamWaitEvent(s_copy_, m.consumed[slot]));
-                HC_CUDA(cudaMemcpyAsync(m.wbuf[slot], m.h_w + static_cast<size_t>(l) * m.LE, m.LE * 2,
+                HC_CUDA(cudaMemcpyAsync(m.wbuf[slot], m.h_w + static_cast<size_t>(l % m.Lw) * m.LE, m.LE * 2,
                                         cudaMemcpyHostToDevice, s_copy_));
                 HC_CUDA(cudaEventRecord(m.loaded[slot], s_copy_));
                 HC_CUDA(cudaStreamWaitEvent(s_compute_, m.loaded[slot]));
@@ -529,6 +557,8 @@ void Engine::decode_step(const std::vector<std::string>& ids, const int* tokens,
     const int* dm = m.d_meta;
 
     StepStats st{};
+    m.pev_used = 0;
+    m.spans.clear();
     const bool stream_any = !m.w_all || !kv_runs.empty() || !act_runs.empty();
     HC_CUDA(cudaEventRecord(m.ev0, s_compute_));
     HC_CUDA(cudaMemcpyAsync(m.d_meta, m.h_meta, meta.size() * 4, cudaMemcpyHostToDevice, s_compute_));
@@ -543,8 +573,9 @@ void Engine::decode_step(const std::vector<std::string>& ids, const int* tokens,
             // copy stream: weights + this layer's host blocks into slot l%2,
             // after compute released the slot (layer l-2)
             HC_CUDA(cudaStreamWaitEvent(s_copy_, m.consumed[slot]));
+            m.span_begin(profile_, s_copy_, 3);
             if (!m.w_all) {
-                HC_CUDA(cudaMemcpyAsync(m.wbuf[slot], m.h_w + static_cast<size_t>(l) * m.LE, m.LE * 2,
+                HC_CUDA(cudaMemcpyAsync(m.wbuf[slot], m.h_w + static_cast<size_t>(l % m.Lw) * m.LE, m.LE * 2,
                                         cudaMemcpyHostToDevice, s_copy_));
                 st.h2d_bytes += m.LE * 2.0;
             }
@@ -563,6 +594,7 @@ void Engine::decode_step(const std::vector<std::string>& ids, const int* tokens,
                                         cudaMemcpyHostToDevice, s_copy_));
                 st.h2d_bytes += bytes;
             }
+            m.span_end(profile_, s_copy_);
             HC_CUDA(cudaEventRecord(m.loaded[slot], s_copy_));
             HC_CUDA(cudaStreamWaitEvent(s_compute_, m.loaded[slot]));
         }
@@ -612,12 +644,15 @@ void Engine::decode_step(const std::vector<std::string>& ids, const int* tokens,
             c.d = m.d;
             c.hd = m.hd;
             c.blk_off = which == 0 ? static_cast<int>(m.act_gpu_cap) : 0;
-            if (profile_) HC_CUDA(cudaEventRecord(m.ev1, s_compute_));
+            m.span_begin(profile_, s_compute_, 0);
             run_gemm(c, s_compute_);
+            m.span_end(profile_, s_compute_);
             st.launches += 1;
             st.recompute_tokens += static_cast<double>(tl.size()) * gemm::BM;
         }
+        m.span_begin(profile_, s_compute_, 2);
         gemm_rows(gemm::kStore, xin, n, m.d, W + m.off.wqkv, 3 * m.d, m.qkv, 3 * m.d, s_compute_);
+        m.span_end(profile_, s_compute_);
         if (any_kv) {  // new token's K|V -> its KV slot (device + host)
             ap.src = m.qkv;
             ap.ld = 3 * m.d;
@@ -642,10 +677,14 @@ void Engine::decode_step(const std::vector<std::string>& ids, const int* tokens,
         a.scale = scale;
         a.work = m.attn_work;
         a.splits = splits;
+        m.span_begin(profile_, s_compute_, 1);
         decode_attention(a, s_compute_);
+        m.span_end(profile_, s_compute_);
+        m.span_begin(profile_, s_compute_, 2);
         gemm_rows(gemm::kStore, m.att, n, m.d, W + m.off.wproj, m.d, m.proj, m.d, s_compute_);
         gemm_rows(gemm::kRelu, m.proj, n, m.d, W + m.off.w1, m.f, m.hbuf, m.f, s_compute_);
         gemm_rows(gemm::kStore, m.hbuf, n, m.f, W + m.off.w2, m.d, xout, m.d, s_compute_);
+        m.span_end(profile_, s_compute_);
         st.launches += 4 + (splits > 1 ? 2 : 1);
         HC_CUDA(cudaEventRecord(m.consumed[slot], s_compute_));
     }
@@ -671,6 +710,20 @@ void Engine::decode_step(const std::vector<std::string>& ids, const int* tokens,
     float ms = 0;
     HC_CUDA(cudaEventElapsedTime(&ms, m.ev0, m.ev1));
     st.step_ms = ms;
+    for (const auto& sp : m.spans) {
+        float t = 0;
+        HC_CUDA(cudaEventElapsedTime(&t, sp.a, sp.b));
+        if (sp.kind == 0) {
+            st.recompute_ms += t;
+            st.recompute_launches += 1;
+        } else if (sp.kind == 1) {
+            st.attn_ms += t;
+        } else if (sp.kind == 2) {
+            st.gemm_ms += t;
+        } else {
+            st.copy_ms += t;
+        }
+    }
     for (int b = 0; b < n; ++b) {
         if (act_host[b] >= 0) st.d2h_bytes += static_cast<double>(m.d) * 2 * m.L;
         if (kv_host[b] >= 0) st.d2h_bytes += static_cast<double>(m.d) * 4 * m.L;

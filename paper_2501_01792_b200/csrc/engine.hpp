@@ -43,6 +43,8 @@ struct EngineOptions {
     long kv_host_cap = 0, kv_gpu_cap = 0, act_host_cap = 0, act_gpu_cap = 0;
     int kv_on_gpu = 0;
     int host_layers = 0;          // Lp (0 = num_layers)
+    int weight_layers = 0;        // physical pinned weight layers (0 = num_layers; < L folds
+                                  // layer l onto copy l % Lw — benchmark hosts with small DRAM)
     CacheMode mode = CacheMode::Hybrid;
     HostAllocation alloc{};       // hybrid-ratio setting (next_block_kind target)
     double recompute_ratio = 0.0;
@@ -58,8 +60,10 @@ struct StepStats {
     double recompute_tokens = 0;  // ACT rows recomputed (incl. padding rows)
     double recompute_ms = 0;      // summed recompute GEMM time (when profiled)
     double attn_ms = 0;
-    double gemm_ms = 0;
+    double gemm_ms = 0;           // QKV + proj + FFN GEMMs
     int launches = 0;             // kernels launched this step
+    double copy_ms = 0;           // summed copy-stream time of the H2D streams (profiled)
+    int recompute_launches = 0;
 };
 
 class Engine {

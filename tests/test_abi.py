@@ -1,0 +1,43 @@
+"""The C-ABI library loads without a GPU and exports every symbol
+include/hybridcache.h declares; the ctypes table matches the header."""
+import os
+import re
+import subprocess
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "hybridcache.h")
+
+
+def declared():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(hc_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_header_matches_ctypes_table():
+    from paper_2501_01792_b200._signatures import SIGNATURES
+    assert declared() == sorted(SIGNATURES)
+
+
+def test_library_exports_every_symbol():
+    from paper_2501_01792_b200 import _native
+    lib = _native.lib()  # loads on a CPU-only host
+    out = subprocess.run(["nm", "-D", "--defined-only", _native.LIB_PATH], capture_output=True, text=True).stdout
+    exported = set(re.findall(r"\bT (hc_[a-z0-9_]+)", out))
+    missing = [s for s in declared() if s not in exported]
+    assert not missing, missing
+    for s in declared():
+        assert getattr(lib, s) is not None
+    assert lib.hc_abi_version() == 1
+
+
+def test_no_gpu_compute_fails_loudly():
+    """Without a device the compute entry points return status 4 (no CPU
+    fallback); bookkeeping works."""
+    from paper_2501_01792_b200 import HcError, kernels
+    import numpy as np
+    import pytest
+    if kernels.device_count() > 0:
+        pytest.skip("GPU present")
+    with pytest.raises(HcError):
+        kernels.gemm_bf16(np.zeros((128, 64), np.uint16), np.zeros((64, 64), np.uint16))

@@ -1,0 +1,238 @@
+"""The product's host logic (C++ behind the C ABI, no GPU needed) against the
+reference's golden fixtures and the oracle: block tables and pbns bit-exact,
+planner / fits bit-exact, weight generation bit-exact to the oracle's bf16."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import hybridsim_oracle as O
+from paper_2501_01792_b200 import CapacityError, ConfigError, InputError, api
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+@pytest.fixture(scope="module")
+def gjson():
+    with open(os.path.join(GOLD, "golden.json")) as fh:
+        return json.load(fh)
+
+
+def replay(args):
+    """The simulator's add_token order on the product's HybridCache."""
+    a, k, g = args["act_host"], args["kv_host"], args["act_gpu"]
+    mode = args["mode"]
+    if mode == "kv_only":
+        k += a // 2
+        a, g = 0, 0
+    elif mode == "act_only":
+        a += 2 * k
+        k = 0
+    c = api.HybridCache(args["tpb"], api.PoolCaps(k, 0, a, g))
+    alloc = api.HostAllocation(a, k)
+    ids = [f"r{i}" for i in range(len(args["lens"]))]
+    for rid, n in zip(ids, args["lens"]):
+        c.create_request(rid, n)
+
+    def add(rid):
+        if c.context_len(rid) % args["tpb"] == 0:
+            if mode == "hybrid":
+                kind = api.next_block_kind(*c.blocks_by_kind(rid), alloc)
+            else:
+                kind = api.BlockKind.ACT if mode == "act_only" else api.BlockKind.KV
+            c.append_block(rid, kind)
+        c.fill_token(rid)
+
+    for rid, n in zip(ids, args["lens"]):
+        for _ in range(n):
+            add(rid)
+    for it in range(max(args["gens"])):
+        for rid, gl in zip(ids, args["gens"]):
+            if it < gl:
+                add(rid)
+    for rid in args.get("frees", []):
+        c.free_request(rid)
+    return c
+
+
+def test_block_tables_bit_exact(gjson):
+    for case in gjson["block_tables"]:
+        c = replay(case["args"])
+        assert c.dump_json() == O.dumps(case["dump"])
+        # the same document parsed, entry by entry
+        for req in case["dump"]["requests"]:
+            t = c.table(req["id"])
+            assert [(str(e.kind), str(e.location), e.pbn, e.filled_tokens) for e in t.entries] == \
+                   [(e["kind"], e["location"], e["pbn"], e["filled"]) for e in req["entries"]]
+
+
+def test_next_block_kind(gjson):
+    for a, k, ah, kh, want in gjson["next_block_kind"]:
+        assert str(api.next_block_kind(a, k, api.HostAllocation(ah, kh))) == want
+    with pytest.raises(InputError):
+        api.next_block_kind(0, 0, api.HostAllocation())
+    with pytest.raises(InputError):
+        api.next_block_kind(-1, 0, api.HostAllocation(1, 1))
+
+
+def test_planner_bit_exact(gjson):
+    for c in gjson["plan"]:
+        b = api.TimingBundle(api.LinearTimeModel(c["bundle"][0], c["bundle"][1]),
+                             api.LinearTimeModel(c["bundle"][2], c["bundle"][3]), c["bundle"][4])
+        mem = api.MemoryBudget(*c["mem"])
+        assert list(api.initial_cache_allocation(b, c["tpb"], c["act_gpu"])) == c["init"]
+        if c["err"] is not None:
+            with pytest.raises(CapacityError):
+                api.plan_host_allocation(b, mem, c["tpb"], c["act_gpu"])
+            continue
+        a = api.plan_host_allocation(b, mem, c["tpb"], c["act_gpu"])
+        assert [a.act_host, a.kv_host, a.act_init, a.kv_init, a.act_remain, a.kv_remain] == c["alloc"]
+
+
+def test_planner_worked_examples():
+    B = lambda ks, ki, ls, li, w: api.TimingBundle(api.LinearTimeModel(ks, ki), api.LinearTimeModel(ls, li), w)
+    assert api.initial_cache_allocation(B(1e-5, 0, 4e-6, 0, 0.01), 16, 0) == (62, 0)
+    assert api.initial_cache_allocation(B(1e-5, 0, 4e-6, 0, 0.01008), 16, 88) == (0, 62)
+    assert api.alloc_remaining(B(2e-5, 0, 1e-5, 0, 0), api.MemoryBudget(500, 0, 2, 1), 16, 0, 0) == (100, 200)
+    with pytest.raises(CapacityError):
+        api.alloc_remaining(B(1e-5, 0, 1e-5, 0, 0), api.MemoryBudget(100, 90, 2, 1), 16, 20, 0)
+    a = api.plan_host_allocation(B(1e-5, 0, 4e-6, 0, 0.01), api.MemoryBudget(1e6, 0, 4, 2), 16, 0)
+    assert (a.act_init, a.kv_init) == (62, 0) and 2 * a.act_host + 4 * a.kv_host <= 1e6
+
+
+def test_fit_linear_and_bundle(gjson):
+    for c in gjson["fit_linear"]:
+        m = api.fit_linear(list(zip(c["x"], c["y"])))
+        assert [m.slope, m.intercept, m.r_squared, float(m.intercept_clamped)] == c["fit"]
+    with pytest.raises(InputError):
+        api.fit_linear([(1.0, 1.0)])
+    cfg = api.ModelConfig.preset("opt-30b")
+    b = api.bundle_from_samples([(64, 1e-4), (128, 2e-4)], [(64, 3e-5), (128, 6e-5)], 55e9, cfg)
+    per, total = api.weight_bytes(cfg)
+    assert b.s_weight_layer == per and b.t_load_w == per / 55e9
+    assert abs(b.t_kv_gen.slope - 1e-4 / 64) < 1e-18
+
+
+def test_flops_and_bytes(gjson):
+    for kind, d, f, n, k, L, want in gjson["flops"]:
+        cfg = api.ModelConfig(num_layers=L, hidden_dim=d, ffn_dim=f)
+        assert api.flop_count(kind, cfg, n, k) == want
+    for d, tpb, kv, act in gjson["bytes_of"]:
+        cfg = api.ModelConfig(hidden_dim=d, tokens_per_block=tpb)
+        assert (api.HybridCache.bytes_of("KV", cfg), api.HybridCache.bytes_of("ACT", cfg)) == (kv, act)
+
+
+def test_cache_reference_unit_cases():
+    """test_cache.cpp:35-141 on the product's cache."""
+    c = api.HybridCache(16, api.PoolCaps(10, 0, 10, 2))
+    c.create_request("r", 0)
+    locs = []
+    for kind in ("ACT", "ACT", "ACT", "KV"):
+        e = c.append_block("r", kind)
+        for _ in range(16):
+            c.fill_token("r")
+        locs.append(str(e.location))
+    assert locs == ["gpu", "gpu", "host", "host"]
+    with pytest.raises(InputError):
+        c.create_request("r", 1)
+    t = api.HybridCache(16, api.PoolCaps(1, 0, 0, 0))
+    t.create_request("x", 0)
+    with pytest.raises(InputError):
+        t.fill_token("x")
+    t.append_block("x", "KV")
+    with pytest.raises(InputError):
+        t.append_block("x", "KV")            # last block not full
+    for _ in range(16):
+        t.fill_token("x")
+    with pytest.raises(InputError):
+        t.fill_token("x")
+    with pytest.raises(CapacityError):
+        t.append_block("x", "KV")
+    assert len(t.table("x").entries) == 1
+    kv = api.HybridCache(16, api.PoolCaps(4, 1, 0, 0), kv_on_gpu=True)
+    kv.create_request("k", 0)
+    assert str(kv.append_block("k", "KV").location) == "gpu"
+    f = api.HybridCache(16, api.PoolCaps(8, 0, 8, 4))
+    f.create_request("r", 0)
+    for kind in ["KV"] * 5 + ["ACT"] * 6:
+        f.append_block("r", kind)
+        for _ in range(16):
+            f.fill_token("r")
+    assert f.free_blocks("KV", "host") == 3
+    f.free_request("r")
+    assert (f.free_blocks("KV", "host"), f.free_blocks("ACT", "gpu"), f.free_blocks("ACT", "host")) == (8, 4, 8)
+    with pytest.raises(InputError):
+        f.free_request("r")
+    with pytest.raises(InputError):
+        api.HybridCache(0)
+
+
+def test_cache_fuzz_against_oracle():
+    """test_cache.cpp:143-201 style fuzz: every op on the product cache and the
+    oracle cache gives identical results and identical tables."""
+    rng = O.SplitMix64(2024)
+    prod = api.HybridCache(8, api.PoolCaps(30, 0, 30, 10))
+    orac = O.HybridCache(8, kv_host=30, act_host=30, act_gpu=10)
+    live, nxt = [], 0
+    for step in range(1500):
+        op = rng.uniform_int(0, 3)
+        res = []
+        for c in (prod, orac):
+            try:
+                if op == 0:
+                    c.create_request(f"q{nxt}", 0)
+                    res.append("ok")
+                elif live:
+                    rid = live[rng.uniform_int(0, len(live) - 1) if c is prod else pick]
+                    if op == 1:
+                        kind = "ACT" if (kbit if c is orac else rng.uniform01() < 0.5) else "KV"
+                        if c is prod:
+                            kbit = kind == "ACT"
+                        e = c.append_block(rid, kind)
+                        res.append((str(e.location), e.pbn))
+                    elif op == 2:
+                        c.fill_token(rid)
+                        res.append("ok")
+                    else:
+                        c.free_request(rid)
+                        res.append("ok")
+                else:
+                    res.append("skip")
+                if c is prod and live and op != 0:
+                    pick = live.index(rid)
+            except (CapacityError, InputError, O.CapacityError, O.InputError) as e:
+                res.append(type(e).__name__)
+                if c is prod and live and op != 0:
+                    pick = live.index(rid)
+        assert res[0] == res[1], (step, res)
+        if op == 0:
+            live.append(f"q{nxt}")
+            nxt += 1
+        elif live and op == 3 and res[0] == "ok":
+            live.remove(rid)
+    assert prod.dump_json() == O.dumps(orac.dump_json())
+
+
+def test_generate_weights_bit_exact_to_oracle():
+    """C++ generate + rescale + bf16 (device layout) == oracle's bf16 bits."""
+    cfg = api.ModelConfig(num_layers=2, hidden_dim=64, num_heads=2, ffn_dim=128, vocab_size=96)
+    w = api.generate_weights(cfg, 42, 24, rescale=True)
+    ocfg = O.ModelConfig(num_layers=2, hidden_dim=64, num_heads=2, ffn_dim=128, vocab_size=96).validate()
+    ow = O.prepare_weights(O.generate_weights(ocfg, 42, 24))
+    assert np.array_equal(w["embedding"], O.to_bf16_bits(ow.embedding))
+    assert np.array_equal(w["positional"], O.to_bf16_bits(ow.positional))
+    for l in range(2):
+        lay = api.unpack_layer(cfg.validate(), w["layers"][l])
+        for n in O.WEIGHT_NAMES:
+            assert np.array_equal(lay[n], O.to_bf16_bits(ow.layers[l][n])), n
+
+
+def test_model_config_validation():
+    with pytest.raises(InputError):
+        api.ModelConfig(hidden_dim=30, num_heads=4).validate()
+    with pytest.raises(InputError):
+        api.ModelConfig.preset("opt-1t")
+    c = api.ModelConfig(hidden_dim=64).validate()
+    assert c.ffn_dim == 256
+    assert api.ModelConfig.preset("opt-66b").num_layers == 64

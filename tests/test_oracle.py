@@ -1,0 +1,216 @@
+"""Pins the CPU oracle (oracle/hybridsim_oracle.py) to the reference:
+golden fixtures produced by the unmodified reference (tests/golden/
+make_golden.py) plus the reference's own known-answer tests."""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+import hybridsim_oracle as O
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+@pytest.fixture(scope="module")
+def gnpz():
+    return np.load(os.path.join(GOLD, "golden.npz"))
+
+
+@pytest.fixture(scope="module")
+def gjson():
+    with open(os.path.join(GOLD, "golden.json")) as fh:
+        return json.load(fh)
+
+
+def rel(a, b):
+    return float(np.abs(a - b).max() / max(np.abs(b).max(), 1e-300))
+
+
+def test_generator_bit_exact(gnpz):
+    """DecoderWeights::generate draws (model.cpp:94-117) reproduced bit-for-bit."""
+    cfg = O.ModelConfig(num_layers=2, hidden_dim=32, num_heads=4, ffn_dim=64, vocab_size=50,
+                        tokens_per_block=4).validate()
+    w = O.generate_weights(cfg, 42, 40)
+    assert np.array_equal(w.embedding, gnpz["toy/raw/emb"])
+    assert np.array_equal(w.positional, gnpz["toy/raw/pos"])
+    for l in range(2):
+        for n in O.WEIGHT_NAMES:
+            assert np.array_equal(w.layers[l][n], gnpz[f"toy/raw/{n}{l}"])
+
+
+@pytest.mark.parametrize("tag,shape,seed,max_seq,prepared", [
+    ("toy", (2, 32, 4, 64, 50, 4), 42, 40, False),
+    ("toy_rescaled", (3, 256, 2, 512, 512, 16), 7, 40, True),
+    ("opt125m_shape", (12, 768, 12, 3072, 50272, 16), 42, 160, True),
+])
+def test_decoder_numerics_match_reference(gnpz, tag, shape, seed, max_seq, prepared):
+    """forward_prompt / generation_step / recompute_kv_from_activation vs the
+    reference's fp64 outputs (decoder.cpp:123-174)."""
+    L, d, H, f, V, tpb = shape
+    cfg = O.ModelConfig(num_layers=L, hidden_dim=d, num_heads=H, ffn_dim=f, vocab_size=V,
+                        tokens_per_block=tpb).validate()
+    w = O.generate_weights(cfg, seed, max_seq)
+    if prepared:
+        w = O.prepare_weights(w)
+    ids = gnpz[f"{tag}/ids"].tolist()
+    tr = O.forward_prompt(ids, w)
+    assert rel(tr.output, gnpz[f"{tag}/output"]) < 1e-10
+    for l in range(L):
+        assert rel(tr.layer_inputs[l], gnpz[f"{tag}/layer_inputs"][l]) < 1e-10
+        assert rel(tr.k[l], gnpz[f"{tag}/k"][l]) < 1e-10
+        assert rel(tr.v[l], gnpz[f"{tag}/v"][l]) < 1e-10
+    tok = int(gnpz[f"{tag}/gen_token"][0])
+    st = O.generation_step(tok, len(ids), tr.k, tr.v, w)
+    assert rel(st.output, gnpz[f"{tag}/gen_output"]) < 1e-10
+    assert rel(np.concatenate(st.new_k), gnpz[f"{tag}/gen_k"]) < 1e-10
+    k, v = O.recompute_kv_from_activation(tr.layer_inputs[L - 1], L - 1, w)
+    assert rel(k, gnpz[f"{tag}/recompute_k"]) < 1e-10
+    assert rel(v, gnpz[f"{tag}/recompute_v"]) < 1e-10
+
+
+def test_generation_step_equals_forward_row():
+    """Decode-time X / new K,V equal forward_prompt on the extended sequence
+    (SURVEY.md probe3; the ACT writer's decode-time oracle)."""
+    cfg = O.ModelConfig(num_layers=3, hidden_dim=32, num_heads=4, ffn_dim=64, vocab_size=40).validate()
+    w = O.prepare_weights(O.generate_weights(cfg, 3, 32))
+    ids = [1, 5, 9, 2, 33, 7]
+    tr = O.forward_prompt(ids, w)
+    st = O.generation_step(11, len(ids), tr.k, tr.v, w)
+    full = O.forward_prompt(ids + [11], w)
+    assert rel(st.output, full.output[-1:]) < 1e-12
+    for l in range(3):
+        assert rel(st.layer_inputs[l], full.layer_inputs[l][-1:]) < 1e-12
+        assert rel(st.new_k[l], full.k[l][-1:]) < 1e-12
+
+
+def test_block_tables_bit_exact(gjson):
+    """add_token replay (sim.cpp:194-223, 308-310) -> identical dump_json."""
+    for case in gjson["block_tables"]:
+        a = case["args"]
+        ba = O.BlockAssigner(a["tpb"], a["mode"], O.HostAllocation(a["act_host"], a["kv_host"]), a["act_gpu"])
+        ids = [f"r{i}" for i in range(len(a["lens"]))]
+        for rid, n in zip(ids, a["lens"]):
+            ba.add_request(rid, n)
+        for rid, n in zip(ids, a["lens"]):
+            for _ in range(n):
+                ba.add_token(rid)
+        for it in range(max(a["gens"])):
+            for rid, g in zip(ids, a["gens"]):
+                if it < g:
+                    ba.add_token(rid)
+        for rid in a.get("frees", []):
+            ba.cache.free_request(rid)
+        assert ba.cache.dump_json() == case["dump"]
+
+
+def test_survey_golden_tables():
+    """SURVEY.md §8(a) golden block table for config 1 (probe7)."""
+    ba = O.assign_batch(16, [128] * 4, [32] * 4, O.HYBRID, O.HostAllocation(40, 40), act_gpu=6)
+    r0 = " ".join(f"{e['kind']}/{e['location']}#{e['pbn']}" for e in ba.cache.dump_json()["requests"][0]["entries"])
+    assert r0 == ("ACT/gpu#0 KV/host#0 ACT/gpu#1 KV/host#1 ACT/gpu#2 KV/host#2 ACT/gpu#3 KV/host#3 "
+                  "ACT/host#10 KV/host#16")
+
+
+def test_next_block_kind(gjson):
+    for a, k, ah, kh, want in gjson["next_block_kind"]:
+        assert O.next_block_kind(a, k, O.HostAllocation(ah, kh)) == want
+    # test_plan.cpp:192-205
+    assert O.next_block_kind(5, 2, O.HostAllocation(300, 100)) == O.ACT
+    with pytest.raises(O.InputError):
+        O.next_block_kind(0, 0, O.HostAllocation())
+    # test_plan.cpp:207-223: running share within one block of the target
+    rng = O.SplitMix64(31337)
+    for _ in range(10):
+        al = O.HostAllocation(rng.uniform_int(1, 1000), rng.uniform_int(1, 1000))
+        target = al.act_host / (al.act_host + al.kv_host)
+        act = kv = 0
+        for _ in range(10000):
+            if O.next_block_kind(act, kv, al) == O.ACT:
+                act += 1
+            else:
+                kv += 1
+        assert abs(act - target * 10000) <= 1.0
+
+
+def test_planner_bit_exact(gjson):
+    for c in gjson["plan"]:
+        b = O.TimingBundle(O.LinearTimeModel(c["bundle"][0], c["bundle"][1]),
+                           O.LinearTimeModel(c["bundle"][2], c["bundle"][3]), c["bundle"][4])
+        mem = O.MemoryBudget(*c["mem"])
+        assert list(O.initial_cache_allocation(b, c["tpb"], c["act_gpu"])) == c["init"]
+        if c["err"] is not None:
+            with pytest.raises(O.CapacityError):
+                O.plan_host_allocation(b, mem, c["tpb"], c["act_gpu"])
+            continue
+        a = O.plan_host_allocation(b, mem, c["tpb"], c["act_gpu"])
+        assert [a.act_host, a.kv_host, a.act_init, a.kv_init, a.act_remain, a.kv_remain] == c["alloc"]
+
+
+def test_planner_worked_examples():
+    """test_plan.cpp:55-110 known answers."""
+    def bundle(ks, ki, ls, li, w):
+        return O.TimingBundle(O.LinearTimeModel(ks, ki), O.LinearTimeModel(ls, li), w)
+    assert O.initial_cache_allocation(bundle(1e-5, 0, 4e-6, 0, 0.01), 16, 0) == (62, 0)
+    assert O.initial_cache_allocation(bundle(1e-5, 0, 4e-6, 0, 0.01), 10, 100) == (0, 0)
+    assert O.initial_cache_allocation(bundle(1e-5, 0, 4e-6, 0, 0.01008), 16, 88) == (0, 62)
+    assert O.alloc_remaining(bundle(1e-5, 0, 1e-5, 0, 0), O.MemoryBudget(300, 0, 2, 1), 16, 0, 0) == (100, 100)
+    assert O.alloc_remaining(bundle(2e-5, 0, 1e-5, 0, 0), O.MemoryBudget(500, 0, 2, 1), 16, 0, 0) == (100, 200)
+    assert O.alloc_remaining(bundle(1e-5, 5, 1e-5, 0, 0), O.MemoryBudget(100, 0, 2, 1), 16, 0, 0) == (0, 50)
+    assert O.alloc_remaining(bundle(1e-5, 0, 1e-5, 5, 0), O.MemoryBudget(100, 0, 2, 1), 16, 0, 0) == (100, 0)
+    with pytest.raises(O.CapacityError):
+        O.alloc_remaining(bundle(1e-5, 0, 1e-5, 0, 0), O.MemoryBudget(100, 90, 2, 1), 16, 20, 0)
+
+
+def test_fit_linear(gjson):
+    for c in gjson["fit_linear"]:
+        m = O.fit_linear(list(zip(c["x"], c["y"])))
+        assert [m.slope, m.intercept, m.r_squared, float(m.intercept_clamped)] == c["fit"]
+    with pytest.raises(O.InputError):
+        O.fit_linear([(1.0, 1.0), (1.0, 2.0)])
+
+
+def test_flops_and_bytes(gjson):
+    for kind, d, f, n, k, L, want in gjson["flops"]:
+        cfg = O.ModelConfig(num_layers=L, hidden_dim=d, ffn_dim=f).validate()
+        assert O.flop_count(kind, cfg, n, k) == want
+    for d, tpb, kv, act in gjson["bytes_of"]:
+        cfg = O.ModelConfig(hidden_dim=d, tokens_per_block=tpb)
+        assert (O.bytes_of(O.KV, cfg), O.bytes_of(O.ACT, cfg)) == (kv, act)
+    # test_decoder.cpp:229-235, test_cache.cpp:203-217
+    assert O.flop_count(O.KVGEN, O.ModelConfig(hidden_dim=4096, num_heads=32, num_layers=48).validate(), 1) == 67108864.0
+    c30 = O.preset("opt-30b")
+    c30.tokens_per_block = 1
+    per_tok = O.bytes_of(O.KV, c30) * c30.num_layers
+    assert O.bytes_of(O.KV, c30) == 28672 and O.bytes_of(O.ACT, c30) == 14336
+    assert abs(per_tok * 1024 * 16 / 2 ** 30 / 21.0 - 1) <= 0.10
+    assert abs(per_tok * 1024 * 128 / 2 ** 30 / 168.0 - 1) <= 0.10
+
+
+def test_reference_equivalence_property(gjson):
+    """run_equivalence_case (verify.cpp:26-95): all 4 context assemblies are
+    bit-identical in the reference — the property the GPU path keeps at bf16."""
+    for seed, dev, exact in gjson["equivalence"]:
+        assert exact and dev == 0.0
+
+
+def test_cache_error_paths():
+    """test_cache.cpp:35-141"""
+    c = O.HybridCache(16, kv_host=1)
+    c.create_request("r", 0)
+    with pytest.raises(O.InputError):
+        c.fill_token("r")
+    c.append_block("r", O.KV)
+    for _ in range(16):
+        c.fill_token("r")
+    with pytest.raises(O.CapacityError):
+        c.append_block("r", O.KV)
+    with pytest.raises(O.CapacityError):
+        c.append_block("r", O.ACT)
+    assert len(c.table("r").entries) == 1
+    with pytest.raises(O.InputError):
+        c.create_request("r", 1)
+    c.free_request("r")
+    with pytest.raises(O.InputError):
+        c.free_request("r")
