@@ -138,6 +138,18 @@ int hc_engine_admit_synthetic(void* engine, int n, const char* const* ids, const
 int hc_engine_decode_step(void* engine, int n, const char* const* ids, const int* tokens, uint16_t* x_out,
                           float* logits, int* argmax);
 int hc_engine_free_request(void* engine, const char* id);
+/* Drop all requests and rebuild the pools / ratio setting (weights kept). */
+int hc_engine_configure_cache(void* engine, long kv_host, long kv_gpu, long act_host, long act_gpu, int kv_on_gpu,
+                              int mode, long alloc_act_host, long alloc_kv_host, int host_layers);
+/* forward_prompt (decoder.cpp:144-157) of one sequence without cache effects:
+ * layer_inputs / k / v [L x n x d], out [n x d] (bf16); any may be NULL.
+ * token_recompute_kv(ids, layer) (decoder.cpp:131-142) = (k, v)[layer]. */
+int hc_engine_forward_trace(void* engine, const int* ids, int n, uint16_t* layer_inputs, uint16_t* k, uint16_t* v,
+                            uint16_t* out);
+/* One layer of forward_prompt on given input rows x [n x d] (qkv_generate +
+ * attention_causal + project_ffn, decoder.cpp:150-153): k, v, out [n x d]. */
+int hc_engine_layer_forward(void* engine, int layer, const uint16_t* x, int n, uint16_t* k, uint16_t* v,
+                            uint16_t* out);
 /* Borrowed HybridCache handle of the engine (use with hc_cache_* read calls). */
 int hc_engine_cache(void* engine, void** cache);
 /* Payload of one block at one layer (KV [2][H][tpb][hd], ACT [tpb][d]). */

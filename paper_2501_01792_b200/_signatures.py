@@ -72,6 +72,9 @@ SIGNATURES = {
     "hc_engine_admit_synthetic": (i, [vp, i, cpp, ip, u64]),
     "hc_engine_decode_step": (i, [vp, i, cpp, ip, u16p, fp, ip]),
     "hc_engine_free_request": (i, [vp, cp]),
+    "hc_engine_configure_cache": (i, [vp, l, l, l, l, i, i, l, l, i]),
+    "hc_engine_forward_trace": (i, [vp, ip, i, u16p, u16p, u16p, u16p]),
+    "hc_engine_layer_forward": (i, [vp, i, u16p, i, u16p, u16p, u16p]),
     "hc_engine_cache": (i, [vp, vpp]),
     "hc_engine_read_block": (i, [vp, i, i, i, i, u16p]),
     "hc_engine_capture_inputs": (i, [vp, i]),

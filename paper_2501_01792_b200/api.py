@@ -476,6 +476,43 @@ class Engine:
     def free_request(self, rid: str) -> None:
         check(lib().hc_engine_free_request(self._h, rid.encode()))
 
+    def configure_cache(self, caps: PoolCaps, *, mode: str = "hybrid", allocation: Optional[HostAllocation] = None,
+                        kv_on_gpu: bool = False, host_layers: int = 0) -> None:
+        """Drop all requests and rebuild pools / ratio setting (weights kept)."""
+        if mode not in MODES:
+            raise InputError(f"unknown mode: {mode}")
+        a = allocation or HostAllocation(1, 1)
+        check(lib().hc_engine_configure_cache(self._h, caps.kv_host, caps.kv_gpu, caps.act_host, caps.act_gpu,
+                                              int(kv_on_gpu), MODES[mode], a.act_host, a.kv_host, host_layers))
+
+    def forward_trace(self, ids: Sequence[int]) -> dict:
+        """GPU forward_prompt (decoder.cpp:144-157): layer inputs, K, V per layer
+        and the output, as bf16 bits."""
+        n, L, d = len(ids), self.cfg.num_layers, self.cfg.hidden_dim
+        t = np.ascontiguousarray(ids, np.int32)
+        res = {k: np.zeros((L, n, d), np.uint16) for k in ("layer_inputs", "k", "v")}
+        res["output"] = np.zeros((n, d), np.uint16)
+        check(lib().hc_engine_forward_trace(self._h, ptr(t, C.c_int), n, ptr(res["layer_inputs"], C.c_uint16),
+                                            ptr(res["k"], C.c_uint16), ptr(res["v"], C.c_uint16),
+                                            ptr(res["output"], C.c_uint16)))
+        return res
+
+    def layer_forward(self, layer: int, x_bits: np.ndarray) -> dict:
+        """One layer of forward_prompt on given bf16 input rows (teacher forcing)."""
+        x = np.ascontiguousarray(x_bits, np.uint16)
+        n, d = x.shape
+        res = {k: np.zeros((n, d), np.uint16) for k in ("k", "v", "output")}
+        check(lib().hc_engine_layer_forward(self._h, layer, ptr(x, C.c_uint16), n, ptr(res["k"], C.c_uint16),
+                                            ptr(res["v"], C.c_uint16), ptr(res["output"], C.c_uint16)))
+        return res
+
+    def token_recompute_kv(self, ids: Sequence[int], layer: int):
+        """token_recompute_kv (decoder.cpp:131-142) on the GPU."""
+        if layer < 0 or layer >= self.cfg.num_layers:
+            raise InputError(f"layer index out of range: {layer}")
+        tr = self.forward_trace(ids)
+        return tr["k"][layer], tr["v"][layer]
+
     def read_block(self, kind, loc, pbn: int, layer: int) -> np.ndarray:
         d, tpb, H = self.cfg.hidden_dim, self.cfg.tokens_per_block, self.cfg.num_heads
         if _kind(kind) == 0:

@@ -333,6 +333,24 @@ int hc_engine_decode_step(void* e, int n, const char* const* ids, const int* tok
                           int* argmax) {
     return hc_guard([&] { eng(e)->decode_step(ids_of(n, ids), tokens, x_out, logits, argmax); });
 }
+int hc_engine_configure_cache(void* e, long kv_host, long kv_gpu, long act_host, long act_gpu, int kv_on_gpu, int mode,
+                              long alloc_act_host, long alloc_kv_host, int host_layers) {
+    return hc_guard([&] {
+        if (mode < 0 || mode > 2) throw InputError("engine mode must be 0 hybrid, 1 kv_only, 2 act_only");
+        HostAllocation a;
+        a.act_host = alloc_act_host;
+        a.kv_host = alloc_kv_host;
+        eng(e)->configure_cache(PoolCaps{kv_host, kv_gpu, act_host, act_gpu}, kv_on_gpu != 0,
+                                static_cast<CacheMode>(mode), a, host_layers);
+    });
+}
+int hc_engine_forward_trace(void* e, const int* ids, int n, uint16_t* layer_inputs, uint16_t* k, uint16_t* v,
+                            uint16_t* out) {
+    return hc_guard([&] { eng(e)->forward_trace(std::vector<int>(ids, ids + n), layer_inputs, k, v, out); });
+}
+int hc_engine_layer_forward(void* e, int layer, const uint16_t* x, int n, uint16_t* k, uint16_t* v, uint16_t* out) {
+    return hc_guard([&] { eng(e)->layer_forward(layer, x, n, k, v, out); });
+}
 int hc_engine_free_request(void* e, const char* id) {
     return hc_guard([&] { eng(e)->free_request(sid(id)); });
 }

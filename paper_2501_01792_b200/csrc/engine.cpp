@@ -71,6 +71,9 @@ T* halloc(size_t n, bool mapped) {
 
 }  // namespace
 
+void gemm_rows(int epi, const bf16* A, int M, int K, const bf16* W, int N, void* out, long long ldc, cudaStream_t st,
+               long long lda = 0);
+
 struct Engine::Impl {
     int L = 0, d = 0, H = 0, hd = 0, f = 0, V = 0, tpb = 0, B = 0, max_seq = 0, max_blocks = 0, Lp = 0, Lw = 0;
     size_t LE = 0, kvb = 0, actb = 0;
@@ -228,16 +231,6 @@ void Engine::init(const ModelConfig& c, int w_max_seq, const uint16_t* emb, cons
     m.LE = m.off.total;
     m.kvb = static_cast<size_t>(2) * m.d * m.tpb;
     m.actb = static_cast<size_t>(m.d) * m.tpb;
-    m.kv_host_cap = opt_.kv_host_cap;
-    m.kv_gpu_cap = opt_.kv_gpu_cap;
-    m.act_host_cap = opt_.act_host_cap;
-    m.act_gpu_cap = opt_.act_gpu_cap;
-
-    cache_ = std::make_unique<HybridCache>(m.tpb, PoolCaps{m.kv_host_cap, m.kv_gpu_cap, m.act_host_cap, m.act_gpu_cap},
-                                           opt_.kv_on_gpu != 0);
-    assigner_ = std::make_unique<BlockAssigner>(*cache_, opt_.mode, opt_.alloc, opt_.recompute_ratio);
-    if (opt_.mode == CacheMode::Hybrid && opt_.alloc.act_host + opt_.alloc.kv_host <= 0)
-        throw ConfigError("Engine: hybrid mode needs a nonempty host allocation (ratio target)");
 
     HC_CUDA(cudaStreamCreateWithFlags(&s_compute_, cudaStreamNonBlocking));
     HC_CUDA(cudaStreamCreateWithFlags(&s_copy_, cudaStreamNonBlocking));
@@ -269,17 +262,6 @@ void Engine::init(const ModelConfig& c, int w_max_seq, const uint16_t* emb, cons
         m.wbuf[1] = dalloc<bf16>(m.LE);
     }
 
-    // pools
-    m.kv_gpu = dalloc<bf16>(static_cast<size_t>(m.L) * m.kv_gpu_cap * m.kvb);
-    m.act_gpu = dalloc<bf16>(static_cast<size_t>(m.L) * m.act_gpu_cap * m.actb);
-    m.kv_host = halloc<bf16>(static_cast<size_t>(m.Lp) * m.kv_host_cap * m.kvb, true);
-    m.act_host = halloc<bf16>(static_cast<size_t>(m.Lp) * m.act_host_cap * m.actb, true);
-    for (int s = 0; s < 2; ++s) {
-        m.kv_stage[s] = dalloc<bf16>(static_cast<size_t>(m.kv_host_cap) * m.kvb);
-        m.act_stage[s] = dalloc<bf16>(static_cast<size_t>(m.act_host_cap) * m.actb);
-    }
-    m.kvr = dalloc<bf16>(static_cast<size_t>(m.act_gpu_cap + m.act_host_cap) * m.kvb);
-
     // decode scratch
     m.x[0] = dalloc<bf16>(static_cast<size_t>(m.B) * m.d);
     m.x[1] = dalloc<bf16>(static_cast<size_t>(m.B) * m.d);
@@ -289,7 +271,88 @@ void Engine::init(const ModelConfig& c, int w_max_seq, const uint16_t* emb, cons
     m.hbuf = dalloc<bf16>(static_cast<size_t>(m.B) * m.f);
     m.logits = dalloc<float>(static_cast<size_t>(m.B) * m.V);
     m.amax = dalloc<int>(m.B);
+    configure_cache(PoolCaps{opt_.kv_host_cap, opt_.kv_gpu_cap, opt_.act_host_cap, opt_.act_gpu_cap}, opt_.kv_on_gpu != 0,
+                    opt_.mode, opt_.alloc, opt_.host_layers);
+}
+
+void Engine::configure_cache(const PoolCaps& caps, bool kv_on_gpu, CacheMode mode, const HostAllocation& alloc,
+                             int host_layers) {
+    Impl& m = *impl_;
+    if (mode == CacheMode::TokenRecompute)
+        throw ConfigError("Engine: token_recompute mode is modelled by the planner only (not executed)");
+    if (mode == CacheMode::Hybrid && alloc.act_host + alloc.kv_host <= 0)
+        throw ConfigError("Engine: hybrid mode needs a nonempty host allocation (ratio target)");
     HC_CUDA(cudaDeviceSynchronize());
+    for (bf16** p : {&m.kv_gpu, &m.act_gpu, &m.kvr, &m.kv_stage[0], &m.kv_stage[1], &m.act_stage[0], &m.act_stage[1]}) {
+        if (*p) cudaFree(*p);
+        *p = nullptr;
+    }
+    for (bf16** p : {&m.kv_host, &m.act_host}) {
+        if (*p) cudaFreeHost(*p);
+        *p = nullptr;
+    }
+    assigner_.reset();
+    cache_.reset();
+    opt_.kv_host_cap = caps.kv_host;
+    opt_.kv_gpu_cap = caps.kv_gpu;
+    opt_.act_host_cap = caps.act_host;
+    opt_.act_gpu_cap = caps.act_gpu;
+    opt_.kv_on_gpu = kv_on_gpu;
+    opt_.mode = mode;
+    opt_.alloc = alloc;
+    opt_.host_layers = host_layers;
+    m.kv_host_cap = caps.kv_host;
+    m.kv_gpu_cap = caps.kv_gpu;
+    m.act_host_cap = caps.act_host;
+    m.act_gpu_cap = caps.act_gpu;
+    m.Lp = host_layers > 0 ? std::min(host_layers, m.L) : m.L;
+    cache_ = std::make_unique<HybridCache>(m.tpb, caps, kv_on_gpu);
+    assigner_ = std::make_unique<BlockAssigner>(*cache_, mode, alloc, opt_.recompute_ratio);
+    m.kv_gpu = dalloc<bf16>(static_cast<size_t>(m.L) * m.kv_gpu_cap * m.kvb);
+    m.act_gpu = dalloc<bf16>(static_cast<size_t>(m.L) * m.act_gpu_cap * m.actb);
+    m.kv_host = halloc<bf16>(static_cast<size_t>(m.Lp) * m.kv_host_cap * m.kvb, true);
+    m.act_host = halloc<bf16>(static_cast<size_t>(m.Lp) * m.act_host_cap * m.actb, true);
+    for (int s = 0; s < 2; ++s) {
+        m.kv_stage[s] = dalloc<bf16>(static_cast<size_t>(m.kv_host_cap) * m.kvb);
+        m.act_stage[s] = dalloc<bf16>(static_cast<size_t>(m.act_host_cap) * m.actb);
+    }
+    m.kvr = dalloc<bf16>(static_cast<size_t>(m.act_gpu_cap + m.act_host_cap) * m.kvb);
+    m.pools_filled = false;
+    HC_CUDA(cudaDeviceSynchronize());
+}
+
+void Engine::forward_trace(const std::vector<int>& ids, uint16_t* layer_inputs, uint16_t* k, uint16_t* v,
+                           uint16_t* out) {
+    Impl& m = *impl_;
+    const int T = static_cast<int>(ids.size());
+    if (T == 0) return;
+    if (T > m.max_seq) throw InputError("embed: sequence longer than max_seq");
+    for (int t : ids)
+        if (t < 0 || t >= m.V) throw InputError("embed: token id out of range: " + std::to_string(t));
+    m.ensure_prefill(T);
+    std::vector<int> meta(ids);
+    for (int t = 0; t < T; ++t) meta.push_back(t);
+    meta.push_back(0);
+    meta.push_back(T);
+    m.ensure_meta(meta.size());
+    std::memcpy(m.h_meta, meta.data(), meta.size() * 4);
+    HC_CUDA(cudaMemcpyAsync(m.d_meta, m.h_meta, meta.size() * 4, cudaMemcpyHostToDevice, s_compute_));
+    embed(m.emb, m.pos, m.d_meta, m.d_meta + T, T, m.d, m.px[0], m.d, s_compute_);
+    run_layers(T, 0, m.L, m.d_meta + 2 * T, layer_inputs, k, v, out);
+}
+
+void Engine::layer_forward(int layer, const uint16_t* x, int T, uint16_t* k, uint16_t* v, uint16_t* out) {
+    Impl& m = *impl_;
+    if (layer < 0 || layer >= m.L) throw InputError("layer index out of range: " + std::to_string(layer));
+    if (T <= 0) return;
+    if (T > m.max_seq) throw InputError("layer_forward: more rows than max_seq");
+    m.ensure_prefill(T);
+    const int cu[2] = {0, T};
+    m.ensure_meta(2);
+    std::memcpy(m.h_meta, cu, sizeof cu);
+    HC_CUDA(cudaMemcpyAsync(m.d_meta, m.h_meta, sizeof cu, cudaMemcpyHostToDevice, s_compute_));
+    HC_CUDA(cudaMemcpyAsync(m.px[layer & 1], x, static_cast<size_t>(T) * m.d * 2, cudaMemcpyHostToDevice, s_compute_));
+    run_layers(T, layer, layer + 1, m.d_meta, nullptr, k, v, out);
 }
 
 Engine::~Engine() {
@@ -315,11 +378,51 @@ Engine::~Engine() {
     cudaStreamDestroy(s_copy_);
 }
 
+// Causal forward of T rows (one sequence) through layers [l0, l1); the input
+// is in px[l0 & 1]; captures are [l1-l0][T][d] host arrays (optional).
+void Engine::run_layers(int T, int l0, int l1, const int* d_cu, uint16_t* layer_inputs, uint16_t* k, uint16_t* v,
+                        uint16_t* out) {
+    Impl& m = *impl_;
+    const size_t per = static_cast<size_t>(T) * m.d;
+    std::vector<uint16_t> qkv_h((k || v) ? static_cast<size_t>(T) * 3 * m.d : 0);
+    for (int l = l0; l < l1; ++l) {
+        const int slot = l & 1;
+        const size_t li = static_cast<size_t>(l - l0);
+        if (!m.w_all) {
+            HC_CUDA(cudaStreamSynchronize(s_compute_));
+            HC_CUDA(cudaMemcpy(m.wbuf[slot], m.h_w + static_cast<size_t>(l % m.Lw) * m.LE, m.LE * 2,
+                               cudaMemcpyHostToDevice));
+        }
+        const bf16* W = m.layer_w(l, slot);
+        bf16* xin = m.px[l & 1];
+        bf16* xout = m.px[(l + 1) & 1];
+        if (layer_inputs)
+            HC_CUDA(cudaMemcpyAsync(layer_inputs + per * li, xin, per * 2, cudaMemcpyDeviceToHost, s_compute_));
+        gemm_rows(gemm::kStore, xin, T, m.d, W + m.off.wqkv, 3 * m.d, m.pqkv, 3 * m.d, s_compute_);
+        if (k || v) {
+            HC_CUDA(cudaMemcpyAsync(qkv_h.data(), m.pqkv, qkv_h.size() * 2, cudaMemcpyDeviceToHost, s_compute_));
+            HC_CUDA(cudaStreamSynchronize(s_compute_));
+            for (int t = 0; t < T; ++t) {
+                const uint16_t* row = qkv_h.data() + static_cast<size_t>(t) * 3 * m.d;
+                if (k) std::memcpy(k + per * li + static_cast<size_t>(t) * m.d, row + m.d, m.d * 2);
+                if (v) std::memcpy(v + per * li + static_cast<size_t>(t) * m.d, row + 2 * m.d, m.d * 2);
+            }
+        }
+        prefill_attention(m.pqkv, m.patt, d_cu, 1, T, m.H, m.hd,
+                          opt_.scaled ? 1.0f / std::sqrt(static_cast<float>(m.hd)) : 1.0f, s_compute_);
+        gemm_rows(gemm::kStore, m.patt, T, m.d, W + m.off.wproj, m.d, m.pproj, m.d, s_compute_);
+        gemm_rows(gemm::kRelu, m.pproj, T, m.d, W + m.off.w1, m.f, m.ph, m.f, s_compute_);
+        gemm_rows(gemm::kStore, m.ph, T, m.f, W + m.off.w2, m.d, xout, m.d, s_compute_);
+    }
+    if (out) HC_CUDA(cudaMemcpyAsync(out, m.px[l1 & 1], per * 2, cudaMemcpyDeviceToHost, s_compute_));
+    HC_CUDA(cudaGetLastError());
+    HC_CUDA(cudaStreamSynchronize(s_compute_));
+}
+
 // ---------------------------------------------------------------------------
 // GEMM helpers (weights transposed [out][in]; see model.hpp)
-namespace {
 void gemm_rows(int epi, const bf16* A, int M, int K, const bf16* W, int N, void* out, long long ldc, cudaStream_t st,
-               long long lda = 0) {
+               long long lda) {
     GemmCall c;
     c.epi = epi;
     c.A = A;
@@ -334,7 +437,6 @@ void gemm_rows(int epi, const bf16* A, int M, int K, const bf16* W, int N, void*
     c.ldc = ldc;
     run_gemm(c, st);
 }
-}  // namespace
 
 // ---------------------------------------------------------------------------
 void Engine::prefill(const std::vector<std::string>& ids, const std::vector<std::vector<int>>& prompts) {

@@ -91,6 +91,21 @@ public:
                      int* argmax);
     void free_request(const std::string& id);
 
+    // Drop every request and re-create the block pools with new capacities /
+    // ratio setting (weights and scratch stay): ratio sweeps on one engine.
+    void configure_cache(const PoolCaps& caps, bool kv_on_gpu, CacheMode mode, const HostAllocation& alloc,
+                         int host_layers);
+
+    // forward_prompt (decoder.cpp:144-157) of one sequence on the GPU without
+    // touching the cache: per-layer inputs X, K, V ([L][n][d]) and the output
+    // [n][d], bf16 bits. token_recompute_kv(ids, k) = (K, V)[k].
+    void forward_trace(const std::vector<int>& ids, uint16_t* layer_inputs, uint16_t* k, uint16_t* v,
+                       uint16_t* out);
+    // One layer of forward_prompt on caller-given input rows x [T x d]
+    // (qkv_generate + attention_causal + project_ffn, decoder.cpp:150-153):
+    // K, V [T x d] and the layer output [T x d]. Teacher-forced parity.
+    void layer_forward(int layer, const uint16_t* x, int T, uint16_t* k, uint16_t* v, uint16_t* out);
+
     // Payload of one block at one layer (bf16 bits; KV: [2][H][tpb][hd],
     // ACT: [tpb][d]) — for parity tests of the cache writers.
     void read_block(BlockKind kind, Location loc, int pbn, int layer, uint16_t* out);
@@ -116,6 +131,8 @@ private:
     struct Impl;
     void init(const ModelConfig& c, int max_seq, const uint16_t* emb, const uint16_t* pos,
               void (*fill_layer)(const void* ctx, int l, uint16_t* dst), const void* ctx);
+    void run_layers(int T, int l0, int l1, const int* d_cu, uint16_t* layer_inputs, uint16_t* k, uint16_t* v,
+                    uint16_t* out);
     std::unique_ptr<Impl> impl_;
     ModelConfig cfg_;
     EngineOptions opt_;

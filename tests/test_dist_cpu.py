@@ -1,0 +1,86 @@
+"""N>1 host path on CPU: world_size-2 gloo process group exercising bench.py's
+rank plumbing (barrier, max-over-ranks timing, summed tokens) and the
+batch partition (each rank its own requests / cache, no data collective)."""
+import os
+import socket
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+WORKER = r"""
+import os, sys, json
+sys.path.insert(0, ROOT)
+import bench
+from paper_2501_01792_b200 import api
+world, rank, local, dist = bench.dist_setup(None)
+assert world == 2 and dist.get_backend() == "gloo"
+# per-rank partition of the batch: rank-local allocator, identical policy
+cache = api.HybridCache(16, api.PoolCaps(64, 0, 64, 0))
+alloc = api.HostAllocation(1, 2)
+ids = [f"g{rank}r{i}" for i in range(4)]
+for rid in ids:
+    cache.create_request(rid, 40)
+    for _ in range(40):
+        if cache.context_len(rid) % 16 == 0:
+            cache.append_block(rid, api.next_block_kind(*cache.blocks_by_kind(rid), alloc))
+        cache.fill_token(rid)
+t_local = 1.5 + rank          # pretend device seconds
+bench.barrier(dist)
+t = bench.max_over_ranks(dist, t_local)
+tok = bench.sum_over_ranks(dist, 4.0 * 10)
+print(json.dumps({"rank": rank, "max_t": t, "tokens": tok,
+                  "tables": json.loads(cache.dump_json())["requests"][0]["entries"]}))
+dist.destroy_process_group()
+"""
+
+
+def free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def test_two_rank_gloo_bench_plumbing(tmp_path):
+    script = tmp_path / "w.py"
+    script.write_text(f"ROOT = {ROOT!r}\n" + WORKER)
+    port = free_port()
+    procs = []
+    for r in range(2):
+        env = dict(os.environ, RANK=str(r), LOCAL_RANK=str(r), WORLD_SIZE="2", LOCAL_WORLD_SIZE="2",
+                   MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), CUDA_VISIBLE_DEVICES="")
+        procs.append(subprocess.Popen([sys.executable, str(script)], env=env, stdout=subprocess.PIPE,
+                                      stderr=subprocess.PIPE, text=True))
+    outs = []
+    for p in procs:
+        o, e = p.communicate(timeout=240)
+        assert p.returncode == 0, e
+        outs.append(o.strip().splitlines()[-1])
+    import json
+    res = [json.loads(o) for o in outs]
+    assert all(r["max_t"] == 2.5 for r in res)            # max over ranks
+    assert all(r["tokens"] == 80.0 for r in res)          # whole-job tokens
+    assert res[0]["tables"] == res[1]["tables"]           # same policy, independent pools
+
+
+def test_reference_arm_nonzero_ranks_exit_silently(tmp_path):
+    """--impl reference under N>1: rank 0 alone prints; others exit 0 (tested
+    with a stubbed sample to stay fast)."""
+    code = f"""
+import sys, json
+sys.path.insert(0, {ROOT!r})
+import bench
+class A: pass
+a = A(); a.gpus = 2; a.steps = 1; a.warmup = 0; a.prompt = 8; a.ratio = 0.5; a.batch = 2; a.gen = 4
+from paper_2501_01792_b200 import api
+cfg = api.ModelConfig(num_layers=2, hidden_dim=64, num_heads=1, ffn_dim=128, vocab_size=64, name="tiny")
+bench.reference_arm(a, cfg, 2, 1, None)
+print("done")
+"""
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=120)
+    assert out.returncode == 0, out.stderr
+    assert out.stdout.strip() == "done"
