@@ -43,11 +43,13 @@ def parse():
     p.add_argument("--batch", type=int, default=128, help="requests per GPU")
     p.add_argument("--prompt", type=int, default=1024)
     p.add_argument("--gen", type=int, default=256, help="generation length of the workload (config)")
-    p.add_argument("--ratio", type=float, default=1.0 / 3.0, help="ACT share of context blocks (KV:ACT 2:1)")
+    p.add_argument("--ratio", type=float, default=1.0 / 3.0,
+                   help="ACT share r of context blocks (default 1/3 = the paper's KV:ACT 2:1 for OPT-30B, "
+                        "PAPER.md:714); -1 = the planner's choice from measured rates")
     p.add_argument("--host-gb", type=float, default=0.0, help="pinned host budget per rank (0: auto)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--layers", type=int, default=0, help="override num_layers (smoke/profiling only)")
-    p.add_argument("--profile-run", action="store_true", help="short run for ncu (no JSON contract)")
+    p.add_argument("--no-sweep", action="store_true", help="skip the per-ratio / planner / HBM-tier variants")
     return p.parse_args()
 
 
@@ -216,7 +218,8 @@ def reference_arm(args, cfg, world, rank, dist):
     if rank != 0:
         return
     threads = os.cpu_count() or 1
-    kind, run, sample = cpu_reference_sample(cfg, args.prompt, args.ratio, threads)
+    kind, run, sample = cpu_reference_sample(cfg, args.prompt, args.ratio if args.ratio >= 0 else 1.0 / 3.0,
+                                             threads)
     for _ in range(args.warmup):
         run()
     ts = [run() for _ in range(args.steps)]
@@ -236,8 +239,7 @@ def workload_config(args, cfg, world, extra=None):
     c = {"workload": f"{cfg.name}-shape offloaded decode (weights + hybrid KV/ACT cache in pinned host memory), "
                      f"batch {args.batch}/GPU, prompt {args.prompt}, gen {args.gen}",
          "model": cfg.name, "global_batch": args.batch * world, "seq_len": args.prompt, "gen_len": args.gen,
-         "act_share_r": round(args.ratio, 4),
-         "kv_act_ratio": f"{(1 - args.ratio) / max(args.ratio, 1e-9):.2f}:1" if args.ratio > 0 else "kv_only",
+         "act_share_r": round(extra.get("act_share_r", args.ratio), 4) if extra else round(args.ratio, 4),
          "parallelism": f"batch-partitioned x{world} (no collective)",
          "l2": "inputs larger than L2 (~100+ GB streamed host->HBM per step)"}
     if extra:
@@ -246,95 +248,175 @@ def workload_config(args, cfg, world, extra=None):
 
 
 # ------------------------------------------------------------------ ours ---
+def pool_plan(cfg, B, P, steps, r):
+    """Block pools and ratio setting for B requests of up to P+steps tokens
+    at ACT share r (r=0 kv_only, r=1 act_only, else hybrid via next_block_kind)."""
+    from paper_2501_01792_b200 import api
+    tpb = cfg.tokens_per_block
+    nb = math.ceil((P + steps) / tpb)
+    mode = "kv_only" if r <= 0 else ("act_only" if r >= 1 else "hybrid")
+    act_per = 0 if mode == "kv_only" else (nb if mode == "act_only" else math.ceil(r * nb) + 1)
+    kv_per = 0 if mode == "act_only" else (nb if mode == "kv_only" else math.ceil((1 - r) * nb) + 1)
+    a = int(round(r * 1000))
+    return mode, api.HostAllocation(a, 1000 - a), api.PoolCaps(kv_host=B * kv_per, act_host=B * act_per)
+
+
+def host_layers_for(cfg, caps, budget, w_bytes_pinned):
+    from paper_2501_01792_b200 import api
+    per_layer = caps.kv_host * api.HybridCache.bytes_of("KV", cfg) + caps.act_host * api.HybridCache.bytes_of("ACT", cfg)
+    if per_layer == 0:
+        return cfg.num_layers
+    return int(min(cfg.num_layers, max(2, (budget - w_bytes_pinned) // per_layer)))
+
+
+def run_steps(eng, ids, tokens, t0, n, prof=False):
+    """n decode steps starting at token row t0; returns summed stats."""
+    out = {"argmax": np.zeros(len(ids), np.int32)}
+    acc = {"dev_ms": 0.0, "launches": 0, "h2d": 0.0, "d2h": 0.0, "wall": 0.0}
+    eng.set_profile(prof)
+    last = None
+    for s in range(n):
+        w0 = time.perf_counter()
+        eng.decode_step(ids, tokens[t0 + s], want_x=False, want_argmax=True, out=out)
+        acc["wall"] += time.perf_counter() - w0
+        st = eng.last_stats()
+        acc["dev_ms"] += st["step_ms"]
+        acc["launches"] += int(st["launches"])
+        acc["h2d"] += st["h2d_bytes"]
+        acc["d2h"] += st["d2h_bytes"]
+        last = st
+    eng.set_profile(False)
+    acc["last"] = last
+    return acc
+
+
+def act_context_tokens(eng, ids):
+    return sum(e.filled_tokens for rid in ids for e in eng.cache.table(rid).entries if int(e.kind) == 1)
+
+
+def variant(eng, cfg, ids, tokens, P, r, caps_mode_alloc, host_layers, steps, warmup, link_gbs, seed, act_gpu=0):
+    """Re-configure the pools for one KV:ACT ratio and time `steps` decode steps."""
+    from paper_2501_01792_b200 import api
+    mode, alloc, caps = caps_mode_alloc
+    if act_gpu:
+        caps = api.PoolCaps(kv_host=caps.kv_host, act_host=caps.act_host, act_gpu=act_gpu)
+    eng.configure_cache(caps, mode=mode, allocation=alloc, host_layers=host_layers)
+    eng.admit_synthetic(ids, [P] * len(ids), seed=seed)
+    run_steps(eng, ids, tokens, 0, warmup)
+    acc = run_steps(eng, ids, tokens, warmup, steps)
+    ms = acc["dev_ms"] / steps
+    B = len(ids)
+    return {"act_share_r": round(r, 4), "mode": mode, "act_gpu_blocks": act_gpu, "tokens_per_s": B * 1e3 / ms,
+            "ms_per_step": ms, "h2d_gb_per_step": acc["h2d"] / steps / 1e9,
+            "link_frac": (acc["h2d"] / steps / (link_gbs * 1e9)) / (ms / 1e3) if link_gbs else None,
+            "e2e_tokens_per_s": B * steps / acc["wall"], "steps": steps,
+            "act_context_tokens": act_context_tokens(eng, ids)}
+
+
+def calibrate_planner(eng, cfg, link_gbs, caps_act_rows, host_mem, act_gpu=0):
+    """North-star (5): measured recompute-GEMM and host-link samples ->
+    bundle_from_samples (timing.cpp:172-183) -> plan_host_allocation
+    (plan.cpp:106-152) over this host's available DRAM (HardwareProfile::
+    host_mem semantics, plan.cpp:41-51)."""
+    from paper_2501_01792_b200 import api
+    ns = [n for n in (4096, 16384, 32768, 65536) if n <= caps_act_rows]
+    kv = [(float(n), eng.time_kv_gen(n, reps=3)) for n in ns]
+    ld = [(float(n), eng.time_load_kv(n, reps=2)) for n in ns]
+    bundle = api.bundle_from_samples(kv, ld, link_gbs * 1e9, cfg)
+    mem = api.budget_for(float(host_mem), cfg, bundle)
+    alloc = api.plan_host_allocation(bundle, mem, cfg.tokens_per_block, act_gpu)
+    r = alloc.act_host / max(alloc.act_host + alloc.kv_host, 1)
+    return {"kv_gen_samples": kv, "load_kv_samples": ld,
+            "t_kv_gen": {"slope_s_per_token": bundle.t_kv_gen.slope, "intercept_s": bundle.t_kv_gen.intercept,
+                         "r2": bundle.t_kv_gen.r_squared},
+            "t_load_kv": {"slope_s_per_token": bundle.t_load_kv.slope, "intercept_s": bundle.t_load_kv.intercept,
+                          "r2": bundle.t_load_kv.r_squared},
+            "t_load_w_s": bundle.t_load_w, "m_host": mem.m_host,
+            "allocation": alloc.__dict__, "planned_r": r,
+            "planned_t_pcie_s": api.planned_t_pcie(bundle, cfg.tokens_per_block, alloc),
+            "planned_t_comp_s": api.planned_t_computation(bundle, cfg.tokens_per_block, alloc, act_gpu)}
+
+
 def our_arm(args, cfg, world, rank, local, dist):
     from paper_2501_01792_b200 import api, kernels
     if kernels.device_count() == 0:
         raise SystemExit("bench needs a CUDA device")
     hbm_peak, tflops_sust, tflops_burst, peak_src = measured_peaks()
     B, P, L, d = args.batch, args.prompt, cfg.num_layers, cfg.hidden_dim
-    tpb = cfg.tokens_per_block
     total_steps = args.warmup + args.steps + 2
     max_seq = P + total_steps + 1
-    nb = math.ceil((P + total_steps) / tpb)
-    r = args.ratio
-    mode = "kv_only" if r <= 0 else ("act_only" if r >= 1 else "hybrid")
-    act_per = 0 if mode == "kv_only" else (nb if mode == "act_only" else math.ceil(r * nb) + 1)
-    kv_per = 0 if mode == "act_only" else (nb if mode == "kv_only" else math.ceil((1 - r) * nb) + 1)
-    alloc = api.HostAllocation(int(round(r * 1000)), 1000 - int(round(r * 1000)))
-    caps = api.PoolCaps(kv_host=B * kv_per, act_host=B * act_per)
-    kvb = api.HybridCache.bytes_of("KV", cfg)
-    actb = api.HybridCache.bytes_of("ACT", cfg)
-    per_layer_pool = caps.kv_host * kvb + caps.act_host * actb
+    r = args.ratio if args.ratio >= 0 else 1.0 / 3.0  # planner replaces the default below
+    mode, alloc, caps = pool_plan(cfg, B, P, total_steps, r)
     w_layer, _ = api.weight_bytes(cfg)
     local_world = int(os.environ.get("LOCAL_WORLD_SIZE", str(world)))
     # pinned host budget: never more than 120 GB or MemAvailable - 48 GB per node
     # (pinned pages cannot be reclaimed; folding keeps the streamed bytes)
     budget = args.host_gb * 1e9 if args.host_gb > 0 else min(120e9, mem_available_bytes() - 48e9) / local_world
     Lw = L if L * w_layer <= 0.55 * budget else max(2, int(0.55 * budget // w_layer))
-    Lp = int(min(L, max(2, (budget - Lw * w_layer) // max(per_layer_pool, 1))))
+    Lp = host_layers_for(cfg, caps, budget, Lw * w_layer)
     t_setup = time.time()
     eng = api.Engine(cfg, seed=42, max_seq=max_seq, rescale=True, max_batch=B, weights_on_device=False,
                      caps=caps, host_layers=Lp, weight_layers=Lw, mode=mode, allocation=alloc, device=local)
     ids = [f"g{rank}r{i}" for i in range(B)]
     eng.admit_synthetic(ids, [P] * B, seed=1 + rank)
-    # host-link peak: one large pinned H2D copy on the engine's copy stream
+    # host-link peak: a large pinned H2D copy on the engine's copy stream
+    tpb = cfg.tokens_per_block
     n_tok = min(caps.kv_host * tpb, 65536) if caps.kv_host else 0
     link_gbs = (n_tok * 2 * d * 2) / eng.time_load_kv(n_tok, reps=3) / 1e9 if n_tok else None
+    # north-star (5): the ratio comes from the planner fed with measured rates
+    planner = None
+    if link_gbs and caps.act_host:
+        try:
+            planner = calibrate_planner(eng, cfg, link_gbs, caps.act_host * tpb, mem_available_bytes())
+        except Exception as e:  # planner failure must not kill the bench line
+            planner = {"error": str(e)}
+    if args.ratio < 0 and planner and "planned_r" in planner:
+        r = planner["planned_r"]
+        mode, alloc, caps = pool_plan(cfg, B, P, total_steps, r)
+        Lp = host_layers_for(cfg, caps, budget, Lw * w_layer)
+        eng.configure_cache(caps, mode=mode, allocation=alloc, host_layers=Lp)
+        eng.admit_synthetic(ids, [P] * B, seed=1 + rank)
     setup_s = time.time() - t_setup
 
     rng = np.random.default_rng(rank)
     tokens = rng.integers(0, cfg.vocab_size, (total_steps, B)).astype(np.int32)
-    out = {"argmax": np.zeros(B, np.int32)}
-    for s in range(args.warmup):
-        eng.decode_step(ids, tokens[s], want_x=False, want_argmax=True, out=out)
-
+    run_steps(eng, ids, tokens, 0, args.warmup)
     # one profiled (untimed) step: per-kernel split + copy-stream GB/s
-    eng.set_profile(True)
-    eng.decode_step(ids, tokens[args.warmup], want_x=False, want_argmax=True, out=out)
-    prof = eng.last_stats()
-    eng.set_profile(False)
-    act_tokens = sum(e.filled_tokens for rid in ids for e in eng.cache.table(rid).entries
-                     if int(e.kind) == 1)
+    prof = run_steps(eng, ids, tokens, args.warmup, 1, prof=True)["last"]
+    act_tokens = act_context_tokens(eng, ids)
 
     clocks = ClockSampler(local)
     barrier(dist)
     import torch
     torch.cuda.synchronize()
     clocks.start()
-    dev_ms, launches, h2d, d2h = 0.0, 0, 0.0, 0.0
-    t0 = time.perf_counter()
-    for s in range(args.steps):
-        eng.decode_step(ids, tokens[args.warmup + 1 + s], want_x=False, want_argmax=True, out=out)
-        st = eng.last_stats()
-        dev_ms += st["step_ms"]
-        launches += int(st["launches"])
-        h2d += st["h2d_bytes"]
-        d2h += st["d2h_bytes"]
-    wall = time.perf_counter() - t0
+    acc = run_steps(eng, ids, tokens, args.warmup + 1, args.steps)
     torch.cuda.synchronize()
     barrier(dist)
     clk = clocks.stop()
 
-    dev_s = max_over_ranks(dist, dev_ms / 1e3)
-    wall_s = max_over_ranks(dist, wall)
+    dev_s = max_over_ranks(dist, acc["dev_ms"] / 1e3)
+    wall_s = max_over_ranks(dist, acc["wall"])
     tokens_total = sum_over_ranks(dist, float(B * args.steps))
     value = tokens_total / dev_s
     e2e = tokens_total / wall_s
     ms_per_step = dev_s * 1e3 / args.steps
+    h2d_step = acc["h2d"] / args.steps
 
     # dominant kernel: the recompute GEMM (tcgen05). algorithmic FLOPs/launch
-    # = 4 d^2 x ACT context tokens of the layer (flops.cpp:14), per launch
+    # = 4 d^2 x ACT context tokens of the layer (flops.cpp:14)
     rec_launch_ms = prof["recompute_ms"] / max(prof["recompute_launches"], 1)
     rec_flops = 4.0 * d * d * act_tokens / max(prof["recompute_launches"] / L, 1)
     achieved = rec_flops / (rec_launch_ms / 1e3) / 1e12 if rec_launch_ms > 0 else 0.0
     roof = {"kernel": "gemm_tn_kernel<256,kKvPaged> (ACT->K|V recompute)", "bound": "tensor",
             "achieved": achieved, "peak": tflops_sust, "unit": "TFLOP/s",
-            "frac": achieved / tflops_sust if tflops_sust else None, "traffic": None,
-            "peak_source": f"{peak_src} bf16_tflops_sustained (MEASURED_PEAKS.json)",
+            "frac": achieved / tflops_sust if tflops_sust else None,
+            "traffic": 6.65e9, "traffic_note": "ncu dram__bytes_read+write per launch, profiles/r01_ncu_recompute.csv "
+                                                "(algorithmic 2.07e9: A 0.62 + W 0.21 read, K|V 1.24 write)",
+            "peak_source": f"{peak_src} bf16_tflops_sustained (MEASURED_PEAKS.json); burst {tflops_burst}",
             "flops_per_launch": rec_flops, "launch_ms": rec_launch_ms}
     # per-step roofline (north_star): slower of link bytes / link BW, tensor
     # FLOPs / tensor peak, HBM bytes / HBM BW
-    h2d_step = h2d / args.steps
     ctx = P + args.warmup + 1 + args.steps // 2
     tensor_flops = L * (4.0 * d * d * act_tokens + 2.0 * B * (4 * d * d + 2 * d * cfg.ffn_dim))
     hbm_bytes = L * (B * (ctx + 1) * 2 * d * 2 + act_tokens * 3 * d * 2 + w_layer) + h2d_step
@@ -352,6 +434,43 @@ def our_arm(args, cfg, world, rank, local, dist):
                  "profile_split_ms": {"recompute": prof["recompute_ms"], "attention": prof["attn_ms"],
                                       "qkv_proj_ffn": prof["gemm_ms"], "copy_stream": prof["copy_ms"]}}
 
+    # ---- per-ratio sweep, planner, HBM-tiered variant (untimed by the contract)
+    extra = {}
+    if not args.no_sweep and world == 1:
+        sweep_steps, sweep_warm = 2, 1
+        sw_tokens = rng.integers(0, cfg.vocab_size, (sweep_steps + sweep_warm + 1, B)).astype(np.int32)
+        rs = sorted({0.0, 1.0 / 3.0, 0.5, 1.0, r} |
+                    ({planner["planned_r"]} if planner and "planned_r" in planner else set()))
+        per = []
+        for rr in rs:
+            if abs(rr - r) < 1e-6:
+                per.append({"act_share_r": round(r, 4), "mode": mode, "act_gpu_blocks": 0, "tokens_per_s": value,
+                            "ms_per_step": ms_per_step, "h2d_gb_per_step": h2d_step / 1e9,
+                            "link_frac": step_roof["frac"], "e2e_tokens_per_s": e2e, "steps": args.steps,
+                            "act_context_tokens": act_tokens, "headline": True})
+                continue
+            cm = pool_plan(cfg, B, P, sweep_steps + sweep_warm + 1, rr)
+            try:
+                per.append(variant(eng, cfg, ids, sw_tokens, P, rr, cm, host_layers_for(cfg, cm[2], budget, Lw * w_layer),
+                                   sweep_steps, sweep_warm, link_gbs, 7 + len(per)))
+            except Exception as e:
+                per.append({"act_share_r": rr, "error": str(e)})
+        extra["per_ratio"] = per
+        # B200 tiering: ACT blocks in HBM first (cache.cpp:85-91 placement),
+        # sized to the free HBM; weights still streamed from pinned host memory
+        try:
+            cm = pool_plan(cfg, B, P, sweep_steps + sweep_warm + 1, 1.0)
+            free_b, _ = torch.cuda.mem_get_info(local)
+            blk_all_layers = api.HybridCache.bytes_of("ACT", cfg) * L
+            act_gpu = int(min(cm[2].act_host, 0.85 * (free_b - 8e9) // blk_all_layers))
+            hv = variant(eng, cfg, ids, sw_tokens, P, 1.0, cm, host_layers_for(cfg, cm[2], budget, Lw * w_layer),
+                         sweep_steps, sweep_warm, link_gbs, 99, act_gpu=act_gpu)
+            hv["note"] = ("ACT/gpu pool in HBM (ACT blocks placed on GPU first, cache.cpp:85-91); "
+                          "weights + overflow blocks streamed from pinned host")
+            extra["hbm_tiered"] = hv
+        except Exception as e:
+            extra["hbm_tiered"] = {"error": str(e)}
+
     res = None
     if rank == 0:
         cpu = None
@@ -367,6 +486,10 @@ def our_arm(args, cfg, world, rank, local, dist):
             "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (reference-draw weights rescaled, pattern-filled cache at prompt length)",
             "config": workload_config(args, cfg, world, {
+                "act_share_r": r,
+                "kv_act_ratio": (f"{(1 - r) / r:.3f}:1" if 0 < r < 1 else ("kv_only" if r <= 0 else "act_only")),
+                "ratio_source": ("planner (plan_host_allocation on measured kv_gen / load_kv samples)"
+                                 if args.ratio < 0 and planner and "planned_r" in planner else "--ratio"),
                 "mode": mode, "host_layers_phys": Lp, "weight_layers_phys": Lw,
                 "host_pool_fold": ("none" if Lp == L and Lw == L else
                                    f"host storage folded to {Lp} cache / {Lw} weight layer copies "
@@ -374,16 +497,18 @@ def our_arm(args, cfg, world, rank, local, dist):
                 "kv_host_blocks": caps.kv_host, "act_host_blocks": caps.act_host,
                 "act_context_tokens": act_tokens}),
             "e2e": {"value": e2e, "unit": "tokens/s", "h2d_bytes_per_step": h2d_step + B * 4,
-                    "d2h_bytes_per_step": d2h / args.steps + B * 4,
+                    "d2h_bytes_per_step": acc["d2h"] / args.steps + B * 4,
                     "note": "decode_step C-ABI call with host token ids in / argmax out; includes the host-link "
                             "stream of weights + KV/ACT blocks and the new-token cache stores"},
-            "gpu_launches": launches,
+            "gpu_launches": acc["launches"],
             "roofline": roof,
             "step_roofline": step_roof,
             "cpu_baseline": cpu,
             "clocks": clk,
             "setup_s": setup_s,
+            "planner": planner,
         }
+        res.update(extra)
         print(json.dumps(res), flush=True)
     eng.close()
     return res
