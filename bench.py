@@ -106,6 +106,17 @@ def mem_available_bytes() -> float:
     return 64e9
 
 
+def mem_total_bytes() -> float:
+    try:
+        with open("/proc/meminfo") as fh:
+            for line in fh:
+                if line.startswith("MemTotal:"):
+                    return float(line.split()[1]) * 1024
+    except OSError:
+        pass
+    return 64e9
+
+
 def measured_peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -367,7 +378,7 @@ def our_arm(args, cfg, world, rank, local, dist):
     planner = None
     if link_gbs and caps.act_host:
         try:
-            planner = calibrate_planner(eng, cfg, link_gbs, caps.act_host * tpb, mem_available_bytes())
+            planner = calibrate_planner(eng, cfg, link_gbs, caps.act_host * tpb, mem_total_bytes())
         except Exception as e:  # planner failure must not kill the bench line
             planner = {"error": str(e)}
     if args.ratio < 0 and planner and "planned_r" in planner:
@@ -509,9 +520,53 @@ def our_arm(args, cfg, world, rank, local, dist):
             "planner": planner,
         }
         res.update(extra)
-        print(json.dumps(res), flush=True)
     eng.close()
+    if rank == 0:
+        if not args.no_sweep and world == 1:
+            try:
+                res["config2_resident"] = config2_resident(local)
+            except Exception as e:
+                res["config2_resident"] = {"error": str(e)}
+        print(json.dumps(res), flush=True)
     return res
+
+
+def config2_resident(local, B=64, P=512, steps=3, warmup=2):
+    """BASELINE configs[1]: OPT-6.7B shape, batch 64, prompt 512, ACT-only
+    cache resident in HBM, weights resident — the tensor-bound configuration
+    (every step recomputes K|V of the whole context from X)."""
+    from paper_2501_01792_b200 import api
+    hbm_peak, tflops_sust, tflops_burst, _ = measured_peaks()
+    cfg = api.ModelConfig.preset("opt-6.7b")
+    L, d, f = cfg.num_layers, cfg.hidden_dim, cfg.ffn_dim
+    total = steps + warmup + 2
+    nb = math.ceil((P + total) / cfg.tokens_per_block)
+    eng = api.Engine(cfg, seed=42, max_seq=P + total + 1, max_batch=B, weights_on_device=True,
+                     caps=api.PoolCaps(act_gpu=B * nb), mode="act_only", device=local)
+    ids = [f"c2r{i}" for i in range(B)]
+    eng.admit_synthetic(ids, [P] * B, seed=5)
+    tokens = np.random.default_rng(2).integers(0, cfg.vocab_size, (total, B)).astype(np.int32)
+    run_steps(eng, ids, tokens, 0, warmup)
+    prof = run_steps(eng, ids, tokens, warmup, 1, prof=True)["last"]
+    act = act_context_tokens(eng, ids)
+    acc = run_steps(eng, ids, tokens, warmup + 1, steps)
+    eng.close()
+    ms = acc["dev_ms"] / steps
+    rec_ms = prof["recompute_ms"] / max(prof["recompute_launches"], 1)
+    rec_tflops = 4.0 * d * d * act / (rec_ms / 1e3) / 1e12 if rec_ms else None
+    flops = L * (4.0 * d * d * act + 2.0 * B * (4 * d * d + 2 * d * f))
+    ctx = P + warmup + 2
+    hbm = L * (B * (ctx + 1) * 2 * d * 2 + act * 3 * d * 2 + (4 * d * d + 2 * d * f) * 2)
+    t_roof = max(flops / (tflops_sust * 1e12), hbm / (hbm_peak * 1e9))
+    return {"workload": "opt-6.7b-shape, batch 64, prompt 512, ACT-only cache + weights resident in HBM",
+            "tokens_per_s": B * 1e3 / ms, "ms_per_step": ms, "e2e_tokens_per_s": B * steps / acc["wall"],
+            "recompute_tflops": rec_tflops, "recompute_frac_of_sustained": rec_tflops / tflops_sust if rec_tflops else None,
+            "step_roofline": {"bound": "tensor" if flops / (tflops_sust * 1e12) >= hbm / (hbm_peak * 1e9) else "hbm",
+                              "t_roof_ms": t_roof * 1e3, "frac": t_roof * 1e3 / ms,
+                              "roofline_tokens_per_s": B / t_roof},
+            "profile_split_ms": {"recompute": prof["recompute_ms"], "attention": prof["attn_ms"],
+                                 "qkv_proj_ffn": prof["gemm_ms"]},
+            "act_context_tokens": act, "launches_per_step": acc["launches"] / steps}
 
 
 def main():
