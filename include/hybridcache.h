@@ -114,13 +114,14 @@ typedef struct hc_engine_options {
     long kv_host_cap, kv_gpu_cap, act_host_cap, act_gpu_cap; /* PoolCaps (cache.hpp:40-45), blocks */
     int kv_on_gpu;
     int host_layers;         /* physical host-pool layer copies (0 = num_layers) */
-    int mode;                /* 0 hybrid, 1 kv_only, 2 act_only (SimMode, sim.hpp:21) */
+    int mode;                /* 0 hybrid, 1 kv_only, 2 act_only, 3 token_recompute (SimMode, sim.hpp:21) */
     long alloc_act_host;     /* hybrid-ratio setting: HostAllocation target (plan.hpp:17-25) */
     long alloc_kv_host;
     int scaled;              /* 1/sqrt(head_dim) attention scale (decoder.hpp:28) */
     int max_prefill_tokens;  /* rows per prefill chunk (0: 65536) */
     int device;
     int weight_layers;       /* physical pinned weight layers (0 = num_layers) */
+    double recompute_ratio;  /* mode 3 (token_recompute): share of each prompt kept as ids only */
 } hc_engine_options;
 
 int hc_engine_create(const hc_model_config* cfg, uint64_t seed, int max_seq, int rescale,
@@ -140,7 +141,8 @@ int hc_engine_decode_step(void* engine, int n, const char* const* ids, const int
 int hc_engine_free_request(void* engine, const char* id);
 /* Drop all requests and rebuild the pools / ratio setting (weights kept). */
 int hc_engine_configure_cache(void* engine, long kv_host, long kv_gpu, long act_host, long act_gpu, int kv_on_gpu,
-                              int mode, long alloc_act_host, long alloc_kv_host, int host_layers);
+                              int mode, long alloc_act_host, long alloc_kv_host, int host_layers,
+                              double recompute_ratio);
 /* forward_prompt (decoder.cpp:144-157) of one sequence without cache effects:
  * layer_inputs / k / v [L x n x d], out [n x d] (bf16); any may be NULL.
  * token_recompute_kv(ids, layer) (decoder.cpp:131-142) = (k, v)[layer]. */

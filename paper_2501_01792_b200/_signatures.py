@@ -23,7 +23,7 @@ class EngineOptionsC(C.Structure):
                 ("act_gpu_cap", C.c_long), ("kv_on_gpu", C.c_int), ("host_layers", C.c_int),
                 ("mode", C.c_int), ("alloc_act_host", C.c_long), ("alloc_kv_host", C.c_long),
                 ("scaled", C.c_int), ("max_prefill_tokens", C.c_int), ("device", C.c_int),
-                ("weight_layers", C.c_int)]
+                ("weight_layers", C.c_int), ("recompute_ratio", C.c_double)]
 
 
 cfgp = C.POINTER(ModelConfigC)
@@ -72,7 +72,7 @@ SIGNATURES = {
     "hc_engine_admit_synthetic": (i, [vp, i, cpp, ip, u64]),
     "hc_engine_decode_step": (i, [vp, i, cpp, ip, u16p, fp, ip]),
     "hc_engine_free_request": (i, [vp, cp]),
-    "hc_engine_configure_cache": (i, [vp, l, l, l, l, i, i, l, l, i]),
+    "hc_engine_configure_cache": (i, [vp, l, l, l, l, i, i, l, l, i, d]),
     "hc_engine_forward_trace": (i, [vp, ip, i, u16p, u16p, u16p, u16p]),
     "hc_engine_layer_forward": (i, [vp, i, u16p, i, u16p, u16p, u16p]),
     "hc_engine_cache": (i, [vp, vpp]),

@@ -373,7 +373,7 @@ def weight_bytes(cfg: ModelConfig) -> Tuple[int, int]:
 
 
 # ---------------------------------------------------------------- engine ---
-MODES = {"hybrid": 0, "kv_only": 1, "act_only": 2}
+MODES = {"hybrid": 0, "kv_only": 1, "act_only": 2, "token_recompute": 3}
 
 
 def _ids(ids: Sequence[str]):
@@ -393,7 +393,8 @@ class Engine:
                  weights: Optional[dict] = None, max_batch: int = 1, weights_on_device: bool = True,
                  caps: Optional[PoolCaps] = None, kv_on_gpu: bool = False, host_layers: int = 0,
                  mode: str = "hybrid", allocation: Optional[HostAllocation] = None, scaled: bool = True,
-                 max_prefill_tokens: int = 0, device: int = 0, weight_layers: int = 0):
+                 max_prefill_tokens: int = 0, device: int = 0, weight_layers: int = 0,
+                 recompute_ratio: float = 0.0):
         self.cfg = ModelConfig(**cfg.__dict__).validate()
         caps = caps or PoolCaps()
         alloc = allocation or HostAllocation(1, 1)
@@ -402,7 +403,7 @@ class Engine:
         self.opts = EngineOptionsC(max_batch, max_seq, int(weights_on_device), caps.kv_host, caps.kv_gpu,
                                    caps.act_host, caps.act_gpu, int(kv_on_gpu), host_layers, MODES[mode],
                                    alloc.act_host, alloc.kv_host, int(scaled), max_prefill_tokens, device,
-                                   weight_layers)
+                                   weight_layers, recompute_ratio)
         self.max_batch = max_batch
         h = C.c_void_p()
         c = self.cfg.to_c()
@@ -477,13 +478,14 @@ class Engine:
         check(lib().hc_engine_free_request(self._h, rid.encode()))
 
     def configure_cache(self, caps: PoolCaps, *, mode: str = "hybrid", allocation: Optional[HostAllocation] = None,
-                        kv_on_gpu: bool = False, host_layers: int = 0) -> None:
+                        kv_on_gpu: bool = False, host_layers: int = 0, recompute_ratio: float = 0.0) -> None:
         """Drop all requests and rebuild pools / ratio setting (weights kept)."""
         if mode not in MODES:
             raise InputError(f"unknown mode: {mode}")
         a = allocation or HostAllocation(1, 1)
         check(lib().hc_engine_configure_cache(self._h, caps.kv_host, caps.kv_gpu, caps.act_host, caps.act_gpu,
-                                              int(kv_on_gpu), MODES[mode], a.act_host, a.kv_host, host_layers))
+                                              int(kv_on_gpu), MODES[mode], a.act_host, a.kv_host, host_layers,
+                                              float(recompute_ratio)))
 
     def forward_trace(self, ids: Sequence[int]) -> dict:
         """GPU forward_prompt (decoder.cpp:144-157): layer inputs, K, V per layer

@@ -69,7 +69,8 @@ EngineOptions opts_of(const hc_engine_options* o) {
     e.act_gpu_cap = o->act_gpu_cap;
     e.kv_on_gpu = o->kv_on_gpu;
     e.host_layers = o->host_layers;
-    if (o->mode < 0 || o->mode > 2) throw InputError("engine mode must be 0 hybrid, 1 kv_only, 2 act_only");
+    if (o->mode < 0 || o->mode > 3)
+        throw InputError("engine mode must be 0 hybrid, 1 kv_only, 2 act_only, 3 token_recompute");
     e.mode = static_cast<CacheMode>(o->mode);
     e.alloc.act_host = o->alloc_act_host;
     e.alloc.kv_host = o->alloc_kv_host;
@@ -77,6 +78,7 @@ EngineOptions opts_of(const hc_engine_options* o) {
     e.max_prefill_tokens = o->max_prefill_tokens > 0 ? o->max_prefill_tokens : 65536;
     e.device = o->device;
     e.weight_layers = o->weight_layers;
+    e.recompute_ratio = o->recompute_ratio;
     return e;
 }
 
@@ -334,14 +336,15 @@ int hc_engine_decode_step(void* e, int n, const char* const* ids, const int* tok
     return hc_guard([&] { eng(e)->decode_step(ids_of(n, ids), tokens, x_out, logits, argmax); });
 }
 int hc_engine_configure_cache(void* e, long kv_host, long kv_gpu, long act_host, long act_gpu, int kv_on_gpu, int mode,
-                              long alloc_act_host, long alloc_kv_host, int host_layers) {
+                              long alloc_act_host, long alloc_kv_host, int host_layers, double recompute_ratio) {
     return hc_guard([&] {
-        if (mode < 0 || mode > 2) throw InputError("engine mode must be 0 hybrid, 1 kv_only, 2 act_only");
+        if (mode < 0 || mode > 3)
+            throw InputError("engine mode must be 0 hybrid, 1 kv_only, 2 act_only, 3 token_recompute");
         HostAllocation a;
         a.act_host = alloc_act_host;
         a.kv_host = alloc_kv_host;
         eng(e)->configure_cache(PoolCaps{kv_host, kv_gpu, act_host, act_gpu}, kv_on_gpu != 0,
-                                static_cast<CacheMode>(mode), a, host_layers);
+                                static_cast<CacheMode>(mode), a, host_layers, recompute_ratio);
     });
 }
 int hc_engine_forward_trace(void* e, const int* ids, int n, uint16_t* layer_inputs, uint16_t* k, uint16_t* v,

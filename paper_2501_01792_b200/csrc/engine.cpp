@@ -22,6 +22,7 @@ enum Region : int {
     R_ACT_GPU = 4,    // resident ACT/gpu pool, layer l
     R_KV_HOST = 5,    // pinned KV/host pool, physical layer l%Lp (mapped)
     R_ACT_HOST = 6,   // pinned ACT/host pool (mapped)
+    R_TOKREC = 7,     // K|V of token-recompute prefixes, rebuilt every layer of every step
 };
 
 struct Run {
@@ -99,6 +100,10 @@ struct Engine::Impl {
     size_t prefill_rows = 0;
     cudaEvent_t loaded[2]{}, consumed[2]{}, ev0{}, ev1{};
     bool pools_filled = false;
+    bf16* tr_kv = nullptr;  // [max_batch * max_blocks] KV blocks for token-recompute prefixes
+    void ensure_tr() {
+        if (!tr_kv) tr_kv = dalloc<bf16>(static_cast<size_t>(B) * max_blocks * kvb);
+    }
     // profiling: timing events handed out per step
     std::vector<cudaEvent_t> pev;
     size_t pev_used = 0;
@@ -135,6 +140,7 @@ struct Engine::Impl {
         r[R_ACT_GPU] = act_gpu ? act_gpu + static_cast<size_t>(l) * act_gpu_cap * actb : nullptr;
         r[R_KV_HOST] = kv_host ? kv_host + static_cast<size_t>(l % Lp) * kv_host_cap * kvb : nullptr;
         r[R_ACT_HOST] = act_host ? act_host + static_cast<size_t>(l % Lp) * act_host_cap * actb : nullptr;
+        r[R_TOKREC] = tr_kv;
     }
     const bf16* layer_w(int l, int slot) const { return w_all ? w_all + static_cast<size_t>(l) * LE : wbuf[slot]; }
 
@@ -211,8 +217,6 @@ void Engine::init(const ModelConfig& c, int w_max_seq, const uint16_t* emb, cons
     if (cfg_.head_dim() != 64 && cfg_.head_dim() != 128) throw InputError("Engine: head_dim must be 64 or 128");
     if (cfg_.ffn_dim % 64) throw InputError("Engine: ffn_dim must be a multiple of 64");
     if (cfg_.vocab_size % 16) throw InputError("Engine: vocab_size must be a multiple of 16");
-    if (opt_.mode == CacheMode::TokenRecompute)
-        throw ConfigError("Engine: token_recompute mode is modelled by the planner only (not executed)");
     if (opt_.max_batch < 1) throw InputError("Engine: max_batch must be >= 1");
     HC_CUDA(cudaSetDevice(opt_.device));
     m.L = cfg_.num_layers;
@@ -272,14 +276,15 @@ void Engine::init(const ModelConfig& c, int w_max_seq, const uint16_t* emb, cons
     m.logits = dalloc<float>(static_cast<size_t>(m.B) * m.V);
     m.amax = dalloc<int>(m.B);
     configure_cache(PoolCaps{opt_.kv_host_cap, opt_.kv_gpu_cap, opt_.act_host_cap, opt_.act_gpu_cap}, opt_.kv_on_gpu != 0,
-                    opt_.mode, opt_.alloc, opt_.host_layers);
+                    opt_.mode, opt_.alloc, opt_.host_layers, opt_.recompute_ratio);
 }
 
 void Engine::configure_cache(const PoolCaps& caps, bool kv_on_gpu, CacheMode mode, const HostAllocation& alloc,
-                             int host_layers) {
+                             int host_layers, double recompute_ratio) {
     Impl& m = *impl_;
-    if (mode == CacheMode::TokenRecompute)
-        throw ConfigError("Engine: token_recompute mode is modelled by the planner only (not executed)");
+    opt_.recompute_ratio = recompute_ratio;
+    if (mode == CacheMode::TokenRecompute && (opt_.recompute_ratio < 0.0 || opt_.recompute_ratio > 1.0))
+        throw ConfigError("Engine: recompute_ratio must lie in [0, 1]");
     if (mode == CacheMode::Hybrid && alloc.act_host + alloc.kv_host <= 0)
         throw ConfigError("Engine: hybrid mode needs a nonempty host allocation (ratio target)");
     HC_CUDA(cudaDeviceSynchronize());
@@ -307,7 +312,11 @@ void Engine::configure_cache(const PoolCaps& caps, bool kv_on_gpu, CacheMode mod
     m.act_gpu_cap = caps.act_gpu;
     m.Lp = host_layers > 0 ? std::min(host_layers, m.L) : m.L;
     cache_ = std::make_unique<HybridCache>(m.tpb, caps, kv_on_gpu);
-    assigner_ = std::make_unique<BlockAssigner>(*cache_, mode, alloc, opt_.recompute_ratio);
+    // token recompute keeps a block-aligned PREFIX of every prompt as ids only
+    // (exact recompute needs a prefix) and caches the rest as KV
+    token_mode_ = mode == CacheMode::TokenRecompute;
+    rc_ids_.clear();
+    assigner_ = std::make_unique<BlockAssigner>(*cache_, token_mode_ ? CacheMode::KvOnly : mode, alloc, 0.0);
     m.kv_gpu = dalloc<bf16>(static_cast<size_t>(m.L) * m.kv_gpu_cap * m.kvb);
     m.act_gpu = dalloc<bf16>(static_cast<size_t>(m.L) * m.act_gpu_cap * m.actb);
     m.kv_host = halloc<bf16>(static_cast<size_t>(m.Lp) * m.kv_host_cap * m.kvb, true);
@@ -363,7 +372,8 @@ Engine::~Engine() {
                     (void*)m.act_gpu, (void*)m.kvr, (void*)m.kv_stage[0], (void*)m.kv_stage[1], (void*)m.act_stage[0],
                     (void*)m.act_stage[1], (void*)m.x[0], (void*)m.x[1], (void*)m.qkv, (void*)m.att, (void*)m.proj,
                     (void*)m.hbuf, (void*)m.logits, (void*)m.amax, (void*)m.attn_work, (void*)m.d_meta,
-                    (void*)m.px[0], (void*)m.px[1], (void*)m.pqkv, (void*)m.patt, (void*)m.pproj, (void*)m.ph})
+                    (void*)m.px[0], (void*)m.px[1], (void*)m.pqkv, (void*)m.patt, (void*)m.pproj, (void*)m.ph,
+                    (void*)m.tr_kv})
         if (p) cudaFree(p);
     for (void* p : {(void*)m.h_w, (void*)m.kv_host, (void*)m.act_host, (void*)m.h_meta})
         if (p) cudaFreeHost(p);
@@ -466,13 +476,15 @@ void Engine::prefill(const std::vector<std::string>& ids, const std::vector<std:
         for (size_t r = r0; r < r1; ++r) {
             assigner_->add_request(ids[r], static_cast<int>(prompts[r].size()));
             const int base = cu.back();
+            const int rc = rc_prefix(static_cast<int>(prompts[r].size()));
+            if (token_mode_) rc_ids_[ids[r]].assign(prompts[r].begin(), prompts[r].begin() + rc);
             for (size_t t = 0; t < prompts[r].size(); ++t) {
                 tokens.push_back(prompts[r][t]);
                 positions.push_back(static_cast<int>(t));
-                assigner_->add_token(ids[r]);
+                if (static_cast<int>(t) >= rc) assigner_->add_token(ids[r]);
             }
             const BlockTable& tb = cache_->table(ids[r]);
-            int row = base;
+            int row = base + rc;
             for (const auto& e : tb.entries) {
                 const bool gpu = e.location == Location::GpuMem;
                 if (e.kind == BlockKind::ACT) {
@@ -565,7 +577,13 @@ void Engine::admit_synthetic(const std::vector<std::string>& ids, const std::vec
     for (size_t r = 0; r < ids.size(); ++r) {
         if (prompt_lens[r] > m.max_seq) throw InputError("embed: sequence longer than max_seq");
         assigner_->add_request(ids[r], prompt_lens[r]);
-        for (int t = 0; t < prompt_lens[r]; ++t) assigner_->add_token(ids[r]);
+        const int rc = rc_prefix(prompt_lens[r]);
+        if (token_mode_) {
+            std::vector<int>& v = rc_ids_[ids[r]];
+            v.resize(rc);
+            for (int t = 0; t < rc; ++t) v[t] = static_cast<int>((seed + 7919u * (t + 1) + 31u * r) % m.V);
+        }
+        for (int t = rc; t < prompt_lens[r]; ++t) assigner_->add_token(ids[r]);
     }
     if (m.pools_filled) return;
     // activations ~U(-0.1,0.1) like the embeddings; K,V of matching scale
@@ -581,7 +599,21 @@ void Engine::admit_synthetic(const std::vector<std::string>& ids, const std::vec
     m.pools_filled = true;
 }
 
-void Engine::free_request(const std::string& id) { cache_->free_request(id); }
+void Engine::free_request(const std::string& id) {
+    cache_->free_request(id);
+    rc_ids_.erase(id);
+}
+
+int Engine::rc_prefix(int prompt_len) const {
+    if (!token_mode_) return 0;
+    const int tpb = cfg_.tokens_per_block;
+    return static_cast<int>(std::floor(opt_.recompute_ratio * prompt_len / tpb)) * tpb;
+}
+
+long Engine::recompute_prefix_len(const std::string& id) const {
+    auto it = rc_ids_.find(id);
+    return it == rc_ids_.end() ? 0 : static_cast<long>(it->second.size());
+}
 
 // ---------------------------------------------------------------------------
 void Engine::decode_step(const std::vector<std::string>& ids, const int* tokens, uint16_t* x_out, float* logits_out,
@@ -597,7 +629,7 @@ void Engine::decode_step(const std::vector<std::string>& ids, const int* tokens,
             if (!seen.insert(ids[b]).second) throw InputError("decode_step: duplicate request id " + ids[b]);
             if (tokens[b] < 0 || tokens[b] >= m.V)
                 throw InputError("embed: token id out of range: " + std::to_string(tokens[b]));
-            pos[b] = cache_->table(ids[b]).context_len();  // throws InputError for unknown ids
+            pos[b] = cache_->table(ids[b]).context_len() + static_cast<int>(recompute_prefix_len(ids[b]));
             if (pos[b] >= m.max_seq) throw InputError("embed: position exceeds max_seq: " + std::to_string(pos[b]));
         }
     }
@@ -606,7 +638,34 @@ void Engine::decode_step(const std::vector<std::string>& ids, const int* tokens,
     std::vector<int> refs(static_cast<size_t>(n) * m.max_blocks, 0);
     std::vector<int> kvh_pbns, acth_pbns, actg_pbns;
     bool any_act = false, any_kv = false;
+    // token-recompute prefixes: rows of a batched causal forward rebuilt
+    // through every layer each step (the FlexGen-style baseline, sim.cpp:196-206)
+    std::vector<int> rc_tok, rc_pos, rc_cu(1, 0), tr_src, tr_n, tr_ref;
+    int rc_max = 0;
+    if (token_mode_) m.ensure_tr();
     for (int b = 0; b < n; ++b) {
+        const std::vector<int>* pre = nullptr;
+        if (token_mode_) {
+            auto it = rc_ids_.find(ids[b]);
+            if (it != rc_ids_.end()) pre = &it->second;
+        }
+        const int rc = pre ? static_cast<int>(pre->size()) : 0;
+        for (int t = 0; t < rc; ++t) {
+            rc_tok.push_back((*pre)[t]);
+            rc_pos.push_back(t);
+        }
+        for (int i = 0; i < rc / m.tpb; ++i) {
+            tr_src.push_back(rc_cu.back() + i * m.tpb);
+            tr_n.push_back(m.tpb);
+            tr_ref.push_back(pack_ref(R_TOKREC, b * m.max_blocks + i));
+        }
+        rc_cu.push_back(rc_cu.back() + rc);
+        rc_max = std::max(rc_max, rc);
+    }
+    const int n_rc = rc_cu.back();
+    if (n_rc) m.ensure_prefill(n_rc);
+    for (int b = 0; b < n; ++b) {
+        const int rcb = (rc_cu[b + 1] - rc_cu[b]) / m.tpb;
         const TokenSlot s = assigner_->add_token(ids[b]);
         const BlockTableEntry& e = s.entry;
         const bool gpu = e.location == Location::GpuMem;
@@ -621,9 +680,10 @@ void Engine::decode_step(const std::vector<std::string>& ids, const int* tokens,
             if (!gpu) kv_host[b] = pack_ref(R_KV_HOST, e.pbn);
         }
         const BlockTable& t = cache_->table(ids[b]);
-        nblk[b] = static_cast<int>(t.entries.size());
-        ctx[b] = t.context_len();
+        nblk[b] = rcb + static_cast<int>(t.entries.size());
+        ctx[b] = rcb * m.tpb + t.context_len();
         int* rb = refs.data() + static_cast<size_t>(b) * m.max_blocks;
+        for (int i = 0; i < rcb; ++i) *rb++ = pack_ref(R_TOKREC, b * m.max_blocks + i);
         for (size_t i = 0; i < t.entries.size(); ++i) {
             const auto& en = t.entries[i];
             const bool g = en.location == Location::GpuMem;
@@ -653,7 +713,9 @@ void Engine::decode_step(const std::vector<std::string>& ids, const int* tokens,
     };
     const size_t o_tok = put(std::vector<int>(tokens, tokens + n)), o_pos = put(pos), o_ad = put(act_dev),
                  o_ah = put(act_host), o_kd = put(kv_dev), o_kh = put(kv_host), o_t = put(tok), o_nb = put(nblk),
-                 o_ctx = put(ctx), o_ref = put(refs), o_th = put(tiles_h), o_tg = put(tiles_g);
+                 o_ctx = put(ctx), o_ref = put(refs), o_th = put(tiles_h), o_tg = put(tiles_g),
+                 o_rtok = put(rc_tok), o_rpos = put(rc_pos), o_rcu = put(rc_cu), o_trs = put(tr_src),
+                 o_trn = put(tr_n), o_trr = put(tr_ref);
     m.ensure_meta(meta.size());
     std::memcpy(m.h_meta, meta.data(), meta.size() * 4);
     const int* dm = m.d_meta;
@@ -666,6 +728,10 @@ void Engine::decode_step(const std::vector<std::string>& ids, const int* tokens,
     HC_CUDA(cudaMemcpyAsync(m.d_meta, m.h_meta, meta.size() * 4, cudaMemcpyHostToDevice, s_compute_));
     embed(m.emb, m.pos, dm + o_tok, dm + o_pos, n, m.d, m.x[0], m.d, s_compute_);
     st.launches += 1;
+    if (n_rc) {
+        embed(m.emb, m.pos, dm + o_rtok, dm + o_rpos, n_rc, m.d, m.px[0], m.d, s_compute_);
+        st.launches += 1;
+    }
     if (capture_inputs_) captured_.assign(static_cast<size_t>(m.L) * n * m.d, 0);
     const float scale = opt_.scaled ? 1.0f / std::sqrt(static_cast<float>(m.hd)) : 1.0f;
 
@@ -705,6 +771,37 @@ void Engine::decode_step(const std::vector<std::string>& ids, const int* tokens,
         m.regions(l, slot, R);
         bf16* xin = m.x[l & 1];
         bf16* xout = m.x[(l + 1) & 1];
+        if (n_rc) {
+            // token recompute: full layer l over every prefix (FullLayer(rc) FLOPs,
+            // flops.cpp:20-22), its K|V written into the prefix blocks
+            m.span_begin(profile_, s_compute_, 0);
+            bf16* pin = m.px[l & 1];
+            bf16* pout = m.px[(l + 1) & 1];
+            gemm_rows(gemm::kStore, pin, n_rc, m.d, W + m.off.wqkv, 3 * m.d, m.pqkv, 3 * m.d, s_compute_);
+            BlockScatter sk;
+            sk.src = m.pqkv;
+            sk.ld = 3 * m.d;
+            sk.src_row = dm + o_trs;
+            sk.n_tok = dm + o_trn;
+            sk.dst_ref = dm + o_trr;
+            std::copy(R, R + 16, sk.region);
+            sk.n_blocks = static_cast<int>(tr_src.size());
+            sk.d = m.d;
+            sk.H = m.H;
+            sk.hd = m.hd;
+            sk.tpb = m.tpb;
+            scatter_kv_blocks(sk, s_compute_);
+            if (l + 1 < m.L) {  // the last layer's prefix output is never needed
+                prefill_attention(m.pqkv, m.patt, dm + o_rcu, n, rc_max, m.H, m.hd, scale, s_compute_);
+                gemm_rows(gemm::kStore, m.patt, n_rc, m.d, W + m.off.wproj, m.d, m.pproj, m.d, s_compute_);
+                gemm_rows(gemm::kRelu, m.pproj, n_rc, m.d, W + m.off.w1, m.f, m.ph, m.f, s_compute_);
+                gemm_rows(gemm::kStore, m.ph, n_rc, m.f, W + m.off.w2, m.d, pout, m.d, s_compute_);
+                st.launches += 4;
+            }
+            st.launches += 2;
+            st.recompute_tokens += n_rc;
+            m.span_end(profile_, s_compute_);
+        }
         if (capture_inputs_)
             HC_CUDA(cudaMemcpyAsync(captured_.data() + static_cast<size_t>(l) * n * m.d, xin,
                                     static_cast<size_t>(n) * m.d * 2, cudaMemcpyDeviceToHost, s_compute_));
@@ -771,7 +868,7 @@ void Engine::decode_step(const std::vector<std::string>& ids, const int* tokens,
         a.n_blocks = dm + o_nb;
         a.ctx_len = dm + o_ctx;
         a.max_blocks = m.max_blocks;
-        for (int i = 0; i < 3; ++i) a.region[i] = R[i];
+        for (int i = 0; i < 16; ++i) a.region[i] = R[i];
         a.B = n;
         a.H = m.H;
         a.hd = m.hd;

@@ -28,6 +28,7 @@
 
 #include <memory>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "host/cache.hpp"
@@ -90,11 +91,14 @@ public:
     void decode_step(const std::vector<std::string>& ids, const int* tokens, uint16_t* x_out, float* logits,
                      int* argmax);
     void free_request(const std::string& id);
+    // Token-recompute mode: tokens of the request kept as ids only (a
+    // block-aligned prompt prefix, rebuilt through all layers every step).
+    long recompute_prefix_len(const std::string& id) const;
 
     // Drop every request and re-create the block pools with new capacities /
     // ratio setting (weights and scratch stay): ratio sweeps on one engine.
     void configure_cache(const PoolCaps& caps, bool kv_on_gpu, CacheMode mode, const HostAllocation& alloc,
-                         int host_layers);
+                         int host_layers, double recompute_ratio = 0.0);
 
     // forward_prompt (decoder.cpp:144-157) of one sequence on the GPU without
     // touching the cache: per-layer inputs X, K, V ([L][n][d]) and the output
@@ -142,6 +146,9 @@ private:
     StepStats stats_{};
     bool profile_ = false;
     bool capture_inputs_ = false;
+    bool token_mode_ = false;                                     // CacheMode::TokenRecompute
+    std::unordered_map<std::string, std::vector<int>> rc_ids_;    // recompute-only prompt prefixes
+    int rc_prefix(int prompt_len) const;
     std::vector<uint16_t> captured_;
 };
 

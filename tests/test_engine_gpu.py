@@ -181,6 +181,29 @@ def test_engine_modes_agree(native):
     assert rel(outs["hybrid"], outs["kv_only"]) <= TOL
 
 
+@pytest.mark.parametrize("ratio", [0.5, 1.0])
+def test_engine_token_recompute_mode_matches_oracle(native, ratio):
+    """Token-recompute baseline (SimMode::TokenRecompute, sim.cpp:196-206): a
+    block-aligned prompt prefix is kept as ids only and re-run through every
+    layer each step; decode outputs still equal the oracle."""
+    from paper_2501_01792_b200.api import PoolCaps
+    cfg = small_cfg(L=3, d=256, H=2, f=512, tpb=8)
+    w = oracle_weights(cfg)
+    rng = np.random.default_rng(6)
+    lens = [40, 27]
+    prompts = [rng.integers(0, cfg.vocab_size, n).tolist() for n in lens]
+    dec = [rng.integers(0, cfg.vocab_size, 3).tolist() for _ in prompts]
+    eng, ids, got, want = run_case(cfg, w, prompts, dec, caps=PoolCaps(kv_host=16, kv_gpu=0),
+                                   mode="token_recompute", recompute_ratio=ratio)
+    check_outputs(got, want)
+    from paper_2501_01792_b200 import _native
+    import ctypes
+    for rid, n in zip(ids, lens):
+        rc = (int(ratio * n) // cfg.tokens_per_block) * cfg.tokens_per_block
+        assert eng.cache.context_len(rid) == n - rc + 3
+    assert eng.last_stats()["recompute_rows"] > 0
+
+
 def test_engine_greedy_generation_matches_oracle(native):
     """Greedy decode (tied LM head argmax) reproduces the oracle's tokens."""
     from paper_2501_01792_b200.api import HostAllocation, PoolCaps
