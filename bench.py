@@ -50,6 +50,9 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--layers", type=int, default=0, help="override num_layers (smoke/profiling only)")
     p.add_argument("--no-sweep", action="store_true", help="skip the per-ratio / planner / HBM-tier variants")
+    p.add_argument("--sweep", default="0,0.3333333333333333,0.5,1,tr0.5",
+                   help="ACT shares r to time besides the headline; trX = token-recompute baseline at ratio X")
+    p.add_argument("--no-config2", action="store_true", help="skip the OPT-6.7B resident (config 2) variant")
     return p.parse_args()
 
 
@@ -305,19 +308,24 @@ def act_context_tokens(eng, ids):
     return sum(e.filled_tokens for rid in ids for e in eng.cache.table(rid).entries if int(e.kind) == 1)
 
 
-def variant(eng, cfg, ids, tokens, P, r, caps_mode_alloc, host_layers, steps, warmup, link_gbs, seed, act_gpu=0):
+def variant(eng, cfg, ids, tokens, P, r, caps_mode_alloc, host_layers, steps, warmup, link_gbs, seed, act_gpu=0,
+            token_recompute=None):
     """Re-configure the pools for one KV:ACT ratio and time `steps` decode steps."""
     from paper_2501_01792_b200 import api
     mode, alloc, caps = caps_mode_alloc
     if act_gpu:
         caps = api.PoolCaps(kv_host=caps.kv_host, act_host=caps.act_host, act_gpu=act_gpu)
-    eng.configure_cache(caps, mode=mode, allocation=alloc, host_layers=host_layers)
+    rc_ratio = 0.0
+    if token_recompute is not None:  # SimMode::TokenRecompute baseline on the KV-only pools
+        mode, rc_ratio = "token_recompute", token_recompute
+    eng.configure_cache(caps, mode=mode, allocation=alloc, host_layers=host_layers, recompute_ratio=rc_ratio)
     eng.admit_synthetic(ids, [P] * len(ids), seed=seed)
     run_steps(eng, ids, tokens, 0, warmup)
     acc = run_steps(eng, ids, tokens, warmup, steps)
     ms = acc["dev_ms"] / steps
     B = len(ids)
-    return {"act_share_r": round(r, 4), "mode": mode, "act_gpu_blocks": act_gpu, "tokens_per_s": B * 1e3 / ms,
+    return {"act_share_r": round(r, 4), "mode": mode, "recompute_ratio": rc_ratio, "act_gpu_blocks": act_gpu,
+            "tokens_per_s": B * 1e3 / ms,
             "ms_per_step": ms, "h2d_gb_per_step": acc["h2d"] / steps / 1e9,
             "link_frac": (acc["h2d"] / steps / (link_gbs * 1e9)) / (ms / 1e3) if link_gbs else None,
             "e2e_tokens_per_s": B * steps / acc["wall"], "steps": steps,
@@ -450,9 +458,17 @@ def our_arm(args, cfg, world, rank, local, dist):
     if not args.no_sweep and world == 1:
         sweep_steps, sweep_warm = 2, 1
         sw_tokens = rng.integers(0, cfg.vocab_size, (sweep_steps + sweep_warm + 1, B)).astype(np.int32)
-        rs = sorted({0.0, 1.0 / 3.0, 0.5, 1.0, r} |
+        rs = sorted(set(float(x) for x in args.sweep.split(",") if x and not x.startswith("tr")) | {r} |
                     ({planner["planned_r"]} if planner and "planned_r" in planner else set()))
         per = []
+        for tr in [float(x[2:]) for x in args.sweep.split(",") if x.startswith("tr")]:
+            cm = pool_plan(cfg, B, P, sweep_steps + sweep_warm + 1, 0.0)
+            try:
+                per.append(variant(eng, cfg, ids, sw_tokens, P, 0.0, cm,
+                                   host_layers_for(cfg, cm[2], budget, Lw * w_layer), sweep_steps, sweep_warm,
+                                   link_gbs, 5, token_recompute=tr))
+            except Exception as e:
+                per.append({"token_recompute": tr, "error": str(e)})
         for rr in rs:
             if abs(rr - r) < 1e-6:
                 per.append({"act_share_r": round(r, 4), "mode": mode, "act_gpu_blocks": 0, "tokens_per_s": value,
@@ -522,7 +538,7 @@ def our_arm(args, cfg, world, rank, local, dist):
         res.update(extra)
     eng.close()
     if rank == 0:
-        if not args.no_sweep and world == 1:
+        if not args.no_sweep and not args.no_config2 and world == 1:
             try:
                 res["config2_resident"] = config2_resident(local)
             except Exception as e:
