@@ -156,6 +156,9 @@ int hc_engine_layer_forward(void* engine, int layer, const uint16_t* x, int n, u
 int hc_engine_cache(void* engine, void** cache);
 /* Payload of one block at one layer (KV [2][H][tpb][hd], ACT [tpb][d]). */
 int hc_engine_read_block(void* engine, int kind, int loc, int pbn, int layer, uint16_t* out);
+/* Engine-held weights (bf16): layer >= 0 packed layer, -1 embedding [V x d],
+ * -2 positional [max_seq x d]. */
+int hc_engine_read_weights(void* engine, int layer, uint16_t* out);
 int hc_engine_capture_inputs(void* engine, int on);
 /* Decode-time layer inputs of the last step, [L][n][d] bf16 (n = last batch). */
 int hc_engine_captured_inputs(void* engine, uint16_t* out, long count);

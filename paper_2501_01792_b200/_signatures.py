@@ -77,6 +77,7 @@ SIGNATURES = {
     "hc_engine_layer_forward": (i, [vp, i, u16p, i, u16p, u16p, u16p]),
     "hc_engine_cache": (i, [vp, vpp]),
     "hc_engine_read_block": (i, [vp, i, i, i, i, u16p]),
+    "hc_engine_read_weights": (i, [vp, i, u16p]),
     "hc_engine_capture_inputs": (i, [vp, i]),
     "hc_engine_captured_inputs": (i, [vp, u16p, l]),
     "hc_engine_last_stats": (i, [vp, dp]),

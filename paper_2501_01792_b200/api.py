@@ -425,6 +425,8 @@ class Engine:
             check(lib().hc_engine_create_from_f64(C.byref(c), pos.shape[0], ptr(emb, C.c_double),
                                                   ptr(pos, C.c_double), ptrs, C.byref(self.opts), C.byref(h)))
         self._h = h
+        w_max_seq = max_seq if weights is None else np.asarray(weights["positional"]).shape[0]
+        self._max_seq = min(max_seq, w_max_seq) if max_seq > 0 else w_max_seq
         ch = C.c_void_p()
         check(lib().hc_engine_cache(self._h, C.byref(ch)))
         self.cache = HybridCache(self.cfg.tokens_per_block, _borrowed=ch, _owner=self)
@@ -522,6 +524,18 @@ class Engine:
         else:
             out = np.zeros((tpb, d), np.uint16)
         check(lib().hc_engine_read_block(self._h, _kind(kind), _loc(loc), pbn, layer, ptr(out, C.c_uint16)))
+        return out
+
+    def read_weights(self, layer: int) -> np.ndarray:
+        """Engine-held bf16 weights: packed layer (layer >= 0), -1 embedding, -2 positional."""
+        d, f = self.cfg.hidden_dim, self.cfg.ffn_dim
+        if layer == -1:
+            out = np.zeros((self.cfg.vocab_size, d), np.uint16)
+        elif layer == -2:
+            out = np.zeros((self._max_seq, d), np.uint16)
+        else:
+            out = np.zeros(4 * d * d + 2 * d * f, np.uint16)
+        check(lib().hc_engine_read_weights(self._h, layer, ptr(out, C.c_uint16)))
         return out
 
     def capture_inputs(self, on: bool = True) -> None:

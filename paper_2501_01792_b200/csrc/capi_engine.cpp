@@ -363,6 +363,9 @@ int hc_engine_cache(void* e, void** cache) {
 int hc_engine_read_block(void* e, int kind, int loc, int pbn, int layer, uint16_t* out) {
     return hc_guard([&] { eng(e)->read_block(kind_of(kind), loc_of(loc), pbn, layer, out); });
 }
+int hc_engine_read_weights(void* e, int layer, uint16_t* out) {
+    return hc_guard([&] { eng(e)->read_weights(layer, out); });
+}
 int hc_engine_capture_inputs(void* e, int on) {
     return hc_guard([&] { eng(e)->set_capture_layer_inputs(on != 0); });
 }

@@ -180,15 +180,6 @@ void fill_from_hostweights(const void* ctx, int l, uint16_t* dst) {
     const HostWeights* w = static_cast<const HostWeightsCtx*>(ctx)->w;
     std::memcpy(dst, w->layer(l), w->layer_elems() * 2);
 }
-struct GenCtx {
-    ModelConfig c;
-    uint64_t seed;
-    bool rescale;
-};
-void fill_from_generator(const void* ctx, int l, uint16_t* dst) {
-    const GenCtx* g = static_cast<const GenCtx*>(ctx);
-    generate_layer(g->c, g->seed, l, g->rescale, dst);
-}
 }  // namespace
 
 Engine::Engine(const HostWeights& w, const EngineOptions& o) : opt_(o) {
@@ -200,11 +191,37 @@ Engine::Engine(const ModelConfig& c, uint64_t seed, int max_seq, bool rescale, c
     ModelConfig cc = c;
     cc.validate();
     if (max_seq < 1) throw InputError("DecoderWeights: max_seq must be >= 1");
-    std::vector<uint16_t> emb(static_cast<size_t>(cc.vocab_size) * cc.hidden_dim);
-    std::vector<uint16_t> pos(static_cast<size_t>(max_seq) * cc.hidden_dim);
-    generate_tables(cc, seed, max_seq, emb.data(), pos.data());
-    GenCtx g{cc, seed, rescale};
-    init(cc, max_seq, emb.data(), pos.data(), fill_from_generator, &g);
+    // draw on the GPU (bit-exact with the host generator, weights_gen.cu)
+    init(cc, max_seq, nullptr, nullptr, nullptr, nullptr);
+    Impl& m = *impl_;
+    gen_weights_plain(reinterpret_cast<uint16_t*>(m.emb), static_cast<size_t>(m.V) * m.d, mix_seed(seed, 0),
+                      s_compute_);
+    gen_weights_plain(reinterpret_cast<uint16_t*>(m.pos), static_cast<size_t>(max_seq) * m.d, mix_seed(seed, 1),
+                      s_compute_);
+    double fac[6];
+    rescale_factors(cfg_, fac);
+    const int d = m.d, f = m.f;
+    auto draw_layer = [&](int l, bf16* dst) {
+        uint16_t* L = reinterpret_cast<uint16_t*>(dst);
+        const uint64_t base = 100 + static_cast<uint64_t>(l) * 8;  // model.cpp:90, 106-113
+        for (int k = 0; k < 3; ++k)
+            gen_weights_transposed(L + m.off.wqkv + static_cast<size_t>(k) * d * d, d, d, mix_seed(seed, base + k),
+                                   fac[k], rescale, s_compute_);
+        gen_weights_transposed(L + m.off.wproj, d, d, mix_seed(seed, base + 3), fac[3], rescale, s_compute_);
+        gen_weights_transposed(L + m.off.w1, d, f, mix_seed(seed, base + 4), fac[4], rescale, s_compute_);
+        gen_weights_transposed(L + m.off.w2, f, d, mix_seed(seed, base + 5), fac[5], rescale, s_compute_);
+    };
+    for (int l = 0; l < (m.w_all ? m.L : m.Lw); ++l) {
+        if (m.w_all) {
+            draw_layer(l, m.w_all + static_cast<size_t>(l) * m.LE);
+        } else {
+            draw_layer(l, m.wbuf[l & 1]);
+            HC_CUDA(cudaMemcpyAsync(m.h_w + static_cast<size_t>(l) * m.LE, m.wbuf[l & 1], m.LE * 2,
+                                    cudaMemcpyDeviceToHost, s_compute_));
+        }
+    }
+    HC_CUDA(cudaGetLastError());
+    HC_CUDA(cudaStreamSynchronize(s_compute_));
 }
 
 void Engine::init(const ModelConfig& c, int w_max_seq, const uint16_t* emb, const uint16_t* pos,
@@ -248,20 +265,20 @@ void Engine::init(const ModelConfig& c, int w_max_seq, const uint16_t* emb, cons
     // tables
     m.emb = dalloc<bf16>(static_cast<size_t>(m.V) * m.d);
     m.pos = dalloc<bf16>(static_cast<size_t>(w_max_seq) * m.d);
-    HC_CUDA(cudaMemcpy(m.emb, emb, static_cast<size_t>(m.V) * m.d * 2, cudaMemcpyHostToDevice));
-    HC_CUDA(cudaMemcpy(m.pos, pos, static_cast<size_t>(w_max_seq) * m.d * 2, cudaMemcpyHostToDevice));
+    if (emb) HC_CUDA(cudaMemcpy(m.emb, emb, static_cast<size_t>(m.V) * m.d * 2, cudaMemcpyHostToDevice));
+    if (pos) HC_CUDA(cudaMemcpy(m.pos, pos, static_cast<size_t>(w_max_seq) * m.d * 2, cudaMemcpyHostToDevice));
 
-    // weights
+    // weights (fill_layer == nullptr: the caller draws them on the device)
     if (opt_.weights_on_device) {
         m.w_all = dalloc<bf16>(m.LE * m.L);
-        std::vector<uint16_t> tmp(m.LE);
-        for (int l = 0; l < m.L; ++l) {
+        std::vector<uint16_t> tmp(fill_layer ? m.LE : 0);
+        for (int l = 0; fill_layer && l < m.L; ++l) {
             fill_layer(ctx, l, tmp.data());
             HC_CUDA(cudaMemcpy(m.w_all + static_cast<size_t>(l) * m.LE, tmp.data(), m.LE * 2, cudaMemcpyHostToDevice));
         }
     } else {
         m.h_w = halloc<uint16_t>(m.LE * m.Lw, false);
-        for (int l = 0; l < m.Lw; ++l) fill_layer(ctx, l, m.h_w + static_cast<size_t>(l) * m.LE);
+        for (int l = 0; fill_layer && l < m.Lw; ++l) fill_layer(ctx, l, m.h_w + static_cast<size_t>(l) * m.LE);
         m.wbuf[0] = dalloc<bf16>(m.LE);
         m.wbuf[1] = dalloc<bf16>(m.LE);
     }
@@ -931,6 +948,23 @@ void Engine::decode_step(const std::vector<std::string>& ids, const int* tokens,
 }
 
 // ---------------------------------------------------------------------------
+void Engine::read_weights(int layer, uint16_t* out) {
+    Impl& m = *impl_;
+    HC_CUDA(cudaStreamSynchronize(s_compute_));
+    if (layer == -1) {
+        HC_CUDA(cudaMemcpy(out, m.emb, static_cast<size_t>(m.V) * m.d * 2, cudaMemcpyDeviceToHost));
+    } else if (layer == -2) {
+        HC_CUDA(cudaMemcpy(out, m.pos, static_cast<size_t>(m.max_seq) * m.d * 2, cudaMemcpyDeviceToHost));
+    } else if (layer >= 0 && layer < m.L) {
+        if (m.w_all)
+            HC_CUDA(cudaMemcpy(out, m.w_all + static_cast<size_t>(layer) * m.LE, m.LE * 2, cudaMemcpyDeviceToHost));
+        else
+            std::memcpy(out, m.h_w + static_cast<size_t>(layer % m.Lw) * m.LE, m.LE * 2);
+    } else {
+        throw InputError("read_weights: layer out of range");
+    }
+}
+
 void Engine::read_block(BlockKind kind, Location loc, int pbn, int layer, uint16_t* out) {
     Impl& m = *impl_;
     if (layer < 0 || layer >= m.L) throw InputError("read_block: layer out of range");

@@ -113,6 +113,9 @@ public:
     // Payload of one block at one layer (bf16 bits; KV: [2][H][tpb][hd],
     // ACT: [tpb][d]) — for parity tests of the cache writers.
     void read_block(BlockKind kind, Location loc, int pbn, int layer, uint16_t* out);
+    // Engine-held weights (bf16 bits): layer >= 0 packed layer (model.hpp
+    // layout), -1 embedding [V x d], -2 positional [max_seq x d].
+    void read_weights(int layer, uint16_t* out);
     // Decode-time layer inputs of the last step: [L][n][d] (debug / parity).
     void set_capture_layer_inputs(bool on) { capture_inputs_ = on; }
     const std::vector<uint16_t>& captured_layer_inputs() const { return captured_; }

@@ -102,6 +102,13 @@ void scatter_kv_blocks(const BlockScatter& c, cudaStream_t st);
 // argmax over each row of fp32 logits [B x V]
 void argmax_rows(const float* logits, int B, int V, int* out, cudaStream_t st);
 
+// DecoderWeights::generate draws on the GPU (bit-exact with host/model.cpp):
+// U(-0.1, 0.1) stream `seed`, times scale (if apply_scale), -> bf16 bits;
+// transposed: dst[c*rows + r] = value(r, c) of the reference's [rows x cols].
+void gen_weights_transposed(uint16_t* dst, int rows, int cols, uint64_t seed, double scale, bool apply_scale,
+                            cudaStream_t st);
+void gen_weights_plain(uint16_t* dst, size_t n, uint64_t seed, cudaStream_t st);
+
 // fill a bf16 buffer with a deterministic hash pattern in [-a, a]
 void fill_pattern(bf16* dst, size_t n, uint64_t seed, float amp, cudaStream_t st);
 

@@ -158,3 +158,17 @@ def test_equivalence_seeded_models(seed):
         assert rel(o, ref) <= TOL, m
     assert rel(outs["act_only"], outs["kv_only"]) <= TOL
     assert rel(outs["hybrid"], outs["kv_only"]) <= TOL
+
+
+@pytest.mark.parametrize("on_device", [True, False])
+def test_gpu_weight_generation_bit_exact(on_device):
+    """DecoderWeights::generate drawn on the GPU (weights_gen.cu) equals the
+    host generator (itself bit-exact with the reference draws) bit for bit."""
+    from paper_2501_01792_b200 import api
+    cfg = api.ModelConfig(num_layers=2, hidden_dim=256, num_heads=2, ffn_dim=768, vocab_size=320)
+    host = api.generate_weights(cfg, 1234, 48, rescale=True)
+    eng = api.Engine(cfg, seed=1234, max_seq=48, rescale=True, weights_on_device=on_device)
+    assert np.array_equal(eng.read_weights(-1), host["embedding"])
+    assert np.array_equal(eng.read_weights(-2), host["positional"])
+    for l in range(2):
+        assert np.array_equal(eng.read_weights(l), host["layers"][l])
