@@ -175,6 +175,9 @@ int hc_engine_time_load_kv(void* engine, int n_tokens, int reps, double* seconds
  * Single kernels of the path on host buffers (parity-test boundary). */
 /* C = A . W, W passed transposed (Wt [N x K]); epi 0 bf16, 1 relu bf16, 3 fp32. */
 int hc_gemm_bf16(int epi, int M, int N, int K, const uint16_t* A, const uint16_t* Wt, void* out, int bn);
+/* Split-K weight-streaming GEMM (epi 0 / 1), fp32 partials reduced in a second kernel. */
+int hc_gemm_bf16_splitk(int epi, int M, int N, int K, const uint16_t* A, const uint16_t* Wt, uint16_t* out, int bn,
+                        int splits);
 /* recompute_kv_from_activation (decoder.cpp:123-129) into the paged layout. */
 int hc_recompute_kv_paged(int n_blocks, int tpb, int d, int heads, const uint16_t* act_pool, const uint16_t* wkv_t,
                           const int* tiles, int n_tiles, uint16_t* kv_out, int bn);

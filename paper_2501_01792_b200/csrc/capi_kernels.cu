@@ -70,6 +70,38 @@ int hc_gemm_bf16(int epi, int M, int N, int K, const uint16_t* A, const uint16_t
     });
 }
 
+// Split-K variant of hc_gemm_bf16 (epi 0 / 1): fp32 partials over `splits`
+// K ranges reduced by splitk_reduce — the weight-streaming decode GEMMs.
+int hc_gemm_bf16_splitk(int epi, int M, int N, int K, const uint16_t* A, const uint16_t* Wt, uint16_t* out, int bn,
+                        int splits) {
+    return hc_guard([&] {
+        if (epi != gemm::kStore && epi != gemm::kRelu) throw hc_input_error("hc_gemm_bf16_splitk: epi must be 0 or 1");
+        if (splits < 1) throw hc_input_error("hc_gemm_bf16_splitk: splits must be >= 1");
+        DevBuf<uint16_t> a(A, size_t(M) * K), w(Wt, size_t(N) * K), o(size_t(M) * N);
+        DevBuf<float> ws(size_t(splits) * M * N);
+        GemmCall c;
+        c.epi = epi;
+        c.A = reinterpret_cast<const bf16*>(a.p);
+        c.lda = K;
+        c.a_rows = M;
+        c.B = reinterpret_cast<const bf16*>(w.p);
+        c.ldb = K;
+        c.M = M;
+        c.N = N;
+        c.K = K;
+        c.out = o.p;
+        c.ldc = N;
+        c.bn = bn;
+        c.ws = ws.p;
+        c.ws_floats = ws.n;
+        c.splits = splits;
+        run_gemm(c, nullptr);
+        HC_CUDA(cudaGetLastError());
+        HC_CUDA(cudaDeviceSynchronize());
+        o.to_host(out);
+    });
+}
+
 // Recompute K|V of the ACT-cached blocks straight into the paged KV layout
 // (north-star (2); recompute_kv_from_activation, decoder.cpp:123-129).
 //   act_pool  [n_blocks x tpb x d]        ACT block payloads (bf16 bits)

@@ -73,7 +73,7 @@ T* halloc(size_t n, bool mapped) {
 }  // namespace
 
 void gemm_rows(int epi, const bf16* A, int M, int K, const bf16* W, int N, void* out, long long ldc, cudaStream_t st,
-               long long lda = 0);
+               long long lda = 0, float* ws = nullptr, size_t ws_floats = 0);
 
 struct Engine::Impl {
     int L = 0, d = 0, H = 0, hd = 0, f = 0, V = 0, tpb = 0, B = 0, max_seq = 0, max_blocks = 0, Lp = 0, Lw = 0;
@@ -91,6 +91,8 @@ struct Engine::Impl {
     float* logits = nullptr;
     int* amax = nullptr;
     float* attn_work = nullptr;
+    float* splitk_ws = nullptr;  // split-K partials of the weight-streaming decode GEMMs
+    size_t splitk_floats = 0;
     size_t attn_work_elems = 0;
     int* d_meta = nullptr;
     int* h_meta = nullptr;
@@ -292,6 +294,8 @@ void Engine::init(const ModelConfig& c, int w_max_seq, const uint16_t* emb, cons
     m.hbuf = dalloc<bf16>(static_cast<size_t>(m.B) * m.f);
     m.logits = dalloc<float>(static_cast<size_t>(m.B) * m.V);
     m.amax = dalloc<int>(m.B);
+    m.splitk_floats = static_cast<size_t>(16) * m.B * std::max(3 * m.d, m.f);
+    m.splitk_ws = dalloc<float>(m.splitk_floats);
     configure_cache(PoolCaps{opt_.kv_host_cap, opt_.kv_gpu_cap, opt_.act_host_cap, opt_.act_gpu_cap}, opt_.kv_on_gpu != 0,
                     opt_.mode, opt_.alloc, opt_.host_layers, opt_.recompute_ratio);
 }
@@ -390,7 +394,7 @@ Engine::~Engine() {
                     (void*)m.act_stage[1], (void*)m.x[0], (void*)m.x[1], (void*)m.qkv, (void*)m.att, (void*)m.proj,
                     (void*)m.hbuf, (void*)m.logits, (void*)m.amax, (void*)m.attn_work, (void*)m.d_meta,
                     (void*)m.px[0], (void*)m.px[1], (void*)m.pqkv, (void*)m.patt, (void*)m.pproj, (void*)m.ph,
-                    (void*)m.tr_kv})
+                    (void*)m.tr_kv, (void*)m.splitk_ws})
         if (p) cudaFree(p);
     for (void* p : {(void*)m.h_w, (void*)m.kv_host, (void*)m.act_host, (void*)m.h_meta})
         if (p) cudaFreeHost(p);
@@ -449,7 +453,7 @@ void Engine::run_layers(int T, int l0, int l1, const int* d_cu, uint16_t* layer_
 // ---------------------------------------------------------------------------
 // GEMM helpers (weights transposed [out][in]; see model.hpp)
 void gemm_rows(int epi, const bf16* A, int M, int K, const bf16* W, int N, void* out, long long ldc, cudaStream_t st,
-               long long lda) {
+               long long lda, float* ws, size_t ws_floats) {
     GemmCall c;
     c.epi = epi;
     c.A = A;
@@ -462,6 +466,8 @@ void gemm_rows(int epi, const bf16* A, int M, int K, const bf16* W, int N, void*
     c.K = K;
     c.out = out;
     c.ldc = ldc;
+    c.ws = ws;
+    c.ws_floats = ws_floats;
     run_gemm(c, st);
 }
 
@@ -867,7 +873,7 @@ void Engine::decode_step(const std::vector<std::string>& ids, const int* tokens,
             st.recompute_tokens += static_cast<double>(tl.size()) * gemm::BM;
         }
         m.span_begin(profile_, s_compute_, 2);
-        gemm_rows(gemm::kStore, xin, n, m.d, W + m.off.wqkv, 3 * m.d, m.qkv, 3 * m.d, s_compute_);
+        gemm_rows(gemm::kStore, xin, n, m.d, W + m.off.wqkv, 3 * m.d, m.qkv, 3 * m.d, s_compute_, 0, m.splitk_ws, m.splitk_floats);
         m.span_end(profile_, s_compute_);
         if (any_kv) {  // new token's K|V -> its KV slot (device + host)
             ap.src = m.qkv;
@@ -897,9 +903,9 @@ void Engine::decode_step(const std::vector<std::string>& ids, const int* tokens,
         decode_attention(a, s_compute_);
         m.span_end(profile_, s_compute_);
         m.span_begin(profile_, s_compute_, 2);
-        gemm_rows(gemm::kStore, m.att, n, m.d, W + m.off.wproj, m.d, m.proj, m.d, s_compute_);
-        gemm_rows(gemm::kRelu, m.proj, n, m.d, W + m.off.w1, m.f, m.hbuf, m.f, s_compute_);
-        gemm_rows(gemm::kStore, m.hbuf, n, m.f, W + m.off.w2, m.d, xout, m.d, s_compute_);
+        gemm_rows(gemm::kStore, m.att, n, m.d, W + m.off.wproj, m.d, m.proj, m.d, s_compute_, 0, m.splitk_ws, m.splitk_floats);
+        gemm_rows(gemm::kRelu, m.proj, n, m.d, W + m.off.w1, m.f, m.hbuf, m.f, s_compute_, 0, m.splitk_ws, m.splitk_floats);
+        gemm_rows(gemm::kStore, m.hbuf, n, m.f, W + m.off.w2, m.d, xout, m.d, s_compute_, 0, m.splitk_ws, m.splitk_floats);
         m.span_end(profile_, s_compute_);
         st.launches += 4 + (splits > 1 ? 2 : 1);
         HC_CUDA(cudaEventRecord(m.consumed[slot], s_compute_));

@@ -2,7 +2,9 @@
 // tile-shape heuristic and template dispatch.
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <mutex>
 #include <stdexcept>
 #include <string>
@@ -57,7 +59,7 @@ void launch(const GemmCall& c, const gemm::Params& p, cudaStream_t st) {
     }
     const CUtensorMap ta = make_map(c.A, c.a_rows, c.K, c.lda, gemm::BM);
     const CUtensorMap tb = make_map(c.B, c.N, c.K, c.ldb, BN);
-    const int tiles = p.num_m_tiles * p.num_n_tiles;
+    const int tiles = p.num_m_tiles * p.num_n_tiles * p.splits;
     int grid = tiles < num_sms() ? tiles : num_sms();
     if (c.max_ctas > 0 && grid > c.max_ctas) grid = c.max_ctas;
     kern<<<grid, gemm::kThreads, Cf::kSmemBytes, st>>>(ta, tb, p);
@@ -70,6 +72,7 @@ void dispatch_epi(const GemmCall& c, const gemm::Params& p, cudaStream_t st) {
         case gemm::kRelu: return launch<BN, gemm::kRelu>(c, p, st);
         case gemm::kKvPaged: return launch<BN, gemm::kKvPaged>(c, p, st);
         case gemm::kF32: return launch<BN, gemm::kF32>(c, p, st);
+        case gemm::kSplitF32: return launch<BN, gemm::kSplitF32>(c, p, st);
     }
     throw std::invalid_argument("gemm: unknown epilogue");
 }
@@ -90,6 +93,34 @@ int pick_bn(int num_m_tiles, int N) {
         }
     }
     return best;
+}
+
+// split-K planner for the weight-streaming regime (M <= 2 tiles): choose
+// (BN, splits) so every SM streams weights; per-CTA cost ~ units/SM x
+// (A + B tile bytes of one split) + the fp32 partial round trip.
+void pick_split(int num_m_tiles, int M, int N, int K, size_t ws_floats, int& bn_out, int& splits_out) {
+    const int sms = num_sms();
+    const int num_kb = (K + gemm::BK - 1) / gemm::BK;
+    double best = -1;
+    bn_out = pick_bn(num_m_tiles, N);
+    splits_out = 1;
+    for (int bn : {256, 128, 64}) {
+        for (int s = 1; s <= 16; ++s) {
+            const int kps = (num_kb + s - 1) / s;
+            if (s > 1 && kps < 4) break;
+            if (s > 1 && static_cast<size_t>(s) * M * N > ws_floats) break;
+            const long units = static_cast<long>(num_m_tiles) * ((N + bn - 1) / bn) * s;
+            const long per_cta = (units + sms - 1) / sms;
+            double cost = static_cast<double>(per_cta) * (gemm::BM + bn) * kps * gemm::BK * 2.0;
+            // fp32 partial write + reduce read per SM, plus ~5 us of extra launch
+            if (s > 1) cost += 2.0 * s * M * N * 4.0 / sms + 2.2e5;
+            if (best < 0 || cost < best) {
+                best = cost;
+                bn_out = bn;
+                splits_out = s;
+            }
+        }
+    }
 }
 
 }  // namespace
@@ -125,9 +156,32 @@ void run_gemm(const GemmCall& c, cudaStream_t st) {
     p.d = c.d;
     p.hd = c.hd;
     p.blk_off = c.blk_off;
+    p.group_m = c.group_m > 0 ? c.group_m : (c.K <= 4096 ? 32 : 16);
+    if (const char* g = std::getenv("HC_GEMM_GROUP_M")) p.group_m = std::max(1, std::atoi(g));  // tuning knob
+    p.splits = 1;
+    p.kb_per_split = (c.K + gemm::BK - 1) / gemm::BK;
     GemmCall cc = c;
     if (cc.a_rows <= 0) cc.a_rows = c.M;
-    const int bn = c.bn ? c.bn : pick_bn(p.num_m_tiles, c.N);
+    int bn = c.bn ? c.bn : pick_bn(p.num_m_tiles, c.N);
+    const bool can_split = c.ws && c.ws_floats && !c.m_tile_rows && p.num_m_tiles <= 2 &&
+                           (c.epi == gemm::kStore || c.epi == gemm::kRelu) && c.ldc == c.N && (!c.bn || c.splits);
+    if (can_split) {
+        int s = 1;
+        if (c.splits)
+            s = c.splits;
+        else
+            pick_split(p.num_m_tiles, c.M, c.N, c.K, c.ws_floats, bn, s);
+        if (static_cast<size_t>(s) * c.M * c.N > c.ws_floats) s = 1;
+        if (const char* e = std::getenv("HC_GEMM_SPLITS")) s = std::max(1, std::atoi(e));  // tuning knob
+        if (s > 1) {
+            const int num_kb = (c.K + gemm::BK - 1) / gemm::BK;
+            p.kb_per_split = (num_kb + s - 1) / s;
+            p.splits = (num_kb + p.kb_per_split - 1) / p.kb_per_split;
+            p.out = c.ws;
+            p.ldc = c.N;
+            cc.epi = gemm::kSplitF32;
+        }
+    }
     p.num_n_tiles = (c.N + bn - 1) / bn;
     switch (bn) {
         case 32: dispatch_epi<32>(cc, p, st); break;
@@ -136,6 +190,7 @@ void run_gemm(const GemmCall& c, cudaStream_t st) {
         case 256: dispatch_epi<256>(cc, p, st); break;
         default: throw std::invalid_argument("gemm: bn must be 32/64/128/256");
     }
+    if (p.splits > 1) splitk_reduce(c.ws, p.splits, c.M, c.N, static_cast<bf16*>(c.out), c.epi == gemm::kRelu, st);
 }
 
 }  // namespace hc

@@ -36,6 +36,11 @@ struct Params {
     long long ldc;
     // kKvPaged: row r -> block r / tpb + blk_off, token r % tpb
     int tpb, d, hd, blk_off;
+    int group_m;  // M tiles per rasterisation group (A tiles kept in L2 while N is swept)
+    // split-K (kSplitF32): work unit = (tile, split); split s covers k-blocks
+    // [s*kb_per_split, (s+1)*kb_per_split) and writes fp32 partials to
+    // out + (s*M + row)*ldc
+    int splits, kb_per_split;
 };
 
 template <int BN>
@@ -50,9 +55,10 @@ struct Cfg {
 };
 
 __device__ __forceinline__ void tile_coords(int tile, const Params& p, int& m_idx, int& n_idx) {
-    // grouped rasterisation: 16 M-tiles share each sweep over N so concurrently
-    // running CTAs reuse A and B tiles from L2
-    const int G = p.num_m_tiles < 16 ? p.num_m_tiles : 16;
+    // grouped rasterisation: group_m M-tiles share each sweep over N so
+    // concurrently running CTAs reuse A and B tiles from L2
+    tile %= p.num_m_tiles * p.num_n_tiles;  // split-K units repeat the tile grid
+    const int G = p.num_m_tiles < p.group_m ? p.num_m_tiles : p.group_m;
     const int group = G * p.num_n_tiles;
     const int g = tile / group;
     const int first_m = g * G;
@@ -63,10 +69,10 @@ __device__ __forceinline__ void tile_coords(int tile, const Params& p, int& m_id
 }
 
 template <int BN, int EPI>
-__device__ __forceinline__ void epilogue_chunk(const Params& p, int row, int col, const uint32_t (&v)[16]) {
+__device__ __forceinline__ void epilogue_chunk(const Params& p, int row, int col, int split, const uint32_t (&v)[16]) {
     if (row >= p.M || col >= p.N) return;
-    if constexpr (EPI == kF32) {
-        float* dst = static_cast<float*>(p.out) + static_cast<long long>(row) * p.ldc + col;
+    if constexpr (EPI == kF32 || EPI == kSplitF32) {
+        float* dst = static_cast<float*>(p.out) + static_cast<long long>(row + split * p.M) * p.ldc + col;
 #pragma unroll
         for (int j = 0; j < 16; j += 4) ptx::st_global_v4(dst + j, v[j], v[j + 1], v[j + 2], v[j + 3]);
         return;
@@ -140,19 +146,27 @@ __global__ void __launch_bounds__(kThreads, 1)
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
-    const int num_tiles = p.num_m_tiles * p.num_n_tiles;
+    const int grid_tiles = p.num_m_tiles * p.num_n_tiles;
+    const int num_tiles = grid_tiles * p.splits;
     const int num_kb = (p.K + BK - 1) / BK;
+    // k-block range of work unit `tile` (whole K unless split-K)
+    auto kb_range = [&](int tile, int& kb0, int& kb1) {
+        const int s = tile / grid_tiles;
+        kb0 = s * p.kb_per_split;
+        kb1 = kb0 + p.kb_per_split < num_kb ? kb0 + p.kb_per_split : num_kb;
+    };
 
     if (warp == 0) {
         if (lane == 0) {
             int stage = 0;
             uint32_t phase = 0;
             for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-                int mi, ni;
+                int mi, ni, kb0, kb1;
                 tile_coords(tile, p, mi, ni);
+                kb_range(tile, kb0, kb1);
                 const int m_row = p.m_tile_rows ? p.m_tile_rows[mi] : mi * BM;
                 const int n_row = ni * BN;
-                for (int kb = 0; kb < num_kb; ++kb) {
+                for (int kb = kb0; kb < kb1; ++kb) {
                     ptx::mbar_wait(&empty[stage], phase ^ 1);
                     ptx::mbar_arrive_expect_tx(&full[stage], C::kStageBytes);
                     ptx::tma_load_2d(smem_a + stage * C::kABytes, &tmA, &full[stage], kb * BK, m_row);
@@ -172,10 +186,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             int as = 0;
             uint32_t aphase = 0;
             for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+                int kb0, kb1;
+                kb_range(tile, kb0, kb1);
                 ptx::mbar_wait(&tempty[as], aphase ^ 1);
                 ptx::tc_fence_after();
                 const uint32_t d_tmem = tmem_base + as * BN;
-                for (int kb = 0; kb < num_kb; ++kb) {
+                for (int kb = kb0; kb < kb1; ++kb) {
                     ptx::mbar_wait(&full[stage], phase);
                     ptx::tc_fence_after();
                     const uint64_t a_desc = ptx::sw128_kmajor_desc(ptx::smem_u32(smem_a + stage * C::kABytes));
@@ -183,7 +199,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                     for (int k = 0; k < BK / 16; ++k) {
                         // +32 B per 16-element K step inside the 128 B swizzle atom
-                        ptx::mma_bf16_ss(d_tmem, a_desc + 2 * k, b_desc + 2 * k, idesc, (kb | k) != 0);
+                        ptx::mma_bf16_ss(d_tmem, a_desc + 2 * k, b_desc + 2 * k, idesc, ((kb - kb0) | k) != 0);
                     }
                     ptx::mma_commit(&empty[stage]);
                     if (++stage == S) {
@@ -209,6 +225,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int m_row = p.m_tile_rows ? p.m_tile_rows[mi] : mi * BM;
             const int row = m_row + r_in_tile;
             const int n0 = ni * BN;
+            const int split = tile / grid_tiles;
             ptx::mbar_wait(&tfull[as], aphase);
             ptx::tc_fence_after();
             const uint32_t t_row = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + as * BN;
@@ -217,7 +234,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 uint32_t v[16];
                 ptx::tmem_ld_x16(t_row + c, v);
                 ptx::tmem_ld_wait();
-                epilogue_chunk<BN, EPI>(p, row, n0 + c, v);
+                epilogue_chunk<BN, EPI>(p, row, n0 + c, split, v);
             }
             ptx::tc_fence_before();
             ptx::mbar_arrive(&tempty[as]);

@@ -26,7 +26,13 @@ struct GemmCall {
     int tpb = 0, d = 0, hd = 0, blk_off = 0;  // kKvPaged
     int bn = 0;                  // 0 = heuristic
     int max_ctas = 0;            // 0 = all SMs
+    int group_m = 0;             // rasterisation group (0 = default 16)
+    float* ws = nullptr;         // split-K workspace (fp32); null disables split-K
+    size_t ws_floats = 0;
+    int splits = 0;              // 0 = planner (pick_split), else forced split count
 };
+// out[m][n] = bf16(epi(sum_s ws[s][m][n])) — the split-K finish (relu optional)
+void splitk_reduce(const float* ws, int splits, int M, int N, bf16* out, bool relu, cudaStream_t st);
 void run_gemm(const GemmCall& c, cudaStream_t st);
 int num_sms();
 

@@ -1,6 +1,7 @@
 // Small HBM-bound kernels of the path: embedding gather, the activation-cache
 // writer / KV append for decode tokens, prefill block scatter, argmax.
 // All move 16-byte vectors; one CTA per row / block.
+#include <algorithm>
 #include <cfloat>
 #include <stdexcept>
 
@@ -151,6 +152,34 @@ __global__ void argmax_kernel(const float* __restrict__ logits, int V, int* __re
     }
 }
 
+// 8 columns per thread; partial s of element (m, n) at ws[(s*M + m)*N + n]
+__global__ void splitk_reduce_kernel(const float* __restrict__ ws, int splits, int M, int N, bf16* __restrict__ out,
+                                     int relu) {
+    const size_t n8 = static_cast<size_t>(M) * N / 8;
+    const size_t plane = static_cast<size_t>(M) * N;
+    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n8;
+         i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        for (int s = 0; s < splits; ++s) {
+            const float4* src = reinterpret_cast<const float4*>(ws + s * plane + i * 8);
+            const float4 a = __ldg(src), b = __ldg(src + 1);
+            acc[0] += a.x; acc[1] += a.y; acc[2] += a.z; acc[3] += a.w;
+            acc[4] += b.x; acc[5] += b.y; acc[6] += b.z; acc[7] += b.w;
+        }
+        uint32_t o[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            float x = acc[2 * j], y = acc[2 * j + 1];
+            if (relu) {
+                x = fmaxf(x, 0.f);
+                y = fmaxf(y, 0.f);
+            }
+            o[j] = ptx::pack_bf16x2(x, y);
+        }
+        *reinterpret_cast<uint4*>(out + i * 8) = make_uint4(o[0], o[1], o[2], o[3]);
+    }
+}
+
 __global__ void fill_pattern_kernel(bf16* dst, size_t n, uint64_t seed, float amp) {
     for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
          i += static_cast<size_t>(gridDim.x) * blockDim.x) {
@@ -190,6 +219,13 @@ void scatter_kv_blocks(const BlockScatter& c, cudaStream_t st) {
 
 void argmax_rows(const float* logits, int B, int V, int* out, cudaStream_t st) {
     if (B > 0) argmax_kernel<<<B, 256, 0, st>>>(logits, V, out);
+}
+
+void splitk_reduce(const float* ws, int splits, int M, int N, bf16* out, bool relu, cudaStream_t st) {
+    if (N % 8) throw std::invalid_argument("splitk_reduce: N must be a multiple of 8");
+    const size_t n8 = static_cast<size_t>(M) * N / 8;
+    const int blocks = static_cast<int>(std::min<size_t>((n8 + 255) / 256, 4 * static_cast<size_t>(num_sms())));
+    if (n8) splitk_reduce_kernel<<<blocks, 256, 0, st>>>(ws, splits, M, N, out, relu ? 1 : 0);
 }
 
 void fill_pattern(bf16* dst, size_t n, uint64_t seed, float amp, cudaStream_t st) {

@@ -41,6 +41,17 @@ def gemm_bf16(a_bits: np.ndarray, wt_bits: np.ndarray, epi: int = 0, bn: int = 0
     return out
 
 
+def gemm_bf16_splitk(a_bits: np.ndarray, wt_bits: np.ndarray, splits: int, epi: int = 0, bn: int = 128) -> np.ndarray:
+    """Split-K C = A . W (W transposed [N x K]); bf16 out (epi 0 store, 1 relu)."""
+    M, K = a_bits.shape
+    N, _ = wt_bits.shape
+    a, ap = _u16(a_bits)
+    w, wp = _u16(wt_bits)
+    out = np.zeros((M, N), np.uint16)
+    check(lib().hc_gemm_bf16_splitk(epi, M, N, K, ap, wp, ptr(out, C.c_uint16), bn, splits))
+    return out
+
+
 def recompute_kv_paged(act_pool_bits: np.ndarray, wkv_t_bits: np.ndarray, heads: int,
                        tiles: np.ndarray, bn: int = 0) -> np.ndarray:
     """act_pool [n_blocks, tpb, d] -> kv [n_blocks, 2, H, tpb, hd] (bf16 bits)."""

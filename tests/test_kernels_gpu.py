@@ -156,3 +156,20 @@ def test_prefill_attention_causal(native, n_req, P, H, hd):
         sl = slice(r * P, (r + 1) * P)
         want = O.attention_rows(x[sl, :d], x[sl, d:2 * d], x[sl, 2 * d:], list(range(1, P + 1)), H, True)
         assert rel(got[sl], want) <= TOL_BF16
+
+
+@pytest.mark.parametrize("M,N,K,bn,splits,epi", [
+    (128, 512, 2048, 128, 4, 0), (64, 768, 3072, 64, 3, 1), (100, 1024, 4096, 256, 8, 0), (128, 256, 448, 128, 2, 1),
+    (128, 384, 1000, 64, 5, 0),
+])
+def test_gemm_splitk(native, M, N, K, bn, splits, epi):
+    """Split-K decode GEMM: fp32 partials over K ranges + reduce == the full GEMM."""
+    from paper_2501_01792_b200.kernels import gemm_bf16_splitk
+    rng = np.random.default_rng(K + splits)
+    a = rand_bits(rng, (M, K))
+    wt = rand_bits(rng, (N, K), 1.0 / np.sqrt(K))
+    ref = f64(a) @ f64(wt).T
+    if epi == 1:
+        ref = np.maximum(ref, 0)
+    got = f64(gemm_bf16_splitk(a, wt, splits, epi, bn))
+    assert rel(got, ref) <= TOL_BF16
