@@ -1,0 +1,44 @@
+"""Small run of every kernel of the path for compute-sanitizer
+(memcheck / racecheck / synccheck): engine prefill + decode in hybrid mode
+with host pools and streamed weights, token-recompute mode, split-K and
+split-attention paths.
+
+    compute-sanitizer --tool memcheck python scripts/sanitize_smoke.py
+"""
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+from paper_2501_01792_b200 import api, kernels  # noqa: E402
+
+
+def main():
+    cfg = api.ModelConfig(num_layers=2, hidden_dim=256, num_heads=2, ffn_dim=512, vocab_size=512, tokens_per_block=16)
+    rng = np.random.default_rng(0)
+    prompts = [rng.integers(0, 512, 37).tolist(), rng.integers(0, 512, 20).tolist()]
+    eng = api.Engine(cfg, seed=3, max_seq=64, max_batch=2, weights_on_device=False,
+                     caps=api.PoolCaps(kv_host=8, act_host=8, act_gpu=1), allocation=api.HostAllocation(1, 1))
+    eng.prefill(["a", "b"], prompts)
+    for _ in range(2):
+        eng.decode_step(["a", "b"], [1, 2], want_logits=True, want_argmax=True)
+    eng.configure_cache(api.PoolCaps(kv_host=8), mode="token_recompute", recompute_ratio=0.5)
+    eng.prefill(["a"], [prompts[0]])
+    eng.decode_step(["a"], [5])
+    eng.close()
+    a = kernels.f32_to_bf16_bits(rng.uniform(-1, 1, (64, 1024)))
+    w = kernels.f32_to_bf16_bits(rng.uniform(-0.05, 0.05, (256, 1024)))
+    kernels.gemm_bf16_splitk(a, w, 4, 1, 128)
+    q = kernels.f32_to_bf16_bits(rng.uniform(-1, 1, (2, 256)))
+    pool = kernels.f32_to_bf16_bits(rng.uniform(-1, 1, (8, 2, 2, 16, 128)))
+    refs = np.array([[0, 1, 2, 3], [4, 5, 6, 7]], np.int32)
+    kernels.decode_attention(q, pool, pool, refs, np.array([4, 3], np.int32), np.array([60, 40], np.int32), 2,
+                             True, 2)
+    print("sanitize smoke ok")
+
+
+if __name__ == "__main__":
+    main()
