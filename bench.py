@@ -53,6 +53,8 @@ def parse():
     p.add_argument("--sweep", default="0,0.3333333333333333,0.5,1,tr0.5",
                    help="ACT shares r to time besides the headline; trX = token-recompute baseline at ratio X")
     p.add_argument("--no-config2", action="store_true", help="skip the OPT-6.7B resident (config 2) variant")
+    p.add_argument("--artifacts", default="", help="write the reference CLI's artifacts (kv_gen.csv, load_kv.csv, "
+                                                    "bundle.json, plan.json, metrics.json, trace.json) here")
     return p.parse_args()
 
 
@@ -332,6 +334,65 @@ def variant(eng, cfg, ids, tokens, P, r, caps_mode_alloc, host_layers, steps, wa
             "act_context_tokens": act_context_tokens(eng, ids)}
 
 
+def _np_default(o):
+    return o.item() if hasattr(o, "item") else str(o)
+
+
+def write_artifacts(out_dir, eng, cfg, ids, planner, prof, mode, r):
+    """The reference CLI's artifacts from MEASURED B200 data, in its schemas
+    (main.cpp:75-115, 146-166, 255-275; timing.cpp:147-153; plan.cpp:22-28):
+    the unmodified `hybridsim plan --bundle` / `simulate --plan` can consume them."""
+    from paper_2501_01792_b200 import api
+    os.makedirs(out_dir, exist_ok=True)
+    meta = {"version": "b200-measured", "seed": 42, "inputs": {}}
+    cfgj = {"name": cfg.name, "num_layers": cfg.num_layers, "hidden_dim": cfg.hidden_dim,
+            "num_heads": cfg.num_heads, "ffn_dim": cfg.ffn_dim, "vocab_size": cfg.vocab_size,
+            "tokens_per_block": cfg.tokens_per_block, "bytes_per_scalar": cfg.bytes_per_scalar, "seed": 0}
+    if planner and "kv_gen_samples" in planner:
+        for name, key in (("kv_gen.csv", "kv_gen_samples"), ("load_kv.csv", "load_kv_samples")):
+            with open(os.path.join(out_dir, name), "w") as fh:
+                fh.write("n_tokens,seconds\n" + "".join(f"{n:.0f},{s:.9e}\n" for n, s in planner[key]))
+        per, total = api.weight_bytes(cfg)
+        bundle = {"kv_gen": {"slope": planner["t_kv_gen"]["slope_s_per_token"],
+                             "intercept": planner["t_kv_gen"]["intercept_s"], "r2": planner["t_kv_gen"]["r2"],
+                             "intercept_clamped": planner["t_kv_gen"]["intercept_s"] == 0.0},
+                  "load_kv": {"slope": planner["t_load_kv"]["slope_s_per_token"],
+                              "intercept": planner["t_load_kv"]["intercept_s"], "r2": planner["t_load_kv"]["r2"],
+                              "intercept_clamped": planner["t_load_kv"]["intercept_s"] == 0.0},
+                  "t_load_w": planner["t_load_w_s"], "s_weight_layer": per, "s_weight_total": total,
+                  "model": cfgj, "meta": meta}
+        with open(os.path.join(out_dir, "bundle.json"), "w") as fh:
+            json.dump(bundle, fh, indent=2, default=_np_default)
+        plan = dict(planner["allocation"])
+        plan["predicted"] = {"t_pcie": planner["planned_t_pcie_s"], "t_computation": planner["planned_t_comp_s"]}
+        plan["meta"] = meta
+        with open(os.path.join(out_dir, "plan.json"), "w") as fh:
+            json.dump(plan, fh, indent=2, default=_np_default)
+    L = cfg.num_layers
+    kvb, actb = api.HybridCache.bytes_of("KV", cfg), api.HybridCache.bytes_of("ACT", cfg)
+    kv_blocks = act_host_blocks = 0
+    for rid in ids:
+        for e in eng.cache.table(rid).entries:
+            if int(e.kind) == 0 and int(e.location) == 0:
+                kv_blocks += 1
+            elif int(e.kind) == 1 and int(e.location) == 0:
+                act_host_blocks += 1
+    w_layer, _ = api.weight_bytes(cfg)
+    step_s = prof["step_ms"] / 1e3
+    metrics = {"tokens_generated": len(ids), "makespan_s": step_s, "throughput_tok_s": len(ids) / step_s,
+               "pcie_busy": prof["copy_ms"] / prof["step_ms"], "gpu_busy": None, "prefill_s": 0.0, "gen_s": step_s,
+               "traffic": {"weights": w_layer * L, "kv_load": kv_blocks * kvb * L, "act_load": act_host_blocks * actb * L,
+                           "kv_store": None, "act_store": None},
+               "mode": mode, "act_share_r": r, "batch": len(ids), "measured_on": "B200 (one profiled decode step)",
+               "meta": meta}
+    with open(os.path.join(out_dir, "metrics.json"), "w") as fh:
+        json.dump(metrics, fh, indent=2, default=_np_default)
+    tr = eng.trace()
+    tr["meta"] = meta
+    with open(os.path.join(out_dir, "trace.json"), "w") as fh:
+        json.dump(tr, fh, default=_np_default)
+
+
 def calibrate_planner(eng, cfg, link_gbs, caps_act_rows, host_mem, act_gpu=0):
     """North-star (5): measured recompute-GEMM and host-link samples ->
     bundle_from_samples (timing.cpp:172-183) -> plan_host_allocation
@@ -403,6 +464,8 @@ def our_arm(args, cfg, world, rank, local, dist):
     # one profiled (untimed) step: per-kernel split + copy-stream GB/s
     prof = run_steps(eng, ids, tokens, args.warmup, 1, prof=True)["last"]
     act_tokens = act_context_tokens(eng, ids)
+    if args.artifacts and rank == 0:
+        write_artifacts(args.artifacts, eng, cfg, ids, planner, prof, mode, r)
 
     clocks = ClockSampler(local)
     barrier(dist)

@@ -167,6 +167,10 @@ int hc_engine_captured_inputs(void* engine, uint16_t* out, long count);
 int hc_engine_last_stats(void* engine, double* out10);
 /* Per-kernel CUDA-event timing of the next steps (small overhead). */
 int hc_engine_set_profile(void* engine, int on);
+/* Events of the last profiled step in the reference's trace.json schema
+ * {"events":[{name, track, start_us, end_us, iteration, layer, minibatch}]}
+ * (SimEvent, sim.hpp:50-58; main.cpp:263-275). */
+int hc_engine_trace_json(void* engine, char* buf, long len, long* needed);
 /* Planner calibration on this engine: seconds per layer. */
 int hc_engine_time_kv_gen(void* engine, int n_tokens, int reps, double* seconds);
 int hc_engine_time_load_kv(void* engine, int n_tokens, int reps, double* seconds);

@@ -346,6 +346,34 @@ int ref_plan_host_allocation(const double* bundle, const double* mem, int tpb, l
     });
 }
 
+// Parse a bundle.json / plan.json with the reference's own loaders
+// (TimingBundle::from_json timing.cpp:155-163, HostAllocation::from_json
+// plan.cpp:30-39): out7 = {kv slope, kv icept, load slope, load icept,
+// t_load_w, s_weight_layer, s_weight_total}; alloc6 as ref_plan_host_allocation.
+int ref_parse_artifacts(const char* bundle_json, const char* plan_json, double* out7, long* alloc6) {
+    return guarded([&] {
+        if (bundle_json) {
+            const TimingBundle b = TimingBundle::from_json(nlohmann::json::parse(bundle_json));
+            out7[0] = b.t_kv_gen.slope;
+            out7[1] = b.t_kv_gen.intercept;
+            out7[2] = b.t_load_kv.slope;
+            out7[3] = b.t_load_kv.intercept;
+            out7[4] = b.t_load_w;
+            out7[5] = static_cast<double>(b.s_weight_layer);
+            out7[6] = static_cast<double>(b.s_weight_total);
+        }
+        if (plan_json) {
+            const HostAllocation a = HostAllocation::from_json(nlohmann::json::parse(plan_json));
+            alloc6[0] = a.act_host;
+            alloc6[1] = a.kv_host;
+            alloc6[2] = a.act_init;
+            alloc6[3] = a.kv_init;
+            alloc6[4] = a.act_remain;
+            alloc6[5] = a.kv_remain;
+        }
+    });
+}
+
 // out4 = {slope, intercept, r2, clamped}
 int ref_fit_linear(const double* n_tokens, const double* seconds, int count, double* out4) {
     return guarded([&] {

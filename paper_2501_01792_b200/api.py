@@ -556,6 +556,14 @@ class Engine:
     def set_profile(self, on: bool = True) -> None:
         check(lib().hc_engine_set_profile(self._h, int(on)))
 
+    def trace(self) -> dict:
+        """Events of the last profiled step (reference trace.json schema)."""
+        need = C.c_long()
+        check(lib().hc_engine_trace_json(self._h, None, 0, C.byref(need)))
+        buf = C.create_string_buffer(need.value)
+        check(lib().hc_engine_trace_json(self._h, buf, need.value, C.byref(need)))
+        return json.loads(buf.value.decode()) if buf.value else {"events": []}
+
     def time_kv_gen(self, n_tokens: int, reps: int = 5) -> float:
         s = C.c_double()
         check(lib().hc_engine_time_kv_gen(self._h, n_tokens, reps, C.byref(s)))

@@ -385,6 +385,17 @@ int hc_engine_last_stats(void* e, double* o) {
         std::memcpy(o, v, sizeof v);
     });
 }
+int hc_engine_trace_json(void* e, char* buf, long len, long* needed) {
+    return hc_guard([&] {
+        const std::string& s = eng(e)->last_trace();
+        if (needed) *needed = static_cast<long>(s.size() + 1);
+        if (buf && len > 0) {
+            const size_t k = std::min<size_t>(s.size(), static_cast<size_t>(len - 1));
+            std::memcpy(buf, s.data(), k);
+            buf[k] = '\0';
+        }
+    });
+}
 int hc_engine_set_profile(void* e, int on) {
     return hc_guard([&] { eng(e)->set_profile(on != 0); });
 }

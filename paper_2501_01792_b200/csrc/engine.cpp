@@ -2,6 +2,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <numeric>
 #include <unordered_set>
@@ -120,11 +121,13 @@ struct Engine::Impl {
     struct Span {
         int kind;  // 0 recompute, 1 attention, 2 other gemm, 3 copy
         cudaEvent_t a, b;
+        int layer;
     };
     std::vector<Span> spans;
+    int cur_layer = -1;
     void span_begin(bool on, cudaStream_t s, int kind) {
         if (!on) return;
-        spans.push_back({kind, take_event(), nullptr});
+        spans.push_back({kind, take_event(), nullptr, cur_layer});
         HC_CUDA(cudaEventRecord(spans.back().a, s));
     }
     void span_end(bool on, cudaStream_t s) {
@@ -760,6 +763,7 @@ void Engine::decode_step(const std::vector<std::string>& ids, const int* tokens,
 
     for (int l = 0; l < m.L; ++l) {
         const int slot = l & 1;
+        m.cur_layer = l;
         if (stream_any) {
             // copy stream: weights + this layer's host blocks into slot l%2,
             // after compute released the slot (layer l-2)
@@ -932,6 +936,31 @@ void Engine::decode_step(const std::vector<std::string>& ids, const int* tokens,
     float ms = 0;
     HC_CUDA(cudaEventElapsedTime(&ms, m.ev0, m.ev1));
     st.step_ms = ms;
+    // trace of the profiled step: the reference's SimEvent schema
+    // (sim.hpp:50-58; trace.json main.cpp:263-275) from CUDA events
+    std::string trace;
+    if (profile_) {
+        trace = "{\"events\":[";
+        bool first = true;
+        for (const auto& sp : m.spans) {
+            float t0 = 0, t1 = 0;
+            HC_CUDA(cudaEventElapsedTime(&t0, m.ev0, sp.a));
+            HC_CUDA(cudaEventElapsedTime(&t1, m.ev0, sp.b));
+            static const char* names[4] = {"kv_gen", "attention", "qkv_and_forward", "host_load"};
+            char buf[256];
+            std::snprintf(buf, sizeof buf,
+                          "%s{\"name\":\"%s\",\"track\":\"%s\",\"start_us\":%.3f,\"end_us\":%.3f,\"iteration\":%ld,"
+                          "\"layer\":%d,\"minibatch\":0}",
+                          first ? "" : ",", (sp.kind == 0 && token_mode_) ? "token_recompute" : names[sp.kind],
+                          sp.kind == 3 ? "PCIe" : "GPU", t0 * 1e3, t1 * 1e3, static_cast<long>(step_counter_),
+                          sp.layer);
+            trace += buf;
+            first = false;
+        }
+        trace += "]}";
+        last_trace_ = trace;
+    }
+    ++step_counter_;
     for (const auto& sp : m.spans) {
         float t = 0;
         HC_CUDA(cudaEventElapsedTime(&t, sp.a, sp.b));

@@ -132,6 +132,9 @@ public:
     const ModelConfig& config() const { return cfg_; }
     const StepStats& last_stats() const { return stats_; }
     void set_profile(bool on) { profile_ = on; }
+    // {"events":[{name, track, start_us, end_us, iteration, layer, minibatch}]}
+    // of the last profiled decode step — the reference's trace.json schema.
+    const std::string& last_trace() const { return last_trace_; }
     cudaStream_t compute_stream() const { return s_compute_; }
 
 private:
@@ -149,6 +152,8 @@ private:
     StepStats stats_{};
     bool profile_ = false;
     bool capture_inputs_ = false;
+    std::string last_trace_;     // events of the last profiled step (JSON)
+    long step_counter_ = 0;
     bool token_mode_ = false;                                     // CacheMode::TokenRecompute
     std::unordered_map<std::string, std::vector<int>> rc_ids_;    // recompute-only prompt prefixes
     int rc_prefix(int prompt_len) const;
