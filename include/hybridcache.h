@@ -103,6 +103,16 @@ int hc_flop_count(int kind, const hc_model_config* cfg, long n_tokens, int k, do
 /* weight_bytes (timing.cpp:118-127): out2 = {per_layer, total} */
 int hc_weight_bytes(const hc_model_config* cfg, uint64_t* out2);
 
+/* -------------------------------------------------- mini-batch packer ---
+ * form_minibatches (minibatch.cpp:36-83): order[k] = request index in packing
+ * order, batch_of[i] = mini-batch of request i. */
+int hc_form_minibatches(int n, const char* const* ids, const long* act_blocks, const long* kv_blocks, long act_max,
+                        long kv_max, const double* bundle5, int tpb, int* order, int* batch_of, int* n_batches);
+/* balance / cost_fb (minibatch.cpp:10-23): out2 = {balance, F_b} */
+int hc_cost_fb(long act_mb, long kv_mb, const double* bundle5, int tpb, double* out2);
+/* default_packer (sim.cpp:122-132): out2 = {act_max, kv_max} */
+int hc_default_packer(double gpu_mem_bytes, const hc_model_config* cfg, long* out2);
+
 /* -------------------------------------------------------------- engine ---
  * The decode path proper: prefill / decode-step calls over the hybrid cache
  * (forward_prompt decoder.cpp:144-157, generation_step 159-174, batched),

@@ -721,6 +721,61 @@ def plan_host_allocation(b: TimingBundle, mem: MemoryBudget, tpb: int, act_gpu: 
 
 
 # --------------------------------------------------------------------------
+# Mini-batch packer — minibatch.cpp:10-83 (greedy) and 148-170 (brute force)
+# --------------------------------------------------------------------------
+def balance(act_mb: int, kv_mb: int, b: TimingBundle, tpb: int) -> float:
+    if act_mb < 0 or kv_mb < 0:
+        raise InputError("balance: negative block count")
+    num = eval_model(b.t_kv_gen, float(act_mb) * tpb)
+    den = eval_model(b.t_load_kv, float(kv_mb) * tpb)
+    if num == 0.0 and den == 0.0:
+        return 1.0
+    if den == 0.0:
+        return math.inf
+    return num / den
+
+
+def cost_fb(act_mb: int, kv_mb: int, b: TimingBundle, tpb: int) -> float:
+    x = balance(act_mb, kv_mb, b, tpb)
+    if x == 0.0:
+        return math.inf
+    return max(x, 1.0 / x)
+
+
+def form_minibatches(requests, act_max: int, kv_max: int, b: TimingBundle, tpb: int):
+    """requests: [(id, act_blocks, kv_blocks)] -> [[ids], ...] (minibatch.cpp:36-83)."""
+    if act_max < 1 or kv_max < 1:
+        raise InputError("form_minibatches: capacities must be >= 1")
+    for rid, a, k in requests:
+        if a < 0 or k < 0:
+            raise InputError("form_minibatches: negative block count for request " + rid)
+        if a > act_max or k > kv_max:
+            raise InputError("request too large for GPU buffer capacities: " + rid)
+    order = sorted(requests, key=lambda r: (-(r[1] + r[2]), r[0]))
+    used = [False] * len(order)
+    left = len(order)
+    out = []
+    while left:
+        ids, am, km, fb = [], 0, 0, math.inf
+        changed = True
+        while changed:
+            changed = False
+            for i, (rid, a, k) in enumerate(order):
+                if used[i] or am + a > act_max or km + k > kv_max:
+                    continue
+                after = cost_fb(am + a, km + k, b, tpb)
+                if ids and after > fb:
+                    continue
+                ids.append(rid)
+                am, km, fb = am + a, km + k, after
+                used[i] = True
+                left -= 1
+                changed = True
+        out.append(ids)
+    return out
+
+
+# --------------------------------------------------------------------------
 # Block-kind assignment in the simulator's call order — sim.cpp:150-223,308-310
 # --------------------------------------------------------------------------
 HYBRID, KV_ONLY, ACT_ONLY, TOKEN_RECOMPUTE_MODE = "hybrid", "kv_only", "act_only", "token_recompute"

@@ -30,6 +30,7 @@
 #include "hybridsim/decoder.hpp"
 #include "hybridsim/errors.hpp"
 #include "hybridsim/flops.hpp"
+#include "hybridsim/minibatch.hpp"
 #include "hybridsim/plan.hpp"
 #include "hybridsim/timing.hpp"
 #include "hybridsim/verify.hpp"
@@ -371,6 +372,25 @@ int ref_parse_artifacts(const char* bundle_json, const char* plan_json, double* 
             alloc6[4] = a.act_remain;
             alloc6[5] = a.kv_remain;
         }
+    });
+}
+
+// form_minibatches (minibatch.cpp:36-83): order / batch_of as hc_form_minibatches
+int ref_form_minibatches(int n, const char* const* ids, const long* act, const long* kv, long act_max, long kv_max,
+                         const double* b5, int tpb, int* order, int* batch_of, int* n_batches) {
+    return guarded([&] {
+        std::vector<RequestBlocks> reqs;
+        for (int i = 0; i < n; ++i) reqs.push_back(RequestBlocks{ids[i], act[i], kv[i]});
+        const auto mbs = form_minibatches(reqs, PackerConfig{act_max, kv_max}, bundle_of(b5), tpb);
+        int k = 0;
+        for (size_t m = 0; m < mbs.size(); ++m)
+            for (const std::string& id : mbs[m].ids) {
+                int i = 0;
+                while (reqs[i].id != id) ++i;
+                order[k++] = i;
+                batch_of[i] = static_cast<int>(m);
+            }
+        *n_batches = static_cast<int>(mbs.size());
     });
 }
 

@@ -64,6 +64,10 @@ SIGNATURES = {
     "hc_budget_for": (i, [d, cfgp, d, dp]),
     "hc_flop_count": (i, [i, cfgp, l, i, dp]),
     "hc_weight_bytes": (i, [cfgp, u64p]),
+    # mini-batch packer
+    "hc_form_minibatches": (i, [i, cpp, lp, lp, l, l, dp, i, ip, ip, ip]),
+    "hc_cost_fb": (i, [l, l, dp, i, dp]),
+    "hc_default_packer": (i, [d, cfgp, lp]),
     # engine
     "hc_engine_create": (i, [cfgp, u64, i, i, optp, vpp]),
     "hc_engine_create_from_f64": (i, [cfgp, i, dp, dp, C.POINTER(dp), optp, vpp]),

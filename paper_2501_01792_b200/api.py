@@ -354,6 +354,51 @@ def planned_t_computation(bundle: TimingBundle, tpb: int, a: HostAllocation, act
     return float(out[1])
 
 
+@dataclass
+class MiniBatch:
+    ids: List[str]
+    act_mb: int = 0
+    kv_mb: int = 0
+
+
+def form_minibatches(requests: Sequence[Tuple[str, int, int]], act_max: int, kv_max: int, bundle: TimingBundle,
+                     tpb: int) -> List[MiniBatch]:
+    """form_minibatches (minibatch.cpp:36-83): requests = [(id, act_blocks, kv_blocks)]."""
+    n = len(requests)
+    ids = (C.c_char_p * max(n, 1))(*[r[0].encode() for r in requests])
+    act = (C.c_long * max(n, 1))(*[r[1] for r in requests])
+    kv = (C.c_long * max(n, 1))(*[r[2] for r in requests])
+    order = (C.c_int * max(n, 1))()
+    bof = (C.c_int * max(n, 1))()
+    nb = C.c_int()
+    b, bp = bundle.arr5()
+    check(lib().hc_form_minibatches(n, ids, act, kv, act_max, kv_max, bp, tpb, order, bof, C.byref(nb)))
+    out = [MiniBatch([]) for _ in range(nb.value)]
+    for k in range(n):
+        i = order[k]
+        mb = out[bof[i]]
+        mb.ids.append(requests[i][0])
+        mb.act_mb += requests[i][1]
+        mb.kv_mb += requests[i][2]
+    return out
+
+
+def cost_fb(act_mb: int, kv_mb: int, bundle: TimingBundle, tpb: int) -> Tuple[float, float]:
+    """(balance, F_b) of minibatch.cpp:10-23."""
+    b, bp = bundle.arr5()
+    out, op = _darr(np.zeros(2))
+    check(lib().hc_cost_fb(act_mb, kv_mb, bp, tpb, op))
+    return float(out[0]), float(out[1])
+
+
+def default_packer(gpu_mem_bytes: float, cfg: ModelConfig) -> Tuple[int, int]:
+    """default_packer (sim.cpp:122-132) -> (act_max, kv_max)."""
+    out = (C.c_long * 2)()
+    c = cfg.to_c()
+    check(lib().hc_default_packer(gpu_mem_bytes, C.byref(c), out))
+    return out[0], out[1]
+
+
 FLOP_KINDS = {"kv_gen": 0, "qkv_gen": 1, "attention": 2, "proj_ffn": 3, "token_recompute": 4, "full_layer": 5}
 
 

@@ -2,11 +2,13 @@
 // (include/hybridcache.h). Pure forwarding onto the C++ host API.
 #include <cstring>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "capi_util.hpp"
 #include "engine.hpp"
 #include "host/cache.hpp"
+#include "host/minibatch.hpp"
 #include "host/model.hpp"
 #include "host/plan.hpp"
 #include "hybridcache.h"
@@ -300,6 +302,40 @@ int hc_weight_bytes(const hc_model_config* cfg, uint64_t* out2) {
         const WeightBytes w = weight_bytes(c);
         out2[0] = w.per_layer;
         out2[1] = w.total;
+    });
+}
+
+// ---- mini-batch packer ----------------------------------------------------
+int hc_form_minibatches(int n, const char* const* ids, const long* act_blocks, const long* kv_blocks, long act_max,
+                        long kv_max, const double* b5, int tpb, int* order, int* batch_of, int* n_batches) {
+    return hc_guard([&] {
+        std::vector<RequestBlocks> reqs;
+        for (int i = 0; i < n; ++i) reqs.push_back(RequestBlocks{sid(ids[i]), act_blocks[i], kv_blocks[i]});
+        const auto mbs = form_minibatches(reqs, PackerConfig{act_max, kv_max}, bundle_of(b5), tpb);
+        std::unordered_map<std::string, int> pos;
+        for (int i = 0; i < n; ++i) pos[reqs[i].id] = i;
+        int k = 0;
+        for (size_t m = 0; m < mbs.size(); ++m)
+            for (const std::string& id : mbs[m].ids) {
+                order[k++] = pos.at(id);
+                batch_of[pos.at(id)] = static_cast<int>(m);
+            }
+        *n_batches = static_cast<int>(mbs.size());
+    });
+}
+int hc_cost_fb(long act_mb, long kv_mb, const double* b5, int tpb, double* out2) {
+    return hc_guard([&] {
+        out2[0] = balance(act_mb, kv_mb, bundle_of(b5), tpb);
+        out2[1] = cost_fb(act_mb, kv_mb, bundle_of(b5), tpb);
+    });
+}
+int hc_default_packer(double gpu_mem_bytes, const hc_model_config* cfg, long* out2) {
+    return hc_guard([&] {
+        ModelConfig c = to_cfg(cfg);
+        c.validate();
+        const PackerConfig p = default_packer(gpu_mem_bytes, c);
+        out2[0] = p.act_max;
+        out2[1] = p.kv_max;
     });
 }
 
