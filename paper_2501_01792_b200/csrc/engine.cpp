@@ -321,7 +321,6 @@ void Engine::configure_cache(const PoolCaps& caps, bool kv_on_gpu, CacheMode mod
         *p = nullptr;
     }
     assigner_.reset();
-    cache_.reset();
     opt_.kv_host_cap = caps.kv_host;
     opt_.kv_gpu_cap = caps.kv_gpu;
     opt_.act_host_cap = caps.act_host;
@@ -335,7 +334,11 @@ void Engine::configure_cache(const PoolCaps& caps, bool kv_on_gpu, CacheMode mod
     m.act_host_cap = caps.act_host;
     m.act_gpu_cap = caps.act_gpu;
     m.Lp = host_layers > 0 ? std::min(host_layers, m.L) : m.L;
-    cache_ = std::make_unique<HybridCache>(m.tpb, caps, kv_on_gpu);
+    // rebuilt IN PLACE: borrowed handles (hc_engine_cache) stay valid
+    if (cache_)
+        *cache_ = HybridCache(m.tpb, caps, kv_on_gpu);
+    else
+        cache_ = std::make_unique<HybridCache>(m.tpb, caps, kv_on_gpu);
     // token recompute keeps a block-aligned PREFIX of every prompt as ids only
     // (exact recompute needs a prefix) and caches the rest as KV
     token_mode_ = mode == CacheMode::TokenRecompute;

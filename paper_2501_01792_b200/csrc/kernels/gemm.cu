@@ -65,6 +65,22 @@ void launch(const GemmCall& c, const gemm::Params& p, cudaStream_t st) {
     kern<<<grid, gemm::kThreads, Cf::kSmemBytes, st>>>(ta, tb, p);
 }
 
+template <int EPI>
+void launch_pair(const GemmCall& c, const gemm::Params& p, cudaStream_t st) {
+    using Cf = gemm::Cfg2;
+    auto kern = gemm::gemm2_tn_kernel<EPI>;
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::kSmemBytes);
+        attr_set = true;
+    }
+    const CUtensorMap ta = make_map(c.A, c.a_rows, c.K, c.lda, gemm::BM);
+    const CUtensorMap tb = make_map(c.B, c.N, c.K, c.ldb, Cf::BN / 2);
+    const int tiles = ((p.num_m_tiles + 1) / 2) * p.num_n_tiles;
+    const int pairs = std::min(tiles, num_sms() / 2);
+    kern<<<2 * pairs, gemm::kThreads, Cf::kSmemBytes, st>>>(ta, tb, p);
+}
+
 template <int BN>
 void dispatch_epi(const GemmCall& c, const gemm::Params& p, cudaStream_t st) {
     switch (c.epi) {
@@ -180,6 +196,21 @@ void run_gemm(const GemmCall& c, cudaStream_t st) {
             p.out = c.ws;
             p.ldc = c.N;
             cc.epi = gemm::kSplitF32;
+        }
+    }
+    // large M: CTA-pair (cta_group::2) 256x256 tiles
+    static const bool pair_ok = [] {
+        const char* e = std::getenv("HC_GEMM_PAIR");
+        return !(e && e[0] == '0');
+    }();
+    if (pair_ok && p.splits == 1 && !c.bn && p.num_m_tiles >= 8 && cc.epi != gemm::kSplitF32) {
+        p.num_n_tiles = (c.N + gemm::Cfg2::BN - 1) / gemm::Cfg2::BN;
+        p.group_m = std::max(1, p.group_m / 2);
+        switch (cc.epi) {
+            case gemm::kStore: launch_pair<gemm::kStore>(cc, p, st); return;
+            case gemm::kRelu: launch_pair<gemm::kRelu>(cc, p, st); return;
+            case gemm::kKvPaged: launch_pair<gemm::kKvPaged>(cc, p, st); return;
+            case gemm::kF32: launch_pair<gemm::kF32>(cc, p, st); return;
         }
     }
     p.num_n_tiles = (c.N + bn - 1) / bn;

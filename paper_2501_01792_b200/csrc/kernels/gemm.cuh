@@ -252,4 +252,178 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
 }
 
+// ---------------------------------------------------------------------------
+// CTA-pair variant (cta_group::2) for large M: a 2-CTA cluster computes a
+// 256 x 256 tile with one UMMA M=256 stream issued by the leader CTA. Each CTA
+// TMA-loads its own 128 rows of A and 128 rows (N) of B per stage, so the
+// smem/L2 traffic per MAC drops by a third vs the 1-SM 128 x 256 tile — the
+// large-M GEMMs (ACT recompute, prefill) are L2-feed bound otherwise.
+// M tiles are counted in 128-row units (m_tile_rows lists pair up
+// consecutively; an odd tail repeats the last tile, writing identical values).
+struct Cfg2 {
+    static constexpr int BN = 256;
+    static constexpr int kABytes = BM * BK * 2;          // 128 rows of A per CTA
+    static constexpr int kBBytes = (BN / 2) * BK * 2;    // 128 rows of B per CTA
+    static constexpr int kStageBytes = kABytes + kBBytes;
+    static constexpr int kStages = 6;
+    static constexpr int kTmemCols = 512;                // 2 x 256 accumulator columns
+    static constexpr int kBarBytes = (2 * kStages + 4) * 8 + 16;
+    static constexpr int kSmemBytes = kStages * kStageBytes + kBarBytes + 1024;
+};
+
+__device__ __forceinline__ void pair_tile_coords(int tile, int num_pm, int num_n, int group, int& pm, int& ni) {
+    const int G = num_pm < group ? num_pm : group;
+    const int per = G * num_n;
+    const int g = tile / per;
+    const int first = g * G;
+    const int gm = (num_pm - first) < G ? (num_pm - first) : G;
+    const int within = tile - g * per;
+    pm = first + within % gm;
+    ni = within / gm;
+}
+
+template <int EPI>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    gemm2_tn_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                    const Params p) {
+    using C = Cfg2;
+    constexpr int S = C::kStages;
+    constexpr int BN = C::BN;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* smem_a = smem;
+    uint8_t* smem_b = smem + S * C::kABytes;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S * C::kStageBytes);
+    uint64_t* full = bars;
+    uint64_t* empty = bars + S;
+    uint64_t* tfull = bars + 2 * S;
+    uint64_t* tempty = bars + 2 * S + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * S + 4);
+
+    const int warp = threadIdx.x / 32;
+    const int lane = threadIdx.x % 32;
+    const uint32_t rank = ptx::cluster_ctarank();
+    const int pair = blockIdx.x / 2;
+    const int num_pairs = gridDim.x / 2;
+
+    if (warp == 0 && lane == 0) {
+        ptx::tma_prefetch(&tmA);
+        ptx::tma_prefetch(&tmB);
+        for (int s = 0; s < S; ++s) {
+            ptx::mbar_init(&full[s], 1);
+            ptx::mbar_init(&empty[s], 1);
+        }
+        for (int s = 0; s < 2; ++s) {
+            ptx::mbar_init(&tfull[s], 1);
+            ptx::mbar_init(&tempty[s], 256);  // both CTAs' epilogues arrive on the leader's
+        }
+        ptx::fence_mbar_init();
+    }
+    if (warp == 1) ptx::tmem_alloc_pair<C::kTmemCols>(tmem_slot);
+    ptx::tc_fence_before();
+    ptx::cluster_sync();
+    ptx::tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    const int num_pm = (p.num_m_tiles + 1) / 2;
+    const int num_tiles = num_pm * p.num_n_tiles;
+    const int num_kb = (p.K + BK - 1) / BK;
+    auto m_row_of = [&](int pm, uint32_t r) {
+        int t = 2 * pm + static_cast<int>(r);
+        if (p.m_tile_rows) {
+            if (t >= p.num_m_tiles) t = p.num_m_tiles - 1;
+            return p.m_tile_rows[t];
+        }
+        return t * BM;
+    };
+
+    if (warp == 0) {
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int tile = pair; tile < num_tiles; tile += num_pairs) {
+                int pm, ni;
+                pair_tile_coords(tile, num_pm, p.num_n_tiles, p.group_m, pm, ni);
+                const int m_row = m_row_of(pm, rank);
+                const int n_row = ni * BN + static_cast<int>(rank) * (BN / 2);
+                for (int kb = 0; kb < num_kb; ++kb) {
+                    ptx::mbar_wait(&empty[stage], phase ^ 1);
+                    if (rank == 0) ptx::mbar_arrive_expect_tx(&full[stage], 2 * C::kStageBytes);
+                    ptx::tma_load_2d_pair(smem_a + stage * C::kABytes, &tmA, &full[stage], kb * BK, m_row);
+                    ptx::tma_load_2d_pair(smem_b + stage * C::kBBytes, &tmB, &full[stage], kb * BK, n_row);
+                    if (++stage == S) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0 && rank == 0) {
+            constexpr uint32_t idesc = ptx::idesc_bf16_f32(2 * BM, BN);
+            int stage = 0;
+            uint32_t phase = 0;
+            int as = 0;
+            uint32_t aphase = 0;
+            for (int tile = pair; tile < num_tiles; tile += num_pairs) {
+                ptx::mbar_wait(&tempty[as], aphase ^ 1);
+                ptx::tc_fence_after();
+                const uint32_t d_tmem = tmem_base + as * BN;
+                for (int kb = 0; kb < num_kb; ++kb) {
+                    ptx::mbar_wait(&full[stage], phase);
+                    ptx::tc_fence_after();
+                    const uint64_t a_desc = ptx::sw128_kmajor_desc(ptx::smem_u32(smem_a + stage * C::kABytes));
+                    const uint64_t b_desc = ptx::sw128_kmajor_desc(ptx::smem_u32(smem_b + stage * C::kBBytes));
+#pragma unroll
+                    for (int k = 0; k < BK / 16; ++k)
+                        ptx::mma_bf16_ss_pair(d_tmem, a_desc + 2 * k, b_desc + 2 * k, idesc, (kb | k) != 0);
+                    ptx::mma_commit_pair_mc(&empty[stage], 0x3);
+                    if (++stage == S) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+                ptx::mma_commit_pair_mc(&tfull[as], 0x3);
+                if (++as == 2) {
+                    as = 0;
+                    aphase ^= 1;
+                }
+            }
+        }
+    } else {
+        const int q = warp % 4;
+        int as = 0;
+        uint32_t aphase = 0;
+        for (int tile = pair; tile < num_tiles; tile += num_pairs) {
+            int pm, ni;
+            pair_tile_coords(tile, num_pm, p.num_n_tiles, p.group_m, pm, ni);
+            const int row = m_row_of(pm, rank) + q * 32 + lane;
+            const int n0 = ni * BN;
+            ptx::mbar_wait(&tfull[as], aphase);
+            ptx::tc_fence_after();
+            const uint32_t t_row = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + as * BN;
+#pragma unroll 1
+            for (int c = 0; c < BN; c += 16) {
+                uint32_t v[16];
+                ptx::tmem_ld_x16(t_row + c, v);
+                ptx::tmem_ld_wait();
+                epilogue_chunk<BN, EPI>(p, row, n0 + c, 0, v);
+            }
+            ptx::tc_fence_before();
+            ptx::mbar_arrive_cluster(&tempty[as], 0);
+            if (++as == 2) {
+                as = 0;
+                aphase ^= 1;
+            }
+        }
+    }
+
+    __syncthreads();
+    ptx::cluster_sync();
+    if (warp == 1) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc_pair<C::kTmemCols>(tmem_base);
+    }
+}
+
 }  // namespace hc::gemm

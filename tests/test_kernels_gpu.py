@@ -158,6 +158,39 @@ def test_prefill_attention_causal(native, n_req, P, H, hd):
         assert rel(got[sl], want) <= TOL_BF16
 
 
+@pytest.mark.parametrize("M,N,K", [(1024, 512, 512), (1100, 768, 320), (2560, 1024, 1024), (4096, 256, 7168 // 4)])
+@pytest.mark.parametrize("epi", [0, 1, 3])
+def test_gemm_cta_pair(native, M, N, K, epi):
+    """Large-M GEMMs run on the CTA-pair (cta_group::2, 256x256) kernel."""
+    from paper_2501_01792_b200.kernels import gemm_bf16
+    rng = np.random.default_rng(M + N + epi)
+    a = rand_bits(rng, (M, K))
+    wt = rand_bits(rng, (N, K), 1.0 / np.sqrt(K))
+    ref = f64(a) @ f64(wt).T
+    if epi == 1:
+        ref = np.maximum(ref, 0)
+    got = gemm_bf16(a, wt, epi, 0).astype(np.float64) if epi == 3 else f64(gemm_bf16(a, wt, epi, 0))
+    assert rel(got, ref) <= (1e-4 if epi == 3 else TOL_BF16)
+
+
+@pytest.mark.parametrize("nb,tpb,d,heads", [(100, 16, 512, 4), (129, 16, 1024, 8), (64, 8, 256, 2)])
+def test_recompute_kv_paged_cta_pair(native, nb, tpb, d, heads):
+    """Paged recompute on the pair kernel, odd tile counts (tail tile repeated)."""
+    from paper_2501_01792_b200.kernels import recompute_kv_paged
+    rng = np.random.default_rng(nb + d)
+    act = rand_bits(rng, (nb, tpb, d))
+    wkv_t = rand_bits(rng, (2 * d, d), 1.0 / np.sqrt(d))
+    rows = nb * tpb
+    tiles = np.arange(0, rows, 128, dtype=np.int32)
+    got = f64(recompute_kv_paged(act, wkv_t, heads, tiles))
+    a = f64(act).reshape(rows, d)
+    kv = a @ f64(wkv_t).T
+    hd = d // heads
+    ref = np.stack([kv[:, :d].reshape(nb, tpb, heads, hd).transpose(0, 2, 1, 3),
+                    kv[:, d:].reshape(nb, tpb, heads, hd).transpose(0, 2, 1, 3)], axis=1)
+    assert rel(got, ref) <= TOL_BF16
+
+
 @pytest.mark.parametrize("M,N,K,bn,splits,epi", [
     (128, 512, 2048, 128, 4, 0), (64, 768, 3072, 64, 3, 1), (100, 1024, 4096, 256, 8, 0), (128, 256, 448, 128, 2, 1),
     (128, 384, 1000, 64, 5, 0),

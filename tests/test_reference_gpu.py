@@ -146,16 +146,18 @@ def test_equivalence_seeded_models(seed):
     ids = [rng.uniform_int(0, 63) for _ in range(P)]
     tok = rng.uniform_int(0, 63)
     eng = api.Engine(cfg, seed=wseed, max_seq=P + 2, max_batch=1)
-    outs = {}
+    outs, stats = {}, {}
     for mode, alloc in (("kv_only", None), ("act_only", None), ("hybrid", api.HostAllocation(1, 1))):
         eng.configure_cache(api.PoolCaps(kv_host=8, act_host=8, act_gpu=2), mode=mode, allocation=alloc)
         eng.prefill(["q"], [ids])
+        eng.set_profile(True)
         outs[mode] = f64(eng.decode_step(["q"], [tok])["x"])
+        stats[mode] = (eng.last_stats(), eng.cache.dump_json())
     ocfg = O.ModelConfig(num_layers=L, hidden_dim=d, num_heads=H, ffn_dim=2 * d, vocab_size=64).validate()
     w = O.prepare_weights(O.generate_weights(ocfg, wseed, P + 2))
     ref = O.forward_prompt(ids + [tok], w).output[-1:]
     for m, o in outs.items():
-        assert rel(o, ref) <= TOL, m
+        assert rel(o, ref) <= TOL, (m, stats[m], (L, H, d, tpb, P))
     assert rel(outs["act_only"], outs["kv_only"]) <= TOL
     assert rel(outs["hybrid"], outs["kv_only"]) <= TOL
 
