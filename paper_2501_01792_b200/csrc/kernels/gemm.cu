@@ -203,9 +203,14 @@ void run_gemm(const GemmCall& c, cudaStream_t st) {
         const char* e = std::getenv("HC_GEMM_PAIR");
         return !(e && e[0] == '0');
     }();
-    if (pair_ok && p.splits == 1 && !c.bn && p.num_m_tiles >= 8 && cc.epi != gemm::kSplitF32) {
+    // Measured on B200 (profiles/r01_gemm_pair.txt): the pair kernel reaches
+    // 99.7 % tensor-pipe activity but, under the 1 kW cap, its extra DRAM
+    // traffic at K = 7168 costs clock (1.17 vs 1.36 GHz in situ), so it only
+    // wins for K <= 4096 (OPT-6.7B recompute: +10 % in situ).
+    if (pair_ok && p.splits == 1 && !c.bn && p.num_m_tiles >= 8 && c.K <= 4096 && cc.epi != gemm::kSplitF32) {
         p.num_n_tiles = (c.N + gemm::Cfg2::BN - 1) / gemm::Cfg2::BN;
-        p.group_m = std::max(1, p.group_m / 2);
+        p.group_m = c.group_m > 0 ? std::max(1, c.group_m / 2) : 8;
+        if (const char* g = std::getenv("HC_GEMM_GROUP_M")) p.group_m = std::max(1, std::atoi(g) / 2);
         switch (cc.epi) {
             case gemm::kStore: launch_pair<gemm::kStore>(cc, p, st); return;
             case gemm::kRelu: launch_pair<gemm::kRelu>(cc, p, st); return;
