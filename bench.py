@@ -39,15 +39,23 @@ def parse():
     p.add_argument("--steps", type=int, default=5)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    p.add_argument("--model", default="opt-30b")
-    p.add_argument("--batch", type=int, default=128, help="requests per GPU")
+    p.add_argument("--config", type=int, default=3, choices=[3, 4],
+                   help="BASELINE configs[] entry (1-based): 3 = OPT-30B, 128 requests per GPU (weak scaling); "
+                        "4 = OPT-66B fully offloaded, global batch 128 split across the ranks (strong scaling), "
+                        "planner-chosen ratio")
+    p.add_argument("--model", default="")
+    p.add_argument("--batch", type=int, default=0, help="requests per GPU (config 3 default 128)")
+    p.add_argument("--global-batch", type=int, default=0, help="total requests split across ranks (config 4: 128)")
     p.add_argument("--prompt", type=int, default=1024)
     p.add_argument("--gen", type=int, default=256, help="generation length of the workload (config)")
-    p.add_argument("--ratio", type=float, default=1.0 / 3.0,
+    p.add_argument("--ratio", type=float, default=None,
                    help="ACT share r of context blocks (default 1/3 = the paper's KV:ACT 2:1 for OPT-30B, "
                         "PAPER.md:714); -1 = the planner's choice from measured rates")
     p.add_argument("--host-gb", type=float, default=0.0, help="pinned host budget per rank (0: auto)")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--prefill", default="real", choices=["real", "synthetic"],
+                   help="build the decode cache by the real prefill of synthetic prompts (default) or by "
+                        "pattern-filled bookkeeping-only admission")
     p.add_argument("--layers", type=int, default=0, help="override num_layers (smoke/profiling only)")
     p.add_argument("--no-sweep", action="store_true", help="skip the per-ratio / planner / HBM-tier variants")
     p.add_argument("--sweep", default="0,0.3333333333333333,0.5,1,tr0.5",
@@ -55,7 +63,24 @@ def parse():
     p.add_argument("--no-config2", action="store_true", help="skip the OPT-6.7B resident (config 2) variant")
     p.add_argument("--artifacts", default="", help="write the reference CLI's artifacts (kv_gen.csv, load_kv.csv, "
                                                     "bundle.json, plan.json, metrics.json, trace.json) here")
-    return p.parse_args()
+    a = p.parse_args()
+    if a.config == 4:
+        a.model = a.model or "opt-66b"
+        a.global_batch = a.global_batch or 128
+        a.ratio = -1.0 if a.ratio is None else a.ratio
+    a.model = a.model or "opt-30b"
+    a.ratio = 1.0 / 3.0 if a.ratio is None else a.ratio
+    a.scaling = "strong" if a.global_batch else "weak"
+    return a
+
+
+def per_rank_batch(args, world, rank):
+    """Requests this rank owns: --batch per GPU (weak scaling), or an even
+    split of --global-batch (strong scaling)."""
+    if args.global_batch:
+        base, extra = divmod(args.global_batch, world)
+        return base + (1 if rank < extra else 0)
+    return args.batch or 128
 
 
 # ---------------------------------------------------------------- helpers ---
@@ -244,7 +269,7 @@ def reference_arm(args, cfg, world, rank, dist):
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": v, "unit": "tokens/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "scaling": args.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": workload_config(args, cfg, world),
         "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": threads, "kind": kind, "sample": sample},
         "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -252,9 +277,13 @@ def reference_arm(args, cfg, world, rank, dist):
 
 
 def workload_config(args, cfg, world, extra=None):
-    c = {"workload": f"{cfg.name}-shape offloaded decode (weights + hybrid KV/ACT cache in pinned host memory), "
-                     f"batch {args.batch}/GPU, prompt {args.prompt}, gen {args.gen}",
-         "model": cfg.name, "global_batch": args.batch * world, "seq_len": args.prompt, "gen_len": args.gen,
+    B = per_rank_batch(args, world, 0)
+    gb = args.global_batch or B * world
+    c = {"workload": f"BASELINE configs[{args.config - 1}]: {cfg.name}-shape offloaded decode (weights + hybrid KV/ACT "
+                     f"cache in pinned host memory), " +
+                     (f"global batch {gb} split over {world} GPU(s)" if args.global_batch else f"batch {B}/GPU") +
+                     f", prompt {args.prompt}, gen {args.gen}",
+         "model": cfg.name, "global_batch": gb, "batch_per_gpu": B, "seq_len": args.prompt, "gen_len": args.gen,
          "act_share_r": round(extra.get("act_share_r", args.ratio), 4) if extra else round(args.ratio, 4),
          "parallelism": f"batch-partitioned x{world} (no collective)",
          "l2": "inputs larger than L2 (~100+ GB streamed host->HBM per step)"}
@@ -393,6 +422,37 @@ def write_artifacts(out_dir, eng, cfg, ids, planner, prof, mode, r):
         json.dump(tr, fh, default=_np_default)
 
 
+def run_prefill(eng, cfg, ids, P, rank, tflops_sust, link_gbs):
+    """Offloaded prefill of len(ids) random prompts of P tokens (one profiled
+    call): time, tensor FLOPs (flops.cpp:16-22: QKV + causal attention +
+    proj/FFN per layer), bytes streamed in (weights) and stored out (blocks)."""
+    import torch
+    d, f, L, H = cfg.hidden_dim, cfg.ffn_dim, cfg.num_layers, cfg.num_heads
+    rng = np.random.default_rng(100 + rank)
+    prompts = [rng.integers(0, cfg.vocab_size, P).tolist() for _ in ids]
+    torch.cuda.synchronize()
+    eng.set_profile(True)
+    w0 = time.perf_counter()
+    eng.prefill(ids, prompts)
+    wall = time.perf_counter() - w0
+    eng.set_profile(False)
+    st = eng.last_stats()
+    n = len(ids)
+    gemm_flops = L * 2.0 * n * P * (4 * d * d + 2 * d * f)
+    attn_flops = L * n * 2.0 * d * P * (P + 1)  # attention_causal FLOPs (flops.cpp:19)
+    s = st["step_ms"] / 1e3
+    return {"requests": n, "prompt": P, "prefill_s": s, "wall_s": wall, "prompt_tokens_per_s": n * P / s,
+            "gemm_tflops": gemm_flops / (st["gemm_ms"] / 1e3) / 1e12 if st["gemm_ms"] else None,
+            "attention_tflops": attn_flops / (st["attn_ms"] / 1e3) / 1e12 if st["attn_ms"] else None,
+            "split_ms": {"qkv_proj_ffn_gemms": st["gemm_ms"], "causal_attention": st["attn_ms"],
+                         "weight_h2d_stream": st["copy_ms"], "block_d2h_stream": st["store_ms"]},
+            "h2d_gb": st["h2d_bytes"] / 1e9, "d2h_gb": st["d2h_bytes"] / 1e9,
+            "d2h_gbs": st["d2h_bytes"] / (st["store_ms"] / 1e3) / 1e9 if st["store_ms"] else None,
+            "tensor_roofline_s": (gemm_flops + attn_flops) / (tflops_sust * 1e12),
+            "link_roofline_s": max(st["h2d_bytes"], st["d2h_bytes"]) / (link_gbs * 1e9) if link_gbs else None,
+            "launches": int(st["launches"])}
+
+
 def calibrate_planner(eng, cfg, link_gbs, caps_act_rows, host_mem, act_gpu=0):
     """North-star (5): measured recompute-GEMM and host-link samples ->
     bundle_from_samples (timing.cpp:172-183) -> plan_host_allocation
@@ -422,7 +482,7 @@ def our_arm(args, cfg, world, rank, local, dist):
     if kernels.device_count() == 0:
         raise SystemExit("bench needs a CUDA device")
     hbm_peak, tflops_sust, tflops_burst, peak_src = measured_peaks()
-    B, P, L, d = args.batch, args.prompt, cfg.num_layers, cfg.hidden_dim
+    B, P, L, d = per_rank_batch(args, world, rank), args.prompt, cfg.num_layers, cfg.hidden_dim
     total_steps = args.warmup + args.steps + 2
     max_seq = P + total_steps + 1
     r = args.ratio if args.ratio >= 0 else 1.0 / 3.0  # planner replaces the default below
@@ -438,7 +498,6 @@ def our_arm(args, cfg, world, rank, local, dist):
     eng = api.Engine(cfg, seed=42, max_seq=max_seq, rescale=True, max_batch=B, weights_on_device=False,
                      caps=caps, host_layers=Lp, weight_layers=Lw, mode=mode, allocation=alloc, device=local)
     ids = [f"g{rank}r{i}" for i in range(B)]
-    eng.admit_synthetic(ids, [P] * B, seed=1 + rank)
     # host-link peak: a large pinned H2D copy on the engine's copy stream
     tpb = cfg.tokens_per_block
     n_tok = min(caps.kv_host * tpb, 65536) if caps.kv_host else 0
@@ -455,8 +514,13 @@ def our_arm(args, cfg, world, rank, local, dist):
         mode, alloc, caps = pool_plan(cfg, B, P, total_steps, r)
         Lp = host_layers_for(cfg, caps, budget, Lw * w_layer)
         eng.configure_cache(caps, mode=mode, allocation=alloc, host_layers=Lp)
-        eng.admit_synthetic(ids, [P] * B, seed=1 + rank)
     setup_s = time.time() - t_setup
+    # the cache the decode steps read is built by the real offloaded prefill
+    # of B synthetic prompts (weights streamed once per layer, host blocks
+    # stored by D2H runs) — measured, and reported as its own stage
+    prefill = run_prefill(eng, cfg, ids, P, rank, tflops_sust, link_gbs) if args.prefill == "real" else None
+    if prefill is None:
+        eng.admit_synthetic(ids, [P] * B, seed=1 + rank)
 
     rng = np.random.default_rng(rank)
     tokens = rng.integers(0, cfg.vocab_size, (total_steps, B)).astype(np.int32)
@@ -516,6 +580,23 @@ def our_arm(args, cfg, world, rank, local, dist):
                  "profile_split_ms": {"recompute": prof["recompute_ms"], "attention": prof["attn_ms"],
                                       "qkv_proj_ffn": prof["gemm_ms"], "copy_stream": prof["copy_ms"]}}
 
+    # whole-generation throughput (prefill + G decode steps, the paper's and
+    # the sim's definition, sim.cpp:618-628): prefill measured above; decode
+    # steps at context P+g projected from the measured step by streamed bytes
+    # (the step is link-bound: step_roofline.bound == "link")
+    gen = None
+    if prefill is not None:
+        w_all = L * w_layer
+        cache0 = max(h2d_step - w_all, 0.0)
+        ctx0 = P + args.warmup + 1 + (args.steps - 1) / 2.0
+        dec_s = sum(ms_per_step / 1e3 * (w_all + cache0 * (P + g) / ctx0) / h2d_step for g in range(args.gen))
+        gen = {"prefill_s": prefill["prefill_s"], "decode_s_projected": dec_s, "gen_len": args.gen,
+               "tokens_per_s": B * args.gen / (prefill["prefill_s"] + dec_s),
+               "tokens_per_s_all_ranks": B * args.gen * world / (prefill["prefill_s"] + dec_s),
+               "prefill_share": prefill["prefill_s"] / (prefill["prefill_s"] + dec_s),
+               "method": "prefill measured; decode step(P+g) = measured step x streamed bytes(P+g)/bytes(P) "
+                         "(link-bound), summed over the gen length"}
+
     # ---- per-ratio sweep, planner, HBM-tiered variant (untimed by the contract)
     extra = {}
     if not args.no_sweep and world == 1:
@@ -572,9 +653,11 @@ def our_arm(args, cfg, world, rank, local, dist):
             cpu = {"value": 1.0 / (L * t), "unit": "tokens/s", "cores": threads, "kind": kind, "sample": sample}
         res = {
             "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": args.scaling,
             "vs_baseline": None, "dtype": "bf16",
-            "data": "synthetic (reference-draw weights rescaled, pattern-filled cache at prompt length)",
+            "data": ("synthetic (reference-draw weights rescaled; random prompts, cache built by the real offloaded "
+                     "prefill)" if prefill else "synthetic (reference-draw weights rescaled, pattern-filled cache "
+                                                "at prompt length)"),
             "config": workload_config(args, cfg, world, {
                 "act_share_r": r,
                 "kv_act_ratio": (f"{(1 - r) / r:.3f}:1" if 0 < r < 1 else ("kv_only" if r <= 0 else "act_only")),
@@ -597,11 +680,13 @@ def our_arm(args, cfg, world, rank, local, dist):
             "clocks": clk,
             "setup_s": setup_s,
             "planner": planner,
+            "prefill": prefill,
+            "generation_e2e_projected": gen,
         }
         res.update(extra)
     eng.close()
     if rank == 0:
-        if not args.no_sweep and not args.no_config2 and world == 1:
+        if not args.no_sweep and not args.no_config2 and world == 1 and args.config == 3:
             try:
                 res["config2_resident"] = config2_resident(local)
             except Exception as e:

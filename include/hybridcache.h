@@ -172,9 +172,10 @@ int hc_engine_read_weights(void* engine, int layer, uint16_t* out);
 int hc_engine_capture_inputs(void* engine, int on);
 /* Decode-time layer inputs of the last step, [L][n][d] bf16 (n = last batch). */
 int hc_engine_captured_inputs(void* engine, uint16_t* out, long count);
-/* out10 = {step_ms, h2d_bytes, d2h_bytes, recompute_rows, recompute_ms, attn_ms, gemm_ms, launches,
- *          copy_ms, recompute_launches}; the *_ms splits need hc_engine_set_profile(1). */
-int hc_engine_last_stats(void* engine, double* out10);
+/* out11 = {step_ms, h2d_bytes, d2h_bytes, recompute_rows, recompute_ms, attn_ms, gemm_ms, launches,
+ *          copy_ms, recompute_launches, store_ms} of the last decode step or prefill; the *_ms
+ *          splits need hc_engine_set_profile(1). */
+int hc_engine_last_stats(void* engine, double* out11);
 /* Per-kernel CUDA-event timing of the next steps (small overhead). */
 int hc_engine_set_profile(void* engine, int on);
 /* Events of the last profiled step in the reference's trace.json schema

@@ -592,10 +592,10 @@ class Engine:
         return out
 
     def last_stats(self) -> dict:
-        out, op = _darr(np.zeros(10))
+        out, op = _darr(np.zeros(11))
         check(lib().hc_engine_last_stats(self._h, op))
         keys = ("step_ms", "h2d_bytes", "d2h_bytes", "recompute_rows", "recompute_ms", "attn_ms", "gemm_ms",
-                "launches", "copy_ms", "recompute_launches")
+                "launches", "copy_ms", "recompute_launches", "store_ms")
         return dict(zip(keys, out.tolist()))
 
     def set_profile(self, on: bool = True) -> None:

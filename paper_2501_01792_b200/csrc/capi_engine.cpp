@@ -415,9 +415,9 @@ int hc_engine_captured_inputs(void* e, uint16_t* out, long count) {
 int hc_engine_last_stats(void* e, double* o) {
     return hc_guard([&] {
         const StepStats& s = eng(e)->last_stats();
-        const double v[10] = {s.step_ms, s.h2d_bytes, s.d2h_bytes, s.recompute_tokens, s.recompute_ms,
+        const double v[11] = {s.step_ms, s.h2d_bytes, s.d2h_bytes, s.recompute_tokens, s.recompute_ms,
                               s.attn_ms, s.gemm_ms, static_cast<double>(s.launches), s.copy_ms,
-                              static_cast<double>(s.recompute_launches)};
+                              static_cast<double>(s.recompute_launches), s.store_ms};
         std::memcpy(o, v, sizeof v);
     });
 }

@@ -100,8 +100,8 @@ struct Engine::Impl {
     size_t meta_cap = 0;
     // prefill scratch
     bf16 *px[2] = {nullptr, nullptr}, *pqkv = nullptr, *patt = nullptr, *pproj = nullptr, *ph = nullptr;
-    size_t prefill_rows = 0;
-    cudaEvent_t loaded[2]{}, consumed[2]{}, ev0{}, ev1{};
+    size_t prefill_rows = 0, prefill_chunk_rows = 0;
+    cudaEvent_t loaded[2]{}, consumed[2]{}, stored[2]{}, ev0{}, ev1{};
     bool pools_filled = false;
     bf16* tr_kv = nullptr;  // [max_batch * max_blocks] KV blocks for token-recompute prefixes
     void ensure_tr() {
@@ -163,17 +163,26 @@ struct Engine::Impl {
         attn_work_elems = elems;
         attn_work = dalloc<float>(elems);
     }
-    void ensure_prefill(size_t rows) {
-        if (rows <= prefill_rows) return;
-        for (bf16* p : {px[0], px[1], pqkv, patt, pproj, ph})
-            if (p) cudaFree(p);
-        prefill_rows = rows;
-        px[0] = dalloc<bf16>(rows * d);
-        px[1] = dalloc<bf16>(rows * d);
-        pqkv = dalloc<bf16>(rows * 3 * d);
-        patt = dalloc<bf16>(rows * d);
-        pproj = dalloc<bf16>(rows * d);
-        ph = dalloc<bf16>(rows * f);
+    // px: layer input/output rows of the whole prefill (all requests);
+    // pqkv/patt/pproj/ph: per-chunk scratch (chunk_rows <= rows)
+    void ensure_prefill(size_t rows, size_t chunk_rows = 0) {
+        if (!chunk_rows) chunk_rows = rows;
+        if (rows > prefill_rows) {
+            for (bf16* p : {px[0], px[1]})
+                if (p) cudaFree(p);
+            prefill_rows = rows;
+            px[0] = dalloc<bf16>(rows * d);
+            px[1] = dalloc<bf16>(rows * d);
+        }
+        if (chunk_rows > prefill_chunk_rows) {
+            for (bf16* p : {pqkv, patt, pproj, ph})
+                if (p) cudaFree(p);
+            prefill_chunk_rows = chunk_rows;
+            pqkv = dalloc<bf16>(chunk_rows * 3 * d);
+            patt = dalloc<bf16>(chunk_rows * d);
+            pproj = dalloc<bf16>(chunk_rows * d);
+            ph = dalloc<bf16>(chunk_rows * f);
+        }
     }
 };
 
@@ -260,9 +269,11 @@ void Engine::init(const ModelConfig& c, int w_max_seq, const uint16_t* emb, cons
 
     HC_CUDA(cudaStreamCreateWithFlags(&s_compute_, cudaStreamNonBlocking));
     HC_CUDA(cudaStreamCreateWithFlags(&s_copy_, cudaStreamNonBlocking));
+    HC_CUDA(cudaStreamCreateWithFlags(&s_store_, cudaStreamNonBlocking));
     for (int i = 0; i < 2; ++i) {
         HC_CUDA(cudaEventCreateWithFlags(&m.loaded[i], cudaEventDisableTiming));
         HC_CUDA(cudaEventCreateWithFlags(&m.consumed[i], cudaEventDisableTiming));
+        HC_CUDA(cudaEventCreateWithFlags(&m.stored[i], cudaEventDisableTiming));
     }
     HC_CUDA(cudaEventCreate(&m.ev0));
     HC_CUDA(cudaEventCreate(&m.ev1));
@@ -407,12 +418,14 @@ Engine::~Engine() {
     for (int i = 0; i < 2; ++i) {
         cudaEventDestroy(m.loaded[i]);
         cudaEventDestroy(m.consumed[i]);
+        cudaEventDestroy(m.stored[i]);
     }
     cudaEventDestroy(m.ev0);
     cudaEventDestroy(m.ev1);
     for (cudaEvent_t e : m.pev) cudaEventDestroy(e);
     cudaStreamDestroy(s_compute_);
     cudaStreamDestroy(s_copy_);
+    cudaStreamDestroy(s_store_);
 }
 
 // Causal forward of T rows (one sequence) through layers [l0, l1); the input
@@ -481,123 +494,209 @@ void gemm_rows(int epi, const bf16* A, int M, int K, const bf16* W, int N, void*
 void Engine::prefill(const std::vector<std::string>& ids, const std::vector<std::vector<int>>& prompts) {
     Impl& m = *impl_;
     if (ids.size() != prompts.size()) throw InputError("prefill: ids and prompts differ in length");
-    for (size_t r = 0; r < ids.size(); ++r) {
-        if (cache_->has_request(ids[r])) throw InputError("duplicate request id: " + ids[r]);
-        if (static_cast<int>(prompts[r].size()) > m.max_seq) throw InputError("embed: sequence longer than max_seq");
-        for (int t : prompts[r])
-            if (t < 0 || t >= m.V) throw InputError("embed: token id out of range: " + std::to_string(t));
+    {
+        std::unordered_set<std::string> seen;
+        for (size_t r = 0; r < ids.size(); ++r) {
+            if (cache_->has_request(ids[r]) || !seen.insert(ids[r]).second)
+                throw InputError("duplicate request id: " + ids[r]);
+            if (static_cast<int>(prompts[r].size()) > m.max_seq) throw InputError("embed: sequence longer than max_seq");
+            for (int t : prompts[r])
+                if (t < 0 || t >= m.V) throw InputError("embed: token id out of range: " + std::to_string(t));
+        }
     }
-    size_t r0 = 0;
-    while (r0 < ids.size()) {
-        // chunk of requests with <= max_prefill_tokens rows (at least one request)
-        size_t r1 = r0;
-        size_t rows = 0;
-        while (r1 < ids.size() && (r1 == r0 || rows + prompts[r1].size() <= static_cast<size_t>(opt_.max_prefill_tokens))) {
-            rows += prompts[r1].size();
-            ++r1;
+    // Offloaded prefill pipeline (forward_prompt semantics per request,
+    // decoder.cpp:144-157; one compute stage, sim.cpp:237-253):
+    //   layer-outer / request-chunk-inner, so each layer's weights cross the
+    //   host link once for the whole prefill (copy stream, double-buffered);
+    //   host-located blocks are scattered into the device staging slot of
+    //   the layer (indexed by pbn, the host pool's own layout) and leave on a
+    //   store stream as pbn-contiguous D2H runs that overlap the next layer's
+    //   compute (full duplex with the weight stream).
+    // 1. bookkeeping, prompt tokens request by request (sim.cpp:222-223);
+    //    all requests' rows laid end to end.
+    struct Chunk {
+        int row0 = 0, rows = 0, n = 0, max_len = 0;
+        std::vector<int> cu, k_src, k_n, k_ref;
+        size_t o_cu = 0, o_ks = 0, o_kn = 0, o_kr = 0;
+    };
+    std::vector<Chunk> chunks;
+    std::vector<int> tokens, positions, a_src, a_n, a_ref, acth, kvh;
+    for (size_t r = 0; r < ids.size(); ++r) {
+        const int P = static_cast<int>(prompts[r].size());
+        if (chunks.empty() || (chunks.back().rows > 0 && chunks.back().rows + P > opt_.max_prefill_tokens)) {
+            chunks.emplace_back();
+            chunks.back().row0 = static_cast<int>(tokens.size());
+            chunks.back().cu.push_back(0);
         }
-        const int n = static_cast<int>(r1 - r0);
-        // bookkeeping: blocks chosen by the ratio policy, prompt tokens
-        // request by request (sim.cpp:222-223)
-        std::vector<int> tokens, positions, cu(1, 0);
-        std::vector<int> a_src, a_n, a_ref, k_src, k_n, k_ref;
-        int max_len = 0;
-        for (size_t r = r0; r < r1; ++r) {
-            assigner_->add_request(ids[r], static_cast<int>(prompts[r].size()));
-            const int base = cu.back();
-            const int rc = rc_prefix(static_cast<int>(prompts[r].size()));
-            if (token_mode_) rc_ids_[ids[r]].assign(prompts[r].begin(), prompts[r].begin() + rc);
-            for (size_t t = 0; t < prompts[r].size(); ++t) {
-                tokens.push_back(prompts[r][t]);
-                positions.push_back(static_cast<int>(t));
-                if (static_cast<int>(t) >= rc) assigner_->add_token(ids[r]);
-            }
-            const BlockTable& tb = cache_->table(ids[r]);
-            int row = base + rc;
-            for (const auto& e : tb.entries) {
-                const bool gpu = e.location == Location::GpuMem;
-                if (e.kind == BlockKind::ACT) {
-                    a_src.push_back(row);
-                    a_n.push_back(e.filled_tokens);
-                    a_ref.push_back(pack_ref(gpu ? R_ACT_GPU : R_ACT_HOST, e.pbn));
-                } else {
-                    k_src.push_back(row);
-                    k_n.push_back(e.filled_tokens);
-                    k_ref.push_back(pack_ref(gpu ? R_KV_GPU : R_KV_HOST, e.pbn));
-                }
-                row += e.filled_tokens;
-            }
-            cu.push_back(base + static_cast<int>(prompts[r].size()));
-            max_len = std::max<int>(max_len, static_cast<int>(prompts[r].size()));
+        Chunk& c = chunks.back();
+        assigner_->add_request(ids[r], P);
+        const int base = static_cast<int>(tokens.size());
+        const int rc = rc_prefix(P);
+        if (token_mode_) rc_ids_[ids[r]].assign(prompts[r].begin(), prompts[r].begin() + rc);
+        for (int t = 0; t < P; ++t) {
+            tokens.push_back(prompts[r][t]);
+            positions.push_back(t);
+            if (t >= rc) assigner_->add_token(ids[r]);
         }
-        const int T = cu.back();
-        if (T == 0) {
-            r0 = r1;
-            continue;
-        }
-        m.ensure_prefill(T);
-        // metadata: tokens | positions | cu | a_src | a_n | a_ref | k_src | k_n | k_ref
-        std::vector<int> meta;
-        auto put = [&](const std::vector<int>& v) {
-            const size_t o = meta.size();
-            meta.insert(meta.end(), v.begin(), v.end());
-            return o;
-        };
-        const size_t o_tok = put(tokens), o_pos = put(positions), o_cu = put(cu), o_as = put(a_src), o_an = put(a_n),
-                     o_ar = put(a_ref), o_ks = put(k_src), o_kn = put(k_n), o_kr = put(k_ref);
-        m.ensure_meta(meta.size());
-        std::memcpy(m.h_meta, meta.data(), meta.size() * 4);
-        HC_CUDA(cudaMemcpyAsync(m.d_meta, m.h_meta, meta.size() * 4, cudaMemcpyHostToDevice, s_compute_));
-        const int* dm = m.d_meta;
-        embed(m.emb, m.pos, dm + o_tok, dm + o_pos, T, m.d, m.px[0], m.d, s_compute_);
-        for (int l = 0; l < m.L; ++l) {
-            const int slot = l & 1;
-            if (!m.w_all) {
-                HC_CUDA(cudaStreamWaitEvent(s_copy_, m.consumed[slot]));
-                HC_CUDA(cudaMemcpyAsync(m.wbuf[slot], m.h_w + static_cast<size_t>(l % m.Lw) * m.LE, m.LE * 2,
-                                        cudaMemcpyHostToDevice, s_copy_));
-                HC_CUDA(cudaEventRecord(m.loaded[slot], s_copy_));
-                HC_CUDA(cudaStreamWaitEvent(s_compute_, m.loaded[slot]));
+        int row = base + rc;
+        for (const auto& e : cache_->table(ids[r]).entries) {
+            const bool gpu = e.location == Location::GpuMem;
+            if (e.kind == BlockKind::ACT) {
+                a_src.push_back(row);
+                a_n.push_back(e.filled_tokens);
+                a_ref.push_back(pack_ref(gpu ? R_ACT_GPU : R_ACT_STAGE, e.pbn));
+                if (!gpu) acth.push_back(e.pbn);
+            } else {
+                c.k_src.push_back(row - c.row0);
+                c.k_n.push_back(e.filled_tokens);
+                c.k_ref.push_back(pack_ref(gpu ? R_KV_GPU : R_KV_STAGE, e.pbn));
+                if (!gpu) kvh.push_back(e.pbn);
             }
-            const bf16* W = m.layer_w(l, slot);
-            bf16* R[16];
-            m.regions(l, slot, R);
-            bf16* xin = m.px[l & 1];
-            bf16* xout = m.px[(l + 1) & 1];
-            // activation-cache writer: this layer's input rows of ACT blocks
-            BlockScatter sa;
-            sa.src = xin;
-            sa.ld = m.d;
-            sa.src_row = dm + o_as;
-            sa.n_tok = dm + o_an;
-            sa.dst_ref = dm + o_ar;
-            std::copy(R, R + 16, sa.region);
-            sa.n_blocks = static_cast<int>(a_src.size());
-            sa.d = m.d;
-            sa.H = m.H;
-            sa.hd = m.hd;
-            sa.tpb = m.tpb;
-            scatter_act_blocks(sa, s_compute_);
-            gemm_rows(gemm::kStore, xin, T, m.d, W + m.off.wqkv, 3 * m.d, m.pqkv, 3 * m.d, s_compute_);
+            row += e.filled_tokens;
+        }
+        c.rows += P;
+        c.n += 1;
+        c.cu.push_back(c.rows);
+        c.max_len = std::max(c.max_len, P);
+    }
+    const int T = static_cast<int>(tokens.size());
+    if (T == 0) return;
+    int max_chunk = 0;
+    for (const Chunk& c : chunks) max_chunk = std::max(max_chunk, c.rows);
+    m.ensure_prefill(T, max_chunk);
+    const std::vector<Run> act_runs = runs_of(acth), kv_runs = runs_of(kvh);
+    const bool stores = !act_runs.empty() || !kv_runs.empty();
+
+    std::vector<int> meta;
+    auto put = [&](const std::vector<int>& v) {
+        const size_t o = meta.size();
+        meta.insert(meta.end(), v.begin(), v.end());
+        return o;
+    };
+    const size_t o_tok = put(tokens), o_pos = put(positions), o_as = put(a_src), o_an = put(a_n), o_ar = put(a_ref);
+    for (Chunk& c : chunks) {
+        c.o_cu = put(c.cu);
+        c.o_ks = put(c.k_src);
+        c.o_kn = put(c.k_n);
+        c.o_kr = put(c.k_ref);
+    }
+    m.ensure_meta(meta.size());
+    std::memcpy(m.h_meta, meta.data(), meta.size() * 4);
+    const int* dm = m.d_meta;
+
+    StepStats st{};
+    m.pev_used = 0;
+    m.spans.clear();
+    const float scale = opt_.scaled ? 1.0f / std::sqrt(static_cast<float>(m.hd)) : 1.0f;
+    HC_CUDA(cudaEventRecord(m.ev0, s_compute_));
+    HC_CUDA(cudaMemcpyAsync(m.d_meta, m.h_meta, meta.size() * 4, cudaMemcpyHostToDevice, s_compute_));
+    embed(m.emb, m.pos, dm + o_tok, dm + o_pos, T, m.d, m.px[0], m.d, s_compute_);
+    st.launches += 1;
+    for (int l = 0; l < m.L; ++l) {
+        const int slot = l & 1;
+        m.cur_layer = l;
+        if (!m.w_all) {
+            HC_CUDA(cudaStreamWaitEvent(s_copy_, m.consumed[slot]));
+            m.span_begin(profile_, s_copy_, 3);
+            HC_CUDA(cudaMemcpyAsync(m.wbuf[slot], m.h_w + static_cast<size_t>(l % m.Lw) * m.LE, m.LE * 2,
+                                    cudaMemcpyHostToDevice, s_copy_));
+            m.span_end(profile_, s_copy_);
+            st.h2d_bytes += m.LE * 2.0;
+            HC_CUDA(cudaEventRecord(m.loaded[slot], s_copy_));
+            HC_CUDA(cudaStreamWaitEvent(s_compute_, m.loaded[slot]));
+        }
+        // the staging slot is free once layer l-2's stores have left
+        if (stores && l >= 2) HC_CUDA(cudaStreamWaitEvent(s_compute_, m.stored[slot]));
+        const bf16* W = m.layer_w(l, slot);
+        bf16* R[16];
+        m.regions(l, slot, R);
+        bf16* xin = m.px[l & 1];
+        bf16* xout = m.px[(l + 1) & 1];
+        // activation-cache writer: this layer's input rows of every ACT block
+        BlockScatter sa;
+        sa.src = xin;
+        sa.ld = m.d;
+        sa.src_row = dm + o_as;
+        sa.n_tok = dm + o_an;
+        sa.dst_ref = dm + o_ar;
+        std::copy(R, R + 16, sa.region);
+        sa.n_blocks = static_cast<int>(a_src.size());
+        sa.d = m.d;
+        sa.H = m.H;
+        sa.hd = m.hd;
+        sa.tpb = m.tpb;
+        scatter_act_blocks(sa, s_compute_);
+        st.launches += sa.n_blocks > 0;
+        for (const Chunk& c : chunks) {
+            const bf16* cin = xin + static_cast<size_t>(c.row0) * m.d;
+            bf16* cout = xout + static_cast<size_t>(c.row0) * m.d;
+            m.span_begin(profile_, s_compute_, 2);
+            gemm_rows(gemm::kStore, cin, c.rows, m.d, W + m.off.wqkv, 3 * m.d, m.pqkv, 3 * m.d, s_compute_);
+            m.span_end(profile_, s_compute_);
             BlockScatter sk = sa;
             sk.src = m.pqkv;
             sk.ld = 3 * m.d;
-            sk.src_row = dm + o_ks;
-            sk.n_tok = dm + o_kn;
-            sk.dst_ref = dm + o_kr;
-            sk.n_blocks = static_cast<int>(k_src.size());
+            sk.src_row = dm + c.o_ks;
+            sk.n_tok = dm + c.o_kn;
+            sk.dst_ref = dm + c.o_kr;
+            sk.n_blocks = static_cast<int>(c.k_src.size());
             scatter_kv_blocks(sk, s_compute_);
-            prefill_attention(m.pqkv, m.patt, dm + o_cu, n, max_len, m.H, m.hd,
-                              opt_.scaled ? 1.0f / std::sqrt(static_cast<float>(m.hd)) : 1.0f, s_compute_);
-            gemm_rows(gemm::kStore, m.patt, T, m.d, W + m.off.wproj, m.d, m.pproj, m.d, s_compute_);
-            gemm_rows(gemm::kRelu, m.pproj, T, m.d, W + m.off.w1, m.f, m.ph, m.f, s_compute_);
-            gemm_rows(gemm::kStore, m.ph, T, m.f, W + m.off.w2, m.d, xout, m.d, s_compute_);
-            HC_CUDA(cudaEventRecord(m.consumed[slot], s_compute_));
+            m.span_begin(profile_, s_compute_, 1);
+            prefill_attention(m.pqkv, m.patt, dm + c.o_cu, c.n, c.max_len, m.H, m.hd, scale, s_compute_);
+            m.span_end(profile_, s_compute_);
+            m.span_begin(profile_, s_compute_, 2);
+            gemm_rows(gemm::kStore, m.patt, c.rows, m.d, W + m.off.wproj, m.d, m.pproj, m.d, s_compute_);
+            gemm_rows(gemm::kRelu, m.pproj, c.rows, m.d, W + m.off.w1, m.f, m.ph, m.f, s_compute_);
+            gemm_rows(gemm::kStore, m.ph, c.rows, m.f, W + m.off.w2, m.d, cout, m.d, s_compute_);
+            m.span_end(profile_, s_compute_);
+            st.launches += 5 + (sk.n_blocks > 0);
         }
-        HC_CUDA(cudaGetLastError());
-        HC_CUDA(cudaStreamSynchronize(s_compute_));
-        r0 = r1;
+        HC_CUDA(cudaEventRecord(m.consumed[slot], s_compute_));
+        if (stores) {  // this layer's host blocks: staging slot -> pinned pool (copy engine, D2H)
+            HC_CUDA(cudaStreamWaitEvent(s_store_, m.consumed[slot]));
+            m.span_begin(profile_, s_store_, 4);
+            const size_t lp = static_cast<size_t>(l % m.Lp);
+            for (const Run& r : act_runs) {
+                const size_t bytes = static_cast<size_t>(r.count) * m.actb * 2;
+                HC_CUDA(cudaMemcpyAsync(m.act_host + (lp * m.act_host_cap + r.start) * m.actb,
+                                        m.act_stage[slot] + static_cast<size_t>(r.start) * m.actb, bytes,
+                                        cudaMemcpyDeviceToHost, s_store_));
+                st.d2h_bytes += bytes;
+            }
+            for (const Run& r : kv_runs) {
+                const size_t bytes = static_cast<size_t>(r.count) * m.kvb * 2;
+                HC_CUDA(cudaMemcpyAsync(m.kv_host + (lp * m.kv_host_cap + r.start) * m.kvb,
+                                        m.kv_stage[slot] + static_cast<size_t>(r.start) * m.kvb, bytes,
+                                        cudaMemcpyDeviceToHost, s_store_));
+                st.d2h_bytes += bytes;
+            }
+            m.span_end(profile_, s_store_);
+            HC_CUDA(cudaEventRecord(m.stored[slot], s_store_));
+        }
     }
+    if (stores) {
+        HC_CUDA(cudaStreamWaitEvent(s_compute_, m.stored[0]));
+        HC_CUDA(cudaStreamWaitEvent(s_compute_, m.stored[1]));
+    }
+    HC_CUDA(cudaEventRecord(m.ev1, s_compute_));
+    HC_CUDA(cudaGetLastError());
+    HC_CUDA(cudaStreamSynchronize(s_compute_));
+    float ms = 0;
+    HC_CUDA(cudaEventElapsedTime(&ms, m.ev0, m.ev1));
+    st.step_ms = ms;
+    for (const auto& sp : m.spans) {
+        float t = 0;
+        HC_CUDA(cudaEventElapsedTime(&t, sp.a, sp.b));
+        if (sp.kind == 1)
+            st.attn_ms += t;
+        else if (sp.kind == 2)
+            st.gemm_ms += t;
+        else if (sp.kind == 3)
+            st.copy_ms += t;
+        else if (sp.kind == 4)
+            st.store_ms += t;
+    }
+    stats_ = st;
 }
 
 void Engine::admit_synthetic(const std::vector<std::string>& ids, const std::vector<int>& prompt_lens, uint64_t seed) {

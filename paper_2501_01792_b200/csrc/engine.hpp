@@ -65,6 +65,7 @@ struct StepStats {
     int launches = 0;             // kernels launched this step
     double copy_ms = 0;           // summed copy-stream time of the H2D streams (profiled)
     int recompute_launches = 0;
+    double store_ms = 0;          // summed store-stream (D2H) time (profiled prefill)
 };
 
 class Engine {
@@ -79,6 +80,9 @@ public:
 
     // Prefill (forward_prompt semantics, decoder.cpp:144-157) of new requests;
     // writes every layer's ACT / KV blocks chosen by the ratio policy.
+    // Layer-outer pipeline: weights streamed once per layer, host blocks
+    // stored by D2H copies on a store stream (last_stats(): step_ms = the
+    // whole prefill, h2d = weights, d2h = stored blocks).
     void prefill(const std::vector<std::string>& ids, const std::vector<std::vector<int>>& prompts);
     // Admit requests with prompt_len tokens of bookkeeping only and fill their
     // blocks with a deterministic pattern (benchmark setup; no numerics).
@@ -148,7 +152,7 @@ private:
     EngineOptions opt_;
     std::unique_ptr<HybridCache> cache_;
     std::unique_ptr<BlockAssigner> assigner_;
-    cudaStream_t s_compute_ = nullptr, s_copy_ = nullptr;
+    cudaStream_t s_compute_ = nullptr, s_copy_ = nullptr, s_store_ = nullptr;
     StepStats stats_{};
     bool profile_ = false;
     bool capture_inputs_ = false;

@@ -1,6 +1,5 @@
-// Decode attention over the hybrid block table (north-star (3)) and causal
-// prefill attention.
-//
+// Decode attention over the hybrid block table (north-star (3)). The causal
+// prefill attention lives in prefill_attention.cu.
 // Semantics: attention_row, decoder.cpp:15-43 — per head h,
 //   out_h = softmax(q_h . K_h^T * s) . V_h,  s = 1/sqrt(hd) (scaled=true),
 // max-subtracted. Here the softmax is computed online (flash-decoding) over
@@ -207,100 +206,6 @@ __global__ void attn_combine_kernel(const AttnCall c) {
 }
 
 // ---------------------------------------------------------------------------
-// Causal prefill attention (attention_causal, decoder.cpp:55-63): CUDA cores,
-// one CTA per (request, head, 64-query tile); 2 threads per query each own
-// half of the head dims; K/V tiles of 32 keys staged in shared memory.
-template <int HD>
-__global__ void __launch_bounds__(128)
-    prefill_attn_kernel(const bf16* __restrict__ qkv, bf16* __restrict__ out, const int* __restrict__ cu, int H,
-                        float scale) {
-    constexpr int QT = 64, KT = 32, HALF = HD / 2;
-    const int d = H * HD;
-    const int ld = 3 * d;
-    const int req = blockIdx.z;
-    const int h = blockIdx.y;
-    const int q0 = blockIdx.x * QT;
-    const int row0 = cu[req];
-    const int P = cu[req + 1] - row0;
-    if (q0 >= P) return;
-    const int tq = threadIdx.x / 2;
-    const int half = threadIdx.x % 2;
-    const int t = q0 + tq;
-    const bool active = t < P;
-
-    __shared__ __align__(16) bf16 sk[KT][HD];
-    __shared__ __align__(16) bf16 sv[KT][HD];
-
-    const bf16* rowbase = qkv + static_cast<long long>(row0) * ld;
-    float q[HALF];
-    {
-        const bf16* qp = rowbase + static_cast<long long>(active ? t : 0) * ld + h * HD + half * HALF;
-#pragma unroll
-        for (int j = 0; j < HALF; j += 8) {
-            float f[8];
-            load8(qp + j, f);
-#pragma unroll
-            for (int i = 0; i < 8; ++i) q[j + i] = f[i] * scale * kLog2e;
-        }
-    }
-    float m = -FLT_MAX, l = 0.f;
-    float acc[HALF];
-#pragma unroll
-    for (int j = 0; j < HALF; ++j) acc[j] = 0.f;
-
-    const int kmax = min(P, q0 + QT);  // keys needed by this tile
-    for (int k0 = 0; k0 < kmax; k0 += KT) {
-        __syncthreads();
-        for (int idx = threadIdx.x; idx < KT * HD / 8; idx += blockDim.x) {
-            const int r = idx / (HD / 8), cc = (idx % (HD / 8)) * 8;
-            const int key = k0 + r;
-            uint4 kv = make_uint4(0, 0, 0, 0), vv = make_uint4(0, 0, 0, 0);
-            if (key < P) {
-                const bf16* kp = rowbase + static_cast<long long>(key) * ld + d + h * HD + cc;
-                kv = *reinterpret_cast<const uint4*>(kp);
-                vv = *reinterpret_cast<const uint4*>(kp + d);
-            }
-            *reinterpret_cast<uint4*>(&sk[r][cc]) = kv;
-            *reinterpret_cast<uint4*>(&sv[r][cc]) = vv;
-        }
-        __syncthreads();
-        const int kend = min(KT, kmax - k0);
-        for (int r = 0; r < kend; ++r) {
-            const int key = k0 + r;
-            float dot = 0.f;
-#pragma unroll
-            for (int j = 0; j < HALF; j += 2) {
-                const float2 kf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&sk[r][half * HALF + j]));
-                dot = fmaf(q[j], kf.x, dot);
-                dot = fmaf(q[j + 1], kf.y, dot);
-            }
-            dot += __shfl_xor_sync(0xffffffffu, dot, 1);
-            if (key > t) continue;  // causal mask (uniform within the thread pair)
-            const float m_new = fmaxf(m, dot);
-            const float corr = exp2f(m - m_new);
-            const float pr = exp2f(dot - m_new);
-            l = l * corr + pr;
-#pragma unroll
-            for (int j = 0; j < HALF; j += 2) {
-                const float2 vf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&sv[r][half * HALF + j]));
-                acc[j] = fmaf(pr, vf.x, acc[j] * corr);
-                acc[j + 1] = fmaf(pr, vf.y, acc[j + 1] * corr);
-            }
-            m = m_new;
-        }
-    }
-    if (!active) return;
-    bf16* op = out + static_cast<long long>(row0 + t) * d + h * HD + half * HALF;
-    const float inv = 1.f / l;
-#pragma unroll
-    for (int j = 0; j < HALF; j += 8) {
-        uint32_t w[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) w[i] = ptx::pack_bf16x2(acc[j + 2 * i] * inv, acc[j + 2 * i + 1] * inv);
-        *reinterpret_cast<uint4*>(op + j) = make_uint4(w[0], w[1], w[2], w[3]);
-    }
-}
-
 }  // namespace
 
 int attention_splits(int B, int H, int max_ctx, int tpb) {
@@ -329,18 +234,6 @@ void decode_attention(const AttnCall& c, cudaStream_t st) {
     HC_ATTN(64, 32)
 #undef HC_ATTN
     throw std::invalid_argument("decode_attention: unsupported (head_dim, tokens_per_block)");
-}
-
-void prefill_attention(const bf16* qkv, bf16* out, const int* cu, int n_req, int max_len, int H, int hd,
-                       float scale, cudaStream_t st) {
-    if (n_req <= 0 || max_len <= 0) return;
-    const dim3 grid((max_len + 63) / 64, H, n_req);
-    if (hd == 128)
-        prefill_attn_kernel<128><<<grid, 128, 0, st>>>(qkv, out, cu, H, scale);
-    else if (hd == 64)
-        prefill_attn_kernel<64><<<grid, 128, 0, st>>>(qkv, out, cu, H, scale);
-    else
-        throw std::invalid_argument("prefill_attention: head_dim must be 64 or 128");
 }
 
 }  // namespace hc

@@ -84,3 +84,20 @@ print("done")
     out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=120)
     assert out.returncode == 0, out.stderr
     assert out.stdout.strip() == "done"
+
+
+def test_config4_strong_split_covers_global_batch():
+    """Config 4 (OPT-66B, global batch 128 over 2/4/8 ranks): the per-rank
+    slices partition the global batch exactly (strong scaling)."""
+    sys.path.insert(0, ROOT)
+    import bench
+    sys.argv = ["bench.py", "--config", "4"]
+    a = bench.parse()
+    assert a.model == "opt-66b" and a.global_batch == 128 and a.ratio == -1.0 and a.scaling == "strong"
+    for world in (1, 2, 3, 4, 8):
+        sizes = [bench.per_rank_batch(a, world, r) for r in range(world)]
+        assert sum(sizes) == 128 and max(sizes) - min(sizes) <= 1
+    sys.argv = ["bench.py"]
+    b = bench.parse()
+    assert b.model == "opt-30b" and b.scaling == "weak" and abs(b.ratio - 1 / 3) < 1e-12
+    assert bench.per_rank_batch(b, 8, 7) == 128
