@@ -53,6 +53,8 @@ def parse():
                         "PAPER.md:714); -1 = the planner's choice from measured rates")
     p.add_argument("--host-gb", type=float, default=0.0, help="pinned host budget per rank (0: auto)")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--arch", default="reference", choices=["reference", "opt"],
+                   help="decoder layer: the reference's (default) or OPT's (biases, pre-LN, residuals)")
     p.add_argument("--prefill", default="real", choices=["real", "synthetic"],
                    help="build the decode cache by the real prefill of synthetic prompts (default) or by "
                         "pattern-filled bookkeeping-only admission")
@@ -285,7 +287,7 @@ def workload_config(args, cfg, world, extra=None):
                      f", prompt {args.prompt}, gen {args.gen}",
          "model": cfg.name, "global_batch": gb, "batch_per_gpu": B, "seq_len": args.prompt, "gen_len": args.gen,
          "act_share_r": round(extra.get("act_share_r", args.ratio), 4) if extra else round(args.ratio, 4),
-         "parallelism": f"batch-partitioned x{world} (no collective)",
+         "parallelism": f"batch-partitioned x{world} (no collective)", "arch": args.arch,
          "l2": "inputs larger than L2 (~100+ GB streamed host->HBM per step)"}
     if extra:
         c.update(extra)
@@ -453,17 +455,22 @@ def run_prefill(eng, cfg, ids, P, rank, tflops_sust, link_gbs):
             "launches": int(st["launches"])}
 
 
-def calibrate_planner(eng, cfg, link_gbs, caps_act_rows, host_mem, act_gpu=0):
+def calibrate_planner(eng, cfg, link_gbs, caps_act_rows, workload_tokens, act_gpu=0):
     """North-star (5): measured recompute-GEMM and host-link samples ->
     bundle_from_samples (timing.cpp:172-183) -> plan_host_allocation
-    (plan.cpp:106-152) over this host's available DRAM (HardwareProfile::
-    host_mem semantics, plan.cpp:41-51)."""
+    (plan.cpp:106-152) over a WORKLOAD-sized host budget, as the reference's
+    own interior-balance test sizes it (test_sim.cpp:281-282: m_host =
+    s_weight + 0.9 x workload blocks x s_kv_block) — the whole-DRAM budget
+    (plan.cpp:41-51) cannot even hold OPT-66B's weights plus the initial ACT
+    blocks on a 196 GB host (CapacityError, plan.cpp:79)."""
     from paper_2501_01792_b200 import api
     ns = [n for n in (4096, 16384, 32768, 65536) if n <= caps_act_rows]
     kv = [(float(n), eng.time_kv_gen(n, reps=3)) for n in ns]
     ld = [(float(n), eng.time_load_kv(n, reps=2)) for n in ns]
     bundle = api.bundle_from_samples(kv, ld, link_gbs * 1e9, cfg)
-    mem = api.budget_for(float(host_mem), cfg, bundle)
+    mem = api.budget_for(0.0, cfg, bundle)
+    workload_blocks = workload_tokens / cfg.tokens_per_block
+    mem.m_host = mem.s_weight + workload_blocks * mem.s_kv_block * 0.9
     alloc = api.plan_host_allocation(bundle, mem, cfg.tokens_per_block, act_gpu)
     r = alloc.act_host / max(alloc.act_host + alloc.kv_host, 1)
     return {"kv_gen_samples": kv, "load_kv_samples": ld,
@@ -472,6 +479,7 @@ def calibrate_planner(eng, cfg, link_gbs, caps_act_rows, host_mem, act_gpu=0):
             "t_load_kv": {"slope_s_per_token": bundle.t_load_kv.slope, "intercept_s": bundle.t_load_kv.intercept,
                           "r2": bundle.t_load_kv.r_squared},
             "t_load_w_s": bundle.t_load_w, "m_host": mem.m_host,
+            "m_host_source": "workload-sized: s_weight + 0.9 x B(P+G)/tpb x s_kv_block (test_sim.cpp:281-282)",
             "allocation": alloc.__dict__, "planned_r": r,
             "planned_t_pcie_s": api.planned_t_pcie(bundle, cfg.tokens_per_block, alloc),
             "planned_t_comp_s": api.planned_t_computation(bundle, cfg.tokens_per_block, alloc, act_gpu)}
@@ -496,7 +504,8 @@ def our_arm(args, cfg, world, rank, local, dist):
     Lp = host_layers_for(cfg, caps, budget, Lw * w_layer)
     t_setup = time.time()
     eng = api.Engine(cfg, seed=42, max_seq=max_seq, rescale=True, max_batch=B, weights_on_device=False,
-                     caps=caps, host_layers=Lp, weight_layers=Lw, mode=mode, allocation=alloc, device=local)
+                     caps=caps, host_layers=Lp, weight_layers=Lw, mode=mode, allocation=alloc, device=local,
+                     arch=args.arch)
     ids = [f"g{rank}r{i}" for i in range(B)]
     # host-link peak: a large pinned H2D copy on the engine's copy stream
     tpb = cfg.tokens_per_block
@@ -506,7 +515,7 @@ def our_arm(args, cfg, world, rank, local, dist):
     planner = None
     if link_gbs and caps.act_host:
         try:
-            planner = calibrate_planner(eng, cfg, link_gbs, caps.act_host * tpb, mem_total_bytes())
+            planner = calibrate_planner(eng, cfg, link_gbs, caps.act_host * tpb, B * (P + args.gen))
         except Exception as e:  # planner failure must not kill the bench line
             planner = {"error": str(e)}
     if args.ratio < 0 and planner and "planned_r" in planner:

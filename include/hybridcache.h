@@ -132,6 +132,9 @@ typedef struct hc_engine_options {
     int device;
     int weight_layers;       /* physical pinned weight layers (0 = num_layers) */
     double recompute_ratio;  /* mode 3 (token_recompute): share of each prompt kept as ids only */
+    int arch;                /* 0 reference decoder (decoder.cpp: no bias/LN/residual); 1 OPT (pre-LN,
+                              * biases, residuals, final LN; the ACT cache holds LN1(x)). Seeded engines
+                              * draw the OPT extras; f64 engines take them from _create_from_f64_opt. */
 } hc_engine_options;
 
 int hc_engine_create(const hc_model_config* cfg, uint64_t seed, int max_seq, int rescale,
@@ -140,6 +143,11 @@ int hc_engine_create(const hc_model_config* cfg, uint64_t seed, int max_seq, int
  * pos [max_seq x d], layer_tensors[6*l + {0 q,1 k,2 v,3 proj,4 ffn1,5 ffn2}]. */
 int hc_engine_create_from_f64(const hc_model_config* cfg, int max_seq, const double* emb, const double* pos,
                               const double* const* layer_tensors, const hc_engine_options* opt, void** out);
+/* Same for arch 1 (OPT): + layer_extras[10*l + {0 b_q,1 b_k,2 b_v,3 b_o [d],4 b_1 [f],5 b_2,6 gamma1,
+ * 7 beta1,8 gamma2,9 beta2 [d]}] and final_ln = gamma_f | beta_f [2d]. No reference counterpart. */
+int hc_engine_create_from_f64_opt(const hc_model_config* cfg, int max_seq, const double* emb, const double* pos,
+                                  const double* const* layer_tensors, const double* const* layer_extras,
+                                  const double* final_ln, const hc_engine_options* opt, void** out);
 int hc_engine_destroy(void* engine);
 /* Prefill n requests; prompt r = tokens[offsets[r] .. offsets[r+1]). */
 int hc_engine_prefill(void* engine, int n, const char* const* ids, const int* offsets, const int* tokens);
@@ -168,7 +176,7 @@ int hc_engine_cache(void* engine, void** cache);
 int hc_engine_read_block(void* engine, int kind, int loc, int pbn, int layer, uint16_t* out);
 /* Engine-held weights (bf16): layer >= 0 packed layer, -1 embedding [V x d],
  * -2 positional [max_seq x d]. */
-int hc_engine_read_weights(void* engine, int layer, uint16_t* out);
+int hc_engine_read_weights(void* engine, int layer, uint16_t* out);  /* -3: final LN (arch 1) */
 int hc_engine_capture_inputs(void* engine, int on);
 /* Decode-time layer inputs of the last step, [L][n][d] bf16 (n = last batch). */
 int hc_engine_captured_inputs(void* engine, uint16_t* out, long count);

@@ -157,6 +157,9 @@ class DecoderWeights:
     embedding: np.ndarray
     positional: np.ndarray
     layers: List[Dict[str, np.ndarray]] = field(default_factory=list)
+    # OPT decoder-layer variant only (extension, see forward_prompt_opt)
+    extras: Optional[List[Dict[str, np.ndarray]]] = None
+    final_ln: Optional[Dict[str, np.ndarray]] = None
 
 
 def generate_weights(cfg: ModelConfig, seed: int, max_seq: int) -> DecoderWeights:
@@ -351,6 +354,83 @@ def logits_tied(x: np.ndarray, w: DecoderWeights) -> np.ndarray:
     """Extension (parity unpinned by the reference, which has no LM head —
     decoder.hpp:56-59): tied head x @ E^T, as OPT does."""
     return x @ w.embedding.T
+
+
+# --------------------------------------------------------------------------
+# OPT decoder-layer variant — an EXTENSION (SURVEY.md §8(f) rank 4: bias,
+# LayerNorm, residual). The reference's layer has none of these
+# (decoder.cpp:97-129, SPEC.md:112), so this restatement is parity-unpinned
+# by reference tests; it is the checker for the product's kArchOpt
+# (csrc/host/model.hpp). Extras use the reference's RNG (rng.hpp:10-49) on
+# tags the reference leaves free: 100+8l+6 biases, 100+8l+7 LayerNorms,
+# 2 the final LayerNorm.
+# --------------------------------------------------------------------------
+OPT_EXTRAS = ("b_q", "b_k", "b_v", "b_o", "b_1", "b_2", "ln1_g", "ln1_b", "ln2_g", "ln2_b")
+LN_EPS = 1e-5
+
+
+def generate_opt_extras(cfg: ModelConfig, seed: int):
+    """Per-layer biases + LayerNorm parameters and the final LayerNorm
+    (gamma = 1 + u, beta = u, biases = u; u ~ U(-0.1, 0.1))."""
+    d, f = cfg.hidden_dim, cfg.ffn_dim
+    layers = []
+    for l in range(cfg.num_layers):
+        base = 100 + 8 * l
+        b = seeded_matrix(1, 5 * d + f, mix_seed(seed, base + 6)).ravel()
+        u = seeded_matrix(1, 4 * d, mix_seed(seed, base + 7)).ravel()
+        layers.append({"b_q": b[:d], "b_k": b[d:2 * d], "b_v": b[2 * d:3 * d], "b_o": b[3 * d:4 * d],
+                       "b_1": b[4 * d:4 * d + f], "b_2": b[4 * d + f:],
+                       "ln1_g": 1.0 + u[:d], "ln1_b": u[d:2 * d], "ln2_g": 1.0 + u[2 * d:3 * d], "ln2_b": u[3 * d:]})
+    u = seeded_matrix(1, 2 * d, mix_seed(seed, 2)).ravel()
+    return layers, {"gamma": 1.0 + u[:d], "beta": u[d:]}
+
+
+def with_opt_extras(w: DecoderWeights, seed: int, bf16: bool = True) -> DecoderWeights:
+    """w plus the OPT extras, bf16-rounded like the GPU's copies."""
+    rnd = bf16_round if bf16 else (lambda a: a)
+    ex, lnf = generate_opt_extras(w.config, seed)
+    return DecoderWeights(w.config, w.max_seq, w.embedding, w.positional, w.layers,
+                          [{k: rnd(v) for k, v in e.items()} for e in ex], {k: rnd(v) for k, v in lnf.items()})
+
+
+def layer_norm(x: np.ndarray, g: np.ndarray, b: np.ndarray, eps: float = LN_EPS) -> np.ndarray:
+    mu = x.mean(axis=-1, keepdims=True)
+    var = ((x - mu) ** 2).mean(axis=-1, keepdims=True)
+    return (x - mu) / np.sqrt(var + eps) * g + b
+
+
+@dataclass
+class OptTrace:
+    layer_inputs: List[np.ndarray]   # residual stream x entering layer l
+    act: List[np.ndarray]            # LN1(x): the ACT-cache payload
+    k: List[np.ndarray]
+    v: List[np.ndarray]
+    output: np.ndarray               # LN_f(x_L): the model output
+
+
+def forward_prompt_opt(ids: Sequence[int], w: DecoderWeights, scaled: bool = True) -> OptTrace:
+    """OPT pre-LN decoder over a prompt: x^ = LN1(x); q,k,v = x^ W + b;
+    x' = x + attn W_o + b_o; x_next = x' + relu(LN2(x') W1 + b1) W2 + b2;
+    output LN_f(x_L). Recompute from the ACT payload is K|V = x^ [W_k|W_v] +
+    [b_k|b_v] — Eq. 7 with OPT's bias."""
+    if w.extras is None or w.final_ln is None:
+        raise InputError("forward_prompt_opt: weights carry no OPT extras")
+    x = embed(ids, w)
+    n = x.shape[0]
+    ins, acts, ks, vs = [], [], [], []
+    for l in range(w.config.num_layers):
+        lw, e = w.layers[l], w.extras[l]
+        ins.append(x)
+        xa = layer_norm(x, e["ln1_g"], e["ln1_b"])
+        acts.append(xa)
+        q, k, v = xa @ lw["w_q"] + e["b_q"], xa @ lw["w_k"] + e["b_k"], xa @ lw["w_v"] + e["b_v"]
+        ks.append(k)
+        vs.append(v)
+        att = attention_rows(q, k, v, [t + 1 for t in range(n)], w.config.num_heads, scaled)
+        x1 = x + att @ lw["w_proj"] + e["b_o"]
+        h = np.maximum(layer_norm(x1, e["ln2_g"], e["ln2_b"]) @ lw["w_ffn1"] + e["b_1"], 0.0)
+        x = x1 + h @ lw["w_ffn2"] + e["b_2"]
+    return OptTrace(ins, acts, ks, vs, layer_norm(x, w.final_ln["gamma"], w.final_ln["beta"]))
 
 
 # --------------------------------------------------------------------------

@@ -23,7 +23,7 @@ class EngineOptionsC(C.Structure):
                 ("act_gpu_cap", C.c_long), ("kv_on_gpu", C.c_int), ("host_layers", C.c_int),
                 ("mode", C.c_int), ("alloc_act_host", C.c_long), ("alloc_kv_host", C.c_long),
                 ("scaled", C.c_int), ("max_prefill_tokens", C.c_int), ("device", C.c_int),
-                ("weight_layers", C.c_int), ("recompute_ratio", C.c_double)]
+                ("weight_layers", C.c_int), ("recompute_ratio", C.c_double), ("arch", C.c_int)]
 
 
 cfgp = C.POINTER(ModelConfigC)
@@ -71,6 +71,7 @@ SIGNATURES = {
     # engine
     "hc_engine_create": (i, [cfgp, u64, i, i, optp, vpp]),
     "hc_engine_create_from_f64": (i, [cfgp, i, dp, dp, C.POINTER(dp), optp, vpp]),
+    "hc_engine_create_from_f64_opt": (i, [cfgp, i, dp, dp, C.POINTER(dp), C.POINTER(dp), dp, optp, vpp]),
     "hc_engine_destroy": (i, [vp]),
     "hc_engine_prefill": (i, [vp, i, cpp, ip, ip]),
     "hc_engine_admit_synthetic": (i, [vp, i, cpp, ip, u64]),

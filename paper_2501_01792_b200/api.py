@@ -419,6 +419,10 @@ def weight_bytes(cfg: ModelConfig) -> Tuple[int, int]:
 
 # ---------------------------------------------------------------- engine ---
 MODES = {"hybrid": 0, "kv_only": 1, "act_only": 2, "token_recompute": 3}
+# decoder-layer variants (csrc/host/model.hpp Arch): the reference's (no bias /
+# LayerNorm / residual) and OPT's pre-LN layer with biases, residuals, final LN
+ARCHS = {"reference": 0, "opt": 1}
+OPT_EXTRAS = ("b_q", "b_k", "b_v", "b_o", "b_1", "b_2", "ln1_g", "ln1_b", "ln2_g", "ln2_b")
 
 
 def _ids(ids: Sequence[str]):
@@ -439,16 +443,19 @@ class Engine:
                  caps: Optional[PoolCaps] = None, kv_on_gpu: bool = False, host_layers: int = 0,
                  mode: str = "hybrid", allocation: Optional[HostAllocation] = None, scaled: bool = True,
                  max_prefill_tokens: int = 0, device: int = 0, weight_layers: int = 0,
-                 recompute_ratio: float = 0.0):
+                 recompute_ratio: float = 0.0, arch: str = "reference"):
         self.cfg = ModelConfig(**cfg.__dict__).validate()
         caps = caps or PoolCaps()
         alloc = allocation or HostAllocation(1, 1)
         if mode not in MODES:
             raise InputError(f"unknown mode: {mode}")
+        if arch not in ARCHS:
+            raise InputError(f"unknown arch: {arch}")
+        self.arch = arch
         self.opts = EngineOptionsC(max_batch, max_seq, int(weights_on_device), caps.kv_host, caps.kv_gpu,
                                    caps.act_host, caps.act_gpu, int(kv_on_gpu), host_layers, MODES[mode],
                                    alloc.act_host, alloc.kv_host, int(scaled), max_prefill_tokens, device,
-                                   weight_layers, recompute_ratio)
+                                   weight_layers, recompute_ratio, ARCHS[arch])
         self.max_batch = max_batch
         h = C.c_void_p()
         c = self.cfg.to_c()
@@ -467,8 +474,21 @@ class Engine:
                     a = np.ascontiguousarray(lw[nme], np.float64)
                     keep.append(a)
                     ptrs[6 * l + j] = ptr(a, C.c_double)
-            check(lib().hc_engine_create_from_f64(C.byref(c), pos.shape[0], ptr(emb, C.c_double),
-                                                  ptr(pos, C.c_double), ptrs, C.byref(self.opts), C.byref(h)))
+            if arch == "opt":
+                ex = (C.POINTER(C.c_double) * (10 * self.cfg.num_layers))()
+                for l, lx in enumerate(weights["extras"]):
+                    for j, nme in enumerate(OPT_EXTRAS):
+                        a = np.ascontiguousarray(lx[nme], np.float64)
+                        keep.append(a)
+                        ex[10 * l + j] = ptr(a, C.c_double)
+                lnf = np.ascontiguousarray(np.concatenate([weights["final_ln"]["gamma"],
+                                                          weights["final_ln"]["beta"]]), np.float64)
+                check(lib().hc_engine_create_from_f64_opt(C.byref(c), pos.shape[0], ptr(emb, C.c_double),
+                                                          ptr(pos, C.c_double), ptrs, ex, ptr(lnf, C.c_double),
+                                                          C.byref(self.opts), C.byref(h)))
+            else:
+                check(lib().hc_engine_create_from_f64(C.byref(c), pos.shape[0], ptr(emb, C.c_double),
+                                                      ptr(pos, C.c_double), ptrs, C.byref(self.opts), C.byref(h)))
         self._h = h
         w_max_seq = max_seq if weights is None else np.asarray(weights["positional"]).shape[0]
         self._max_seq = min(max_seq, w_max_seq) if max_seq > 0 else w_max_seq
@@ -578,8 +598,10 @@ class Engine:
             out = np.zeros((self.cfg.vocab_size, d), np.uint16)
         elif layer == -2:
             out = np.zeros((self._max_seq, d), np.uint16)
+        elif layer == -3:
+            out = np.zeros(2 * d, np.uint16)
         else:
-            out = np.zeros(4 * d * d + 2 * d * f, np.uint16)
+            out = np.zeros(4 * d * d + 2 * d * f + (9 * d + f if self.arch == "opt" else 0), np.uint16)
         check(lib().hc_engine_read_weights(self._h, layer, ptr(out, C.c_uint16)))
         return out
 

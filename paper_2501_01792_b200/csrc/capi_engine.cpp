@@ -81,6 +81,7 @@ EngineOptions opts_of(const hc_engine_options* o) {
     e.device = o->device;
     e.weight_layers = o->weight_layers;
     e.recompute_ratio = o->recompute_ratio;
+    e.arch = o->arch;
     return e;
 }
 
@@ -348,6 +349,14 @@ int hc_engine_create_from_f64(const hc_model_config* cfg, int max_seq, const dou
                               const double* const* layer_tensors, const hc_engine_options* opt, void** out) {
     return hc_guard([&] {
         const HostWeights w = weights_from_f64(to_cfg(cfg), max_seq, emb, pos, layer_tensors);
+        *out = new Engine(w, opts_of(opt));
+    });
+}
+int hc_engine_create_from_f64_opt(const hc_model_config* cfg, int max_seq, const double* emb, const double* pos,
+                                  const double* const* layer_tensors, const double* const* layer_extras,
+                                  const double* final_ln, const hc_engine_options* opt, void** out) {
+    return hc_guard([&] {
+        const HostWeights w = weights_from_f64_opt(to_cfg(cfg), max_seq, emb, pos, layer_tensors, layer_extras, final_ln);
         *out = new Engine(w, opts_of(opt));
     });
 }

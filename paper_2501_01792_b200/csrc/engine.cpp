@@ -74,10 +74,15 @@ T* halloc(size_t n, bool mapped) {
 }  // namespace
 
 void gemm_rows(int epi, const bf16* A, int M, int K, const bf16* W, int N, void* out, long long ldc, cudaStream_t st,
-               long long lda = 0, float* ws = nullptr, size_t ws_floats = 0);
+               long long lda = 0, float* ws = nullptr, size_t ws_floats = 0, const bf16* bias = nullptr,
+               const bf16* res = nullptr, long long ldr = 0);
 
 struct Engine::Impl {
     int L = 0, d = 0, H = 0, hd = 0, f = 0, V = 0, tpb = 0, B = 0, max_seq = 0, max_blocks = 0, Lp = 0, Lw = 0;
+    int arch = kArchReference;
+    bf16* lnf = nullptr;  // kArchOpt final LayerNorm gamma | beta [2d]
+    bf16* xn = nullptr;   // kArchOpt decode LN output [B x d]
+    bf16* pxn = nullptr;  // kArchOpt prefill LN1 output [prefill_rows x d]
     size_t LE = 0, kvb = 0, actb = 0;
     LayerOffsets off{};
     bf16 *emb = nullptr, *pos = nullptr;
@@ -88,7 +93,7 @@ struct Engine::Impl {
     bf16 *kv_stage[2] = {nullptr, nullptr}, *act_stage[2] = {nullptr, nullptr};
     bf16 *kv_host = nullptr, *act_host = nullptr;  // pinned, mapped
     long kv_host_cap = 0, kv_gpu_cap = 0, act_host_cap = 0, act_gpu_cap = 0;
-    bf16 *x[2] = {nullptr, nullptr}, *qkv = nullptr, *att = nullptr, *proj = nullptr, *hbuf = nullptr;
+    bf16 *x[2] = {nullptr, nullptr}, *qkvb = nullptr, *att = nullptr, *proj = nullptr, *hbuf = nullptr;
     float* logits = nullptr;
     int* amax = nullptr;
     float* attn_work = nullptr;
@@ -149,6 +154,41 @@ struct Engine::Impl {
     }
     const bf16* layer_w(int l, int slot) const { return w_all ? w_all + static_cast<size_t>(l) * LE : wbuf[slot]; }
 
+    // ---- decoder-layer arithmetic shared by decode, prefill and traces ----
+    bool opt() const { return arch == kArchOpt; }
+    const bf16* bias(const bf16* W, size_t o) const { return opt() ? W + o : nullptr; }
+    // LN1 (which = 1) / LN2 (2) of T rows of x into out for kArchOpt; the
+    // reference arch has no LayerNorm and returns x itself
+    const bf16* ln(const bf16* W, int which, const bf16* x, int T, bf16* out, cudaStream_t st) const {
+        if (!opt()) return x;
+        layernorm_rows(x, d, W + (which == 1 ? off.ln1g : off.ln2g), W + (which == 1 ? off.ln1b : off.ln2b), out, d,
+                       T, d, static_cast<float>(kLnEps), st);
+        return out;
+    }
+    // qkv [T x 3d] = LN1(x) . Wqkv (+ b_qkv)   (qkv_generate, decoder.cpp:97-103)
+    void qkv(const bf16* W, const bf16* xa, int T, bf16* out, cudaStream_t st, float* ws = nullptr,
+             size_t wsf = 0) const {
+        gemm_rows(gemm::kStore, xa, T, d, W + off.wqkv, 3 * d, out, 3 * d, st, 0, ws, wsf, bias(W, off.bqkv));
+    }
+    // project_ffn (decoder.cpp:113-121) of T attention rows; kArchOpt adds the
+    // biases, the two residuals (x, then x') and LN2. lnbuf may alias att.
+    void tail(const bf16* W, const bf16* att, const bf16* x, int T, bf16* proj, bf16* lnbuf, bf16* h, bf16* out,
+              cudaStream_t st, float* ws = nullptr, size_t wsf = 0) const {
+        gemm_rows(gemm::kStore, att, T, d, W + off.wproj, d, proj, d, st, 0, ws, wsf, bias(W, off.bproj),
+                  opt() ? x : nullptr, d);
+        const bf16* p2 = ln(W, 2, proj, T, lnbuf, st);
+        gemm_rows(gemm::kRelu, p2, T, d, W + off.w1, f, h, f, st, 0, ws, wsf, bias(W, off.b1));
+        gemm_rows(gemm::kStore, h, T, f, W + off.w2, d, out, d, st, 0, ws, wsf, bias(W, off.b2),
+                  opt() ? proj : nullptr, d);
+    }
+    int tail_launches() const { return opt() ? 4 : 3; }
+    // model output: LN_f(x) for kArchOpt (into out), x itself otherwise
+    const bf16* final_norm(const bf16* x, int T, bf16* out, cudaStream_t st) const {
+        if (!opt()) return x;
+        layernorm_rows(x, d, lnf, lnf + d, out, d, T, d, static_cast<float>(kLnEps), st);
+        return out;
+    }
+
     void ensure_meta(size_t ints) {
         if (ints <= meta_cap) return;
         if (d_meta) cudaFree(d_meta);
@@ -168,11 +208,12 @@ struct Engine::Impl {
     void ensure_prefill(size_t rows, size_t chunk_rows = 0) {
         if (!chunk_rows) chunk_rows = rows;
         if (rows > prefill_rows) {
-            for (bf16* p : {px[0], px[1]})
+            for (bf16* p : {px[0], px[1], pxn})
                 if (p) cudaFree(p);
             prefill_rows = rows;
             px[0] = dalloc<bf16>(rows * d);
             px[1] = dalloc<bf16>(rows * d);
+            pxn = opt() ? dalloc<bf16>(rows * d) : nullptr;
         }
         if (chunk_rows > prefill_chunk_rows) {
             for (bf16* p : {pqkv, patt, pproj, ph})
@@ -198,15 +239,25 @@ void fill_from_hostweights(const void* ctx, int l, uint16_t* dst) {
 
 Engine::Engine(const HostWeights& w, const EngineOptions& o) : opt_(o) {
     HostWeightsCtx ctx{&w};
-    init(w.config, w.max_seq, w.embedding.data(), w.positional.data(), fill_from_hostweights, &ctx);
+    opt_.arch = w.arch;
+    if (w.arch == kArchOpt && w.final_ln.size() != 2 * static_cast<size_t>(w.config.hidden_dim))
+        throw InputError("opt arch weights need the final LayerNorm (2 x hidden_dim)");
+    init(w.config, w.max_seq, w.embedding.data(), w.positional.data(), w.arch == kArchOpt ? w.final_ln.data() : nullptr,
+         fill_from_hostweights, &ctx);
 }
 
 Engine::Engine(const ModelConfig& c, uint64_t seed, int max_seq, bool rescale, const EngineOptions& o) : opt_(o) {
     ModelConfig cc = c;
     cc.validate();
     if (max_seq < 1) throw InputError("DecoderWeights: max_seq must be >= 1");
-    // draw on the GPU (bit-exact with the host generator, weights_gen.cu)
-    init(cc, max_seq, nullptr, nullptr, nullptr, nullptr);
+    // draw on the GPU (bit-exact with the host generator, weights_gen.cu);
+    // the kArchOpt vectors (a few d-sized draws per layer) on the host
+    std::vector<uint16_t> lnf;
+    if (opt_.arch == kArchOpt) {
+        lnf.resize(2 * static_cast<size_t>(cc.hidden_dim));
+        generate_final_ln(cc, seed, lnf.data());
+    }
+    init(cc, max_seq, nullptr, nullptr, lnf.empty() ? nullptr : lnf.data(), nullptr, nullptr);
     Impl& m = *impl_;
     gen_weights_plain(reinterpret_cast<uint16_t*>(m.emb), static_cast<size_t>(m.V) * m.d, mix_seed(seed, 0),
                       s_compute_);
@@ -224,6 +275,13 @@ Engine::Engine(const ModelConfig& c, uint64_t seed, int max_seq, bool rescale, c
         gen_weights_transposed(L + m.off.wproj, d, d, mix_seed(seed, base + 3), fac[3], rescale, s_compute_);
         gen_weights_transposed(L + m.off.w1, d, f, mix_seed(seed, base + 4), fac[4], rescale, s_compute_);
         gen_weights_transposed(L + m.off.w2, f, d, mix_seed(seed, base + 5), fac[5], rescale, s_compute_);
+        if (m.opt()) {
+            const size_t n = m.LE - m.off.bqkv;
+            std::vector<uint16_t> ex(m.LE);
+            generate_layer_extras(cfg_, seed, l, ex.data());
+            HC_CUDA(cudaMemcpyAsync(L + m.off.bqkv, ex.data() + m.off.bqkv, n * 2, cudaMemcpyHostToDevice, s_compute_));
+            HC_CUDA(cudaStreamSynchronize(s_compute_));  // ex is pageable and goes out of scope
+        }
     };
     for (int l = 0; l < (m.w_all ? m.L : m.Lw); ++l) {
         if (m.w_all) {
@@ -238,12 +296,14 @@ Engine::Engine(const ModelConfig& c, uint64_t seed, int max_seq, bool rescale, c
     HC_CUDA(cudaStreamSynchronize(s_compute_));
 }
 
-void Engine::init(const ModelConfig& c, int w_max_seq, const uint16_t* emb, const uint16_t* pos,
+void Engine::init(const ModelConfig& c, int w_max_seq, const uint16_t* emb, const uint16_t* pos, const uint16_t* lnf,
                   void (*fill_layer)(const void*, int, uint16_t*), const void* ctx) {
     cfg_ = c;
     cfg_.validate();
     impl_ = std::make_unique<Impl>();
     Impl& m = *impl_;
+    if (opt_.arch != kArchReference && opt_.arch != kArchOpt) throw InputError("Engine: unknown arch");
+    m.arch = opt_.arch;
     if (cfg_.hidden_dim % 64) throw InputError("Engine: hidden_dim must be a multiple of 64");
     if (cfg_.head_dim() != 64 && cfg_.head_dim() != 128) throw InputError("Engine: head_dim must be 64 or 128");
     if (cfg_.ffn_dim % 64) throw InputError("Engine: ffn_dim must be a multiple of 64");
@@ -262,7 +322,7 @@ void Engine::init(const ModelConfig& c, int w_max_seq, const uint16_t* emb, cons
     m.max_blocks = (m.max_seq + m.tpb - 1) / m.tpb;
     m.Lp = opt_.host_layers > 0 ? std::min(opt_.host_layers, m.L) : m.L;
     m.Lw = opt_.weight_layers > 0 ? std::min(opt_.weight_layers, m.L) : m.L;
-    m.off = LayerOffsets::of(cfg_);
+    m.off = LayerOffsets::of(cfg_, m.arch);
     m.LE = m.off.total;
     m.kvb = static_cast<size_t>(2) * m.d * m.tpb;
     m.actb = static_cast<size_t>(m.d) * m.tpb;
@@ -283,6 +343,12 @@ void Engine::init(const ModelConfig& c, int w_max_seq, const uint16_t* emb, cons
     m.pos = dalloc<bf16>(static_cast<size_t>(w_max_seq) * m.d);
     if (emb) HC_CUDA(cudaMemcpy(m.emb, emb, static_cast<size_t>(m.V) * m.d * 2, cudaMemcpyHostToDevice));
     if (pos) HC_CUDA(cudaMemcpy(m.pos, pos, static_cast<size_t>(w_max_seq) * m.d * 2, cudaMemcpyHostToDevice));
+    if (m.opt()) {
+        if (!lnf) throw InputError("Engine: opt arch needs the final LayerNorm");
+        m.lnf = dalloc<bf16>(2 * static_cast<size_t>(m.d));
+        HC_CUDA(cudaMemcpy(m.lnf, lnf, 2 * static_cast<size_t>(m.d) * 2, cudaMemcpyHostToDevice));
+        m.xn = dalloc<bf16>(static_cast<size_t>(m.B) * m.d);
+    }
 
     // weights (fill_layer == nullptr: the caller draws them on the device)
     if (opt_.weights_on_device) {
@@ -302,7 +368,7 @@ void Engine::init(const ModelConfig& c, int w_max_seq, const uint16_t* emb, cons
     // decode scratch
     m.x[0] = dalloc<bf16>(static_cast<size_t>(m.B) * m.d);
     m.x[1] = dalloc<bf16>(static_cast<size_t>(m.B) * m.d);
-    m.qkv = dalloc<bf16>(static_cast<size_t>(m.B) * 3 * m.d);
+    m.qkvb = dalloc<bf16>(static_cast<size_t>(m.B) * 3 * m.d);
     m.att = dalloc<bf16>(static_cast<size_t>(m.B) * m.d);
     m.proj = dalloc<bf16>(static_cast<size_t>(m.B) * m.d);
     m.hbuf = dalloc<bf16>(static_cast<size_t>(m.B) * m.f);
@@ -385,7 +451,7 @@ void Engine::forward_trace(const std::vector<int>& ids, uint16_t* layer_inputs, 
     std::memcpy(m.h_meta, meta.data(), meta.size() * 4);
     HC_CUDA(cudaMemcpyAsync(m.d_meta, m.h_meta, meta.size() * 4, cudaMemcpyHostToDevice, s_compute_));
     embed(m.emb, m.pos, m.d_meta, m.d_meta + T, T, m.d, m.px[0], m.d, s_compute_);
-    run_layers(T, 0, m.L, m.d_meta + 2 * T, layer_inputs, k, v, out);
+    run_layers(T, 0, m.L, m.d_meta + 2 * T, layer_inputs, k, v, out, true);
 }
 
 void Engine::layer_forward(int layer, const uint16_t* x, int T, uint16_t* k, uint16_t* v, uint16_t* out) {
@@ -399,7 +465,7 @@ void Engine::layer_forward(int layer, const uint16_t* x, int T, uint16_t* k, uin
     std::memcpy(m.h_meta, cu, sizeof cu);
     HC_CUDA(cudaMemcpyAsync(m.d_meta, m.h_meta, sizeof cu, cudaMemcpyHostToDevice, s_compute_));
     HC_CUDA(cudaMemcpyAsync(m.px[layer & 1], x, static_cast<size_t>(T) * m.d * 2, cudaMemcpyHostToDevice, s_compute_));
-    run_layers(T, layer, layer + 1, m.d_meta, nullptr, k, v, out);
+    run_layers(T, layer, layer + 1, m.d_meta, nullptr, k, v, out, false);
 }
 
 Engine::~Engine() {
@@ -408,10 +474,10 @@ Engine::~Engine() {
     cudaDeviceSynchronize();
     for (void* p : {(void*)m.emb, (void*)m.pos, (void*)m.w_all, (void*)m.wbuf[0], (void*)m.wbuf[1], (void*)m.kv_gpu,
                     (void*)m.act_gpu, (void*)m.kvr, (void*)m.kv_stage[0], (void*)m.kv_stage[1], (void*)m.act_stage[0],
-                    (void*)m.act_stage[1], (void*)m.x[0], (void*)m.x[1], (void*)m.qkv, (void*)m.att, (void*)m.proj,
+                    (void*)m.act_stage[1], (void*)m.x[0], (void*)m.x[1], (void*)m.qkvb, (void*)m.att, (void*)m.proj,
                     (void*)m.hbuf, (void*)m.logits, (void*)m.amax, (void*)m.attn_work, (void*)m.d_meta,
                     (void*)m.px[0], (void*)m.px[1], (void*)m.pqkv, (void*)m.patt, (void*)m.pproj, (void*)m.ph,
-                    (void*)m.tr_kv, (void*)m.splitk_ws})
+                    (void*)m.tr_kv, (void*)m.splitk_ws, (void*)m.lnf, (void*)m.xn, (void*)m.pxn})
         if (p) cudaFree(p);
     for (void* p : {(void*)m.h_w, (void*)m.kv_host, (void*)m.act_host, (void*)m.h_meta})
         if (p) cudaFreeHost(p);
@@ -431,7 +497,7 @@ Engine::~Engine() {
 // Causal forward of T rows (one sequence) through layers [l0, l1); the input
 // is in px[l0 & 1]; captures are [l1-l0][T][d] host arrays (optional).
 void Engine::run_layers(int T, int l0, int l1, const int* d_cu, uint16_t* layer_inputs, uint16_t* k, uint16_t* v,
-                        uint16_t* out) {
+                        uint16_t* out, bool final_ln) {
     Impl& m = *impl_;
     const size_t per = static_cast<size_t>(T) * m.d;
     std::vector<uint16_t> qkv_h((k || v) ? static_cast<size_t>(T) * 3 * m.d : 0);
@@ -448,7 +514,7 @@ void Engine::run_layers(int T, int l0, int l1, const int* d_cu, uint16_t* layer_
         bf16* xout = m.px[(l + 1) & 1];
         if (layer_inputs)
             HC_CUDA(cudaMemcpyAsync(layer_inputs + per * li, xin, per * 2, cudaMemcpyDeviceToHost, s_compute_));
-        gemm_rows(gemm::kStore, xin, T, m.d, W + m.off.wqkv, 3 * m.d, m.pqkv, 3 * m.d, s_compute_);
+        m.qkv(W, m.ln(W, 1, xin, T, m.pxn, s_compute_), T, m.pqkv, s_compute_);
         if (k || v) {
             HC_CUDA(cudaMemcpyAsync(qkv_h.data(), m.pqkv, qkv_h.size() * 2, cudaMemcpyDeviceToHost, s_compute_));
             HC_CUDA(cudaStreamSynchronize(s_compute_));
@@ -460,11 +526,10 @@ void Engine::run_layers(int T, int l0, int l1, const int* d_cu, uint16_t* layer_
         }
         prefill_attention(m.pqkv, m.patt, d_cu, 1, T, m.H, m.hd,
                           opt_.scaled ? 1.0f / std::sqrt(static_cast<float>(m.hd)) : 1.0f, s_compute_);
-        gemm_rows(gemm::kStore, m.patt, T, m.d, W + m.off.wproj, m.d, m.pproj, m.d, s_compute_);
-        gemm_rows(gemm::kRelu, m.pproj, T, m.d, W + m.off.w1, m.f, m.ph, m.f, s_compute_);
-        gemm_rows(gemm::kStore, m.ph, T, m.f, W + m.off.w2, m.d, xout, m.d, s_compute_);
+        m.tail(W, m.patt, xin, T, m.pproj, m.patt, m.ph, xout, s_compute_);
     }
-    if (out) HC_CUDA(cudaMemcpyAsync(out, m.px[l1 & 1], per * 2, cudaMemcpyDeviceToHost, s_compute_));
+    const bf16* y = final_ln ? m.final_norm(m.px[l1 & 1], T, m.pxn, s_compute_) : m.px[l1 & 1];
+    if (out) HC_CUDA(cudaMemcpyAsync(out, y, per * 2, cudaMemcpyDeviceToHost, s_compute_));
     HC_CUDA(cudaGetLastError());
     HC_CUDA(cudaStreamSynchronize(s_compute_));
 }
@@ -472,7 +537,7 @@ void Engine::run_layers(int T, int l0, int l1, const int* d_cu, uint16_t* layer_
 // ---------------------------------------------------------------------------
 // GEMM helpers (weights transposed [out][in]; see model.hpp)
 void gemm_rows(int epi, const bf16* A, int M, int K, const bf16* W, int N, void* out, long long ldc, cudaStream_t st,
-               long long lda, float* ws, size_t ws_floats) {
+               long long lda, float* ws, size_t ws_floats, const bf16* bias, const bf16* res, long long ldr) {
     GemmCall c;
     c.epi = epi;
     c.A = A;
@@ -487,6 +552,9 @@ void gemm_rows(int epi, const bf16* A, int M, int K, const bf16* W, int N, void*
     c.ldc = ldc;
     c.ws = ws;
     c.ws_floats = ws_floats;
+    c.bias = bias;
+    c.res = res;
+    c.ldr = ldr;
     run_gemm(c, st);
 }
 
@@ -612,9 +680,12 @@ void Engine::prefill(const std::vector<std::string>& ids, const std::vector<std:
         m.regions(l, slot, R);
         bf16* xin = m.px[l & 1];
         bf16* xout = m.px[(l + 1) & 1];
+        // the layer's GEMM input: x (reference arch) or LN1(x) (kArchOpt)
+        const bf16* xa = m.ln(W, 1, xin, T, m.pxn, s_compute_);
+        st.launches += m.opt();
         // activation-cache writer: this layer's input rows of every ACT block
         BlockScatter sa;
-        sa.src = xin;
+        sa.src = xa;
         sa.ld = m.d;
         sa.src_row = dm + o_as;
         sa.n_tok = dm + o_an;
@@ -631,7 +702,7 @@ void Engine::prefill(const std::vector<std::string>& ids, const std::vector<std:
             const bf16* cin = xin + static_cast<size_t>(c.row0) * m.d;
             bf16* cout = xout + static_cast<size_t>(c.row0) * m.d;
             m.span_begin(profile_, s_compute_, 2);
-            gemm_rows(gemm::kStore, cin, c.rows, m.d, W + m.off.wqkv, 3 * m.d, m.pqkv, 3 * m.d, s_compute_);
+            m.qkv(W, xa + static_cast<size_t>(c.row0) * m.d, c.rows, m.pqkv, s_compute_);
             m.span_end(profile_, s_compute_);
             BlockScatter sk = sa;
             sk.src = m.pqkv;
@@ -645,11 +716,9 @@ void Engine::prefill(const std::vector<std::string>& ids, const std::vector<std:
             prefill_attention(m.pqkv, m.patt, dm + c.o_cu, c.n, c.max_len, m.H, m.hd, scale, s_compute_);
             m.span_end(profile_, s_compute_);
             m.span_begin(profile_, s_compute_, 2);
-            gemm_rows(gemm::kStore, m.patt, c.rows, m.d, W + m.off.wproj, m.d, m.pproj, m.d, s_compute_);
-            gemm_rows(gemm::kRelu, m.pproj, c.rows, m.d, W + m.off.w1, m.f, m.ph, m.f, s_compute_);
-            gemm_rows(gemm::kStore, m.ph, c.rows, m.f, W + m.off.w2, m.d, cout, m.d, s_compute_);
+            m.tail(W, m.patt, cin, c.rows, m.pproj, m.patt, m.ph, cout, s_compute_);
             m.span_end(profile_, s_compute_);
-            st.launches += 5 + (sk.n_blocks > 0);
+            st.launches += 2 + m.tail_launches() + (sk.n_blocks > 0);
         }
         HC_CUDA(cudaEventRecord(m.consumed[slot], s_compute_));
         if (stores) {  // this layer's host blocks: staging slot -> pinned pool (copy engine, D2H)
@@ -906,7 +975,8 @@ void Engine::decode_step(const std::vector<std::string>& ids, const int* tokens,
             m.span_begin(profile_, s_compute_, 0);
             bf16* pin = m.px[l & 1];
             bf16* pout = m.px[(l + 1) & 1];
-            gemm_rows(gemm::kStore, pin, n_rc, m.d, W + m.off.wqkv, 3 * m.d, m.pqkv, 3 * m.d, s_compute_);
+            m.qkv(W, m.ln(W, 1, pin, n_rc, m.pxn, s_compute_), n_rc, m.pqkv, s_compute_);
+            st.launches += m.opt();
             BlockScatter sk;
             sk.src = m.pqkv;
             sk.ld = 3 * m.d;
@@ -922,10 +992,8 @@ void Engine::decode_step(const std::vector<std::string>& ids, const int* tokens,
             scatter_kv_blocks(sk, s_compute_);
             if (l + 1 < m.L) {  // the last layer's prefix output is never needed
                 prefill_attention(m.pqkv, m.patt, dm + o_rcu, n, rc_max, m.H, m.hd, scale, s_compute_);
-                gemm_rows(gemm::kStore, m.patt, n_rc, m.d, W + m.off.wproj, m.d, m.pproj, m.d, s_compute_);
-                gemm_rows(gemm::kRelu, m.pproj, n_rc, m.d, W + m.off.w1, m.f, m.ph, m.f, s_compute_);
-                gemm_rows(gemm::kStore, m.ph, n_rc, m.f, W + m.off.w2, m.d, pout, m.d, s_compute_);
-                st.launches += 4;
+                m.tail(W, m.patt, pin, n_rc, m.pproj, m.patt, m.ph, pout, s_compute_);
+                st.launches += 1 + m.tail_launches();
             }
             st.launches += 2;
             st.recompute_tokens += n_rc;
@@ -934,6 +1002,9 @@ void Engine::decode_step(const std::vector<std::string>& ids, const int* tokens,
         if (capture_inputs_)
             HC_CUDA(cudaMemcpyAsync(captured_.data() + static_cast<size_t>(l) * n * m.d, xin,
                                     static_cast<size_t>(n) * m.d * 2, cudaMemcpyDeviceToHost, s_compute_));
+        // the layer's GEMM input (and ACT payload): x, or LN1(x) for kArchOpt
+        const bf16* xa = m.ln(W, 1, xin, n, m.xn, s_compute_);
+        st.launches += m.opt();
         AppendCall ap;
         std::copy(R, R + 16, ap.region);
         ap.B = n;
@@ -943,7 +1014,7 @@ void Engine::decode_step(const std::vector<std::string>& ids, const int* tokens,
         ap.tpb = m.tpb;
         ap.tok = dm + o_t;
         if (any_act) {  // ACT writer: X of the new token -> its ACT slot (device + host)
-            ap.src = xin;
+            ap.src = xa;
             ap.ld = m.d;
             ap.dev_ref = dm + o_ad;
             ap.host_ref = dm + o_ah;
@@ -972,6 +1043,7 @@ void Engine::decode_step(const std::vector<std::string>& ids, const int* tokens,
             c.d = m.d;
             c.hd = m.hd;
             c.blk_off = which == 0 ? static_cast<int>(m.act_gpu_cap) : 0;
+            c.bias = m.bias(W, m.off.bqkv + m.d);  // [b_k | b_v]
             m.span_begin(profile_, s_compute_, 0);
             run_gemm(c, s_compute_);
             m.span_end(profile_, s_compute_);
@@ -979,10 +1051,10 @@ void Engine::decode_step(const std::vector<std::string>& ids, const int* tokens,
             st.recompute_tokens += static_cast<double>(tl.size()) * gemm::BM;
         }
         m.span_begin(profile_, s_compute_, 2);
-        gemm_rows(gemm::kStore, xin, n, m.d, W + m.off.wqkv, 3 * m.d, m.qkv, 3 * m.d, s_compute_, 0, m.splitk_ws, m.splitk_floats);
+        m.qkv(W, xa, n, m.qkvb, s_compute_, m.splitk_ws, m.splitk_floats);
         m.span_end(profile_, s_compute_);
         if (any_kv) {  // new token's K|V -> its KV slot (device + host)
-            ap.src = m.qkv;
+            ap.src = m.qkvb;
             ap.ld = 3 * m.d;
             ap.dev_ref = dm + o_kd;
             ap.host_ref = dm + o_kh;
@@ -990,7 +1062,7 @@ void Engine::decode_step(const std::vector<std::string>& ids, const int* tokens,
             st.launches += 1;
         }
         AttnCall a;
-        a.q = m.qkv;
+        a.q = m.qkvb;
         a.ldq = 3 * m.d;
         a.out = m.att;
         a.blk_ref = dm + o_ref;
@@ -1009,14 +1081,13 @@ void Engine::decode_step(const std::vector<std::string>& ids, const int* tokens,
         decode_attention(a, s_compute_);
         m.span_end(profile_, s_compute_);
         m.span_begin(profile_, s_compute_, 2);
-        gemm_rows(gemm::kStore, m.att, n, m.d, W + m.off.wproj, m.d, m.proj, m.d, s_compute_, 0, m.splitk_ws, m.splitk_floats);
-        gemm_rows(gemm::kRelu, m.proj, n, m.d, W + m.off.w1, m.f, m.hbuf, m.f, s_compute_, 0, m.splitk_ws, m.splitk_floats);
-        gemm_rows(gemm::kStore, m.hbuf, n, m.f, W + m.off.w2, m.d, xout, m.d, s_compute_, 0, m.splitk_ws, m.splitk_floats);
+        m.tail(W, m.att, xin, n, m.proj, m.att, m.hbuf, xout, s_compute_, m.splitk_ws, m.splitk_floats);
         m.span_end(profile_, s_compute_);
-        st.launches += 4 + (splits > 1 ? 2 : 1);
+        st.launches += 1 + m.tail_launches() + (splits > 1 ? 2 : 1);
         HC_CUDA(cudaEventRecord(m.consumed[slot], s_compute_));
     }
-    bf16* xf = m.x[m.L & 1];
+    const bf16* xf = m.final_norm(m.x[m.L & 1], n, m.xn, s_compute_);
+    st.launches += m.opt();
     if (logits_out || argmax_out) {
         gemm_rows(gemm::kF32, xf, n, m.d, m.emb, m.V, m.logits, m.V, s_compute_);
         st.launches += 1;
@@ -1092,6 +1163,9 @@ void Engine::read_weights(int layer, uint16_t* out) {
         HC_CUDA(cudaMemcpy(out, m.emb, static_cast<size_t>(m.V) * m.d * 2, cudaMemcpyDeviceToHost));
     } else if (layer == -2) {
         HC_CUDA(cudaMemcpy(out, m.pos, static_cast<size_t>(m.max_seq) * m.d * 2, cudaMemcpyDeviceToHost));
+    } else if (layer == -3) {
+        if (!m.opt()) throw InputError("read_weights: the reference arch has no final LayerNorm");
+        HC_CUDA(cudaMemcpy(out, m.lnf, 2 * static_cast<size_t>(m.d) * 2, cudaMemcpyDeviceToHost));
     } else if (layer >= 0 && layer < m.L) {
         if (m.w_all)
             HC_CUDA(cudaMemcpy(out, m.w_all + static_cast<size_t>(layer) * m.LE, m.LE * 2, cudaMemcpyDeviceToHost));
@@ -1152,6 +1226,7 @@ double Engine::time_kv_gen(int n_tokens, int reps) {
     c.tpb = m.tpb;
     c.d = m.d;
     c.hd = m.hd;
+    c.bias = m.bias(W, m.off.bqkv + m.d);
     run_gemm(c, s_compute_);  // warm-up
     HC_CUDA(cudaEventRecord(m.ev0, s_compute_));
     for (int i = 0; i < reps; ++i) run_gemm(c, s_compute_);

@@ -52,6 +52,7 @@ struct EngineOptions {
     int scaled = 1;
     int max_prefill_tokens = 65536;
     int device = 0;
+    int arch = kArchReference;    // decoder layer variant (host/model.hpp); from the weights when given
 };
 
 struct StepStats {
@@ -118,7 +119,8 @@ public:
     // ACT: [tpb][d]) — for parity tests of the cache writers.
     void read_block(BlockKind kind, Location loc, int pbn, int layer, uint16_t* out);
     // Engine-held weights (bf16 bits): layer >= 0 packed layer (model.hpp
-    // layout), -1 embedding [V x d], -2 positional [max_seq x d].
+    // layout), -1 embedding [V x d], -2 positional [max_seq x d], -3 final
+    // LayerNorm gamma|beta [2d] (kArchOpt).
     void read_weights(int layer, uint16_t* out);
     // Decode-time layer inputs of the last step: [L][n][d] (debug / parity).
     void set_capture_layer_inputs(bool on) { capture_inputs_ = on; }
@@ -143,10 +145,10 @@ public:
 
 private:
     struct Impl;
-    void init(const ModelConfig& c, int max_seq, const uint16_t* emb, const uint16_t* pos,
+    void init(const ModelConfig& c, int max_seq, const uint16_t* emb, const uint16_t* pos, const uint16_t* final_ln,
               void (*fill_layer)(const void* ctx, int l, uint16_t* dst), const void* ctx);
     void run_layers(int T, int l0, int l1, const int* d_cu, uint16_t* layer_inputs, uint16_t* k, uint16_t* v,
-                    uint16_t* out);
+                    uint16_t* out, bool final_ln);
     std::unique_ptr<Impl> impl_;
     ModelConfig cfg_;
     EngineOptions opt_;

@@ -2,6 +2,7 @@
 
 #include <cmath>
 #include <cstring>
+#include <string>
 #include <thread>
 
 #include "host/errors.hpp"
@@ -71,7 +72,7 @@ void rescale_factors(const ModelConfig& c, double out[6]) {
     out[5] = 10.0 * std::sqrt(3.0 * std::sqrt(2.0) / f);
 }
 
-LayerOffsets LayerOffsets::of(const ModelConfig& c) {
+LayerOffsets LayerOffsets::of(const ModelConfig& c, int arch) {
     const size_t d = c.hidden_dim, f = c.ffn_dim;
     LayerOffsets o;
     o.wqkv = 0;
@@ -79,10 +80,23 @@ LayerOffsets LayerOffsets::of(const ModelConfig& c) {
     o.w1 = o.wproj + d * d;
     o.w2 = o.w1 + f * d;
     o.total = o.w2 + d * f;
+    if (arch == kArchOpt) {
+        o.bqkv = o.total;
+        o.bproj = o.bqkv + 3 * d;
+        o.b1 = o.bproj + d;
+        o.b2 = o.b1 + f;
+        o.ln1g = o.b2 + d;
+        o.ln1b = o.ln1g + d;
+        o.ln2g = o.ln1b + d;
+        o.ln2b = o.ln2g + d;
+        o.total = o.ln2b + d;
+    } else if (arch != kArchReference) {
+        throw InputError("unknown model arch: " + std::to_string(arch));
+    }
     return o;
 }
 
-size_t HostWeights::layer_elems() const { return LayerOffsets::of(config).total; }
+size_t HostWeights::layer_elems() const { return LayerOffsets::of(config, arch).total; }
 
 namespace {
 
@@ -154,6 +168,30 @@ void generate_layer(const ModelConfig& c, uint64_t seed, int l, bool rescale, ui
     draw_transposed(L + off.w2, f, d, mix_seed(seed, base + 5), fac[5]);
 }
 
+namespace {
+// n draws of stream `seed`; entries in blocks [k*blk, (k+1)*blk) with k even get +1
+// (LayerNorm gammas), the others stay raw (betas / biases when blk == 0)
+void draw_vec(uint16_t* dst, size_t n, uint64_t seed, size_t blk) {
+    for (size_t i = 0; i < n; ++i) {
+        const uint64_t z = SplitMix64::mix(seed + (i + 1) * 0x9e3779b97f4a7c15ULL);
+        const double u = -0.1 + (0.1 - -0.1) * (static_cast<double>(z >> 11) * 0x1.0p-53);
+        dst[i] = to_bf16(blk && (i / blk) % 2 == 0 ? 1.0 + u : u);
+    }
+}
+}  // namespace
+
+void generate_layer_extras(const ModelConfig& c, uint64_t seed, int l, uint16_t* L) {
+    const size_t d = c.hidden_dim, f = c.ffn_dim;
+    const LayerOffsets off = LayerOffsets::of(c, kArchOpt);
+    const uint64_t base = 100 + static_cast<uint64_t>(l) * 8;
+    draw_vec(L + off.bqkv, 5 * d + f, mix_seed(seed, base + 6), 0);  // b_qkv | b_o | b_1 | b_2 (contiguous)
+    draw_vec(L + off.ln1g, 4 * d, mix_seed(seed, base + 7), d);      // g1 | b1 | g2 | b2
+}
+
+void generate_final_ln(const ModelConfig& c, uint64_t seed, uint16_t* dst) {
+    draw_vec(dst, 2 * static_cast<size_t>(c.hidden_dim), mix_seed(seed, 2), c.hidden_dim);
+}
+
 HostWeights generate_weights(const ModelConfig& config, uint64_t seed, int max_seq, bool rescale) {
     ModelConfig c = config;
     c.validate();
@@ -195,6 +233,35 @@ HostWeights weights_from_f64(const ModelConfig& config, int max_seq, const doubl
         put_t(L + off.w1, t[4], d, f);
         put_t(L + off.w2, t[5], f, d);
     }
+    return w;
+}
+
+HostWeights weights_from_f64_opt(const ModelConfig& config, int max_seq, const double* emb, const double* pos,
+                                 const double* const* layer_tensors, const double* const* layer_extras,
+                                 const double* final_ln) {
+    if (!layer_extras || !final_ln) throw InputError("opt arch needs layer extras and the final LayerNorm");
+    HostWeights ref = weights_from_f64(config, max_seq, emb, pos, layer_tensors);
+    HostWeights w;
+    w.config = ref.config;
+    w.arch = kArchOpt;
+    w.max_seq = max_seq;
+    w.embedding = std::move(ref.embedding);
+    w.positional = std::move(ref.positional);
+    const LayerOffsets r = LayerOffsets::of(w.config), o = LayerOffsets::of(w.config, kArchOpt);
+    const size_t d = w.config.hidden_dim, f = w.config.ffn_dim;
+    w.layers.resize(o.total * w.config.num_layers);
+    for (int l = 0; l < w.config.num_layers; ++l) {
+        uint16_t* L = w.layer(l);
+        std::memcpy(L, ref.layers.data() + r.total * l, r.total * 2);
+        const double* const* e = layer_extras + 10 * l;
+        const size_t dst[10] = {o.bqkv, o.bqkv + d, o.bqkv + 2 * d, o.bproj, o.b1, o.b2, o.ln1g, o.ln1b, o.ln2g, o.ln2b};
+        for (int k = 0; k < 10; ++k) {
+            const size_t n = k == 4 ? f : d;
+            for (size_t i = 0; i < n; ++i) L[dst[k] + i] = to_bf16(e[k][i]);
+        }
+    }
+    w.final_ln.resize(2 * d);
+    for (size_t i = 0; i < 2 * d; ++i) w.final_ln[i] = to_bf16(final_ln[i]);
     return w;
 }
 

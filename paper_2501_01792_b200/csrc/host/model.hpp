@@ -54,22 +54,46 @@ double from_bf16(uint16_t b);
 // Per-tensor rescale factors (index: 0 q,1 k,2 v,3 proj,4 ffn1,5 ffn2).
 void rescale_factors(const ModelConfig& c, double out[6]);
 
+// Model architecture of the decoder layer.
+//   kArchReference: exactly the reference (decoder.cpp:97-129): no bias,
+//                   no LayerNorm, no residual.
+//   kArchOpt:       OPT (pre-LN): x^ = LN1(x); q,k,v = x^ W + b; x' = x +
+//                   attn W_o + b_o; x_next = x' + relu(LN2(x') W1 + b1) W2 + b2;
+//                   model output LN_f(x_L). The activation cache stores x^
+//                   (the GEMM input of K|V), so the recompute stays
+//                   K|V = x^ [W_k|W_v] + [b_k|b_v]. Not in the reference: its
+//                   parity is pinned only by the oracle's restatement.
+enum Arch : int { kArchReference = 0, kArchOpt = 1 };
+
+// Extras of kArchOpt (bf16, drawn like the matrices: one SplitMix64 stream
+// per tag, U(-0.1, 0.1); tags the reference leaves unused):
+//   layer l, tag 100+8l+6: b_q | b_k | b_v | b_o | b_1 [f] | b_2   (raw draws)
+//   layer l, tag 100+8l+7: u -> gamma1 = 1+u | beta1 = u | gamma2 = 1+u | beta2 = u
+//   tag 2 (final LayerNorm): gamma_f = 1+u | beta_f = u
+constexpr double kLnEps = 1e-5;
+
 // Host copy of the bf16 weights in device layout.
 struct HostWeights {
     ModelConfig config;
+    int arch = kArchReference;
+    std::vector<uint16_t> final_ln;    // kArchOpt: gamma_f | beta_f [2d]
     int max_seq = 0;
     std::vector<uint16_t> embedding;   // [vocab x d] (also the tied LM head, K-major)
     std::vector<uint16_t> positional;  // [max_seq x d]
     std::vector<uint16_t> layers;      // L x layer_elems(), packed as documented above
-    size_t layer_elems() const;
+    size_t layer_elems() const;  // LayerOffsets::of(config, arch).total
     uint16_t* layer(int l) { return layers.data() + static_cast<size_t>(l) * layer_elems(); }
     const uint16_t* layer(int l) const { return layers.data() + static_cast<size_t>(l) * layer_elems(); }
 };
 
-// Offsets (elements) of each matrix inside a packed layer.
+// Offsets (elements) of each tensor inside a packed layer. kArchOpt appends
+// b_qkv [3d] | b_o [d] | b_1 [f] | b_2 [d] | gamma1 | beta1 | gamma2 | beta2 [d]
+// (all 16-byte aligned: d, f are multiples of 64).
 struct LayerOffsets {
-    size_t wqkv, wproj, w1, w2, total;
-    static LayerOffsets of(const ModelConfig& c);
+    size_t wqkv, wproj, w1, w2;
+    size_t bqkv = 0, bproj = 0, b1 = 0, b2 = 0, ln1g = 0, ln1b = 0, ln2g = 0, ln2b = 0;
+    size_t total;
+    static LayerOffsets of(const ModelConfig& c, int arch = kArchReference);
 };
 
 // DecoderWeights::generate (model.cpp:94-117) + rescale + bf16 + transpose.
@@ -81,11 +105,20 @@ HostWeights generate_weights(const ModelConfig& config, uint64_t seed, int max_s
 // straight into pinned / staging memory): one packed layer, or the two tables.
 void generate_layer(const ModelConfig& config, uint64_t seed, int layer, bool rescale, uint16_t* dst);
 void generate_tables(const ModelConfig& config, uint64_t seed, int max_seq, uint16_t* emb, uint16_t* pos);
+// kArchOpt extras: dst = packed layer base (writes from LayerOffsets::bqkv on);
+// final LayerNorm gamma_f | beta_f into dst [2d].
+void generate_layer_extras(const ModelConfig& config, uint64_t seed, int layer, uint16_t* layer_base);
+void generate_final_ln(const ModelConfig& config, uint64_t seed, uint16_t* dst);
 
 // Build from externally supplied fp64 tensors in the reference layout
 // ([in x out], row-major): emb [V x d], pos [S x d], per layer q,k,v,proj
 // [d x d], ffn1 [d x f], ffn2 [f x d].
 HostWeights weights_from_f64(const ModelConfig& config, int max_seq, const double* emb, const double* pos,
                              const double* const* layer_tensors /* L*6 pointers */);
+// kArchOpt: + layer_extras (L*10 pointers: b_q, b_k, b_v, b_o [d], b_1 [f],
+// b_2, gamma1, beta1, gamma2, beta2 [d]) and final_ln (gamma_f | beta_f [2d]).
+HostWeights weights_from_f64_opt(const ModelConfig& config, int max_seq, const double* emb, const double* pos,
+                                 const double* const* layer_tensors, const double* const* layer_extras,
+                                 const double* final_ln);
 
 }  // namespace hc

@@ -172,6 +172,14 @@ void run_gemm(const GemmCall& c, cudaStream_t st) {
     p.d = c.d;
     p.hd = c.hd;
     p.blk_off = c.blk_off;
+    if ((c.bias || c.res) && (c.epi == gemm::kF32 || c.epi == gemm::kSplitF32))
+        throw std::invalid_argument("gemm: bias / residual apply to bf16 epilogues only");
+    if ((c.bias && reinterpret_cast<uintptr_t>(c.bias) % 16) ||
+        (c.res && (reinterpret_cast<uintptr_t>(c.res) % 16 || (c.ldr * 2) % 16)))
+        throw std::invalid_argument("gemm: bias / residual must be 16-byte aligned");
+    p.bias = c.bias;
+    p.res = c.res;
+    p.ldr = c.ldr;
     p.group_m = c.group_m > 0 ? c.group_m : (c.K <= 4096 ? 32 : 16);
     if (const char* g = std::getenv("HC_GEMM_GROUP_M")) p.group_m = std::max(1, std::atoi(g));  // tuning knob
     p.splits = 1;
@@ -195,6 +203,8 @@ void run_gemm(const GemmCall& c, cudaStream_t st) {
             p.splits = (num_kb + p.kb_per_split - 1) / p.kb_per_split;
             p.out = c.ws;
             p.ldc = c.N;
+            p.bias = nullptr;  // applied once, by the reduce
+            p.res = nullptr;
             cc.epi = gemm::kSplitF32;
         }
     }
@@ -226,7 +236,9 @@ void run_gemm(const GemmCall& c, cudaStream_t st) {
         case 256: dispatch_epi<256>(cc, p, st); break;
         default: throw std::invalid_argument("gemm: bn must be 32/64/128/256");
     }
-    if (p.splits > 1) splitk_reduce(c.ws, p.splits, c.M, c.N, static_cast<bf16*>(c.out), c.epi == gemm::kRelu, st);
+    if (p.splits > 1)
+        splitk_reduce(c.ws, p.splits, c.M, c.N, static_cast<bf16*>(c.out), c.epi == gemm::kRelu, st, c.bias, c.res,
+                      c.ldr);
 }
 
 }  // namespace hc

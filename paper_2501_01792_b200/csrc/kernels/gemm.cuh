@@ -41,6 +41,11 @@ struct Params {
     // [s*kb_per_split, (s+1)*kb_per_split) and writes fp32 partials to
     // out + (s*M + row)*ldc
     int splits, kb_per_split;
+    // optional epilogue operands (bf16; applied before relu, not to fp32 outputs):
+    // C[m][n] += bias[n] + res[m * ldr + n]
+    const __nv_bfloat16* bias;
+    const __nv_bfloat16* res;
+    long long ldr;
 };
 
 template <int BN>
@@ -68,6 +73,22 @@ __device__ __forceinline__ void tile_coords(int tile, const Params& p, int& m_id
     n_idx = within / gm;
 }
 
+// acc[0..16) += 16 consecutive bf16 at src (32-byte aligned run)
+__device__ __forceinline__ void add16(float (&acc)[16], const __nv_bfloat16* src) {
+    const uint4* s4 = reinterpret_cast<const uint4*>(src);
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+        const uint4 u = __ldg(s4 + q);
+        const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const float2 f = __bfloat1622float2(h2[i]);
+            acc[8 * q + 2 * i] += f.x;
+            acc[8 * q + 2 * i + 1] += f.y;
+        }
+    }
+}
+
 template <int BN, int EPI>
 __device__ __forceinline__ void epilogue_chunk(const Params& p, int row, int col, int split, const uint32_t (&v)[16]) {
     if (row >= p.M || col >= p.N) return;
@@ -77,10 +98,15 @@ __device__ __forceinline__ void epilogue_chunk(const Params& p, int row, int col
         for (int j = 0; j < 16; j += 4) ptx::st_global_v4(dst + j, v[j], v[j + 1], v[j + 2], v[j + 3]);
         return;
     } else {
+        float add[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) add[j] = 0.f;
+        if (p.bias) add16(add, p.bias + col);
+        if (p.res) add16(add, p.res + static_cast<long long>(row) * p.ldr + col);
         uint32_t h[8];
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-            float a = __uint_as_float(v[2 * j]), b = __uint_as_float(v[2 * j + 1]);
+            float a = __uint_as_float(v[2 * j]) + add[2 * j], b = __uint_as_float(v[2 * j + 1]) + add[2 * j + 1];
             if constexpr (EPI == kRelu) {
                 a = fmaxf(a, 0.f);
                 b = fmaxf(b, 0.f);

@@ -30,9 +30,16 @@ struct GemmCall {
     float* ws = nullptr;         // split-K workspace (fp32); null disables split-K
     size_t ws_floats = 0;
     int splits = 0;              // 0 = planner (pick_split), else forced split count
+    // bf16 epilogue operands (kStore / kRelu / kKvPaged): C += bias[n] + res[m*ldr + n]
+    // before relu (OPT linear biases and residual connections)
+    const bf16* bias = nullptr;
+    const bf16* res = nullptr;
+    long long ldr = 0;
 };
-// out[m][n] = bf16(epi(sum_s ws[s][m][n])) — the split-K finish (relu optional)
-void splitk_reduce(const float* ws, int splits, int M, int N, bf16* out, bool relu, cudaStream_t st);
+// out[m][n] = bf16(epi(sum_s ws[s][m][n] + bias[n] + res[m*ldr + n])) — the
+// split-K finish (relu, bias, res optional)
+void splitk_reduce(const float* ws, int splits, int M, int N, bf16* out, bool relu, cudaStream_t st,
+                   const bf16* bias = nullptr, const bf16* res = nullptr, long long ldr = 0);
 void run_gemm(const GemmCall& c, cudaStream_t st);
 int num_sms();
 
@@ -104,6 +111,11 @@ struct BlockScatter {
 };
 void scatter_act_blocks(const BlockScatter& c, cudaStream_t st);
 void scatter_kv_blocks(const BlockScatter& c, cudaStream_t st);
+
+// y[r] = (x[r] - mean_r) / sqrt(var_r + eps) * gamma + beta over rows r < n of
+// width d (kArchOpt LayerNorms); bf16 in/out, fp32 statistics.
+void layernorm_rows(const bf16* x, long long ldx, const bf16* gamma, const bf16* beta, bf16* y, long long ldy, int n,
+                    int d, float eps, cudaStream_t st);
 
 // argmax over each row of fp32 logits [B x V]
 void argmax_rows(const float* logits, int B, int V, int* out, cudaStream_t st);

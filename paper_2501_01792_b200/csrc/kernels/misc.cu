@@ -153,8 +153,21 @@ __global__ void argmax_kernel(const float* __restrict__ logits, int V, int* __re
 }
 
 // 8 columns per thread; partial s of element (m, n) at ws[(s*M + m)*N + n]
+// acc[0..8) += 8 consecutive bf16 at src (16-byte aligned)
+__device__ __forceinline__ void add8(float (&acc)[8], const bf16* src) {
+    const uint4 u = __ldg(reinterpret_cast<const uint4*>(src));
+    const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const float2 f = __bfloat1622float2(h2[i]);
+        acc[2 * i] += f.x;
+        acc[2 * i + 1] += f.y;
+    }
+}
+
 __global__ void splitk_reduce_kernel(const float* __restrict__ ws, int splits, int M, int N, bf16* __restrict__ out,
-                                     int relu) {
+                                     int relu, const bf16* __restrict__ bias, const bf16* __restrict__ res,
+                                     long long ldr) {
     const size_t n8 = static_cast<size_t>(M) * N / 8;
     const size_t plane = static_cast<size_t>(M) * N;
     for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n8;
@@ -166,6 +179,10 @@ __global__ void splitk_reduce_kernel(const float* __restrict__ ws, int splits, i
             acc[0] += a.x; acc[1] += a.y; acc[2] += a.z; acc[3] += a.w;
             acc[4] += b.x; acc[5] += b.y; acc[6] += b.z; acc[7] += b.w;
         }
+        const size_t e0 = i * 8;
+        const int col = static_cast<int>(e0 % N);
+        if (bias) add8(acc, bias + col);
+        if (res) add8(acc, res + static_cast<long long>(e0 / N) * ldr + col);
         uint32_t o[4];
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
@@ -192,7 +209,83 @@ __global__ void fill_pattern_kernel(bf16* dst, size_t n, uint64_t seed, float am
     }
 }
 
+// LayerNorm of one row per CTA (256 threads): the row stays in registers
+// (8 bf16 per 16-byte chunk, <= kLnChunks chunks per thread), two-pass fp32
+// mean / variance with warp-shuffle + smem block reductions.
+constexpr int kLnThreads = 256, kLnChunks = 8;  // d <= 16384
+
+__device__ __forceinline__ float block_sum(float v, float* red) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    const int w = threadIdx.x / 32, lane = threadIdx.x % 32;
+    __syncthreads();  // red[] reuse across calls
+    if (lane == 0) red[w] = v;
+    __syncthreads();
+    float t = lane < kLnThreads / 32 ? red[lane] : 0.f;
+#pragma unroll
+    for (int o = 4; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    return t;
+}
+
+__global__ void __launch_bounds__(kLnThreads)
+    layernorm_kernel(const bf16* __restrict__ x, long long ldx, const bf16* __restrict__ g,
+                     const bf16* __restrict__ b, bf16* __restrict__ y, long long ldy, int d, float eps) {
+    __shared__ float red[kLnThreads / 32];
+    const bf16* xr = x + blockIdx.x * ldx;
+    const int nch = d / 8;
+    float v[kLnChunks][8];
+    float s = 0.f;
+#pragma unroll
+    for (int k = 0; k < kLnChunks; ++k) {
+        const int ch = threadIdx.x + k * kLnThreads;
+        if (ch < nch) {
+            const uint4 u = __ldg(reinterpret_cast<const uint4*>(xr) + ch);
+            const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const float2 f = __bfloat1622float2(h[i]);
+                v[k][2 * i] = f.x;
+                v[k][2 * i + 1] = f.y;
+                s += f.x + f.y;
+            }
+        }
+    }
+    const float mean = block_sum(s, red) / d;
+    float q = 0.f;
+#pragma unroll
+    for (int k = 0; k < kLnChunks; ++k)
+        if (threadIdx.x + k * kLnThreads < nch)
+#pragma unroll
+            for (int i = 0; i < 8; ++i) q += (v[k][i] - mean) * (v[k][i] - mean);
+    const float rstd = rsqrtf(block_sum(q, red) / d + eps);
+    bf16* yr = y + blockIdx.x * ldy;
+#pragma unroll
+    for (int k = 0; k < kLnChunks; ++k) {
+        const int ch = threadIdx.x + k * kLnThreads;
+        if (ch < nch) {
+            const uint4 gu = __ldg(reinterpret_cast<const uint4*>(g) + ch);
+            const uint4 bu = __ldg(reinterpret_cast<const uint4*>(b) + ch);
+            const __nv_bfloat162* gh = reinterpret_cast<const __nv_bfloat162*>(&gu);
+            const __nv_bfloat162* bh = reinterpret_cast<const __nv_bfloat162*>(&bu);
+            uint32_t o[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const float2 gf = __bfloat1622float2(gh[i]), bf = __bfloat1622float2(bh[i]);
+                o[i] = ptx::pack_bf16x2((v[k][2 * i] - mean) * rstd * gf.x + bf.x,
+                                        (v[k][2 * i + 1] - mean) * rstd * gf.y + bf.y);
+            }
+            reinterpret_cast<uint4*>(yr)[ch] = make_uint4(o[0], o[1], o[2], o[3]);
+        }
+    }
+}
+
 }  // namespace
+
+void layernorm_rows(const bf16* x, long long ldx, const bf16* gamma, const bf16* beta, bf16* y, long long ldy, int n,
+                    int d, float eps, cudaStream_t st) {
+    if (d % 8 || d > kLnThreads * kLnChunks * 8) throw std::invalid_argument("layernorm: d must be a multiple of 8, <= 16384");
+    if (n > 0) layernorm_kernel<<<n, kLnThreads, 0, st>>>(x, ldx, gamma, beta, y, ldy, d, eps);
+}
 
 void embed(const bf16* E, const bf16* Pos, const int* ids, const int* pos, int n, int d, bf16* X,
            long long ldx, cudaStream_t st) {
@@ -221,11 +314,12 @@ void argmax_rows(const float* logits, int B, int V, int* out, cudaStream_t st) {
     if (B > 0) argmax_kernel<<<B, 256, 0, st>>>(logits, V, out);
 }
 
-void splitk_reduce(const float* ws, int splits, int M, int N, bf16* out, bool relu, cudaStream_t st) {
+void splitk_reduce(const float* ws, int splits, int M, int N, bf16* out, bool relu, cudaStream_t st,
+                   const bf16* bias, const bf16* res, long long ldr) {
     if (N % 8) throw std::invalid_argument("splitk_reduce: N must be a multiple of 8");
     const size_t n8 = static_cast<size_t>(M) * N / 8;
     const int blocks = static_cast<int>(std::min<size_t>((n8 + 255) / 256, 4 * static_cast<size_t>(num_sms())));
-    if (n8) splitk_reduce_kernel<<<blocks, 256, 0, st>>>(ws, splits, M, N, out, relu ? 1 : 0);
+    if (n8) splitk_reduce_kernel<<<blocks, 256, 0, st>>>(ws, splits, M, N, out, relu ? 1 : 0, bias, res, ldr);
 }
 
 void fill_pattern(bf16* dst, size_t n, uint64_t seed, float amp, cudaStream_t st) {

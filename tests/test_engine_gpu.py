@@ -310,3 +310,100 @@ def test_engine_chunked_offloaded_prefill_matches_oracle(native, weights_on_devi
     for b, p in enumerate(prompts):
         ref = O.forward_prompt(p + [toks[b]], w).output[-1]
         assert rel(f64(res["x"][b]), ref) <= TOL
+
+
+# ---------------------------------------------------------------- OPT arch ---
+def opt_weights(cfg, seed=42, max_seq=128):
+    return O.with_opt_extras(oracle_weights(cfg, seed, max_seq), seed)
+
+
+def make_opt_engine(cfg, w, **kw):
+    from paper_2501_01792_b200.api import Engine, ModelConfig
+    mc = ModelConfig(num_layers=cfg.num_layers, hidden_dim=cfg.hidden_dim, num_heads=cfg.num_heads,
+                     ffn_dim=cfg.ffn_dim, vocab_size=cfg.vocab_size, tokens_per_block=cfg.tokens_per_block)
+    wd = dict(as_engine_weights(w), extras=w.extras, final_ln=w.final_ln)
+    return Engine(mc, weights=wd, arch="opt", **kw)
+
+
+@pytest.mark.parametrize("weights_on_device", [True, False])
+def test_engine_opt_arch_matches_oracle(native, weights_on_device):
+    """OPT decoder-layer variant (biases, pre-LN, residuals, final LN; §8(f)
+    rank 4): hybrid offloaded prefill + batched decode equal the oracle's
+    forward_prompt_opt; ACT blocks hold LN1(x), KV blocks x^ W + b, and the
+    recompute (with [b_k|b_v] in the GEMM epilogue) reproduces them."""
+    from paper_2501_01792_b200.api import HostAllocation, PoolCaps
+    cfg = small_cfg(L=3, d=256, H=2, f=512, tpb=8)
+    w = opt_weights(cfg)
+    rng = np.random.default_rng(21)
+    lens = [29, 40, 13]
+    prompts = [rng.integers(0, cfg.vocab_size, n).tolist() for n in lens]
+    ids = [f"o{i}" for i in range(len(lens))]
+    eng = make_opt_engine(cfg, w, max_batch=len(lens), caps=PoolCaps(kv_host=24, act_host=24, act_gpu=2),
+                          allocation=HostAllocation(1, 1), mode="hybrid", weights_on_device=weights_on_device,
+                          max_prefill_tokens=50)
+    eng.prefill(ids, prompts)
+    tpb, d = cfg.tokens_per_block, cfg.hidden_dim
+    for rid, p in zip(ids, prompts):
+        tr = O.forward_prompt_opt(p, w)
+        row = 0
+        for e in eng.cache.table(rid).entries:
+            n = e.filled_tokens
+            for l in range(cfg.num_layers):
+                blk = f64(eng.read_block(e.kind, e.location, e.pbn, l))
+                if int(e.kind) == 1:
+                    assert rel(blk[:n], tr.act[l][row:row + n]) <= TOL
+                else:
+                    assert rel(blk[0].transpose(1, 0, 2).reshape(tpb, d)[:n], tr.k[l][row:row + n]) <= TOL
+                    assert rel(blk[1].transpose(1, 0, 2).reshape(tpb, d)[:n], tr.v[l][row:row + n]) <= TOL
+            row += n
+    seqs = [list(p) for p in prompts]
+    for s in range(3):
+        toks = rng.integers(0, cfg.vocab_size, len(lens)).tolist()
+        res = eng.decode_step(ids, toks, want_x=True, want_logits=True)
+        for b in range(len(lens)):
+            seqs[b].append(toks[b])
+            out = O.forward_prompt_opt(seqs[b], w).output[-1:]
+            assert rel(f64(res["x"][b]), out[0]) <= TOL
+            assert rel(res["logits"][b], O.logits_tied(out, w)[0]) <= TOL
+
+
+def test_engine_opt_arch_seeded_extras_and_trace(native):
+    """Seeded OPT engine: extras drawn bit-exactly like the oracle's
+    generate_opt_extras; forward_trace equals forward_prompt_opt."""
+    from paper_2501_01792_b200.api import Engine, ModelConfig, PoolCaps
+    cfg = small_cfg(L=2, d=256, H=4, f=512)
+    mc = ModelConfig(num_layers=2, hidden_dim=256, num_heads=4, ffn_dim=512, vocab_size=cfg.vocab_size)
+    eng = Engine(mc, seed=9, max_seq=64, rescale=True, arch="opt", caps=PoolCaps(act_gpu=8), mode="act_only")
+    w = O.with_opt_extras(O.prepare_weights(O.generate_weights(cfg, 9, 64)), 9)
+    d, f = 256, 512
+    for l in range(2):
+        got = eng.read_weights(l)[4 * d * d + 2 * d * f:]
+        e = w.extras[l]
+        want = np.concatenate([e[k] for k in O.OPT_EXTRAS])
+        assert np.array_equal(got, O.to_bf16_bits(want))
+    assert np.array_equal(eng.read_weights(-3),
+                          O.to_bf16_bits(np.concatenate([w.final_ln["gamma"], w.final_ln["beta"]])))
+    ids = np.random.default_rng(3).integers(0, cfg.vocab_size, 37).tolist()
+    tr = eng.forward_trace(ids)
+    ref = O.forward_prompt_opt(ids, w)
+    assert rel(f64(tr["output"]), ref.output) <= TOL
+    for l in range(2):
+        assert rel(f64(tr["k"][l]), ref.k[l]) <= TOL
+        assert rel(f64(tr["layer_inputs"][l]), ref.layer_inputs[l]) <= TOL
+
+
+def test_engine_opt_arch_token_recompute(native):
+    """Token-recompute baseline on the OPT variant (prefix rebuilt through LN,
+    biases and residuals every step)."""
+    from paper_2501_01792_b200.api import PoolCaps
+    cfg = small_cfg(L=2, d=256, H=2, f=512, tpb=8)
+    w = opt_weights(cfg)
+    rng = np.random.default_rng(22)
+    prompts = [rng.integers(0, cfg.vocab_size, 33).tolist(), rng.integers(0, cfg.vocab_size, 20).tolist()]
+    eng = make_opt_engine(cfg, w, max_batch=2, caps=PoolCaps(kv_host=16), mode="token_recompute",
+                          recompute_ratio=0.5)
+    eng.prefill(["a", "b"], prompts)
+    toks = rng.integers(0, cfg.vocab_size, 2).tolist()
+    res = eng.decode_step(["a", "b"], toks, want_x=True)
+    for b in range(2):
+        assert rel(f64(res["x"][b]), O.forward_prompt_opt(prompts[b] + [toks[b]], w).output[-1]) <= TOL
