@@ -105,6 +105,11 @@ __global__ void __launch_bounds__(kWarps * 32)
             kr[i] = ldg16(base + t * HD + col);
             vr[i] = ldg16(base + v_off + t * HD + col);
         }
+        if (valid < TPB) {  // unfilled slots of the last block may hold any bits (even NaN): 0 * NaN != 0
+#pragma unroll
+            for (int i = 0; i < ITERS; ++i)
+                if (i * TPW + grp >= valid) vr[i] = make_uint4(0, 0, 0, 0);
+        }
         float s[ITERS];
         float bmax = -FLT_MAX;
 #pragma unroll

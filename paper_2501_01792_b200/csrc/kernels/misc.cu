@@ -84,10 +84,12 @@ __global__ void scatter_act_kernel(const BlockScatter c) {
     bf16* blk = ref_ptr(c.region, c.dst_ref[i], block_elems);
     const bf16* src = c.src + static_cast<long long>(c.src_row[i]) * c.ld;
     const int per_row = c.d / 8;
-    for (int idx = threadIdx.x; idx < n * per_row; idx += blockDim.x) {
+    // rows past n_tok (a partial last block) are zeroed: the block's bytes
+    // are deterministic wherever they are copied (HBM staging -> pinned host)
+    for (int idx = threadIdx.x; idx < c.tpb * per_row; idx += blockDim.x) {
         const int t = idx / per_row, x = (idx - t * per_row) * 8;
         *reinterpret_cast<uint4*>(blk + static_cast<long long>(t) * c.d + x) =
-            *reinterpret_cast<const uint4*>(src + t * c.ld + x);
+            t < n ? *reinterpret_cast<const uint4*>(src + t * c.ld + x) : make_uint4(0, 0, 0, 0);
     }
 }
 
@@ -106,10 +108,10 @@ __global__ void scatter_kv_kernel(const BlockScatter c) {
         const int w = idx - ph * chunks_per_head;
         const int t = (w * 8) / c.hd;
         const int cc = (w * 8) - t * c.hd;
-        if (t >= n) continue;
         const int part = ph / (c.d / c.hd);
         const int h = ph - part * (c.d / c.hd);
-        const uint4 v = *reinterpret_cast<const uint4*>(src + t * c.ld + part * c.d + h * c.hd + cc);
+        const uint4 v = t < n ? *reinterpret_cast<const uint4*>(src + t * c.ld + part * c.d + h * c.hd + cc)
+                              : make_uint4(0, 0, 0, 0);  // unfilled slots of a partial block
         *reinterpret_cast<uint4*>(blk + static_cast<long long>(ph) * c.tpb * c.hd + t * c.hd + cc) = v;
     }
 }
@@ -223,7 +225,7 @@ __device__ __forceinline__ float block_sum(float v, float* red) {
     __syncthreads();
     float t = lane < kLnThreads / 32 ? red[lane] : 0.f;
 #pragma unroll
-    for (int o = 4; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);  // every lane gets the total
     return t;
 }
 

@@ -4,7 +4,8 @@
 //
 // Tensor-core flash attention: one CTA (4 warps) per (64-query tile, head,
 // request); each warp owns 16 query rows. S = Q.K^T and O += P.V run on
-// mma.sync m16n8k16 bf16 (fp32 accumulate); the online softmax lives in the
+// mma.sync m16n8k16 bf16 (fp32 accumulate; P.V as hi+lo bf16 halves of P);
+// the online softmax lives in the
 // accumulator registers (a thread owns 2 rows, quad shuffles reduce them) and
 // P is re-packed register-to-register as the A operand of P.V. K and V tiles
 // of 64 keys are double-buffered in XOR-swizzled shared memory with cp.async
@@ -59,6 +60,15 @@ __device__ __forceinline__ void mma16816(float (&c)[4], const uint32_t (&a)[4], 
         "{%0,%1,%2,%3};\n"
         : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
         : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+// (a, b) -> bf16x2 hi = rn(a, b) and lo = rn((a, b) - hi)
+__device__ __forceinline__ void split_bf16x2(float a, float b, uint32_t& hi, uint32_t& lo) {
+    const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+    const float2 hf = __bfloat1622float2(h);
+    const __nv_bfloat162 l = __floats2bfloat162_rn(a - hf.x, b - hf.y);
+    hi = *reinterpret_cast<const uint32_t*>(&h);
+    lo = *reinterpret_cast<const uint32_t*>(&l);
 }
 
 // byte offset of 16-B chunk `ch` of row `row` in a [rows][HD] bf16 tile
@@ -187,15 +197,19 @@ __global__ void __launch_bounds__(128)
             o[j][2] *= alpha[1];
             o[j][3] *= alpha[1];
         }
-        uint32_t pa[4][4];  // P as the A operand, k16 chunk = keys 16kk..16kk+15
+        // P as the A operand (k16 chunk = keys 16kk..16kk+15), split into
+        // bf16 hi + lo parts: P.V = P_hi.V + P_lo.V keeps P to ~16 bits, so
+        // the prefill matches fp32 softmax weights (a single bf16 P costs ~2^-9
+        // relative per weight, visible after a dozen layers)
+        uint32_t pa[4][4], pl[4][4];
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
             const float p0 = exp2f(s[j][0] - m_r[0]), p1 = exp2f(s[j][1] - m_r[0]);
             const float p2 = exp2f(s[j][2] - m_r[1]), p3 = exp2f(s[j][3] - m_r[1]);
             l_r[0] += p0 + p1;
             l_r[1] += p2 + p3;
-            pa[j / 2][(j & 1) * 2 + 0] = ptx::pack_bf16x2(p0, p1);
-            pa[j / 2][(j & 1) * 2 + 1] = ptx::pack_bf16x2(p2, p3);
+            split_bf16x2(p0, p1, pa[j / 2][(j & 1) * 2 + 0], pl[j / 2][(j & 1) * 2 + 0]);
+            split_bf16x2(p2, p3, pa[j / 2][(j & 1) * 2 + 1], pl[j / 2][(j & 1) * 2 + 1]);
         }
         // O += P.V : V tile [key][hd] read transposed as the col-major B operand
 #pragma unroll
@@ -208,6 +222,8 @@ __global__ void __launch_bounds__(128)
                 ldsm_x4_t(sV(cur) + swz<HD>(key, ch), b0, b1, b2, b3);
                 mma16816(o[2 * jp], pa[kk], b0, b1);
                 mma16816(o[2 * jp + 1], pa[kk], b2, b3);
+                mma16816(o[2 * jp], pl[kk], b0, b1);
+                mma16816(o[2 * jp + 1], pl[kk], b2, b3);
             }
         }
         __syncthreads();  // tile `cur` is overwritten by the load issued next iteration

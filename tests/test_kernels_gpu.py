@@ -144,6 +144,38 @@ def test_decode_attention_single_token_returns_v(native):
         assert np.array_equal(got[b], v)
 
 
+@pytest.mark.parametrize("splits", [1, 2])
+def test_decode_attention_ignores_unfilled_slots(native, splits):
+    """Unfilled token slots of a partial last block may hold any bits (a block
+    staged in HBM and copied out whole): NaN there must not reach the output
+    (0 * NaN = NaN, so they are excluded, not zero-weighted)."""
+    from paper_2501_01792_b200.kernels import decode_attention
+    rng = np.random.default_rng(7)
+    B, H, hd, tpb = 3, 2, 128, 16
+    ctxs = [5, 17, 40]
+    d = H * hd
+    q = rand_bits(rng, (B, d))
+    nb = [(c + tpb - 1) // tpb for c in ctxs]
+    r0 = rand_bits(rng, (sum(nb), 2, H, tpb, hd))
+    r1 = rand_bits(rng, (1, 2, H, tpb, hd))
+    refs = np.full((B, max(nb)), -1, np.int32)
+    want = np.zeros((B, d))
+    k0 = 0
+    for b, c in enumerate(ctxs):
+        refs[b, :nb[b]] = np.arange(k0, k0 + nb[b])
+        last = k0 + nb[b] - 1
+        r0[last, :, :, c - (nb[b] - 1) * tpb:, :] = 0x7FC0  # NaN in every unfilled slot
+        blk = f64(r0[k0:k0 + nb[b]])
+        K = blk[:, 0].transpose(0, 2, 1, 3).reshape(-1, d)[:c]
+        V = blk[:, 1].transpose(0, 2, 1, 3).reshape(-1, d)[:c]
+        want[b] = O.attention_rows(f64(q)[b:b + 1], K, V, [c], H, True)[0]
+        k0 += nb[b]
+    got = f64(decode_attention(q, r0, r1, refs, np.asarray(nb, np.int32), np.asarray(ctxs, np.int32), H, True,
+                               splits))
+    assert np.isfinite(got).all()
+    assert rel(got, want) <= TOL_BF16
+
+
 @pytest.mark.parametrize("n_req,P,H,hd", [(2, 37, 2, 128), (3, 130, 4, 64), (1, 256, 8, 128), (2, 1, 2, 128),
                                           (2, 64, 2, 64), (1, 321, 2, 128)])
 def test_prefill_attention_causal(native, n_req, P, H, hd):
