@@ -695,12 +695,154 @@ def our_arm(args, cfg, world, rank, local, dist):
         res.update(extra)
     eng.close()
     if rank == 0:
+        if not args.no_sweep and world == 1:
+            try:
+                res["hbm_resident"] = resident_variants(local, cfg, B, P, args.arch)
+            except Exception as e:
+                res["hbm_resident"] = {"error": str(e)}
+        if not args.no_sweep and world == 1 and args.config == 3:
+            try:
+                res["config1_e2e"] = config1_e2e(local, None if args.no_cpu_baseline else os.cpu_count() or 1)
+            except Exception as e:
+                res["config1_e2e"] = {"error": str(e)}
         if not args.no_sweep and not args.no_config2 and world == 1 and args.config == 3:
             try:
                 res["config2_resident"] = config2_resident(local)
             except Exception as e:
                 res["config2_resident"] = {"error": str(e)}
         print(json.dumps(res), flush=True)
+    return res
+
+
+def resident_variants(local, cfg, B, P, arch, steps=2, warmup=1, reserve=6e9):
+    """The same workload with the weights AND the cache in HBM (B200 has 180 GB):
+    KV and ACT blocks both placed on the GPU first (kv_on_gpu / ACT-first,
+    cache.cpp:64-91). Pure KV does not fit, so its overflow blocks stream from
+    pinned host memory; pure ACT fits but recomputes every context token each
+    step. The capacity-constrained end of Alg. 1: with no
+    link time left to hide recompute under, every KV block that fits saves
+    4 d^2 tpb FLOPs per layer per step, so the planned ACT share is the smallest
+    one whose blocks fit the free HBM (r_fit). Sweeps r = 0 (KV, overflow to
+    host), r_fit, (1 + r_fit)/2 and r = 1."""
+    import torch
+    from paper_2501_01792_b200 import api
+    L, tpb = cfg.num_layers, cfg.tokens_per_block
+    total = steps + warmup + 2
+    nb = math.ceil((P + total) / tpb)
+    N = B * nb
+    kv_all = api.HybridCache.bytes_of("KV", cfg) * L
+    act_all = api.HybridCache.bytes_of("ACT", cfg) * L
+    kv_one = api.HybridCache.bytes_of("KV", cfg)  # recompute output buffer per ACT block (one layer)
+    eng = api.Engine(cfg, seed=42, max_seq=P + total + 1, rescale=True, max_batch=B, weights_on_device=True,
+                     caps=api.PoolCaps(), mode="act_only", device=local, arch=arch)
+    free = torch.cuda.mem_get_info(local)[0] - reserve
+    # x ACT blocks + (N - x) KV blocks (+ x recompute slots) <= free
+    x_fit = max(0, math.ceil((N * kv_all - free) / (kv_all - act_all - kv_one)))
+    r_fit = min(1.0, (x_fit + B) / N)
+    ids = [f"h{i}" for i in range(B)]
+    tokens = np.random.default_rng(9).integers(0, cfg.vocab_size, (total, B)).astype(np.int32)
+    out = {"workload": f"{cfg.name}-shape, batch {B}, prompt {P}: weights + cache in HBM (KV and ACT placed on "
+                       "the GPU first); overflow blocks in pinned host memory",
+           "free_hbm_gb": free / 1e9, "blocks": N, "r_fit": r_fit, "per_ratio": []}
+    for r in sorted({0.0, r_fit, (1.0 + r_fit) / 2, 1.0}):
+        a = int(round(r * 1000))
+        act_cap = 0 if r <= 0 else (N if r >= 1 else B * (math.ceil(r * nb) + 1))
+        kv_need = 0 if r >= 1 else (N if r <= 0 else B * (math.ceil((1 - r) * nb) + 1))
+        # KV/gpu blocks that fit next to the ACT blocks, their recompute slots and
+        # the two per-layer staging slots of the overflow (kv_host) blocks
+        room = free - act_cap * (act_all + kv_one) - 2 * kv_need * kv_one
+        kv_gpu = int(max(0, min(kv_need, room // (kv_all - 2 * kv_one))))
+        caps = api.PoolCaps(kv_host=kv_need - kv_gpu, kv_gpu=kv_gpu, act_gpu=act_cap)
+        mode = "kv_only" if r <= 0 else ("act_only" if r >= 1 else "hybrid")
+        try:
+            eng.configure_cache(caps, mode=mode, allocation=api.HostAllocation(a, 1000 - a), kv_on_gpu=True)
+            eng.admit_synthetic(ids, [P] * B, seed=11)
+            run_steps(eng, ids, tokens, 0, warmup)
+            acc = run_steps(eng, ids, tokens, warmup, steps)
+            ms = acc["dev_ms"] / steps
+            out["per_ratio"].append({"act_share_r": round(r, 4), "mode": mode, "tokens_per_s": B * 1e3 / ms,
+                                     "ms_per_step": ms, "kv_gpu_blocks": kv_gpu, "kv_host_blocks": caps.kv_host,
+                                     "act_gpu_blocks": act_cap, "h2d_gb_per_step": acc["h2d"] / steps / 1e9,
+                                     "planned": abs(r - r_fit) < 1e-9})
+        except Exception as e:
+            out["per_ratio"].append({"act_share_r": round(r, 4), "error": str(e)})
+    eng.close()
+    return out
+
+
+def config1_e2e(local, cpu_threads, B=4, P=128, G=32):
+    """BASELINE configs[0] end to end: OPT-125M shape, batch 4, prompt 128, gen
+    32, KV:ACT 0.5 (HostAllocation{K, K}: ACT, KV, ACT, ... blocks in pinned
+    host pools). GPU: prefill + 32 greedy decode steps through the C ABI
+    (token ids in, argmax out, fed back), wall clock. CPU reference (the
+    reference library on this host): one request's prefill + 32 steps, each
+    assembling its context from stored KV blocks and ACT blocks recomputed by
+    recompute_kv_from_activation (verify.cpp:62-73), then generation_step +
+    tied-head greedy token; tokens/s scaled to the request."""
+    from paper_2501_01792_b200 import api
+    cfg = api.ModelConfig(num_layers=12, hidden_dim=768, num_heads=12, ffn_dim=3072, vocab_size=50272,
+                          name="opt-125m")
+    tpb = cfg.tokens_per_block
+    nb = math.ceil((P + G) / tpb)
+    K = B * nb
+    rng = np.random.default_rng(3)
+    prompts = [rng.integers(0, cfg.vocab_size, P).tolist() for _ in range(B)]
+    eng = api.Engine(cfg, seed=42, max_seq=P + G + 1, rescale=True, max_batch=B, weights_on_device=True,
+                     caps=api.PoolCaps(kv_host=K, act_host=K), allocation=api.HostAllocation(K, K), mode="hybrid",
+                     device=local)
+
+    def generate(tag):
+        rids = [f"{tag}{i}" for i in range(B)]
+        t0 = time.perf_counter()
+        eng.prefill(rids, prompts)
+        toks = [p[-1] for p in prompts]
+        out = {"argmax": np.zeros(B, np.int32)}
+        seqs = []
+        for _ in range(G):
+            eng.decode_step(rids, toks, want_x=False, want_argmax=True, out=out)
+            toks = out["argmax"].tolist()
+            seqs.append(toks)
+        wall = time.perf_counter() - t0
+        for r in rids:
+            eng.free_request(r)
+        return wall, seqs
+
+    generate("w")  # warm-up
+    walls = [generate(f"t{i}_")[0] for i in range(3)]
+    wall = statistics.median(walls)
+    eng.close()
+    res = {"workload": "opt-125m-shape, batch 4, prompt 128, gen 32 greedy, KV:ACT 0.5, cache in pinned host pools",
+           "gpu": {"tokens_per_s": B * G / wall, "wall_s": wall, "includes": "prefill + 32 decode steps, C-ABI "
+                   "calls with host token ids / argmax"}}
+    if cpu_threads:
+        os.environ["OMP_NUM_THREADS"] = str(cpu_threads)
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+        import ref_lib as R  # noqa: E402  (CPU baseline only)
+        if R.available():
+            rw = R.RefWeights(12, 768, 12, 3072, 50272, tpb, 42, P + G + 1)
+            emb = rw.get(0)
+            t0 = time.perf_counter()
+            ins, k, v, out = rw.forward_prompt(prompts[0])
+            ctx_k = np.array(k)
+            ctx_v = np.array(v)
+            tok = int(np.argmax(out[-1] @ emb.T))
+            for g in range(G):
+                # ACT-kind blocks (every other block) are rebuilt from their activations
+                kk, vv = ctx_k.copy(), ctx_v.copy()
+                n = ctx_k.shape[1]
+                for blk in range(0, (min(n, P) + tpb - 1) // tpb, 2):
+                    sl = slice(blk * tpb, min((blk + 1) * tpb, P))
+                    for l in range(12):
+                        kk[l, sl], vv[l, sl] = rw.recompute_kv(l, ins[l, sl])
+                o, nk, nv = rw.generation_step(tok, n, kk, vv)
+                ctx_k = np.concatenate([ctx_k, nk[:, None, :]], axis=1)
+                ctx_v = np.concatenate([ctx_v, nv[:, None, :]], axis=1)
+                tok = int(np.argmax(o[0] @ emb.T))
+            cpu_s = time.perf_counter() - t0
+            res["cpu_reference"] = {"tokens_per_s": G / cpu_s, "wall_s": cpu_s, "cores": cpu_threads,
+                                    "kind": "reference", "sample": "1 request: forward_prompt(128) + 32 greedy "
+                                    "steps (ACT blocks recomputed each step + generation_step)"}
+            res["gpu_over_cpu"] = res["gpu"]["tokens_per_s"] / res["cpu_reference"]["tokens_per_s"]
     return res
 
 

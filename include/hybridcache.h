@@ -135,7 +135,24 @@ typedef struct hc_engine_options {
     int arch;                /* 0 reference decoder (decoder.cpp: no bias/LN/residual); 1 OPT (pre-LN,
                               * biases, residuals, final LN; the ACT cache holds LN1(x)). Seeded engines
                               * draw the OPT extras; f64 engines take them from _create_from_f64_opt. */
+    void* tp;                /* NULL, or a tensor-parallel rank handle (hc_tp_*): head-sharded variant */
 } hc_engine_options;
+
+/* ------------------------------------------ tensor parallelism (optional) ---
+ * Head-sharded variant of SURVEY.md §8(e): rank g of N owns heads
+ * [gH/N, (g+1)H/N) (W_q|W_k|W_v columns, W_proj rows, an FFN slice, its heads'
+ * K|V in every KV block) and the ACT/host blocks with pbn % N == g; per layer
+ * two all-reduces (compute stream) and one ACT all-gather (copy stream).
+ * Every rank is driven with the same request ids / tokens. No reference
+ * counterpart (the reference is single-process). */
+int hc_tp_nccl_unique_id(uint8_t* out128);
+/* NCCL group (one process per GPU): two ids from rank 0, broadcast by the caller. */
+int hc_tp_create_nccl(const uint8_t* id_compute128, const uint8_t* id_copy128, int rank, int size, int device,
+                      void** tp);
+/* In-process group (N engines, one host thread each; tests on one GPU). */
+int hc_tp_create_local_group(int size, void** group);
+int hc_tp_local_member(void* group, int rank, void** tp); /* owned by the group */
+int hc_tp_destroy(void* handle, int is_group);
 
 int hc_engine_create(const hc_model_config* cfg, uint64_t seed, int max_seq, int rescale,
                      const hc_engine_options* opt, void** out);

@@ -23,7 +23,8 @@ class EngineOptionsC(C.Structure):
                 ("act_gpu_cap", C.c_long), ("kv_on_gpu", C.c_int), ("host_layers", C.c_int),
                 ("mode", C.c_int), ("alloc_act_host", C.c_long), ("alloc_kv_host", C.c_long),
                 ("scaled", C.c_int), ("max_prefill_tokens", C.c_int), ("device", C.c_int),
-                ("weight_layers", C.c_int), ("recompute_ratio", C.c_double), ("arch", C.c_int)]
+                ("weight_layers", C.c_int), ("recompute_ratio", C.c_double), ("arch", C.c_int),
+                ("tp", C.c_void_p)]
 
 
 cfgp = C.POINTER(ModelConfigC)
@@ -71,6 +72,11 @@ SIGNATURES = {
     # engine
     "hc_engine_create": (i, [cfgp, u64, i, i, optp, vpp]),
     "hc_engine_create_from_f64": (i, [cfgp, i, dp, dp, C.POINTER(dp), optp, vpp]),
+    "hc_tp_nccl_unique_id": (i, [C.c_char_p]),
+    "hc_tp_create_nccl": (i, [C.c_char_p, C.c_char_p, i, i, i, vpp]),
+    "hc_tp_create_local_group": (i, [i, vpp]),
+    "hc_tp_local_member": (i, [vp, i, vpp]),
+    "hc_tp_destroy": (i, [vp, i]),
     "hc_engine_create_from_f64_opt": (i, [cfgp, i, dp, dp, C.POINTER(dp), C.POINTER(dp), dp, optp, vpp]),
     "hc_engine_destroy": (i, [vp]),
     "hc_engine_prefill": (i, [vp, i, cpp, ip, ip]),

@@ -430,6 +430,51 @@ def _ids(ids: Sequence[str]):
     return arr
 
 
+class TensorParallel:
+    """Rank handle of the optional head-sharded variant (csrc/tp.hpp): rank g
+    of N owns heads [gH/N, (g+1)H/N) and the ACT/host blocks with pbn % N == g.
+    Every rank's Engine gets the same request ids and tokens."""
+
+    def __init__(self, handle, owner=None, is_group=False, rank=0, size=1):
+        self._h = handle
+        self._owner = owner          # keeps a local group alive while members exist
+        self._is_group = is_group
+        self.rank, self.size = rank, size
+
+    @staticmethod
+    def nccl_unique_ids() -> bytes:
+        """Two ncclUniqueIds (compute channel | copy channel), 256 bytes; made on
+        rank 0 and broadcast to the others by the caller."""
+        a, b = C.create_string_buffer(128), C.create_string_buffer(128)
+        check(lib().hc_tp_nccl_unique_id(a))
+        check(lib().hc_tp_nccl_unique_id(b))
+        return a.raw + b.raw
+
+    @classmethod
+    def nccl(cls, ids: bytes, rank: int, size: int, device: int = 0) -> "TensorParallel":
+        h = C.c_void_p()
+        check(lib().hc_tp_create_nccl(ids[:128], ids[128:256], rank, size, device, C.byref(h)))
+        return cls(h, rank=rank, size=size)
+
+    @classmethod
+    def local_group(cls, size: int) -> List["TensorParallel"]:
+        """size ranks in this process (drive each rank's engine from its own thread)."""
+        g = C.c_void_p()
+        check(lib().hc_tp_create_local_group(size, C.byref(g)))
+        group = cls(g, is_group=True, size=size)
+        out = []
+        for r in range(size):
+            h = C.c_void_p()
+            check(lib().hc_tp_local_member(g, r, C.byref(h)))
+            out.append(cls(h, owner=group, rank=r, size=size))
+        return out
+
+    def __del__(self):
+        if getattr(self, "_h", None) and (self._is_group or self._owner is None):
+            lib().hc_tp_destroy(self._h, int(self._is_group))
+            self._h = None
+
+
 class Engine:
     """B200 decode engine over the hybrid KV/ACT cache (csrc/engine.hpp).
 
@@ -443,7 +488,7 @@ class Engine:
                  caps: Optional[PoolCaps] = None, kv_on_gpu: bool = False, host_layers: int = 0,
                  mode: str = "hybrid", allocation: Optional[HostAllocation] = None, scaled: bool = True,
                  max_prefill_tokens: int = 0, device: int = 0, weight_layers: int = 0,
-                 recompute_ratio: float = 0.0, arch: str = "reference"):
+                 recompute_ratio: float = 0.0, arch: str = "reference", tp: Optional[TensorParallel] = None):
         self.cfg = ModelConfig(**cfg.__dict__).validate()
         caps = caps or PoolCaps()
         alloc = allocation or HostAllocation(1, 1)
@@ -455,7 +500,8 @@ class Engine:
         self.opts = EngineOptionsC(max_batch, max_seq, int(weights_on_device), caps.kv_host, caps.kv_gpu,
                                    caps.act_host, caps.act_gpu, int(kv_on_gpu), host_layers, MODES[mode],
                                    alloc.act_host, alloc.kv_host, int(scaled), max_prefill_tokens, device,
-                                   weight_layers, recompute_ratio, ARCHS[arch])
+                                   weight_layers, recompute_ratio, ARCHS[arch], tp._h if tp else None)
+        self._tp = tp
         self.max_batch = max_batch
         h = C.c_void_p()
         c = self.cfg.to_c()
@@ -584,8 +630,8 @@ class Engine:
 
     def read_block(self, kind, loc, pbn: int, layer: int) -> np.ndarray:
         d, tpb, H = self.cfg.hidden_dim, self.cfg.tokens_per_block, self.cfg.num_heads
-        if _kind(kind) == 0:
-            out = np.zeros((2, H, tpb, d // H), np.uint16)
+        if _kind(kind) == 0:  # a tensor-parallel rank holds its own heads of every KV block
+            out = np.zeros((2, H // (self._tp.size if self._tp else 1), tpb, d // H), np.uint16)
         else:
             out = np.zeros((tpb, d), np.uint16)
         check(lib().hc_engine_read_block(self._h, _kind(kind), _loc(loc), pbn, layer, ptr(out, C.c_uint16)))
@@ -601,7 +647,9 @@ class Engine:
         elif layer == -3:
             out = np.zeros(2 * d, np.uint16)
         else:
-            out = np.zeros(4 * d * d + 2 * d * f + (9 * d + f if self.arch == "opt" else 0), np.uint16)
+            n = self._tp.size if self._tp else 1
+            out = np.zeros((4 * d * d + 2 * d * f) // n + ((3 * d + f) // n + 6 * d if self.arch == "opt" else 0),
+                           np.uint16)
         check(lib().hc_engine_read_weights(self._h, layer, ptr(out, C.c_uint16)))
         return out
 

@@ -82,6 +82,7 @@ EngineOptions opts_of(const hc_engine_options* o) {
     e.weight_layers = o->weight_layers;
     e.recompute_ratio = o->recompute_ratio;
     e.arch = o->arch;
+    e.tp = static_cast<TpGroup*>(o->tp);
     return e;
 }
 
@@ -358,6 +359,41 @@ int hc_engine_create_from_f64_opt(const hc_model_config* cfg, int max_seq, const
     return hc_guard([&] {
         const HostWeights w = weights_from_f64_opt(to_cfg(cfg), max_seq, emb, pos, layer_tensors, layer_extras, final_ln);
         *out = new Engine(w, opts_of(opt));
+    });
+}
+int hc_tp_nccl_unique_id(uint8_t* out) {
+    return hc_guard([&] {
+        if (!out) throw InputError("null id buffer");
+        nccl_unique_id(out);
+    });
+}
+int hc_tp_create_nccl(const uint8_t* idc, const uint8_t* idk, int rank, int size, int device, void** tp) {
+    return hc_guard([&] {
+        if (!idc || !idk || !tp) throw InputError("null argument");
+        *tp = make_nccl_group(idc, idk, rank, size, device).release();
+    });
+}
+struct LocalGroupHolder {
+    std::shared_ptr<LocalGroupState> g;
+};
+int hc_tp_create_local_group(int size, void** group) {
+    return hc_guard([&] {
+        if (!group) throw InputError("null argument");
+        *group = new LocalGroupHolder{make_local_group(size)};
+    });
+}
+int hc_tp_local_member(void* group, int rank, void** tp) {
+    return hc_guard([&] {
+        if (!group || !tp) throw InputError("null argument");
+        *tp = local_group_member(static_cast<LocalGroupHolder*>(group)->g, rank);
+    });
+}
+int hc_tp_destroy(void* h, int is_group) {
+    return hc_guard([&] {
+        if (is_group)
+            delete static_cast<LocalGroupHolder*>(h);
+        else
+            delete static_cast<TpGroup*>(h);
     });
 }
 int hc_engine_destroy(void* e) {

@@ -80,11 +80,23 @@ void gemm_rows(int epi, const bf16* A, int M, int K, const bf16* W, int N, void*
 struct Engine::Impl {
     int L = 0, d = 0, H = 0, hd = 0, f = 0, V = 0, tpb = 0, B = 0, max_seq = 0, max_blocks = 0, Lp = 0, Lw = 0;
     int arch = kArchReference;
+    // head-sharded tensor parallelism (tp.hpp): this rank's heads / hidden
+    // columns / FFN slice; ACT/host blocks are owned round-robin by pbn and
+    // staged at act_pos(pbn) so one all-gather of the per-rank chunks fills
+    // every rank's staging
+    TpGroup* tp = nullptr;
+    int tpr = 0, tpn = 1, Hg = 0, dg = 0, fg = 0;
+    long act_cap_n = 0;  // ACT/host blocks per rank = ceil(act_host_cap / tpn)
+    bf16* wfull = nullptr;  // init only: one unsharded layer when tpn > 1
+    bool owns(int pbn) const { return pbn % tpn == tpr; }
+    int act_pos(int pbn) const { return static_cast<int>((pbn % tpn) * act_cap_n + pbn / tpn); }
     bf16* lnf = nullptr;  // kArchOpt final LayerNorm gamma | beta [2d]
     bf16* xn = nullptr;   // kArchOpt decode LN output [B x d]
     bf16* pxn = nullptr;  // kArchOpt prefill LN1 output [prefill_rows x d]
     size_t LE = 0, kvb = 0, actb = 0;
-    LayerOffsets off{};
+    LayerOffsets off{};        // this rank's packed layer (== offF when tpn == 1)
+    LayerOffsets offF{};       // the unsharded packed layer
+    size_t LEF = 0;
     bf16 *emb = nullptr, *pos = nullptr;
     bf16* w_all = nullptr;
     bf16* wbuf[2] = {nullptr, nullptr};
@@ -149,10 +161,35 @@ struct Engine::Impl {
         r[R_ACT_STAGE] = act_stage[slot];
         r[R_ACT_GPU] = act_gpu ? act_gpu + static_cast<size_t>(l) * act_gpu_cap * actb : nullptr;
         r[R_KV_HOST] = kv_host ? kv_host + static_cast<size_t>(l % Lp) * kv_host_cap * kvb : nullptr;
-        r[R_ACT_HOST] = act_host ? act_host + static_cast<size_t>(l % Lp) * act_host_cap * actb : nullptr;
+        r[R_ACT_HOST] = act_host ? act_host + static_cast<size_t>(l % Lp) * act_cap_n * actb : nullptr;
         r[R_TOKREC] = tr_kv;
     }
     const bf16* layer_w(int l, int slot) const { return w_all ? w_all + static_cast<size_t>(l) * LE : wbuf[slot]; }
+
+    // unsharded packed layer `full` (device) -> this rank's shard at dst
+    // (device or pinned host; kind says which)
+    void extract_shard(const bf16* full, void* dstv, cudaMemcpyKind kind, cudaStream_t st) const {
+        uint16_t* dst = static_cast<uint16_t*>(dstv);
+        const uint16_t* F = reinterpret_cast<const uint16_t*>(full);
+        const size_t D = d, Fd = f, g = tpr, DG = dg, FG = fg;
+        auto cp = [&](size_t o, size_t so, size_t n) {
+            HC_CUDA(cudaMemcpyAsync(dst + o, F + so, n * 2, kind, st));
+        };
+        auto cp2 = [&](size_t o, size_t dpitch, size_t so, size_t spitch, size_t width, size_t rows) {
+            HC_CUDA(cudaMemcpy2DAsync(dst + o, dpitch * 2, F + so, spitch * 2, width * 2, rows, kind, st));
+        };
+        for (size_t k = 0; k < 3; ++k) cp(off.wqkv + k * DG * D, offF.wqkv + (k * D + g * DG) * D, DG * D);  // head rows
+        cp2(off.wproj, DG, offF.wproj + g * DG, D, DG, D);  // Wproj^T columns = the heads' input rows of W_o
+        cp(off.w1, offF.w1 + g * FG * D, FG * D);
+        cp2(off.w2, FG, offF.w2 + g * FG, Fd, FG, D);
+        if (opt()) {
+            for (size_t k = 0; k < 3; ++k) cp(off.bqkv + k * DG, offF.bqkv + k * D + g * DG, DG);
+            cp(off.bproj, offF.bproj, D);
+            cp(off.b1, offF.b1 + g * FG, FG);
+            cp(off.b2, offF.b2, D);
+            cp(off.ln1g, offF.ln1g, 4 * D);
+        }
+    }
 
     // ---- decoder-layer arithmetic shared by decode, prefill and traces ----
     bool opt() const { return arch == kArchOpt; }
@@ -165,23 +202,50 @@ struct Engine::Impl {
                        T, d, static_cast<float>(kLnEps), st);
         return out;
     }
-    // qkv [T x 3d] = LN1(x) . Wqkv (+ b_qkv)   (qkv_generate, decoder.cpp:97-103)
+    // qkv [T x 3dg] = LN1(x) . Wqkv (+ b_qkv) for this rank's heads
+    // (qkv_generate, decoder.cpp:97-103)
     void qkv(const bf16* W, const bf16* xa, int T, bf16* out, cudaStream_t st, float* ws = nullptr,
              size_t wsf = 0) const {
-        gemm_rows(gemm::kStore, xa, T, d, W + off.wqkv, 3 * d, out, 3 * d, st, 0, ws, wsf, bias(W, off.bqkv));
+        gemm_rows(gemm::kStore, xa, T, d, W + off.wqkv, 3 * dg, out, 3 * dg, st, 0, ws, wsf, bias(W, off.bqkv));
     }
-    // project_ffn (decoder.cpp:113-121) of T attention rows; kArchOpt adds the
-    // biases, the two residuals (x, then x') and LN2. lnbuf may alias att.
+    // project_ffn (decoder.cpp:113-121) of T attention rows [T x dg]; kArchOpt
+    // adds the biases, the two residuals (x, then x') and LN2. Head-sharded:
+    // W_proj / W2 are row slices, so their outputs are partial sums that one
+    // all-reduce each completes (bias and residual enter once, on rank 0).
+    // lnbuf may alias att.
     void tail(const bf16* W, const bf16* att, const bf16* x, int T, bf16* proj, bf16* lnbuf, bf16* h, bf16* out,
-              cudaStream_t st, float* ws = nullptr, size_t wsf = 0) const {
-        gemm_rows(gemm::kStore, att, T, d, W + off.wproj, d, proj, d, st, 0, ws, wsf, bias(W, off.bproj),
-                  opt() ? x : nullptr, d);
+              cudaStream_t st, float* ws = nullptr, size_t wsf = 0) {
+        if (tpn == 1) {  // bias + residual fused into the GEMM epilogues
+            gemm_rows(gemm::kStore, att, T, d, W + off.wproj, d, proj, d, st, 0, ws, wsf, bias(W, off.bproj),
+                      opt() ? x : nullptr, d);
+            const bf16* p2 = ln(W, 2, proj, T, lnbuf, st);
+            gemm_rows(gemm::kRelu, p2, T, d, W + off.w1, f, h, f, st, 0, ws, wsf, bias(W, off.b1));
+            gemm_rows(gemm::kStore, h, T, f, W + off.w2, d, out, d, st, 0, ws, wsf, bias(W, off.b2),
+                      opt() ? proj : nullptr, d);
+            return;
+        }
+        // head-sharded: fp32 partial sums -> all-reduce -> + bias + residual
+        float* r = ensure_red(static_cast<size_t>(T) * d);
+        gemm_rows(gemm::kF32, att, T, dg, W + off.wproj, d, r, d, st, 0, ws, wsf);
+        tp->all_reduce_sum(r, static_cast<size_t>(T) * d, st);
+        add_bias_residual(r, bias(W, off.bproj), opt() ? x : nullptr, d, T, d, proj, st);
         const bf16* p2 = ln(W, 2, proj, T, lnbuf, st);
-        gemm_rows(gemm::kRelu, p2, T, d, W + off.w1, f, h, f, st, 0, ws, wsf, bias(W, off.b1));
-        gemm_rows(gemm::kStore, h, T, f, W + off.w2, d, out, d, st, 0, ws, wsf, bias(W, off.b2),
-                  opt() ? proj : nullptr, d);
+        gemm_rows(gemm::kRelu, p2, T, d, W + off.w1, fg, h, fg, st, 0, ws, wsf, bias(W, off.b1));
+        gemm_rows(gemm::kF32, h, T, fg, W + off.w2, d, r, d, st, 0, ws, wsf);
+        tp->all_reduce_sum(r, static_cast<size_t>(T) * d, st);
+        add_bias_residual(r, bias(W, off.b2), opt() ? proj : nullptr, d, T, d, out, st);
     }
-    int tail_launches() const { return opt() ? 4 : 3; }
+    int tail_launches() const { return (opt() ? 4 : 3) + (tpn > 1 ? 2 : 0); }
+    float* red = nullptr;  // tensor-parallel partial sums [rows x d] fp32
+    size_t red_elems = 0;
+    float* ensure_red(size_t elems) {
+        if (elems > red_elems) {
+            if (red) HC_CUDA(cudaFree(red));
+            red = dalloc<float>(elems);
+            red_elems = elems;
+        }
+        return red;
+    }
     // model output: LN_f(x) for kArchOpt (into out), x itself otherwise
     const bf16* final_norm(const bf16* x, int T, bf16* out, cudaStream_t st) const {
         if (!opt()) return x;
@@ -266,34 +330,44 @@ Engine::Engine(const ModelConfig& c, uint64_t seed, int max_seq, bool rescale, c
     double fac[6];
     rescale_factors(cfg_, fac);
     const int d = m.d, f = m.f;
+    // the unsharded layer (reference tags and layout), drawn in place or into
+    // wfull and then cut to this rank's shard
     auto draw_layer = [&](int l, bf16* dst) {
         uint16_t* L = reinterpret_cast<uint16_t*>(dst);
+        const LayerOffsets& o = m.offF;
         const uint64_t base = 100 + static_cast<uint64_t>(l) * 8;  // model.cpp:90, 106-113
         for (int k = 0; k < 3; ++k)
-            gen_weights_transposed(L + m.off.wqkv + static_cast<size_t>(k) * d * d, d, d, mix_seed(seed, base + k),
+            gen_weights_transposed(L + o.wqkv + static_cast<size_t>(k) * d * d, d, d, mix_seed(seed, base + k),
                                    fac[k], rescale, s_compute_);
-        gen_weights_transposed(L + m.off.wproj, d, d, mix_seed(seed, base + 3), fac[3], rescale, s_compute_);
-        gen_weights_transposed(L + m.off.w1, d, f, mix_seed(seed, base + 4), fac[4], rescale, s_compute_);
-        gen_weights_transposed(L + m.off.w2, f, d, mix_seed(seed, base + 5), fac[5], rescale, s_compute_);
+        gen_weights_transposed(L + o.wproj, d, d, mix_seed(seed, base + 3), fac[3], rescale, s_compute_);
+        gen_weights_transposed(L + o.w1, d, f, mix_seed(seed, base + 4), fac[4], rescale, s_compute_);
+        gen_weights_transposed(L + o.w2, f, d, mix_seed(seed, base + 5), fac[5], rescale, s_compute_);
         if (m.opt()) {
-            const size_t n = m.LE - m.off.bqkv;
-            std::vector<uint16_t> ex(m.LE);
+            const size_t n = m.LEF - o.bqkv;
+            std::vector<uint16_t> ex(m.LEF);
             generate_layer_extras(cfg_, seed, l, ex.data());
-            HC_CUDA(cudaMemcpyAsync(L + m.off.bqkv, ex.data() + m.off.bqkv, n * 2, cudaMemcpyHostToDevice, s_compute_));
+            HC_CUDA(cudaMemcpyAsync(L + o.bqkv, ex.data() + o.bqkv, n * 2, cudaMemcpyHostToDevice, s_compute_));
             HC_CUDA(cudaStreamSynchronize(s_compute_));  // ex is pageable and goes out of scope
         }
     };
     for (int l = 0; l < (m.w_all ? m.L : m.Lw); ++l) {
-        if (m.w_all) {
-            draw_layer(l, m.w_all + static_cast<size_t>(l) * m.LE);
+        bf16* shard = m.w_all ? m.w_all + static_cast<size_t>(l) * m.LE : m.wbuf[l & 1];
+        if (m.tpn == 1) {
+            draw_layer(l, shard);
         } else {
-            draw_layer(l, m.wbuf[l & 1]);
-            HC_CUDA(cudaMemcpyAsync(m.h_w + static_cast<size_t>(l) * m.LE, m.wbuf[l & 1], m.LE * 2,
-                                    cudaMemcpyDeviceToHost, s_compute_));
+            draw_layer(l, m.wfull);
+            m.extract_shard(m.wfull, shard, cudaMemcpyDeviceToDevice, s_compute_);
         }
+        if (!m.w_all)
+            HC_CUDA(cudaMemcpyAsync(m.h_w + static_cast<size_t>(l) * m.LE, shard, m.LE * 2, cudaMemcpyDeviceToHost,
+                                    s_compute_));
     }
     HC_CUDA(cudaGetLastError());
     HC_CUDA(cudaStreamSynchronize(s_compute_));
+    if (m.wfull) {
+        HC_CUDA(cudaFree(m.wfull));
+        m.wfull = nullptr;
+    }
 }
 
 void Engine::init(const ModelConfig& c, int w_max_seq, const uint16_t* emb, const uint16_t* pos, const uint16_t* lnf,
@@ -322,9 +396,19 @@ void Engine::init(const ModelConfig& c, int w_max_seq, const uint16_t* emb, cons
     m.max_blocks = (m.max_seq + m.tpb - 1) / m.tpb;
     m.Lp = opt_.host_layers > 0 ? std::min(opt_.host_layers, m.L) : m.L;
     m.Lw = opt_.weight_layers > 0 ? std::min(opt_.weight_layers, m.L) : m.L;
-    m.off = LayerOffsets::of(cfg_, m.arch);
+    m.tp = opt_.tp;
+    m.tpn = m.tp ? m.tp->size() : 1;
+    m.tpr = m.tp ? m.tp->rank() : 0;
+    if (m.H % m.tpn || m.f % m.tpn) throw InputError("tensor parallel size must divide num_heads and ffn_dim");
+    m.Hg = m.H / m.tpn;
+    m.dg = m.d / m.tpn;
+    m.fg = m.f / m.tpn;
+    if (m.dg % 64 || m.fg % 64) throw InputError("tensor parallel: per-rank hidden / ffn slices must be multiples of 64");
+    m.off = LayerOffsets::of(cfg_, m.arch, m.tpn);
+    m.offF = LayerOffsets::of(cfg_, m.arch, 1);
     m.LE = m.off.total;
-    m.kvb = static_cast<size_t>(2) * m.d * m.tpb;
+    m.LEF = m.offF.total;
+    m.kvb = static_cast<size_t>(2) * m.dg * m.tpb;  // this rank's heads of a KV block
     m.actb = static_cast<size_t>(m.d) * m.tpb;
 
     HC_CUDA(cudaStreamCreateWithFlags(&s_compute_, cudaStreamNonBlocking));
@@ -350,19 +434,42 @@ void Engine::init(const ModelConfig& c, int w_max_seq, const uint16_t* emb, cons
         m.xn = dalloc<bf16>(static_cast<size_t>(m.B) * m.d);
     }
 
-    // weights (fill_layer == nullptr: the caller draws them on the device)
+    // weights (fill_layer == nullptr: the caller draws them on the device);
+    // fill_layer delivers the unsharded layer, cut to the rank's shard here
+    if (m.tpn > 1) m.wfull = dalloc<bf16>(m.LEF);
+    std::vector<uint16_t> tmp(fill_layer && m.tpn > 1 ? m.LEF : 0);
+    auto place = [&](int l, void* dst, cudaMemcpyKind kind) {
+        fill_layer(ctx, l, tmp.data());
+        HC_CUDA(cudaMemcpy(m.wfull, tmp.data(), m.LEF * 2, cudaMemcpyHostToDevice));
+        m.extract_shard(m.wfull, dst, kind, s_compute_);
+        HC_CUDA(cudaStreamSynchronize(s_compute_));
+    };
     if (opt_.weights_on_device) {
         m.w_all = dalloc<bf16>(m.LE * m.L);
-        std::vector<uint16_t> tmp(fill_layer ? m.LE : 0);
+        std::vector<uint16_t> t1(fill_layer && m.tpn == 1 ? m.LE : 0);
         for (int l = 0; fill_layer && l < m.L; ++l) {
-            fill_layer(ctx, l, tmp.data());
-            HC_CUDA(cudaMemcpy(m.w_all + static_cast<size_t>(l) * m.LE, tmp.data(), m.LE * 2, cudaMemcpyHostToDevice));
+            bf16* dst = m.w_all + static_cast<size_t>(l) * m.LE;
+            if (m.tpn > 1) {
+                place(l, dst, cudaMemcpyDeviceToDevice);
+            } else {
+                fill_layer(ctx, l, t1.data());
+                HC_CUDA(cudaMemcpy(dst, t1.data(), m.LE * 2, cudaMemcpyHostToDevice));
+            }
         }
     } else {
         m.h_w = halloc<uint16_t>(m.LE * m.Lw, false);
-        for (int l = 0; fill_layer && l < m.Lw; ++l) fill_layer(ctx, l, m.h_w + static_cast<size_t>(l) * m.LE);
+        for (int l = 0; fill_layer && l < m.Lw; ++l) {
+            if (m.tpn > 1)
+                place(l, m.h_w + static_cast<size_t>(l) * m.LE, cudaMemcpyDeviceToHost);
+            else
+                fill_layer(ctx, l, m.h_w + static_cast<size_t>(l) * m.LE);
+        }
         m.wbuf[0] = dalloc<bf16>(m.LE);
         m.wbuf[1] = dalloc<bf16>(m.LE);
+    }
+    if (fill_layer && m.wfull) {
+        HC_CUDA(cudaFree(m.wfull));
+        m.wfull = nullptr;
     }
 
     // decode scratch
@@ -388,6 +495,8 @@ void Engine::configure_cache(const PoolCaps& caps, bool kv_on_gpu, CacheMode mod
         throw ConfigError("Engine: recompute_ratio must lie in [0, 1]");
     if (mode == CacheMode::Hybrid && alloc.act_host + alloc.kv_host <= 0)
         throw ConfigError("Engine: hybrid mode needs a nonempty host allocation (ratio target)");
+    if (mode == CacheMode::TokenRecompute && m.tpn > 1)
+        throw ConfigError("Engine: the token-recompute baseline runs without tensor parallelism");
     HC_CUDA(cudaDeviceSynchronize());
     for (bf16** p : {&m.kv_gpu, &m.act_gpu, &m.kvr, &m.kv_stage[0], &m.kv_stage[1], &m.act_stage[0], &m.act_stage[1]}) {
         if (*p) cudaFree(*p);
@@ -423,13 +532,14 @@ void Engine::configure_cache(const PoolCaps& caps, bool kv_on_gpu, CacheMode mod
     assigner_ = std::make_unique<BlockAssigner>(*cache_, token_mode_ ? CacheMode::KvOnly : mode, alloc, 0.0);
     m.kv_gpu = dalloc<bf16>(static_cast<size_t>(m.L) * m.kv_gpu_cap * m.kvb);
     m.act_gpu = dalloc<bf16>(static_cast<size_t>(m.L) * m.act_gpu_cap * m.actb);
+    m.act_cap_n = (m.act_host_cap + m.tpn - 1) / m.tpn;
     m.kv_host = halloc<bf16>(static_cast<size_t>(m.Lp) * m.kv_host_cap * m.kvb, true);
-    m.act_host = halloc<bf16>(static_cast<size_t>(m.Lp) * m.act_host_cap * m.actb, true);
+    m.act_host = halloc<bf16>(static_cast<size_t>(m.Lp) * m.act_cap_n * m.actb, true);
     for (int s = 0; s < 2; ++s) {
         m.kv_stage[s] = dalloc<bf16>(static_cast<size_t>(m.kv_host_cap) * m.kvb);
-        m.act_stage[s] = dalloc<bf16>(static_cast<size_t>(m.act_host_cap) * m.actb);
+        m.act_stage[s] = dalloc<bf16>(static_cast<size_t>(m.tpn) * m.act_cap_n * m.actb);
     }
-    m.kvr = dalloc<bf16>(static_cast<size_t>(m.act_gpu_cap + m.act_host_cap) * m.kvb);
+    m.kvr = dalloc<bf16>(static_cast<size_t>(m.act_gpu_cap + m.tpn * m.act_cap_n) * m.kvb);
     m.pools_filled = false;
     HC_CUDA(cudaDeviceSynchronize());
 }
@@ -477,7 +587,7 @@ Engine::~Engine() {
                     (void*)m.act_stage[1], (void*)m.x[0], (void*)m.x[1], (void*)m.qkvb, (void*)m.att, (void*)m.proj,
                     (void*)m.hbuf, (void*)m.logits, (void*)m.amax, (void*)m.attn_work, (void*)m.d_meta,
                     (void*)m.px[0], (void*)m.px[1], (void*)m.pqkv, (void*)m.patt, (void*)m.pproj, (void*)m.ph,
-                    (void*)m.tr_kv, (void*)m.splitk_ws, (void*)m.lnf, (void*)m.xn, (void*)m.pxn})
+                    (void*)m.tr_kv, (void*)m.splitk_ws, (void*)m.lnf, (void*)m.xn, (void*)m.pxn, (void*)m.red})
         if (p) cudaFree(p);
     for (void* p : {(void*)m.h_w, (void*)m.kv_host, (void*)m.act_host, (void*)m.h_meta})
         if (p) cudaFreeHost(p);
@@ -499,6 +609,7 @@ Engine::~Engine() {
 void Engine::run_layers(int T, int l0, int l1, const int* d_cu, uint16_t* layer_inputs, uint16_t* k, uint16_t* v,
                         uint16_t* out, bool final_ln) {
     Impl& m = *impl_;
+    if (m.tpn > 1) throw ConfigError("forward_trace / layer_forward run on an engine without tensor parallelism");
     const size_t per = static_cast<size_t>(T) * m.d;
     std::vector<uint16_t> qkv_h((k || v) ? static_cast<size_t>(T) * 3 * m.d : 0);
     for (int l = l0; l < l1; ++l) {
@@ -561,6 +672,7 @@ void gemm_rows(int epi, const bf16* A, int M, int K, const bf16* W, int N, void*
 // ---------------------------------------------------------------------------
 void Engine::prefill(const std::vector<std::string>& ids, const std::vector<std::vector<int>>& prompts) {
     Impl& m = *impl_;
+    HC_CUDA(cudaSetDevice(opt_.device));
     if (ids.size() != prompts.size()) throw InputError("prefill: ids and prompts differ in length");
     {
         std::unordered_set<std::string> seen;
@@ -610,10 +722,12 @@ void Engine::prefill(const std::vector<std::string>& ids, const std::vector<std:
         for (const auto& e : cache_->table(ids[r]).entries) {
             const bool gpu = e.location == Location::GpuMem;
             if (e.kind == BlockKind::ACT) {
-                a_src.push_back(row);
-                a_n.push_back(e.filled_tokens);
-                a_ref.push_back(pack_ref(gpu ? R_ACT_GPU : R_ACT_STAGE, e.pbn));
-                if (!gpu) acth.push_back(e.pbn);
+                if (gpu || m.owns(e.pbn)) {  // a host ACT block is written by its owning rank only
+                    a_src.push_back(row);
+                    a_n.push_back(e.filled_tokens);
+                    a_ref.push_back(pack_ref(gpu ? R_ACT_GPU : R_ACT_STAGE, gpu ? e.pbn : m.act_pos(e.pbn)));
+                    if (!gpu) acth.push_back(e.pbn / m.tpn);
+                }
             } else {
                 c.k_src.push_back(row - c.row0);
                 c.k_n.push_back(e.filled_tokens);
@@ -706,14 +820,16 @@ void Engine::prefill(const std::vector<std::string>& ids, const std::vector<std:
             m.span_end(profile_, s_compute_);
             BlockScatter sk = sa;
             sk.src = m.pqkv;
-            sk.ld = 3 * m.d;
+            sk.ld = 3 * m.dg;
+            sk.d = m.dg;
+            sk.H = m.Hg;
             sk.src_row = dm + c.o_ks;
             sk.n_tok = dm + c.o_kn;
             sk.dst_ref = dm + c.o_kr;
             sk.n_blocks = static_cast<int>(c.k_src.size());
             scatter_kv_blocks(sk, s_compute_);
             m.span_begin(profile_, s_compute_, 1);
-            prefill_attention(m.pqkv, m.patt, dm + c.o_cu, c.n, c.max_len, m.H, m.hd, scale, s_compute_);
+            prefill_attention(m.pqkv, m.patt, dm + c.o_cu, c.n, c.max_len, m.Hg, m.hd, scale, s_compute_);
             m.span_end(profile_, s_compute_);
             m.span_begin(profile_, s_compute_, 2);
             m.tail(W, m.patt, cin, c.rows, m.pproj, m.patt, m.ph, cout, s_compute_);
@@ -725,11 +841,12 @@ void Engine::prefill(const std::vector<std::string>& ids, const std::vector<std:
             HC_CUDA(cudaStreamWaitEvent(s_store_, m.consumed[slot]));
             m.span_begin(profile_, s_store_, 4);
             const size_t lp = static_cast<size_t>(l % m.Lp);
+            const bf16* own = m.act_stage[slot] + static_cast<size_t>(m.tpr) * m.act_cap_n * m.actb;
             for (const Run& r : act_runs) {
                 const size_t bytes = static_cast<size_t>(r.count) * m.actb * 2;
-                HC_CUDA(cudaMemcpyAsync(m.act_host + (lp * m.act_host_cap + r.start) * m.actb,
-                                        m.act_stage[slot] + static_cast<size_t>(r.start) * m.actb, bytes,
-                                        cudaMemcpyDeviceToHost, s_store_));
+                HC_CUDA(cudaMemcpyAsync(m.act_host + (lp * m.act_cap_n + r.start) * m.actb,
+                                        own + static_cast<size_t>(r.start) * m.actb, bytes, cudaMemcpyDeviceToHost,
+                                        s_store_));
                 st.d2h_bytes += bytes;
             }
             for (const Run& r : kv_runs) {
@@ -790,7 +907,7 @@ void Engine::admit_synthetic(const std::vector<std::string>& ids, const std::vec
     fill(m.kv_gpu, static_cast<size_t>(m.L) * m.kv_gpu_cap * m.kvb, seed + 1);
     fill(m.act_gpu, static_cast<size_t>(m.L) * m.act_gpu_cap * m.actb, seed + 2);
     fill(m.kv_host, static_cast<size_t>(m.Lp) * m.kv_host_cap * m.kvb, seed + 3);
-    fill(m.act_host, static_cast<size_t>(m.Lp) * m.act_host_cap * m.actb, seed + 4);
+    fill(m.act_host, static_cast<size_t>(m.Lp) * m.act_cap_n * m.actb, seed + 4);
     HC_CUDA(cudaGetLastError());
     HC_CUDA(cudaStreamSynchronize(s_compute_));
     m.pools_filled = true;
@@ -816,6 +933,7 @@ long Engine::recompute_prefix_len(const std::string& id) const {
 void Engine::decode_step(const std::vector<std::string>& ids, const int* tokens, uint16_t* x_out, float* logits_out,
                          int* argmax_out) {
     Impl& m = *impl_;
+    HC_CUDA(cudaSetDevice(opt_.device));  // the calling thread may differ from the constructing one
     const int n = static_cast<int>(ids.size());
     if (n == 0) return;
     if (n > m.B) throw InputError("decode_step: batch larger than max_batch");
@@ -833,7 +951,9 @@ void Engine::decode_step(const std::vector<std::string>& ids, const int* tokens,
     // grow every context by this step's token (sim.cpp:308-310)
     std::vector<int> act_dev(n, -1), act_host(n, -1), kv_dev(n, -1), kv_host(n, -1), tok(n, 0), nblk(n), ctx(n);
     std::vector<int> refs(static_cast<size_t>(n) * m.max_blocks, 0);
-    std::vector<int> kvh_pbns, acth_pbns, actg_pbns;
+    // acth_pos: staging positions of every ACT/host block (recompute tiles);
+    // acth_own: host-pool indices of the ones this rank streams (pbn % tpn == tpr)
+    std::vector<int> kvh_pbns, acth_pos, acth_own, actg_pbns;
     bool any_act = false, any_kv = false;
     // token-recompute prefixes: rows of a batched causal forward rebuilt
     // through every layer each step (the FlexGen-style baseline, sim.cpp:196-206)
@@ -869,8 +989,8 @@ void Engine::decode_step(const std::vector<std::string>& ids, const int* tokens,
         tok[b] = s.token_index;
         if (e.kind == BlockKind::ACT) {
             any_act = true;
-            act_dev[b] = pack_ref(gpu ? R_ACT_GPU : R_ACT_STAGE, e.pbn);
-            if (!gpu) act_host[b] = pack_ref(R_ACT_HOST, e.pbn);
+            act_dev[b] = pack_ref(gpu ? R_ACT_GPU : R_ACT_STAGE, gpu ? e.pbn : m.act_pos(e.pbn));
+            if (!gpu && m.owns(e.pbn)) act_host[b] = pack_ref(R_ACT_HOST, e.pbn / m.tpn);
         } else {
             any_kv = true;
             kv_dev[b] = pack_ref(gpu ? R_KV_GPU : R_KV_STAGE, e.pbn);
@@ -887,19 +1007,24 @@ void Engine::decode_step(const std::vector<std::string>& ids, const int* tokens,
             if (en.kind == BlockKind::KV) {
                 rb[i] = pack_ref(g ? R_KV_GPU : R_KV_STAGE, en.pbn);
                 if (!g) kvh_pbns.push_back(en.pbn);
+            } else if (g) {
+                rb[i] = pack_ref(R_KVR, en.pbn);
+                actg_pbns.push_back(en.pbn);
             } else {
-                rb[i] = pack_ref(R_KVR, g ? en.pbn : static_cast<int>(m.act_gpu_cap) + en.pbn);
-                (g ? actg_pbns : acth_pbns).push_back(en.pbn);
+                rb[i] = pack_ref(R_KVR, static_cast<int>(m.act_gpu_cap) + m.act_pos(en.pbn));
+                acth_pos.push_back(m.act_pos(en.pbn));
+                if (m.owns(en.pbn)) acth_own.push_back(en.pbn / m.tpn);
             }
         }
     }
     const std::vector<Run> kv_runs = runs_of(kvh_pbns);
-    const std::vector<Run> act_runs = runs_of(acth_pbns);
-    const std::vector<int> tiles_h = tiles_of(acth_pbns, m.tpb);
+    const std::vector<Run> act_runs = runs_of(acth_own);
+    const std::vector<int> tiles_h = tiles_of(acth_pos, m.tpb);
+    const bool gather_act = m.tpn > 1 && !acth_pos.empty();
     const std::vector<int> tiles_g = tiles_of(actg_pbns, m.tpb);
     const int max_ctx = *std::max_element(ctx.begin(), ctx.end());
-    const int splits = attention_splits(n, m.H, max_ctx, m.tpb);
-    if (splits > 1) m.ensure_attn_work(static_cast<size_t>(n) * m.H * splits * (m.hd + 2));
+    const int splits = attention_splits(n, m.Hg, max_ctx, m.tpb);
+    if (splits > 1) m.ensure_attn_work(static_cast<size_t>(n) * m.Hg * splits * (m.hd + 2));
 
     // one upload of all step metadata
     std::vector<int> meta;
@@ -920,7 +1045,7 @@ void Engine::decode_step(const std::vector<std::string>& ids, const int* tokens,
     StepStats st{};
     m.pev_used = 0;
     m.spans.clear();
-    const bool stream_any = !m.w_all || !kv_runs.empty() || !act_runs.empty();
+    const bool stream_any = !m.w_all || !kv_runs.empty() || !act_runs.empty() || gather_act;
     HC_CUDA(cudaEventRecord(m.ev0, s_compute_));
     HC_CUDA(cudaMemcpyAsync(m.d_meta, m.h_meta, meta.size() * 4, cudaMemcpyHostToDevice, s_compute_));
     embed(m.emb, m.pos, dm + o_tok, dm + o_pos, n, m.d, m.x[0], m.d, s_compute_);
@@ -946,13 +1071,17 @@ void Engine::decode_step(const std::vector<std::string>& ids, const int* tokens,
                 st.h2d_bytes += m.LE * 2.0;
             }
             const size_t lp = static_cast<size_t>(l % m.Lp);
+            bf16* own = m.act_stage[slot] + static_cast<size_t>(m.tpr) * m.act_cap_n * m.actb;
             for (const Run& r : act_runs) {
                 const size_t bytes = static_cast<size_t>(r.count) * m.actb * 2;
-                HC_CUDA(cudaMemcpyAsync(m.act_stage[slot] + static_cast<size_t>(r.start) * m.actb,
-                                        m.act_host + (lp * m.act_host_cap + r.start) * m.actb, bytes,
+                HC_CUDA(cudaMemcpyAsync(own + static_cast<size_t>(r.start) * m.actb,
+                                        m.act_host + (lp * m.act_cap_n + r.start) * m.actb, bytes,
                                         cudaMemcpyHostToDevice, s_copy_));
                 st.h2d_bytes += bytes;
             }
+            // every rank streamed its 1/tpn of the ACT blocks; NVLink all-gather
+            // completes the staging (the recompute needs all of X for its heads)
+            if (gather_act) m.tp->copy_channel()->all_gather(own, m.act_stage[slot], m.act_cap_n * m.actb, s_copy_);
             for (const Run& r : kv_runs) {
                 const size_t bytes = static_cast<size_t>(r.count) * m.kvb * 2;
                 HC_CUDA(cudaMemcpyAsync(m.kv_stage[slot] + static_cast<size_t>(r.start) * m.kvb,
@@ -1008,7 +1137,7 @@ void Engine::decode_step(const std::vector<std::string>& ids, const int* tokens,
         AppendCall ap;
         std::copy(R, R + 16, ap.region);
         ap.B = n;
-        ap.d = m.d;
+        ap.d = m.d;  // ACT rows are full width; K|V slots below are this rank's heads
         ap.H = m.H;
         ap.hd = m.hd;
         ap.tpb = m.tpb;
@@ -1030,20 +1159,20 @@ void Engine::decode_step(const std::vector<std::string>& ids, const int* tokens,
             c.epi = gemm::kKvPaged;
             c.A = which == 0 ? m.act_stage[slot] : R[R_ACT_GPU];
             c.lda = m.d;
-            c.a_rows = static_cast<int>((which == 0 ? m.act_host_cap : m.act_gpu_cap) * m.tpb);
-            c.B = W + m.off.wqkv + static_cast<size_t>(m.d) * m.d;  // rows d..3d of Wqkv^T = [Wk|Wv]^T
+            c.a_rows = static_cast<int>((which == 0 ? m.tpn * m.act_cap_n : m.act_gpu_cap) * m.tpb);
+            c.B = W + m.off.wqkv + static_cast<size_t>(m.dg) * m.d;  // rows dg..3dg of Wqkv^T = [Wk|Wv]^T (own heads)
             c.ldb = m.d;
             c.M = c.a_rows;
-            c.N = 2 * m.d;
+            c.N = 2 * m.dg;
             c.K = m.d;
             c.m_tile_rows = dm + (which == 0 ? o_th : o_tg);
             c.num_m_tiles = static_cast<int>(tl.size());
             c.out = m.kvr;
             c.tpb = m.tpb;
-            c.d = m.d;
+            c.d = m.dg;
             c.hd = m.hd;
             c.blk_off = which == 0 ? static_cast<int>(m.act_gpu_cap) : 0;
-            c.bias = m.bias(W, m.off.bqkv + m.d);  // [b_k | b_v]
+            c.bias = m.bias(W, m.off.bqkv + m.dg);  // [b_k | b_v] of the own heads
             m.span_begin(profile_, s_compute_, 0);
             run_gemm(c, s_compute_);
             m.span_end(profile_, s_compute_);
@@ -1055,7 +1184,9 @@ void Engine::decode_step(const std::vector<std::string>& ids, const int* tokens,
         m.span_end(profile_, s_compute_);
         if (any_kv) {  // new token's K|V -> its KV slot (device + host)
             ap.src = m.qkvb;
-            ap.ld = 3 * m.d;
+            ap.ld = 3 * m.dg;
+            ap.d = m.dg;
+            ap.H = m.Hg;
             ap.dev_ref = dm + o_kd;
             ap.host_ref = dm + o_kh;
             kv_append(ap, s_compute_);
@@ -1063,7 +1194,7 @@ void Engine::decode_step(const std::vector<std::string>& ids, const int* tokens,
         }
         AttnCall a;
         a.q = m.qkvb;
-        a.ldq = 3 * m.d;
+        a.ldq = 3 * m.dg;
         a.out = m.att;
         a.blk_ref = dm + o_ref;
         a.n_blocks = dm + o_nb;
@@ -1071,7 +1202,7 @@ void Engine::decode_step(const std::vector<std::string>& ids, const int* tokens,
         a.max_blocks = m.max_blocks;
         for (int i = 0; i < 16; ++i) a.region[i] = R[i];
         a.B = n;
-        a.H = m.H;
+        a.H = m.Hg;
         a.hd = m.hd;
         a.tpb = m.tpb;
         a.scale = scale;
@@ -1150,7 +1281,7 @@ void Engine::decode_step(const std::vector<std::string>& ids, const int* tokens,
     }
     for (int b = 0; b < n; ++b) {
         if (act_host[b] >= 0) st.d2h_bytes += static_cast<double>(m.d) * 2 * m.L;
-        if (kv_host[b] >= 0) st.d2h_bytes += static_cast<double>(m.d) * 4 * m.L;
+        if (kv_host[b] >= 0) st.d2h_bytes += static_cast<double>(m.dg) * 4 * m.L;
     }
     stats_ = st;
 }
@@ -1183,6 +1314,8 @@ void Engine::read_block(BlockKind kind, Location loc, int pbn, int layer, uint16
     const long cap = kv ? (loc == Location::GpuMem ? m.kv_gpu_cap : m.kv_host_cap)
                         : (loc == Location::GpuMem ? m.act_gpu_cap : m.act_host_cap);
     if (pbn < 0 || pbn >= cap) throw InputError("read_block: pbn out of range");
+    const bool act_host = !kv && loc == Location::HostMem;
+    if (act_host && !m.owns(pbn)) throw InputError("read_block: ACT block owned by another tensor-parallel rank");
     const size_t be = kv ? m.kvb : m.actb;
     HC_CUDA(cudaStreamSynchronize(s_compute_));
     if (loc == Location::GpuMem) {
@@ -1190,7 +1323,9 @@ void Engine::read_block(BlockKind kind, Location loc, int pbn, int layer, uint16
         HC_CUDA(cudaMemcpy(out, base + (static_cast<size_t>(layer) * cap + pbn) * be, be * 2, cudaMemcpyDeviceToHost));
     } else {
         const bf16* base = kv ? m.kv_host : m.act_host;
-        std::memcpy(out, base + (static_cast<size_t>(layer % m.Lp) * cap + pbn) * be, be * 2);
+        const long hcap = kv ? cap : m.act_cap_n;
+        const int idx = kv ? pbn : pbn / m.tpn;
+        std::memcpy(out, base + (static_cast<size_t>(layer % m.Lp) * hcap + idx) * be, be * 2);
     }
 }
 
@@ -1199,9 +1334,10 @@ double Engine::time_kv_gen(int n_tokens, int reps) {
     Impl& m = *impl_;
     if (n_tokens <= 0) throw InputError("time_kv_gen: n_tokens must be positive");
     // recompute GEMM over n tokens of the ACT staging (or GPU) pool, layer 0
-    const long cap_rows = std::max(m.act_host_cap, m.act_gpu_cap) * m.tpb;
+    const long stage_rows = static_cast<long>(m.tpn) * m.act_cap_n * m.tpb;
+    const long cap_rows = std::max(stage_rows, m.act_gpu_cap * m.tpb);
     if (n_tokens > cap_rows) throw InputError("time_kv_gen: more tokens than the ACT pools hold");
-    const bf16* A = m.act_host_cap * m.tpb >= n_tokens ? m.act_stage[0] : m.act_gpu;
+    const bf16* A = stage_rows >= n_tokens ? m.act_stage[0] : m.act_gpu;
     if (!m.w_all)
         HC_CUDA(cudaMemcpy(m.wbuf[0], m.h_w, m.LE * 2, cudaMemcpyHostToDevice));
     const bf16* W = m.layer_w(0, 0);
@@ -1215,18 +1351,18 @@ double Engine::time_kv_gen(int n_tokens, int reps) {
     c.A = A;
     c.lda = m.d;
     c.a_rows = static_cast<int>(cap_rows);
-    c.B = W + m.off.wqkv + static_cast<size_t>(m.d) * m.d;
+    c.B = W + m.off.wqkv + static_cast<size_t>(m.dg) * m.d;
     c.ldb = m.d;
     c.M = n_tokens;
-    c.N = 2 * m.d;
+    c.N = 2 * m.dg;
     c.K = m.d;
     c.m_tile_rows = m.d_meta;
     c.num_m_tiles = static_cast<int>(tiles.size());
     c.out = m.kvr;
     c.tpb = m.tpb;
-    c.d = m.d;
+    c.d = m.dg;
     c.hd = m.hd;
-    c.bias = m.bias(W, m.off.bqkv + m.d);
+    c.bias = m.bias(W, m.off.bqkv + m.dg);
     run_gemm(c, s_compute_);  // warm-up
     HC_CUDA(cudaEventRecord(m.ev0, s_compute_));
     for (int i = 0; i < reps; ++i) run_gemm(c, s_compute_);

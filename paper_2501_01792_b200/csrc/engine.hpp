@@ -34,6 +34,7 @@
 #include "host/cache.hpp"
 #include "host/model.hpp"
 #include "kernels/kernels.hpp"
+#include "tp.hpp"
 
 namespace hc {
 
@@ -53,6 +54,7 @@ struct EngineOptions {
     int max_prefill_tokens = 65536;
     int device = 0;
     int arch = kArchReference;    // decoder layer variant (host/model.hpp); from the weights when given
+    TpGroup* tp = nullptr;        // head-sharded tensor parallelism (tp.hpp); nullptr = one GPU holds all heads
 };
 
 struct StepStats {

@@ -72,19 +72,20 @@ void rescale_factors(const ModelConfig& c, double out[6]) {
     out[5] = 10.0 * std::sqrt(3.0 * std::sqrt(2.0) / f);
 }
 
-LayerOffsets LayerOffsets::of(const ModelConfig& c, int arch) {
-    const size_t d = c.hidden_dim, f = c.ffn_dim;
+LayerOffsets LayerOffsets::of(const ModelConfig& c, int arch, int tp) {
+    if (tp < 1 || c.num_heads % tp || c.ffn_dim % tp) throw InputError("tensor parallel size must divide heads and ffn_dim");
+    const size_t d = c.hidden_dim, f = c.ffn_dim, dg = d / tp, fg = f / tp;
     LayerOffsets o;
     o.wqkv = 0;
-    o.wproj = 3 * d * d;
-    o.w1 = o.wproj + d * d;
-    o.w2 = o.w1 + f * d;
-    o.total = o.w2 + d * f;
+    o.wproj = 3 * dg * d;
+    o.w1 = o.wproj + d * dg;
+    o.w2 = o.w1 + fg * d;
+    o.total = o.w2 + d * fg;
     if (arch == kArchOpt) {
         o.bqkv = o.total;
-        o.bproj = o.bqkv + 3 * d;
+        o.bproj = o.bqkv + 3 * dg;
         o.b1 = o.bproj + d;
-        o.b2 = o.b1 + f;
+        o.b2 = o.b1 + fg;
         o.ln1g = o.b2 + d;
         o.ln1b = o.ln1g + d;
         o.ln2g = o.ln1b + d;

@@ -93,7 +93,10 @@ struct LayerOffsets {
     size_t wqkv, wproj, w1, w2;
     size_t bqkv = 0, bproj = 0, b1 = 0, b2 = 0, ln1g = 0, ln1b = 0, ln2g = 0, ln2b = 0;
     size_t total;
-    static LayerOffsets of(const ModelConfig& c, int arch = kArchReference);
+    // tp > 1: the rank's shard of the head-sharded variant (tp.hpp):
+    // Wqkv^T [3d/tp x d] | Wproj^T [d x d/tp] | W1^T [f/tp x d] | W2^T [d x f/tp]
+    // | b_qkv [3d/tp] | b_o [d] | b_1 [f/tp] | b_2 [d] | LayerNorms [4d]
+    static LayerOffsets of(const ModelConfig& c, int arch = kArchReference, int tp = 1);
 };
 
 // DecoderWeights::generate (model.cpp:94-117) + rescale + bf16 + transpose.

@@ -188,7 +188,8 @@ void run_gemm(const GemmCall& c, cudaStream_t st) {
     if (cc.a_rows <= 0) cc.a_rows = c.M;
     int bn = c.bn ? c.bn : pick_bn(p.num_m_tiles, c.N);
     const bool can_split = c.ws && c.ws_floats && !c.m_tile_rows && p.num_m_tiles <= 2 &&
-                           (c.epi == gemm::kStore || c.epi == gemm::kRelu) && c.ldc == c.N && (!c.bn || c.splits);
+                           (c.epi == gemm::kStore || c.epi == gemm::kRelu || c.epi == gemm::kF32) && c.ldc == c.N &&
+                           (!c.bn || c.splits);
     if (can_split) {
         int s = 1;
         if (c.splits)
@@ -236,7 +237,9 @@ void run_gemm(const GemmCall& c, cudaStream_t st) {
         case 256: dispatch_epi<256>(cc, p, st); break;
         default: throw std::invalid_argument("gemm: bn must be 32/64/128/256");
     }
-    if (p.splits > 1)
+    if (p.splits > 1 && c.epi == gemm::kF32)
+        splitk_reduce_f32(c.ws, p.splits, c.M, c.N, static_cast<float*>(c.out), st);
+    else if (p.splits > 1)
         splitk_reduce(c.ws, p.splits, c.M, c.N, static_cast<bf16*>(c.out), c.epi == gemm::kRelu, st, c.bias, c.res,
                       c.ldr);
 }

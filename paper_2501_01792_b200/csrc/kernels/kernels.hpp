@@ -117,6 +117,15 @@ void scatter_kv_blocks(const BlockScatter& c, cudaStream_t st);
 void layernorm_rows(const bf16* x, long long ldx, const bf16* gamma, const bf16* beta, bf16* y, long long ldy, int n,
                     int d, float eps, cudaStream_t st);
 
+// out[i] = sum_j src[j*n + i] for i < n, j < parts (in-process all-reduce)
+void sum_rows_f32(const float* src, int parts, size_t n, float* out, cudaStream_t st);
+// out[m][n] = bf16(sum[m][n] + bias[n] + res[m*ldr + n]) (bias / res optional):
+// the finish of a tensor-parallel all-reduce (W_proj, W2 partial sums)
+void add_bias_residual(const float* sum, const bf16* bias, const bf16* res, long long ldr, int M, int N, bf16* out,
+                       cudaStream_t st);
+// fp32 split-K finish: out[m][n] = sum_s ws[s][m][n]
+void splitk_reduce_f32(const float* ws, int splits, int M, int N, float* out, cudaStream_t st);
+
 // argmax over each row of fp32 logits [B x V]
 void argmax_rows(const float* logits, int B, int V, int* out, cudaStream_t st);
 

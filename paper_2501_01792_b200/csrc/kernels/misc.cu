@@ -281,7 +281,74 @@ __global__ void __launch_bounds__(kLnThreads)
     }
 }
 
+__global__ void sum_rows_kernel(const float* __restrict__ src, int parts, size_t n, float* __restrict__ out) {
+    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        float acc = 0.f;
+        for (int j = 0; j < parts; ++j) acc += src[j * n + i];
+        out[i] = acc;
+    }
+}
+
+// 8 columns per thread: 2 x float4 of the sum, 16 B of bias and residual
+__global__ void add_bias_residual_kernel(const float* __restrict__ sum, const bf16* __restrict__ bias,
+                                         const bf16* __restrict__ res, long long ldr, int M, int N,
+                                         bf16* __restrict__ out) {
+    const size_t n8 = static_cast<size_t>(M) * N / 8;
+    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n8;
+         i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        const size_t e0 = i * 8;
+        const int row = static_cast<int>(e0 / N), col = static_cast<int>(e0 % N);
+        const float4 a = __ldg(reinterpret_cast<const float4*>(sum + e0));
+        const float4 b = __ldg(reinterpret_cast<const float4*>(sum + e0) + 1);
+        float acc[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+        if (bias) add8(acc, bias + col);
+        if (res) add8(acc, res + static_cast<long long>(row) * ldr + col);
+        uint32_t o[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) o[j] = ptx::pack_bf16x2(acc[2 * j], acc[2 * j + 1]);
+        *reinterpret_cast<uint4*>(out + e0) = make_uint4(o[0], o[1], o[2], o[3]);
+    }
+}
+
+__global__ void splitk_reduce_f32_kernel(const float* __restrict__ ws, int splits, size_t n4, size_t plane,
+                                         float* __restrict__ out) {
+    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n4;
+         i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int s = 0; s < splits; ++s) {
+            const float4 v = __ldg(reinterpret_cast<const float4*>(ws + s * plane) + i);
+            acc.x += v.x;
+            acc.y += v.y;
+            acc.z += v.z;
+            acc.w += v.w;
+        }
+        reinterpret_cast<float4*>(out)[i] = acc;
+    }
+}
+
 }  // namespace
+
+static int grid_for(size_t work) {
+    return static_cast<int>(std::min<size_t>((work + 255) / 256, 4 * static_cast<size_t>(num_sms())));
+}
+
+void sum_rows_f32(const float* src, int parts, size_t n, float* out, cudaStream_t st) {
+    if (n) sum_rows_kernel<<<grid_for(n), 256, 0, st>>>(src, parts, n, out);
+}
+
+void add_bias_residual(const float* sum, const bf16* bias, const bf16* res, long long ldr, int M, int N, bf16* out,
+                       cudaStream_t st) {
+    if (N % 8) throw std::invalid_argument("add_bias_residual: N must be a multiple of 8");
+    const size_t n8 = static_cast<size_t>(M) * N / 8;
+    if (n8) add_bias_residual_kernel<<<grid_for(n8), 256, 0, st>>>(sum, bias, res, ldr, M, N, out);
+}
+
+void splitk_reduce_f32(const float* ws, int splits, int M, int N, float* out, cudaStream_t st) {
+    if (N % 4) throw std::invalid_argument("splitk_reduce_f32: N must be a multiple of 4");
+    const size_t plane = static_cast<size_t>(M) * N;
+    if (plane) splitk_reduce_f32_kernel<<<grid_for(plane / 4), 256, 0, st>>>(ws, splits, plane / 4, plane, out);
+}
 
 void layernorm_rows(const bf16* x, long long ldx, const bf16* gamma, const bf16* beta, bf16* y, long long ldy, int n,
                     int d, float eps, cudaStream_t st) {

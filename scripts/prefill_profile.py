@@ -26,6 +26,7 @@ def main():
     ap.add_argument("--layers", type=int, default=2)
     ap.add_argument("--ratio", type=float, default=1.0 / 3.0)
     ap.add_argument("--reps", type=int, default=2)
+    ap.add_argument("--arch", default="reference", choices=["reference", "opt"])
     a = ap.parse_args()
     from paper_2501_01792_b200 import api
     cfg = api.ModelConfig.preset(a.model)
@@ -37,7 +38,7 @@ def main():
     k = int(round(a.ratio * 1000))
     eng = api.Engine(cfg, seed=42, max_seq=P + 2, rescale=True, max_batch=B, weights_on_device=False,
                      caps=api.PoolCaps(kv_host=B * kv, act_host=B * act), mode="hybrid",
-                     allocation=api.HostAllocation(k, 1000 - k))
+                     allocation=api.HostAllocation(k, 1000 - k), arch=a.arch)
     rng = np.random.default_rng(0)
     prompts = [rng.integers(0, cfg.vocab_size, P).tolist() for _ in range(B)]
     d, f, L = cfg.hidden_dim, cfg.ffn_dim, cfg.num_layers
@@ -51,7 +52,7 @@ def main():
             eng.free_request(i)
     gemm = L * 2.0 * B * P * (4 * d * d + 2 * d * f)
     attn = L * B * 2.0 * d * P * (P + 1)
-    print(json.dumps({"model": a.model, "batch": B, "prompt": P, "layers": L, "prefill_ms": st["step_ms"],
+    print(json.dumps({"model": a.model, "arch": a.arch, "batch": B, "prompt": P, "layers": L, "prefill_ms": st["step_ms"],
                       "gemm_ms": st["gemm_ms"], "attn_ms": st["attn_ms"], "weight_h2d_ms": st["copy_ms"],
                       "block_d2h_ms": st["store_ms"], "gemm_tflops": gemm / st["gemm_ms"] / 1e9,
                       "attn_tflops_causal": attn / st["attn_ms"] / 1e9,

@@ -407,3 +407,123 @@ def test_engine_opt_arch_token_recompute(native):
     res = eng.decode_step(["a", "b"], toks, want_x=True)
     for b in range(2):
         assert rel(f64(res["x"][b]), O.forward_prompt_opt(prompts[b] + [toks[b]], w).output[-1]) <= TOL
+
+
+# ------------------------------------------------- tensor parallel (heads) ---
+def _run_ranks(fns):
+    """Run one callable per tensor-parallel rank concurrently (the in-process
+    group rendezvouses inside prefill / decode_step)."""
+    import threading
+    res, errs = [None] * len(fns), []
+
+    def wrap(i):
+        try:
+            res[i] = fns[i]()
+        except Exception as e:  # noqa: BLE001 — surfaced below
+            errs.append(e)
+
+    ts = [threading.Thread(target=wrap, args=(i,)) for i in range(len(fns))]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join(timeout=300)
+    if errs:
+        raise errs[0]
+    return res
+
+
+@pytest.mark.parametrize("tpn,arch,weights_on_device", [(2, "reference", False), (2, "opt", True),
+                                                        (4, "reference", True), (4, "opt", False)])
+def test_engine_tensor_parallel_matches_oracle(native, tpn, arch, weights_on_device):
+    """Head-sharded variant (§8(e)): rank g holds heads [gH/N, (g+1)H/N), a 1/N
+    FFN slice and the ACT/host blocks with pbn % N == g (streamed by it, then
+    all-gathered); proj / FFN2 partial sums are all-reduced. Every rank's
+    decode output equals the oracle, KV blocks hold the rank's heads of the
+    oracle's K/V, and ACT blocks sit on their owner rank."""
+    from paper_2501_01792_b200.api import HostAllocation, PoolCaps, TensorParallel
+    cfg = small_cfg(L=3, d=256, H=4, f=512, tpb=8)
+    w = oracle_weights(cfg) if arch == "reference" else opt_weights(cfg)
+    rng = np.random.default_rng(31 + tpn)
+    lens = [29, 40, 13]
+    prompts = [rng.integers(0, cfg.vocab_size, n).tolist() for n in lens]
+    steps = [rng.integers(0, cfg.vocab_size, len(lens)).tolist() for _ in range(3)]
+    ids = [f"t{i}" for i in range(len(lens))]
+    group = TensorParallel.local_group(tpn)
+    kw = dict(max_batch=len(lens), caps=PoolCaps(kv_host=24, act_host=24, act_gpu=2), allocation=HostAllocation(1, 1),
+              mode="hybrid", weights_on_device=weights_on_device, max_prefill_tokens=50)
+    engs = [(make_opt_engine if arch == "opt" else make_engine)(cfg, w, tp=group[r], **kw) for r in range(tpn)]
+
+    def rank_fn(eng):
+        def run():
+            eng.prefill(ids, prompts)
+            return [eng.decode_step(ids, t, want_x=True, want_logits=True) for t in steps]
+        return run
+
+    outs = _run_ranks([rank_fn(e) for e in engs])
+    fwd = O.forward_prompt_opt if arch == "opt" else O.forward_prompt
+    seqs = [list(p) for p in prompts]
+    for s, t in enumerate(steps):
+        for b in range(len(lens)):
+            seqs[b].append(t[b])
+            ref = fwd(seqs[b], w).output[-1:]
+            for r in range(tpn):
+                assert rel(f64(outs[r][s]["x"][b]), ref[0]) <= TOL
+                assert rel(outs[r][s]["logits"][b], O.logits_tied(ref, w)[0]) <= TOL
+    # cache contents: KV blocks = the rank's heads; ACT/host blocks on their owner only
+    tpb, d, H = cfg.tokens_per_block, cfg.hidden_dim, cfg.num_heads
+    hd, Hg = d // H, H // tpn
+    for rid, p in zip(ids, prompts):
+        tr = fwd(p, w)
+        row = 0
+        for e in engs[0].cache.table(rid).entries:
+            n = min(e.filled_tokens, len(p) - row)
+            if n <= 0:
+                break
+            for r, eng in enumerate(engs):
+                heads = slice(r * Hg * hd, (r + 1) * Hg * hd)
+                if int(e.kind) == 0:
+                    blk = f64(eng.read_block(e.kind, e.location, e.pbn, 1))
+                    k = blk[0].transpose(1, 0, 2).reshape(tpb, Hg * hd)[:n]
+                    assert rel(k, tr.k[1][row:row + n, heads]) <= TOL
+                elif int(e.location) == 0:  # ACT/host: owner rank pbn % N
+                    if e.pbn % tpn == r:
+                        blk = f64(eng.read_block(e.kind, e.location, e.pbn, 1))
+                        want = tr.act[1] if arch == "opt" else tr.layer_inputs[1]
+                        assert rel(blk[:n], want[row:row + n]) <= TOL
+                    else:
+                        with pytest.raises(Exception):
+                            eng.read_block(e.kind, e.location, e.pbn, 1)
+            row += e.filled_tokens
+    # every rank streamed 1/N of the weights
+    st = [e.last_stats() for e in engs]
+    if not weights_on_device:
+        full = 2 * (4 * d * d + 2 * d * cfg.ffn_dim) * cfg.num_layers
+        assert all(abs(x["h2d_bytes"] - full / tpn) < full / tpn * 0.5 for x in st)
+
+
+def test_engine_tensor_parallel_seeded_shards(native):
+    """Seeded weights drawn unsharded on the GPU and cut per rank equal the
+    matching slices of a single-GPU engine's weights (bit-exact)."""
+    from paper_2501_01792_b200.api import Engine, ModelConfig, PoolCaps, TensorParallel
+    mc = ModelConfig(num_layers=2, hidden_dim=256, num_heads=4, ffn_dim=512, vocab_size=512)
+    full = Engine(mc, seed=5, max_seq=32, caps=PoolCaps(act_gpu=4), mode="act_only", arch="opt")
+    group = TensorParallel.local_group(2)
+    d, f, dg, fg = 256, 512, 128, 256
+    for r in range(2):
+        eng = Engine(mc, seed=5, max_seq=32, caps=PoolCaps(act_gpu=4), mode="act_only", arch="opt", tp=group[r],
+                     weights_on_device=bool(r))
+        for l in range(2):
+            F = full.read_weights(l)
+            o = 0
+            wqkv = F[:3 * d * d].reshape(3, d, d)[:, r * dg:(r + 1) * dg]
+            wproj = F[3 * d * d:4 * d * d].reshape(d, d)[:, r * dg:(r + 1) * dg]
+            w1 = F[4 * d * d:4 * d * d + f * d].reshape(f, d)[r * fg:(r + 1) * fg]
+            w2 = F[4 * d * d + f * d:4 * d * d + 2 * f * d].reshape(d, f)[:, r * fg:(r + 1) * fg]
+            ex = F[4 * d * d + 2 * f * d:]
+            bqkv = ex[:3 * d].reshape(3, d)[:, r * dg:(r + 1) * dg]
+            want = np.concatenate([wqkv.ravel(), wproj.ravel(), w1.ravel(), w2.ravel(), bqkv.ravel(),
+                                   ex[3 * d:4 * d], ex[4 * d + r * fg:4 * d + (r + 1) * fg], ex[4 * d + f:]])
+            got = eng.read_weights(l)[:want.size]
+            assert np.array_equal(got, want), (r, l)
+            o += 1
+        eng.close()
