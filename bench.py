@@ -46,11 +46,17 @@ def parse():
     p.add_argument("--model", default="")
     p.add_argument("--batch", type=int, default=0, help="requests per GPU (config 3 default 128)")
     p.add_argument("--global-batch", type=int, default=0, help="total requests split across ranks (config 4: 128)")
+    p.add_argument("--tp", type=int, default=1,
+                   help="head-sharded tensor parallelism over the torchrun ranks (NCCL): every rank serves the whole "
+                        "global batch for H/N heads and streams 1/N of the weights, KV and ACT bytes")
+    p.add_argument("--tp-emulate", type=int, default=0,
+                   help="time ONE rank of an N-way head-sharded group on this single GPU (collectives skipped, "
+                        "NVLink time modelled) and print a projection line instead of the bench line")
     p.add_argument("--prompt", type=int, default=1024)
     p.add_argument("--gen", type=int, default=256, help="generation length of the workload (config)")
     p.add_argument("--ratio", type=float, default=None,
-                   help="ACT share r of context blocks (default 1/3 = the paper's KV:ACT 2:1 for OPT-30B, "
-                        "PAPER.md:714); -1 = the planner's choice from measured rates")
+                   help="ACT share r of context blocks; default -1 = the planner's choice from measured rates "
+                        "(north-star (5)); 0.3333 = the paper's KV:ACT 2:1 for OPT-30B on an RTX 4090 (PAPER.md:714)")
     p.add_argument("--host-gb", type=float, default=0.0, help="pinned host budget per rank (0: auto)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--arch", default="reference", choices=["reference", "opt"],
@@ -69,9 +75,8 @@ def parse():
     if a.config == 4:
         a.model = a.model or "opt-66b"
         a.global_batch = a.global_batch or 128
-        a.ratio = -1.0 if a.ratio is None else a.ratio
     a.model = a.model or "opt-30b"
-    a.ratio = 1.0 / 3.0 if a.ratio is None else a.ratio
+    a.ratio = -1.0 if a.ratio is None else a.ratio
     a.scaling = "strong" if a.global_batch else "weak"
     return a
 
@@ -308,9 +313,10 @@ def pool_plan(cfg, B, P, steps, r):
     return mode, api.HostAllocation(a, 1000 - a), api.PoolCaps(kv_host=B * kv_per, act_host=B * act_per)
 
 
-def host_layers_for(cfg, caps, budget, w_bytes_pinned):
+def host_layers_for(cfg, caps, budget, w_bytes_pinned, tpn=1):
     from paper_2501_01792_b200 import api
-    per_layer = caps.kv_host * api.HybridCache.bytes_of("KV", cfg) + caps.act_host * api.HybridCache.bytes_of("ACT", cfg)
+    per_layer = (caps.kv_host * api.HybridCache.bytes_of("KV", cfg) +
+                 caps.act_host * api.HybridCache.bytes_of("ACT", cfg)) / tpn  # a TP rank holds 1/N of both
     if per_layer == 0:
         return cfg.num_layers
     return int(min(cfg.num_layers, max(2, (budget - w_bytes_pinned) // per_layer)))
@@ -455,7 +461,7 @@ def run_prefill(eng, cfg, ids, P, rank, tflops_sust, link_gbs):
             "launches": int(st["launches"])}
 
 
-def calibrate_planner(eng, cfg, link_gbs, caps_act_rows, workload_tokens, act_gpu=0):
+def calibrate_planner(eng, cfg, link_gbs, caps_act_rows, workload_tokens, act_gpu=0, tpn=1):
     """North-star (5): measured recompute-GEMM and host-link samples ->
     bundle_from_samples (timing.cpp:172-183) -> plan_host_allocation
     (plan.cpp:106-152) over a WORKLOAD-sized host budget, as the reference's
@@ -468,7 +474,14 @@ def calibrate_planner(eng, cfg, link_gbs, caps_act_rows, workload_tokens, act_gp
     kv = [(float(n), eng.time_kv_gen(n, reps=3)) for n in ns]
     ld = [(float(n), eng.time_load_kv(n, reps=2)) for n in ns]
     bundle = api.bundle_from_samples(kv, ld, link_gbs * 1e9, cfg)
+    if tpn > 1:  # a head-sharded rank streams and stores 1/N of every weight and block
+        bundle.t_load_w /= tpn
+        bundle.s_weight_layer //= tpn
+        bundle.s_weight_total //= tpn
     mem = api.budget_for(0.0, cfg, bundle)
+    if tpn > 1:
+        mem.s_kv_block /= tpn
+        mem.s_act_block /= tpn
     workload_blocks = workload_tokens / cfg.tokens_per_block
     mem.m_host = mem.s_weight + workload_blocks * mem.s_kv_block * 0.9
     alloc = api.plan_host_allocation(bundle, mem, cfg.tokens_per_block, act_gpu)
@@ -485,12 +498,33 @@ def calibrate_planner(eng, cfg, link_gbs, caps_act_rows, workload_tokens, act_gp
             "planned_t_comp_s": api.planned_t_computation(bundle, cfg.tokens_per_block, alloc, act_gpu)}
 
 
+def tp_group(args, world, rank, local, dist):
+    """--tp N: NCCL group over the torchrun ranks (ids from rank 0, broadcast
+    over torch.distributed); --tp-emulate N: one rank's timing stand-in."""
+    from paper_2501_01792_b200 import api
+    if args.tp > 1:
+        if world != args.tp:
+            raise SystemExit("--tp N needs exactly N torchrun ranks")
+        obj = [api.TensorParallel.nccl_unique_ids() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        return api.TensorParallel.nccl(obj[0], rank, world, local), args.tp
+    if args.tp_emulate > 1:
+        return api.TensorParallel.emulated(0, args.tp_emulate), args.tp_emulate
+    return None, 1
+
+
 def our_arm(args, cfg, world, rank, local, dist):
     from paper_2501_01792_b200 import api, kernels
     if kernels.device_count() == 0:
         raise SystemExit("bench needs a CUDA device")
     hbm_peak, tflops_sust, tflops_burst, peak_src = measured_peaks()
-    B, P, L, d = per_rank_batch(args, world, rank), args.prompt, cfg.num_layers, cfg.hidden_dim
+    tp, tpn = tp_group(args, world, rank, local, dist)
+    if tp is not None:  # heads are sharded, requests are not: every rank serves the global batch
+        args.no_sweep = True
+        B = args.global_batch or args.batch or 128
+    else:
+        B = per_rank_batch(args, world, rank)
+    P, L, d = args.prompt, cfg.num_layers, cfg.hidden_dim
     total_steps = args.warmup + args.steps + 2
     max_seq = P + total_steps + 1
     r = args.ratio if args.ratio >= 0 else 1.0 / 3.0  # planner replaces the default below
@@ -500,28 +534,29 @@ def our_arm(args, cfg, world, rank, local, dist):
     # pinned host budget: never more than 120 GB or MemAvailable - 48 GB per node
     # (pinned pages cannot be reclaimed; folding keeps the streamed bytes)
     budget = args.host_gb * 1e9 if args.host_gb > 0 else min(120e9, mem_available_bytes() - 48e9) / local_world
-    Lw = L if L * w_layer <= 0.55 * budget else max(2, int(0.55 * budget // w_layer))
-    Lp = host_layers_for(cfg, caps, budget, Lw * w_layer)
+    w_rank = w_layer / tpn  # pinned weight bytes per layer on this rank
+    Lw = L if L * w_rank <= 0.55 * budget else max(2, int(0.55 * budget // w_rank))
+    Lp = host_layers_for(cfg, caps, budget, Lw * w_rank, tpn)
     t_setup = time.time()
     eng = api.Engine(cfg, seed=42, max_seq=max_seq, rescale=True, max_batch=B, weights_on_device=False,
                      caps=caps, host_layers=Lp, weight_layers=Lw, mode=mode, allocation=alloc, device=local,
-                     arch=args.arch)
-    ids = [f"g{rank}r{i}" for i in range(B)]
+                     arch=args.arch, tp=tp)
+    ids = [f"g{0 if tp else rank}r{i}" for i in range(B)]
     # host-link peak: a large pinned H2D copy on the engine's copy stream
     tpb = cfg.tokens_per_block
     n_tok = min(caps.kv_host * tpb, 65536) if caps.kv_host else 0
-    link_gbs = (n_tok * 2 * d * 2) / eng.time_load_kv(n_tok, reps=3) / 1e9 if n_tok else None
+    link_gbs = (n_tok * 2 * (d // tpn) * 2) / eng.time_load_kv(n_tok, reps=3) / 1e9 if n_tok else None
     # north-star (5): the ratio comes from the planner fed with measured rates
     planner = None
     if link_gbs and caps.act_host:
         try:
-            planner = calibrate_planner(eng, cfg, link_gbs, caps.act_host * tpb, B * (P + args.gen))
+            planner = calibrate_planner(eng, cfg, link_gbs, caps.act_host * tpb, B * (P + args.gen), tpn=tpn)
         except Exception as e:  # planner failure must not kill the bench line
             planner = {"error": str(e)}
     if args.ratio < 0 and planner and "planned_r" in planner:
         r = planner["planned_r"]
         mode, alloc, caps = pool_plan(cfg, B, P, total_steps, r)
-        Lp = host_layers_for(cfg, caps, budget, Lw * w_layer)
+        Lp = host_layers_for(cfg, caps, budget, Lw * w_rank, tpn)
         eng.configure_cache(caps, mode=mode, allocation=alloc, host_layers=Lp)
     setup_s = time.time() - t_setup
     # the cache the decode steps read is built by the real offloaded prefill
@@ -552,7 +587,8 @@ def our_arm(args, cfg, world, rank, local, dist):
 
     dev_s = max_over_ranks(dist, acc["dev_ms"] / 1e3)
     wall_s = max_over_ranks(dist, acc["wall"])
-    tokens_total = sum_over_ranks(dist, float(B * args.steps))
+    # TP ranks produce the same tokens (heads are sharded); batch-partitioned ranks add up
+    tokens_total = float(B * args.steps) if tp is not None else sum_over_ranks(dist, float(B * args.steps))
     value = tokens_total / dev_s
     e2e = tokens_total / wall_s
     ms_per_step = dev_s * 1e3 / args.steps
@@ -573,8 +609,9 @@ def our_arm(args, cfg, world, rank, local, dist):
     # per-step roofline (north_star): slower of link bytes / link BW, tensor
     # FLOPs / tensor peak, HBM bytes / HBM BW
     ctx = P + args.warmup + 1 + args.steps // 2
-    tensor_flops = L * (4.0 * d * d * act_tokens + 2.0 * B * (4 * d * d + 2 * d * cfg.ffn_dim))
-    hbm_bytes = L * (B * (ctx + 1) * 2 * d * 2 + act_tokens * 3 * d * 2 + w_layer) + h2d_step
+    # (a head-sharded rank does 1/N of the FLOPs and HBM traffic)
+    tensor_flops = L * (4.0 * d * d * act_tokens + 2.0 * B * (4 * d * d + 2 * d * cfg.ffn_dim)) / tpn
+    hbm_bytes = L * (B * (ctx + 1) * 2 * d * 2 + act_tokens * 3 * d * 2 + w_layer) / tpn + h2d_step
     t_link = h2d_step / (link_gbs * 1e9) if link_gbs else 0.0
     t_tensor = tensor_flops / (tflops_sust * 1e12)
     t_hbm = hbm_bytes / (hbm_peak * 1e9)
@@ -651,6 +688,28 @@ def our_arm(args, cfg, world, rank, local, dist):
         except Exception as e:
             extra["hbm_tiered"] = {"error": str(e)}
 
+    tp_info = None
+    if tp is not None:
+        # per layer: ACT all-gather (gather stream, overlaps the link and compute)
+        # + two fp32 all-reduces of [B x d] (compute stream, serial)
+        act_blk = api.HybridCache.bytes_of("ACT", cfg)
+        cap_n = math.ceil(caps.act_host / tpn)
+        ag_bytes = (tpn - 1) * cap_n * act_blk
+        ar_bytes = 2 * (2.0 * (tpn - 1) / tpn) * B * d * 4
+        tp_info = {"size": tpn, "mode": "nccl" if args.tp > 1 else "emulated",
+                   "rank_h2d_gb_per_step": h2d_step / 1e9,
+                   "allgather_bytes_per_layer": ag_bytes, "allreduce_bytes_per_layer": ar_bytes}
+        if args.tp_emulate > 1:
+            busbw = 650e9  # assumed NCCL bus bandwidth on NVLink 5 (900 GB/s/direction nominal)
+            t_ag, t_ar = L * ag_bytes / busbw, L * ar_bytes / busbw
+            t_proj = max(ms_per_step / 1e3, t_ag) + t_ar
+            tp_info.update({"note": "ONE rank of the N-way head-sharded group timed on one GPU: its weight / KV / "
+                                    "ACT shards streamed, its heads computed, collectives skipped; NVLink time "
+                                    "modelled at an assumed 650 GB/s NCCL bus bandwidth (gather overlapped on its "
+                                    "own stream, all-reduces serial)",
+                            "rank_step_ms_measured": ms_per_step, "nvlink_allgather_ms_per_step": t_ag * 1e3,
+                            "nvlink_allreduce_ms_per_step": t_ar * 1e3, "projected_step_ms": t_proj * 1e3,
+                            "projected_tokens_per_s": B / t_proj})
     res = None
     if rank == 0:
         cpu = None
@@ -691,7 +750,15 @@ def our_arm(args, cfg, world, rank, local, dist):
             "planner": planner,
             "prefill": prefill,
             "generation_e2e_projected": gen,
+            "tensor_parallel": tp_info,
         }
+        if tp is not None:
+            res["scaling"] = "strong"
+            res["config"]["parallelism"] = f"head-sharded tensor parallel x{tpn}" + (
+                " (EMULATED: one rank on one GPU, collectives skipped)" if args.tp_emulate > 1 else " (NCCL)")
+            res["config"]["global_batch"] = B
+            if args.tp_emulate > 1:
+                res["metric"] = METRIC + " [tp-emulate: single-rank timing, NOT a whole-job measurement]"
         res.update(extra)
     eng.close()
     if rank == 0:

@@ -152,6 +152,8 @@ int hc_tp_create_nccl(const uint8_t* id_compute128, const uint8_t* id_copy128, i
 /* In-process group (N engines, one host thread each; tests on one GPU). */
 int hc_tp_create_local_group(int size, void** group);
 int hc_tp_local_member(void* group, int rank, void** tp); /* owned by the group */
+/* Timing stand-in for one rank of a size-N group on one GPU (collectives skipped). */
+int hc_tp_create_emulated(int rank, int size, void** tp);
 int hc_tp_destroy(void* handle, int is_group);
 
 int hc_engine_create(const hc_model_config* cfg, uint64_t seed, int max_seq, int rescale,

@@ -76,6 +76,7 @@ SIGNATURES = {
     "hc_tp_create_nccl": (i, [C.c_char_p, C.c_char_p, i, i, i, vpp]),
     "hc_tp_create_local_group": (i, [i, vpp]),
     "hc_tp_local_member": (i, [vp, i, vpp]),
+    "hc_tp_create_emulated": (i, [i, i, vpp]),
     "hc_tp_destroy": (i, [vp, i]),
     "hc_engine_create_from_f64_opt": (i, [cfgp, i, dp, dp, C.POINTER(dp), C.POINTER(dp), dp, optp, vpp]),
     "hc_engine_destroy": (i, [vp]),

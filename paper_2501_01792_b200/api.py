@@ -457,6 +457,15 @@ class TensorParallel:
         return cls(h, rank=rank, size=size)
 
     @classmethod
+    def emulated(cls, rank: int, size: int) -> "TensorParallel":
+        """Timing stand-in for one rank of a size-N group on one GPU: the rank's
+        shard shapes, streams and bytes, collectives skipped (outputs are NOT
+        meaningful)."""
+        h = C.c_void_p()
+        check(lib().hc_tp_create_emulated(rank, size, C.byref(h)))
+        return cls(h, rank=rank, size=size)
+
+    @classmethod
     def local_group(cls, size: int) -> List["TensorParallel"]:
         """size ranks in this process (drive each rank's engine from its own thread)."""
         g = C.c_void_p()
@@ -471,7 +480,10 @@ class TensorParallel:
 
     def __del__(self):
         if getattr(self, "_h", None) and (self._is_group or self._owner is None):
-            lib().hc_tp_destroy(self._h, int(self._is_group))
+            try:
+                lib().hc_tp_destroy(self._h, int(self._is_group))
+            except TypeError:  # interpreter shutdown: module globals already cleared
+                pass
             self._h = None
 
 

@@ -388,6 +388,12 @@ int hc_tp_local_member(void* group, int rank, void** tp) {
         *tp = local_group_member(static_cast<LocalGroupHolder*>(group)->g, rank);
     });
 }
+int hc_tp_create_emulated(int rank, int size, void** tp) {
+    return hc_guard([&] {
+        if (!tp) throw InputError("null argument");
+        *tp = make_emulated_group(rank, size).release();
+    });
+}
 int hc_tp_destroy(void* h, int is_group) {
     return hc_guard([&] {
         if (is_group)

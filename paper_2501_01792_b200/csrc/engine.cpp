@@ -118,7 +118,7 @@ struct Engine::Impl {
     // prefill scratch
     bf16 *px[2] = {nullptr, nullptr}, *pqkv = nullptr, *patt = nullptr, *pproj = nullptr, *ph = nullptr;
     size_t prefill_rows = 0, prefill_chunk_rows = 0;
-    cudaEvent_t loaded[2]{}, consumed[2]{}, stored[2]{}, ev0{}, ev1{};
+    cudaEvent_t loaded[2]{}, consumed[2]{}, stored[2]{}, h2d_act[2]{}, gathered[2]{}, ev0{}, ev1{};
     bool pools_filled = false;
     bf16* tr_kv = nullptr;  // [max_batch * max_blocks] KV blocks for token-recompute prefixes
     void ensure_tr() {
@@ -414,10 +414,13 @@ void Engine::init(const ModelConfig& c, int w_max_seq, const uint16_t* emb, cons
     HC_CUDA(cudaStreamCreateWithFlags(&s_compute_, cudaStreamNonBlocking));
     HC_CUDA(cudaStreamCreateWithFlags(&s_copy_, cudaStreamNonBlocking));
     HC_CUDA(cudaStreamCreateWithFlags(&s_store_, cudaStreamNonBlocking));
+    HC_CUDA(cudaStreamCreateWithFlags(&s_gather_, cudaStreamNonBlocking));
     for (int i = 0; i < 2; ++i) {
         HC_CUDA(cudaEventCreateWithFlags(&m.loaded[i], cudaEventDisableTiming));
         HC_CUDA(cudaEventCreateWithFlags(&m.consumed[i], cudaEventDisableTiming));
         HC_CUDA(cudaEventCreateWithFlags(&m.stored[i], cudaEventDisableTiming));
+        HC_CUDA(cudaEventCreateWithFlags(&m.h2d_act[i], cudaEventDisableTiming));
+        HC_CUDA(cudaEventCreateWithFlags(&m.gathered[i], cudaEventDisableTiming));
     }
     HC_CUDA(cudaEventCreate(&m.ev0));
     HC_CUDA(cudaEventCreate(&m.ev1));
@@ -595,6 +598,8 @@ Engine::~Engine() {
         cudaEventDestroy(m.loaded[i]);
         cudaEventDestroy(m.consumed[i]);
         cudaEventDestroy(m.stored[i]);
+        cudaEventDestroy(m.h2d_act[i]);
+        cudaEventDestroy(m.gathered[i]);
     }
     cudaEventDestroy(m.ev0);
     cudaEventDestroy(m.ev1);
@@ -602,6 +607,7 @@ Engine::~Engine() {
     cudaStreamDestroy(s_compute_);
     cudaStreamDestroy(s_copy_);
     cudaStreamDestroy(s_store_);
+    cudaStreamDestroy(s_gather_);
 }
 
 // Causal forward of T rows (one sequence) through layers [l0, l1); the input
@@ -1079,9 +1085,17 @@ void Engine::decode_step(const std::vector<std::string>& ids, const int* tokens,
                                         cudaMemcpyHostToDevice, s_copy_));
                 st.h2d_bytes += bytes;
             }
-            // every rank streamed its 1/tpn of the ACT blocks; NVLink all-gather
-            // completes the staging (the recompute needs all of X for its heads)
-            if (gather_act) m.tp->copy_channel()->all_gather(own, m.act_stage[slot], m.act_cap_n * m.actb, s_copy_);
+            // every rank streamed its 1/tpn of the ACT blocks; an NVLink all-gather
+            // on the gather stream completes the staging (the recompute needs all
+            // of X for its heads) while the copy stream moves on to the KV blocks
+            // and the next layer
+            if (gather_act) {
+                HC_CUDA(cudaEventRecord(m.h2d_act[slot], s_copy_));
+                HC_CUDA(cudaStreamWaitEvent(s_gather_, m.h2d_act[slot]));
+                m.tp->copy_channel()->all_gather(own, m.act_stage[slot], m.act_cap_n * m.actb, s_gather_);
+                HC_CUDA(cudaEventRecord(m.gathered[slot], s_gather_));
+                HC_CUDA(cudaStreamWaitEvent(s_compute_, m.gathered[slot]));
+            }
             for (const Run& r : kv_runs) {
                 const size_t bytes = static_cast<size_t>(r.count) * m.kvb * 2;
                 HC_CUDA(cudaMemcpyAsync(m.kv_stage[slot] + static_cast<size_t>(r.start) * m.kvb,
@@ -1389,7 +1403,8 @@ double Engine::time_load_bytes(size_t bytes, int reps) {
 }
 
 double Engine::time_load_kv(int n_tokens, int reps) {
-    return time_load_bytes(static_cast<size_t>(n_tokens) * 2 * cfg_.hidden_dim * 2, reps);
+    // this rank's bytes of n KV tokens (all heads, or its 1/tpn under tensor parallelism)
+    return time_load_bytes(static_cast<size_t>(n_tokens) * 2 * impl_->dg * 2, reps);
 }
 
 }  // namespace hc

@@ -156,7 +156,7 @@ private:
     EngineOptions opt_;
     std::unique_ptr<HybridCache> cache_;
     std::unique_ptr<BlockAssigner> assigner_;
-    cudaStream_t s_compute_ = nullptr, s_copy_ = nullptr, s_store_ = nullptr;
+    cudaStream_t s_compute_ = nullptr, s_copy_ = nullptr, s_store_ = nullptr, s_gather_ = nullptr;
     StepStats stats_{};
     bool profile_ = false;
     bool capture_inputs_ = false;

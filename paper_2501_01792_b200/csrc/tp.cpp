@@ -124,6 +124,27 @@ std::unique_ptr<TpGroup> make_nccl_group(const uint8_t idc[128], const uint8_t i
     return std::make_unique<NcclGroup>(idc, idk, rank, size);
 }
 
+// ------------------------------------------------------------- Emulated ---
+namespace {
+class EmulatedRank final : public TpGroup {
+public:
+    EmulatedRank(int rank, int size) : rank_(rank), size_(size) {}
+    int rank() const override { return rank_; }
+    int size() const override { return size_; }
+    void all_reduce_sum(float*, size_t, cudaStream_t) override {}
+    void all_gather(const bf16*, bf16*, size_t, cudaStream_t) override {}
+    TpGroup* copy_channel() override { return this; }
+
+private:
+    int rank_, size_;
+};
+}  // namespace
+
+std::unique_ptr<TpGroup> make_emulated_group(int rank, int size) {
+    if (size < 1 || rank < 0 || rank >= size) throw InputError("tensor parallel: bad rank / size");
+    return std::make_unique<EmulatedRank>(rank, size);
+}
+
 // ----------------------------------------------------------- LocalGroup ---
 // Host-thread rendezvous: every collective is (post pointers, barrier, each
 // rank pulls what it needs with peer copies into its own memory, barrier).

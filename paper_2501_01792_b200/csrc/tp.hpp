@@ -47,6 +47,12 @@ void nccl_unique_id(uint8_t out[128]);
 std::unique_ptr<TpGroup> make_nccl_group(const uint8_t id_compute[128], const uint8_t id_copy[128], int rank, int size,
                                          int device);
 
+// Timing stand-in for ONE rank of an N-rank group on a single GPU: every
+// shard shape, stream and byte count of rank `rank`, collectives skipped
+// (outputs are not meaningful). bench.py --tp-emulate uses it to time a
+// rank's step where only one GPU is available; NVLink time is modelled.
+std::unique_ptr<TpGroup> make_emulated_group(int rank, int size);
+
 // LocalGroup: make_local_group(N) returns the shared state; member(r) the rank-r
 // handle (owned by the group).
 class LocalGroupState;

@@ -4,6 +4,8 @@ import os
 import re
 import subprocess
 
+import pytest
+
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 HEADER = os.path.join(ROOT, "include", "hybridcache.h")
 
@@ -41,3 +43,17 @@ def test_no_gpu_compute_fails_loudly():
         pytest.skip("GPU present")
     with pytest.raises(HcError):
         kernels.gemm_bf16(np.zeros((128, 64), np.uint16), np.zeros((64, 64), np.uint16))
+
+
+def test_tensor_parallel_handles_cpu():
+    """Host side of the head-sharded variant: NCCL ids (two channels, 256 B,
+    distinct per call) and in-process / emulated group handles, no GPU needed."""
+    from paper_2501_01792_b200 import api
+    a, b = api.TensorParallel.nccl_unique_ids(), api.TensorParallel.nccl_unique_ids()
+    assert len(a) == 256 and a != b and a[:128] != a[128:]
+    g = api.TensorParallel.local_group(3)
+    assert [m.rank for m in g] == [0, 1, 2] and all(m.size == 3 for m in g)
+    e = api.TensorParallel.emulated(2, 8)
+    assert (e.rank, e.size) == (2, 8)
+    with pytest.raises(api.InputError):
+        api.TensorParallel.emulated(8, 8)

@@ -99,5 +99,5 @@ def test_config4_strong_split_covers_global_batch():
         assert sum(sizes) == 128 and max(sizes) - min(sizes) <= 1
     sys.argv = ["bench.py"]
     b = bench.parse()
-    assert b.model == "opt-30b" and b.scaling == "weak" and abs(b.ratio - 1 / 3) < 1e-12
+    assert b.model == "opt-30b" and b.scaling == "weak" and b.ratio == -1.0  # planner-chosen by default
     assert bench.per_rank_batch(b, 8, 7) == 128
