@@ -218,7 +218,11 @@ void run_gemm(const GemmCall& c, cudaStream_t st) {
     // 99.7 % tensor-pipe activity but, under the 1 kW cap, its extra DRAM
     // traffic at K = 7168 costs clock (1.17 vs 1.36 GHz in situ), so it only
     // wins for K <= 4096 (OPT-6.7B recompute: +10 % in situ).
-    if (pair_ok && p.splits == 1 && !c.bn && p.num_m_tiles >= 8 && c.K <= 4096 && cc.epi != gemm::kSplitF32) {
+    static const int pair_max_k = [] {
+        const char* e = std::getenv("HC_GEMM_PAIR_MAX_K");  // tuning knob
+        return e ? std::atoi(e) : 4096;
+    }();
+    if (pair_ok && p.splits == 1 && !c.bn && p.num_m_tiles >= 8 && c.K <= pair_max_k && cc.epi != gemm::kSplitF32) {
         p.num_n_tiles = (c.N + gemm::Cfg2::BN - 1) / gemm::Cfg2::BN;
         p.group_m = c.group_m > 0 ? std::max(1, c.group_m / 2) : 8;
         if (const char* g = std::getenv("HC_GEMM_GROUP_M")) p.group_m = std::max(1, std::atoi(g) / 2);

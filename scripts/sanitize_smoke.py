@@ -1,7 +1,8 @@
 """Small run of every kernel of the path for compute-sanitizer
-(memcheck / racecheck / synccheck): engine prefill + decode in hybrid mode
-with host pools and streamed weights, token-recompute mode, split-K and
-split-attention paths.
+(memcheck / racecheck / synccheck / initcheck): engine prefill + decode in
+hybrid mode with host pools and streamed weights, token-recompute mode,
+split-K and split-attention paths, the chunked prefill pipeline, OPT layers
+and the head-sharded tensor-parallel group.
 
     compute-sanitizer --tool memcheck python scripts/sanitize_smoke.py
 """
@@ -37,6 +38,32 @@ def main():
     refs = np.array([[0, 1, 2, 3], [4, 5, 6, 7]], np.int32)
     kernels.decode_attention(q, pool, pool, refs, np.array([4, 3], np.int32), np.array([60, 40], np.int32), 2,
                              True, 2)
+    # session-2 paths: chunked offloaded prefill (store stream), OPT layers
+    # (LayerNorm, bias / residual epilogues), head-sharded TP over the
+    # in-process group (all-gather + fp32 all-reduce), flash prefill attention
+    ocfg = api.ModelConfig(num_layers=2, hidden_dim=256, num_heads=4, ffn_dim=512, vocab_size=512)
+    e2 = api.Engine(ocfg, seed=5, max_seq=64, max_batch=2, weights_on_device=False, arch="opt",
+                    caps=api.PoolCaps(kv_host=8, act_host=8, act_gpu=1), allocation=api.HostAllocation(1, 1),
+                    max_prefill_tokens=24)
+    e2.prefill(["a", "b"], prompts)
+    e2.decode_step(["a", "b"], [3, 4], want_logits=True)
+    e2.close()
+    import threading
+    group = api.TensorParallel.local_group(2)
+    engs = [api.Engine(ocfg, seed=5, max_seq=64, max_batch=2, weights_on_device=bool(r), arch="opt", tp=group[r],
+                       caps=api.PoolCaps(kv_host=8, act_host=8, act_gpu=1), allocation=api.HostAllocation(1, 1))
+            for r in range(2)]
+
+    def run(e):
+        e.prefill(["a", "b"], prompts)
+        e.decode_step(["a", "b"], [3, 4])
+    ts = [threading.Thread(target=run, args=(e,)) for e in engs]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    for e in engs:
+        e.close()
     print("sanitize smoke ok")
 
 
