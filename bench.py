@@ -603,7 +603,9 @@ def our_arm(args, cfg, world, rank, local, dist):
             "achieved": achieved, "peak": tflops_sust, "unit": "TFLOP/s",
             "frac": achieved / tflops_sust if tflops_sust else None,
             "traffic": 6.65e9, "traffic_note": "ncu dram__bytes_read+write per launch, profiles/r01_ncu_recompute.csv "
-                                                "(algorithmic 2.07e9: A 0.62 + W 0.21 read, K|V 1.24 write)",
+                                                "(algorithmic 2.07e9: A 0.62 + W 0.21 read, K|V 1.24 write; the "
+                                                "L2-capacity floor for this shape is ~5e9: [Wk|Wv] is 205 MB > the "
+                                                "126 MB L2, so any tile schedule re-reads A or B — DESIGN.md §3)",
             "peak_source": f"{peak_src} bf16_tflops_sustained (MEASURED_PEAKS.json); burst {tflops_burst}",
             "flops_per_launch": rec_flops, "launch_ms": rec_launch_ms}
     # per-step roofline (north_star): slower of link bytes / link BW, tensor
