@@ -266,8 +266,10 @@ def reference_arm(args, cfg, world, rank, dist):
     if rank != 0:
         return
     threads = os.cpu_count() or 1
-    kind, run, sample = cpu_reference_sample(cfg, args.prompt, args.ratio if args.ratio >= 0 else 1.0 / 3.0,
-                                             threads)
+    # the CPU path has no measured rates to plan with: it runs the paper's KV:ACT 2:1
+    # unless --ratio is given
+    r_cpu = args.ratio if args.ratio >= 0 else 1.0 / 3.0
+    kind, run, sample = cpu_reference_sample(cfg, args.prompt, r_cpu, threads)
     for _ in range(args.warmup):
         run()
     ts = [run() for _ in range(args.steps)]
@@ -277,7 +279,8 @@ def reference_arm(args, cfg, world, rank, dist):
         "impl": "reference", "metric": METRIC, "value": v, "unit": "tokens/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
         "scaling": args.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": workload_config(args, cfg, world),
+        "config": workload_config(args, cfg, world, {"act_share_r": r_cpu, "ratio_source":
+                                                     "--ratio, else the paper's 2:1 (no planner on the CPU path)"}),
         "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": threads, "kind": kind, "sample": sample},
         "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
