@@ -799,7 +799,7 @@ def resident_variants(local, cfg, B, P, arch, steps=2, warmup=1, reserve=6e9):
     import torch
     from paper_2501_01792_b200 import api
     L, tpb = cfg.num_layers, cfg.tokens_per_block
-    total = steps + warmup + 2
+    total = steps + warmup + 3
     nb = math.ceil((P + total) / tpb)
     N = B * nb
     kv_all = api.HybridCache.bytes_of("KV", cfg) * L
@@ -810,7 +810,7 @@ def resident_variants(local, cfg, B, P, arch, steps=2, warmup=1, reserve=6e9):
     free = torch.cuda.mem_get_info(local)[0] - reserve
     # x ACT blocks + (N - x) KV blocks (+ x recompute slots) <= free
     x_fit = max(0, math.ceil((N * kv_all - free) / (kv_all - act_all - kv_one)))
-    r_fit = min(1.0, (x_fit + B) / N)
+    r_fit = 0.0 if x_fit == 0 else min(1.0, (x_fit + B) / N)  # all-KV fits: nothing to recompute
     ids = [f"h{i}" for i in range(B)]
     tokens = np.random.default_rng(9).integers(0, cfg.vocab_size, (total, B)).astype(np.int32)
     out = {"workload": f"{cfg.name}-shape, batch {B}, prompt {P}: weights + cache in HBM (KV and ACT placed on "
@@ -831,8 +831,15 @@ def resident_variants(local, cfg, B, P, arch, steps=2, warmup=1, reserve=6e9):
             eng.admit_synthetic(ids, [P] * B, seed=11)
             run_steps(eng, ids, tokens, 0, warmup)
             acc = run_steps(eng, ids, tokens, warmup, steps)
+            prof = run_steps(eng, ids, tokens, warmup + steps, 1, prof=True)["last"]
             ms = acc["dev_ms"] / steps
             out["per_ratio"].append({"act_share_r": round(r, 4), "mode": mode, "tokens_per_s": B * 1e3 / ms,
+                                     "profile_split_ms": {"recompute": prof["recompute_ms"],
+                                                          "attention": prof["attn_ms"],
+                                                          "qkv_proj_ffn": prof["gemm_ms"],
+                                                          "copy_stream": prof["copy_ms"],
+                                                          "step_profiled": prof["step_ms"]},
+                                     "recompute_rows": prof["recompute_rows"],
                                      "ms_per_step": ms, "kv_gpu_blocks": kv_gpu, "kv_host_blocks": caps.kv_host,
                                      "act_gpu_blocks": act_cap, "h2d_gb_per_step": acc["h2d"] / steps / 1e9,
                                      "planned": abs(r - r_fit) < 1e-9})

@@ -543,6 +543,13 @@ void Engine::configure_cache(const PoolCaps& caps, bool kv_on_gpu, CacheMode mod
         m.act_stage[s] = dalloc<bf16>(static_cast<size_t>(m.tpn) * m.act_cap_n * m.actb);
     }
     m.kvr = dalloc<bf16>(static_cast<size_t>(m.act_gpu_cap + m.tpn * m.act_cap_n) * m.kvb);
+    // staging slots start zeroed: whole-chunk copies (D2H runs, TP all-gathers)
+    // never move uninitialised bytes, even for slots no block occupies yet
+    for (int s = 0; s < 2; ++s) {
+        if (m.kv_stage[s]) HC_CUDA(cudaMemset(m.kv_stage[s], 0, static_cast<size_t>(m.kv_host_cap) * m.kvb * 2));
+        if (m.act_stage[s])
+            HC_CUDA(cudaMemset(m.act_stage[s], 0, static_cast<size_t>(m.tpn) * m.act_cap_n * m.actb * 2));
+    }
     m.pools_filled = false;
     HC_CUDA(cudaDeviceSynchronize());
 }

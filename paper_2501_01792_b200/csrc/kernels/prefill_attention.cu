@@ -13,6 +13,8 @@
 // tile j is multiplied. Causality skips every key tile right of the
 // diagonal; heavier (later) query tiles launch first.
 //
+// Q shares buffer 1's K slot (64 KB of smem per CTA at HD 128) and registers
+// are capped for 3 resident CTAs per SM.
 // Prefill is <2% of an offloaded decode run, so this kernel
 // uses the warp-level MMA path rather than a TMEM-resident tcgen05 pipeline.
 #include <cfloat>
@@ -27,6 +29,7 @@ namespace {
 
 constexpr int kQT = 64;   // query rows per CTA
 constexpr int kKT = 64;   // keys per tile
+static_assert(kQT == kKT, "Q is staged in a K tile slot");
 constexpr float kLog2e = 1.4426950408889634f;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -91,7 +94,7 @@ __device__ __forceinline__ void load_tile(uint32_t sbase, const bf16* g, long lo
 }
 
 template <int HD>
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(128, 3)
     prefill_flash_kernel(const bf16* __restrict__ qkv, bf16* __restrict__ out, const int* __restrict__ cu, int H,
                          float scale) {
     constexpr int NK = HD / 16;  // k16 steps over the head dim
@@ -108,10 +111,13 @@ __global__ void __launch_bounds__(128)
     const bf16* base = qkv + static_cast<long long>(row0) * ld + h * HD;
 
     extern __shared__ __align__(128) unsigned char smem[];
-    const uint32_t sQ = smem_u32(smem);
-    // buffer c: K at sQ + (kQT + 2 kKT c) HD 2 bytes, V right after it
-    auto sK = [&](int c) { return sQ + static_cast<uint32_t>((kQT + 2 * kKT * c) * HD * 2); };
+    const uint32_t s0 = smem_u32(smem);
+    // buffer c: K at s0 + 2 kKT HD 2 c bytes, V right after it. Q is staged in
+    // buffer 1's K slot: it moves to registers before tile 1 is prefetched, so
+    // the CTA needs 4 tiles of smem (64 KB at HD 128) and 3 CTAs fit an SM
+    auto sK = [&](int c) { return s0 + static_cast<uint32_t>(2 * kKT * c * HD * 2); };
     auto sV = [&](int c) { return sK(c) + static_cast<uint32_t>(kKT * HD * 2); };
+    const uint32_t sQ = sK(1);
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const int kend = min(P, q0 + kQT);           // keys this tile needs (causal)
@@ -129,6 +135,14 @@ __global__ void __launch_bounds__(128)
     uint32_t qa[NK][4];
     const float sl = scale * kLog2e;
     const int qrow = q0 + warp * 16 + lane / 4;  // rows qrow and qrow + 8
+    cp_async_wait<0>();
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < NK; ++kk) {
+        const int r = warp * 16 + (lane % 16), ch = kk * 2 + lane / 16;
+        ldsm_x4(sQ + swz<HD>(r, ch), qa[kk][0], qa[kk][1], qa[kk][2], qa[kk][3]);
+    }
+    __syncthreads();  // the Q slot is buffer 1's K: free it before the first prefetch
 
     for (int kt = 0; kt < n_kt; ++kt) {
         const int cur = kt & 1;
@@ -140,13 +154,6 @@ __global__ void __launch_bounds__(128)
         cp_async_commit();
         cp_async_wait<1>();
         __syncthreads();
-        if (kt == 0) {
-#pragma unroll
-            for (int kk = 0; kk < NK; ++kk) {
-                const int r = warp * 16 + (lane % 16), ch = kk * 2 + lane / 16;
-                ldsm_x4(sQ + swz<HD>(r, ch), qa[kk][0], qa[kk][1], qa[kk][2], qa[kk][3]);
-            }
-        }
         // S = Q.K^T : 16 x 64 per warp
         float s[8][4];
 #pragma unroll
@@ -249,7 +256,7 @@ __global__ void __launch_bounds__(128)
 template <int HD>
 void launch_prefill(const bf16* qkv, bf16* out, const int* cu, int n_req, int max_len, int H, float scale,
                     cudaStream_t st) {
-    constexpr size_t smem = static_cast<size_t>(kQT + 4 * kKT) * HD * 2;
+    constexpr size_t smem = static_cast<size_t>(4 * kKT) * HD * 2;
     static bool configured = false;
     if (!configured) {
         cudaFuncSetAttribute(prefill_flash_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
