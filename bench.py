@@ -786,7 +786,7 @@ def our_arm(args, cfg, world, rank, local, dist):
     return res
 
 
-def resident_variants(local, cfg, B, P, arch, steps=2, warmup=1, reserve=6e9):
+def resident_variants(local, cfg, B, P, arch, steps=2, warmup=1, reserve=6e9, only_planned=False):
     """The same workload with the weights AND the cache in HBM (B200 has 180 GB):
     KV and ACT blocks both placed on the GPU first (kv_on_gpu / ACT-first,
     cache.cpp:64-91). Pure KV does not fit, so its overflow blocks stream from
@@ -816,7 +816,7 @@ def resident_variants(local, cfg, B, P, arch, steps=2, warmup=1, reserve=6e9):
     out = {"workload": f"{cfg.name}-shape, batch {B}, prompt {P}: weights + cache in HBM (KV and ACT placed on "
                        "the GPU first); overflow blocks in pinned host memory",
            "free_hbm_gb": free / 1e9, "blocks": N, "r_fit": r_fit, "per_ratio": []}
-    for r in sorted({0.0, r_fit, (1.0 + r_fit) / 2, 1.0}):
+    for r in ([r_fit] if only_planned else sorted({0.0, r_fit, (1.0 + r_fit) / 2, 1.0})):
         a = int(round(r * 1000))
         act_cap = 0 if r <= 0 else (N if r >= 1 else B * (math.ceil(r * nb) + 1))
         kv_need = 0 if r >= 1 else (N if r <= 0 else B * (math.ceil((1 - r) * nb) + 1))

@@ -442,9 +442,21 @@ class TensorParallel:
         self.rank, self.size = rank, size
 
     @staticmethod
+    def _nccl_provider() -> None:
+        """libhybridcache dlopens "libnccl.so.2" and reuses a copy already in
+        the process. torch links its own (newer) NCCL under the same soname,
+        so load torch first: if the system NCCL were loaded first, a later
+        `import torch` would bind to it and fail (missing symbols)."""
+        try:
+            import torch  # noqa: F401
+        except ImportError:
+            pass
+
+    @staticmethod
     def nccl_unique_ids() -> bytes:
         """Two ncclUniqueIds (compute channel | copy channel), 256 bytes; made on
         rank 0 and broadcast to the others by the caller."""
+        TensorParallel._nccl_provider()
         a, b = C.create_string_buffer(128), C.create_string_buffer(128)
         check(lib().hc_tp_nccl_unique_id(a))
         check(lib().hc_tp_nccl_unique_id(b))
@@ -452,6 +464,7 @@ class TensorParallel:
 
     @classmethod
     def nccl(cls, ids: bytes, rank: int, size: int, device: int = 0) -> "TensorParallel":
+        TensorParallel._nccl_provider()
         h = C.c_void_p()
         check(lib().hc_tp_create_nccl(ids[:128], ids[128:256], rank, size, device, C.byref(h)))
         return cls(h, rank=rank, size=size)

@@ -3,6 +3,7 @@
 #include <dlfcn.h>
 
 #include <condition_variable>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -36,8 +37,13 @@ const NcclApi& nccl() {
     static std::once_flag once;
     static std::string err;
     std::call_once(once, [] {
-        // RTLD_NOLOAD first: reuse the libnccl a host framework (torch) already loaded
-        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
+        // HC_NCCL_LIB names a specific libnccl; otherwise reuse the copy a host
+        // framework (torch) already loaded (RTLD_NOLOAD), else the system one.
+        // Loading ours first would shadow torch's same-soname NCCL for a later
+        // `import torch` — the Python API therefore imports torch first.
+        void* h = nullptr;
+        if (const char* p = std::getenv("HC_NCCL_LIB")) h = dlopen(p, RTLD_NOW | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
         if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
         if (!h) {
             err = std::string("libnccl.so.2 not loadable: ") + dlerror();

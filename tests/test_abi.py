@@ -57,3 +57,16 @@ def test_tensor_parallel_handles_cpu():
     assert (e.rank, e.size) == (2, 8)
     with pytest.raises(api.InputError):
         api.TensorParallel.emulated(8, 8)
+
+
+def test_cpp_caller_fails_loudly_without_gpu():
+    """examples/decode_demo (C++ caller of the C ABI only, built by build())
+    exits with the 'no CUDA device' code here — no CPU fallback."""
+    exe = os.path.join(ROOT, "examples", "decode_demo")
+    if not os.path.exists(exe):
+        pytest.skip("examples/decode_demo not built (run __graft_entry__.build())")
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present: covered by test_engine_gpu.py::test_cpp_caller_decodes")
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+    assert out.returncode == 3, out.stderr

@@ -527,3 +527,17 @@ def test_engine_tensor_parallel_seeded_shards(native):
             assert np.array_equal(got, want), (r, l)
             o += 1
         eng.close()
+
+
+def test_cpp_caller_decodes(native):
+    """examples/decode_demo: a reference-style C++ program linking only the C
+    ABI runs prefill + 4 greedy batched decode steps, dumps the block table
+    and sees the reference's InputError for an unknown request."""
+    import os
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = os.path.join(root, "examples", "decode_demo")
+    assert os.path.exists(exe), "examples/decode_demo not built"
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "decode_demo ok" in out.stdout and '"requests"' in out.stdout
