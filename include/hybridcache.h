@@ -205,6 +205,9 @@ int hc_engine_captured_inputs(void* engine, uint16_t* out, long count);
 int hc_engine_last_stats(void* engine, double* out11);
 /* Per-kernel CUDA-event timing of the next steps (small overhead). */
 int hc_engine_set_profile(void* engine, int on);
+/* Replay decode steps as CUDA graphs keyed by their launch structure (default on,
+ * HC_DECODE_GRAPHS=0 disables; profiled steps and TP engines run eagerly). */
+int hc_engine_set_graphs(void* engine, int on);
 /* Events of the last profiled step in the reference's trace.json schema
  * {"events":[{name, track, start_us, end_us, iteration, layer, minibatch}]}
  * (SimEvent, sim.hpp:50-58; main.cpp:263-275). */

@@ -94,6 +94,7 @@ SIGNATURES = {
     "hc_engine_captured_inputs": (i, [vp, u16p, l]),
     "hc_engine_last_stats": (i, [vp, dp]),
     "hc_engine_set_profile": (i, [vp, i]),
+    "hc_engine_set_graphs": (i, [vp, i]),
     "hc_engine_trace_json": (i, [vp, cp, l, lp]),
     "hc_engine_time_kv_gen": (i, [vp, i, i, dp]),
     "hc_engine_time_load_kv": (i, [vp, i, i, dp]),

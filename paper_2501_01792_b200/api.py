@@ -696,6 +696,10 @@ class Engine:
     def set_profile(self, on: bool = True) -> None:
         check(lib().hc_engine_set_profile(self._h, int(on)))
 
+    def set_graphs(self, on: bool = True) -> None:
+        """CUDA-graph replay of decode steps (default on)."""
+        check(lib().hc_engine_set_graphs(self._h, int(on)))
+
     def trace(self) -> dict:
         """Events of the last profiled step (reference trace.json schema)."""
         need = C.c_long()

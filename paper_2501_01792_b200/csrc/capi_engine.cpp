@@ -472,6 +472,9 @@ int hc_engine_last_stats(void* e, double* o) {
         std::memcpy(o, v, sizeof v);
     });
 }
+int hc_engine_set_graphs(void* e, int on) {
+    return hc_guard([&] { eng(e)->set_graphs(on != 0); });
+}
 int hc_engine_trace_json(void* e, char* buf, long len, long* needed) {
     return hc_guard([&] {
         const std::string& s = eng(e)->last_trace();

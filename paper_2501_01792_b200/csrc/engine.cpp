@@ -3,6 +3,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <unordered_set>
@@ -118,11 +119,33 @@ struct Engine::Impl {
     // prefill scratch
     bf16 *px[2] = {nullptr, nullptr}, *pqkv = nullptr, *patt = nullptr, *pproj = nullptr, *ph = nullptr;
     size_t prefill_rows = 0, prefill_chunk_rows = 0;
-    cudaEvent_t loaded[2]{}, consumed[2]{}, stored[2]{}, h2d_act[2]{}, gathered[2]{}, ev0{}, ev1{};
+    cudaEvent_t loaded[2]{}, consumed[2]{}, stored[2]{}, h2d_act[2]{}, gathered[2]{}, ev0{}, ev1{}, tg0{}, tg1{};
     bool pools_filled = false;
     bf16* tr_kv = nullptr;  // [max_batch * max_blocks] KV blocks for token-recompute prefixes
     void ensure_tr() {
-        if (!tr_kv) tr_kv = dalloc<bf16>(static_cast<size_t>(B) * max_blocks * kvb);
+        if (!tr_kv) {
+            clear_graphs();
+            tr_kv = dalloc<bf16>(static_cast<size_t>(B) * max_blocks * kvb);
+        }
+    }
+    // CUDA graphs of the decode step, keyed by the step's launch structure
+    // (the per-step data travels in the pinned metadata block the graph's
+    // first node uploads, so a graph replays until blocks are appended)
+    struct StepGraph {
+        cudaGraphExec_t exec = nullptr;
+        StepStats stats{};
+        long last_use = 0;
+    };
+    std::unordered_map<std::string, StepGraph> graphs;
+    long graph_gen = 0;  // bumped when any buffer a graph references is reallocated
+    long graph_clock = 0;
+    uint16_t* h_x = nullptr;   // pinned outputs of graph-mode steps
+    float* h_logits = nullptr;
+    int* h_amax = nullptr;
+    void clear_graphs() {
+        for (auto& g : graphs) cudaGraphExecDestroy(g.second.exec);
+        graphs.clear();
+        ++graph_gen;
     }
     // profiling: timing events handed out per step
     std::vector<cudaEvent_t> pev;
@@ -255,6 +278,7 @@ struct Engine::Impl {
 
     void ensure_meta(size_t ints) {
         if (ints <= meta_cap) return;
+        clear_graphs();
         if (d_meta) cudaFree(d_meta);
         if (h_meta) cudaFreeHost(h_meta);
         meta_cap = ints + ints / 2 + 1024;
@@ -263,6 +287,7 @@ struct Engine::Impl {
     }
     void ensure_attn_work(size_t elems) {
         if (elems <= attn_work_elems) return;
+        clear_graphs();
         if (attn_work) cudaFree(attn_work);
         attn_work_elems = elems;
         attn_work = dalloc<float>(elems);
@@ -271,6 +296,7 @@ struct Engine::Impl {
     // pqkv/patt/pproj/ph: per-chunk scratch (chunk_rows <= rows)
     void ensure_prefill(size_t rows, size_t chunk_rows = 0) {
         if (!chunk_rows) chunk_rows = rows;
+        if (rows > prefill_rows || chunk_rows > prefill_chunk_rows) clear_graphs();
         if (rows > prefill_rows) {
             for (bf16* p : {px[0], px[1], pxn})
                 if (p) cudaFree(p);
@@ -377,6 +403,7 @@ void Engine::init(const ModelConfig& c, int w_max_seq, const uint16_t* emb, cons
     impl_ = std::make_unique<Impl>();
     Impl& m = *impl_;
     if (opt_.arch != kArchReference && opt_.arch != kArchOpt) throw InputError("Engine: unknown arch");
+    if (const char* e = std::getenv("HC_DECODE_GRAPHS")) graphs_ = e[0] != '0';
     m.arch = opt_.arch;
     if (cfg_.hidden_dim % 64) throw InputError("Engine: hidden_dim must be a multiple of 64");
     if (cfg_.head_dim() != 64 && cfg_.head_dim() != 128) throw InputError("Engine: head_dim must be 64 or 128");
@@ -424,6 +451,8 @@ void Engine::init(const ModelConfig& c, int w_max_seq, const uint16_t* emb, cons
     }
     HC_CUDA(cudaEventCreate(&m.ev0));
     HC_CUDA(cudaEventCreate(&m.ev1));
+    HC_CUDA(cudaEventCreate(&m.tg0));
+    HC_CUDA(cudaEventCreate(&m.tg1));
 
     // tables
     m.emb = dalloc<bf16>(static_cast<size_t>(m.V) * m.d);
@@ -501,6 +530,7 @@ void Engine::configure_cache(const PoolCaps& caps, bool kv_on_gpu, CacheMode mod
     if (mode == CacheMode::TokenRecompute && m.tpn > 1)
         throw ConfigError("Engine: the token-recompute baseline runs without tensor parallelism");
     HC_CUDA(cudaDeviceSynchronize());
+    m.clear_graphs();
     for (bf16** p : {&m.kv_gpu, &m.act_gpu, &m.kvr, &m.kv_stage[0], &m.kv_stage[1], &m.act_stage[0], &m.act_stage[1]}) {
         if (*p) cudaFree(*p);
         *p = nullptr;
@@ -599,7 +629,9 @@ Engine::~Engine() {
                     (void*)m.px[0], (void*)m.px[1], (void*)m.pqkv, (void*)m.patt, (void*)m.pproj, (void*)m.ph,
                     (void*)m.tr_kv, (void*)m.splitk_ws, (void*)m.lnf, (void*)m.xn, (void*)m.pxn, (void*)m.red})
         if (p) cudaFree(p);
-    for (void* p : {(void*)m.h_w, (void*)m.kv_host, (void*)m.act_host, (void*)m.h_meta})
+    for (auto& g : m.graphs) cudaGraphExecDestroy(g.second.exec);
+    for (void* p : {(void*)m.h_w, (void*)m.kv_host, (void*)m.act_host, (void*)m.h_meta, (void*)m.h_x,
+                    (void*)m.h_logits, (void*)m.h_amax})
         if (p) cudaFreeHost(p);
     for (int i = 0; i < 2; ++i) {
         cudaEventDestroy(m.loaded[i]);
@@ -610,6 +642,8 @@ Engine::~Engine() {
     }
     cudaEventDestroy(m.ev0);
     cudaEventDestroy(m.ev1);
+    cudaEventDestroy(m.tg0);
+    cudaEventDestroy(m.tg1);
     for (cudaEvent_t e : m.pev) cudaEventDestroy(e);
     cudaStreamDestroy(s_compute_);
     cudaStreamDestroy(s_copy_);
@@ -1059,6 +1093,8 @@ void Engine::decode_step(const std::vector<std::string>& ids, const int* tokens,
     m.pev_used = 0;
     m.spans.clear();
     const bool stream_any = !m.w_all || !kv_runs.empty() || !act_runs.empty() || gather_act;
+    // everything the step puts on the streams; outputs land in xo / lo / ao
+  auto enqueue = [&](StepStats& st, uint16_t* xo, float* lo, int* ao) {
     HC_CUDA(cudaEventRecord(m.ev0, s_compute_));
     HC_CUDA(cudaMemcpyAsync(m.d_meta, m.h_meta, meta.size() * 4, cudaMemcpyHostToDevice, s_compute_));
     embed(m.emb, m.pos, dm + o_tok, dm + o_pos, n, m.d, m.x[0], m.d, s_compute_);
@@ -1075,8 +1111,10 @@ void Engine::decode_step(const std::vector<std::string>& ids, const int* tokens,
         m.cur_layer = l;
         if (stream_any) {
             // copy stream: weights + this layer's host blocks into slot l%2,
-            // after compute released the slot (layer l-2)
-            HC_CUDA(cudaStreamWaitEvent(s_copy_, m.consumed[slot]));
+            // after compute released the slot (layer l-2; the previous step,
+            // fully synchronised, for the first two layers — so a captured
+            // graph only waits on events it records itself)
+            HC_CUDA(cudaStreamWaitEvent(s_copy_, l >= 2 ? m.consumed[slot] : m.ev0));
             m.span_begin(profile_, s_copy_, 3);
             if (!m.w_all) {
                 HC_CUDA(cudaMemcpyAsync(m.wbuf[slot], m.h_w + static_cast<size_t>(l % m.Lw) * m.LE, m.LE * 2,
@@ -1240,26 +1278,88 @@ void Engine::decode_step(const std::vector<std::string>& ids, const int* tokens,
     }
     const bf16* xf = m.final_norm(m.x[m.L & 1], n, m.xn, s_compute_);
     st.launches += m.opt();
-    if (logits_out || argmax_out) {
+    if (lo || ao) {
         gemm_rows(gemm::kF32, xf, n, m.d, m.emb, m.V, m.logits, m.V, s_compute_);
         st.launches += 1;
-        if (argmax_out) {
+        if (ao) {
             argmax_rows(m.logits, n, m.V, m.amax, s_compute_);
             st.launches += 1;
         }
     }
     HC_CUDA(cudaEventRecord(m.ev1, s_compute_));
     HC_CUDA(cudaGetLastError());
-    if (x_out)
-        HC_CUDA(cudaMemcpyAsync(x_out, xf, static_cast<size_t>(n) * m.d * 2, cudaMemcpyDeviceToHost, s_compute_));
-    if (logits_out)
-        HC_CUDA(cudaMemcpyAsync(logits_out, m.logits, static_cast<size_t>(n) * m.V * 4, cudaMemcpyDeviceToHost,
-                                s_compute_));
-    if (argmax_out)
-        HC_CUDA(cudaMemcpyAsync(argmax_out, m.amax, static_cast<size_t>(n) * 4, cudaMemcpyDeviceToHost, s_compute_));
+    if (xo) HC_CUDA(cudaMemcpyAsync(xo, xf, static_cast<size_t>(n) * m.d * 2, cudaMemcpyDeviceToHost, s_compute_));
+    if (lo)
+        HC_CUDA(cudaMemcpyAsync(lo, m.logits, static_cast<size_t>(n) * m.V * 4, cudaMemcpyDeviceToHost, s_compute_));
+    if (ao) HC_CUDA(cudaMemcpyAsync(ao, m.amax, static_cast<size_t>(n) * 4, cudaMemcpyDeviceToHost, s_compute_));
+  };
+
+    // CUDA graph of the step: its launch structure (sizes, copy runs, splits,
+    // outputs) is the key; the data rides in the metadata block
+    const bool use_graph = graphs_ && !profile_ && !capture_inputs_ && m.tpn == 1;
+    if (!use_graph) {
+        enqueue(st, x_out, logits_out, argmax_out);
+    } else {
+        if (!m.h_x) {
+            m.h_x = halloc<uint16_t>(static_cast<size_t>(m.B) * m.d, false);
+            m.h_logits = halloc<float>(static_cast<size_t>(m.B) * m.V, false);
+            m.h_amax = halloc<int>(m.B, false);
+        }
+        std::string key;
+        auto add = [&](long v) { key.append(reinterpret_cast<const char*>(&v), sizeof v); };
+        for (long v : {static_cast<long>(n), static_cast<long>(n_rc), static_cast<long>(rc_max),
+                       static_cast<long>(meta.size()), static_cast<long>(tiles_h.size()),
+                       static_cast<long>(tiles_g.size()), static_cast<long>(tr_src.size()), static_cast<long>(splits),
+                       static_cast<long>(any_act), static_cast<long>(any_kv), static_cast<long>(stream_any),
+                       static_cast<long>(x_out != nullptr), static_cast<long>(logits_out != nullptr),
+                       static_cast<long>(argmax_out != nullptr), m.graph_gen})
+            add(v);
+        for (const auto* runs : {&kv_runs, &act_runs}) {
+            add(static_cast<long>(runs->size()));
+            for (const Run& r : *runs) add((static_cast<long>(r.start) << 32) | r.count);
+        }
+        auto it = m.graphs.find(key);
+        if (it == m.graphs.end()) {
+            if (m.graphs.size() >= 8) {  // evict the least recently used
+                auto lru = m.graphs.begin();
+                for (auto g = m.graphs.begin(); g != m.graphs.end(); ++g)
+                    if (g->second.last_use < lru->second.last_use) lru = g;
+                cudaGraphExecDestroy(lru->second.exec);
+                m.graphs.erase(lru);
+            }
+            Impl::StepGraph sg;
+            cudaGraph_t g = nullptr;
+            HC_CUDA(cudaStreamBeginCapture(s_compute_, cudaStreamCaptureModeThreadLocal));
+            try {
+                enqueue(sg.stats, x_out ? m.h_x : nullptr, logits_out ? m.h_logits : nullptr,
+                        argmax_out ? m.h_amax : nullptr);
+            } catch (...) {
+                cudaStreamEndCapture(s_compute_, &g);
+                if (g) cudaGraphDestroy(g);
+                throw;
+            }
+            HC_CUDA(cudaStreamEndCapture(s_compute_, &g));
+            const cudaError_t e = cudaGraphInstantiate(&sg.exec, g, 0);
+            cudaGraphDestroy(g);
+            HC_CUDA(e);
+            it = m.graphs.emplace(key, sg).first;
+        }
+        it->second.last_use = ++m.graph_clock;
+        st = it->second.stats;
+        // timing events around the launch (events recorded inside a graph
+        // cannot be timed)
+        HC_CUDA(cudaEventRecord(m.tg0, s_compute_));
+        HC_CUDA(cudaGraphLaunch(it->second.exec, s_compute_));
+        HC_CUDA(cudaEventRecord(m.tg1, s_compute_));
+    }
     HC_CUDA(cudaStreamSynchronize(s_compute_));
+    if (use_graph) {
+        if (x_out) std::memcpy(x_out, m.h_x, static_cast<size_t>(n) * m.d * 2);
+        if (logits_out) std::memcpy(logits_out, m.h_logits, static_cast<size_t>(n) * m.V * 4);
+        if (argmax_out) std::memcpy(argmax_out, m.h_amax, static_cast<size_t>(n) * 4);
+    }
     float ms = 0;
-    HC_CUDA(cudaEventElapsedTime(&ms, m.ev0, m.ev1));
+    HC_CUDA(cudaEventElapsedTime(&ms, use_graph ? m.tg0 : m.ev0, use_graph ? m.tg1 : m.ev1));
     st.step_ms = ms;
     // trace of the profiled step: the reference's SimEvent schema
     // (sim.hpp:50-58; trace.json main.cpp:263-275) from CUDA events

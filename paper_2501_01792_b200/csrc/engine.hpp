@@ -140,6 +140,8 @@ public:
     const ModelConfig& config() const { return cfg_; }
     const StepStats& last_stats() const { return stats_; }
     void set_profile(bool on) { profile_ = on; }
+    // CUDA-graph replay of decode steps (default on; off with HC_DECODE_GRAPHS=0)
+    void set_graphs(bool on) { graphs_ = on; }
     // {"events":[{name, track, start_us, end_us, iteration, layer, minibatch}]}
     // of the last profiled decode step — the reference's trace.json schema.
     const std::string& last_trace() const { return last_trace_; }
@@ -159,6 +161,7 @@ private:
     cudaStream_t s_compute_ = nullptr, s_copy_ = nullptr, s_store_ = nullptr, s_gather_ = nullptr;
     StepStats stats_{};
     bool profile_ = false;
+    bool graphs_ = true;
     bool capture_inputs_ = false;
     std::string last_trace_;     // events of the last profiled step (JSON)
     long step_counter_ = 0;

@@ -541,3 +541,33 @@ def test_cpp_caller_decodes(native):
     out = subprocess.run([exe], capture_output=True, text=True, timeout=300)
     assert out.returncode == 0, out.stdout + out.stderr
     assert "decode_demo ok" in out.stdout and '"requests"' in out.stdout
+
+
+@pytest.mark.parametrize("weights_on_device", [True, False])
+def test_engine_graph_replay_matches_eager(native, weights_on_device):
+    """Decode steps replayed as CUDA graphs (keyed by launch structure, data in
+    the uploaded metadata) give bit-identical outputs, stats and block tables
+    to eager launches — across block boundaries (new graphs) and reuse."""
+    from paper_2501_01792_b200.api import HostAllocation, PoolCaps
+    cfg = small_cfg(L=3, d=256, H=2, f=512, tpb=8)
+    w = oracle_weights(cfg)
+    rng = np.random.default_rng(41)
+    prompts = [rng.integers(0, cfg.vocab_size, n).tolist() for n in (21, 30)]
+    steps = [rng.integers(0, cfg.vocab_size, 2).tolist() for _ in range(12)]
+    outs = {}
+    for graphs in (False, True):
+        eng = make_engine(cfg, w, max_batch=2, caps=PoolCaps(kv_host=16, act_host=16, act_gpu=2),
+                          allocation=HostAllocation(1, 1), weights_on_device=weights_on_device)
+        eng.set_graphs(graphs)
+        eng.prefill(["a", "b"], prompts)
+        res = []
+        for t in steps:
+            r = eng.decode_step(["a", "b"], t, want_x=True, want_logits=True, want_argmax=True)
+            st = eng.last_stats()
+            res.append((r["x"].copy(), r["logits"].copy(), r["argmax"].copy(), st["h2d_bytes"], st["launches"]))
+        outs[graphs] = (res, eng.cache.dump_json())
+        eng.close()
+    for (a, b) in zip(outs[False][0], outs[True][0]):
+        assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1]) and np.array_equal(a[2], b[2])
+        assert a[3] == b[3] and a[4] == b[4]
+    assert outs[False][1] == outs[True][1]
