@@ -810,9 +810,8 @@ def resident_variants(local, cfg, B, P, arch, steps=2, warmup=1, reserve=6e9, on
     eng = api.Engine(cfg, seed=42, max_seq=P + total + 1, rescale=True, max_batch=B, weights_on_device=True,
                      caps=api.PoolCaps(), mode="act_only", device=local, arch=arch)
     free = torch.cuda.mem_get_info(local)[0] - reserve
-    # x ACT blocks + (N - x) KV blocks (+ x recompute slots) <= free
-    x_fit = max(0, math.ceil((N * kv_all - free) / (kv_all - act_all - kv_one)))
-    r_fit = 0.0 if x_fit == 0 else min(1.0, (x_fit + B) / N)  # all-KV fits: nothing to recompute
+    # the library's HBM-residency planner (csrc/host/plan.hpp: plan_hbm_residency)
+    r_fit, caps_fit = api.plan_hbm_residency(cfg, B, nb, free)
     ids = [f"h{i}" for i in range(B)]
     tokens = np.random.default_rng(9).integers(0, cfg.vocab_size, (total, B)).astype(np.int32)
     out = {"workload": f"{cfg.name}-shape, batch {B}, prompt {P}: weights + cache in HBM (KV and ACT placed on "
@@ -820,13 +819,17 @@ def resident_variants(local, cfg, B, P, arch, steps=2, warmup=1, reserve=6e9, on
            "free_hbm_gb": free / 1e9, "blocks": N, "r_fit": r_fit, "per_ratio": []}
     for r in ([r_fit] if only_planned else sorted({0.0, r_fit, (1.0 + r_fit) / 2, 1.0})):
         a = int(round(r * 1000))
-        act_cap = 0 if r <= 0 else (N if r >= 1 else B * (math.ceil(r * nb) + 1))
-        kv_need = 0 if r >= 1 else (N if r <= 0 else B * (math.ceil((1 - r) * nb) + 1))
-        # KV/gpu blocks that fit next to the ACT blocks, their recompute slots and
-        # the two per-layer staging slots of the overflow (kv_host) blocks
-        room = free - act_cap * (act_all + kv_one) - 2 * kv_need * kv_one
-        kv_gpu = int(max(0, min(kv_need, room // (kv_all - 2 * kv_one))))
-        caps = api.PoolCaps(kv_host=kv_need - kv_gpu, kv_gpu=kv_gpu, act_gpu=act_cap)
+        if r == r_fit:
+            caps = caps_fit
+        else:  # the same capacity rule at a forced share
+            act_cap = 0 if r <= 0 else (N if r >= 1 else B * (math.ceil(r * nb) + 1))
+            kv_need = 0 if r >= 1 else (N if r <= 0 else B * (math.ceil((1 - r) * nb) + 1))
+            # KV/gpu blocks that fit next to the ACT blocks, their recompute slots and
+            # the two per-layer staging slots of the overflow (kv_host) blocks
+            room = free - act_cap * (act_all + kv_one) - 2 * kv_need * kv_one
+            kv_gpu = int(max(0, min(kv_need, room // (kv_all - 2 * kv_one))))
+            caps = api.PoolCaps(kv_host=kv_need - kv_gpu, kv_gpu=kv_gpu, act_gpu=act_cap)
+        act_cap, kv_gpu = caps.act_gpu, caps.kv_gpu
         mode = "kv_only" if r <= 0 else ("act_only" if r >= 1 else "hybrid")
         try:
             eng.configure_cache(caps, mode=mode, allocation=api.HostAllocation(a, 1000 - a), kv_on_gpu=True)

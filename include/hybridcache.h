@@ -89,6 +89,11 @@ int hc_plan_host_allocation(const double* bundle5, const double* mem4, int tpb, 
                             long* alloc6);                                                  /* plan.cpp:106-152 */
 int hc_planned_times(const double* bundle5, int tpb, long act_host, long kv_host, long act_gpu,
                      double* out2);                                   /* planned_t_pcie / _computation 166-177 */
+/* HBM residency (B200 extension, no reference counterpart): smallest ACT share
+ * whose blocks fit hbm_bytes with KV and ACT placed on the GPU first.
+ * out_share = r; out4 = {act_gpu, kv_gpu, act_host, kv_host} pool capacities. */
+int hc_plan_hbm_residency(const hc_model_config* cfg, long requests, long blocks_per_request, double hbm_bytes,
+                          double* out_share, long* out4);
 /* bundle_from_samples (timing.cpp:172-183) from MEASURED samples; out =
  * {kv slope, kv icept, kv r2, kv clamped, load slope, load icept, load r2,
  *  load clamped, t_load_w, s_weight_layer, s_weight_total} */

@@ -331,6 +331,16 @@ def alloc_remaining(bundle: TimingBundle, mem: MemoryBudget, tpb: int, act_init:
     return out[0], out[1]
 
 
+def plan_hbm_residency(cfg: ModelConfig, requests: int, blocks_per_request: int, hbm_bytes: float):
+    """B200 extension of Alg. 1 (csrc/host/plan.hpp): (r, PoolCaps) for a cache placed in
+    HBM first — the smallest ACT share whose blocks fit, the rest in pinned host memory."""
+    c = cfg.to_c()
+    r = C.c_double()
+    out = (C.c_long * 4)()
+    check(lib().hc_plan_hbm_residency(C.byref(c), requests, blocks_per_request, float(hbm_bytes), C.byref(r), out))
+    return r.value, PoolCaps(kv_host=out[3], kv_gpu=out[1], act_host=out[2], act_gpu=out[0])
+
+
 def plan_host_allocation(bundle: TimingBundle, mem: MemoryBudget, tpb: int, act_gpu: int) -> HostAllocation:
     """plan.cpp:106-152 (paper Alg. 1 + frontier polish)."""
     b, bp = bundle.arr5()

@@ -250,6 +250,17 @@ int hc_plan_host_allocation(const double* b, const double* m, int tpb, long act_
         std::memcpy(a6, v, sizeof v);
     });
 }
+int hc_plan_hbm_residency(const hc_model_config* cfg, long requests, long bpr, double hbm_bytes, double* share,
+                          long* out4) {
+    return hc_guard([&] {
+        ModelConfig c = to_cfg(cfg);
+        c.validate();
+        const HbmPlan p = plan_hbm_residency(c, requests, bpr, hbm_bytes);
+        *share = p.act_share;
+        const long v[4] = {p.act_gpu, p.kv_gpu, p.act_host, p.kv_host};
+        std::memcpy(out4, v, sizeof v);
+    });
+}
 int hc_planned_times(const double* b, int tpb, long act_host, long kv_host, long act_gpu, double* out2) {
     return hc_guard([&] {
         HostAllocation a;

@@ -202,4 +202,31 @@ double attention_step_flops(const ModelConfig& c, long ctx) {
     return 4.0 * static_cast<double>(c.hidden_dim) * static_cast<double>(ctx);
 }
 
+HbmPlan plan_hbm_residency(const ModelConfig& c, long requests, long blocks_per_request, double hbm_bytes) {
+    if (requests < 1 || blocks_per_request < 1) throw InputError("plan_hbm_residency: empty workload");
+    if (hbm_bytes <= 0) throw InputError("plan_hbm_residency: no device memory");
+    const double L = c.num_layers;
+    const double kv_one = static_cast<double>(HybridCache::bytes_of(BlockKind::KV, c));
+    const double kv_all = kv_one * L, act_all = static_cast<double>(HybridCache::bytes_of(BlockKind::ACT, c)) * L;
+    const long N = requests * blocks_per_request;
+    HbmPlan p;
+    // x ACT blocks (+ x recompute slots) and N - x KV blocks within hbm_bytes
+    const double x_exact = (N * kv_all - hbm_bytes) / (kv_all - act_all - kv_one);
+    const long x_fit = x_exact <= 0 ? 0 : static_cast<long>(std::ceil(x_exact));
+    p.act_share = x_fit == 0 ? 0.0 : std::min(1.0, static_cast<double>(x_fit + requests) / N);
+    const double r = p.act_share;
+    // per-kind capacities with one block of slack per request (block-boundary rounding)
+    const long act_need = r <= 0 ? 0 : (r >= 1 ? N : requests * (static_cast<long>(std::ceil(r * blocks_per_request)) + 1));
+    const long kv_need = r >= 1 ? 0 : (r <= 0 ? N : requests * (static_cast<long>(std::ceil((1 - r) * blocks_per_request)) + 1));
+    const long act_gpu = static_cast<long>(
+        std::min<double>(act_need, std::floor(hbm_bytes / (act_all + kv_one))));
+    const double room = hbm_bytes - act_gpu * (act_all + kv_one) - 2.0 * kv_need * kv_one;
+    const long kv_gpu = static_cast<long>(std::max(0.0, std::min<double>(kv_need, std::floor(room / (kv_all - 2 * kv_one)))));
+    p.act_gpu = act_gpu;
+    p.act_host = act_need - act_gpu;
+    p.kv_gpu = kv_gpu;
+    p.kv_host = kv_need - kv_gpu;
+    return p;
+}
+
 }  // namespace hc

@@ -64,6 +64,21 @@ HostAllocation plan_host_allocation(const TimingBundle& b, const MemoryBudget& m
 double planned_t_pcie(const TimingBundle& b, int tpb, const HostAllocation& a);
 double planned_t_computation(const TimingBundle& b, int tpb, const HostAllocation& a, long act_gpu);
 
+// HBM residency (B200 extension of Alg. 1; no reference counterpart): the
+// blocks of `requests` x `blocks_per_request` context blocks placed on the GPU
+// first (kv_on_gpu, cache.cpp:64-91) within `hbm_bytes`. With the cache in
+// HBM there is no link time to hide recompute under, so every KV block that
+// fits saves 4 d^2 tpb FLOPs per layer per step: the planned ACT share is the
+// smallest one whose blocks fit (0 when all-KV fits). Each ACT block also
+// needs a recompute slot (one layer of a KV block); blocks that do not fit
+// stay in pinned host memory (KV, streamed through two staging slots).
+struct HbmPlan {
+    double act_share = 0;         // r: HostAllocation target act / (act + kv)
+    long act_gpu = 0, kv_gpu = 0;  // pool capacities (blocks)
+    long act_host = 0, kv_host = 0;
+};
+HbmPlan plan_hbm_residency(const ModelConfig& c, long requests, long blocks_per_request, double hbm_bytes);
+
 // FLOP model (flops.cpp:7-37); kinds: 0 KvGen, 1 QkvGen, 2 Attention,
 // 3 ProjFfn, 4 TokenRecomputeToLayerK, 5 FullLayer.
 double flop_count(int kind, const ModelConfig& c, long n_tokens, int k = 0);

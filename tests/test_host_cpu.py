@@ -236,3 +236,45 @@ def test_model_config_validation():
     c = api.ModelConfig(hidden_dim=64).validate()
     assert c.ffn_dim == 256
     assert api.ModelConfig.preset("opt-66b").num_layers == 64
+
+
+def _hbm_plan_restated(cfg, B, nb, hbm):
+    """Python restatement of plan_hbm_residency (csrc/host/plan.hpp)."""
+    import math
+    from paper_2501_01792_b200 import api
+    L = cfg.num_layers
+    kv_one = api.HybridCache.bytes_of("KV", cfg)
+    kv_all, act_all = kv_one * L, api.HybridCache.bytes_of("ACT", cfg) * L
+    N = B * nb
+    x_exact = (N * kv_all - hbm) / (kv_all - act_all - kv_one)
+    x_fit = 0 if x_exact <= 0 else math.ceil(x_exact)
+    r = 0.0 if x_fit == 0 else min(1.0, (x_fit + B) / N)
+    act_need = 0 if r <= 0 else (N if r >= 1 else B * (math.ceil(r * nb) + 1))
+    kv_need = 0 if r >= 1 else (N if r <= 0 else B * (math.ceil((1 - r) * nb) + 1))
+    act_gpu = int(min(act_need, math.floor(hbm / (act_all + kv_one))))
+    room = hbm - act_gpu * (act_all + kv_one) - 2.0 * kv_need * kv_one
+    kv_gpu = int(max(0, min(kv_need, math.floor(room / (kv_all - 2 * kv_one)))))
+    return r, (act_gpu, kv_gpu, act_need - act_gpu, kv_need - kv_gpu)
+
+
+@pytest.mark.parametrize("model,B,nb,hbm_gb", [("opt-30b", 128, 65, 124.6), ("opt-13b", 64, 129, 150.0),
+                                               ("opt-66b", 128, 65, 40.0), ("opt-6.7b", 8, 10, 500.0),
+                                               ("opt-30b", 128, 65, 20.0)])
+def test_plan_hbm_residency(model, B, nb, hbm_gb):
+    """HBM-residency planner (B200 extension of Alg. 1): smallest ACT share
+    whose blocks fit; 0 when all-KV fits; capacities cover the workload."""
+    from paper_2501_01792_b200 import api
+    cfg = api.ModelConfig.preset(model)
+    r, caps = api.plan_hbm_residency(cfg, B, nb, hbm_gb * 1e9)
+    r2, c2 = _hbm_plan_restated(cfg, B, nb, hbm_gb * 1e9)
+    assert r == pytest.approx(r2, abs=1e-15)
+    assert (caps.act_gpu, caps.kv_gpu, caps.act_host, caps.kv_host) == c2
+    assert 0.0 <= r <= 1.0
+    kv_one = api.HybridCache.bytes_of("KV", cfg)
+    used = (caps.act_gpu * (api.HybridCache.bytes_of("ACT", cfg) * cfg.num_layers + kv_one) +
+            caps.kv_gpu * kv_one * cfg.num_layers + 2 * caps.kv_host * kv_one)
+    assert used <= hbm_gb * 1e9 * 1.0000001
+    if hbm_gb >= 500:
+        assert r == 0.0 and caps.kv_host == 0
+    with pytest.raises(api.InputError):
+        api.plan_hbm_residency(cfg, 0, nb, 1e9)
