@@ -571,3 +571,21 @@ def test_engine_graph_replay_matches_eager(native, weights_on_device):
         assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1]) and np.array_equal(a[2], b[2])
         assert a[3] == b[3] and a[4] == b[4]
     assert outs[False][1] == outs[True][1]
+
+
+def test_engine_tp_nccl_group_of_one(native):
+    """The NCCL path of the head-sharded variant on the box: libnccl is
+    dlopen'ed (torch's copy), a 1-rank communicator pair is created, and an
+    engine driven through it matches the oracle (collectives degenerate)."""
+    import torch  # noqa: F401  (NCCL provider first)
+    from paper_2501_01792_b200.api import HostAllocation, PoolCaps, TensorParallel
+    cfg = small_cfg(L=2, d=256, H=2, f=512, tpb=8)
+    w = oracle_weights(cfg)
+    tp = TensorParallel.nccl(TensorParallel.nccl_unique_ids(), 0, 1, 0)
+    eng = make_engine(cfg, w, max_batch=1, caps=PoolCaps(kv_host=8, act_host=8), allocation=HostAllocation(1, 1),
+                      tp=tp)
+    prompt = np.random.default_rng(3).integers(0, cfg.vocab_size, 19).tolist()
+    eng.prefill(["n"], [prompt])
+    x = f64(eng.decode_step(["n"], [5])["x"][0])
+    assert rel(x, O.forward_prompt(prompt + [5], w).output[-1]) <= TOL
+    eng.close()
