@@ -191,7 +191,8 @@ int hc_prefill_attention(int n_req, int P, int H, int hd, const uint16_t* qkv, i
         for (int r = 0; r <= n_req; ++r) cu[r] = r * P;
         DevBuf<int> dcu(cu.data(), cu.size());
         prefill_attention(reinterpret_cast<const bf16*>(dq.p), reinterpret_cast<bf16*>(o.p), dcu.p, n_req, P, H, hd,
-                          scaled ? 1.0f / std::sqrt(static_cast<float>(hd)) : 1.0f, nullptr);
+                          scaled ? 1.0f / std::sqrt(static_cast<float>(hd)) : 1.0f, nullptr,
+                          static_cast<long long>(n_req) * P);
         HC_CUDA(cudaGetLastError());
         HC_CUDA(cudaDeviceSynchronize());
         o.to_host(out);

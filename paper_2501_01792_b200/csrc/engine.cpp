@@ -683,7 +683,7 @@ void Engine::run_layers(int T, int l0, int l1, const int* d_cu, uint16_t* layer_
             }
         }
         prefill_attention(m.pqkv, m.patt, d_cu, 1, T, m.H, m.hd,
-                          opt_.scaled ? 1.0f / std::sqrt(static_cast<float>(m.hd)) : 1.0f, s_compute_);
+                          opt_.scaled ? 1.0f / std::sqrt(static_cast<float>(m.hd)) : 1.0f, s_compute_, T);
         m.tail(W, m.patt, xin, T, m.pproj, m.patt, m.ph, xout, s_compute_);
     }
     const bf16* y = final_ln ? m.final_norm(m.px[l1 & 1], T, m.pxn, s_compute_) : m.px[l1 & 1];
@@ -876,7 +876,7 @@ void Engine::prefill(const std::vector<std::string>& ids, const std::vector<std:
             sk.n_blocks = static_cast<int>(c.k_src.size());
             scatter_kv_blocks(sk, s_compute_);
             m.span_begin(profile_, s_compute_, 1);
-            prefill_attention(m.pqkv, m.patt, dm + c.o_cu, c.n, c.max_len, m.Hg, m.hd, scale, s_compute_);
+            prefill_attention(m.pqkv, m.patt, dm + c.o_cu, c.n, c.max_len, m.Hg, m.hd, scale, s_compute_, c.rows);
             m.span_end(profile_, s_compute_);
             m.span_begin(profile_, s_compute_, 2);
             m.tail(W, m.patt, cin, c.rows, m.pproj, m.patt, m.ph, cout, s_compute_);
@@ -1179,7 +1179,7 @@ void Engine::decode_step(const std::vector<std::string>& ids, const int* tokens,
             sk.tpb = m.tpb;
             scatter_kv_blocks(sk, s_compute_);
             if (l + 1 < m.L) {  // the last layer's prefix output is never needed
-                prefill_attention(m.pqkv, m.patt, dm + o_rcu, n, rc_max, m.H, m.hd, scale, s_compute_);
+                prefill_attention(m.pqkv, m.patt, dm + o_rcu, n, rc_max, m.H, m.hd, scale, s_compute_, n_rc);
                 m.tail(W, m.patt, pin, n_rc, m.pproj, m.patt, m.ph, pout, s_compute_);
                 st.launches += 1 + m.tail_launches();
             }

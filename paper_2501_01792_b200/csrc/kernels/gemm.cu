@@ -11,6 +11,7 @@
 
 #include "gemm.cuh"
 #include "kernels.hpp"
+#include "tma.hpp"
 
 namespace hc {
 
@@ -30,6 +31,8 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     return fn;
 }
 
+}  // namespace
+
 // 2-D bf16 tensor [rows x cols] with row stride ld (elements); box = box_rows x 64.
 CUtensorMap make_map(const void* ptr, long long rows, long long cols, long long ld, int box_rows) {
     CUtensorMap m;
@@ -47,6 +50,8 @@ CUtensorMap make_map(const void* ptr, long long rows, long long cols, long long 
                                  " ld=" + std::to_string(ld));
     return m;
 }
+
+namespace {
 
 template <int BN, int EPI>
 void launch(const GemmCall& c, const gemm::Params& p, cudaStream_t st) {

@@ -269,9 +269,13 @@ void launch_prefill(const bf16* qkv, bf16* out, const int* cu, int n_req, int ma
 
 }  // namespace
 
+bool prefill_attention_tc(const bf16* qkv, long long rows, bf16* out, const int* cu, int n_req, int max_len, int H,
+                          int hd, float scale, cudaStream_t st);
+
 void prefill_attention(const bf16* qkv, bf16* out, const int* cu, int n_req, int max_len, int H, int hd,
-                       float scale, cudaStream_t st) {
+                       float scale, cudaStream_t st, long long rows) {
     if (n_req <= 0 || max_len <= 0) return;
+    if (prefill_attention_tc(qkv, rows, out, cu, n_req, max_len, H, hd, scale, st)) return;
     if (hd == 128)
         launch_prefill<128>(qkv, out, cu, n_req, max_len, H, scale, st);
     else if (hd == 64)

@@ -1,0 +1,318 @@
+// Causal prefill attention on the 5th-gen tensor cores (tcgen05 + TMEM + TMA),
+// head_dim 128 (attention_causal, decoder.cpp:55-63).
+//
+// One CTA per (128-query tile, head, request); 192 threads:
+//   warp 0      TMA producer: Q once, then K|V tiles of 128 keys into a
+//               2-stage ring (one tensor map over the packed Q|K|V rows)
+//   warp 1      TMEM owner + single-thread MMA issuer:
+//                 S[j%2] = Q . K_j^T        (M=128, N=128 keys, K=hd)
+//                 O     += P_j . V_j        (M=128, N=hd, K=128 keys; V read
+//                                            MN-major straight from its tile)
+//               S_{j+1} is issued before P_j arrives, so the QK^T of the next
+//               tile overlaps the softmax of this one (two S buffers in TMEM)
+//   warps 2..5  softmax: thread = query row = TMEM lane; S row via tcgen05.ld,
+//               causal / ragged mask, online max in the exp2 domain with a
+//               lazy O correction (only when the max grows by > 2^8, so P
+//               stays <= 256 and O is rescaled in TMEM rarely), P (bf16) into
+//               a 128B-swizzled K-major smem tile for the P.V MMA; finally
+//               O / l from TMEM to HBM.
+// TMEM: S0 | S1 | O = 384 of 512 columns. smem: Q 32 KB, 2 x (K 32 + V 32) KB,
+// P 32 KB = 192 KB -> one CTA per SM. Heavy (late) query tiles launch first.
+#include <cuda.h>
+
+#include <cfloat>
+#include <cstdlib>
+#include <stdexcept>
+
+#include "kernels.hpp"
+#include "ptx.cuh"
+#include "tma.hpp"
+
+namespace hc {
+
+namespace {
+
+constexpr int kT = 128;        // queries per CTA = keys per tile
+constexpr int kHD = 128;       // head dim
+constexpr int kBox = kT * 64 * 2;           // one [128 rows][64 cols] bf16 box = 16 KB
+constexpr int kTile = 2 * kBox;             // [128][128] = 32 KB
+constexpr int kStages = 2;
+constexpr int kThreads = 192;
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr float kRescale = 8.0f;            // lazy correction threshold (log2 units)
+
+struct Smem {
+    static constexpr int q = 0;
+    static constexpr int k = kTile;                       // stage s at k + s * 2 * kTile
+    static constexpr int v = 2 * kTile;                   // stage s at v + s * 2 * kTile
+    static constexpr int p = (1 + 2 * kStages) * kTile;
+    static constexpr int bars = p + kTile;
+    static constexpr int bytes = bars + 256 + 1024;       // + barrier block + 1 KB alignment slack
+};
+
+__device__ __forceinline__ void tmem_st_x16(uint32_t taddr, const uint32_t (&r)[16]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+        "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+        "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+        : "memory");
+}
+__device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// MN-major, 128B-swizzled operand (V: rows = K (keys), 64 N (hd) per 128 B row):
+// SBO = 1024 B between 8-row (K) groups, LBO = 16 KB between 64-wide N boxes.
+__device__ __forceinline__ uint64_t sw128_mnmajor_desc(uint32_t smem_addr, uint32_t lbo, uint32_t sbo) {
+    uint64_t d = 0;
+    d |= static_cast<uint64_t>((smem_addr >> 4) & 0x3FFF);
+    d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFF) << 16;
+    d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFF) << 32;
+    d |= static_cast<uint64_t>(1) << 46;
+    d |= static_cast<uint64_t>(2) << 61;
+    return d;
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    prefill_tc_kernel(const __grid_constant__ CUtensorMap tm, bf16* __restrict__ out, const int* __restrict__ cu,
+                      int H, float scale, uint32_t v_lbo, uint32_t v_sbo) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Smem::bars);
+    uint64_t* q_full = bars + 0;
+    uint64_t* kv_full = bars + 1;      // [kStages]
+    uint64_t* kv_empty = bars + 3;     // [kStages]
+    uint64_t* s_full = bars + 5;       // [2]
+    uint64_t* s_free = bars + 7;       // [2]
+    uint64_t* p_full = bars + 9;
+    uint64_t* pv_done = bars + 10;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
+
+    const int req = blockIdx.z, h = blockIdx.y;
+    const int row0 = cu[req];
+    const int P = cu[req + 1] - row0;
+    const int n_qt = (P + kT - 1) / kT;
+    const int qt = static_cast<int>(gridDim.x) - 1 - static_cast<int>(blockIdx.x);
+    if (qt >= n_qt) return;
+    const int q0 = qt * kT;
+    const int n_kt = qt + 1;  // causal: key tiles 0..qt (q and key tiles aligned)
+    const int d = H * kHD;
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+
+    if (threadIdx.x == 0) {
+        ptx::tma_prefetch(&tm);
+        ptx::mbar_init(q_full, 1);
+        for (int s = 0; s < kStages; ++s) {
+            ptx::mbar_init(&kv_full[s], 1);
+            ptx::mbar_init(&kv_empty[s], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            ptx::mbar_init(&s_full[b], 1);
+            ptx::mbar_init(&s_free[b], 128);
+        }
+        ptx::mbar_init(p_full, 128);
+        ptx::mbar_init(pv_done, 1);
+        ptx::fence_mbar_init();
+    }
+    if (warp == 1) ptx::tmem_alloc<512>(tmem_slot);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    auto t_s = [&](int b) { return tmem + 128u * static_cast<uint32_t>(b); };  // S double buffer
+    const uint32_t t_o = tmem + 256;
+
+    if (warp == 0) {
+        if (lane == 0) {  // ---------------------------------------- TMA producer
+            const int qc = h * kHD, kc = d + h * kHD, vc = 2 * d + h * kHD;
+            ptx::mbar_arrive_expect_tx(q_full, kTile);
+            ptx::tma_load_2d(smem + Smem::q, &tm, q_full, qc, row0 + q0);
+            ptx::tma_load_2d(smem + Smem::q + kBox, &tm, q_full, qc + 64, row0 + q0);
+            for (int j = 0; j < n_kt; ++j) {
+                const int s = j % kStages;
+                ptx::mbar_wait(&kv_empty[s], ((j / kStages) & 1) ^ 1);
+                uint8_t* kb = smem + Smem::k + s * 2 * kTile;
+                uint8_t* vb = smem + Smem::v + s * 2 * kTile;
+                ptx::mbar_arrive_expect_tx(&kv_full[s], 2 * kTile);
+                const int r = row0 + j * kT;
+                ptx::tma_load_2d(kb, &tm, &kv_full[s], kc, r);
+                ptx::tma_load_2d(kb + kBox, &tm, &kv_full[s], kc + 64, r);
+                ptx::tma_load_2d(vb, &tm, &kv_full[s], vc, r);
+                ptx::tma_load_2d(vb + kBox, &tm, &kv_full[s], vc + 64, r);
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {  // ------------------------------------------ MMA issuer
+            constexpr uint32_t id_s = ptx::idesc_bf16_f32(kT, kT);               // A, B K-major
+            constexpr uint32_t id_o = ptx::idesc_bf16_f32(kT, kHD) | (1u << 16);  // B MN-major (V)
+            const uint32_t qa = ptx::smem_u32(smem + Smem::q);
+            const uint32_t pa = ptx::smem_u32(smem + Smem::p);
+            auto issue_s = [&](int j) {
+                const int s = j % kStages, b = j & 1;
+                ptx::mbar_wait(&kv_full[s], (j / kStages) & 1);
+                if (j >= 2) ptx::mbar_wait(&s_free[b], ((j - 2) / 2) & 1);
+                ptx::tc_fence_after();
+                const uint32_t kb = ptx::smem_u32(smem + Smem::k + s * 2 * kTile);
+#pragma unroll
+                for (int k = 0; k < kHD / 16; ++k) {  // hd in two 64-wide boxes, 4 k-steps each
+                    const uint32_t off = (k / 4) * kBox;
+                    ptx::mma_bf16_ss(t_s(b), ptx::sw128_kmajor_desc(qa + off) + 2 * (k % 4),
+                                     ptx::sw128_kmajor_desc(kb + off) + 2 * (k % 4), id_s, k > 0);
+                }
+                ptx::mma_commit(&s_full[b]);
+            };
+            ptx::mbar_wait(q_full, 0);
+            issue_s(0);
+            for (int j = 0; j < n_kt; ++j) {
+                if (j + 1 < n_kt) issue_s(j + 1);
+                ptx::mbar_wait(p_full, j & 1);
+                ptx::tc_fence_after();
+                const int s = j % kStages;
+                const uint32_t vb = ptx::smem_u32(smem + Smem::v + s * 2 * kTile);
+#pragma unroll
+                for (int k = 0; k < kT / 16; ++k) {  // keys: P in two 64-wide boxes; V rows 16 per step
+                    const uint64_t a = ptx::sw128_kmajor_desc(pa + (k / 4) * kBox) + 2 * (k % 4);
+                    const uint64_t bdesc = sw128_mnmajor_desc(vb + k * 16 * 128, v_lbo, v_sbo);
+                    ptx::mma_bf16_ss(t_o, a, bdesc, id_o, (j > 0 || k > 0) ? 1u : 0u);
+                }
+                ptx::mma_commit(pv_done);
+                ptx::mma_commit(&kv_empty[s]);
+            }
+        }
+    } else {  // ----------------------------------------------------- softmax
+        const int q = warp % 4;
+        const int r = q * 32 + lane;            // query row within the tile = TMEM lane
+        const int qrow = q0 + r;                // row within the request
+        const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
+        const float sl = scale * kLog2e;
+        float m = -FLT_MAX, l = 0.f;
+        uint8_t* prow = smem + Smem::p;
+        for (int j = 0; j < n_kt; ++j) {
+            const int b = j & 1;
+            ptx::mbar_wait(&s_full[b], (j / 2) & 1);
+            ptx::tc_fence_after();
+            float sv[kT];
+#pragma unroll
+            for (int c = 0; c < kT; c += 16) {
+                uint32_t v[16];
+                ptx::tmem_ld_x16(t_s(b) + lane_off + c, v);
+                ptx::tmem_ld_wait();
+#pragma unroll
+                for (int i = 0; i < 16; ++i) sv[c + i] = __uint_as_float(v[i]);
+            }
+            ptx::tc_fence_before();
+            ptx::mbar_arrive(&s_free[b]);
+            const int k0 = j * kT;
+            const bool diag = j == n_kt - 1 || k0 + kT > P;
+            float mx = -FLT_MAX;
+#pragma unroll
+            for (int i = 0; i < kT; ++i) {
+                float x = sv[i] * sl;
+                if (diag && (k0 + i > qrow || k0 + i >= P)) x = -FLT_MAX;
+                sv[i] = x;
+                mx = fmaxf(mx, x);
+            }
+            // lazy correction: keep the reference max unless it grows by > 2^8
+            float alpha = 1.f;
+            bool rescale = false;
+            if (mx > m + kRescale || j == 0) {
+                alpha = exp2f(m - mx);
+                rescale = j > 0;
+                m = mx;
+                l *= alpha;
+            }
+            // the P buffer and O are free once the previous P.V has completed
+            if (j > 0) {
+                ptx::mbar_wait(pv_done, (j - 1) & 1);
+                ptx::tc_fence_after();
+            }
+            if (rescale) {
+#pragma unroll 1
+                for (int c = 0; c < kHD; c += 16) {
+                    uint32_t v[16];
+                    ptx::tmem_ld_x16(t_o + lane_off + c, v);
+                    ptx::tmem_ld_wait();
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * alpha);
+                    tmem_st_x16(t_o + lane_off + c, v);
+                }
+                tmem_st_wait();
+            }
+            // P row -> two 64-key 128B-swizzled K-major boxes
+#pragma unroll
+            for (int c = 0; c < kT / 8; ++c) {  // 16-byte chunks of 8 keys
+                uint32_t w[4];
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                    const float p0 = exp2f(sv[8 * c + 2 * t] - m), p1 = exp2f(sv[8 * c + 2 * t + 1] - m);
+                    l += p0 + p1;
+                    w[t] = ptx::pack_bf16x2(p0, p1);
+                }
+                const int box = c / 8, ch = c % 8;
+                uint8_t* dst = prow + box * kBox + (r / 8) * 1024 + (r % 8) * 128 + ((ch ^ (r % 8)) * 16);
+                *reinterpret_cast<uint4*>(dst) = make_uint4(w[0], w[1], w[2], w[3]);
+            }
+            fence_async_smem();
+            ptx::tc_fence_before();
+            ptx::mbar_arrive(p_full);
+        }
+        // O / l -> HBM
+        ptx::mbar_wait(pv_done, (n_kt - 1) & 1);
+        ptx::tc_fence_after();
+        const float inv = l > 0.f ? 1.f / l : 0.f;
+        bf16* orow = out + static_cast<long long>(row0 + qrow) * d + h * kHD;
+#pragma unroll 1
+        for (int c = 0; c < kHD; c += 16) {
+            uint32_t v[16];
+            ptx::tmem_ld_x16(t_o + lane_off + c, v);
+            ptx::tmem_ld_wait();
+            uint32_t o[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+                o[i] = ptx::pack_bf16x2(__uint_as_float(v[2 * i]) * inv, __uint_as_float(v[2 * i + 1]) * inv);
+            if (qrow < P) {
+                ptx::st_global_v4(orow + c, o[0], o[1], o[2], o[3]);
+                ptx::st_global_v4(orow + c + 8, o[4], o[5], o[6], o[7]);
+            }
+        }
+        ptx::tc_fence_before();
+    }
+    __syncthreads();
+    if (warp == 1) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc<512>(tmem);
+    }
+}
+
+}  // namespace
+
+// Tensor-core path for head_dim 128 (prefill_attention.cu dispatches here);
+// rows = total rows of qkv (the TMA map bounds).
+bool prefill_attention_tc(const bf16* qkv, long long rows, bf16* out, const int* cu, int n_req, int max_len, int H,
+                          int hd, float scale, cudaStream_t st) {
+    static const int enabled = [] {
+        const char* e = std::getenv("HC_PREFILL_TC");
+        return e ? std::atoi(e) : 1;
+    }();
+    if (!enabled || hd != kHD || rows <= 0) return false;
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(prefill_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem::bytes);
+        configured = true;
+    }
+    const long long d3 = 3LL * H * kHD;
+    const CUtensorMap tm = make_map(qkv, rows, d3, d3, kT);
+    static const uint32_t lbo = [] {
+        const char* e = std::getenv("HC_PREFILL_TC_LBO");
+        return e ? static_cast<uint32_t>(std::atoi(e)) : static_cast<uint32_t>(kBox);
+    }();
+    static const uint32_t sbo = [] {
+        const char* e = std::getenv("HC_PREFILL_TC_SBO");
+        return e ? static_cast<uint32_t>(std::atoi(e)) : 1024u;
+    }();
+    const dim3 grid((max_len + kT - 1) / kT, H, n_req);
+    prefill_tc_kernel<<<grid, kThreads, Smem::bytes, st>>>(tm, out, cu, H, scale, lbo, sbo);
+    return true;
+}
+
+}  // namespace hc
