@@ -603,14 +603,17 @@ def our_arm(args, cfg, world, rank, local, dist):
     # = 4 d^2 x ACT context tokens of the layer (flops.cpp:14)
     rec_launch_ms = prof["recompute_ms"] / max(prof["recompute_launches"], 1)
     rec_flops = 4.0 * d * d * act_tokens / max(prof["recompute_launches"] / L, 1)
+    rec_rows = act_tokens / max(prof["recompute_launches"] / L, 1)  # ACT rows per launch
     achieved = rec_flops / (rec_launch_ms / 1e3) / 1e12 if rec_launch_ms > 0 else 0.0
     roof = {"kernel": "gemm_tn_kernel<256,kKvPaged> (ACT->K|V recompute)", "bound": "tensor",
             "achieved": achieved, "peak": tflops_sust, "unit": "TFLOP/s",
             "frac": achieved / tflops_sust if tflops_sust else None,
-            "traffic": 6.65e9, "traffic_note": "ncu dram__bytes_read+write per launch, profiles/r01_ncu_recompute.csv "
-                                                "(algorithmic 2.07e9: A 0.62 + W 0.21 read, K|V 1.24 write; the "
-                                                "L2-capacity floor for this shape is ~5e9: [Wk|Wv] is 205 MB > the "
-                                                "126 MB L2, so any tile schedule re-reads A or B — DESIGN.md §3)",
+            "traffic": rec_rows * 1.525e5,
+            "traffic_note": ("ncu dram__bytes_read+write per launch scaled by ACT rows: 18.73e9 B at 122880 rows "
+                             "(1.525e5 B/row, OPT-30B width; profiles/r01_ncu_recompute.csv). Algorithmic "
+                             f"{rec_rows * (3 * d * 2) + 2 * d * d * 2:.3e} B (A + [Wk|Wv] read once, K|V written "
+                             "once); the excess is [Wk|Wv] (205 MB > the 126 MB L2) re-read once per 16-tile M "
+                             "group — the L2-capacity floor for this shape, DESIGN.md §3"),
             "peak_source": f"{peak_src} bf16_tflops_sustained (MEASURED_PEAKS.json); burst {tflops_burst}",
             "flops_per_launch": rec_flops, "launch_ms": rec_launch_ms}
     # per-step roofline (north_star): slower of link bytes / link BW, tensor
