@@ -187,6 +187,11 @@ void run_gemm(const GemmCall& c, cudaStream_t st) {
     p.ldr = c.ldr;
     p.group_m = c.group_m > 0 ? c.group_m : (c.K <= 4096 ? 32 : 16);
     if (const char* g = std::getenv("HC_GEMM_GROUP_M")) p.group_m = std::max(1, std::atoi(g));  // tuning knob
+    static const int group_n_env = [] {
+        const char* g = std::getenv("HC_GEMM_GROUP_N");  // tuning knob: weight-stationary raster
+        return g ? std::atoi(g) : 0;
+    }();
+    p.group_n = group_n_env;
     p.splits = 1;
     p.kb_per_split = (c.K + gemm::BK - 1) / gemm::BK;
     GemmCall cc = c;

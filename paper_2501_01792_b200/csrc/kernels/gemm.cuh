@@ -37,6 +37,7 @@ struct Params {
     // kKvPaged: row r -> block r / tpb + blk_off, token r % tpb
     int tpb, d, hd, blk_off;
     int group_m;  // M tiles per rasterisation group (A tiles kept in L2 while N is swept)
+    int group_n;  // > 0: N tiles per group instead (B tiles kept in L2 while M is swept)
     // split-K (kSplitF32): work unit = (tile, split); split s covers k-blocks
     // [s*kb_per_split, (s+1)*kb_per_split) and writes fp32 partials to
     // out + (s*M + row)*ldc
@@ -63,6 +64,17 @@ __device__ __forceinline__ void tile_coords(int tile, const Params& p, int& m_id
     // grouped rasterisation: group_m M-tiles share each sweep over N so
     // concurrently running CTAs reuse A and B tiles from L2
     tile %= p.num_m_tiles * p.num_n_tiles;  // split-K units repeat the tile grid
+    if (p.group_n > 0) {  // weight-stationary: a group of N tiles sweeps all of M
+        const int G = p.num_n_tiles < p.group_n ? p.num_n_tiles : p.group_n;
+        const int group = G * p.num_m_tiles;
+        const int g = tile / group;
+        const int first_n = g * G;
+        const int gn = (p.num_n_tiles - first_n) < G ? (p.num_n_tiles - first_n) : G;
+        const int within = tile - g * group;
+        n_idx = first_n + within % gn;
+        m_idx = within / gn;
+        return;
+    }
     const int G = p.num_m_tiles < p.group_m ? p.num_m_tiles : p.group_m;
     const int group = G * p.num_n_tiles;
     const int g = tile / group;
@@ -297,7 +309,19 @@ struct Cfg2 {
     static constexpr int kSmemBytes = kStages * kStageBytes + kBarBytes + 1024;
 };
 
-__device__ __forceinline__ void pair_tile_coords(int tile, int num_pm, int num_n, int group, int& pm, int& ni) {
+__device__ __forceinline__ void pair_tile_coords(int tile, int num_pm, int num_n, int group, int group_n, int& pm,
+                                                 int& ni) {
+    if (group_n > 0) {  // weight-stationary raster (see tile_coords)
+        const int G = num_n < group_n ? num_n : group_n;
+        const int per = G * num_pm;
+        const int g = tile / per;
+        const int first = g * G;
+        const int gn = (num_n - first) < G ? (num_n - first) : G;
+        const int within = tile - g * per;
+        ni = first + within % gn;
+        pm = within / gn;
+        return;
+    }
     const int G = num_pm < group ? num_pm : group;
     const int per = G * num_n;
     const int g = tile / per;
@@ -369,7 +393,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             uint32_t phase = 0;
             for (int tile = pair; tile < num_tiles; tile += num_pairs) {
                 int pm, ni;
-                pair_tile_coords(tile, num_pm, p.num_n_tiles, p.group_m, pm, ni);
+                pair_tile_coords(tile, num_pm, p.num_n_tiles, p.group_m, p.group_n, pm, ni);
                 const int m_row = m_row_of(pm, rank);
                 const int n_row = ni * BN + static_cast<int>(rank) * (BN / 2);
                 for (int kb = 0; kb < num_kb; ++kb) {
@@ -422,7 +446,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         uint32_t aphase = 0;
         for (int tile = pair; tile < num_tiles; tile += num_pairs) {
             int pm, ni;
-            pair_tile_coords(tile, num_pm, p.num_n_tiles, p.group_m, pm, ni);
+            pair_tile_coords(tile, num_pm, p.num_n_tiles, p.group_m, p.group_n, pm, ni);
             const int row = m_row_of(pm, rank) + q * 32 + lane;
             const int n0 = ni * BN;
             ptx::mbar_wait(&tfull[as], aphase);
