@@ -529,7 +529,7 @@ def our_arm(args, cfg, world, rank, local, dist):
         B = per_rank_batch(args, world, rank)
     P, L, d = args.prompt, cfg.num_layers, cfg.hidden_dim
     total_steps = args.warmup + args.steps + 2
-    max_seq = P + total_steps + 1
+    max_seq = P + max(total_steps, args.gen + 4) + 1  # room for the end-of-generation step (below)
     r = args.ratio if args.ratio >= 0 else 1.0 / 3.0  # planner replaces the default below
     mode, alloc, caps = pool_plan(cfg, B, P, total_steps, r)
     w_layer, _ = api.weight_bytes(cfg)
@@ -641,17 +641,30 @@ def our_arm(args, cfg, world, rank, local, dist):
     # steps at context P+g projected from the measured step by streamed bytes
     # (the step is link-bound: step_roofline.bound == "link")
     gen = None
-    if prefill is not None:
-        w_all = L * w_layer
-        cache0 = max(h2d_step - w_all, 0.0)
-        ctx0 = P + args.warmup + 1 + (args.steps - 1) / 2.0
-        dec_s = sum(ms_per_step / 1e3 * (w_all + cache0 * (P + g) / ctx0) / h2d_step for g in range(args.gen))
-        gen = {"prefill_s": prefill["prefill_s"], "decode_s_projected": dec_s, "gen_len": args.gen,
-               "tokens_per_s": B * args.gen / (prefill["prefill_s"] + dec_s),
-               "tokens_per_s_all_ranks": B * args.gen * world / (prefill["prefill_s"] + dec_s),
-               "prefill_share": prefill["prefill_s"] / (prefill["prefill_s"] + dec_s),
-               "method": "prefill measured; decode step(P+g) = measured step x streamed bytes(P+g)/bytes(P) "
-                         "(link-bound), summed over the gen length"}
+    if prefill is not None and not args.no_sweep:
+        # the decode step at the END of the generation (context P + G), measured on
+        # the same engine and ratio: step time is linear in the context (streamed
+        # blocks, attention bytes), so the G steps sum to G x the endpoint mean
+        try:
+            ctx_end = P + args.gen
+            _, alloc_e, caps_e = pool_plan(cfg, B, ctx_end, 4, r)
+            eng.configure_cache(caps_e, mode=mode, allocation=alloc_e,
+                                host_layers=host_layers_for(cfg, caps_e, budget, Lw * w_rank, tpn))
+            eng.admit_synthetic(ids, [ctx_end] * B, seed=3 + rank)
+            run_steps(eng, ids, tokens, 0, 1)
+            end = run_steps(eng, ids, tokens, 1, 2)
+            ms_end = end["dev_ms"] / 2
+            dec_s = args.gen * (ms_per_step + ms_end) / 2e3
+            gen = {"prefill_s": prefill["prefill_s"], "step_ms_at_prompt": ms_per_step,
+                   "step_ms_at_prompt_plus_gen": ms_end, "decode_s": dec_s, "gen_len": args.gen,
+                   "tokens_per_s": B * args.gen / (prefill["prefill_s"] + dec_s),
+                   "tokens_per_s_all_ranks": B * args.gen * world / (prefill["prefill_s"] + dec_s),
+                   "prefill_share": prefill["prefill_s"] / (prefill["prefill_s"] + dec_s),
+                   "method": "prefill measured; decode steps measured at context P and P+G (same ratio, real "
+                             "allocator, pattern-filled blocks), summed as G x their mean (step time is linear "
+                             "in the context)"}
+        except Exception as e:  # must not cost the bench line
+            gen = {"error": str(e)}
 
     # ---- per-ratio sweep, planner, HBM-tiered variant (untimed by the contract)
     extra = {}
@@ -759,7 +772,7 @@ def our_arm(args, cfg, world, rank, local, dist):
             "setup_s": setup_s,
             "planner": planner,
             "prefill": prefill,
-            "generation_e2e_projected": gen,
+            "generation_e2e": gen,
             "tensor_parallel": tp_info,
         }
         if tp is not None:
