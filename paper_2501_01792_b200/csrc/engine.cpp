@@ -104,7 +104,9 @@ struct Engine::Impl {
     uint16_t* h_w = nullptr;
     bf16 *kv_gpu = nullptr, *act_gpu = nullptr, *kvr = nullptr;
     bf16 *kv_stage[2] = {nullptr, nullptr}, *act_stage[2] = {nullptr, nullptr};
-    bf16 *kv_host = nullptr, *act_host = nullptr;  // pinned, mapped
+    bf16 *kv_host = nullptr, *act_host = nullptr;  // pinned, mapped (views into h_arena)
+    bf16* h_arena = nullptr;
+    size_t h_arena_elems = 0;
     long kv_host_cap = 0, kv_gpu_cap = 0, act_host_cap = 0, act_gpu_cap = 0;
     bf16 *x[2] = {nullptr, nullptr}, *qkvb = nullptr, *att = nullptr, *proj = nullptr, *hbuf = nullptr;
     float* logits = nullptr;
@@ -535,10 +537,7 @@ void Engine::configure_cache(const PoolCaps& caps, bool kv_on_gpu, CacheMode mod
         if (*p) cudaFree(*p);
         *p = nullptr;
     }
-    for (bf16** p : {&m.kv_host, &m.act_host}) {
-        if (*p) cudaFreeHost(*p);
-        *p = nullptr;
-    }
+    m.kv_host = m.act_host = nullptr;  // views into the pinned arena (re-carved below)
     assigner_.reset();
     opt_.kv_host_cap = caps.kv_host;
     opt_.kv_gpu_cap = caps.kv_gpu;
@@ -566,8 +565,21 @@ void Engine::configure_cache(const PoolCaps& caps, bool kv_on_gpu, CacheMode mod
     m.kv_gpu = dalloc<bf16>(static_cast<size_t>(m.L) * m.kv_gpu_cap * m.kvb);
     m.act_gpu = dalloc<bf16>(static_cast<size_t>(m.L) * m.act_gpu_cap * m.actb);
     m.act_cap_n = (m.act_host_cap + m.tpn - 1) / m.tpn;
-    m.kv_host = halloc<bf16>(static_cast<size_t>(m.Lp) * m.kv_host_cap * m.kvb, true);
-    m.act_host = halloc<bf16>(static_cast<size_t>(m.Lp) * m.act_cap_n * m.actb, true);
+    // pinned, mapped host pools: one arena, kept across configure_cache calls
+    // while it is large enough (pinning tens of GB takes seconds per call)
+    {
+        const size_t kv_e = static_cast<size_t>(m.Lp) * m.kv_host_cap * m.kvb;
+        const size_t kv_e_al = (kv_e + 127) / 128 * 128;  // 256-byte aligned ACT pool
+        const size_t act_e = static_cast<size_t>(m.Lp) * m.act_cap_n * m.actb;
+        const size_t need = kv_e_al + act_e;
+        if (need > m.h_arena_elems) {
+            if (m.h_arena) HC_CUDA(cudaFreeHost(m.h_arena));
+            m.h_arena = halloc<bf16>(need, true);
+            m.h_arena_elems = need;
+        }
+        m.kv_host = kv_e ? m.h_arena : nullptr;
+        m.act_host = act_e ? m.h_arena + kv_e_al : nullptr;
+    }
     for (int s = 0; s < 2; ++s) {
         m.kv_stage[s] = dalloc<bf16>(static_cast<size_t>(m.kv_host_cap) * m.kvb);
         m.act_stage[s] = dalloc<bf16>(static_cast<size_t>(m.tpn) * m.act_cap_n * m.actb);
@@ -630,7 +642,7 @@ Engine::~Engine() {
                     (void*)m.tr_kv, (void*)m.splitk_ws, (void*)m.lnf, (void*)m.xn, (void*)m.pxn, (void*)m.red})
         if (p) cudaFree(p);
     for (auto& g : m.graphs) cudaGraphExecDestroy(g.second.exec);
-    for (void* p : {(void*)m.h_w, (void*)m.kv_host, (void*)m.act_host, (void*)m.h_meta, (void*)m.h_x,
+    for (void* p : {(void*)m.h_w, (void*)m.h_arena, (void*)m.h_meta, (void*)m.h_x,
                     (void*)m.h_logits, (void*)m.h_amax})
         if (p) cudaFreeHost(p);
     for (int i = 0; i < 2; ++i) {
