@@ -1106,205 +1106,205 @@ void Engine::decode_step(const std::vector<std::string>& ids, const int* tokens,
     m.spans.clear();
     const bool stream_any = !m.w_all || !kv_runs.empty() || !act_runs.empty() || gather_act;
     // everything the step puts on the streams; outputs land in xo / lo / ao
-  auto enqueue = [&](StepStats& st, uint16_t* xo, float* lo, int* ao) {
-    HC_CUDA(cudaEventRecord(m.ev0, s_compute_));
-    HC_CUDA(cudaMemcpyAsync(m.d_meta, m.h_meta, meta.size() * 4, cudaMemcpyHostToDevice, s_compute_));
-    embed(m.emb, m.pos, dm + o_tok, dm + o_pos, n, m.d, m.x[0], m.d, s_compute_);
-    st.launches += 1;
-    if (n_rc) {
-        embed(m.emb, m.pos, dm + o_rtok, dm + o_rpos, n_rc, m.d, m.px[0], m.d, s_compute_);
+    auto enqueue = [&](StepStats& st, uint16_t* xo, float* lo, int* ao) {
+        HC_CUDA(cudaEventRecord(m.ev0, s_compute_));
+        HC_CUDA(cudaMemcpyAsync(m.d_meta, m.h_meta, meta.size() * 4, cudaMemcpyHostToDevice, s_compute_));
+        embed(m.emb, m.pos, dm + o_tok, dm + o_pos, n, m.d, m.x[0], m.d, s_compute_);
         st.launches += 1;
-    }
-    if (capture_inputs_) captured_.assign(static_cast<size_t>(m.L) * n * m.d, 0);
-    const float scale = opt_.scaled ? 1.0f / std::sqrt(static_cast<float>(m.hd)) : 1.0f;
-
-    for (int l = 0; l < m.L; ++l) {
-        const int slot = l & 1;
-        m.cur_layer = l;
-        if (stream_any) {
-            // copy stream: weights + this layer's host blocks into slot l%2,
-            // after compute released the slot (layer l-2; the previous step,
-            // fully synchronised, for the first two layers — so a captured
-            // graph only waits on events it records itself)
-            HC_CUDA(cudaStreamWaitEvent(s_copy_, l >= 2 ? m.consumed[slot] : m.ev0));
-            m.span_begin(profile_, s_copy_, 3);
-            if (!m.w_all) {
-                HC_CUDA(cudaMemcpyAsync(m.wbuf[slot], m.h_w + static_cast<size_t>(l % m.Lw) * m.LE, m.LE * 2,
-                                        cudaMemcpyHostToDevice, s_copy_));
-                st.h2d_bytes += m.LE * 2.0;
-            }
-            const size_t lp = static_cast<size_t>(l % m.Lp);
-            bf16* own = m.act_stage[slot] + static_cast<size_t>(m.tpr) * m.act_cap_n * m.actb;
-            for (const Run& r : act_runs) {
-                const size_t bytes = static_cast<size_t>(r.count) * m.actb * 2;
-                HC_CUDA(cudaMemcpyAsync(own + static_cast<size_t>(r.start) * m.actb,
-                                        m.act_host + (lp * m.act_cap_n + r.start) * m.actb, bytes,
-                                        cudaMemcpyHostToDevice, s_copy_));
-                st.h2d_bytes += bytes;
-            }
-            // every rank streamed its 1/tpn of the ACT blocks; an NVLink all-gather
-            // on the gather stream completes the staging (the recompute needs all
-            // of X for its heads) while the copy stream moves on to the KV blocks
-            // and the next layer
-            if (gather_act) {
-                HC_CUDA(cudaEventRecord(m.h2d_act[slot], s_copy_));
-                HC_CUDA(cudaStreamWaitEvent(s_gather_, m.h2d_act[slot]));
-                m.tp->copy_channel()->all_gather(own, m.act_stage[slot], m.act_cap_n * m.actb, s_gather_);
-                HC_CUDA(cudaEventRecord(m.gathered[slot], s_gather_));
-                HC_CUDA(cudaStreamWaitEvent(s_compute_, m.gathered[slot]));
-            }
-            for (const Run& r : kv_runs) {
-                const size_t bytes = static_cast<size_t>(r.count) * m.kvb * 2;
-                HC_CUDA(cudaMemcpyAsync(m.kv_stage[slot] + static_cast<size_t>(r.start) * m.kvb,
-                                        m.kv_host + (lp * m.kv_host_cap + r.start) * m.kvb, bytes,
-                                        cudaMemcpyHostToDevice, s_copy_));
-                st.h2d_bytes += bytes;
-            }
-            m.span_end(profile_, s_copy_);
-            HC_CUDA(cudaEventRecord(m.loaded[slot], s_copy_));
-            HC_CUDA(cudaStreamWaitEvent(s_compute_, m.loaded[slot]));
-        }
-        const bf16* W = m.layer_w(l, slot);
-        bf16* R[16];
-        m.regions(l, slot, R);
-        bf16* xin = m.x[l & 1];
-        bf16* xout = m.x[(l + 1) & 1];
         if (n_rc) {
-            // token recompute: full layer l over every prefix (FullLayer(rc) FLOPs,
-            // flops.cpp:20-22), its K|V written into the prefix blocks
-            m.span_begin(profile_, s_compute_, 0);
-            bf16* pin = m.px[l & 1];
-            bf16* pout = m.px[(l + 1) & 1];
-            m.qkv(W, m.ln(W, 1, pin, n_rc, m.pxn, s_compute_), n_rc, m.pqkv, s_compute_);
-            st.launches += m.opt();
-            BlockScatter sk;
-            sk.src = m.pqkv;
-            sk.ld = 3 * m.d;
-            sk.src_row = dm + o_trs;
-            sk.n_tok = dm + o_trn;
-            sk.dst_ref = dm + o_trr;
-            std::copy(R, R + 16, sk.region);
-            sk.n_blocks = static_cast<int>(tr_src.size());
-            sk.d = m.d;
-            sk.H = m.H;
-            sk.hd = m.hd;
-            sk.tpb = m.tpb;
-            scatter_kv_blocks(sk, s_compute_);
-            if (l + 1 < m.L) {  // the last layer's prefix output is never needed
-                prefill_attention(m.pqkv, m.patt, dm + o_rcu, n, rc_max, m.H, m.hd, scale, s_compute_, n_rc);
-                m.tail(W, m.patt, pin, n_rc, m.pproj, m.patt, m.ph, pout, s_compute_);
-                st.launches += 1 + m.tail_launches();
+            embed(m.emb, m.pos, dm + o_rtok, dm + o_rpos, n_rc, m.d, m.px[0], m.d, s_compute_);
+            st.launches += 1;
+        }
+        if (capture_inputs_) captured_.assign(static_cast<size_t>(m.L) * n * m.d, 0);
+        const float scale = opt_.scaled ? 1.0f / std::sqrt(static_cast<float>(m.hd)) : 1.0f;
+
+        for (int l = 0; l < m.L; ++l) {
+            const int slot = l & 1;
+            m.cur_layer = l;
+            if (stream_any) {
+                // copy stream: weights + this layer's host blocks into slot l%2,
+                // after compute released the slot (layer l-2; the previous step,
+                // fully synchronised, for the first two layers — so a captured
+                // graph only waits on events it records itself)
+                HC_CUDA(cudaStreamWaitEvent(s_copy_, l >= 2 ? m.consumed[slot] : m.ev0));
+                m.span_begin(profile_, s_copy_, 3);
+                if (!m.w_all) {
+                    HC_CUDA(cudaMemcpyAsync(m.wbuf[slot], m.h_w + static_cast<size_t>(l % m.Lw) * m.LE, m.LE * 2,
+                                            cudaMemcpyHostToDevice, s_copy_));
+                    st.h2d_bytes += m.LE * 2.0;
+                }
+                const size_t lp = static_cast<size_t>(l % m.Lp);
+                bf16* own = m.act_stage[slot] + static_cast<size_t>(m.tpr) * m.act_cap_n * m.actb;
+                for (const Run& r : act_runs) {
+                    const size_t bytes = static_cast<size_t>(r.count) * m.actb * 2;
+                    HC_CUDA(cudaMemcpyAsync(own + static_cast<size_t>(r.start) * m.actb,
+                                            m.act_host + (lp * m.act_cap_n + r.start) * m.actb, bytes,
+                                            cudaMemcpyHostToDevice, s_copy_));
+                    st.h2d_bytes += bytes;
+                }
+                // every rank streamed its 1/tpn of the ACT blocks; an NVLink all-gather
+                // on the gather stream completes the staging (the recompute needs all
+                // of X for its heads) while the copy stream moves on to the KV blocks
+                // and the next layer
+                if (gather_act) {
+                    HC_CUDA(cudaEventRecord(m.h2d_act[slot], s_copy_));
+                    HC_CUDA(cudaStreamWaitEvent(s_gather_, m.h2d_act[slot]));
+                    m.tp->copy_channel()->all_gather(own, m.act_stage[slot], m.act_cap_n * m.actb, s_gather_);
+                    HC_CUDA(cudaEventRecord(m.gathered[slot], s_gather_));
+                    HC_CUDA(cudaStreamWaitEvent(s_compute_, m.gathered[slot]));
+                }
+                for (const Run& r : kv_runs) {
+                    const size_t bytes = static_cast<size_t>(r.count) * m.kvb * 2;
+                    HC_CUDA(cudaMemcpyAsync(m.kv_stage[slot] + static_cast<size_t>(r.start) * m.kvb,
+                                            m.kv_host + (lp * m.kv_host_cap + r.start) * m.kvb, bytes,
+                                            cudaMemcpyHostToDevice, s_copy_));
+                    st.h2d_bytes += bytes;
+                }
+                m.span_end(profile_, s_copy_);
+                HC_CUDA(cudaEventRecord(m.loaded[slot], s_copy_));
+                HC_CUDA(cudaStreamWaitEvent(s_compute_, m.loaded[slot]));
             }
-            st.launches += 2;
-            st.recompute_tokens += n_rc;
+            const bf16* W = m.layer_w(l, slot);
+            bf16* R[16];
+            m.regions(l, slot, R);
+            bf16* xin = m.x[l & 1];
+            bf16* xout = m.x[(l + 1) & 1];
+            if (n_rc) {
+                // token recompute: full layer l over every prefix (FullLayer(rc) FLOPs,
+                // flops.cpp:20-22), its K|V written into the prefix blocks
+                m.span_begin(profile_, s_compute_, 0);
+                bf16* pin = m.px[l & 1];
+                bf16* pout = m.px[(l + 1) & 1];
+                m.qkv(W, m.ln(W, 1, pin, n_rc, m.pxn, s_compute_), n_rc, m.pqkv, s_compute_);
+                st.launches += m.opt();
+                BlockScatter sk;
+                sk.src = m.pqkv;
+                sk.ld = 3 * m.d;
+                sk.src_row = dm + o_trs;
+                sk.n_tok = dm + o_trn;
+                sk.dst_ref = dm + o_trr;
+                std::copy(R, R + 16, sk.region);
+                sk.n_blocks = static_cast<int>(tr_src.size());
+                sk.d = m.d;
+                sk.H = m.H;
+                sk.hd = m.hd;
+                sk.tpb = m.tpb;
+                scatter_kv_blocks(sk, s_compute_);
+                if (l + 1 < m.L) {  // the last layer's prefix output is never needed
+                    prefill_attention(m.pqkv, m.patt, dm + o_rcu, n, rc_max, m.H, m.hd, scale, s_compute_, n_rc);
+                    m.tail(W, m.patt, pin, n_rc, m.pproj, m.patt, m.ph, pout, s_compute_);
+                    st.launches += 1 + m.tail_launches();
+                }
+                st.launches += 2;
+                st.recompute_tokens += n_rc;
+                m.span_end(profile_, s_compute_);
+            }
+            if (capture_inputs_)
+                HC_CUDA(cudaMemcpyAsync(captured_.data() + static_cast<size_t>(l) * n * m.d, xin,
+                                        static_cast<size_t>(n) * m.d * 2, cudaMemcpyDeviceToHost, s_compute_));
+            // the layer's GEMM input (and ACT payload): x, or LN1(x) for kArchOpt
+            const bf16* xa = m.ln(W, 1, xin, n, m.xn, s_compute_);
+            st.launches += m.opt();
+            AppendCall ap;
+            std::copy(R, R + 16, ap.region);
+            ap.B = n;
+            ap.d = m.d;  // ACT rows are full width; K|V slots below are this rank's heads
+            ap.H = m.H;
+            ap.hd = m.hd;
+            ap.tpb = m.tpb;
+            ap.tok = dm + o_t;
+            if (any_act) {  // ACT writer: X of the new token -> its ACT slot (device + host)
+                ap.src = xa;
+                ap.ld = m.d;
+                ap.dev_ref = dm + o_ad;
+                ap.host_ref = dm + o_ah;
+                act_append(ap, s_compute_);
+                st.launches += 1;
+                st.d2h_bytes += 0;  // counted below from the slot lists
+            }
+            // recompute K|V of every ACT block (streamed and resident) into R_KVR
+            for (int which = 0; which < 2; ++which) {
+                const std::vector<int>& tl = which == 0 ? tiles_h : tiles_g;
+                if (tl.empty()) continue;
+                GemmCall c;
+                c.epi = gemm::kKvPaged;
+                c.A = which == 0 ? m.act_stage[slot] : R[R_ACT_GPU];
+                c.lda = m.d;
+                c.a_rows = static_cast<int>((which == 0 ? m.tpn * m.act_cap_n : m.act_gpu_cap) * m.tpb);
+                c.B = W + m.off.wqkv + static_cast<size_t>(m.dg) * m.d;  // rows dg..3dg of Wqkv^T = [Wk|Wv]^T (own heads)
+                c.ldb = m.d;
+                c.M = c.a_rows;
+                c.N = 2 * m.dg;
+                c.K = m.d;
+                c.m_tile_rows = dm + (which == 0 ? o_th : o_tg);
+                c.num_m_tiles = static_cast<int>(tl.size());
+                c.out = m.kvr;
+                c.tpb = m.tpb;
+                c.d = m.dg;
+                c.hd = m.hd;
+                c.blk_off = which == 0 ? static_cast<int>(m.act_gpu_cap) : 0;
+                c.bias = m.bias(W, m.off.bqkv + m.dg);  // [b_k | b_v] of the own heads
+                m.span_begin(profile_, s_compute_, 0);
+                run_gemm(c, s_compute_);
+                m.span_end(profile_, s_compute_);
+                st.launches += 1;
+                st.recompute_tokens += static_cast<double>(tl.size()) * gemm::BM;
+            }
+            m.span_begin(profile_, s_compute_, 2);
+            m.qkv(W, xa, n, m.qkvb, s_compute_, m.splitk_ws, m.splitk_floats);
             m.span_end(profile_, s_compute_);
+            if (any_kv) {  // new token's K|V -> its KV slot (device + host)
+                ap.src = m.qkvb;
+                ap.ld = 3 * m.dg;
+                ap.d = m.dg;
+                ap.H = m.Hg;
+                ap.dev_ref = dm + o_kd;
+                ap.host_ref = dm + o_kh;
+                kv_append(ap, s_compute_);
+                st.launches += 1;
+            }
+            AttnCall a;
+            a.q = m.qkvb;
+            a.ldq = 3 * m.dg;
+            a.out = m.att;
+            a.blk_ref = dm + o_ref;
+            a.n_blocks = dm + o_nb;
+            a.ctx_len = dm + o_ctx;
+            a.max_blocks = m.max_blocks;
+            for (int i = 0; i < 16; ++i) a.region[i] = R[i];
+            a.B = n;
+            a.H = m.Hg;
+            a.hd = m.hd;
+            a.tpb = m.tpb;
+            a.scale = scale;
+            a.work = m.attn_work;
+            a.splits = splits;
+            m.span_begin(profile_, s_compute_, 1);
+            decode_attention(a, s_compute_);
+            m.span_end(profile_, s_compute_);
+            m.span_begin(profile_, s_compute_, 2);
+            m.tail(W, m.att, xin, n, m.proj, m.att, m.hbuf, xout, s_compute_, m.splitk_ws, m.splitk_floats);
+            m.span_end(profile_, s_compute_);
+            st.launches += 1 + m.tail_launches() + (splits > 1 ? 2 : 1);
+            HC_CUDA(cudaEventRecord(m.consumed[slot], s_compute_));
         }
-        if (capture_inputs_)
-            HC_CUDA(cudaMemcpyAsync(captured_.data() + static_cast<size_t>(l) * n * m.d, xin,
-                                    static_cast<size_t>(n) * m.d * 2, cudaMemcpyDeviceToHost, s_compute_));
-        // the layer's GEMM input (and ACT payload): x, or LN1(x) for kArchOpt
-        const bf16* xa = m.ln(W, 1, xin, n, m.xn, s_compute_);
+        const bf16* xf = m.final_norm(m.x[m.L & 1], n, m.xn, s_compute_);
         st.launches += m.opt();
-        AppendCall ap;
-        std::copy(R, R + 16, ap.region);
-        ap.B = n;
-        ap.d = m.d;  // ACT rows are full width; K|V slots below are this rank's heads
-        ap.H = m.H;
-        ap.hd = m.hd;
-        ap.tpb = m.tpb;
-        ap.tok = dm + o_t;
-        if (any_act) {  // ACT writer: X of the new token -> its ACT slot (device + host)
-            ap.src = xa;
-            ap.ld = m.d;
-            ap.dev_ref = dm + o_ad;
-            ap.host_ref = dm + o_ah;
-            act_append(ap, s_compute_);
+        if (lo || ao) {
+            gemm_rows(gemm::kF32, xf, n, m.d, m.emb, m.V, m.logits, m.V, s_compute_);
             st.launches += 1;
-            st.d2h_bytes += 0;  // counted below from the slot lists
+            if (ao) {
+                argmax_rows(m.logits, n, m.V, m.amax, s_compute_);
+                st.launches += 1;
+            }
         }
-        // recompute K|V of every ACT block (streamed and resident) into R_KVR
-        for (int which = 0; which < 2; ++which) {
-            const std::vector<int>& tl = which == 0 ? tiles_h : tiles_g;
-            if (tl.empty()) continue;
-            GemmCall c;
-            c.epi = gemm::kKvPaged;
-            c.A = which == 0 ? m.act_stage[slot] : R[R_ACT_GPU];
-            c.lda = m.d;
-            c.a_rows = static_cast<int>((which == 0 ? m.tpn * m.act_cap_n : m.act_gpu_cap) * m.tpb);
-            c.B = W + m.off.wqkv + static_cast<size_t>(m.dg) * m.d;  // rows dg..3dg of Wqkv^T = [Wk|Wv]^T (own heads)
-            c.ldb = m.d;
-            c.M = c.a_rows;
-            c.N = 2 * m.dg;
-            c.K = m.d;
-            c.m_tile_rows = dm + (which == 0 ? o_th : o_tg);
-            c.num_m_tiles = static_cast<int>(tl.size());
-            c.out = m.kvr;
-            c.tpb = m.tpb;
-            c.d = m.dg;
-            c.hd = m.hd;
-            c.blk_off = which == 0 ? static_cast<int>(m.act_gpu_cap) : 0;
-            c.bias = m.bias(W, m.off.bqkv + m.dg);  // [b_k | b_v] of the own heads
-            m.span_begin(profile_, s_compute_, 0);
-            run_gemm(c, s_compute_);
-            m.span_end(profile_, s_compute_);
-            st.launches += 1;
-            st.recompute_tokens += static_cast<double>(tl.size()) * gemm::BM;
-        }
-        m.span_begin(profile_, s_compute_, 2);
-        m.qkv(W, xa, n, m.qkvb, s_compute_, m.splitk_ws, m.splitk_floats);
-        m.span_end(profile_, s_compute_);
-        if (any_kv) {  // new token's K|V -> its KV slot (device + host)
-            ap.src = m.qkvb;
-            ap.ld = 3 * m.dg;
-            ap.d = m.dg;
-            ap.H = m.Hg;
-            ap.dev_ref = dm + o_kd;
-            ap.host_ref = dm + o_kh;
-            kv_append(ap, s_compute_);
-            st.launches += 1;
-        }
-        AttnCall a;
-        a.q = m.qkvb;
-        a.ldq = 3 * m.dg;
-        a.out = m.att;
-        a.blk_ref = dm + o_ref;
-        a.n_blocks = dm + o_nb;
-        a.ctx_len = dm + o_ctx;
-        a.max_blocks = m.max_blocks;
-        for (int i = 0; i < 16; ++i) a.region[i] = R[i];
-        a.B = n;
-        a.H = m.Hg;
-        a.hd = m.hd;
-        a.tpb = m.tpb;
-        a.scale = scale;
-        a.work = m.attn_work;
-        a.splits = splits;
-        m.span_begin(profile_, s_compute_, 1);
-        decode_attention(a, s_compute_);
-        m.span_end(profile_, s_compute_);
-        m.span_begin(profile_, s_compute_, 2);
-        m.tail(W, m.att, xin, n, m.proj, m.att, m.hbuf, xout, s_compute_, m.splitk_ws, m.splitk_floats);
-        m.span_end(profile_, s_compute_);
-        st.launches += 1 + m.tail_launches() + (splits > 1 ? 2 : 1);
-        HC_CUDA(cudaEventRecord(m.consumed[slot], s_compute_));
-    }
-    const bf16* xf = m.final_norm(m.x[m.L & 1], n, m.xn, s_compute_);
-    st.launches += m.opt();
-    if (lo || ao) {
-        gemm_rows(gemm::kF32, xf, n, m.d, m.emb, m.V, m.logits, m.V, s_compute_);
-        st.launches += 1;
-        if (ao) {
-            argmax_rows(m.logits, n, m.V, m.amax, s_compute_);
-            st.launches += 1;
-        }
-    }
-    HC_CUDA(cudaEventRecord(m.ev1, s_compute_));
-    HC_CUDA(cudaGetLastError());
-    if (xo) HC_CUDA(cudaMemcpyAsync(xo, xf, static_cast<size_t>(n) * m.d * 2, cudaMemcpyDeviceToHost, s_compute_));
-    if (lo)
-        HC_CUDA(cudaMemcpyAsync(lo, m.logits, static_cast<size_t>(n) * m.V * 4, cudaMemcpyDeviceToHost, s_compute_));
-    if (ao) HC_CUDA(cudaMemcpyAsync(ao, m.amax, static_cast<size_t>(n) * 4, cudaMemcpyDeviceToHost, s_compute_));
-  };
+        HC_CUDA(cudaEventRecord(m.ev1, s_compute_));
+        HC_CUDA(cudaGetLastError());
+        if (xo) HC_CUDA(cudaMemcpyAsync(xo, xf, static_cast<size_t>(n) * m.d * 2, cudaMemcpyDeviceToHost, s_compute_));
+        if (lo)
+            HC_CUDA(cudaMemcpyAsync(lo, m.logits, static_cast<size_t>(n) * m.V * 4, cudaMemcpyDeviceToHost, s_compute_));
+        if (ao) HC_CUDA(cudaMemcpyAsync(ao, m.amax, static_cast<size_t>(n) * 4, cudaMemcpyDeviceToHost, s_compute_));
+    };
 
     // CUDA graph of the step: its launch structure (sizes, copy runs, splits,
     // outputs) is the key; the data rides in the metadata block
