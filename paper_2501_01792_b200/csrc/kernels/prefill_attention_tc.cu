@@ -17,7 +17,8 @@
 //               a 128B-swizzled K-major smem tile for the P.V MMA; finally
 //               O / l from TMEM to HBM.
 // TMEM: S0 | S1 | O = 384 of 512 columns. smem: Q 32 KB, 2 x (K 32 + V 32) KB,
-// P 32 KB = 192 KB -> one CTA per SM. Heavy (late) query tiles launch first.
+// 2 x P 32 KB = 224 KB -> one CTA per SM; with two P buffers the softmax of
+// tile j writes P while P.V(j-1) still runs. Heavy (late) query tiles first.
 #include <cuda.h>
 
 #include <cfloat>
@@ -45,8 +46,8 @@ struct Smem {
     static constexpr int q = 0;
     static constexpr int k = kTile;                       // stage s at k + s * 2 * kTile
     static constexpr int v = 2 * kTile;                   // stage s at v + s * 2 * kTile
-    static constexpr int p = (1 + 2 * kStages) * kTile;
-    static constexpr int bars = p + kTile;
+    static constexpr int p = (1 + 2 * kStages) * kTile;    // P buffer b at p + b * kTile
+    static constexpr int bars = p + 2 * kTile;
     static constexpr int bytes = bars + 256 + 1024;       // + barrier block + 1 KB alignment slack
 };
 
@@ -59,6 +60,15 @@ __device__ __forceinline__ void tmem_st_x16(uint32_t taddr, const uint32_t (&r)[
         : "memory");
 }
 __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+// exp2 on the MUFU (ex2.approx.ftz; arguments are <= 8 by the lazy correction, masked ones -> 0)
+__device__ __forceinline__ float ex2(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ void sts128(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
+}
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
 // MN-major, 128B-swizzled operand (V: rows = K (keys), 64 N (hd) per 128 B row):
@@ -84,9 +94,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t* kv_empty = bars + 3;     // [kStages]
     uint64_t* s_full = bars + 5;       // [2]
     uint64_t* s_free = bars + 7;       // [2]
-    uint64_t* p_full = bars + 9;
-    uint64_t* pv_done = bars + 10;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
+    uint64_t* p_full = bars + 9;       // [2] (per P buffer)
+    uint64_t* pv_done = bars + 11;     // [2] (per P buffer)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 14);
 
     const int req = blockIdx.z, h = blockIdx.y;
     const int row0 = cu[req];
@@ -110,8 +120,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             ptx::mbar_init(&s_full[b], 1);
             ptx::mbar_init(&s_free[b], 128);
         }
-        ptx::mbar_init(p_full, 128);
-        ptx::mbar_init(pv_done, 1);
+        for (int b = 0; b < 2; ++b) {
+            ptx::mbar_init(&p_full[b], 128);
+            ptx::mbar_init(&pv_done[b], 1);
+        }
         ptx::fence_mbar_init();
     }
     if (warp == 1) ptx::tmem_alloc<512>(tmem_slot);
@@ -165,17 +177,19 @@ __global__ void __launch_bounds__(kThreads, 1)
             issue_s(0);
             for (int j = 0; j < n_kt; ++j) {
                 if (j + 1 < n_kt) issue_s(j + 1);
-                ptx::mbar_wait(p_full, j & 1);
+                const int pb = j & 1;
+                ptx::mbar_wait(&p_full[pb], (j / 2) & 1);
                 ptx::tc_fence_after();
                 const int s = j % kStages;
                 const uint32_t vb = ptx::smem_u32(smem + Smem::v + s * 2 * kTile);
+                const uint32_t pbuf = pa + pb * kTile;
 #pragma unroll
                 for (int k = 0; k < kT / 16; ++k) {  // keys: P in two 64-wide boxes; V rows 16 per step
-                    const uint64_t a = ptx::sw128_kmajor_desc(pa + (k / 4) * kBox) + 2 * (k % 4);
+                    const uint64_t a = ptx::sw128_kmajor_desc(pbuf + (k / 4) * kBox) + 2 * (k % 4);
                     const uint64_t bdesc = sw128_mnmajor_desc(vb + k * 16 * 128, v_lbo, v_sbo);
                     ptx::mma_bf16_ss(t_o, a, bdesc, id_o, (j > 0 || k > 0) ? 1u : 0u);
                 }
-                ptx::mma_commit(pv_done);
+                ptx::mma_commit(&pv_done[pb]);
                 ptx::mma_commit(&kv_empty[s]);
             }
         }
@@ -186,47 +200,63 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
         const float sl = scale * kLog2e;
         float m = -FLT_MAX, l = 0.f;
-        uint8_t* prow = smem + Smem::p;
+        const uint32_t prow = ptx::smem_u32(smem + Smem::p);
         for (int j = 0; j < n_kt; ++j) {
             const int b = j & 1;
             ptx::mbar_wait(&s_full[b], (j / 2) & 1);
             ptx::tc_fence_after();
-            float sv[kT];
+            // the whole S row in one batch of TMEM loads, one wait
+            uint32_t sraw[kT];
 #pragma unroll
-            for (int c = 0; c < kT; c += 16) {
-                uint32_t v[16];
-                ptx::tmem_ld_x16(t_s(b) + lane_off + c, v);
-                ptx::tmem_ld_wait();
-#pragma unroll
-                for (int i = 0; i < 16; ++i) sv[c + i] = __uint_as_float(v[i]);
-            }
+            for (int c = 0; c < kT; c += 16)
+                ptx::tmem_ld_x16(t_s(b) + lane_off + c, *reinterpret_cast<uint32_t(*)[16]>(&sraw[c]));
+            ptx::tmem_ld_wait();
             ptx::tc_fence_before();
             ptx::mbar_arrive(&s_free[b]);
             const int k0 = j * kT;
             const bool diag = j == n_kt - 1 || k0 + kT > P;
-            float mx = -FLT_MAX;
+            // 8 independent max / sum chains (a single chain is 128 dependent ops)
+            float mx8[8];
+#pragma unroll
+            for (int t = 0; t < 8; ++t) mx8[t] = -FLT_MAX;
 #pragma unroll
             for (int i = 0; i < kT; ++i) {
-                float x = sv[i] * sl;
+                float x = __uint_as_float(sraw[i]) * sl;
                 if (diag && (k0 + i > qrow || k0 + i >= P)) x = -FLT_MAX;
-                sv[i] = x;
-                mx = fmaxf(mx, x);
+                sraw[i] = __float_as_uint(x);
+                mx8[i % 8] = fmaxf(mx8[i % 8], x);
             }
+            const float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                                   fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
             // lazy correction: keep the reference max unless it grows by > 2^8
             float alpha = 1.f;
             bool rescale = false;
             if (mx > m + kRescale || j == 0) {
-                alpha = exp2f(m - mx);
+                alpha = ex2(m - mx);
                 rescale = j > 0;
                 m = mx;
                 l *= alpha;
             }
-            // the P buffer and O are free once the previous P.V has completed
-            if (j > 0) {
-                ptx::mbar_wait(pv_done, (j - 1) & 1);
+            // P = exp2(s - m) as packed bf16, computed while P.V(j-1) still runs
+            uint32_t pw[kT / 2];
+            float l8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+            for (int i = 0; i < kT / 2; ++i) {
+                const float p0 = ex2(__uint_as_float(sraw[2 * i]) - m), p1 = ex2(__uint_as_float(sraw[2 * i + 1]) - m);
+                l8[i % 8] += p0 + p1;
+                pw[i] = ptx::pack_bf16x2(p0, p1);
+            }
+            l += ((l8[0] + l8[1]) + (l8[2] + l8[3])) + ((l8[4] + l8[5]) + (l8[6] + l8[7]));
+            // P buffer j%2 is free once P.V(j-2) has completed; O may be
+            // rescaled only after P.V(j-1) (the rare lazy correction)
+            const int pb = j & 1;
+            if (j >= 2) {
+                ptx::mbar_wait(&pv_done[pb], ((j - 2) / 2) & 1);
                 ptx::tc_fence_after();
             }
             if (rescale) {
+                ptx::mbar_wait(&pv_done[pb ^ 1], ((j - 1) / 2) & 1);
+                ptx::tc_fence_after();
 #pragma unroll 1
                 for (int c = 0; c < kHD; c += 16) {
                     uint32_t v[16];
@@ -238,26 +268,19 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
                 tmem_st_wait();
             }
-            // P row -> two 64-key 128B-swizzled K-major boxes
+            // P row -> two 64-key 128B-swizzled K-major boxes of buffer pb
+            const uint32_t pbase = prow + pb * kTile + (r / 8) * 1024 + (r % 8) * 128;
 #pragma unroll
             for (int c = 0; c < kT / 8; ++c) {  // 16-byte chunks of 8 keys
-                uint32_t w[4];
-#pragma unroll
-                for (int t = 0; t < 4; ++t) {
-                    const float p0 = exp2f(sv[8 * c + 2 * t] - m), p1 = exp2f(sv[8 * c + 2 * t + 1] - m);
-                    l += p0 + p1;
-                    w[t] = ptx::pack_bf16x2(p0, p1);
-                }
                 const int box = c / 8, ch = c % 8;
-                uint8_t* dst = prow + box * kBox + (r / 8) * 1024 + (r % 8) * 128 + ((ch ^ (r % 8)) * 16);
-                *reinterpret_cast<uint4*>(dst) = make_uint4(w[0], w[1], w[2], w[3]);
+                sts128(pbase + box * kBox + ((ch ^ (r % 8)) * 16), pw[4 * c], pw[4 * c + 1], pw[4 * c + 2], pw[4 * c + 3]);
             }
             fence_async_smem();
             ptx::tc_fence_before();
-            ptx::mbar_arrive(p_full);
+            ptx::mbar_arrive(&p_full[pb]);
         }
         // O / l -> HBM
-        ptx::mbar_wait(pv_done, (n_kt - 1) & 1);
+        ptx::mbar_wait(&pv_done[(n_kt - 1) & 1], ((n_kt - 1) / 2) & 1);
         ptx::tc_fence_after();
         const float inv = l > 0.f ? 1.f / l : 0.f;
         bf16* orow = out + static_cast<long long>(row0 + qrow) * d + h * kHD;
