@@ -589,3 +589,33 @@ def test_engine_tp_nccl_group_of_one(native):
     x = f64(eng.decode_step(["n"], [5])["x"][0])
     assert rel(x, O.forward_prompt(prompt + [5], w).output[-1]) <= TOL
     eng.close()
+
+
+def test_engine_long_greedy_generation_matches_oracle(native):
+    """48 greedy steps for 3 requests of different lengths (hybrid host pools,
+    streamed weights, CUDA-graph replay across 6+ block boundaries): every
+    step's logits match the oracle and the greedy path is followed."""
+    from paper_2501_01792_b200.api import HostAllocation, PoolCaps
+    cfg = small_cfg(L=2, d=256, H=2, f=512, tpb=8)
+    w = oracle_weights(cfg, seed=13, max_seq=128)
+    rng = np.random.default_rng(51)
+    prompts = [rng.integers(0, cfg.vocab_size, n).tolist() for n in (9, 30, 17)]
+    ids = ["g0", "g1", "g2"]
+    eng = make_engine(cfg, w, max_batch=3, caps=PoolCaps(kv_host=40, act_host=40, act_gpu=3),
+                      allocation=HostAllocation(2, 3), weights_on_device=False)
+    eng.prefill(ids, prompts)
+    seqs = [list(p) for p in prompts]
+    toks = [int(rng.integers(0, cfg.vocab_size)) for _ in ids]
+    for step in range(48):
+        res = eng.decode_step(ids, toks, want_logits=True, want_argmax=True)
+        nxt = []
+        for b in range(3):
+            seqs[b].append(toks[b])
+            ref = O.logits_tied(O.forward_prompt(seqs[b], w).output[-1:], w)[0]
+            assert rel(res["logits"][b], ref) <= TOL, (step, b)
+            top2 = np.sort(ref)[-2:]
+            if top2[1] - top2[0] > 2e-2 * np.abs(ref).max():
+                assert int(res["argmax"][b]) == int(np.argmax(ref)), (step, b)
+            nxt.append(int(np.argmax(ref)))  # follow the oracle's greedy path
+        toks = nxt
+    assert [eng.cache.context_len(i) for i in ids] == [len(s) for s in seqs]
