@@ -107,6 +107,46 @@ def dist_setup(args):
     return world, rank, local, dist
 
 
+def parse_cpulist(text):
+    cpus = set()
+    for part in text.strip().split(","):
+        if not part:
+            continue
+        if "-" in part:
+            a, b = part.split("-")
+            cpus.update(range(int(a), int(b) + 1))
+        else:
+            cpus.add(int(part))
+    return cpus
+
+
+_ALL_CPUS = None  # affinity before bind_numa (restored for the CPU baseline)
+
+
+def bind_numa(local):
+    """Pin this rank to the CPUs of its GPU's NUMA node before any pinned host
+    allocation: cudaHostAlloc pages are placed by first touch, so each GPU's
+    host pools (and its DMA reads) stay on the socket its PCIe link hangs off —
+    with 8 ranks streaming ~55 GB/s each, cross-socket traffic would cap the
+    aggregate. Returns the node (or None when the topology is unknown)."""
+    from paper_2501_01792_b200 import kernels
+    try:
+        bus = kernels.device_pci_bus_id(local).lower()
+        with open(f"/sys/bus/pci/devices/{bus}/numa_node") as fh:
+            node = int(fh.read().strip())
+        if node < 0:
+            return None
+        with open(f"/sys/devices/system/node/node{node}/cpulist") as fh:
+            cpus = parse_cpulist(fh.read()) & os.sched_getaffinity(0)
+        if cpus:
+            global _ALL_CPUS
+            _ALL_CPUS = os.sched_getaffinity(0)
+            os.sched_setaffinity(0, cpus)
+        return node
+    except Exception:  # no sysfs / no GPU: leave placement to the OS
+        return None
+
+
 def barrier(dist):
     if dist is not None:
         dist.barrier()
@@ -521,6 +561,7 @@ def our_arm(args, cfg, world, rank, local, dist):
     if kernels.device_count() == 0:
         raise SystemExit("bench needs a CUDA device")
     hbm_peak, tflops_sust, tflops_burst, peak_src = measured_peaks()
+    numa_node = bind_numa(local)
     tp, tpn = tp_group(args, world, rank, local, dist)
     if tp is not None:  # heads are sharded, requests are not: every rank serves the global batch
         args.no_sweep = True
@@ -737,6 +778,8 @@ def our_arm(args, cfg, world, rank, local, dist):
     if rank == 0:
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
+            if _ALL_CPUS:  # the CPU reference gets every host core back
+                os.sched_setaffinity(0, _ALL_CPUS)
             threads = os.cpu_count() or 1
             kind, run, sample = cpu_reference_sample(cfg, P, r, threads)
             run()  # warm
@@ -759,6 +802,7 @@ def our_arm(args, cfg, world, rank, local, dist):
                                    f"host storage folded to {Lp} cache / {Lw} weight layer copies "
                                    "(box DRAM); bytes streamed per layer unchanged"),
                 "kv_host_blocks": caps.kv_host, "act_host_blocks": caps.act_host,
+                "numa_node": numa_node,
                 "act_context_tokens": act_tokens}),
             "e2e": {"value": e2e, "unit": "tokens/s", "h2d_bytes_per_step": h2d_step + B * 4,
                     "d2h_bytes_per_step": acc["d2h"] / args.steps + B * 4,

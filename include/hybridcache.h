@@ -28,6 +28,8 @@ extern "C" {
 const char* hc_last_error(void);
 int hc_abi_version(void);
 int hc_device_count(void);
+/* PCI bus id of a visible device (cudaDeviceGetPCIBusId), e.g. "0000:18:00.0". */
+int hc_device_pci_bus_id(int device, char* buf, int len);
 int hc_set_device(int device);
 
 /* --------------------------------------------------------- model config ---

@@ -35,6 +35,7 @@ SIGNATURES = {
     "hc_last_error": (cp, []),
     "hc_abi_version": (i, []),
     "hc_device_count": (i, []),
+    "hc_device_pci_bus_id": (i, [i, C.c_char_p, i]),
     "hc_set_device": (i, [i]),
     # model
     "hc_model_validate": (i, [cfgp]),

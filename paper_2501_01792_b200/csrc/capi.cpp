@@ -28,6 +28,12 @@ int hc_device_count(void) {
     return n;
 }
 
+// PCI bus id ("0000:18:00.0") of a visible device — for NUMA-local pinning
+// of the host pools (bench.py binds each rank to its GPU's NUMA node).
+int hc_device_pci_bus_id(int dev, char* buf, int len) {
+    return hc_guard([&] { HC_CUDA(cudaDeviceGetPCIBusId(buf, len, dev)); });
+}
+
 int hc_set_device(int dev) {
     return hc_guard([&] { HC_CUDA(cudaSetDevice(dev)); });
 }

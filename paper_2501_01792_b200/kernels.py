@@ -94,3 +94,9 @@ def prefill_attention(qkv_bits, n_req, P, heads, scaled=True):
 
 def device_count() -> int:
     return lib().hc_device_count()
+
+
+def device_pci_bus_id(device: int) -> str:
+    buf = C.create_string_buffer(64)
+    check(lib().hc_device_pci_bus_id(device, buf, 64))
+    return buf.value.decode()
