@@ -18,6 +18,7 @@
 //   ref_fit_linear         -> fit_linear                    timing.cpp:38-73
 //   ref_flop_count         -> flop_count                    flops.cpp:7-33
 //   ref_equivalence        -> run_equivalence_case          verify.cpp:26-95
+//   ref_simulate           -> simulate                      sim.cpp:134-633
 //
 // Status codes: 0 ok, 1 InputError, 2 CapacityError, 3 ConfigError, 4 other.
 #include <cstdint>
@@ -32,6 +33,7 @@
 #include "hybridsim/flops.hpp"
 #include "hybridsim/minibatch.hpp"
 #include "hybridsim/plan.hpp"
+#include "hybridsim/sim.hpp"
 #include "hybridsim/timing.hpp"
 #include "hybridsim/verify.hpp"
 
@@ -407,4 +409,39 @@ int ref_fit_linear(const double* n_tokens, const double* seconds, int count, dou
     });
 }
 
+
+// The reference's discrete-event simulator (sim.cpp:134-633) as the PREDICTOR
+// for a measured B200 bundle: uniform batch of `batch` requests (prompt, gen),
+// allocation counts double as pool capacities (sim.cpp:181), one mini-batch.
+// bundle5 = {kv slope, kv icept, load slope, load icept, t_load_w}; mode 0 hybrid,
+// 1 kv_only, 2 act_only, 3 token_recompute.
+// out6 = {throughput tok/s, makespan s, prefill s, gen s, pcie_busy, gpu_busy}
+int ref_simulate(int layers, int d, int heads, int ffn, int vocab, int tpb, const double* bundle5, long act_host,
+                 long kv_host, long act_gpu, int mode, double recompute_ratio, int batch, int prompt, int gen,
+                 int full_duplex, double* out6) {
+    return guarded([&] {
+        SimConfig cfg;
+        cfg.model.num_layers = layers;
+        cfg.model.hidden_dim = d;
+        cfg.model.num_heads = heads;
+        cfg.model.ffn_dim = ffn;
+        cfg.model.vocab_size = vocab;
+        cfg.model.tokens_per_block = tpb;
+        cfg.bundle = bundle_of(bundle5);
+        const WeightBytes wb = weight_bytes(cfg.model);
+        cfg.bundle.s_weight_layer = wb.per_layer;
+        cfg.bundle.s_weight_total = wb.total;
+        cfg.allocation.act_host = act_host;
+        cfg.allocation.kv_host = kv_host;
+        cfg.act_gpu = GpuResidency{act_gpu};
+        cfg.packer = PackerConfig{1L << 40, 1L << 40};
+        cfg.batch.assign(static_cast<std::size_t>(batch), RequestSpec{prompt, gen});
+        cfg.mode = static_cast<SimMode>(mode);
+        cfg.recompute_ratio = recompute_ratio;
+        cfg.full_duplex_pcie = full_duplex != 0;
+        const SimMetrics m = simulate(cfg).metrics;
+        const double v[6] = {m.throughput, m.makespan, m.prefill_seconds, m.gen_seconds, m.pcie_busy, m.gpu_busy};
+        std::memcpy(out6, v, sizeof v);
+    });
+}
 }  // extern "C"

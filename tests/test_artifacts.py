@@ -65,3 +65,29 @@ def test_trace_schema():
     assert all(e["end_us"] >= e["start_us"] for e in ev)
     layers = {e["layer"] for e in ev}
     assert len(layers) > 1
+
+
+def test_reference_simulator_as_predictor():
+    """The reference's simulate() (sim.cpp:134-633) runs on a B200-measured
+    bundle (scripts/sim_vs_measured.py does it at config-3 scale and commits
+    profiles/r01_sim_vs_measured.json); at toy scale its ordering matches the
+    B200 measurements: ACT-only < hybrid < KV-only step time on a fast GPU."""
+    import math
+    import sys
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "scripts"))
+    import sim_vs_measured as S
+    cfg = {"num_layers": 2, "hidden_dim": 256, "num_heads": 2, "ffn_dim": 1024, "vocab_size": 512}
+    bundle5 = [1.2e-10, 0.0, 5.2e-9, 0.0, 1.0e-4]   # recompute cheap, link slow (B200-like balance)
+    B, P, G = 8, 64, 16
+    nb = math.ceil((P + G) / 16)
+    steps = {}
+    for mode, r in (("kv_only", 0.0), ("hybrid", 0.5), ("act_only", 1.0)):
+        a = 0 if mode == "kv_only" else B * (math.ceil(r * nb) + 1)
+        k = 0 if mode == "act_only" else B * (math.ceil((1 - r) * nb) + 1)
+        steps[mode] = S.simulate(cfg, bundle5, a, k, mode, B, P, G)["gen_s"]
+    assert steps["act_only"] < steps["hybrid"] < steps["kv_only"]
+    j = json.load(open(os.path.join(os.path.dirname(ART), "r01_sim_vs_measured.json")))
+    planned = [r for r in j["rows"] if r["mode"] == "hybrid" and r["act_share_r"] > 0.9][0]
+    gen = j["generation_e2e_measured"]
+    measured_mean = (gen["step_ms_at_prompt"] + gen["step_ms_at_prompt_plus_gen"]) / 2
+    assert abs(planned["sim_mean_step_ms"] / measured_mean - 1) < 0.05
