@@ -99,8 +99,11 @@ def dist_setup(args):
     if world > 1:
         import torch
         import torch.distributed as td
-        backend = "nccl" if torch.cuda.is_available() else "gloo"
-        if backend == "nccl":
+        # HC_DIST_BACKEND=gloo + fewer GPUs than ranks: a plumbing smoke test of
+        # the multi-rank path with several ranks sharing one device
+        backend = os.environ.get("HC_DIST_BACKEND") or ("nccl" if torch.cuda.is_available() else "gloo")
+        if torch.cuda.is_available():
+            local = local % torch.cuda.device_count()
             torch.cuda.set_device(local)
         td.init_process_group(backend=backend)
         dist = td
