@@ -619,3 +619,33 @@ def test_engine_long_greedy_generation_matches_oracle(native):
             nxt.append(int(np.argmax(ref)))  # follow the oracle's greedy path
         toks = nxt
     assert [eng.cache.context_len(i) for i in ids] == [len(s) for s in seqs]
+
+
+def test_engine_hbm_resident_kv_and_act_matches_oracle(native):
+    """The HBM-resident layout of the bench's hbm_resident variant: KV and ACT
+    blocks placed on the GPU first (kv_on_gpu, cache.cpp:64-91) with a small
+    KV/host overflow, weights resident — decode outputs equal the oracle and
+    the block table equals the reference allocator's."""
+    from paper_2501_01792_b200.api import HostAllocation, PoolCaps
+    cfg = small_cfg(L=3, d=256, H=2, f=512, tpb=8)
+    w = oracle_weights(cfg)
+    rng = np.random.default_rng(61)
+    lens = [25, 40]
+    prompts = [rng.integers(0, cfg.vocab_size, n).tolist() for n in lens]
+    dec = [rng.integers(0, cfg.vocab_size, 4).tolist() for _ in prompts]
+    caps = PoolCaps(kv_host=3, kv_gpu=3, act_gpu=6)
+    eng, ids, got, want = run_case(cfg, w, prompts, dec, caps=caps, allocation=HostAllocation(1, 1), mode="hybrid",
+                                   kv_on_gpu=True)
+    check_outputs(got, want)
+    ba = O.BlockAssigner(cfg.tokens_per_block, O.HYBRID, O.HostAllocation(1, 1), act_gpu=6)
+    ba.cache = O.HybridCache(cfg.tokens_per_block, kv_host=3, kv_gpu=3, act_host=0, act_gpu=6, kv_on_gpu=True)
+    for i, n in enumerate(lens):
+        ba.add_request(ids[i], n)
+        for _ in range(n):
+            ba.add_token(ids[i])
+    for _ in range(4):
+        for i in range(len(lens)):
+            ba.add_token(ids[i])
+    assert eng.cache.dump_json() == O.dumps(ba.cache.dump_json())
+    locs = {(int(e.kind), int(e.location)) for rid in ids for e in eng.cache.table(rid).entries}
+    assert (0, 1) in locs and (1, 1) in locs  # KV/gpu and ACT/gpu blocks both used
