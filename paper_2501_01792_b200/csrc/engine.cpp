@@ -121,7 +121,9 @@ struct Engine::Impl {
     // prefill scratch
     bf16 *px[2] = {nullptr, nullptr}, *pqkv = nullptr, *patt = nullptr, *pproj = nullptr, *ph = nullptr;
     size_t prefill_rows = 0, prefill_chunk_rows = 0;
-    cudaEvent_t loaded[2]{}, consumed[2]{}, stored[2]{}, h2d_act[2]{}, gathered[2]{}, ev0{}, ev1{}, tg0{}, tg1{};
+    cudaEvent_t loaded[2]{}, consumed[2]{}, stored[2]{}, h2d_act[2]{}, gathered[2]{}, ev0{}, ev1{}, tg0{}, tg1{},
+        wpre{};
+    bool w_prefetched = false;  // wbuf[0/1] hold layers 0/1 for the next decode step
     bool pools_filled = false;
     bf16* tr_kv = nullptr;  // [max_batch * max_blocks] KV blocks for token-recompute prefixes
     void ensure_tr() {
@@ -455,6 +457,7 @@ void Engine::init(const ModelConfig& c, int w_max_seq, const uint16_t* emb, cons
     HC_CUDA(cudaEventCreate(&m.ev1));
     HC_CUDA(cudaEventCreate(&m.tg0));
     HC_CUDA(cudaEventCreate(&m.tg1));
+    HC_CUDA(cudaEventCreateWithFlags(&m.wpre, cudaEventDisableTiming));
 
     // tables
     m.emb = dalloc<bf16>(static_cast<size_t>(m.V) * m.d);
@@ -656,6 +659,7 @@ Engine::~Engine() {
     cudaEventDestroy(m.ev1);
     cudaEventDestroy(m.tg0);
     cudaEventDestroy(m.tg1);
+    cudaEventDestroy(m.wpre);
     for (cudaEvent_t e : m.pev) cudaEventDestroy(e);
     cudaStreamDestroy(s_compute_);
     cudaStreamDestroy(s_copy_);
@@ -669,6 +673,7 @@ void Engine::run_layers(int T, int l0, int l1, const int* d_cu, uint16_t* layer_
                         uint16_t* out, bool final_ln) {
     Impl& m = *impl_;
     if (m.tpn > 1) throw ConfigError("forward_trace / layer_forward run on an engine without tensor parallelism");
+    m.w_prefetched = false;
     const size_t per = static_cast<size_t>(T) * m.d;
     std::vector<uint16_t> qkv_h((k || v) ? static_cast<size_t>(T) * 3 * m.d : 0);
     for (int l = l0; l < l1; ++l) {
@@ -732,6 +737,7 @@ void gemm_rows(int epi, const bf16* A, int M, int K, const bf16* W, int N, void*
 void Engine::prefill(const std::vector<std::string>& ids, const std::vector<std::vector<int>>& prompts) {
     Impl& m = *impl_;
     HC_CUDA(cudaSetDevice(opt_.device));
+    m.w_prefetched = false;  // the prefill streams weights through the same slots
     if (ids.size() != prompts.size()) throw InputError("prefill: ids and prompts differ in length");
     {
         std::unordered_set<std::string> seen;
@@ -1105,6 +1111,10 @@ void Engine::decode_step(const std::vector<std::string>& ids, const int* tokens,
     m.pev_used = 0;
     m.spans.clear();
     const bool stream_any = !m.w_all || !kv_runs.empty() || !act_runs.empty() || gather_act;
+    // layers 0/1 weights already in their slots (prefetched at the end of the previous step)
+    const bool prefetched = m.w_prefetched && !m.w_all;
+    m.w_prefetched = false;
+    bool capturing = false;  // enqueue() runs under stream capture (graph mode)
     // everything the step puts on the streams; outputs land in xo / lo / ao
     auto enqueue = [&](StepStats& st, uint16_t* xo, float* lo, int* ao) {
         HC_CUDA(cudaEventRecord(m.ev0, s_compute_));
@@ -1128,7 +1138,7 @@ void Engine::decode_step(const std::vector<std::string>& ids, const int* tokens,
                 // graph only waits on events it records itself)
                 HC_CUDA(cudaStreamWaitEvent(s_copy_, l >= 2 ? m.consumed[slot] : m.ev0));
                 m.span_begin(profile_, s_copy_, 3);
-                if (!m.w_all) {
+                if (!m.w_all && !(prefetched && l < 2)) {  // layers 0/1 may have come with the previous step
                     HC_CUDA(cudaMemcpyAsync(m.wbuf[slot], m.h_w + static_cast<size_t>(l % m.Lw) * m.LE, m.LE * 2,
                                             cudaMemcpyHostToDevice, s_copy_));
                     st.h2d_bytes += m.LE * 2.0;
@@ -1286,7 +1296,10 @@ void Engine::decode_step(const std::vector<std::string>& ids, const int* tokens,
             m.tail(W, m.att, xin, n, m.proj, m.att, m.hbuf, xout, s_compute_, m.splitk_ws, m.splitk_floats);
             m.span_end(profile_, s_compute_);
             st.launches += 1 + m.tail_launches() + (splits > 1 ? 2 : 1);
-            HC_CUDA(cudaEventRecord(m.consumed[slot], s_compute_));
+            if (capturing && l >= m.L - 2)  // the weight prefetch waits on these from outside the graph
+                HC_CUDA(cudaEventRecordWithFlags(m.consumed[slot], s_compute_, cudaEventRecordExternal));
+            else
+                HC_CUDA(cudaEventRecord(m.consumed[slot], s_compute_));
         }
         const bf16* xf = m.final_norm(m.x[m.L & 1], n, m.xn, s_compute_);
         st.launches += m.opt();
@@ -1324,7 +1337,7 @@ void Engine::decode_step(const std::vector<std::string>& ids, const int* tokens,
                        static_cast<long>(tiles_g.size()), static_cast<long>(tr_src.size()), static_cast<long>(splits),
                        static_cast<long>(any_act), static_cast<long>(any_kv), static_cast<long>(stream_any),
                        static_cast<long>(x_out != nullptr), static_cast<long>(logits_out != nullptr),
-                       static_cast<long>(argmax_out != nullptr), m.graph_gen})
+                       static_cast<long>(argmax_out != nullptr), static_cast<long>(prefetched), m.graph_gen})
             add(v);
         for (const auto* runs : {&kv_runs, &act_runs}) {
             add(static_cast<long>(runs->size()));
@@ -1342,14 +1355,17 @@ void Engine::decode_step(const std::vector<std::string>& ids, const int* tokens,
             Impl::StepGraph sg;
             cudaGraph_t g = nullptr;
             HC_CUDA(cudaStreamBeginCapture(s_compute_, cudaStreamCaptureModeThreadLocal));
+            capturing = true;
             try {
                 enqueue(sg.stats, x_out ? m.h_x : nullptr, logits_out ? m.h_logits : nullptr,
                         argmax_out ? m.h_amax : nullptr);
             } catch (...) {
+                capturing = false;
                 cudaStreamEndCapture(s_compute_, &g);
                 if (g) cudaGraphDestroy(g);
                 throw;
             }
+            capturing = false;
             HC_CUDA(cudaStreamEndCapture(s_compute_, &g));
             const cudaError_t e = cudaGraphInstantiate(&sg.exec, g, 0);
             cudaGraphDestroy(g);
@@ -1362,8 +1378,22 @@ void Engine::decode_step(const std::vector<std::string>& ids, const int* tokens,
         // cannot be timed)
         HC_CUDA(cudaEventRecord(m.tg0, s_compute_));
         HC_CUDA(cudaGraphLaunch(it->second.exec, s_compute_));
-        HC_CUDA(cudaEventRecord(m.tg1, s_compute_));
     }
+    // next step's layer 0/1 weights (step-independent) over the link while the
+    // last two layers compute — the reference arms weight(step+1) before the
+    // step's tail too (sim.cpp:534-537); the step ends when they have landed
+    if (!m.w_all && stream_any) {
+        for (int l = 0; l < std::min(2, m.L); ++l) {
+            HC_CUDA(cudaStreamWaitEvent(s_copy_, m.consumed[l & 1]));
+            HC_CUDA(cudaMemcpyAsync(m.wbuf[l & 1], m.h_w + static_cast<size_t>(l % m.Lw) * m.LE, m.LE * 2,
+                                    cudaMemcpyHostToDevice, s_copy_));
+            st.h2d_bytes += m.LE * 2.0;
+        }
+        HC_CUDA(cudaEventRecord(m.wpre, s_copy_));
+        HC_CUDA(cudaStreamWaitEvent(s_compute_, m.wpre));
+        m.w_prefetched = true;
+    }
+    HC_CUDA(cudaEventRecord(use_graph ? m.tg1 : m.ev1, s_compute_));
     HC_CUDA(cudaStreamSynchronize(s_compute_));
     if (use_graph) {
         if (x_out) std::memcpy(x_out, m.h_x, static_cast<size_t>(n) * m.d * 2);
@@ -1471,6 +1501,7 @@ double Engine::time_kv_gen(int n_tokens, int reps) {
     const long cap_rows = std::max(stage_rows, m.act_gpu_cap * m.tpb);
     if (n_tokens > cap_rows) throw InputError("time_kv_gen: more tokens than the ACT pools hold");
     const bf16* A = stage_rows >= n_tokens ? m.act_stage[0] : m.act_gpu;
+    m.w_prefetched = false;  // wbuf[0] is reloaded with layer 0 below
     if (!m.w_all)
         HC_CUDA(cudaMemcpy(m.wbuf[0], m.h_w, m.LE * 2, cudaMemcpyHostToDevice));
     const bf16* W = m.layer_w(0, 0);
