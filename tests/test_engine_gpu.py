@@ -649,3 +649,27 @@ def test_engine_hbm_resident_kv_and_act_matches_oracle(native):
     assert eng.cache.dump_json() == O.dumps(ba.cache.dump_json())
     locs = {(int(e.kind), int(e.location)) for rid in ids for e in eng.cache.table(rid).entries}
     assert (0, 1) in locs and (1, 1) in locs  # KV/gpu and ACT/gpu blocks both used
+
+
+def test_engine_empty_prompt_and_partial_batches(native):
+    """Edge cases the reference allows: an empty prompt (embed of 0 tokens is
+    valid, decoder.cpp:83-95) and decode steps over changing subsets of the
+    admitted requests (batch composition changes between graph replays)."""
+    from paper_2501_01792_b200.api import HostAllocation, PoolCaps
+    cfg = small_cfg(L=2, d=256, H=2, f=512, tpb=8)
+    w = oracle_weights(cfg)
+    rng = np.random.default_rng(71)
+    prompts = {"e": [], "a": rng.integers(0, cfg.vocab_size, 13).tolist(), "b": rng.integers(0, cfg.vocab_size, 8).tolist()}
+    eng = make_engine(cfg, w, max_batch=3, caps=PoolCaps(kv_host=16, act_host=16, act_gpu=2),
+                      allocation=HostAllocation(1, 1))
+    eng.prefill(list(prompts), list(prompts.values()))
+    seqs = {k: list(v) for k, v in prompts.items()}
+    for step, batch in enumerate([["e", "a", "b"], ["a"], ["e", "b"], ["b", "a", "e"], ["e"]]):
+        toks = rng.integers(0, cfg.vocab_size, len(batch)).tolist()
+        res = eng.decode_step(batch, toks, want_x=True)
+        for i, rid in enumerate(batch):
+            seqs[rid].append(toks[i])
+            ref = O.forward_prompt(seqs[rid], w).output[-1]
+            assert rel(f64(res["x"][i]), ref) <= TOL, (step, rid)
+    for rid, s in seqs.items():
+        assert eng.cache.context_len(rid) == len(s)
