@@ -851,7 +851,7 @@ def our_arm(args, cfg, world, rank, local, dist):
     return res
 
 
-def resident_variants(local, cfg, B, P, arch, steps=2, warmup=1, reserve=6e9, only_planned=False):
+def resident_variants(local, cfg, B, P, arch, steps=2, warmup=1, reserve=3e9, only_planned=False):
     """The same workload with the weights AND the cache in HBM (B200 has 180 GB):
     KV and ACT blocks both placed on the GPU first (kv_on_gpu / ACT-first,
     cache.cpp:64-91). Pure KV does not fit, so its overflow blocks stream from
