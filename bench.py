@@ -858,9 +858,12 @@ def resident_variants(local, cfg, B, P, arch, steps=2, warmup=1, reserve=3e9, on
     pinned host memory; pure ACT fits but recomputes every context token each
     step. The capacity-constrained end of Alg. 1: with no
     link time left to hide recompute under, every KV block that fits saves
-    4 d^2 tpb FLOPs per layer per step, so the planned ACT share is the smallest
-    one whose blocks fit the free HBM (r_fit). Sweeps r = 0 (KV, overflow to
-    host), r_fit, (1 + r_fit)/2 and r = 1."""
+    4 d^2 tpb FLOPs per layer per step, so the capacity-only ACT share is the
+    smallest one whose blocks fit the free HBM (r_fit); the balanced plan also
+    streams KV blocks from pinned host while the tensor cores recompute (the
+    link is idle with resident weights), minimising max(t_kv_gen, t_load_kv)
+    per layer on rates measured here (r_planned). Sweeps r = 0 (KV, overflow to
+    host), r_planned, r_fit, (1 + r_fit)/2 and r = 1."""
     import torch
     from paper_2501_01792_b200 import api
     L, tpb = cfg.num_layers, cfg.tokens_per_block
@@ -872,17 +875,36 @@ def resident_variants(local, cfg, B, P, arch, steps=2, warmup=1, reserve=3e9, on
     kv_one = api.HybridCache.bytes_of("KV", cfg)  # recompute output buffer per ACT block (one layer)
     eng = api.Engine(cfg, seed=42, max_seq=P + total + 1, rescale=True, max_batch=B, weights_on_device=True,
                      caps=api.PoolCaps(), mode="act_only", device=local, arch=arch)
+    # measured rates on this engine (north-star (5)): recompute GEMM vs ACT
+    # tokens, host link vs KV tokens, through small calibration pools
+    eng.configure_cache(api.PoolCaps(kv_host=1024, act_host=4096), mode="hybrid", host_layers=1)
+    # (sustained rate: enough back-to-back launches for the power cap to settle, as in a step)
+    kv_s = [(float(n), eng.time_kv_gen(n, reps=40)) for n in (4096, 16384, 32768, 65536)]
+    ld_s = [(float(n), eng.time_load_kv(n, reps=2)) for n in (2048, 8192, 16384)]
+    link_bps = 16384 * 2 * cfg.hidden_dim * 2 / ld_s[-1][1]
+    bundle = api.bundle_from_samples(kv_s, ld_s, link_bps, cfg)
+    eng.configure_cache(api.PoolCaps(), mode="act_only")
     free = torch.cuda.mem_get_info(local)[0] - reserve
-    # the library's HBM-residency planner (csrc/host/plan.hpp: plan_hbm_residency)
+    # the library's HBM planners (csrc/host/plan.hpp): capacity-only (smallest
+    # ACT share that fits) and balanced three tiers (ACT + KV in HBM, KV from
+    # host, max(t_kv_gen, t_load_kv) minimised on the measured bundle)
     r_fit, caps_fit = api.plan_hbm_residency(cfg, B, nb, free)
+    r_bal, caps_bal, t_bal = api.plan_hbm_tiers(cfg, B, nb, free, bundle)
     ids = [f"h{i}" for i in range(B)]
     tokens = np.random.default_rng(9).integers(0, cfg.vocab_size, (total, B)).astype(np.int32)
     out = {"workload": f"{cfg.name}-shape, batch {B}, prompt {P}: weights + cache in HBM (KV and ACT placed on "
                        "the GPU first); overflow blocks in pinned host memory",
-           "free_hbm_gb": free / 1e9, "blocks": N, "r_fit": r_fit, "per_ratio": []}
-    for r in ([r_fit] if only_planned else sorted({0.0, r_fit, (1.0 + r_fit) / 2, 1.0})):
+           "free_hbm_gb": free / 1e9, "blocks": N, "r_fit": r_fit, "r_planned": r_bal,
+           "planned_tiers": {"act_gpu": caps_bal.act_gpu, "kv_gpu": caps_bal.kv_gpu, "kv_host": caps_bal.kv_host,
+                             "act_host": caps_bal.act_host, "predicted_t_comp_ms_per_layer": t_bal[0] * 1e3,
+                             "predicted_t_link_ms_per_layer": t_bal[1] * 1e3},
+           "bundle": {"kv_gen_slope": bundle.t_kv_gen.slope, "load_kv_slope": bundle.t_load_kv.slope},
+           "per_ratio": []}
+    for r in ([r_bal] if only_planned else sorted({0.0, r_fit, r_bal, (1.0 + r_fit) / 2, 1.0})):
         a = int(round(r * 1000))
-        if r == r_fit:
+        if r == r_bal:
+            caps = caps_bal
+        elif r == r_fit:
             caps = caps_fit
         else:  # the same capacity rule at a forced share
             act_cap = 0 if r <= 0 else (N if r >= 1 else B * (math.ceil(r * nb) + 1))
@@ -895,7 +917,9 @@ def resident_variants(local, cfg, B, P, arch, steps=2, warmup=1, reserve=3e9, on
         act_cap, kv_gpu = caps.act_gpu, caps.kv_gpu
         mode = "kv_only" if r <= 0 else ("act_only" if r >= 1 else "hybrid")
         try:
-            eng.configure_cache(caps, mode=mode, allocation=api.HostAllocation(a, 1000 - a), kv_on_gpu=True)
+            alloc = (api.HostAllocation(caps_bal.act_gpu, N - caps_bal.act_gpu) if r == r_bal
+                     else api.HostAllocation(a, 1000 - a))
+            eng.configure_cache(caps, mode=mode, allocation=alloc, kv_on_gpu=True)
             eng.admit_synthetic(ids, [P] * B, seed=11)
             run_steps(eng, ids, tokens, 0, warmup)
             acc = run_steps(eng, ids, tokens, warmup, steps)
@@ -910,7 +934,7 @@ def resident_variants(local, cfg, B, P, arch, steps=2, warmup=1, reserve=3e9, on
                                      "recompute_rows": prof["recompute_rows"],
                                      "ms_per_step": ms, "kv_gpu_blocks": kv_gpu, "kv_host_blocks": caps.kv_host,
                                      "act_gpu_blocks": act_cap, "h2d_gb_per_step": acc["h2d"] / steps / 1e9,
-                                     "planned": abs(r - r_fit) < 1e-9})
+                                     "planned": r == r_bal, "capacity_only": r == r_fit})
         except Exception as e:
             out["per_ratio"].append({"act_share_r": round(r, 4), "error": str(e)})
     eng.close()

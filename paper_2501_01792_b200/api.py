@@ -341,6 +341,18 @@ def plan_hbm_residency(cfg: ModelConfig, requests: int, blocks_per_request: int,
     return r.value, PoolCaps(kv_host=out[3], kv_gpu=out[1], act_host=out[2], act_gpu=out[0])
 
 
+def plan_hbm_tiers(cfg: ModelConfig, requests: int, blocks_per_request: int, hbm_bytes: float,
+                   bundle: TimingBundle):
+    """Balanced three-tier plan (csrc/host/plan.hpp): (r, PoolCaps, (t_comp, t_link) per layer)."""
+    c = cfg.to_c()
+    b, bp = bundle.arr5()
+    r = C.c_double()
+    out = (C.c_long * 4)()
+    t, tp = _darr(np.zeros(2))
+    check(lib().hc_plan_hbm_tiers(C.byref(c), requests, blocks_per_request, float(hbm_bytes), bp, C.byref(r), out, tp))
+    return r.value, PoolCaps(kv_host=out[3], kv_gpu=out[1], act_host=out[2], act_gpu=out[0]), tuple(t.tolist())
+
+
 def plan_host_allocation(bundle: TimingBundle, mem: MemoryBudget, tpb: int, act_gpu: int) -> HostAllocation:
     """plan.cpp:106-152 (paper Alg. 1 + frontier polish)."""
     b, bp = bundle.arr5()

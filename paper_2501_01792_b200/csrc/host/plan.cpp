@@ -229,4 +229,41 @@ HbmPlan plan_hbm_residency(const ModelConfig& c, long requests, long blocks_per_
     return p;
 }
 
+HbmTierPlan plan_hbm_tiers(const ModelConfig& c, long requests, long blocks_per_request, double hbm_bytes,
+                           const TimingBundle& b) {
+    if (requests < 1 || blocks_per_request < 1) throw InputError("plan_hbm_tiers: empty workload");
+    if (hbm_bytes <= 0) throw InputError("plan_hbm_tiers: no device memory");
+    const double L = c.num_layers, tpb = c.tokens_per_block, B = static_cast<double>(requests);
+    const double kv_one = static_cast<double>(HybridCache::bytes_of(BlockKind::KV, c));
+    const double act_one = static_cast<double>(HybridCache::bytes_of(BlockKind::ACT, c));
+    const double kv_all = kv_one * L, act_all = act_one * L;
+    const long N = requests * blocks_per_request;
+    auto t_comp = [&](long x) { return x > 0 ? eval(b.t_kv_gen, static_cast<double>(x) * tpb) : 0.0; };
+    auto t_link = [&](long z) { return z > 0 ? eval(b.t_load_kv, static_cast<double>(z) * tpb) : 0.0; };
+    HbmTierPlan best;
+    double best_t = -1;
+    for (long x = 0; x <= N; ++x) {
+        // x ACT/gpu blocks + recompute slots (x + B spill), KV staging for z + B host blocks,
+        // ACT staging for the B spill blocks, y KV/gpu blocks
+        const double rhs = hbm_bytes - x * (act_all + kv_one) - B * kv_one - 2.0 * (N - x + B) * kv_one -
+                           2.0 * B * act_one;
+        if (rhs < 0) break;  // rhs falls with x: an ACT block (all layers) outweighs the staging slot it saves
+        const long y = std::min<long>(N - x, static_cast<long>(std::floor(rhs / (kv_all - 2 * kv_one))));
+        const long z = N - x - std::max<long>(y, 0);
+        const double t = std::max(t_comp(x), t_link(z));
+        if (best_t < 0 || t < best_t) {
+            best_t = t;
+            best.act_share = static_cast<double>(x) / N;
+            best.act_gpu = x;
+            best.act_host = x > 0 && x < N ? requests : 0;
+            best.kv_gpu = std::max<long>(y, 0);
+            best.kv_host = z + (x < N ? requests : 0);
+            best.t_comp = t_comp(x);
+            best.t_link = t_link(z);
+        }
+    }
+    if (best_t < 0) throw CapacityError("plan_hbm_tiers: device memory cannot hold the staging of the workload");
+    return best;
+}
+
 }  // namespace hc

@@ -79,6 +79,22 @@ struct HbmPlan {
 };
 HbmPlan plan_hbm_residency(const ModelConfig& c, long requests, long blocks_per_request, double hbm_bytes);
 
+// Balanced three-tier plan (B200 extension of Alg. 1's balance, Eq. 10): x ACT
+// blocks in HBM (recomputed each step), y KV blocks in HBM, z KV blocks in
+// pinned host memory streamed per layer. Over all x, y is the most KV that
+// still fits next to x ACT blocks, their recompute slots and the staging slots
+// of the z host blocks; the plan minimises the per-layer critical path
+// max(t_kv_gen(x tpb), t_load_kv(z tpb)) from the MEASURED bundle — with
+// weights resident the link is otherwise idle, so streaming some KV from host
+// while the tensor cores recompute beats recomputing it. Capacities add one
+// block of slack per request (ACT spill to host, KV host) for block-boundary
+// rounding of the ratio. t_comp / t_link are the predicted per-layer times.
+struct HbmTierPlan : HbmPlan {
+    double t_comp = 0, t_link = 0;
+};
+HbmTierPlan plan_hbm_tiers(const ModelConfig& c, long requests, long blocks_per_request, double hbm_bytes,
+                           const TimingBundle& b);
+
 // FLOP model (flops.cpp:7-37); kinds: 0 KvGen, 1 QkvGen, 2 Attention,
 // 3 ProjFfn, 4 TokenRecomputeToLayerK, 5 FullLayer.
 double flop_count(int kind, const ModelConfig& c, long n_tokens, int k = 0);
