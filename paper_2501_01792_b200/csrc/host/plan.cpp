@@ -257,7 +257,7 @@ HbmTierPlan plan_hbm_tiers(const ModelConfig& c, long requests, long blocks_per_
             best.act_gpu = x;
             best.act_host = x > 0 && x < N ? requests : 0;
             best.kv_gpu = std::max<long>(y, 0);
-            best.kv_host = z + (x < N ? requests : 0);
+            best.kv_host = z + (x > 0 && x < N ? requests : 0);  // slack only where the ratio rounds
             best.t_comp = t_comp(x);
             best.t_link = t_link(z);
         }

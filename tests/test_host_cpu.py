@@ -278,3 +278,48 @@ def test_plan_hbm_residency(model, B, nb, hbm_gb):
         assert r == 0.0 and caps.kv_host == 0
     with pytest.raises(api.InputError):
         api.plan_hbm_residency(cfg, 0, nb, 1e9)
+
+
+def _hbm_tiers_restated(cfg, B, nb, hbm, slope_gen, slope_load):
+    """Python restatement of plan_hbm_tiers (csrc/host/plan.hpp), zero intercepts."""
+    import math
+    from paper_2501_01792_b200 import api
+    L, tpb = cfg.num_layers, cfg.tokens_per_block
+    kv_one, act_one = api.HybridCache.bytes_of("KV", cfg), api.HybridCache.bytes_of("ACT", cfg)
+    kv_all, act_all = kv_one * L, act_one * L
+    N = B * nb
+    best = None
+    for x in range(N + 1):
+        rhs = hbm - x * (act_all + kv_one) - B * kv_one - 2.0 * (N - x + B) * kv_one - 2.0 * B * act_one
+        if rhs < 0:
+            break
+        y = min(N - x, math.floor(rhs / (kv_all - 2 * kv_one)))
+        z = N - x - max(y, 0)
+        t = max(slope_gen * x * tpb, slope_load * z * tpb)
+        if best is None or t < best[0]:
+            best = (t, x, max(y, 0), z)
+    t, x, y, z = best
+    return x / N, (x, y, (B if 0 < x < N else 0), z + (B if 0 < x < N else 0))
+
+
+@pytest.mark.parametrize("model,B,nb,hbm_gb,gen,load", [("opt-30b", 128, 65, 127.6, 1.3e-7, 5.2e-7),
+                                                          ("opt-30b", 64, 65, 40.0, 1.3e-7, 5.2e-7),
+                                                          ("opt-13b", 64, 129, 150.0, 8e-8, 3.7e-7),
+                                                          ("opt-30b", 128, 65, 127.6, 1e-5, 5.2e-7)])
+def test_plan_hbm_tiers(model, B, nb, hbm_gb, gen, load):
+    """Balanced three-tier plan: matches the restatement; balances the two
+    channels when both are in use; all-KV in HBM when it fits; falls back to
+    capacity-bound KV streaming when recompute is expensive."""
+    from paper_2501_01792_b200 import api
+    cfg = api.ModelConfig.preset(model)
+    kv = [(1024.0, 1024 * gen), (4096.0, 4096 * gen)]
+    ld = [(1024.0, 1024 * load), (4096.0, 4096 * load)]
+    bundle = api.bundle_from_samples(kv, ld, 55e9, cfg)
+    r, caps, (tc, tl) = api.plan_hbm_tiers(cfg, B, nb, hbm_gb * 1e9, bundle)
+    r2, c2 = _hbm_tiers_restated(cfg, B, nb, hbm_gb * 1e9, bundle.t_kv_gen.slope, bundle.t_load_kv.slope)
+    assert r == pytest.approx(r2) and (caps.act_gpu, caps.kv_gpu, caps.act_host, caps.kv_host) == c2
+    if model == "opt-13b":
+        assert caps.act_gpu == 0 and caps.kv_host == 0          # all KV fits in HBM
+    elif gen < 1e-6:
+        assert caps.act_gpu > 0 and caps.kv_host > B            # both channels busy ...
+        assert abs(tc - tl) <= max(tc, tl) * 0.02               # ... and balanced
