@@ -174,3 +174,16 @@ def test_gpu_weight_generation_bit_exact(on_device):
     assert np.array_equal(eng.read_weights(-2), host["positional"])
     for l in range(2):
         assert np.array_equal(eng.read_weights(l), host["layers"][l])
+
+
+def test_full_width_opt30b_layer_parity():
+    """One OPT-30B-width layer (d 7168, 56 heads, f 28672) through the offloaded
+    hybrid engine: prefill + 3 decode steps, and the cache blocks, within 1e-2 of
+    the fp64 oracle (scripts/full_width_parity.py; ~30 s, ~10 GB host RAM)."""
+    import importlib.util
+    import os
+    p = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "scripts", "full_width_parity.py")
+    spec = importlib.util.spec_from_file_location("full_width_parity", p)
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    mod.main()
