@@ -851,6 +851,18 @@ def our_arm(args, cfg, world, rank, local, dist):
     return res
 
 
+def _host_mem_available():
+    """MemAvailable from /proc/meminfo (bytes); 0 when unreadable (= unbounded)."""
+    try:
+        with open("/proc/meminfo") as f:
+            for line in f:
+                if line.startswith("MemAvailable:"):
+                    return float(line.split()[1]) * 1024
+    except OSError:
+        pass
+    return 0.0
+
+
 def resident_variants(local, cfg, B, P, arch, steps=2, warmup=1, reserve=3e9, only_planned=False):
     """The same workload with the weights AND the cache in HBM (B200 has 180 GB):
     KV and ACT blocks both placed on the GPU first (kv_on_gpu / ACT-first,
@@ -885,16 +897,23 @@ def resident_variants(local, cfg, B, P, arch, steps=2, warmup=1, reserve=3e9, on
     bundle = api.bundle_from_samples(kv_s, ld_s, link_bps, cfg)
     eng.configure_cache(api.PoolCaps(), mode="act_only")
     free = torch.cuda.mem_get_info(local)[0] - reserve
+    host_budget = 0.8 * _host_mem_available()  # pinned host tiers (page-locked: leave the OS headroom)
     # the library's HBM planners (csrc/host/plan.hpp): capacity-only (smallest
     # ACT share that fits) and balanced three tiers (ACT + KV in HBM, KV from
     # host, max(t_kv_gen, t_load_kv) minimised on the measured bundle)
     r_fit, caps_fit = api.plan_hbm_residency(cfg, B, nb, free)
-    r_bal, caps_bal, t_bal = api.plan_hbm_tiers(cfg, B, nb, free, bundle)
+    try:
+        r_bal, caps_bal, t_bal = api.plan_hbm_tiers(cfg, B, nb, free, bundle, host_bytes=host_budget)
+    except api.CapacityError as e:  # e.g. OPT-66B: 130 GB of weights leave too little HBM for this cache
+        eng.close()
+        return {"workload": f"{cfg.name}-shape, batch {B}, prompt {P}: weights + cache in HBM",
+                "infeasible": str(e), "free_hbm_gb": free / 1e9, "host_budget_gb": host_budget / 1e9,
+                "cache_gb": {"all_kv": N * kv_all / 1e9, "all_act": N * act_all / 1e9}}
     ids = [f"h{i}" for i in range(B)]
     tokens = np.random.default_rng(9).integers(0, cfg.vocab_size, (total, B)).astype(np.int32)
     out = {"workload": f"{cfg.name}-shape, batch {B}, prompt {P}: weights + cache in HBM (KV and ACT placed on "
                        "the GPU first); overflow blocks in pinned host memory",
-           "free_hbm_gb": free / 1e9, "blocks": N, "r_fit": r_fit, "r_planned": r_bal,
+           "free_hbm_gb": free / 1e9, "host_budget_gb": host_budget / 1e9, "blocks": N, "r_fit": r_fit, "r_planned": r_bal,
            "planned_tiers": {"act_gpu": caps_bal.act_gpu, "kv_gpu": caps_bal.kv_gpu, "kv_host": caps_bal.kv_host,
                              "act_host": caps_bal.act_host, "predicted_t_comp_ms_per_layer": t_bal[0] * 1e3,
                              "predicted_t_link_ms_per_layer": t_bal[1] * 1e3},
@@ -916,6 +935,16 @@ def resident_variants(local, cfg, B, P, arch, steps=2, warmup=1, reserve=3e9, on
             caps = api.PoolCaps(kv_host=kv_need - kv_gpu, kv_gpu=kv_gpu, act_gpu=act_cap)
         act_cap, kv_gpu = caps.act_gpu, caps.kv_gpu
         mode = "kv_only" if r <= 0 else ("act_only" if r >= 1 else "hybrid")
+        host_need = caps.kv_host * kv_all + caps.act_host * act_all
+        if host_budget > 0 and host_need > host_budget:
+            out["per_ratio"].append({"act_share_r": round(r, 4), "skipped":
+                                     f"host tiers need {host_need / 1e9:.0f} GB pinned > budget {host_budget / 1e9:.0f} GB"})
+            continue
+        if r >= 1 and act_cap * (act_all + kv_one) > free:
+            out["per_ratio"].append({"act_share_r": round(r, 4), "skipped":
+                                     f"ACT blocks need {act_cap * (act_all + kv_one) / 1e9:.0f} GB HBM > free "
+                                     f"{free / 1e9:.0f} GB"})
+            continue
         try:
             alloc = (api.HostAllocation(caps_bal.act_gpu, N - caps_bal.act_gpu) if r == r_bal
                      else api.HostAllocation(a, 1000 - a))

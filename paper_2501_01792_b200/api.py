@@ -19,6 +19,7 @@ from typing import Dict, List, Optional, Sequence, Tuple
 import numpy as np
 
 from ._native import check, lib, ptr
+from .errors import CapacityError, ConfigError, InputError  # noqa: F401  (re-exported)
 from ._signatures import EngineOptionsC, ModelConfigC
 from .errors import InputError
 
@@ -342,14 +343,15 @@ def plan_hbm_residency(cfg: ModelConfig, requests: int, blocks_per_request: int,
 
 
 def plan_hbm_tiers(cfg: ModelConfig, requests: int, blocks_per_request: int, hbm_bytes: float,
-                   bundle: TimingBundle):
-    """Balanced three-tier plan (csrc/host/plan.hpp): (r, PoolCaps, (t_comp, t_link) per layer)."""
+                   bundle: TimingBundle, host_bytes: float = 0.0):
+    """Balanced three-tier plan (csrc/host/plan.hpp): (r, PoolCaps, (t_comp, t_link) per layer).
+    host_bytes bounds the pinned host tiers (0 = unbounded)."""
     c = cfg.to_c()
     b, bp = bundle.arr5()
     r = C.c_double()
     out = (C.c_long * 4)()
     t, tp = _darr(np.zeros(2))
-    check(lib().hc_plan_hbm_tiers(C.byref(c), requests, blocks_per_request, float(hbm_bytes), bp, C.byref(r), out, tp))
+    check(lib().hc_plan_hbm_tiers(C.byref(c), requests, blocks_per_request, float(hbm_bytes), float(host_bytes), bp, C.byref(r), out, tp))
     return r.value, PoolCaps(kv_host=out[3], kv_gpu=out[1], act_host=out[2], act_gpu=out[0]), tuple(t.tolist())
 
 

@@ -577,6 +577,8 @@ void Engine::configure_cache(const PoolCaps& caps, bool kv_on_gpu, CacheMode mod
         const size_t need = kv_e_al + act_e;
         if (need > m.h_arena_elems) {
             if (m.h_arena) HC_CUDA(cudaFreeHost(m.h_arena));
+            m.h_arena = nullptr;  // stays null if the new allocation fails
+            m.h_arena_elems = 0;
             m.h_arena = halloc<bf16>(need, true);
             m.h_arena_elems = need;
         }

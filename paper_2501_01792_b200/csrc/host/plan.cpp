@@ -230,9 +230,10 @@ HbmPlan plan_hbm_residency(const ModelConfig& c, long requests, long blocks_per_
 }
 
 HbmTierPlan plan_hbm_tiers(const ModelConfig& c, long requests, long blocks_per_request, double hbm_bytes,
-                           const TimingBundle& b) {
+                           const TimingBundle& b, double host_bytes) {
     if (requests < 1 || blocks_per_request < 1) throw InputError("plan_hbm_tiers: empty workload");
     if (hbm_bytes <= 0) throw InputError("plan_hbm_tiers: no device memory");
+    if (host_bytes < 0) throw InputError("plan_hbm_tiers: negative host budget");
     const double L = c.num_layers, tpb = c.tokens_per_block, B = static_cast<double>(requests);
     const double kv_one = static_cast<double>(HybridCache::bytes_of(BlockKind::KV, c));
     const double act_one = static_cast<double>(HybridCache::bytes_of(BlockKind::ACT, c));
@@ -250,6 +251,10 @@ HbmTierPlan plan_hbm_tiers(const ModelConfig& c, long requests, long blocks_per_
         if (rhs < 0) break;  // rhs falls with x: an ACT block (all layers) outweighs the staging slot it saves
         const long y = std::min<long>(N - x, static_cast<long>(std::floor(rhs / (kv_all - 2 * kv_one))));
         const long z = N - x - std::max<long>(y, 0);
+        if (host_bytes > 0) {  // pinned host tiers: KV host blocks (+ slack) and the ACT spill blocks
+            const double slack = x > 0 && x < N ? B : 0.0;
+            if ((z + slack) * kv_all + slack * act_all > host_bytes) continue;
+        }
         const double t = std::max(t_comp(x), t_link(z));
         if (best_t < 0 || t < best_t) {
             best_t = t;
@@ -262,7 +267,8 @@ HbmTierPlan plan_hbm_tiers(const ModelConfig& c, long requests, long blocks_per_
             best.t_link = t_link(z);
         }
     }
-    if (best_t < 0) throw CapacityError("plan_hbm_tiers: device memory cannot hold the staging of the workload");
+    if (best_t < 0)
+        throw CapacityError("plan_hbm_tiers: device and host memory cannot hold the workload and its staging");
     return best;
 }
 

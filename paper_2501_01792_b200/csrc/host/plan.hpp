@@ -89,11 +89,13 @@ HbmPlan plan_hbm_residency(const ModelConfig& c, long requests, long blocks_per_
 // while the tensor cores recompute beats recomputing it. Capacities add one
 // block of slack per request (ACT spill to host, KV host) for block-boundary
 // rounding of the ratio. t_comp / t_link are the predicted per-layer times.
+// host_bytes (> 0) bounds the pinned host memory of the host tiers (KV host
+// blocks, all layers, plus the ACT spill blocks); 0 = unbounded.
 struct HbmTierPlan : HbmPlan {
     double t_comp = 0, t_link = 0;
 };
 HbmTierPlan plan_hbm_tiers(const ModelConfig& c, long requests, long blocks_per_request, double hbm_bytes,
-                           const TimingBundle& b);
+                           const TimingBundle& b, double host_bytes = 0);
 
 // FLOP model (flops.cpp:7-37); kinds: 0 KvGen, 1 QkvGen, 2 Attention,
 // 3 ProjFfn, 4 TokenRecomputeToLayerK, 5 FullLayer.

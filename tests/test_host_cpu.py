@@ -280,7 +280,7 @@ def test_plan_hbm_residency(model, B, nb, hbm_gb):
         api.plan_hbm_residency(cfg, 0, nb, 1e9)
 
 
-def _hbm_tiers_restated(cfg, B, nb, hbm, slope_gen, slope_load):
+def _hbm_tiers_restated(cfg, B, nb, hbm, slope_gen, slope_load, host=0.0):
     """Python restatement of plan_hbm_tiers (csrc/host/plan.hpp), zero intercepts."""
     import math
     from paper_2501_01792_b200 import api
@@ -295,9 +295,14 @@ def _hbm_tiers_restated(cfg, B, nb, hbm, slope_gen, slope_load):
             break
         y = min(N - x, math.floor(rhs / (kv_all - 2 * kv_one)))
         z = N - x - max(y, 0)
+        slack = B if 0 < x < N else 0
+        if host > 0 and (z + slack) * kv_all + slack * act_all > host:
+            continue
         t = max(slope_gen * x * tpb, slope_load * z * tpb)
         if best is None or t < best[0]:
             best = (t, x, max(y, 0), z)
+    if best is None:
+        return None
     t, x, y, z = best
     return x / N, (x, y, (B if 0 < x < N else 0), z + (B if 0 < x < N else 0))
 
@@ -323,3 +328,31 @@ def test_plan_hbm_tiers(model, B, nb, hbm_gb, gen, load):
     elif gen < 1e-6:
         assert caps.act_gpu > 0 and caps.kv_host > B            # both channels busy ...
         assert abs(tc - tl) <= max(tc, tl) * 0.02               # ... and balanced
+
+
+
+@pytest.mark.parametrize("host_gb", [224.0, 120.0, 60.0, 5.0])
+def test_plan_hbm_tiers_host_budget(host_gb):
+    """A pinned-host budget moves blocks from the KV host tier to recompute
+    (ACT in HBM), matching the restatement; an impossible budget is a
+    CapacityError."""
+    from paper_2501_01792_b200 import api
+    cfg = api.ModelConfig.preset("opt-66b")
+    B, nb = 64, 132
+    kv = [(1024.0, 1024 * 2.5e-7), (4096.0, 4096 * 2.5e-7)]
+    ld = [(1024.0, 1024 * 1.2e-6), (4096.0, 4096 * 1.2e-6)]
+    bundle = api.bundle_from_samples(kv, ld, 55e9, cfg)
+    want = _hbm_tiers_restated(cfg, B, nb, 56e9, bundle.t_kv_gen.slope, bundle.t_load_kv.slope, host_gb * 1e9)
+    if want is None:
+        from paper_2501_01792_b200.errors import CapacityError
+        with pytest.raises(CapacityError):
+            api.plan_hbm_tiers(cfg, B, nb, 56e9, bundle, host_bytes=host_gb * 1e9)
+        return
+    r, caps, _ = api.plan_hbm_tiers(cfg, B, nb, 56e9, bundle, host_bytes=host_gb * 1e9)
+    r2, c2 = want
+    assert r == pytest.approx(r2) and (caps.act_gpu, caps.kv_gpu, caps.act_host, caps.kv_host) == c2
+    kv_all = api.HybridCache.bytes_of("KV", cfg) * cfg.num_layers
+    act_all = api.HybridCache.bytes_of("ACT", cfg) * cfg.num_layers
+    assert caps.kv_host * kv_all + caps.act_host * act_all <= host_gb * 1e9
+    r_free, _, _ = api.plan_hbm_tiers(cfg, B, nb, 56e9, bundle)
+    assert r >= r_free
