@@ -1,5 +1,8 @@
 // Causal prefill attention on the 5th-gen tensor cores (tcgen05 + TMEM + TMA),
-// head_dim 128 (attention_causal, decoder.cpp:55-63).
+// head_dim 128 (attention_causal, decoder.cpp:55-63). Two kernels:
+//   prefill_tc2_kernel (default) — persistent, pairs of query tiles, two
+//                                  softmax warpgroups (see its header below)
+//   prefill_tc_kernel  (HC_PREFILL_TC=1) — one query tile per CTA:
 //
 // One CTA per (128-query tile, head, request); 192 threads:
 //   warp 0      TMA producer: Q once, then K|V tiles of 128 keys into a
@@ -21,6 +24,7 @@
 // tile j writes P while P.V(j-1) still runs. Heavy (late) query tiles first.
 #include <cuda.h>
 
+#include <algorithm>
 #include <cfloat>
 #include <cstdlib>
 #include <stdexcept>
@@ -308,20 +312,27 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 // ---------------------------------------------------------------------------
-// Two-tile variant (default): one CTA per PAIR of 128-query tiles, 320 threads
-//   warps 0..3  softmax of query tile 0 (rows q0 .. q0+127)
+// Two-tile persistent variant (default). A work item is a PAIR of 128-query
+// tiles of one (request, head); one CTA per SM walks the items heaviest pair
+// first (static stride). 320 threads:
+//   warps 0..3  softmax of query tile 0 of the item (rows q0 .. q0+127)
 //   warps 4..7  softmax of query tile 1 (rows q0+128 .. q0+255)
-//   warp 8      TMA producer: Q0|Q1 once, then K_j, V_j into a 3-slot ring
+//   warp 8      TMA producer: Q0|Q1, then K_j, V_j into a 3-slot ring; the
+//               next item's Q and K/V load while this item finishes
 //   warp 9      TMEM owner + MMA issuer, ping-pong between the tiles:
 //                 PV0(j), S0(j+1), PV1(j), S1(j+1)
 //               so the tensor core runs tile 1's MMAs while tile 0's softmax
 //               works and vice versa (one softmax group alone leaves the
-//               tensor pipe idle ~80 % of the time).
+//               tensor pipe idle ~80 % of the time); the next item's first
+//               QK^T runs while the softmax warps write this item's O.
 // TMEM: S0 | S1 | O0 | O1 = 512 columns. smem: Q0, Q1, P0, P1, 3 K/V slots of
 // 32 KB = 224 KB. With one S and one P buffer per tile no free barriers are
-// needed: the commit that signals S_t(j) also covers PV_t(j-1) (tcgen05
-// operations of one thread complete in issue order), so when the softmax sees
-// S_t(j) both P_t and O_t are free to write.
+// needed inside an item: the commit that signals S_t(j) also covers PV_t(j-1)
+// (tcgen05 operations of one thread complete in issue order), so when the
+// softmax sees S_t(j) both P_t and O_t are free to write. Across items: Q is
+// reloaded after the item's last QK^T (q_empty), O_t is overwritten only after
+// the softmax has read it out (o_free). Barrier phases run on per-role
+// counters that continue across items.
 constexpr int kSlots2 = 3;
 constexpr int kThreads2 = 320;
 
@@ -334,35 +345,53 @@ struct Smem2 {
 };
 static_assert(Smem2::bytes <= 232448, "prefill_tc2: shared memory over the per-CTA limit");
 
+struct Item {  // one (request, head, query-tile pair)
+    int row0, P, h, qt0, n0, n1, n_kt;
+    bool has1;
+};
+// heaviest pairs first: item w -> pair n_pairs-1 - w / (H n_req); false if the
+// pair lies beyond its request (every role skips it identically)
+__device__ __forceinline__ bool item_of(int w, int n_pairs, int H, int n_req, const int* cu, Item& it) {
+    const int per = H * n_req;
+    const int pair = n_pairs - 1 - w / per, rem = w % per;
+    it.h = rem % H;
+    const int req = rem / H;
+    it.row0 = cu[req];
+    it.P = cu[req + 1] - it.row0;
+    const int n_qt = (it.P + kT - 1) / kT;
+    it.qt0 = 2 * pair;
+    if (it.qt0 >= n_qt) return false;
+    it.has1 = it.qt0 + 1 < n_qt;
+    it.n0 = it.qt0 + 1;  // causal key tiles per query tile
+    it.n1 = it.has1 ? it.qt0 + 2 : 0;
+    it.n_kt = it.has1 ? it.n1 : it.n0;
+    return true;
+}
+
 __global__ void __launch_bounds__(kThreads2, 1)
     prefill_tc2_kernel(const __grid_constant__ CUtensorMap tm, bf16* __restrict__ out, const int* __restrict__ cu,
-                       int H, float scale, uint32_t v_lbo, uint32_t v_sbo) {
+                       int n_req, int n_pairs, int H, float scale, uint32_t v_lbo, uint32_t v_sbo) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Smem2::bars);
     uint64_t* q_full = bars + 0;
-    uint64_t* kv_full = bars + 1;   // [kSlots2]
-    uint64_t* kv_empty = bars + 4;  // [kSlots2]
-    uint64_t* s_full = bars + 7;    // [2] per tile
-    uint64_t* p_full = bars + 9;    // [2] per tile
-    uint64_t* o_done = bars + 11;   // [2] per tile
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 14);
+    uint64_t* q_empty = bars + 1;
+    uint64_t* kv_full = bars + 2;   // [kSlots2]
+    uint64_t* kv_empty = bars + 5;  // [kSlots2]
+    uint64_t* s_full = bars + 8;    // [2] per tile
+    uint64_t* p_full = bars + 10;   // [2] per tile
+    uint64_t* o_done = bars + 12;   // [2] per tile
+    uint64_t* o_free = bars + 14;   // [2] per tile
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
 
-    const int req = blockIdx.z, h = blockIdx.y;
-    const int row0 = cu[req];
-    const int P = cu[req + 1] - row0;
-    const int n_qt = (P + kT - 1) / kT;
-    const int qt0 = 2 * (static_cast<int>(gridDim.x) - 1 - static_cast<int>(blockIdx.x));  // heavy pairs first
-    if (qt0 >= n_qt) return;
-    const bool has1 = qt0 + 1 < n_qt;
-    const int n0 = qt0 + 1, n1 = has1 ? qt0 + 2 : 0;  // causal key tiles per query tile
-    const int n_kt = has1 ? n1 : n0;
+    const int n_items = n_pairs * H * n_req;
     const int d = H * kHD;
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
 
     if (threadIdx.x == 0) {
         ptx::tma_prefetch(&tm);
         ptx::mbar_init(q_full, 1);
+        ptx::mbar_init(q_empty, 1);
         for (int s = 0; s < kSlots2; ++s) {
             ptx::mbar_init(&kv_full[s], 1);
             ptx::mbar_init(&kv_empty[s], 1);
@@ -371,6 +400,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
             ptx::mbar_init(&s_full[t], 1);
             ptx::mbar_init(&p_full[t], 128);
             ptx::mbar_init(&o_done[t], 1);
+            ptx::mbar_init(&o_free[t], 128);
         }
         ptx::fence_mbar_init();
     }
@@ -382,35 +412,41 @@ __global__ void __launch_bounds__(kThreads2, 1)
 
     if (warp == 8) {
         if (lane == 0) {  // ---------------------------------------- TMA producer
-            const int qc = h * kHD, kc = d + h * kHD, vc = 2 * d + h * kHD;
-            ptx::mbar_arrive_expect_tx(q_full, has1 ? 2 * kTile : kTile);
-            for (int t = 0; t < (has1 ? 2 : 1); ++t) {
-                uint8_t* qb = smem + Smem2::q + t * kTile;
-                ptx::tma_load_2d(qb, &tm, q_full, qc, row0 + (qt0 + t) * kT);
-                ptx::tma_load_2d(qb + kBox, &tm, q_full, qc + 64, row0 + (qt0 + t) * kT);
-            }
-            for (int i = 0; i < 2 * n_kt; ++i) {  // K_0, V_0, K_1, V_1, ...
-                const int s = i % kSlots2;
-                ptx::mbar_wait(&kv_empty[s], ((i / kSlots2) & 1) ^ 1);
-                uint8_t* b = smem + Smem2::kv + s * kTile;
-                ptx::mbar_arrive_expect_tx(&kv_full[s], kTile);
-                const int c = (i & 1) ? vc : kc, r = row0 + (i / 2) * kT;
-                ptx::tma_load_2d(b, &tm, &kv_full[s], c, r);
-                ptx::tma_load_2d(b + kBox, &tm, &kv_full[s], c + 64, r);
+            uint32_t ring = 0, n_it = 0;
+            for (int w = blockIdx.x; w < n_items; w += gridDim.x) {
+                Item it;
+                if (!item_of(w, n_pairs, H, n_req, cu, it)) continue;
+                const int qc = it.h * kHD, kc = d + it.h * kHD, vc = 2 * d + it.h * kHD;
+                if (n_it > 0) ptx::mbar_wait(q_empty, (n_it - 1) & 1);  // last QK^T of the previous item done
+                ptx::mbar_arrive_expect_tx(q_full, it.has1 ? 2 * kTile : kTile);
+                for (int t = 0; t < (it.has1 ? 2 : 1); ++t) {
+                    uint8_t* qb = smem + Smem2::q + t * kTile;
+                    ptx::tma_load_2d(qb, &tm, q_full, qc, it.row0 + (it.qt0 + t) * kT);
+                    ptx::tma_load_2d(qb + kBox, &tm, q_full, qc + 64, it.row0 + (it.qt0 + t) * kT);
+                }
+                for (int i = 0; i < 2 * it.n_kt; ++i) {  // K_0, V_0, K_1, V_1, ...
+                    const uint32_t g = ring + i, s = g % kSlots2;
+                    ptx::mbar_wait(&kv_empty[s], ((g / kSlots2) & 1) ^ 1);
+                    uint8_t* b = smem + Smem2::kv + s * kTile;
+                    ptx::mbar_arrive_expect_tx(&kv_full[s], kTile);
+                    const int c = (i & 1) ? vc : kc, r = it.row0 + (i / 2) * kT;
+                    ptx::tma_load_2d(b, &tm, &kv_full[s], c, r);
+                    ptx::tma_load_2d(b + kBox, &tm, &kv_full[s], c + 64, r);
+                }
+                ring += 2 * it.n_kt;
+                ++n_it;
             }
         }
     } else if (warp == 9) {
         if (lane == 0) {  // ------------------------------------------ MMA issuer
             constexpr uint32_t id_s = ptx::idesc_bf16_f32(kT, kT);               // A, B K-major
             constexpr uint32_t id_o = ptx::idesc_bf16_f32(kT, kHD) | (1u << 16);  // B MN-major (V)
-            auto slot_wait = [&](int i) {  // ring entry i (K_j = 2j, V_j = 2j + 1) landed
-                ptx::mbar_wait(&kv_full[i % kSlots2], (i / kSlots2) & 1);
-            };
-            auto slot_addr = [&](int i) { return ptx::smem_u32(smem + Smem2::kv + (i % kSlots2) * kTile); };
-            auto s_mma = [&](int t, int j) {
-                slot_wait(2 * j);
+            uint32_t ring = 0, n_it = 0, pc[2] = {0, 0}, oc[2] = {0, 0};
+            auto slot_addr = [&](uint32_t g) { return ptx::smem_u32(smem + Smem2::kv + (g % kSlots2) * kTile); };
+            auto s_mma = [&](int t, uint32_t g) {  // S_t = Q_t . K^T, K at ring entry g
+                ptx::mbar_wait(&kv_full[g % kSlots2], (g / kSlots2) & 1);
                 ptx::tc_fence_after();
-                const uint32_t qa = ptx::smem_u32(smem + Smem2::q + t * kTile), kb = slot_addr(2 * j);
+                const uint32_t qa = ptx::smem_u32(smem + Smem2::q + t * kTile), kb = slot_addr(g);
 #pragma unroll
                 for (int k = 0; k < kHD / 16; ++k) {
                     const uint32_t off = (k / 4) * kBox;
@@ -419,131 +455,155 @@ __global__ void __launch_bounds__(kThreads2, 1)
                 }
                 ptx::mma_commit(&s_full[t]);
             };
-            auto pv_mma = [&](int t, int j) {
-                slot_wait(2 * j + 1);
-                ptx::mbar_wait(&p_full[t], j & 1);
+            auto pv_mma = [&](int t, uint32_t g, bool first) {  // O_t += P_t . V, V at ring entry g
+                ptx::mbar_wait(&kv_full[g % kSlots2], (g / kSlots2) & 1);
+                if (first && oc[t] > 0) ptx::mbar_wait(&o_free[t], (oc[t] - 1) & 1);  // previous O_t read out
+                ptx::mbar_wait(&p_full[t], pc[t] & 1);
+                ++pc[t];
                 ptx::tc_fence_after();
-                const uint32_t pa = ptx::smem_u32(smem + Smem2::p + t * kTile), vb = slot_addr(2 * j + 1);
+                const uint32_t pa = ptx::smem_u32(smem + Smem2::p + t * kTile), vb = slot_addr(g);
 #pragma unroll
                 for (int k = 0; k < kT / 16; ++k) {
                     const uint64_t a = ptx::sw128_kmajor_desc(pa + (k / 4) * kBox) + 2 * (k % 4);
                     const uint64_t bdesc = sw128_mnmajor_desc(vb + k * 16 * 128, v_lbo, v_sbo);
-                    ptx::mma_bf16_ss(tmem + 256u + 128u * t, a, bdesc, id_o, (j > 0 || k > 0) ? 1u : 0u);
+                    ptx::mma_bf16_ss(tmem + 256u + 128u * t, a, bdesc, id_o, (!first || k > 0) ? 1u : 0u);
                 }
             };
-            ptx::mbar_wait(q_full, 0);
-            s_mma(0, 0);
-            if (n1) s_mma(1, 0);
-            ptx::mma_commit(&kv_empty[0]);  // K_0 consumed
-            for (int j = 0; j < n_kt; ++j) {
-                if (j < n0) {
-                    pv_mma(0, j);
-                    if (j + 1 == n0) ptx::mma_commit(&o_done[0]);
+            for (int w = blockIdx.x; w < n_items; w += gridDim.x) {
+                Item it;
+                if (!item_of(w, n_pairs, H, n_req, cu, it)) continue;
+                const int n0 = it.n0, n1 = it.n1, n_kt = it.n_kt;
+                ptx::mbar_wait(q_full, n_it & 1);
+                s_mma(0, ring);
+                if (n1) s_mma(1, ring);
+                ptx::mma_commit(&kv_empty[ring % kSlots2]);  // K_0 consumed
+                if (n_kt == 1) ptx::mma_commit(q_empty);       // last QK^T of the item issued
+                for (int j = 0; j < n_kt; ++j) {
+                    const uint32_t gk = ring + 2 * j + 2, gv = ring + 2 * j + 1;  // K_{j+1}, V_j
+                    if (j < n0) {
+                        pv_mma(0, gv, j == 0);
+                        if (j + 1 == n0) ptx::mma_commit(&o_done[0]);
+                    }
+                    if (j + 1 < n0) s_mma(0, gk);
+                    if (j < n1) {
+                        pv_mma(1, gv, j == 0);
+                        if (j + 1 == n1) ptx::mma_commit(&o_done[1]);
+                    }
+                    ptx::mma_commit(&kv_empty[gv % kSlots2]);  // V_j consumed
+                    if (j + 1 < n1) s_mma(1, gk);
+                    if (j + 1 < n_kt) {
+                        ptx::mma_commit(&kv_empty[gk % kSlots2]);  // K_{j+1} consumed
+                        if (j + 2 == n_kt) ptx::mma_commit(q_empty);
+                    }
                 }
-                if (j + 1 < n0) s_mma(0, j + 1);
-                if (j < n1) {
-                    pv_mma(1, j);
-                    if (j + 1 == n1) ptx::mma_commit(&o_done[1]);
-                }
-                ptx::mma_commit(&kv_empty[(2 * j + 1) % kSlots2]);  // V_j consumed
-                if (j + 1 < n1) s_mma(1, j + 1);
-                if (j + 1 < n_kt) ptx::mma_commit(&kv_empty[(2 * j + 2) % kSlots2]);  // K_{j+1} consumed
+                ++oc[0];
+                if (n1) ++oc[1];
+                ring += 2 * n_kt;
+                ++n_it;
             }
         }
-    } else if (warp < 4 || has1) {  // -------------------------------------- softmax
+    } else {  // ------------------------------------------------------------- softmax
         const int t = warp / 4;
         const int q = warp % 4;
-        const int r = q * 32 + lane;              // query row within the tile = TMEM lane
-        const int qrow = (qt0 + t) * kT + r;      // row within the request
-        const int n = t ? n1 : n0;
+        const int r = q * 32 + lane;  // query row within the tile = TMEM lane
         const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
         const uint32_t t_s = tmem + 128u * t, t_o = tmem + 256u + 128u * t;
         const float sl = scale * kLog2e;
-        float m = -FLT_MAX, l = 0.f;  // running max (scaled log2 domain) and sum
         const uint32_t pbase = ptx::smem_u32(smem + Smem2::p + t * kTile) + (r / 8) * 1024 + (r % 8) * 128;
-        for (int j = 0; j < n; ++j) {
-            ptx::mbar_wait(&s_full[t], j & 1);
-            ptx::tc_fence_after();
-            uint32_t sraw[kT];
+        uint32_t sc = 0, oc = 0;
+        for (int w = blockIdx.x; w < n_items; w += gridDim.x) {
+            Item it;
+            if (!item_of(w, n_pairs, H, n_req, cu, it)) continue;
+            if (t == 1 && !it.has1) continue;
+            const int P = it.P, n = t ? it.n1 : it.n0;
+            const int qrow = (it.qt0 + t) * kT + r;  // row within the request
+            float m = -FLT_MAX, l = 0.f;              // running max (scaled log2 domain) and sum
+            for (int j = 0; j < n; ++j) {
+                ptx::mbar_wait(&s_full[t], sc & 1);
+                ++sc;
+                ptx::tc_fence_after();
+                uint32_t sraw[kT];
 #pragma unroll
-            for (int c = 0; c < kT; c += 16)
-                ptx::tmem_ld_x16(t_s + lane_off + c, *reinterpret_cast<uint32_t(*)[16]>(&sraw[c]));
-            ptx::tmem_ld_wait();
-            const int k0 = j * kT;
-            const bool diag = j == n - 1 || k0 + kT > P;
-            if (diag) {
+                for (int c = 0; c < kT; c += 16)
+                    ptx::tmem_ld_x16(t_s + lane_off + c, *reinterpret_cast<uint32_t(*)[16]>(&sraw[c]));
+                ptx::tmem_ld_wait();
+                const int k0 = j * kT;
+                if (j == n - 1 || k0 + kT > P) {
 #pragma unroll
-                for (int i = 0; i < kT; ++i)
-                    if (k0 + i > qrow || k0 + i >= P) sraw[i] = __float_as_uint(-FLT_MAX);
-            }
-            float mx8[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) mx8[u] = -FLT_MAX;
-#pragma unroll
-            for (int i = 0; i < kT; ++i) mx8[i % 8] = fmaxf(mx8[i % 8], __uint_as_float(sraw[i]));
-            const float mraw = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
-                                     fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
-            const float mx = mraw == -FLT_MAX ? -FLT_MAX : mraw * sl;
-            float alpha = 1.f;
-            bool rescale = false;
-            if (mx > m + kRescale || j == 0) {  // lazy correction (see prefill_tc_kernel)
-                alpha = ex2(m - mx);
-                rescale = j > 0;
-                m = mx;
-                l *= alpha;
-            }
-            // p = 2^(s * sl - m) in one FFMA + MUFU; masked entries (-FLT_MAX * sl) underflow to 0
-            uint32_t pw[kT / 2];
-            float l8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-            for (int i = 0; i < kT / 2; ++i) {
-                const float p0 = ex2(fmaf(__uint_as_float(sraw[2 * i]), sl, -m));
-                const float p1 = ex2(fmaf(__uint_as_float(sraw[2 * i + 1]), sl, -m));
-                l8[i % 8] += p0 + p1;
-                pw[i] = ptx::pack_bf16x2(p0, p1);
-            }
-            l += ((l8[0] + l8[1]) + (l8[2] + l8[3])) + ((l8[4] + l8[5]) + (l8[6] + l8[7]));
-            if (rescale) {  // PV_t(j-1) completed before S_t(j) was signalled
-#pragma unroll 1
-                for (int c = 0; c < kHD; c += 16) {
-                    uint32_t v[16];
-                    ptx::tmem_ld_x16(t_o + lane_off + c, v);
-                    ptx::tmem_ld_wait();
-#pragma unroll
-                    for (int i = 0; i < 16; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * alpha);
-                    tmem_st_x16(t_o + lane_off + c, v);
+                    for (int i = 0; i < kT; ++i)
+                        if (k0 + i > qrow || k0 + i >= P) sraw[i] = __float_as_uint(-FLT_MAX);
                 }
-                tmem_st_wait();
-            }
+                float mx8[8];
 #pragma unroll
-            for (int c = 0; c < kT / 8; ++c) {  // 16-byte chunks of 8 keys, 128B swizzle
-                const int box = c / 8, ch = c % 8;
-                sts128(pbase + box * kBox + ((ch ^ (r % 8)) * 16), pw[4 * c], pw[4 * c + 1], pw[4 * c + 2],
-                       pw[4 * c + 3]);
-            }
-            fence_async_smem();
-            ptx::tc_fence_before();
-            ptx::mbar_arrive(&p_full[t]);
-        }
-        ptx::mbar_wait(&o_done[t], 0);
-        ptx::tc_fence_after();
-        const float inv = l > 0.f ? 1.f / l : 0.f;
-        bf16* orow = out + static_cast<long long>(row0 + qrow) * d + h * kHD;
+                for (int u = 0; u < 8; ++u) mx8[u] = -FLT_MAX;
+#pragma unroll
+                for (int i = 0; i < kT; ++i) mx8[i % 8] = fmaxf(mx8[i % 8], __uint_as_float(sraw[i]));
+                const float mraw = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                                         fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
+                const float mx = mraw == -FLT_MAX ? -FLT_MAX : mraw * sl;
+                float alpha = 1.f;
+                bool rescale = false;
+                if (mx > m + kRescale || j == 0) {  // lazy correction (see prefill_tc_kernel)
+                    alpha = ex2(m - mx);
+                    rescale = j > 0;
+                    m = mx;
+                    l *= alpha;
+                }
+                // p = 2^(s * sl - m) in one FFMA + MUFU; masked entries (-FLT_MAX * sl) underflow to 0
+                uint32_t pw[kT / 2];
+                float l8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+                for (int i = 0; i < kT / 2; ++i) {
+                    const float p0 = ex2(fmaf(__uint_as_float(sraw[2 * i]), sl, -m));
+                    const float p1 = ex2(fmaf(__uint_as_float(sraw[2 * i + 1]), sl, -m));
+                    l8[i % 8] += p0 + p1;
+                    pw[i] = ptx::pack_bf16x2(p0, p1);
+                }
+                l += ((l8[0] + l8[1]) + (l8[2] + l8[3])) + ((l8[4] + l8[5]) + (l8[6] + l8[7]));
+                if (rescale) {  // PV_t(j-1) completed before S_t(j) was signalled
 #pragma unroll 1
-        for (int c = 0; c < kHD; c += 16) {
-            uint32_t v[16];
-            ptx::tmem_ld_x16(t_o + lane_off + c, v);
-            ptx::tmem_ld_wait();
-            uint32_t o[8];
+                    for (int c = 0; c < kHD; c += 16) {
+                        uint32_t v[16];
+                        ptx::tmem_ld_x16(t_o + lane_off + c, v);
+                        ptx::tmem_ld_wait();
 #pragma unroll
-            for (int i = 0; i < 8; ++i)
-                o[i] = ptx::pack_bf16x2(__uint_as_float(v[2 * i]) * inv, __uint_as_float(v[2 * i + 1]) * inv);
-            if (qrow < P) {
-                ptx::st_global_v4(orow + c, o[0], o[1], o[2], o[3]);
-                ptx::st_global_v4(orow + c + 8, o[4], o[5], o[6], o[7]);
+                        for (int i = 0; i < 16; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * alpha);
+                        tmem_st_x16(t_o + lane_off + c, v);
+                    }
+                    tmem_st_wait();
+                }
+#pragma unroll
+                for (int c = 0; c < kT / 8; ++c) {  // 16-byte chunks of 8 keys, 128B swizzle
+                    const int box = c / 8, ch = c % 8;
+                    sts128(pbase + box * kBox + ((ch ^ (r % 8)) * 16), pw[4 * c], pw[4 * c + 1], pw[4 * c + 2],
+                           pw[4 * c + 3]);
+                }
+                fence_async_smem();
+                ptx::tc_fence_before();
+                ptx::mbar_arrive(&p_full[t]);
             }
+            ptx::mbar_wait(&o_done[t], oc & 1);
+            ++oc;
+            ptx::tc_fence_after();
+            const float inv = l > 0.f ? 1.f / l : 0.f;
+            bf16* orow = out + static_cast<long long>(it.row0 + qrow) * d + it.h * kHD;
+#pragma unroll 1
+            for (int c = 0; c < kHD; c += 16) {
+                uint32_t v[16];
+                ptx::tmem_ld_x16(t_o + lane_off + c, v);
+                ptx::tmem_ld_wait();
+                uint32_t o[8];
+#pragma unroll
+                for (int i = 0; i < 8; ++i)
+                    o[i] = ptx::pack_bf16x2(__uint_as_float(v[2 * i]) * inv, __uint_as_float(v[2 * i + 1]) * inv);
+                if (qrow < P) {
+                    ptx::st_global_v4(orow + c, o[0], o[1], o[2], o[3]);
+                    ptx::st_global_v4(orow + c + 8, o[4], o[5], o[6], o[7]);
+                }
+            }
+            ptx::tc_fence_before();
+            ptx::mbar_arrive(&o_free[t]);  // O_t may be overwritten by the next item's first PV
         }
-        ptx::tc_fence_before();
     }
     __syncthreads();
     if (warp == 9) {
@@ -583,8 +643,16 @@ bool prefill_attention_tc(const bf16* qkv, long long rows, bf16* out, const int*
     if (enabled == 1) {  // one query tile per CTA (single softmax group)
         prefill_tc_kernel<<<dim3(n_qt, H, n_req), kThreads, Smem::bytes, st>>>(tm, out, cu, H, scale, lbo, sbo);
     } else {  // pairs of query tiles, two softmax groups (default)
-        prefill_tc2_kernel<<<dim3((n_qt + 1) / 2, H, n_req), kThreads2, Smem2::bytes, st>>>(tm, out, cu, H, scale,
-                                                                                              lbo, sbo);
+        static const int sms = [] {
+            int dev = 0, n = 148;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+            return n;
+        }();
+        const int n_pairs = (n_qt + 1) / 2;
+        const long long items = static_cast<long long>(n_pairs) * H * n_req;
+        const int grid = static_cast<int>(std::min<long long>(items, sms));
+        prefill_tc2_kernel<<<grid, kThreads2, Smem2::bytes, st>>>(tm, out, cu, n_req, n_pairs, H, scale, lbo, sbo);
     }
     return true;
 }
