@@ -38,6 +38,9 @@ def main():
     refs = np.array([[0, 1, 2, 3], [4, 5, 6, 7]], np.int32)
     kernels.decode_attention(q, pool, pool, refs, np.array([4, 3], np.int32), np.array([60, 40], np.int32), 2,
                              True, 2)
+    # persistent two-tile prefill attention: several items per CTA, odd tile count
+    qkv = kernels.f32_to_bf16_bits(rng.uniform(-1, 1, (2 * 640, 3 * 256)))
+    kernels.prefill_attention(qkv, 2, 640, 2)
     # session-2 paths: chunked offloaded prefill (store stream), OPT layers
     # (LayerNorm, bias / residual epilogues), head-sharded TP over the
     # in-process group (all-gather + fp32 all-reduce), flash prefill attention
