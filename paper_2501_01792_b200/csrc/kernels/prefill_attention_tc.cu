@@ -70,6 +70,30 @@ __device__ __forceinline__ float ex2(float x) {
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
 }
+// packed fp32x2 FMA / add (FFMA2 / FADD2 on sm_100): half the issue slots of
+// the softmax's per-element scale-and-subtract and row-sum work
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+    uint64_t d;
+    asm("{\n\t.reg .b64 ra, rb, rc;\n\t"
+        "mov.b64 ra, {%1, %2};\n\tmov.b64 rb, {%3, %4};\n\tmov.b64 rc, {%5, %6};\n\t"
+        "fma.rn.f32x2 %0, ra, rb, rc;\n\t}"
+        : "=l"(d)
+        : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+    float2 r;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(d));
+    return r;
+}
+__device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
+    uint64_t d;
+    asm("{\n\t.reg .b64 ra, rb;\n\t"
+        "mov.b64 ra, {%1, %2};\n\tmov.b64 rb, {%3, %4};\n\t"
+        "add.rn.f32x2 %0, ra, rb;\n\t}"
+        : "=l"(d)
+        : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+    float2 r;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(d));
+    return r;
+}
 __device__ __forceinline__ void sts128(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
     asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
 }
@@ -551,15 +575,18 @@ __global__ void __launch_bounds__(kThreads2, 1)
                 }
                 // p = 2^(s * sl - m) in one FFMA + MUFU; masked entries (-FLT_MAX * sl) underflow to 0
                 uint32_t pw[kT / 2];
-                float l8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+                float2 l4[4] = {{0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}};
+                const float2 sl2 = make_float2(sl, sl), nm2 = make_float2(-m, -m);
 #pragma unroll
                 for (int i = 0; i < kT / 2; ++i) {
-                    const float p0 = ex2(fmaf(__uint_as_float(sraw[2 * i]), sl, -m));
-                    const float p1 = ex2(fmaf(__uint_as_float(sraw[2 * i + 1]), sl, -m));
-                    l8[i % 8] += p0 + p1;
-                    pw[i] = ptx::pack_bf16x2(p0, p1);
+                    const float2 y = ffma2(make_float2(__uint_as_float(sraw[2 * i]), __uint_as_float(sraw[2 * i + 1])),
+                                           sl2, nm2);
+                    const float2 pp = make_float2(ex2(y.x), ex2(y.y));
+                    l4[i % 4] = fadd2(l4[i % 4], pp);
+                    pw[i] = ptx::pack_bf16x2(pp.x, pp.y);
                 }
-                l += ((l8[0] + l8[1]) + (l8[2] + l8[3])) + ((l8[4] + l8[5]) + (l8[6] + l8[7]));
+                const float2 ls = fadd2(fadd2(l4[0], l4[1]), fadd2(l4[2], l4[3]));
+                l += ls.x + ls.y;
                 if (rescale) {  // PV_t(j-1) completed before S_t(j) was signalled
 #pragma unroll 1
                     for (int c = 0; c < kHD; c += 16) {
