@@ -20,9 +20,11 @@ using hc_input_error = hc::InputError;
 #define HC_CUDA(expr)                                                                                  \
     do {                                                                                               \
         cudaError_t _e = (expr);                                                                       \
-        if (_e != cudaSuccess)                                                                         \
+        if (_e != cudaSuccess) {                                                                       \
+            (void)cudaGetLastError(); /* reported here: do not resurface it at the next check */      \
             throw hc::CudaError(std::string(#expr) + ": " + cudaGetErrorString(_e) + " @" __FILE__ ":" + \
                                 std::to_string(__LINE__));                                             \
+        }                                                                                              \
     } while (0)
 
 template <class F>

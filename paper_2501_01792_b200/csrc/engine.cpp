@@ -125,6 +125,10 @@ struct Engine::Impl {
         wpre{};
     bool w_prefetched = false;  // wbuf[0/1] hold layers 0/1 for the next decode step
     bool pools_filled = false;
+    bool configured = false;  // false while (or after a failed) configure_cache: pools may be missing
+    void require_configured() const {
+        if (!configured) throw ConfigError("Engine: cache pools are not configured (configure_cache failed)");
+    }
     bf16* tr_kv = nullptr;  // [max_batch * max_blocks] KV blocks for token-recompute prefixes
     void ensure_tr() {
         if (!tr_kv) {
@@ -268,6 +272,8 @@ struct Engine::Impl {
     float* ensure_red(size_t elems) {
         if (elems > red_elems) {
             if (red) HC_CUDA(cudaFree(red));
+            red = nullptr;  // stays null if the new allocation fails
+            red_elems = 0;
             red = dalloc<float>(elems);
             red_elems = elems;
         }
@@ -535,6 +541,7 @@ void Engine::configure_cache(const PoolCaps& caps, bool kv_on_gpu, CacheMode mod
     if (mode == CacheMode::TokenRecompute && m.tpn > 1)
         throw ConfigError("Engine: the token-recompute baseline runs without tensor parallelism");
     HC_CUDA(cudaDeviceSynchronize());
+    m.configured = false;
     m.clear_graphs();
     for (bf16** p : {&m.kv_gpu, &m.act_gpu, &m.kvr, &m.kv_stage[0], &m.kv_stage[1], &m.act_stage[0], &m.act_stage[1]}) {
         if (*p) cudaFree(*p);
@@ -599,6 +606,7 @@ void Engine::configure_cache(const PoolCaps& caps, bool kv_on_gpu, CacheMode mod
     }
     m.pools_filled = false;
     HC_CUDA(cudaDeviceSynchronize());
+    m.configured = true;
 }
 
 void Engine::forward_trace(const std::vector<int>& ids, uint16_t* layer_inputs, uint16_t* k, uint16_t* v,
@@ -739,6 +747,7 @@ void gemm_rows(int epi, const bf16* A, int M, int K, const bf16* W, int N, void*
 void Engine::prefill(const std::vector<std::string>& ids, const std::vector<std::vector<int>>& prompts) {
     Impl& m = *impl_;
     HC_CUDA(cudaSetDevice(opt_.device));
+    m.require_configured();
     m.w_prefetched = false;  // the prefill streams weights through the same slots
     if (ids.size() != prompts.size()) throw InputError("prefill: ids and prompts differ in length");
     {
@@ -954,6 +963,7 @@ void Engine::prefill(const std::vector<std::string>& ids, const std::vector<std:
 
 void Engine::admit_synthetic(const std::vector<std::string>& ids, const std::vector<int>& prompt_lens, uint64_t seed) {
     Impl& m = *impl_;
+    m.require_configured();
     if (ids.size() != prompt_lens.size()) throw InputError("admit_synthetic: ids and lengths differ");
     for (size_t r = 0; r < ids.size(); ++r) {
         if (prompt_lens[r] > m.max_seq) throw InputError("embed: sequence longer than max_seq");
@@ -1001,6 +1011,7 @@ void Engine::decode_step(const std::vector<std::string>& ids, const int* tokens,
                          int* argmax_out) {
     Impl& m = *impl_;
     HC_CUDA(cudaSetDevice(opt_.device));  // the calling thread may differ from the constructing one
+    m.require_configured();
     const int n = static_cast<int>(ids.size());
     if (n == 0) return;
     if (n > m.B) throw InputError("decode_step: batch larger than max_batch");
@@ -1474,6 +1485,7 @@ void Engine::read_weights(int layer, uint16_t* out) {
 
 void Engine::read_block(BlockKind kind, Location loc, int pbn, int layer, uint16_t* out) {
     Impl& m = *impl_;
+    m.require_configured();
     if (layer < 0 || layer >= m.L) throw InputError("read_block: layer out of range");
     const bool kv = kind == BlockKind::KV;
     const long cap = kv ? (loc == Location::GpuMem ? m.kv_gpu_cap : m.kv_host_cap)

@@ -673,3 +673,26 @@ def test_engine_empty_prompt_and_partial_batches(native):
             assert rel(f64(res["x"][i]), ref) <= TOL, (step, rid)
     for rid, s in seqs.items():
         assert eng.cache.context_len(rid) == len(s)
+
+
+def test_engine_failed_configure_cache_is_recoverable(native):
+    """A configure_cache whose pools cannot be allocated (here: a KV/gpu pool
+    far beyond HBM) raises, leaves the engine refusing work with ConfigError
+    instead of touching missing pools, and a later configure_cache with sane
+    capacities restores a working engine."""
+    from paper_2501_01792_b200 import ConfigError, HcError
+    from paper_2501_01792_b200.api import HostAllocation, PoolCaps
+    cfg = small_cfg(L=2, d=256, H=2, f=512, tpb=16)
+    w = oracle_weights(cfg)
+    eng = make_engine(cfg, w, max_batch=1, caps=PoolCaps(kv_host=8, act_host=8), allocation=HostAllocation(1, 1))
+    with pytest.raises(HcError):
+        eng.configure_cache(PoolCaps(kv_gpu=1 << 26), mode="kv_only", kv_on_gpu=True)  # ~ 40 TB of KV blocks
+    with pytest.raises(ConfigError):
+        eng.prefill(["a"], [[1, 2, 3]])
+    with pytest.raises(ConfigError):
+        eng.decode_step(["a"], [1])
+    eng.configure_cache(PoolCaps(kv_host=8, act_host=8), mode="hybrid", allocation=HostAllocation(1, 1))
+    prompt = [5, 6, 7, 8, 9]
+    eng.prefill(["a"], [prompt])
+    res = eng.decode_step(["a"], [11], want_x=True)
+    assert rel(f64(res["x"][0]), O.forward_prompt(prompt + [11], w).output[-1]) <= TOL
