@@ -102,6 +102,13 @@ def dist_setup(args):
         # HC_DIST_BACKEND=gloo + fewer GPUs than ranks: a plumbing smoke test of
         # the multi-rank path with several ranks sharing one device
         backend = os.environ.get("HC_DIST_BACKEND") or ("nccl" if torch.cuda.is_available() else "gloo")
+        local_world = int(os.environ.get("LOCAL_WORLD_SIZE", str(world)))
+        if backend == "nccl" and local_world > torch.cuda.device_count():
+            # NCCL refuses two ranks on one device: fall back to gloo for the
+            # barrier / max-over-ranks plumbing (timing stays on CUDA events)
+            print(f"bench: {local_world} ranks share {torch.cuda.device_count()} GPU(s); using gloo",
+                  file=sys.stderr)
+            backend = "gloo"
         if torch.cuda.is_available():
             local = local % torch.cuda.device_count()
             torch.cuda.set_device(local)
@@ -270,6 +277,7 @@ def cpu_reference_sample(cfg, prompt: int, ratio: float, threads: int):
     n_act = int(round(ratio * prompt))
     if R.available():
         kind = "reference"
+        threads = R.set_threads(threads)  # torchrun exports OMP_NUM_THREADS=1 before libgomp loads
         rw = R.RefWeights(1, d, H, f, V, tpb, 42, prompt + 2)
         rng = np.random.default_rng(0)
         a = rng.uniform(-0.1, 0.1, (max(n_act, 1), d))
@@ -302,7 +310,7 @@ def cpu_reference_sample(cfg, prompt: int, ratio: float, threads: int):
             O.generation_step(1, prompt, ck, cv, w)
             return time.perf_counter() - t0
     return kind, run, (f"1 request x 1 layer of one decode step at {cfg.name} width (d={d}), context {prompt}, "
-                       f"{n_act} ACT-recomputed tokens + generation_step; extrapolated x{cfg.num_layers} layers")
+                       f"{n_act} ACT-recomputed tokens + generation_step; extrapolated x{cfg.num_layers} layers"), threads
 
 
 def reference_arm(args, cfg, world, rank, dist):
@@ -312,7 +320,7 @@ def reference_arm(args, cfg, world, rank, dist):
     # the CPU path has no measured rates to plan with: it runs the paper's KV:ACT 2:1
     # unless --ratio is given
     r_cpu = args.ratio if args.ratio >= 0 else 1.0 / 3.0
-    kind, run, sample = cpu_reference_sample(cfg, args.prompt, r_cpu, threads)
+    kind, run, sample, threads = cpu_reference_sample(cfg, args.prompt, r_cpu, threads)
     for _ in range(args.warmup):
         run()
     ts = [run() for _ in range(args.steps)]
@@ -784,7 +792,7 @@ def our_arm(args, cfg, world, rank, local, dist):
             if _ALL_CPUS:  # the CPU reference gets every host core back
                 os.sched_setaffinity(0, _ALL_CPUS)
             threads = os.cpu_count() or 1
-            kind, run, sample = cpu_reference_sample(cfg, P, r, threads)
+            kind, run, sample, threads = cpu_reference_sample(cfg, P, r, threads)
             run()  # warm
             t = statistics.mean([run() for _ in range(2)])
             cpu = {"value": 1.0 / (L * t), "unit": "tokens/s", "cores": threads, "kind": kind, "sample": sample}
@@ -1019,6 +1027,7 @@ def config1_e2e(local, cpu_threads, B=4, P=128, G=32):
         sys.path.insert(0, os.path.join(ROOT, "oracle"))
         import ref_lib as R  # noqa: E402  (CPU baseline only)
         if R.available():
+            cpu_threads = R.set_threads(cpu_threads)
             rw = R.RefWeights(12, 768, 12, 3072, 50272, tpb, 42, P + G + 1)
             emb = rw.get(0)
             t0 = time.perf_counter()

@@ -28,6 +28,11 @@ def available() -> bool:
 _lib = None
 
 
+def set_threads(n: int) -> int:
+    """OpenMP threads of the reference library (0 = query); returns the count in effect."""
+    return int(lib().ref_set_threads(int(n)))
+
+
 def lib():
     global _lib
     if _lib is None:
@@ -35,6 +40,8 @@ def lib():
             raise FileNotFoundError(f"{LIB_PATH} missing: run `make -C oracle` where /root/reference exists")
         L = C.CDLL(LIB_PATH)
         L.ref_last_error.restype = C.c_char_p
+        L.ref_set_threads.argtypes = [C.c_int]
+        L.ref_set_threads.restype = C.c_int
         L.ref_weights_new.argtypes = [C.c_int] * 6 + [C.c_uint64, C.c_int, C.POINTER(C.c_void_p)]
         L.ref_weights_free.argtypes = [C.c_void_p]
         L.ref_weights_shape.argtypes = [C.c_void_p, C.c_int, C.c_int, _ip, _ip]

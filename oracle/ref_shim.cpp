@@ -21,6 +21,8 @@
 //   ref_simulate           -> simulate                      sim.cpp:134-633
 //
 // Status codes: 0 ok, 1 InputError, 2 CapacityError, 3 ConfigError, 4 other.
+#include <omp.h>
+
 #include <cstdint>
 #include <cstring>
 #include <memory>
@@ -444,4 +446,12 @@ int ref_simulate(int layers, int d, int heads, int ffn, int vocab, int tpb, cons
         std::memcpy(out6, v, sizeof v);
     });
 }
+// OpenMP threads of the reference's parallel loops (matrix.cpp:28,
+// decoder.cpp:58); returns the count now in effect. Overrides an
+// OMP_NUM_THREADS read at load time (torchrun sets it to 1).
+int ref_set_threads(int n) {
+    if (n > 0) omp_set_num_threads(n);
+    return omp_get_max_threads();
+}
+
 }  // extern "C"

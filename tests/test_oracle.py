@@ -243,3 +243,17 @@ def test_reference_acceptance_suite():
     assert len(lines) == 11
     failed = [l for l in lines if l.startswith("FAIL")]
     assert len(failed) == 1 and "packer" in failed[0], failed
+
+
+def test_reference_library_thread_count():
+    """The reference library's OpenMP threads are set explicitly (torchrun
+    exports OMP_NUM_THREADS=1 before libgomp loads; the CPU baseline must still
+    use every host core)."""
+    import ref_lib as R
+    if not R.available():
+        pytest.skip("oracle/_ref not built")
+    before = R.set_threads(0)
+    try:
+        assert R.set_threads(2) == 2
+    finally:
+        R.set_threads(before)
