@@ -52,6 +52,12 @@ def parse():
     p.add_argument("--tp-emulate", type=int, default=0,
                    help="time ONE rank of an N-way head-sharded group on this single GPU (collectives skipped, "
                         "NVLink time modelled) and print a projection line instead of the bench line")
+    p.add_argument("--no-share-weights", action="store_true",
+                   help="N>1: every rank streams whole weight layers over its own host link (default: the ranks "
+                        "share ONE weight stream — 1/N of every layer per link + an NVLink all-gather)")
+    p.add_argument("--share-emulate", type=int, default=0,
+                   help="time ONE rank of N batch-partitioned ranks sharing the weight stream on this single GPU "
+                        "(all-gather skipped, NVLink time modelled) and print a projection line")
     p.add_argument("--prompt", type=int, default=1024)
     p.add_argument("--gen", type=int, default=256, help="generation length of the workload (config)")
     p.add_argument("--ratio", type=float, default=None,
@@ -515,7 +521,7 @@ def run_prefill(eng, cfg, ids, P, rank, tflops_sust, link_gbs):
             "launches": int(st["launches"])}
 
 
-def calibrate_planner(eng, cfg, link_gbs, caps_act_rows, workload_tokens, act_gpu=0, tpn=1):
+def calibrate_planner(eng, cfg, link_gbs, caps_act_rows, workload_tokens, act_gpu=0, tpn=1, wsn=1):
     """North-star (5): measured recompute-GEMM and host-link samples ->
     bundle_from_samples (timing.cpp:172-183) -> plan_host_allocation
     (plan.cpp:106-152) over a WORKLOAD-sized host budget, as the reference's
@@ -532,6 +538,8 @@ def calibrate_planner(eng, cfg, link_gbs, caps_act_rows, workload_tokens, act_gp
         bundle.t_load_w /= tpn
         bundle.s_weight_layer //= tpn
         bundle.s_weight_total //= tpn
+    if wsn > 1:  # ranks sharing the weight stream: each link carries 1/N of every layer
+        bundle.t_load_w /= wsn
     mem = api.budget_for(0.0, cfg, bundle)
     if tpn > 1:
         mem.s_kv_block /= tpn
@@ -567,6 +575,24 @@ def tp_group(args, world, rank, local, dist):
     return None, 1
 
 
+def weight_share_group(args, world, rank, local, dist):
+    """Batch-partitioned ranks sharing one weight stream (Engine(weight_share=)):
+    an NCCL group over the torchrun ranks when every rank has its own GPU
+    (NVLink all-gather); --share-emulate N: one rank's timing stand-in."""
+    from paper_2501_01792_b200 import api
+    if args.share_emulate > 1:
+        return api.TensorParallel.emulated(0, args.share_emulate), args.share_emulate
+    if world > 1 and not args.no_share_weights and args.tp <= 1:
+        import torch
+        local_world = int(os.environ.get("LOCAL_WORLD_SIZE", str(world)))
+        if torch.cuda.device_count() < local_world or local_world != world:
+            return None, 1  # ranks share a GPU (plumbing smoke test) or span nodes: whole-layer streams
+        obj = [api.TensorParallel.nccl_unique_ids() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        return api.TensorParallel.nccl(obj[0], rank, world, local), world
+    return None, 1
+
+
 def our_arm(args, cfg, world, rank, local, dist):
     from paper_2501_01792_b200 import api, kernels
     if kernels.device_count() == 0:
@@ -574,6 +600,9 @@ def our_arm(args, cfg, world, rank, local, dist):
     hbm_peak, tflops_sust, tflops_burst, peak_src = measured_peaks()
     numa_node = bind_numa(local)
     tp, tpn = tp_group(args, world, rank, local, dist)
+    ws, wsn = weight_share_group(args, world, rank, local, dist) if tp is None else (None, 1)
+    if args.share_emulate > 1:
+        args.no_sweep = True
     if tp is not None:  # heads are sharded, requests are not: every rank serves the global batch
         args.no_sweep = True
         B = args.global_batch or args.batch or 128
@@ -595,7 +624,7 @@ def our_arm(args, cfg, world, rank, local, dist):
     t_setup = time.time()
     eng = api.Engine(cfg, seed=42, max_seq=max_seq, rescale=True, max_batch=B, weights_on_device=False,
                      caps=caps, host_layers=Lp, weight_layers=Lw, mode=mode, allocation=alloc, device=local,
-                     arch=args.arch, tp=tp)
+                     arch=args.arch, tp=tp, weight_share=ws)
     ids = [f"g{0 if tp else rank}r{i}" for i in range(B)]
     # host-link peak: a large pinned H2D copy on the engine's copy stream
     tpb = cfg.tokens_per_block
@@ -607,7 +636,8 @@ def our_arm(args, cfg, world, rank, local, dist):
     planner = None
     if link_gbs and caps.act_host:
         try:
-            planner = calibrate_planner(eng, cfg, link_gbs, caps.act_host * tpb, B * (P + args.gen), tpn=tpn)
+            planner = calibrate_planner(eng, cfg, link_gbs, caps.act_host * tpb, B * (P + args.gen), tpn=tpn,
+                                        wsn=wsn)
         except Exception as e:  # planner failure must not kill the bench line
             planner = {"error": str(e)}
     if args.ratio < 0 and planner and "planned_r" in planner:
@@ -763,6 +793,24 @@ def our_arm(args, cfg, world, rank, local, dist):
         except Exception as e:
             extra["hbm_tiered"] = {"error": str(e)}
 
+    ws_info = None
+    if ws is not None:
+        # per layer each rank receives the other ranks' (N-1)/N of the layer over
+        # NVLink, on the gather stream (overlaps the copy stream's KV / ACT blocks)
+        ag = (wsn - 1) / wsn * w_layer
+        ws_info = {"size": wsn, "mode": "emulated" if args.share_emulate > 1 else "nccl",
+                   "rank_h2d_gb_per_step": h2d_step / 1e9, "rank_weight_h2d_gb_per_step": L * w_layer / wsn / 1e9,
+                   "nvlink_allgather_bytes_per_layer": ag}
+        if args.share_emulate > 1:
+            busbw = 650e9  # assumed NCCL all-gather bus bandwidth on NVLink 5 (900 GB/s/direction nominal)
+            t_ag = L * ag / busbw
+            t_proj = max(ms_per_step / 1e3, t_ag + (ag / busbw))  # + one layer's gather exposed at the start
+            ws_info.update({"note": "ONE of N batch-partitioned ranks timed on one GPU with 1/N of every weight "
+                                    "layer streamed over its host link; the all-gather is skipped and NVLink time "
+                                    "modelled at an assumed 650 GB/s (own stream, overlapped)",
+                            "rank_step_ms_measured": ms_per_step, "nvlink_allgather_ms_per_step": t_ag * 1e3,
+                            "projected_step_ms": t_proj * 1e3, "projected_tokens_per_s_per_gpu": B / t_proj,
+                            "projected_tokens_per_s_whole_job": wsn * B / t_proj})
     tp_info = None
     if tp is not None:
         # per layer: ACT all-gather (gather stream, overlaps the link and compute)
@@ -829,7 +877,14 @@ def our_arm(args, cfg, world, rank, local, dist):
             "prefill": prefill,
             "generation_e2e": gen,
             "tensor_parallel": tp_info,
+            "weight_share": ws_info,
         }
+        if ws is not None:
+            res["config"]["parallelism"] = (f"batch-partitioned x{max(world, wsn)}, one weight stream shared over "
+                                            f"NVLink (1/{wsn} of every layer per host link + all-gather)")
+            if args.share_emulate > 1:
+                res["config"]["parallelism"] += " (EMULATED: one rank on one GPU, all-gather skipped)"
+                res["metric"] = METRIC + " [share-emulate: single-rank timing, NOT a whole-job measurement]"
         if tp is not None:
             res["scaling"] = "strong"
             res["config"]["parallelism"] = f"head-sharded tensor parallel x{tpn}" + (

@@ -150,6 +150,10 @@ typedef struct hc_engine_options {
                               * biases, residuals, final LN; the ACT cache holds LN1(x)). Seeded engines
                               * draw the OPT extras; f64 engines take them from _create_from_f64_opt. */
     void* tp;                /* NULL, or a tensor-parallel rank handle (hc_tp_*): head-sharded variant */
+    void* weight_share;      /* NULL, or a group handle (hc_tp_*) of batch-partitioned ranks that share
+                              * ONE weight stream: each rank copies 1/N of every layer over its own host
+                              * link and an NVLink all-gather completes it (streamed weights only; not
+                              * with tp). Every rank must issue the same decode_step sequence. */
 } hc_engine_options;
 
 /* ------------------------------------------ tensor parallelism (optional) ---

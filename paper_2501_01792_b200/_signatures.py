@@ -24,7 +24,7 @@ class EngineOptionsC(C.Structure):
                 ("mode", C.c_int), ("alloc_act_host", C.c_long), ("alloc_kv_host", C.c_long),
                 ("scaled", C.c_int), ("max_prefill_tokens", C.c_int), ("device", C.c_int),
                 ("weight_layers", C.c_int), ("recompute_ratio", C.c_double), ("arch", C.c_int),
-                ("tp", C.c_void_p)]
+                ("tp", C.c_void_p), ("weight_share", C.c_void_p)]
 
 
 cfgp = C.POINTER(ModelConfigC)

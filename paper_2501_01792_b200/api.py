@@ -455,9 +455,11 @@ def _ids(ids: Sequence[str]):
 
 
 class TensorParallel:
-    """Rank handle of the optional head-sharded variant (csrc/tp.hpp): rank g
-    of N owns heads [gH/N, (g+1)H/N) and the ACT/host blocks with pbn % N == g.
-    Every rank's Engine gets the same request ids and tokens."""
+    """Rank handle of a collective group (csrc/tp.hpp). As `Engine(tp=...)`:
+    the optional head-sharded variant — rank g of N owns heads
+    [gH/N, (g+1)H/N) and the ACT/host blocks with pbn % N == g; every rank's
+    Engine gets the same request ids and tokens. As `Engine(weight_share=...)`:
+    batch-partitioned ranks sharing one weight stream."""
 
     def __init__(self, handle, owner=None, is_group=False, rank=0, size=1):
         self._h = handle
@@ -537,7 +539,13 @@ class Engine:
                  caps: Optional[PoolCaps] = None, kv_on_gpu: bool = False, host_layers: int = 0,
                  mode: str = "hybrid", allocation: Optional[HostAllocation] = None, scaled: bool = True,
                  max_prefill_tokens: int = 0, device: int = 0, weight_layers: int = 0,
-                 recompute_ratio: float = 0.0, arch: str = "reference", tp: Optional[TensorParallel] = None):
+                 recompute_ratio: float = 0.0, arch: str = "reference", tp: Optional[TensorParallel] = None,
+                 weight_share: Optional[TensorParallel] = None):
+        """tp: head-sharded tensor parallelism. weight_share: a group (same
+        constructors as tp) of batch-partitioned ranks streaming ONE copy of the
+        weights between them — each rank's host link carries 1/N of every
+        layer, an NVLink all-gather completes it (streamed weights only; every
+        rank must issue the same decode_step sequence)."""
         self.cfg = ModelConfig(**cfg.__dict__).validate()
         caps = caps or PoolCaps()
         alloc = allocation or HostAllocation(1, 1)
@@ -549,8 +557,10 @@ class Engine:
         self.opts = EngineOptionsC(max_batch, max_seq, int(weights_on_device), caps.kv_host, caps.kv_gpu,
                                    caps.act_host, caps.act_gpu, int(kv_on_gpu), host_layers, MODES[mode],
                                    alloc.act_host, alloc.kv_host, int(scaled), max_prefill_tokens, device,
-                                   weight_layers, recompute_ratio, ARCHS[arch], tp._h if tp else None)
+                                   weight_layers, recompute_ratio, ARCHS[arch], tp._h if tp else None,
+                                   weight_share._h if weight_share else None)
         self._tp = tp
+        self._weight_share = weight_share
         self.max_batch = max_batch
         h = C.c_void_p()
         c = self.cfg.to_c()

@@ -83,6 +83,7 @@ EngineOptions opts_of(const hc_engine_options* o) {
     e.recompute_ratio = o->recompute_ratio;
     e.arch = o->arch;
     e.tp = static_cast<TpGroup*>(o->tp);
+    e.weight_share = static_cast<TpGroup*>(o->weight_share);
     return e;
 }
 

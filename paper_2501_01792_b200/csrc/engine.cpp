@@ -124,6 +124,12 @@ struct Engine::Impl {
     cudaEvent_t loaded[2]{}, consumed[2]{}, stored[2]{}, h2d_act[2]{}, gathered[2]{}, ev0{}, ev1{}, tg0{}, tg1{},
         wpre{};
     bool w_prefetched = false;  // wbuf[0/1] hold layers 0/1 for the next decode step
+    // shared weight stream (EngineOptions::weight_share): this rank's slice of
+    // wsS elements at wsr * wsS; wbuf slots hold wsn * wsS >= LE elements
+    TpGroup* ws = nullptr;
+    int wsn = 1, wsr = 0;
+    size_t wsS = 0;
+    cudaEvent_t w_h2d[2]{}, w_gath[2]{};
     bool pools_filled = false;
     bool configured = false;  // false while (or after a failed) configure_cache: pools may be missing
     void require_configured() const {
@@ -436,6 +442,13 @@ void Engine::init(const ModelConfig& c, int w_max_seq, const uint16_t* emb, cons
     m.tp = opt_.tp;
     m.tpn = m.tp ? m.tp->size() : 1;
     m.tpr = m.tp ? m.tp->rank() : 0;
+    if (opt_.weight_share && opt_.weight_share->size() > 1) {
+        if (opt_.weights_on_device) throw ConfigError("weight_share: needs streamed weights (weights_on_device = 0)");
+        if (m.tp) throw ConfigError("weight_share: not combined with tensor parallelism (heads already shard weights)");
+        m.ws = opt_.weight_share;
+        m.wsn = m.ws->size();
+        m.wsr = m.ws->rank();
+    }
     if (m.H % m.tpn || m.f % m.tpn) throw InputError("tensor parallel size must divide num_heads and ffn_dim");
     m.Hg = m.H / m.tpn;
     m.dg = m.d / m.tpn;
@@ -445,6 +458,8 @@ void Engine::init(const ModelConfig& c, int w_max_seq, const uint16_t* emb, cons
     m.offF = LayerOffsets::of(cfg_, m.arch, 1);
     m.LE = m.off.total;
     m.LEF = m.offF.total;
+    m.wsS = (m.LE + m.wsn - 1) / m.wsn;
+    m.wsS = (m.wsS + 63) / 64 * 64;  // 128-byte aligned slices
     m.kvb = static_cast<size_t>(2) * m.dg * m.tpb;  // this rank's heads of a KV block
     m.actb = static_cast<size_t>(m.d) * m.tpb;
 
@@ -458,6 +473,8 @@ void Engine::init(const ModelConfig& c, int w_max_seq, const uint16_t* emb, cons
         HC_CUDA(cudaEventCreateWithFlags(&m.stored[i], cudaEventDisableTiming));
         HC_CUDA(cudaEventCreateWithFlags(&m.h2d_act[i], cudaEventDisableTiming));
         HC_CUDA(cudaEventCreateWithFlags(&m.gathered[i], cudaEventDisableTiming));
+        HC_CUDA(cudaEventCreateWithFlags(&m.w_h2d[i], cudaEventDisableTiming));
+        HC_CUDA(cudaEventCreateWithFlags(&m.w_gath[i], cudaEventDisableTiming));
     }
     HC_CUDA(cudaEventCreate(&m.ev0));
     HC_CUDA(cudaEventCreate(&m.ev1));
@@ -507,8 +524,8 @@ void Engine::init(const ModelConfig& c, int w_max_seq, const uint16_t* emb, cons
             else
                 fill_layer(ctx, l, m.h_w + static_cast<size_t>(l) * m.LE);
         }
-        m.wbuf[0] = dalloc<bf16>(m.LE);
-        m.wbuf[1] = dalloc<bf16>(m.LE);
+        m.wbuf[0] = dalloc<bf16>(m.wsn * m.wsS);  // >= LE (padded slices when the stream is shared)
+        m.wbuf[1] = dalloc<bf16>(m.wsn * m.wsS);
     }
     if (fill_layer && m.wfull) {
         HC_CUDA(cudaFree(m.wfull));
@@ -664,6 +681,8 @@ Engine::~Engine() {
         cudaEventDestroy(m.stored[i]);
         cudaEventDestroy(m.h2d_act[i]);
         cudaEventDestroy(m.gathered[i]);
+        cudaEventDestroy(m.w_h2d[i]);
+        cudaEventDestroy(m.w_gath[i]);
     }
     cudaEventDestroy(m.ev0);
     cudaEventDestroy(m.ev1);
@@ -1128,6 +1147,28 @@ void Engine::decode_step(const std::vector<std::string>& ids, const int* tokens,
     const bool prefetched = m.w_prefetched && !m.w_all;
     m.w_prefetched = false;
     bool capturing = false;  // enqueue() runs under stream capture (graph mode)
+    // one layer's weights into wbuf[slot] on the copy stream; with a shared
+    // weight stream only this rank's slice crosses its host link and an
+    // in-place all-gather on the gather stream (NVLink) completes the layer
+    // while the copy stream moves on to the layer's KV / ACT blocks
+    auto stream_weights = [&](int l, int slot, StepStats& st) {
+        const uint16_t* src = m.h_w + static_cast<size_t>(l % m.Lw) * m.LE;
+        if (m.wsn == 1) {
+            HC_CUDA(cudaMemcpyAsync(m.wbuf[slot], src, m.LE * 2, cudaMemcpyHostToDevice, s_copy_));
+            st.h2d_bytes += m.LE * 2.0;
+            return;
+        }
+        const size_t s0 = static_cast<size_t>(m.wsr) * m.wsS;
+        const size_t cnt = s0 < m.LE ? std::min(m.wsS, m.LE - s0) : 0;
+        if (cnt)
+            HC_CUDA(cudaMemcpyAsync(m.wbuf[slot] + s0, src + s0, cnt * 2, cudaMemcpyHostToDevice, s_copy_));
+        st.h2d_bytes += cnt * 2.0;
+        HC_CUDA(cudaEventRecord(m.w_h2d[slot], s_copy_));
+        HC_CUDA(cudaStreamWaitEvent(s_gather_, m.w_h2d[slot]));
+        m.ws->copy_channel()->all_gather(m.wbuf[slot] + s0, m.wbuf[slot], m.wsS, s_gather_);
+        HC_CUDA(cudaEventRecord(m.w_gath[slot], s_gather_));
+        HC_CUDA(cudaStreamWaitEvent(s_compute_, m.w_gath[slot]));
+    };
     // everything the step puts on the streams; outputs land in xo / lo / ao
     auto enqueue = [&](StepStats& st, uint16_t* xo, float* lo, int* ao) {
         HC_CUDA(cudaEventRecord(m.ev0, s_compute_));
@@ -1151,11 +1192,8 @@ void Engine::decode_step(const std::vector<std::string>& ids, const int* tokens,
                 // graph only waits on events it records itself)
                 HC_CUDA(cudaStreamWaitEvent(s_copy_, l >= 2 ? m.consumed[slot] : m.ev0));
                 m.span_begin(profile_, s_copy_, 3);
-                if (!m.w_all && !(prefetched && l < 2)) {  // layers 0/1 may have come with the previous step
-                    HC_CUDA(cudaMemcpyAsync(m.wbuf[slot], m.h_w + static_cast<size_t>(l % m.Lw) * m.LE, m.LE * 2,
-                                            cudaMemcpyHostToDevice, s_copy_));
-                    st.h2d_bytes += m.LE * 2.0;
-                }
+                if (!m.w_all && !(prefetched && l < 2))  // layers 0/1 may have come with the previous step
+                    stream_weights(l, slot, st);
                 const size_t lp = static_cast<size_t>(l % m.Lp);
                 bf16* own = m.act_stage[slot] + static_cast<size_t>(m.tpr) * m.act_cap_n * m.actb;
                 for (const Run& r : act_runs) {
@@ -1334,7 +1372,7 @@ void Engine::decode_step(const std::vector<std::string>& ids, const int* tokens,
 
     // CUDA graph of the step: its launch structure (sizes, copy runs, splits,
     // outputs) is the key; the data rides in the metadata block
-    const bool use_graph = graphs_ && !profile_ && !capture_inputs_ && m.tpn == 1;
+    const bool use_graph = graphs_ && !profile_ && !capture_inputs_ && m.tpn == 1 && m.wsn == 1;
     if (!use_graph) {
         enqueue(st, x_out, logits_out, argmax_out);
     } else {
@@ -1398,9 +1436,7 @@ void Engine::decode_step(const std::vector<std::string>& ids, const int* tokens,
     if (!m.w_all && stream_any) {
         for (int l = 0; l < std::min(2, m.L); ++l) {
             HC_CUDA(cudaStreamWaitEvent(s_copy_, m.consumed[l & 1]));
-            HC_CUDA(cudaMemcpyAsync(m.wbuf[l & 1], m.h_w + static_cast<size_t>(l % m.Lw) * m.LE, m.LE * 2,
-                                    cudaMemcpyHostToDevice, s_copy_));
-            st.h2d_bytes += m.LE * 2.0;
+            stream_weights(l, l & 1, st);
         }
         HC_CUDA(cudaEventRecord(m.wpre, s_copy_));
         HC_CUDA(cudaStreamWaitEvent(s_compute_, m.wpre));

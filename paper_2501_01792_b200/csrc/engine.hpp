@@ -55,6 +55,11 @@ struct EngineOptions {
     int device = 0;
     int arch = kArchReference;    // decoder layer variant (host/model.hpp); from the weights when given
     TpGroup* tp = nullptr;        // head-sharded tensor parallelism (tp.hpp); nullptr = one GPU holds all heads
+    // batch-partitioned ranks sharing ONE weight stream (streamed weights only):
+    // rank g of N copies 1/N of every layer over its own host link and an
+    // NVLink all-gather completes the layer, so each link carries 1/N of the
+    // weights; nullptr = every rank streams whole layers
+    TpGroup* weight_share = nullptr;
 };
 
 struct StepStats {

@@ -696,3 +696,56 @@ def test_engine_failed_configure_cache_is_recoverable(native):
     eng.prefill(["a"], [prompt])
     res = eng.decode_step(["a"], [11], want_x=True)
     assert rel(f64(res["x"][0]), O.forward_prompt(prompt + [11], w).output[-1]) <= TOL
+
+
+@pytest.mark.parametrize("n", [2, 3])
+def test_engine_shared_weight_stream_matches_oracle(native, n):
+    """Batch-partitioned ranks sharing ONE weight stream (Engine(weight_share=)):
+    each rank serves its own requests, copies 1/N of every layer's weights over
+    its host link and all-gathers the rest. Outputs equal the oracle, graph
+    replay is off, and each rank's weight bytes are 1/N of a full stream."""
+    from paper_2501_01792_b200.api import HostAllocation, PoolCaps, TensorParallel
+    cfg = small_cfg(L=3, d=256, H=2, f=512, tpb=8)
+    w = oracle_weights(cfg)
+    rng = np.random.default_rng(97 + n)
+    group = TensorParallel.local_group(n)
+    kw = dict(max_batch=2, caps=PoolCaps(kv_host=16, act_host=16, act_gpu=1), allocation=HostAllocation(1, 1),
+              mode="hybrid", weights_on_device=False)
+    engs = [make_engine(cfg, w, weight_share=group[r], **kw) for r in range(n)]
+    prompts = [[rng.integers(0, cfg.vocab_size, int(rng.integers(5, 30))).tolist() for _ in range(2)]
+               for _ in range(n)]
+    steps = [[rng.integers(0, cfg.vocab_size, 2).tolist() for _ in range(4)] for _ in range(n)]
+
+    def rank_fn(r):
+        def run():
+            ids = [f"r{r}_{i}" for i in range(2)]
+            engs[r].prefill(ids, prompts[r])
+            return [engs[r].decode_step(ids, t, want_x=True) for t in steps[r]], engs[r].last_stats()
+        return run
+
+    outs = _run_ranks([rank_fn(r) for r in range(n)])
+    for r in range(n):
+        seqs = [list(p) for p in prompts[r]]
+        for s, t in enumerate(steps[r]):
+            for b in range(2):
+                seqs[b].append(t[b])
+                ref = O.forward_prompt(seqs[b], w).output[-1]
+                assert rel(f64(outs[r][0][s]["x"][b]), ref) <= TOL, (r, s, b)
+    full_w = 2 * (4 * cfg.hidden_dim ** 2 + 2 * cfg.hidden_dim * cfg.ffn_dim) * cfg.num_layers
+    for r in range(n):
+        st = outs[r][1]
+        kv_act = st["h2d_bytes"] - full_w / n
+        assert -full_w * 0.05 <= kv_act < full_w, (r, st["h2d_bytes"], full_w / n)  # weights ~ 1/N of a stream
+
+
+def test_engine_shared_weight_stream_rejects_tp_and_resident(native):
+    from paper_2501_01792_b200 import ConfigError
+    from paper_2501_01792_b200.api import TensorParallel
+    cfg = small_cfg(L=1)
+    w = oracle_weights(cfg, max_seq=64)
+    g = TensorParallel.local_group(2)
+    with pytest.raises(ConfigError):
+        make_engine(cfg, w, weight_share=g[0], weights_on_device=True)
+    t = TensorParallel.local_group(2)
+    with pytest.raises(ConfigError):
+        make_engine(cfg, w, weight_share=g[0], tp=t[0], weights_on_device=False)
