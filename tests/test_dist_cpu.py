@@ -101,3 +101,19 @@ def test_config4_strong_split_covers_global_batch():
     b = bench.parse()
     assert b.model == "opt-30b" and b.scaling == "weak" and b.ratio == -1.0  # planner-chosen by default
     assert bench.per_rank_batch(b, 8, 7) == 128
+
+
+def test_weight_share_group_selection(monkeypatch):
+    """The shared weight stream needs one GPU per rank on one node: without
+    (ranks sharing a device, or --no-share-weights, or head-sharded TP) every
+    rank streams whole layers; world 1 never shares."""
+    sys.path.insert(0, ROOT)
+    import bench
+    sys.argv = ["bench.py"]
+    a = bench.parse()
+    assert bench.weight_share_group(a, 1, 0, 0, None) == (None, 1)
+    monkeypatch.setenv("LOCAL_WORLD_SIZE", "2")
+    assert bench.weight_share_group(a, 2, 0, 0, None) == (None, 1)  # no CUDA devices here: ranks share none
+    sys.argv = ["bench.py", "--no-share-weights"]
+    assert bench.weight_share_group(bench.parse(), 2, 0, 0, None) == (None, 1)
+    sys.argv = ["bench.py"]
