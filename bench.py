@@ -91,6 +91,7 @@ def per_rank_batch(args, world, rank):
     """Requests this rank owns: --batch per GPU (weak scaling), or an even
     split of --global-batch (strong scaling)."""
     if args.global_batch:
+        world = max(world, getattr(args, "share_emulate", 0))  # an emulated rank owns its 1/N slice
         base, extra = divmod(args.global_batch, world)
         return base + (1 if rank < extra else 0)
     return args.batch or 128
@@ -531,6 +532,8 @@ def calibrate_planner(eng, cfg, link_gbs, caps_act_rows, workload_tokens, act_gp
     blocks on a 196 GB host (CapacityError, plan.cpp:79)."""
     from paper_2501_01792_b200 import api
     ns = [n for n in (4096, 16384, 32768, 65536) if n <= caps_act_rows]
+    if len(ns) < 2:  # small per-rank batches (config 4 split 8 ways): smaller samples, still >= 2
+        ns = [n for n in (512, 1024, 2048, 4096, 8192) if n <= caps_act_rows][-3:]
     kv = [(float(n), eng.time_kv_gen(n, reps=3)) for n in ns]
     ld = [(float(n), eng.time_load_kv(n, reps=2)) for n in ns]
     bundle = api.bundle_from_samples(kv, ld, link_gbs * 1e9, cfg)
@@ -545,8 +548,17 @@ def calibrate_planner(eng, cfg, link_gbs, caps_act_rows, workload_tokens, act_gp
         mem.s_kv_block /= tpn
         mem.s_act_block /= tpn
     workload_blocks = workload_tokens / cfg.tokens_per_block
-    mem.m_host = mem.s_weight + workload_blocks * mem.s_kv_block * 0.9
-    alloc = api.plan_host_allocation(bundle, mem, cfg.tokens_per_block, act_gpu)
+    # small per-rank batches next to large weights (config 4 split 4-8 ways): the
+    # initial balanced blocks may not fit 0.9 x the workload (CapacityError,
+    # plan.cpp:79) — widen the budget until Alg. 1 has room, and say so
+    for factor in (0.9, 1.5, 3.0, 6.0, 12.0):
+        mem.m_host = mem.s_weight + workload_blocks * mem.s_kv_block * factor
+        try:
+            alloc = api.plan_host_allocation(bundle, mem, cfg.tokens_per_block, act_gpu)
+            break
+        except api.CapacityError:
+            if factor == 12.0:
+                raise
     r = alloc.act_host / max(alloc.act_host + alloc.kv_host, 1)
     return {"kv_gen_samples": kv, "load_kv_samples": ld,
             "t_kv_gen": {"slope_s_per_token": bundle.t_kv_gen.slope, "intercept_s": bundle.t_kv_gen.intercept,
@@ -554,7 +566,8 @@ def calibrate_planner(eng, cfg, link_gbs, caps_act_rows, workload_tokens, act_gp
             "t_load_kv": {"slope_s_per_token": bundle.t_load_kv.slope, "intercept_s": bundle.t_load_kv.intercept,
                           "r2": bundle.t_load_kv.r_squared},
             "t_load_w_s": bundle.t_load_w, "m_host": mem.m_host,
-            "m_host_source": "workload-sized: s_weight + 0.9 x B(P+G)/tpb x s_kv_block (test_sim.cpp:281-282)",
+            "m_host_source": f"workload-sized: s_weight + {factor} x B(P+G)/tpb x s_kv_block (test_sim.cpp:281-282 "
+                             "uses 0.9; widened only when Alg. 1 raises CapacityError)",
             "allocation": alloc.__dict__, "planned_r": r,
             "planned_t_pcie_s": api.planned_t_pcie(bundle, cfg.tokens_per_block, alloc),
             "planned_t_comp_s": api.planned_t_computation(bundle, cfg.tokens_per_block, alloc, act_gpu)}
