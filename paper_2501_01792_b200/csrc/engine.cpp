@@ -1078,6 +1078,7 @@ void Engine::decode_step(const std::vector<std::string>& ids, const int* tokens,
     }
     const int n_rc = rc_cu.back();
     if (n_rc) m.ensure_prefill(n_rc);
+    assigner_->check_batch_capacity(ids);  // all contexts grow, or none (no half-applied step)
     for (int b = 0; b < n; ++b) {
         const int rcb = (rc_cu[b + 1] - rc_cu[b]) / m.tpb;
         const TokenSlot s = assigner_->add_token(ids[b]);

@@ -197,6 +197,40 @@ long BlockAssigner::recompute_tokens(const std::string& id) const {
     return it == rc_.end() ? 0 : it->second;
 }
 
+void BlockAssigner::check_batch_capacity(const std::vector<std::string>& ids) const {
+    long act = 0, kv = 0;
+    for (const std::string& id : ids) {
+        if (mode_ == CacheMode::TokenRecompute) {  // the same rule as add_token, without the update
+            const auto it = rc_.find(id);
+            const long rc = it == rc_.end() ? 0 : it->second;
+            const double total = static_cast<double>(rc + cache_.table(id).context_len() + 1);
+            if (std::abs(static_cast<double>(rc + 1) / total - ratio_) <=
+                std::abs(static_cast<double>(rc) / total - ratio_))
+                continue;
+        }
+        const BlockTable& t = cache_.table(id);
+        if (t.context_len() % cache_.tokens_per_block() != 0) continue;
+        BlockKind kind = BlockKind::KV;
+        if (mode_ == CacheMode::Hybrid) {
+            const auto [a, k] = t.blocks_by_kind();
+            kind = next_block_kind(a, k, alloc_);
+        } else if (mode_ == CacheMode::ActOnly) {
+            kind = BlockKind::ACT;
+        }
+        ++(kind == BlockKind::ACT ? act : kv);
+    }
+    const long act_free =
+        cache_.free_blocks(BlockKind::ACT, Location::GpuMem) + cache_.free_blocks(BlockKind::ACT, Location::HostMem);
+    const long kv_free = cache_.free_blocks(BlockKind::KV, Location::HostMem) +
+                         (cache_.kv_on_gpu() ? cache_.free_blocks(BlockKind::KV, Location::GpuMem) : 0);
+    if (act > act_free)
+        throw CapacityError("append_block: ACT pools exhausted (the step needs " + std::to_string(act) + " blocks, " +
+                            std::to_string(act_free) + " free)");
+    if (kv > kv_free)
+        throw CapacityError("append_block: KV pools exhausted (the step needs " + std::to_string(kv) + " blocks, " +
+                            std::to_string(kv_free) + " free)");
+}
+
 TokenSlot BlockAssigner::add_token(const std::string& id) {
     TokenSlot s;
     if (mode_ == CacheMode::TokenRecompute) {

@@ -117,6 +117,11 @@ public:
     BlockAssigner(HybridCache& cache, CacheMode mode, const HostAllocation& alloc, double recompute_ratio = 0.0);
     void add_request(const std::string& id, int prompt_len);
     TokenSlot add_token(const std::string& id);
+    // Dry run of add_token over a batch (no mutation): throws CapacityError if
+    // the new blocks the batch would append do not fit the free pools, so a
+    // batched decode step either grows every context or none (the reference's
+    // per-token append leaves the table untouched on failure, cache.cpp:91, 98).
+    void check_batch_capacity(const std::vector<std::string>& ids) const;
     long recompute_tokens(const std::string& id) const;
     CacheMode mode() const { return mode_; }
     const HostAllocation& allocation() const { return alloc_; }

@@ -749,3 +749,33 @@ def test_engine_shared_weight_stream_rejects_tp_and_resident(native):
     t = TensorParallel.local_group(2)
     with pytest.raises(ConfigError):
         make_engine(cfg, w, weight_share=g[0], tp=t[0], weights_on_device=False)
+
+
+def test_engine_capacity_error_leaves_batch_untouched(native):
+    """A decode step whose new blocks do not fit raises CapacityError before
+    any context grows (the reference's append leaves the table untouched,
+    cache.cpp:91, 98): after freeing a request the survivors decode on and
+    still match the oracle, and their tables equal a run that never failed."""
+    from paper_2501_01792_b200 import CapacityError
+    from paper_2501_01792_b200.api import PoolCaps
+    cfg = small_cfg(L=2, d=256, H=2, f=512, tpb=8)
+    w = oracle_weights(cfg)
+    rng = np.random.default_rng(5)
+    # three requests at a block boundary, pools with room for exactly two more ACT blocks
+    prompts = {r: rng.integers(0, cfg.vocab_size, 16).tolist() for r in ("a", "b", "c")}
+    eng = make_engine(cfg, w, max_batch=3, caps=PoolCaps(act_gpu=8), mode="act_only")
+    eng.prefill(list(prompts), list(prompts.values()))
+    before = eng.cache.dump_json()
+    with pytest.raises(CapacityError):
+        eng.decode_step(["a", "b", "c"], [1, 2, 3])
+    assert eng.cache.dump_json() == before                 # nothing half-applied
+    eng.free_request("c")
+    seqs = {k: list(v) for k, v in prompts.items() if k != "c"}
+    for step in range(3):
+        toks = rng.integers(0, cfg.vocab_size, 2).tolist()
+        res = eng.decode_step(["a", "b"], toks, want_x=True)
+        for i, rid in enumerate(["a", "b"]):
+            seqs[rid].append(toks[i])
+            assert rel(f64(res["x"][i]), O.forward_prompt(seqs[rid], w).output[-1]) <= TOL, (step, rid)
+    for rid, s in seqs.items():
+        assert eng.cache.context_len(rid) == len(s)
