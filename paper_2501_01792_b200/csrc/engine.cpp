@@ -796,6 +796,7 @@ void Engine::prefill(const std::vector<std::string>& ids, const std::vector<std:
     };
     std::vector<Chunk> chunks;
     std::vector<int> tokens, positions, a_src, a_n, a_ref, acth, kvh;
+    try {  // none of ids existed before this call (checked above): on failure all are released again
     for (size_t r = 0; r < ids.size(); ++r) {
         const int P = static_cast<int>(prompts[r].size());
         if (chunks.empty() || (chunks.back().rows > 0 && chunks.back().rows + P > opt_.max_prefill_tokens)) {
@@ -835,6 +836,11 @@ void Engine::prefill(const std::vector<std::string>& ids, const std::vector<std:
         c.n += 1;
         c.cu.push_back(c.rows);
         c.max_len = std::max(c.max_len, P);
+    }
+    } catch (...) {  // pools exhausted part-way: the prefill admits every request or none
+        for (const std::string& id : ids)
+            if (cache_->has_request(id)) free_request(id);
+        throw;
     }
     const int T = static_cast<int>(tokens.size());
     if (T == 0) return;

@@ -779,3 +779,23 @@ def test_engine_capacity_error_leaves_batch_untouched(native):
             assert rel(f64(res["x"][i]), O.forward_prompt(seqs[rid], w).output[-1]) <= TOL, (step, rid)
     for rid, s in seqs.items():
         assert eng.cache.context_len(rid) == len(s)
+
+
+def test_engine_prefill_capacity_error_admits_none(native):
+    """A prefill whose prompts do not all fit raises CapacityError and admits
+    none of them (the pools are as before); a smaller prefill then works."""
+    from paper_2501_01792_b200 import CapacityError
+    from paper_2501_01792_b200.api import PoolCaps
+    cfg = small_cfg(L=2, d=256, H=2, f=512, tpb=8)
+    w = oracle_weights(cfg)
+    rng = np.random.default_rng(6)
+    eng = make_engine(cfg, w, max_batch=3, caps=PoolCaps(act_gpu=5), mode="act_only")
+    before = eng.cache.dump_json()
+    big = [rng.integers(0, cfg.vocab_size, 12).tolist() for _ in range(3)]   # 3 x 2 blocks > 5
+    with pytest.raises(CapacityError):
+        eng.prefill(["a", "b", "c"], big)
+    assert eng.cache.dump_json() == before
+    eng.prefill(["a", "b"], big[:2])
+    res = eng.decode_step(["a", "b"], [7, 8], want_x=True)
+    for i in range(2):
+        assert rel(f64(res["x"][i]), O.forward_prompt(big[i] + [7 + i], w).output[-1]) <= TOL
