@@ -52,9 +52,10 @@ def parse():
     p.add_argument("--tp-emulate", type=int, default=0,
                    help="time ONE rank of an N-way head-sharded group on this single GPU (collectives skipped, "
                         "NVLink time modelled) and print a projection line instead of the bench line")
-    p.add_argument("--no-share-weights", action="store_true",
-                   help="N>1: every rank streams whole weight layers over its own host link (default: the ranks "
-                        "share ONE weight stream — 1/N of every layer per link + an NVLink all-gather)")
+    p.add_argument("--share-weights", action="store_true",
+                   help="N>1 variant: the batch-partitioned ranks share ONE weight stream (1/N of every layer per "
+                        "host link + an NVLink all-gather). Default off: the north star's partition has no "
+                        "collective — every rank streams whole layers over its own host link")
     p.add_argument("--share-emulate", type=int, default=0,
                    help="time ONE rank of N batch-partitioned ranks sharing the weight stream on this single GPU "
                         "(all-gather skipped, NVLink time modelled) and print a projection line")
@@ -595,7 +596,7 @@ def weight_share_group(args, world, rank, local, dist):
     from paper_2501_01792_b200 import api
     if args.share_emulate > 1:
         return api.TensorParallel.emulated(0, args.share_emulate), args.share_emulate
-    if world > 1 and not args.no_share_weights and args.tp <= 1:
+    if world > 1 and args.share_weights and args.tp <= 1:
         import torch
         local_world = int(os.environ.get("LOCAL_WORLD_SIZE", str(world)))
         if torch.cuda.device_count() < local_world or local_world != world:

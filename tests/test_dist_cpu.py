@@ -104,16 +104,18 @@ def test_config4_strong_split_covers_global_batch():
 
 
 def test_weight_share_group_selection(monkeypatch):
-    """The shared weight stream needs one GPU per rank on one node: without
-    (ranks sharing a device, or --no-share-weights, or head-sharded TP) every
-    rank streams whole layers; world 1 never shares."""
+    """The shared weight stream is an opt-in variant (--share-weights; the
+    default partition has no collective) and needs one GPU per rank on one
+    node; world 1 never shares."""
     sys.path.insert(0, ROOT)
     import bench
     sys.argv = ["bench.py"]
     a = bench.parse()
-    assert bench.weight_share_group(a, 1, 0, 0, None) == (None, 1)
+    assert not a.share_weights
     monkeypatch.setenv("LOCAL_WORLD_SIZE", "2")
-    assert bench.weight_share_group(a, 2, 0, 0, None) == (None, 1)  # no CUDA devices here: ranks share none
-    sys.argv = ["bench.py", "--no-share-weights"]
-    assert bench.weight_share_group(bench.parse(), 2, 0, 0, None) == (None, 1)
+    assert bench.weight_share_group(a, 2, 0, 0, None) == (None, 1)  # default: whole-layer streams
+    sys.argv = ["bench.py", "--share-weights"]
+    b = bench.parse()
+    assert bench.weight_share_group(b, 1, 0, 0, None) == (None, 1)
+    assert bench.weight_share_group(b, 2, 0, 0, None) == (None, 1)  # no CUDA devices here: ranks share none
     sys.argv = ["bench.py"]
