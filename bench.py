@@ -996,20 +996,28 @@ def resident_variants(local, cfg, B, P, arch, steps=2, warmup=1, reserve=3e9, on
                              "predicted_t_link_ms_per_layer": t_bal[1] * 1e3},
            "bundle": {"kv_gen_slope": bundle.t_kv_gen.slope, "load_kv_slope": bundle.t_load_kv.slope},
            "per_ratio": []}
+    def caps_at(r):  # the capacity rule at a forced share
+        act_cap = 0 if r <= 0 else (N if r >= 1 else B * (math.ceil(r * nb) + 1))
+        kv_need = 0 if r >= 1 else (N if r <= 0 else B * (math.ceil((1 - r) * nb) + 1))
+        # KV/gpu blocks that fit next to the ACT blocks, their recompute slots and
+        # the two per-layer staging slots of the overflow (kv_host) blocks
+        room = free - act_cap * (act_all + kv_one) - 2 * kv_need * kv_one
+        kv_gpu = int(max(0, min(kv_need, room // (kv_all - 2 * kv_one))))
+        return api.PoolCaps(kv_host=kv_need - kv_gpu, kv_gpu=kv_gpu, act_gpu=act_cap)
+
+    def tiered_alloc(c):  # HostAllocation target of a three-tier plan: ACT/gpu share of all blocks
+        return api.HostAllocation(c.act_gpu, N - c.act_gpu)
+
+    jobs = []  # (r, caps, allocation, tag)
     for r in ([r_bal] if only_planned else sorted({0.0, r_fit, r_bal, (1.0 + r_fit) / 2, 1.0})):
         a = int(round(r * 1000))
         if r == r_bal:
-            caps = caps_bal
-        elif r == r_fit:
-            caps = caps_fit
-        else:  # the same capacity rule at a forced share
-            act_cap = 0 if r <= 0 else (N if r >= 1 else B * (math.ceil(r * nb) + 1))
-            kv_need = 0 if r >= 1 else (N if r <= 0 else B * (math.ceil((1 - r) * nb) + 1))
-            # KV/gpu blocks that fit next to the ACT blocks, their recompute slots and
-            # the two per-layer staging slots of the overflow (kv_host) blocks
-            room = free - act_cap * (act_all + kv_one) - 2 * kv_need * kv_one
-            kv_gpu = int(max(0, min(kv_need, room // (kv_all - 2 * kv_one))))
-            caps = api.PoolCaps(kv_host=kv_need - kv_gpu, kv_gpu=kv_gpu, act_gpu=act_cap)
+            jobs.append((r, caps_bal, tiered_alloc(caps_bal), "planned"))
+        else:
+            jobs.append((r, caps_fit if r == r_fit else caps_at(r), api.HostAllocation(a, 1000 - a),
+                         "capacity_only" if r == r_fit else ""))
+    while jobs:
+        r, caps, alloc, tag = jobs.pop(0)
         act_cap, kv_gpu = caps.act_gpu, caps.kv_gpu
         mode = "kv_only" if r <= 0 else ("act_only" if r >= 1 else "hybrid")
         host_need = caps.kv_host * kv_all + caps.act_host * act_all
@@ -1023,8 +1031,6 @@ def resident_variants(local, cfg, B, P, arch, steps=2, warmup=1, reserve=3e9, on
                                      f"{free / 1e9:.0f} GB"})
             continue
         try:
-            alloc = (api.HostAllocation(caps_bal.act_gpu, N - caps_bal.act_gpu) if r == r_bal
-                     else api.HostAllocation(a, 1000 - a))
             eng.configure_cache(caps, mode=mode, allocation=alloc, kv_on_gpu=True)
             eng.admit_synthetic(ids, [P] * B, seed=11)
             run_steps(eng, ids, tokens, 0, warmup)
@@ -1040,7 +1046,23 @@ def resident_variants(local, cfg, B, P, arch, steps=2, warmup=1, reserve=3e9, on
                                      "recompute_rows": prof["recompute_rows"],
                                      "ms_per_step": ms, "kv_gpu_blocks": kv_gpu, "kv_host_blocks": caps.kv_host,
                                      "act_gpu_blocks": act_cap, "h2d_gb_per_step": acc["h2d"] / steps / 1e9,
-                                     "planned": r == r_bal, "capacity_only": r == r_fit})
+                                     "planned": tag == "planned", "capacity_only": tag == "capacity_only",
+                                     "replanned": tag == "replanned"})
+            if tag == "planned" and prof["recompute_rows"] > 0 and prof["recompute_ms"] > 0:
+                # closed loop (north-star (5)): the recompute rate measured IN the step
+                # (power cap, concurrent DMA) replaces the isolated calibration slope,
+                # and the balance is re-solved on it
+                slope = prof["recompute_ms"] / 1e3 / prof["recompute_rows"]
+                b2 = api.TimingBundle(api.LinearTimeModel(slope, 0.0, 1.0, False), bundle.t_load_kv,
+                                      bundle.t_load_w, bundle.s_weight_layer, bundle.s_weight_total)
+                r2, caps2, t2 = api.plan_hbm_tiers(cfg, B, nb, free, b2, host_bytes=host_budget)
+                out["replanned"] = {"insitu_kv_gen_slope": slope, "r": r2,
+                                    "tiers": {"act_gpu": caps2.act_gpu, "kv_gpu": caps2.kv_gpu,
+                                              "kv_host": caps2.kv_host, "act_host": caps2.act_host},
+                                    "predicted_t_comp_ms_per_layer": t2[0] * 1e3,
+                                    "predicted_t_link_ms_per_layer": t2[1] * 1e3}
+                if caps2.act_gpu != caps_bal.act_gpu:
+                    jobs.insert(0, (r2, caps2, tiered_alloc(caps2), "replanned"))
         except Exception as e:
             out["per_ratio"].append({"act_share_r": round(r, 4), "error": str(e)})
     eng.close()
