@@ -70,3 +70,29 @@ def test_cpp_caller_fails_loudly_without_gpu():
         pytest.skip("GPU present: covered by test_engine_gpu.py::test_cpp_caller_decodes")
     out = subprocess.run([exe], capture_output=True, text=True, timeout=120)
     assert out.returncode == 3, out.stderr
+
+
+def test_struct_layouts_match_header(tmp_path):
+    """sizeof / offsetof of the C-ABI structs, compiled from include/hybridcache.h,
+    equal the ctypes mirrors the Python API passes (a field added on one side
+    only would shift every later field)."""
+    import ctypes as C
+    from paper_2501_01792_b200._signatures import EngineOptionsC, ModelConfigC
+    lines = []
+    for cname, py in (("hc_model_config", ModelConfigC), ("hc_engine_options", EngineOptionsC)):
+        lines.append(f'printf("{cname} size %zu\\n", sizeof({cname}));')
+        for f, _ in py._fields_:
+            lines.append(f'printf("{cname} {f} %zu\\n", offsetof({cname}, {f}));')
+    src = tmp_path / "layout.c"
+    src.write_text('#include <stddef.h>\n#include <stdio.h>\n#include "hybridcache.h"\nint main(void) {\n' +
+                   "\n".join(lines) + "\nreturn 0;\n}\n")
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-std=c11", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)], check=True)
+    got = {}
+    for line in subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.splitlines():
+        s, f, v = line.split()
+        got[(s, f)] = int(v)
+    for cname, py in (("hc_model_config", ModelConfigC), ("hc_engine_options", EngineOptionsC)):
+        assert got[(cname, "size")] == C.sizeof(py), cname
+        for f, _ in py._fields_:
+            assert got[(cname, f)] == getattr(py, f).offset, (cname, f)
