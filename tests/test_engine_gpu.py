@@ -799,3 +799,65 @@ def test_engine_prefill_capacity_error_admits_none(native):
     res = eng.decode_step(["a", "b"], [7, 8], want_x=True)
     for i in range(2):
         assert rel(f64(res["x"][i]), O.forward_prompt(big[i] + [7 + i], w).output[-1]) <= TOL
+
+
+@pytest.mark.parametrize("seed,mode", [(1, "hybrid"), (2, "hybrid"), (3, "kv_only"), (4, "act_only")])
+def test_engine_fuzz_against_oracle(native, seed, mode):
+    """Randomised serving session on small pools (the end-to-end analogue of the
+    reference's cache fuzz, test_cache.cpp:143-217): admit prompts (empty
+    included), decode random subsets, free requests, hit pool exhaustion.
+    Every decode output equals the oracle's forward over the request's tokens,
+    every CapacityError leaves the block tables unchanged, and the tables stay
+    consistent with the token counts."""
+    from paper_2501_01792_b200 import CapacityError
+    from paper_2501_01792_b200.api import HostAllocation, PoolCaps
+    cfg = small_cfg(L=2, d=256, H=2, f=512, tpb=8)
+    w = oracle_weights(cfg, max_seq=96)
+    rng = np.random.default_rng(1000 + seed)
+    caps = PoolCaps(kv_host=14, act_host=10, act_gpu=3) if mode == "hybrid" else (
+        PoolCaps(kv_host=20) if mode == "kv_only" else PoolCaps(act_host=12, act_gpu=6))
+    eng = make_engine(cfg, w, max_batch=4, max_seq=96, caps=caps, mode=mode,
+                      allocation=HostAllocation(int(rng.integers(1, 4)), int(rng.integers(1, 4))),
+                      weights_on_device=bool(seed % 2))
+    seqs, next_id, checked, exhausted = {}, 0, 0, 0
+    for op in range(70):
+        live = list(seqs)
+        r = rng.random()
+        if (r < 0.25 and len(live) < 4) or not live:
+            n_new = int(rng.integers(1, min(2, 4 - len(live)) + 1))
+            ids = [f"q{next_id + i}" for i in range(n_new)]
+            prompts = [rng.integers(0, cfg.vocab_size, int(rng.integers(0, 30))).tolist() for _ in ids]
+            before = eng.cache.dump_json()
+            try:
+                eng.prefill(ids, prompts)
+            except CapacityError:
+                assert eng.cache.dump_json() == before
+                exhausted += 1
+                continue
+            next_id += n_new
+            seqs.update({i: list(p) for i, p in zip(ids, prompts)})
+        elif r < 0.35:
+            victim = live[int(rng.integers(0, len(live)))]
+            eng.free_request(victim)
+            del seqs[victim]
+        else:
+            batch = [x for x in live if rng.random() < 0.7] or live[:1]
+            batch = [x for x in batch if len(seqs[x]) < 90]
+            if not batch:
+                continue
+            toks = rng.integers(0, cfg.vocab_size, len(batch)).tolist()
+            before = eng.cache.dump_json()
+            try:
+                res = eng.decode_step(batch, toks, want_x=True)
+            except CapacityError:
+                assert eng.cache.dump_json() == before
+                exhausted += 1
+                continue
+            for i, rid in enumerate(batch):
+                seqs[rid].append(toks[i])
+                ref = O.forward_prompt(seqs[rid], w).output[-1]
+                assert rel(f64(res["x"][i]), ref) <= TOL, (op, rid, len(seqs[rid]))
+                checked += 1
+        for rid, s in seqs.items():
+            assert eng.cache.context_len(rid) == len(s)
+    assert checked > 40
