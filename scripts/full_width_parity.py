@@ -25,11 +25,11 @@ def rel(a, b):
     return float(np.abs(np.asarray(a, np.float64) - b).max() / max(np.abs(b).max(), 1e-30))
 
 
-def main():
+def main(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--model", default="opt-30b")
     ap.add_argument("--arch", default="reference", choices=["reference", "opt"])
-    a = ap.parse_args()
+    a = ap.parse_args(argv)
     t0 = time.time()
     pre = api.ModelConfig.preset(a.model)
     d, H, f = pre.hidden_dim, pre.num_heads, pre.ffn_dim

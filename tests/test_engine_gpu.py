@@ -801,8 +801,10 @@ def test_engine_prefill_capacity_error_admits_none(native):
         assert rel(f64(res["x"][i]), O.forward_prompt(big[i] + [7 + i], w).output[-1]) <= TOL
 
 
-@pytest.mark.parametrize("seed,mode", [(1, "hybrid"), (2, "hybrid"), (3, "kv_only"), (4, "act_only")])
-def test_engine_fuzz_against_oracle(native, seed, mode):
+@pytest.mark.parametrize("seed,mode,arch", [(1, "hybrid", "reference"), (2, "hybrid", "reference"),
+                                             (3, "kv_only", "reference"), (4, "act_only", "reference"),
+                                             (5, "hybrid", "opt")])
+def test_engine_fuzz_against_oracle(native, seed, mode, arch):
     """Randomised serving session on small pools (the end-to-end analogue of the
     reference's cache fuzz, test_cache.cpp:143-217): admit prompts (empty
     included), decode random subsets, free requests, hit pool exhaustion.
@@ -812,11 +814,12 @@ def test_engine_fuzz_against_oracle(native, seed, mode):
     from paper_2501_01792_b200 import CapacityError
     from paper_2501_01792_b200.api import HostAllocation, PoolCaps
     cfg = small_cfg(L=2, d=256, H=2, f=512, tpb=8)
-    w = oracle_weights(cfg, max_seq=96)
+    w = opt_weights(cfg, max_seq=96) if arch == "opt" else oracle_weights(cfg, max_seq=96)
+    fwd = O.forward_prompt_opt if arch == "opt" else O.forward_prompt
     rng = np.random.default_rng(1000 + seed)
     caps = PoolCaps(kv_host=14, act_host=10, act_gpu=3) if mode == "hybrid" else (
         PoolCaps(kv_host=20) if mode == "kv_only" else PoolCaps(act_host=12, act_gpu=6))
-    eng = make_engine(cfg, w, max_batch=4, max_seq=96, caps=caps, mode=mode,
+    eng = (make_opt_engine if arch == "opt" else make_engine)(cfg, w, max_batch=4, max_seq=96, caps=caps, mode=mode,
                       allocation=HostAllocation(int(rng.integers(1, 4)), int(rng.integers(1, 4))),
                       weights_on_device=bool(seed % 2))
     seqs, next_id, checked, exhausted = {}, 0, 0, 0
@@ -855,7 +858,7 @@ def test_engine_fuzz_against_oracle(native, seed, mode):
                 continue
             for i, rid in enumerate(batch):
                 seqs[rid].append(toks[i])
-                ref = O.forward_prompt(seqs[rid], w).output[-1]
+                ref = fwd(seqs[rid], w).output[-1]
                 assert rel(f64(res["x"][i]), ref) <= TOL, (op, rid, len(seqs[rid]))
                 checked += 1
         for rid, s in seqs.items():

@@ -186,4 +186,4 @@ def test_full_width_opt30b_layer_parity():
     spec = importlib.util.spec_from_file_location("full_width_parity", p)
     mod = importlib.util.module_from_spec(spec)
     spec.loader.exec_module(mod)
-    mod.main()
+    mod.main([])
