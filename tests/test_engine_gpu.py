@@ -18,6 +18,7 @@ import hybridsim_oracle as O
 pytestmark = pytest.mark.gpu
 
 TOL = 1e-2
+TOL_OPT = 1.5e-2  # OPT layer variant (not in the reference): bf16 LayerNorm outputs, see the fuzz test
 
 
 def rel(got, ref):
@@ -816,6 +817,10 @@ def test_engine_fuzz_against_oracle(native, seed, mode, arch):
     cfg = small_cfg(L=2, d=256, H=2, f=512, tpb=8)
     w = opt_weights(cfg, max_seq=96) if arch == "opt" else oracle_weights(cfg, max_seq=96)
     fwd = O.forward_prompt_opt if arch == "opt" else O.forward_prompt
+    # the OPT variant rounds three LayerNorm outputs per layer (and the final LN) to bf16
+    # — the reference decoder has none — so its error floor sits ~1.5x higher: over 40
+    # soak sessions (scripts/soak_fuzz.py) worst 1.35e-2 vs 7.8e-3 for the reference arch
+    tol = TOL_OPT if arch == "opt" else TOL
     rng = np.random.default_rng(1000 + seed)
     caps = PoolCaps(kv_host=14, act_host=10, act_gpu=3) if mode == "hybrid" else (
         PoolCaps(kv_host=20) if mode == "kv_only" else PoolCaps(act_host=12, act_gpu=6))
@@ -859,7 +864,7 @@ def test_engine_fuzz_against_oracle(native, seed, mode, arch):
             for i, rid in enumerate(batch):
                 seqs[rid].append(toks[i])
                 ref = fwd(seqs[rid], w).output[-1]
-                assert rel(f64(res["x"][i]), ref) <= TOL, (op, rid, len(seqs[rid]))
+                assert rel(f64(res["x"][i]), ref) <= tol, (op, rid, len(seqs[rid]))
                 checked += 1
         for rid, s in seqs.items():
             assert eng.cache.context_len(rid) == len(s)
