@@ -869,3 +869,60 @@ def test_engine_fuzz_against_oracle(native, seed, mode, arch):
         for rid, s in seqs.items():
             assert eng.cache.context_len(rid) == len(s)
     assert checked > 40
+
+
+@pytest.mark.parametrize("tpn,seed", [(2, 11), (2, 12)])
+def test_engine_tensor_parallel_fuzz(native, tpn, seed):
+    """The serving fuzz on the head-sharded variant: every rank runs the same
+    randomised session (same ids, tokens, frees, pool exhaustion) in its own
+    thread; all ranks' outputs equal the oracle and their block tables agree."""
+    from paper_2501_01792_b200 import CapacityError
+    from paper_2501_01792_b200.api import HostAllocation, PoolCaps, TensorParallel
+    cfg = small_cfg(L=2, d=256, H=4, f=512, tpb=8)
+    w = oracle_weights(cfg, max_seq=96)
+    group = TensorParallel.local_group(tpn)
+    engs = [make_engine(cfg, w, max_batch=3, max_seq=96, caps=PoolCaps(kv_host=12, act_host=10, act_gpu=2),
+                        mode="hybrid", allocation=HostAllocation(1, 1), weights_on_device=bool(seed % 2),
+                        tp=group[r]) for r in range(tpn)]
+
+    def session(r):
+        def run():
+            rng = np.random.default_rng(seed)
+            eng, seqs, next_id, outs = engs[r], {}, 0, []
+            for op in range(40):
+                live = list(seqs)
+                u = rng.random()
+                if (u < 0.3 and len(live) < 3) or not live:
+                    ids = [f"t{next_id}"]
+                    prompts = [rng.integers(0, cfg.vocab_size, int(rng.integers(0, 25))).tolist()]
+                    try:
+                        eng.prefill(ids, prompts)
+                    except CapacityError:
+                        continue
+                    next_id += 1
+                    seqs[ids[0]] = list(prompts[0])
+                elif u < 0.4:
+                    victim = live[int(rng.integers(0, len(live)))]
+                    eng.free_request(victim)
+                    del seqs[victim]
+                else:
+                    batch = [x for x in live if len(seqs[x]) < 90]
+                    if not batch:
+                        continue
+                    toks = rng.integers(0, cfg.vocab_size, len(batch)).tolist()
+                    try:
+                        res = eng.decode_step(batch, toks, want_x=True)
+                    except CapacityError:
+                        continue
+                    for i, rid in enumerate(batch):
+                        seqs[rid].append(toks[i])
+                        outs.append((rid, list(seqs[rid]), f64(res["x"][i])))
+            return outs, eng.cache.dump_json()
+        return run
+
+    results = _run_ranks([session(r) for r in range(tpn)])
+    assert all(res[1] == results[0][1] for res in results)  # identical bookkeeping on every rank
+    assert len(results[0][0]) > 20
+    for outs, _ in results:
+        for rid, seq, x in outs:
+            assert rel(x, O.forward_prompt(seq, w).output[-1]) <= TOL, (rid, len(seq))
