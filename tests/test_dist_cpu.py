@@ -119,3 +119,28 @@ def test_weight_share_group_selection(monkeypatch):
     assert bench.weight_share_group(b, 1, 0, 0, None) == (None, 1)
     assert bench.weight_share_group(b, 2, 0, 0, None) == (None, 1)  # no CUDA devices here: ranks share none
     sys.argv = ["bench.py"]
+
+
+def test_calibrate_planner_widens_budget_for_small_batches():
+    """Config 4 split 8 ways (16 requests next to 130 GB of weights): the
+    reference's workload-sized budget (0.9 x the workload) cannot hold Alg. 1's
+    initial blocks; the bench widens the factor until the planner has room
+    and reports it. Larger batches keep the reference's 0.9."""
+    sys.path.insert(0, ROOT)
+    import bench
+    from paper_2501_01792_b200 import api
+
+    class FakeEngine:  # measured rates of a B200: recompute 1.9e-7 s/token, link 6.7e-7 s/token (OPT-66B)
+        def time_kv_gen(self, n, reps=3):
+            return 1.9e-7 * n + 3e-5
+
+        def time_load_kv(self, n, reps=2):
+            return 6.7e-7 * n + 8e-6
+
+    cfg = api.ModelConfig.preset("opt-66b")
+    for batch, want_factor in ((16, "6.0"), (64, "1.5"), (128, "0.9")):
+        p = bench.calibrate_planner(FakeEngine(), cfg, 55.6, 10 * 1024 * 16, batch * (1024 + 256))
+        assert 0.0 < p["planned_r"] <= 1.0
+        assert len(p["kv_gen_samples"]) >= 2
+        if want_factor:
+            assert f"+ {want_factor} x" in p["m_host_source"]
