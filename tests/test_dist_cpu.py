@@ -144,3 +144,40 @@ def test_calibrate_planner_widens_budget_for_small_batches():
         assert len(p["kv_gen_samples"]) >= 2
         if want_factor:
             assert f"+ {want_factor} x" in p["m_host_source"]
+
+
+@pytest.mark.parametrize("r", [0.0, 0.25, 1 / 3, 0.5, 0.75, 0.9432, 1.0])
+def test_pool_plan_covers_the_workload(r):
+    """bench.pool_plan sizes the host pools for B requests growing to P+steps
+    tokens at ACT share r: replaying next_block_kind (plan.cpp:154-164) block
+    by block never needs more blocks of a kind than the plan provides, and
+    host_layers_for folds layers only as far as the pinned budget demands."""
+    sys.path.insert(0, ROOT)
+    import math
+    import bench
+    from paper_2501_01792_b200 import api
+    cfg = api.ModelConfig.preset("opt-30b")
+    B, P, steps = 8, 1024, 12
+    mode, alloc, caps = bench.pool_plan(cfg, B, P, steps, r)
+    nb = math.ceil((P + steps) / cfg.tokens_per_block)
+    act = kv = 0
+    for _ in range(B):
+        a = k = 0
+        for _ in range(nb):
+            if mode == "hybrid":
+                kind = api.next_block_kind(a, k, alloc)
+            else:
+                kind = api.BlockKind.ACT if mode == "act_only" else api.BlockKind.KV
+            if kind == api.BlockKind.ACT:
+                a += 1
+            else:
+                k += 1
+        act, kv = act + a, kv + k
+    assert act <= caps.act_host and kv <= caps.kv_host
+    if 0 < r < 1:
+        assert abs(act / (act + kv) - r) <= 1.0 / nb + 1e-9  # the realised share tracks the setting
+    per_layer = caps.kv_host * api.HybridCache.bytes_of("KV", cfg) + caps.act_host * api.HybridCache.bytes_of("ACT", cfg)
+    for budget in (per_layer * 48 + 1e9, per_layer * 10 + 1e9, 1.0):
+        lp = bench.host_layers_for(cfg, caps, budget, 1e9)
+        assert 2 <= lp <= cfg.num_layers
+        assert lp == cfg.num_layers or lp * per_layer <= budget - 1e9 or lp == 2
