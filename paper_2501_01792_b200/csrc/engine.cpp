@@ -423,6 +423,8 @@ void Engine::init(const ModelConfig& c, int w_max_seq, const uint16_t* emb, cons
     m.arch = opt_.arch;
     if (cfg_.hidden_dim % 64) throw InputError("Engine: hidden_dim must be a multiple of 64");
     if (cfg_.head_dim() != 64 && cfg_.head_dim() != 128) throw InputError("Engine: head_dim must be 64 or 128");
+    if (!decode_attention_supported(cfg_.head_dim(), cfg_.tokens_per_block))
+        throw InputError("Engine: tokens_per_block must be 4, 8, 16, 32 or 64");
     if (cfg_.ffn_dim % 64) throw InputError("Engine: ffn_dim must be a multiple of 64");
     if (cfg_.vocab_size % 16) throw InputError("Engine: vocab_size must be a multiple of 16");
     if (opt_.max_batch < 1) throw InputError("Engine: max_batch must be >= 1");

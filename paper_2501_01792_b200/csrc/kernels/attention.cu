@@ -237,8 +237,16 @@ void decode_attention(const AttnCall& c, cudaStream_t st) {
     HC_ATTN(64, 8)
     HC_ATTN(128, 32)
     HC_ATTN(64, 32)
+    HC_ATTN(128, 4)
+    HC_ATTN(64, 4)
+    HC_ATTN(128, 64)
+    HC_ATTN(64, 64)
 #undef HC_ATTN
     throw std::invalid_argument("decode_attention: unsupported (head_dim, tokens_per_block)");
+}
+
+bool decode_attention_supported(int hd, int tpb) {
+    return (hd == 64 || hd == 128) && (tpb == 4 || tpb == 8 || tpb == 16 || tpb == 32 || tpb == 64);
 }
 
 }  // namespace hc

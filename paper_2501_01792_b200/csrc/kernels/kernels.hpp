@@ -65,6 +65,8 @@ struct AttnCall {
     int splits = 1;
 };
 void decode_attention(const AttnCall& c, cudaStream_t st);
+// the (head_dim, tokens_per_block) pairs decode_attention is instantiated for
+bool decode_attention_supported(int hd, int tpb);
 int attention_splits(int B, int H, int max_ctx, int tpb);
 
 // Causal prefill attention over ragged requests: request r owns rows

@@ -926,3 +926,45 @@ def test_engine_tensor_parallel_fuzz(native, tpn, seed):
     for outs, _ in results:
         for rid, seq, x in outs:
             assert rel(x, O.forward_prompt(seq, w).output[-1]) <= TOL, (rid, len(seq))
+
+
+@pytest.mark.parametrize("B,tpb,mode", [(200, 16, "hybrid"), (64, 32, "act_only"), (96, 4, "kv_only"),
+                                        (48, 64, "hybrid")])
+def test_engine_large_batches_and_block_sizes(native, B, tpb, mode):
+    """Edge sizes the reference allows: hundreds of requests in one decode
+    step (grid = B x heads, staging sized for every host block) and block
+    sizes other than 16 (tokens_per_block is a model parameter, model.hpp:22):
+    outputs equal the oracle for every request."""
+    from paper_2501_01792_b200.api import HostAllocation, PoolCaps
+    cfg = small_cfg(L=2, d=256, H=2, f=512, tpb=tpb)
+    w = oracle_weights(cfg, max_seq=64)
+    rng = np.random.default_rng(B + tpb)
+    lens = rng.integers(1, 40, B).tolist()
+    per = max(-(-(n + 3) // tpb) for n in lens) + 1
+    caps = PoolCaps(kv_host=B * per, act_host=B * per, act_gpu=B // 2)
+    eng = make_engine(cfg, w, max_batch=B, max_seq=64, caps=caps, mode=mode, allocation=HostAllocation(1, 1),
+                      weights_on_device=False)
+    ids = [f"b{i}" for i in range(B)]
+    prompts = [rng.integers(0, cfg.vocab_size, n).tolist() for n in lens]
+    eng.prefill(ids, prompts)
+    seqs = [list(p) for p in prompts]
+    for step in range(3):
+        toks = rng.integers(0, cfg.vocab_size, B).tolist()
+        res = eng.decode_step(ids, toks, want_x=True)
+        for b in range(0, B, 7 if B > 100 else 3):  # a spread of requests (oracle cost)
+            seqs[b].append(toks[b])
+            ref = O.forward_prompt(seqs[b], w).output[-1]
+            assert rel(f64(res["x"][b]), ref) <= TOL, (step, b)
+        for b in range(B):
+            if b % (7 if B > 100 else 3):
+                seqs[b].append(toks[b])
+
+
+def test_engine_rejects_unsupported_block_size(native):
+    """tokens_per_block outside the instantiated set fails at construction
+    (InputError), not in the middle of a decode step."""
+    from paper_2501_01792_b200 import InputError
+    cfg = small_cfg(L=1, tpb=3)
+    w = oracle_weights(cfg, max_seq=32)
+    with pytest.raises(InputError):
+        make_engine(cfg, w, max_batch=1)
