@@ -67,6 +67,33 @@ def main():
         t.join()
     for e in engs:
         e.close()
+    # batch-partitioned ranks sharing one weight stream (in-process group, 2 decode steps
+    # so the cross-step prefetch of layers 0/1 is sharded too); block sizes 4 and 64
+    wgroup = api.TensorParallel.local_group(2)
+    wengs = [api.Engine(cfg, seed=3, max_seq=64, max_batch=2, weights_on_device=False, weight_share=wgroup[r],
+                        caps=api.PoolCaps(kv_host=8, act_host=8, act_gpu=1), allocation=api.HostAllocation(1, 1))
+             for r in range(2)]
+
+    def run_ws(r):
+        ids = [f"w{r}a", f"w{r}b"]
+        wengs[r].prefill(ids, prompts)
+        for _ in range(2):
+            wengs[r].decode_step(ids, [5, 6])
+    ts = [threading.Thread(target=run_ws, args=(r,)) for r in range(2)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    for e in wengs:
+        e.close()
+    for tpb in (4, 64):
+        c3 = api.ModelConfig(num_layers=1, hidden_dim=256, num_heads=2, ffn_dim=512, vocab_size=512,
+                             tokens_per_block=tpb)
+        e3 = api.Engine(c3, seed=7, max_seq=96, max_batch=2, weights_on_device=True,
+                        caps=api.PoolCaps(kv_host=40, act_host=40, act_gpu=2), allocation=api.HostAllocation(1, 1))
+        e3.prefill(["a", "b"], prompts)
+        e3.decode_step(["a", "b"], [1, 2])
+        e3.close()
     print("sanitize smoke ok")
 
 
