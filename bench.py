@@ -711,6 +711,10 @@ def our_arm(args, cfg, world, rank, local, dist):
                              "once); the excess is [Wk|Wv] (205 MB > the 126 MB L2) re-read once per 16-tile M "
                              "group — the L2-capacity floor for this shape, DESIGN.md §3"),
             "peak_source": f"{peak_src} bf16_tflops_sustained (MEASURED_PEAKS.json); burst {tflops_burst}",
+            "frac_vs_burst": achieved / tflops_burst if tflops_burst else None,
+            "frac_note": ("the kernel is timed inside a long step, so the peak is the sustained figure (cuBLAS "
+                          "back to back for 4 s); a launch between copy-stream waits can run cooler than that "
+                          "and exceed it (frac > 1) — frac_vs_burst is the single-launch bound"),
             "flops_per_launch": rec_flops, "launch_ms": rec_launch_ms}
     # per-step roofline (north_star): slower of link bytes / link BW, tensor
     # FLOPs / tensor peak, HBM bytes / HBM BW
