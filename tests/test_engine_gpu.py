@@ -968,3 +968,36 @@ def test_engine_rejects_unsupported_block_size(native):
     w = oracle_weights(cfg, max_seq=32)
     with pytest.raises(InputError):
         make_engine(cfg, w, max_batch=1)
+
+
+def test_engine_reconfigure_across_modes(native):
+    """One engine reconfigured through every cache mode and pool shape in turn
+    (what the bench's sweeps do): each configuration's decode outputs equal
+    the oracle — no graph, prefetch or pool state leaks across configure_cache."""
+    from paper_2501_01792_b200.api import HostAllocation, PoolCaps
+    cfg = small_cfg(L=2, d=256, H=2, f=512, tpb=8)
+    w = oracle_weights(cfg, max_seq=64)
+    rng = np.random.default_rng(77)
+    eng = make_engine(cfg, w, max_batch=2, max_seq=64, weights_on_device=False,
+                      caps=PoolCaps(kv_host=16), mode="kv_only")
+    plans = [("kv_only", PoolCaps(kv_host=16), HostAllocation(0, 1), {}),
+             ("hybrid", PoolCaps(kv_host=12, act_host=12, act_gpu=2), HostAllocation(1, 2), {}),
+             ("act_only", PoolCaps(act_host=4, act_gpu=10), HostAllocation(1, 0), {}),
+             ("hybrid", PoolCaps(kv_host=6, kv_gpu=6, act_gpu=8), HostAllocation(2, 1), {"kv_on_gpu": True}),
+             ("token_recompute", PoolCaps(kv_host=16), HostAllocation(1, 1), {"recompute_ratio": 0.5}),
+             ("hybrid", PoolCaps(kv_host=12, act_host=12), HostAllocation(1, 1), {"host_layers": 1})]
+    for i, (mode, caps, alloc, kw) in enumerate(plans * 2):
+        eng.configure_cache(caps, mode=mode, allocation=alloc, **kw)
+        prompts = [rng.integers(0, cfg.vocab_size, int(rng.integers(5, 30))).tolist() for _ in range(2)]
+        ids = [f"c{i}a", f"c{i}b"]
+        eng.prefill(ids, prompts)
+        seqs = [list(p) for p in prompts]
+        for step in range(3):
+            toks = rng.integers(0, cfg.vocab_size, 2).tolist()
+            res = eng.decode_step(ids, toks, want_x=True)
+            for b in range(2):
+                seqs[b].append(toks[b])
+                if kw.get("host_layers"):
+                    continue  # folded host pools (a benchmark device): payloads alias across layers
+                ref = O.forward_prompt(seqs[b], w).output[-1]
+                assert rel(f64(res["x"][b]), ref) <= TOL, (i, mode, step, b)
