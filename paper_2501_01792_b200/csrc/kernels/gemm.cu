@@ -11,6 +11,7 @@
 
 #include "gemm.cuh"
 #include "kernels.hpp"
+#include "launch.hpp"
 #include "tma.hpp"
 
 namespace hc {
@@ -57,11 +58,8 @@ template <int BN, int EPI>
 void launch(const GemmCall& c, const gemm::Params& p, cudaStream_t st) {
     using Cf = gemm::Cfg<BN>;
     auto kern = gemm::gemm_tn_kernel<BN, EPI>;
-    static bool attr_set = false;  // per instantiation
-    if (!attr_set) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::kSmemBytes);
-        attr_set = true;
-    }
+    static std::atomic<uint64_t> attr_set{0};  // per instantiation, per device
+    max_dynamic_smem_once(kern, Cf::kSmemBytes, attr_set);
     const CUtensorMap ta = make_map(c.A, c.a_rows, c.K, c.lda, gemm::BM);
     const CUtensorMap tb = make_map(c.B, c.N, c.K, c.ldb, BN);
     const int tiles = p.num_m_tiles * p.num_n_tiles * p.splits;
@@ -74,11 +72,8 @@ template <int EPI>
 void launch_pair(const GemmCall& c, const gemm::Params& p, cudaStream_t st) {
     using Cf = gemm::Cfg2;
     auto kern = gemm::gemm2_tn_kernel<EPI>;
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::kSmemBytes);
-        attr_set = true;
-    }
+    static std::atomic<uint64_t> attr_set{0};
+    max_dynamic_smem_once(kern, Cf::kSmemBytes, attr_set);
     const CUtensorMap ta = make_map(c.A, c.a_rows, c.K, c.lda, gemm::BM);
     const CUtensorMap tb = make_map(c.B, c.N, c.K, c.ldb, Cf::BN / 2);
     const int tiles = ((p.num_m_tiles + 1) / 2) * p.num_n_tiles;

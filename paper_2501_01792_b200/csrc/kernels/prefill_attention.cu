@@ -21,6 +21,7 @@
 #include <stdexcept>
 
 #include "kernels.hpp"
+#include "launch.hpp"
 #include "ptx.cuh"
 
 namespace hc {
@@ -257,12 +258,8 @@ template <int HD>
 void launch_prefill(const bf16* qkv, bf16* out, const int* cu, int n_req, int max_len, int H, float scale,
                     cudaStream_t st) {
     constexpr size_t smem = static_cast<size_t>(4 * kKT) * HD * 2;
-    static bool configured = false;
-    if (!configured) {
-        cudaFuncSetAttribute(prefill_flash_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(smem));
-        configured = true;
-    }
+    static std::atomic<uint64_t> configured{0};
+    max_dynamic_smem_once(prefill_flash_kernel<HD>, static_cast<int>(smem), configured);
     const dim3 grid((max_len + kQT - 1) / kQT, H, n_req);
     prefill_flash_kernel<HD><<<grid, 128, smem, st>>>(qkv, out, cu, H, scale);
 }

@@ -30,6 +30,7 @@
 #include <stdexcept>
 
 #include "kernels.hpp"
+#include "launch.hpp"
 #include "ptx.cuh"
 #include "tma.hpp"
 
@@ -650,12 +651,9 @@ bool prefill_attention_tc(const bf16* qkv, long long rows, bf16* out, const int*
         return e ? std::atoi(e) : 2;
     }();
     if (!enabled || hd != kHD || rows <= 0) return false;
-    static bool configured = false;
-    if (!configured) {
-        cudaFuncSetAttribute(prefill_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem::bytes);
-        cudaFuncSetAttribute(prefill_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem2::bytes);
-        configured = true;
-    }
+    static std::atomic<uint64_t> configured1{0}, configured2{0};
+    max_dynamic_smem_once(prefill_tc_kernel, Smem::bytes, configured1);
+    max_dynamic_smem_once(prefill_tc2_kernel, Smem2::bytes, configured2);
     const long long d3 = 3LL * H * kHD;
     const CUtensorMap tm = make_map(qkv, rows, d3, d3, kT);
     static const uint32_t lbo = [] {
