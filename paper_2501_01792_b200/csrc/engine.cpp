@@ -551,6 +551,7 @@ void Engine::init(const ModelConfig& c, int w_max_seq, const uint16_t* emb, cons
 
 void Engine::configure_cache(const PoolCaps& caps, bool kv_on_gpu, CacheMode mode, const HostAllocation& alloc,
                              int host_layers, double recompute_ratio) {
+    HC_CUDA(cudaSetDevice(opt_.device));  // the calling thread may be on another device
     Impl& m = *impl_;
     opt_.recompute_ratio = recompute_ratio;
     if (mode == CacheMode::TokenRecompute && (opt_.recompute_ratio < 0.0 || opt_.recompute_ratio > 1.0))
@@ -630,6 +631,7 @@ void Engine::configure_cache(const PoolCaps& caps, bool kv_on_gpu, CacheMode mod
 
 void Engine::forward_trace(const std::vector<int>& ids, uint16_t* layer_inputs, uint16_t* k, uint16_t* v,
                            uint16_t* out) {
+    HC_CUDA(cudaSetDevice(opt_.device));  // the calling thread may be on another device
     Impl& m = *impl_;
     const int T = static_cast<int>(ids.size());
     if (T == 0) return;
@@ -649,6 +651,7 @@ void Engine::forward_trace(const std::vector<int>& ids, uint16_t* layer_inputs, 
 }
 
 void Engine::layer_forward(int layer, const uint16_t* x, int T, uint16_t* k, uint16_t* v, uint16_t* out) {
+    HC_CUDA(cudaSetDevice(opt_.device));  // the calling thread may be on another device
     Impl& m = *impl_;
     if (layer < 0 || layer >= m.L) throw InputError("layer index out of range: " + std::to_string(layer));
     if (T <= 0) return;
@@ -665,6 +668,7 @@ void Engine::layer_forward(int layer, const uint16_t* x, int T, uint16_t* k, uin
 Engine::~Engine() {
     if (!impl_) return;
     Impl& m = *impl_;
+    cudaSetDevice(opt_.device);
     cudaDeviceSynchronize();
     for (void* p : {(void*)m.emb, (void*)m.pos, (void*)m.w_all, (void*)m.wbuf[0], (void*)m.wbuf[1], (void*)m.kv_gpu,
                     (void*)m.act_gpu, (void*)m.kvr, (void*)m.kv_stage[0], (void*)m.kv_stage[1], (void*)m.act_stage[0],
@@ -989,6 +993,7 @@ void Engine::prefill(const std::vector<std::string>& ids, const std::vector<std:
 }
 
 void Engine::admit_synthetic(const std::vector<std::string>& ids, const std::vector<int>& prompt_lens, uint64_t seed) {
+    HC_CUDA(cudaSetDevice(opt_.device));  // the calling thread may be on another device
     Impl& m = *impl_;
     m.require_configured();
     if (ids.size() != prompt_lens.size()) throw InputError("admit_synthetic: ids and lengths differ");
@@ -1509,6 +1514,7 @@ void Engine::decode_step(const std::vector<std::string>& ids, const int* tokens,
 
 // ---------------------------------------------------------------------------
 void Engine::read_weights(int layer, uint16_t* out) {
+    HC_CUDA(cudaSetDevice(opt_.device));  // the calling thread may be on another device
     Impl& m = *impl_;
     HC_CUDA(cudaStreamSynchronize(s_compute_));
     if (layer == -1) {
@@ -1529,6 +1535,7 @@ void Engine::read_weights(int layer, uint16_t* out) {
 }
 
 void Engine::read_block(BlockKind kind, Location loc, int pbn, int layer, uint16_t* out) {
+    HC_CUDA(cudaSetDevice(opt_.device));  // the calling thread may be on another device
     Impl& m = *impl_;
     m.require_configured();
     if (layer < 0 || layer >= m.L) throw InputError("read_block: layer out of range");
@@ -1553,6 +1560,7 @@ void Engine::read_block(BlockKind kind, Location loc, int pbn, int layer, uint16
 
 // ---------------------------------------------------------------------------
 double Engine::time_kv_gen(int n_tokens, int reps) {
+    HC_CUDA(cudaSetDevice(opt_.device));  // the calling thread may be on another device
     Impl& m = *impl_;
     if (n_tokens <= 0) throw InputError("time_kv_gen: n_tokens must be positive");
     // recompute GEMM over n tokens of the ACT staging (or GPU) pool, layer 0
@@ -1597,6 +1605,7 @@ double Engine::time_kv_gen(int n_tokens, int reps) {
 }
 
 double Engine::time_load_bytes(size_t bytes, int reps) {
+    HC_CUDA(cudaSetDevice(opt_.device));  // the calling thread may be on another device
     Impl& m = *impl_;
     const size_t cap = static_cast<size_t>(m.kv_host_cap) * m.kvb * 2;
     if (bytes == 0 || bytes > cap) throw InputError("time_load: byte count exceeds the KV host pool");
@@ -1612,6 +1621,7 @@ double Engine::time_load_bytes(size_t bytes, int reps) {
 }
 
 double Engine::time_load_kv(int n_tokens, int reps) {
+    HC_CUDA(cudaSetDevice(opt_.device));  // the calling thread may be on another device
     // this rank's bytes of n KV tokens (all heads, or its 1/tpn under tensor parallelism)
     return time_load_bytes(static_cast<size_t>(n_tokens) * 2 * impl_->dg * 2, reps);
 }
