@@ -361,14 +361,23 @@ __global__ void __launch_bounds__(kThreads, 1)
 constexpr int kSlots2 = 3;
 constexpr int kThreads2 = 320;
 
+// head_dim 64 has the smem for a second P buffer per tile: P = P_hi + P_lo (both
+// bf16, P_lo = bf16(p - P_hi)) and O += P_hi V + P_lo V keeps P to ~16 mantissa
+// bits, as the mma.sync kernel's hi/lo split does — halving the head dim
+// doubles the weight of the P rounding per output (12-layer OPT-125M traces).
+template <int HD>
 struct Smem2 {
-    static constexpr int q = 0;                 // tile t at q + t * kTile
-    static constexpr int p = 2 * kTile;         // tile t at p + t * kTile
-    static constexpr int kv = 4 * kTile;        // slot s at kv + s * kTile
-    static constexpr int bars = kv + kSlots2 * kTile;
+    static constexpr bool lo = HD == 64;
+    static constexpr int qkv = kT * HD * 2;     // one Q / K / V tile: HD / 64 boxes of [128 rows][64 cols]
+    static constexpr int q = 0;                 // tile t at q + t * qkv
+    static constexpr int p = 2 * qkv;           // tile t at p + t * kTile (P is [128 queries][128 keys])
+    static constexpr int kv = p + 2 * kTile;    // slot s at kv + s * qkv
+    static constexpr int plo = kv + kSlots2 * qkv;  // P_lo of tile t at plo + t * kTile (head_dim 64)
+    static constexpr int bars = plo + (lo ? 2 * kTile : 0);
     static constexpr int bytes = bars + 256 + 1024;
 };
-static_assert(Smem2::bytes <= 232448, "prefill_tc2: shared memory over the per-CTA limit");
+static_assert(Smem2<64>::bytes <= 232448, "prefill_tc2<64>: shared memory over the per-CTA limit");
+static_assert(Smem2<128>::bytes <= 232448, "prefill_tc2: shared memory over the per-CTA limit");
 
 struct Item {  // one (request, head, query-tile pair)
     int row0, P, h, qt0, n0, n1, n_kt;
@@ -393,12 +402,13 @@ __device__ __forceinline__ bool item_of(int w, int n_pairs, int H, int n_req, co
     return true;
 }
 
+template <int HD>  // head_dim 64 or 128
 __global__ void __launch_bounds__(kThreads2, 1)
     prefill_tc2_kernel(const __grid_constant__ CUtensorMap tm, bf16* __restrict__ out, const int* __restrict__ cu,
                        int n_req, int n_pairs, int H, float scale, uint32_t v_lbo, uint32_t v_sbo) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Smem2::bars);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Smem2<HD>::bars);
     uint64_t* q_full = bars + 0;
     uint64_t* q_empty = bars + 1;
     uint64_t* kv_full = bars + 2;   // [kSlots2]
@@ -410,7 +420,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
 
     const int n_items = n_pairs * H * n_req;
-    const int d = H * kHD;
+    const int d = H * HD;
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
 
     if (threadIdx.x == 0) {
@@ -441,22 +451,22 @@ __global__ void __launch_bounds__(kThreads2, 1)
             for (int w = blockIdx.x; w < n_items; w += gridDim.x) {
                 Item it;
                 if (!item_of(w, n_pairs, H, n_req, cu, it)) continue;
-                const int qc = it.h * kHD, kc = d + it.h * kHD, vc = 2 * d + it.h * kHD;
+                const int qc = it.h * HD, kc = d + it.h * HD, vc = 2 * d + it.h * HD;
                 if (n_it > 0) ptx::mbar_wait(q_empty, (n_it - 1) & 1);  // last QK^T of the previous item done
-                ptx::mbar_arrive_expect_tx(q_full, it.has1 ? 2 * kTile : kTile);
+                ptx::mbar_arrive_expect_tx(q_full, it.has1 ? 2 * Smem2<HD>::qkv : Smem2<HD>::qkv);
                 for (int t = 0; t < (it.has1 ? 2 : 1); ++t) {
-                    uint8_t* qb = smem + Smem2::q + t * kTile;
-                    ptx::tma_load_2d(qb, &tm, q_full, qc, it.row0 + (it.qt0 + t) * kT);
-                    ptx::tma_load_2d(qb + kBox, &tm, q_full, qc + 64, it.row0 + (it.qt0 + t) * kT);
+                    uint8_t* qb = smem + Smem2<HD>::q + t * Smem2<HD>::qkv;
+                    for (int bx = 0; bx < HD / 64; ++bx)
+                        ptx::tma_load_2d(qb + bx * kBox, &tm, q_full, qc + 64 * bx, it.row0 + (it.qt0 + t) * kT);
                 }
                 for (int i = 0; i < 2 * it.n_kt; ++i) {  // K_0, V_0, K_1, V_1, ...
                     const uint32_t g = ring + i, s = g % kSlots2;
                     ptx::mbar_wait(&kv_empty[s], ((g / kSlots2) & 1) ^ 1);
-                    uint8_t* b = smem + Smem2::kv + s * kTile;
-                    ptx::mbar_arrive_expect_tx(&kv_full[s], kTile);
+                    uint8_t* b = smem + Smem2<HD>::kv + s * Smem2<HD>::qkv;
+                    ptx::mbar_arrive_expect_tx(&kv_full[s], Smem2<HD>::qkv);
                     const int c = (i & 1) ? vc : kc, r = it.row0 + (i / 2) * kT;
-                    ptx::tma_load_2d(b, &tm, &kv_full[s], c, r);
-                    ptx::tma_load_2d(b + kBox, &tm, &kv_full[s], c + 64, r);
+                    for (int bx = 0; bx < HD / 64; ++bx)
+                        ptx::tma_load_2d(b + bx * kBox, &tm, &kv_full[s], c + 64 * bx, r);
                 }
                 ring += 2 * it.n_kt;
                 ++n_it;
@@ -465,15 +475,15 @@ __global__ void __launch_bounds__(kThreads2, 1)
     } else if (warp == 9) {
         if (lane == 0) {  // ------------------------------------------ MMA issuer
             constexpr uint32_t id_s = ptx::idesc_bf16_f32(kT, kT);               // A, B K-major
-            constexpr uint32_t id_o = ptx::idesc_bf16_f32(kT, kHD) | (1u << 16);  // B MN-major (V)
+            constexpr uint32_t id_o = ptx::idesc_bf16_f32(kT, HD) | (1u << 16);  // B MN-major (V)
             uint32_t ring = 0, n_it = 0, pc[2] = {0, 0}, oc[2] = {0, 0};
-            auto slot_addr = [&](uint32_t g) { return ptx::smem_u32(smem + Smem2::kv + (g % kSlots2) * kTile); };
+            auto slot_addr = [&](uint32_t g) { return ptx::smem_u32(smem + Smem2<HD>::kv + (g % kSlots2) * Smem2<HD>::qkv); };
             auto s_mma = [&](int t, uint32_t g) {  // S_t = Q_t . K^T, K at ring entry g
                 ptx::mbar_wait(&kv_full[g % kSlots2], (g / kSlots2) & 1);
                 ptx::tc_fence_after();
-                const uint32_t qa = ptx::smem_u32(smem + Smem2::q + t * kTile), kb = slot_addr(g);
+                const uint32_t qa = ptx::smem_u32(smem + Smem2<HD>::q + t * Smem2<HD>::qkv), kb = slot_addr(g);
 #pragma unroll
-                for (int k = 0; k < kHD / 16; ++k) {
+                for (int k = 0; k < HD / 16; ++k) {
                     const uint32_t off = (k / 4) * kBox;
                     ptx::mma_bf16_ss(tmem + 128u * t, ptx::sw128_kmajor_desc(qa + off) + 2 * (k % 4),
                                      ptx::sw128_kmajor_desc(kb + off) + 2 * (k % 4), id_s, k > 0);
@@ -486,12 +496,21 @@ __global__ void __launch_bounds__(kThreads2, 1)
                 ptx::mbar_wait(&p_full[t], pc[t] & 1);
                 ++pc[t];
                 ptx::tc_fence_after();
-                const uint32_t pa = ptx::smem_u32(smem + Smem2::p + t * kTile), vb = slot_addr(g);
+                const uint32_t pa = ptx::smem_u32(smem + Smem2<HD>::p + t * kTile), vb = slot_addr(g);
 #pragma unroll
                 for (int k = 0; k < kT / 16; ++k) {
                     const uint64_t a = ptx::sw128_kmajor_desc(pa + (k / 4) * kBox) + 2 * (k % 4);
                     const uint64_t bdesc = sw128_mnmajor_desc(vb + k * 16 * 128, v_lbo, v_sbo);
-                    ptx::mma_bf16_ss(tmem + 256u + 128u * t, a, bdesc, id_o, (!first || k > 0) ? 1u : 0u);
+                    ptx::mma_bf16_ss(tmem + 256u + static_cast<uint32_t>(HD) * t, a, bdesc, id_o, (!first || k > 0) ? 1u : 0u);
+                }
+                if constexpr (Smem2<HD>::lo) {  // + P_lo . V
+                    const uint32_t pl = ptx::smem_u32(smem + Smem2<HD>::plo + t * kTile);
+#pragma unroll
+                    for (int k = 0; k < kT / 16; ++k) {
+                        const uint64_t a = ptx::sw128_kmajor_desc(pl + (k / 4) * kBox) + 2 * (k % 4);
+                        const uint64_t bdesc = sw128_mnmajor_desc(vb + k * 16 * 128, v_lbo, v_sbo);
+                        ptx::mma_bf16_ss(tmem + 256u + static_cast<uint32_t>(HD) * t, a, bdesc, id_o, 1u);
+                    }
                 }
             };
             for (int w = blockIdx.x; w < n_items; w += gridDim.x) {
@@ -532,9 +551,9 @@ __global__ void __launch_bounds__(kThreads2, 1)
         const int q = warp % 4;
         const int r = q * 32 + lane;  // query row within the tile = TMEM lane
         const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
-        const uint32_t t_s = tmem + 128u * t, t_o = tmem + 256u + 128u * t;
+        const uint32_t t_s = tmem + 128u * t, t_o = tmem + 256u + static_cast<uint32_t>(HD) * t;
         const float sl = scale * kLog2e;
-        const uint32_t pbase = ptx::smem_u32(smem + Smem2::p + t * kTile) + (r / 8) * 1024 + (r % 8) * 128;
+        const uint32_t pbase = ptx::smem_u32(smem + Smem2<HD>::p + t * kTile) + (r / 8) * 1024 + (r % 8) * 128;
         uint32_t sc = 0, oc = 0;
         for (int w = blockIdx.x; w < n_items; w += gridDim.x) {
             Item it;
@@ -576,6 +595,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
                 }
                 // p = 2^(s * sl - m) in one FFMA + MUFU; masked entries (-FLT_MAX * sl) underflow to 0
                 uint32_t pw[kT / 2];
+                uint32_t plw[Smem2<HD>::lo ? kT / 2 : 1];
                 float2 l4[4] = {{0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}};
                 const float2 sl2 = make_float2(sl, sl), nm2 = make_float2(-m, -m);
 #pragma unroll
@@ -585,12 +605,16 @@ __global__ void __launch_bounds__(kThreads2, 1)
                     const float2 pp = make_float2(ex2(y.x), ex2(y.y));
                     l4[i % 4] = fadd2(l4[i % 4], pp);
                     pw[i] = ptx::pack_bf16x2(pp.x, pp.y);
+                    if constexpr (Smem2<HD>::lo) {  // the bf16 residual of each P entry
+                        const float h0 = __uint_as_float(pw[i] << 16), h1 = __uint_as_float(pw[i] & 0xFFFF0000u);
+                        plw[i] = ptx::pack_bf16x2(pp.x - h0, pp.y - h1);
+                    }
                 }
                 const float2 ls = fadd2(fadd2(l4[0], l4[1]), fadd2(l4[2], l4[3]));
                 l += ls.x + ls.y;
                 if (rescale) {  // PV_t(j-1) completed before S_t(j) was signalled
 #pragma unroll 1
-                    for (int c = 0; c < kHD; c += 16) {
+                    for (int c = 0; c < HD; c += 16) {
                         uint32_t v[16];
                         ptx::tmem_ld_x16(t_o + lane_off + c, v);
                         ptx::tmem_ld_wait();
@@ -605,6 +629,9 @@ __global__ void __launch_bounds__(kThreads2, 1)
                     const int box = c / 8, ch = c % 8;
                     sts128(pbase + box * kBox + ((ch ^ (r % 8)) * 16), pw[4 * c], pw[4 * c + 1], pw[4 * c + 2],
                            pw[4 * c + 3]);
+                    if constexpr (Smem2<HD>::lo)
+                        sts128(pbase + (Smem2<HD>::plo - Smem2<HD>::p) + box * kBox + ((ch ^ (r % 8)) * 16),
+                               plw[4 * c], plw[4 * c + 1], plw[4 * c + 2], plw[4 * c + 3]);
                 }
                 fence_async_smem();
                 ptx::tc_fence_before();
@@ -614,9 +641,9 @@ __global__ void __launch_bounds__(kThreads2, 1)
             ++oc;
             ptx::tc_fence_after();
             const float inv = l > 0.f ? 1.f / l : 0.f;
-            bf16* orow = out + static_cast<long long>(it.row0 + qrow) * d + it.h * kHD;
+            bf16* orow = out + static_cast<long long>(it.row0 + qrow) * d + it.h * HD;
 #pragma unroll 1
-            for (int c = 0; c < kHD; c += 16) {
+            for (int c = 0; c < HD; c += 16) {
                 uint32_t v[16];
                 ptx::tmem_ld_x16(t_o + lane_off + c, v);
                 ptx::tmem_ld_wait();
@@ -650,11 +677,13 @@ bool prefill_attention_tc(const bf16* qkv, long long rows, bf16* out, const int*
         const char* e = std::getenv("HC_PREFILL_TC");  // 0 mma.sync, 1 one tile per CTA, 2 tile pairs
         return e ? std::atoi(e) : 2;
     }();
-    if (!enabled || hd != kHD || rows <= 0) return false;
+    if (!enabled || rows <= 0 || (hd != 128 && (hd != 64 || enabled == 1))) return false;
     static std::atomic<uint64_t> configured1{0}, configured2{0};
     max_dynamic_smem_once(prefill_tc_kernel, Smem::bytes, configured1);
-    max_dynamic_smem_once(prefill_tc2_kernel, Smem2::bytes, configured2);
-    const long long d3 = 3LL * H * kHD;
+    static std::atomic<uint64_t> configured3{0};
+    max_dynamic_smem_once(prefill_tc2_kernel<128>, Smem2<128>::bytes, configured2);
+    max_dynamic_smem_once(prefill_tc2_kernel<64>, Smem2<64>::bytes, configured3);
+    const long long d3 = 3LL * H * hd;
     const CUtensorMap tm = make_map(qkv, rows, d3, d3, kT);
     static const uint32_t lbo = [] {
         const char* e = std::getenv("HC_PREFILL_TC_LBO");
@@ -677,7 +706,12 @@ bool prefill_attention_tc(const bf16* qkv, long long rows, bf16* out, const int*
         const int n_pairs = (n_qt + 1) / 2;
         const long long items = static_cast<long long>(n_pairs) * H * n_req;
         const int grid = static_cast<int>(std::min<long long>(items, sms));
-        prefill_tc2_kernel<<<grid, kThreads2, Smem2::bytes, st>>>(tm, out, cu, n_req, n_pairs, H, scale, lbo, sbo);
+        if (hd == 128)
+            prefill_tc2_kernel<128><<<grid, kThreads2, Smem2<128>::bytes, st>>>(tm, out, cu, n_req, n_pairs, H, scale,
+                                                                                 lbo, sbo);
+        else
+            prefill_tc2_kernel<64><<<grid, kThreads2, Smem2<64>::bytes, st>>>(tm, out, cu, n_req, n_pairs, H, scale,
+                                                                               lbo, sbo);
     }
     return true;
 }

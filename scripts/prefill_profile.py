@@ -27,9 +27,12 @@ def main():
     ap.add_argument("--ratio", type=float, default=1.0 / 3.0)
     ap.add_argument("--reps", type=int, default=2)
     ap.add_argument("--arch", default="reference", choices=["reference", "opt"])
+    ap.add_argument("--heads", type=int, default=0, help="override num_heads (e.g. 2x the preset: head_dim 64)")
     a = ap.parse_args()
     from paper_2501_01792_b200 import api
     cfg = api.ModelConfig.preset(a.model)
+    if a.heads:
+        cfg.num_heads = a.heads
     cfg.num_layers = a.layers
     B, P, tpb = a.batch, a.prompt, cfg.tokens_per_block
     nb = math.ceil((P + 1) / tpb)

@@ -178,7 +178,8 @@ def test_decode_attention_ignores_unfilled_slots(native, splits):
 
 @pytest.mark.parametrize("n_req,P,H,hd", [(2, 37, 2, 128), (3, 130, 4, 64), (1, 256, 8, 128), (2, 1, 2, 128),
                                           (2, 64, 2, 64), (1, 321, 2, 128), (1, 640, 2, 128),
-                                          (3, 1000, 2, 128), (2, 129, 3, 128)])
+                                          (3, 1000, 2, 128), (2, 129, 3, 128), (1, 640, 2, 64),
+                                          (3, 1000, 4, 64), (2, 257, 12, 64)])
 def test_prefill_attention_causal(native, n_req, P, H, hd):
     from paper_2501_01792_b200.kernels import prefill_attention
     rng = np.random.default_rng(P)
