@@ -593,22 +593,33 @@ __global__ void __launch_bounds__(kThreads2, 1)
                     m = mx;
                     l *= alpha;
                 }
-                // p = 2^(s * sl - m) in one FFMA + MUFU; masked entries (-FLT_MAX * sl) underflow to 0
-                uint32_t pw[kT / 2];
-                uint32_t plw[Smem2<HD>::lo ? kT / 2 : 1];
+                // p = 2^(s * sl - m) in one FFMA + MUFU; masked entries (-FLT_MAX * sl) underflow to 0.
+                // Each 8-key chunk goes to the 128B-swizzled P tile as soon as it is packed
+                // (P_t is free: S_t(j) completing implies PV_t(j-1) did), so only one chunk
+                // of packed words is live at a time.
                 float2 l4[4] = {{0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}};
                 const float2 sl2 = make_float2(sl, sl), nm2 = make_float2(-m, -m);
 #pragma unroll
-                for (int i = 0; i < kT / 2; ++i) {
-                    const float2 y = ffma2(make_float2(__uint_as_float(sraw[2 * i]), __uint_as_float(sraw[2 * i + 1])),
-                                           sl2, nm2);
-                    const float2 pp = make_float2(ex2(y.x), ex2(y.y));
-                    l4[i % 4] = fadd2(l4[i % 4], pp);
-                    pw[i] = ptx::pack_bf16x2(pp.x, pp.y);
-                    if constexpr (Smem2<HD>::lo) {  // the bf16 residual of each P entry
-                        const float h0 = __uint_as_float(pw[i] << 16), h1 = __uint_as_float(pw[i] & 0xFFFF0000u);
-                        plw[i] = ptx::pack_bf16x2(pp.x - h0, pp.y - h1);
+                for (int c = 0; c < kT / 8; ++c) {
+                    uint32_t pw[4], plw[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int i = 4 * c + u;
+                        const float2 y = ffma2(make_float2(__uint_as_float(sraw[2 * i]), __uint_as_float(sraw[2 * i + 1])),
+                                               sl2, nm2);
+                        const float2 pp = make_float2(ex2(y.x), ex2(y.y));
+                        l4[u] = fadd2(l4[u], pp);
+                        pw[u] = ptx::pack_bf16x2(pp.x, pp.y);
+                        if constexpr (Smem2<HD>::lo) {  // the bf16 residual of each P entry
+                            const float h0 = __uint_as_float(pw[u] << 16), h1 = __uint_as_float(pw[u] & 0xFFFF0000u);
+                            plw[u] = ptx::pack_bf16x2(pp.x - h0, pp.y - h1);
+                        }
                     }
+                    const int box = c / 8, ch = c % 8;
+                    const uint32_t dst = pbase + box * kBox + ((ch ^ (r % 8)) * 16);
+                    sts128(dst, pw[0], pw[1], pw[2], pw[3]);
+                    if constexpr (Smem2<HD>::lo)
+                        sts128(dst + (Smem2<HD>::plo - Smem2<HD>::p), plw[0], plw[1], plw[2], plw[3]);
                 }
                 const float2 ls = fadd2(fadd2(l4[0], l4[1]), fadd2(l4[2], l4[3]));
                 l += ls.x + ls.y;
@@ -623,15 +634,6 @@ __global__ void __launch_bounds__(kThreads2, 1)
                         tmem_st_x16(t_o + lane_off + c, v);
                     }
                     tmem_st_wait();
-                }
-#pragma unroll
-                for (int c = 0; c < kT / 8; ++c) {  // 16-byte chunks of 8 keys, 128B swizzle
-                    const int box = c / 8, ch = c % 8;
-                    sts128(pbase + box * kBox + ((ch ^ (r % 8)) * 16), pw[4 * c], pw[4 * c + 1], pw[4 * c + 2],
-                           pw[4 * c + 3]);
-                    if constexpr (Smem2<HD>::lo)
-                        sts128(pbase + (Smem2<HD>::plo - Smem2<HD>::p) + box * kBox + ((ch ^ (r % 8)) * 16),
-                               plw[4 * c], plw[4 * c + 1], plw[4 * c + 2], plw[4 * c + 3]);
                 }
                 fence_async_smem();
                 ptx::tc_fence_before();
