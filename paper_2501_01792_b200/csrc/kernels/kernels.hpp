@@ -72,8 +72,9 @@ int attention_splits(int B, int H, int max_ctx, int tpb);
 // Causal prefill attention over ragged requests: request r owns rows
 // [cu[r], cu[r+1]) of qkv [rows x 3d] (Q|K|V per row); out [rows x d].
 // cu is a device array of n_req+1 offsets; max_len = max request length.
-// rows = rows of qkv (bounds of the tcgen05 path's TMA map). head_dim 128 runs
-// on tcgen05/TMEM (prefill_attention_tc.cu), 64 on mma.sync.
+// rows = rows of qkv (bounds of the tcgen05 path's TMA map). head_dim 64 and 128
+// run on tcgen05/TMEM (prefill_attention_tc.cu); the mma.sync kernel
+// (prefill_attention.cu) only under HC_PREFILL_TC=0.
 void prefill_attention(const bf16* qkv, bf16* out, const int* cu, int n_req, int max_len, int H, int hd,
                        float scale, cudaStream_t st, long long rows);
 

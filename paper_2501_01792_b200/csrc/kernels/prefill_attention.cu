@@ -2,6 +2,10 @@
 // request r attends to keys [0, t] of the same request; softmax(q.K^T*s).V,
 // s = 1/sqrt(hd), max-subtracted) over ragged requests packed end to end.
 //
+// prefill_attention() dispatches to the tcgen05 kernels (prefill_attention_tc.cu,
+// head_dim 64 and 128); the mma.sync kernel below is the comparison path kept
+// behind HC_PREFILL_TC=0 (and the fallback for other head dims):
+//
 // Tensor-core flash attention: one CTA (4 warps) per (64-query tile, head,
 // request); each warp owns 16 query rows. S = Q.K^T and O += P.V run on
 // mma.sync m16n8k16 bf16 (fp32 accumulate; P.V as hi+lo bf16 halves of P);
