@@ -8,7 +8,7 @@
  *   - every function returns int status: 0 ok, 1 InputError, 2 CapacityError,
  *     3 ConfigError, 4 CUDA/runtime error (errors.hpp:9-21); the message of
  *     the last failure on this thread is hc_last_error();
- *   - bf16 tensors cross the boundary as uint16_t bit patterns, fp64 as double;
+ *   - f16 tensors cross the boundary as uint16_t bit patterns, fp64 as double;
  *   - block kinds: 0 = KV, 1 = ACT; locations: 0 = host, 1 = gpu
  *     (cache.hpp:15-16);
  *   - matrices are row-major; reference-layout weights are [in x out]
@@ -50,7 +50,7 @@ int hc_model_validate(hc_model_config* cfg);
 int hc_model_preset(const char* name, hc_model_config* out);
 
 /* DecoderWeights::generate (model.cpp:94-117) + per-tensor rescale (rescale=1,
- * SURVEY.md §8(d)) + bf16 rounding, in device layout: emb [V x d],
+ * SURVEY.md §8(d)) + f16 rounding, in device layout: emb [V x d],
  * pos [max_seq x d], layers L x {Wqkv^T [3d x d], Wproj^T [d x d],
  * W1^T [f x d], W2^T [d x f]} (transposed, K-major). Any out may be NULL. */
 int hc_generate_weights(const hc_model_config* cfg, uint64_t seed, int max_seq, int rescale, uint16_t* emb,
@@ -190,7 +190,7 @@ int hc_engine_destroy(void* engine);
 int hc_engine_prefill(void* engine, int n, const char* const* ids, const int* offsets, const int* tokens);
 /* Bookkeeping-only admission + pattern-filled pools (benchmark setup). */
 int hc_engine_admit_synthetic(void* engine, int n, const char* const* ids, const int* prompt_lens, uint64_t seed);
-/* One decode step; x_out [n x d] bf16, logits [n x V] fp32, argmax [n]; any may be NULL. */
+/* One decode step; x_out [n x d] f16, logits [n x V] fp32, argmax [n]; any may be NULL. */
 int hc_engine_decode_step(void* engine, int n, const char* const* ids, const int* tokens, uint16_t* x_out,
                           float* logits, int* argmax);
 int hc_engine_free_request(void* engine, const char* id);
@@ -199,7 +199,7 @@ int hc_engine_configure_cache(void* engine, long kv_host, long kv_gpu, long act_
                               int mode, long alloc_act_host, long alloc_kv_host, int host_layers,
                               double recompute_ratio);
 /* forward_prompt (decoder.cpp:144-157) of one sequence without cache effects:
- * layer_inputs / k / v [L x n x d], out [n x d] (bf16); any may be NULL.
+ * layer_inputs / k / v [L x n x d], out [n x d] (f16); any may be NULL.
  * token_recompute_kv(ids, layer) (decoder.cpp:131-142) = (k, v)[layer]. */
 int hc_engine_forward_trace(void* engine, const int* ids, int n, uint16_t* layer_inputs, uint16_t* k, uint16_t* v,
                             uint16_t* out);
@@ -211,11 +211,11 @@ int hc_engine_layer_forward(void* engine, int layer, const uint16_t* x, int n, u
 int hc_engine_cache(void* engine, void** cache);
 /* Payload of one block at one layer (KV [2][H][tpb][hd], ACT [tpb][d]). */
 int hc_engine_read_block(void* engine, int kind, int loc, int pbn, int layer, uint16_t* out);
-/* Engine-held weights (bf16): layer >= 0 packed layer, -1 embedding [V x d],
+/* Engine-held weights (f16): layer >= 0 packed layer, -1 embedding [V x d],
  * -2 positional [max_seq x d]. */
 int hc_engine_read_weights(void* engine, int layer, uint16_t* out);  /* -3: final LN (arch 1) */
 int hc_engine_capture_inputs(void* engine, int on);
-/* Decode-time layer inputs of the last step, [L][n][d] bf16 (n = last batch). */
+/* Decode-time layer inputs of the last step, [L][n][d] f16 (n = last batch). */
 int hc_engine_captured_inputs(void* engine, uint16_t* out, long count);
 /* out11 = {step_ms, h2d_bytes, d2h_bytes, recompute_rows, recompute_ms, attn_ms, gemm_ms, launches,
  *          copy_ms, recompute_launches, store_ms} of the last decode step or prefill; the *_ms
@@ -236,10 +236,10 @@ int hc_engine_time_load_kv(void* engine, int n_tokens, int reps, double* seconds
 
 /* ------------------------------------------------------------- kernels ---
  * Single kernels of the path on host buffers (parity-test boundary). */
-/* C = A . W, W passed transposed (Wt [N x K]); epi 0 bf16, 1 relu bf16, 3 fp32. */
-int hc_gemm_bf16(int epi, int M, int N, int K, const uint16_t* A, const uint16_t* Wt, void* out, int bn);
+/* C = A . W, W passed transposed (Wt [N x K]); epi 0 f16, 1 relu f16, 3 fp32. */
+int hc_gemm_f16(int epi, int M, int N, int K, const uint16_t* A, const uint16_t* Wt, void* out, int bn);
 /* Split-K weight-streaming GEMM (epi 0 / 1), fp32 partials reduced in a second kernel. */
-int hc_gemm_bf16_splitk(int epi, int M, int N, int K, const uint16_t* A, const uint16_t* Wt, uint16_t* out, int bn,
+int hc_gemm_f16_splitk(int epi, int M, int N, int K, const uint16_t* A, const uint16_t* Wt, uint16_t* out, int bn,
                         int splits);
 /* recompute_kv_from_activation (decoder.cpp:123-129) into the paged layout. */
 int hc_recompute_kv_paged(int n_blocks, int tpb, int d, int heads, const uint16_t* act_pool, const uint16_t* wkv_t,

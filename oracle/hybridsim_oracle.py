@@ -194,32 +194,27 @@ def rescale_factors(cfg: ModelConfig) -> Dict[str, float]:
             "w_ffn1": s_f1, "w_ffn2": s_f2}
 
 
-def bf16_round(x: np.ndarray) -> np.ndarray:
-    """fp64 -> fp32 (RNE) -> bf16 (RNE), returned as fp64. Same rule as the
-    product's host conversion (csrc/host/model.cpp: to_bf16)."""
+def f16_round(x: np.ndarray) -> np.ndarray:
+    """fp64 -> fp32 (RNE) -> IEEE binary16 (RNE), returned as fp64. Same rule as
+    the product's host conversion (csrc/host/model.cpp: to_f16) and the GPU
+    draw (weights_gen.cu: __float2half_rn)."""
     f = np.ascontiguousarray(x, dtype=np.float32)
-    u = f.view(np.uint32).astype(np.uint64)
-    bias = ((u >> np.uint64(16)) & np.uint64(1)) + np.uint64(0x7FFF)
-    r = ((u + bias) >> np.uint64(16)) << np.uint64(16)
-    nan = np.isnan(f)
-    out = r.astype(np.uint32).view(np.float32).astype(np.float64)
-    out[nan] = np.nan
-    return out
+    return f.astype(np.float16).astype(np.float64)
 
 
-def to_bf16_bits(x: np.ndarray) -> np.ndarray:
-    return (bf16_round(x).astype(np.float32).view(np.uint32) >> 16).astype(np.uint16)
+def to_f16_bits(x: np.ndarray) -> np.ndarray:
+    return np.ascontiguousarray(x, dtype=np.float32).astype(np.float16).view(np.uint16)
 
 
-def bf16_bits_to_f64(b: np.ndarray) -> np.ndarray:
-    return (b.astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+def f16_bits_to_f64(b: np.ndarray) -> np.ndarray:
+    return np.ascontiguousarray(b, dtype=np.uint16).view(np.float16).astype(np.float64)
 
 
-def prepare_weights(w: DecoderWeights, rescale: bool = True, bf16: bool = True) -> DecoderWeights:
-    """Rescale then round every tensor to bf16 (values kept in fp64) so the
+def prepare_weights(w: DecoderWeights, rescale: bool = True, f16: bool = True) -> DecoderWeights:
+    """Rescale then round every tensor to fp16 (values kept in fp64) so the
     oracle consumes exactly the numbers the GPU consumes."""
     fac = rescale_factors(w.config) if rescale else {n: 1.0 for n in WEIGHT_NAMES}
-    rnd = bf16_round if bf16 else (lambda a: a)
+    rnd = f16_round if f16 else (lambda a: a)
     out = DecoderWeights(w.config, w.max_seq, rnd(w.embedding), rnd(w.positional))
     for lw in w.layers:
         out.layers.append({n: rnd(lw[n] * fac[n]) for n in WEIGHT_NAMES})
@@ -385,9 +380,9 @@ def generate_opt_extras(cfg: ModelConfig, seed: int):
     return layers, {"gamma": 1.0 + u[:d], "beta": u[d:]}
 
 
-def with_opt_extras(w: DecoderWeights, seed: int, bf16: bool = True) -> DecoderWeights:
-    """w plus the OPT extras, bf16-rounded like the GPU's copies."""
-    rnd = bf16_round if bf16 else (lambda a: a)
+def with_opt_extras(w: DecoderWeights, seed: int, f16: bool = True) -> DecoderWeights:
+    """w plus the OPT extras, fp16-rounded like the GPU's copies."""
+    rnd = f16_round if f16 else (lambda a: a)
     ex, lnf = generate_opt_extras(w.config, seed)
     return DecoderWeights(w.config, w.max_seq, w.embedding, w.positional, w.layers,
                           [{k: rnd(v) for k, v in e.items()} for e in ex], {k: rnd(v) for k, v in lnf.items()})

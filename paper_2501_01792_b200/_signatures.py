@@ -102,8 +102,8 @@ SIGNATURES = {
     "hc_engine_time_kv_gen": (i, [vp, i, i, dp]),
     "hc_engine_time_load_kv": (i, [vp, i, i, dp]),
     # kernels (host buffers in / out)
-    "hc_gemm_bf16": (i, [i, i, i, i, u16p, u16p, vp, i]),
-    "hc_gemm_bf16_splitk": (i, [i, i, i, i, u16p, u16p, u16p, i, i]),
+    "hc_gemm_f16": (i, [i, i, i, i, u16p, u16p, vp, i]),
+    "hc_gemm_f16_splitk": (i, [i, i, i, i, u16p, u16p, u16p, i, i]),
     "hc_recompute_kv_paged": (i, [i, i, i, i, u16p, u16p, ip, i, u16p, i]),
     "hc_decode_attention": (i, [i, i, i, i, u16p, u16p, l, u16p, l, ip, i, ip, ip, i, i, u16p]),
     "hc_prefill_attention": (i, [i, i, i, i, u16p, i, u16p]),

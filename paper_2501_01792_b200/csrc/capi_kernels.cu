@@ -40,22 +40,22 @@ struct DevBuf {
 
 extern "C" {
 
-// C[M x N] = A[M x K] . W  with W given transposed as Wt[N x K] (bf16 bits).
-// epi: 0 bf16, 1 relu bf16, 3 fp32 (out sized accordingly). bn: 0 = auto.
-int hc_gemm_bf16(int epi, int M, int N, int K, const uint16_t* A, const uint16_t* Wt, void* out,
+// C[M x N] = A[M x K] . W  with W given transposed as Wt[N x K] (f16 bits).
+// epi: 0 f16, 1 relu f16, 3 fp32 (out sized accordingly). bn: 0 = auto.
+int hc_gemm_f16(int epi, int M, int N, int K, const uint16_t* A, const uint16_t* Wt, void* out,
                  int bn) {
     return hc_guard([&] {
         if (epi != gemm::kStore && epi != gemm::kRelu && epi != gemm::kF32)
-            throw hc_input_error("hc_gemm_bf16: epi must be 0, 1 or 3");
+            throw hc_input_error("hc_gemm_f16: epi must be 0, 1 or 3");
         DevBuf<uint16_t> a(A, size_t(M) * K), w(Wt, size_t(N) * K);
         const size_t out_bytes = size_t(M) * N * (epi == gemm::kF32 ? 4 : 2);
         DevBuf<uint8_t> o(out_bytes);
         GemmCall c;
         c.epi = epi;
-        c.A = reinterpret_cast<const bf16*>(a.p);
+        c.A = reinterpret_cast<const f16*>(a.p);
         c.lda = K;
         c.a_rows = M;
-        c.B = reinterpret_cast<const bf16*>(w.p);
+        c.B = reinterpret_cast<const f16*>(w.p);
         c.ldb = K;
         c.M = M;
         c.N = N;
@@ -70,21 +70,21 @@ int hc_gemm_bf16(int epi, int M, int N, int K, const uint16_t* A, const uint16_t
     });
 }
 
-// Split-K variant of hc_gemm_bf16 (epi 0 / 1): fp32 partials over `splits`
+// Split-K variant of hc_gemm_f16 (epi 0 / 1): fp32 partials over `splits`
 // K ranges reduced by splitk_reduce — the weight-streaming decode GEMMs.
-int hc_gemm_bf16_splitk(int epi, int M, int N, int K, const uint16_t* A, const uint16_t* Wt, uint16_t* out, int bn,
+int hc_gemm_f16_splitk(int epi, int M, int N, int K, const uint16_t* A, const uint16_t* Wt, uint16_t* out, int bn,
                         int splits) {
     return hc_guard([&] {
-        if (epi != gemm::kStore && epi != gemm::kRelu) throw hc_input_error("hc_gemm_bf16_splitk: epi must be 0 or 1");
-        if (splits < 1) throw hc_input_error("hc_gemm_bf16_splitk: splits must be >= 1");
+        if (epi != gemm::kStore && epi != gemm::kRelu) throw hc_input_error("hc_gemm_f16_splitk: epi must be 0 or 1");
+        if (splits < 1) throw hc_input_error("hc_gemm_f16_splitk: splits must be >= 1");
         DevBuf<uint16_t> a(A, size_t(M) * K), w(Wt, size_t(N) * K), o(size_t(M) * N);
         DevBuf<float> ws(size_t(splits) * M * N);
         GemmCall c;
         c.epi = epi;
-        c.A = reinterpret_cast<const bf16*>(a.p);
+        c.A = reinterpret_cast<const f16*>(a.p);
         c.lda = K;
         c.a_rows = M;
-        c.B = reinterpret_cast<const bf16*>(w.p);
+        c.B = reinterpret_cast<const f16*>(w.p);
         c.ldb = K;
         c.M = M;
         c.N = N;
@@ -104,10 +104,10 @@ int hc_gemm_bf16_splitk(int epi, int M, int N, int K, const uint16_t* A, const u
 
 // Recompute K|V of the ACT-cached blocks straight into the paged KV layout
 // (north-star (2); recompute_kv_from_activation, decoder.cpp:123-129).
-//   act_pool  [n_blocks x tpb x d]        ACT block payloads (bf16 bits)
+//   act_pool  [n_blocks x tpb x d]        ACT block payloads (f16 bits)
 //   wkv_t     [2d x d]                     [W_K | W_V] transposed
 //   tiles     [n_tiles]                    first pool row of each 128-row tile
-//   kv_out    [n_blocks x 2 x H x tpb x hd] K|V blocks (bf16 bits)
+//   kv_out    [n_blocks x 2 x H x tpb x hd] K|V blocks (f16 bits)
 int hc_recompute_kv_paged(int n_blocks, int tpb, int d, int heads, const uint16_t* act_pool,
                           const uint16_t* wkv_t, const int* tiles, int n_tiles, uint16_t* kv_out, int bn) {
     return hc_guard([&] {
@@ -119,10 +119,10 @@ int hc_recompute_kv_paged(int n_blocks, int tpb, int d, int heads, const uint16_
         HC_CUDA(cudaMemset(o.p, 0, o.n * 2));
         GemmCall c;
         c.epi = gemm::kKvPaged;
-        c.A = reinterpret_cast<const bf16*>(a.p);
+        c.A = reinterpret_cast<const f16*>(a.p);
         c.lda = d;
         c.a_rows = static_cast<int>(rows);
-        c.B = reinterpret_cast<const bf16*>(w.p);
+        c.B = reinterpret_cast<const f16*>(w.p);
         c.ldb = d;
         c.M = static_cast<int>(rows);
         c.N = 2 * d;
@@ -159,15 +159,15 @@ int hc_decode_attention(int B, int H, int hd, int tpb, const uint16_t* q, const 
         if (splits <= 0) splits = attention_splits(B, H, max_ctx, tpb);
         DevBuf<float> work(size_t(B) * H * splits * (hd + 2));
         AttnCall c;
-        c.q = reinterpret_cast<const bf16*>(dq.p);
+        c.q = reinterpret_cast<const f16*>(dq.p);
         c.ldq = d;
-        c.out = reinterpret_cast<bf16*>(o.p);
+        c.out = reinterpret_cast<f16*>(o.p);
         c.blk_ref = dref.p;
         c.n_blocks = dnb.p;
         c.ctx_len = dctx.p;
         c.max_blocks = max_blocks;
-        c.region[0] = reinterpret_cast<const bf16*>(r0.p);
-        c.region[1] = reinterpret_cast<const bf16*>(r1.p);
+        c.region[0] = reinterpret_cast<const f16*>(r0.p);
+        c.region[1] = reinterpret_cast<const f16*>(r1.p);
         c.B = B;
         c.H = H;
         c.hd = hd;
@@ -190,7 +190,7 @@ int hc_prefill_attention(int n_req, int P, int H, int hd, const uint16_t* qkv, i
         std::vector<int> cu(n_req + 1);
         for (int r = 0; r <= n_req; ++r) cu[r] = r * P;
         DevBuf<int> dcu(cu.data(), cu.size());
-        prefill_attention(reinterpret_cast<const bf16*>(dq.p), reinterpret_cast<bf16*>(o.p), dcu.p, n_req, P, H, hd,
+        prefill_attention(reinterpret_cast<const f16*>(dq.p), reinterpret_cast<f16*>(o.p), dcu.p, n_req, P, H, hd,
                           scaled ? 1.0f / std::sqrt(static_cast<float>(hd)) : 1.0f, nullptr,
                           static_cast<long long>(n_req) * P);
         HC_CUDA(cudaGetLastError());

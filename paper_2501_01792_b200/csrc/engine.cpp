@@ -74,9 +74,9 @@ T* halloc(size_t n, bool mapped) {
 
 }  // namespace
 
-void gemm_rows(int epi, const bf16* A, int M, int K, const bf16* W, int N, void* out, long long ldc, cudaStream_t st,
-               long long lda = 0, float* ws = nullptr, size_t ws_floats = 0, const bf16* bias = nullptr,
-               const bf16* res = nullptr, long long ldr = 0);
+void gemm_rows(int epi, const f16* A, int M, int K, const f16* W, int N, void* out, long long ldc, cudaStream_t st,
+               long long lda = 0, float* ws = nullptr, size_t ws_floats = 0, const f16* bias = nullptr,
+               const f16* res = nullptr, long long ldr = 0);
 
 struct Engine::Impl {
     int L = 0, d = 0, H = 0, hd = 0, f = 0, V = 0, tpb = 0, B = 0, max_seq = 0, max_blocks = 0, Lp = 0, Lw = 0;
@@ -88,27 +88,27 @@ struct Engine::Impl {
     TpGroup* tp = nullptr;
     int tpr = 0, tpn = 1, Hg = 0, dg = 0, fg = 0;
     long act_cap_n = 0;  // ACT/host blocks per rank = ceil(act_host_cap / tpn)
-    bf16* wfull = nullptr;  // init only: one unsharded layer when tpn > 1
+    f16* wfull = nullptr;  // init only: one unsharded layer when tpn > 1
     bool owns(int pbn) const { return pbn % tpn == tpr; }
     int act_pos(int pbn) const { return static_cast<int>((pbn % tpn) * act_cap_n + pbn / tpn); }
-    bf16* lnf = nullptr;  // kArchOpt final LayerNorm gamma | beta [2d]
-    bf16* xn = nullptr;   // kArchOpt decode LN output [B x d]
-    bf16* pxn = nullptr;  // kArchOpt prefill LN1 output [prefill_rows x d]
+    f16* lnf = nullptr;  // kArchOpt final LayerNorm gamma | beta [2d]
+    f16* xn = nullptr;   // kArchOpt decode LN output [B x d]
+    f16* pxn = nullptr;  // kArchOpt prefill LN1 output [prefill_rows x d]
     size_t LE = 0, kvb = 0, actb = 0;
     LayerOffsets off{};        // this rank's packed layer (== offF when tpn == 1)
     LayerOffsets offF{};       // the unsharded packed layer
     size_t LEF = 0;
-    bf16 *emb = nullptr, *pos = nullptr;
-    bf16* w_all = nullptr;
-    bf16* wbuf[2] = {nullptr, nullptr};
+    f16 *emb = nullptr, *pos = nullptr;
+    f16* w_all = nullptr;
+    f16* wbuf[2] = {nullptr, nullptr};
     uint16_t* h_w = nullptr;
-    bf16 *kv_gpu = nullptr, *act_gpu = nullptr, *kvr = nullptr;
-    bf16 *kv_stage[2] = {nullptr, nullptr}, *act_stage[2] = {nullptr, nullptr};
-    bf16 *kv_host = nullptr, *act_host = nullptr;  // pinned, mapped (views into h_arena)
-    bf16* h_arena = nullptr;
+    f16 *kv_gpu = nullptr, *act_gpu = nullptr, *kvr = nullptr;
+    f16 *kv_stage[2] = {nullptr, nullptr}, *act_stage[2] = {nullptr, nullptr};
+    f16 *kv_host = nullptr, *act_host = nullptr;  // pinned, mapped (views into h_arena)
+    f16* h_arena = nullptr;
     size_t h_arena_elems = 0;
     long kv_host_cap = 0, kv_gpu_cap = 0, act_host_cap = 0, act_gpu_cap = 0;
-    bf16 *x[2] = {nullptr, nullptr}, *qkvb = nullptr, *att = nullptr, *proj = nullptr, *hbuf = nullptr;
+    f16 *x[2] = {nullptr, nullptr}, *qkvb = nullptr, *att = nullptr, *proj = nullptr, *hbuf = nullptr;
     float* logits = nullptr;
     int* amax = nullptr;
     float* attn_work = nullptr;
@@ -119,7 +119,7 @@ struct Engine::Impl {
     int* h_meta = nullptr;
     size_t meta_cap = 0;
     // prefill scratch
-    bf16 *px[2] = {nullptr, nullptr}, *pqkv = nullptr, *patt = nullptr, *pproj = nullptr, *ph = nullptr;
+    f16 *px[2] = {nullptr, nullptr}, *pqkv = nullptr, *patt = nullptr, *pproj = nullptr, *ph = nullptr;
     size_t prefill_rows = 0, prefill_chunk_rows = 0;
     cudaEvent_t loaded[2]{}, consumed[2]{}, stored[2]{}, h2d_act[2]{}, gathered[2]{}, ev0{}, ev1{}, tg0{}, tg1{},
         wpre{};
@@ -135,11 +135,11 @@ struct Engine::Impl {
     void require_configured() const {
         if (!configured) throw ConfigError("Engine: cache pools are not configured (configure_cache failed)");
     }
-    bf16* tr_kv = nullptr;  // [max_batch * max_blocks] KV blocks for token-recompute prefixes
+    f16* tr_kv = nullptr;  // [max_batch * max_blocks] KV blocks for token-recompute prefixes
     void ensure_tr() {
         if (!tr_kv) {
             clear_graphs();
-            tr_kv = dalloc<bf16>(static_cast<size_t>(B) * max_blocks * kvb);
+            tr_kv = dalloc<f16>(static_cast<size_t>(B) * max_blocks * kvb);
         }
     }
     // CUDA graphs of the decode step, keyed by the step's launch structure
@@ -190,7 +190,7 @@ struct Engine::Impl {
         HC_CUDA(cudaEventRecord(spans.back().b, s));
     }
 
-    void regions(int l, int slot, bf16* r[16]) const {
+    void regions(int l, int slot, f16* r[16]) const {
         for (int i = 0; i < 16; ++i) r[i] = nullptr;
         r[R_KV_STAGE] = kv_stage[slot];
         r[R_KV_GPU] = kv_gpu ? kv_gpu + static_cast<size_t>(l) * kv_gpu_cap * kvb : nullptr;
@@ -201,11 +201,11 @@ struct Engine::Impl {
         r[R_ACT_HOST] = act_host ? act_host + static_cast<size_t>(l % Lp) * act_cap_n * actb : nullptr;
         r[R_TOKREC] = tr_kv;
     }
-    const bf16* layer_w(int l, int slot) const { return w_all ? w_all + static_cast<size_t>(l) * LE : wbuf[slot]; }
+    const f16* layer_w(int l, int slot) const { return w_all ? w_all + static_cast<size_t>(l) * LE : wbuf[slot]; }
 
     // unsharded packed layer `full` (device) -> this rank's shard at dst
     // (device or pinned host; kind says which)
-    void extract_shard(const bf16* full, void* dstv, cudaMemcpyKind kind, cudaStream_t st) const {
+    void extract_shard(const f16* full, void* dstv, cudaMemcpyKind kind, cudaStream_t st) const {
         uint16_t* dst = static_cast<uint16_t*>(dstv);
         const uint16_t* F = reinterpret_cast<const uint16_t*>(full);
         const size_t D = d, Fd = f, g = tpr, DG = dg, FG = fg;
@@ -230,10 +230,10 @@ struct Engine::Impl {
 
     // ---- decoder-layer arithmetic shared by decode, prefill and traces ----
     bool opt() const { return arch == kArchOpt; }
-    const bf16* bias(const bf16* W, size_t o) const { return opt() ? W + o : nullptr; }
+    const f16* bias(const f16* W, size_t o) const { return opt() ? W + o : nullptr; }
     // LN1 (which = 1) / LN2 (2) of T rows of x into out for kArchOpt; the
     // reference arch has no LayerNorm and returns x itself
-    const bf16* ln(const bf16* W, int which, const bf16* x, int T, bf16* out, cudaStream_t st) const {
+    const f16* ln(const f16* W, int which, const f16* x, int T, f16* out, cudaStream_t st) const {
         if (!opt()) return x;
         layernorm_rows(x, d, W + (which == 1 ? off.ln1g : off.ln2g), W + (which == 1 ? off.ln1b : off.ln2b), out, d,
                        T, d, static_cast<float>(kLnEps), st);
@@ -241,7 +241,7 @@ struct Engine::Impl {
     }
     // qkv [T x 3dg] = LN1(x) . Wqkv (+ b_qkv) for this rank's heads
     // (qkv_generate, decoder.cpp:97-103)
-    void qkv(const bf16* W, const bf16* xa, int T, bf16* out, cudaStream_t st, float* ws = nullptr,
+    void qkv(const f16* W, const f16* xa, int T, f16* out, cudaStream_t st, float* ws = nullptr,
              size_t wsf = 0) const {
         gemm_rows(gemm::kStore, xa, T, d, W + off.wqkv, 3 * dg, out, 3 * dg, st, 0, ws, wsf, bias(W, off.bqkv));
     }
@@ -250,12 +250,12 @@ struct Engine::Impl {
     // W_proj / W2 are row slices, so their outputs are partial sums that one
     // all-reduce each completes (bias and residual enter once, on rank 0).
     // lnbuf may alias att.
-    void tail(const bf16* W, const bf16* att, const bf16* x, int T, bf16* proj, bf16* lnbuf, bf16* h, bf16* out,
+    void tail(const f16* W, const f16* att, const f16* x, int T, f16* proj, f16* lnbuf, f16* h, f16* out,
               cudaStream_t st, float* ws = nullptr, size_t wsf = 0) {
         if (tpn == 1) {  // bias + residual fused into the GEMM epilogues
             gemm_rows(gemm::kStore, att, T, d, W + off.wproj, d, proj, d, st, 0, ws, wsf, bias(W, off.bproj),
                       opt() ? x : nullptr, d);
-            const bf16* p2 = ln(W, 2, proj, T, lnbuf, st);
+            const f16* p2 = ln(W, 2, proj, T, lnbuf, st);
             gemm_rows(gemm::kRelu, p2, T, d, W + off.w1, f, h, f, st, 0, ws, wsf, bias(W, off.b1));
             gemm_rows(gemm::kStore, h, T, f, W + off.w2, d, out, d, st, 0, ws, wsf, bias(W, off.b2),
                       opt() ? proj : nullptr, d);
@@ -266,7 +266,7 @@ struct Engine::Impl {
         gemm_rows(gemm::kF32, att, T, dg, W + off.wproj, d, r, d, st, 0, ws, wsf);
         tp->all_reduce_sum(r, static_cast<size_t>(T) * d, st);
         add_bias_residual(r, bias(W, off.bproj), opt() ? x : nullptr, d, T, d, proj, st);
-        const bf16* p2 = ln(W, 2, proj, T, lnbuf, st);
+        const f16* p2 = ln(W, 2, proj, T, lnbuf, st);
         gemm_rows(gemm::kRelu, p2, T, d, W + off.w1, fg, h, fg, st, 0, ws, wsf, bias(W, off.b1));
         gemm_rows(gemm::kF32, h, T, fg, W + off.w2, d, r, d, st, 0, ws, wsf);
         tp->all_reduce_sum(r, static_cast<size_t>(T) * d, st);
@@ -286,7 +286,7 @@ struct Engine::Impl {
         return red;
     }
     // model output: LN_f(x) for kArchOpt (into out), x itself otherwise
-    const bf16* final_norm(const bf16* x, int T, bf16* out, cudaStream_t st) const {
+    const f16* final_norm(const f16* x, int T, f16* out, cudaStream_t st) const {
         if (!opt()) return x;
         layernorm_rows(x, d, lnf, lnf + d, out, d, T, d, static_cast<float>(kLnEps), st);
         return out;
@@ -314,21 +314,21 @@ struct Engine::Impl {
         if (!chunk_rows) chunk_rows = rows;
         if (rows > prefill_rows || chunk_rows > prefill_chunk_rows) clear_graphs();
         if (rows > prefill_rows) {
-            for (bf16* p : {px[0], px[1], pxn})
+            for (f16* p : {px[0], px[1], pxn})
                 if (p) cudaFree(p);
             prefill_rows = rows;
-            px[0] = dalloc<bf16>(rows * d);
-            px[1] = dalloc<bf16>(rows * d);
-            pxn = opt() ? dalloc<bf16>(rows * d) : nullptr;
+            px[0] = dalloc<f16>(rows * d);
+            px[1] = dalloc<f16>(rows * d);
+            pxn = opt() ? dalloc<f16>(rows * d) : nullptr;
         }
         if (chunk_rows > prefill_chunk_rows) {
-            for (bf16* p : {pqkv, patt, pproj, ph})
+            for (f16* p : {pqkv, patt, pproj, ph})
                 if (p) cudaFree(p);
             prefill_chunk_rows = chunk_rows;
-            pqkv = dalloc<bf16>(chunk_rows * 3 * d);
-            patt = dalloc<bf16>(chunk_rows * d);
-            pproj = dalloc<bf16>(chunk_rows * d);
-            ph = dalloc<bf16>(chunk_rows * f);
+            pqkv = dalloc<f16>(chunk_rows * 3 * d);
+            patt = dalloc<f16>(chunk_rows * d);
+            pproj = dalloc<f16>(chunk_rows * d);
+            ph = dalloc<f16>(chunk_rows * f);
         }
     }
 };
@@ -374,7 +374,7 @@ Engine::Engine(const ModelConfig& c, uint64_t seed, int max_seq, bool rescale, c
     const int d = m.d, f = m.f;
     // the unsharded layer (reference tags and layout), drawn in place or into
     // wfull and then cut to this rank's shard
-    auto draw_layer = [&](int l, bf16* dst) {
+    auto draw_layer = [&](int l, f16* dst) {
         uint16_t* L = reinterpret_cast<uint16_t*>(dst);
         const LayerOffsets& o = m.offF;
         const uint64_t base = 100 + static_cast<uint64_t>(l) * 8;  // model.cpp:90, 106-113
@@ -393,7 +393,7 @@ Engine::Engine(const ModelConfig& c, uint64_t seed, int max_seq, bool rescale, c
         }
     };
     for (int l = 0; l < (m.w_all ? m.L : m.Lw); ++l) {
-        bf16* shard = m.w_all ? m.w_all + static_cast<size_t>(l) * m.LE : m.wbuf[l & 1];
+        f16* shard = m.w_all ? m.w_all + static_cast<size_t>(l) * m.LE : m.wbuf[l & 1];
         if (m.tpn == 1) {
             draw_layer(l, shard);
         } else {
@@ -485,20 +485,20 @@ void Engine::init(const ModelConfig& c, int w_max_seq, const uint16_t* emb, cons
     HC_CUDA(cudaEventCreateWithFlags(&m.wpre, cudaEventDisableTiming));
 
     // tables
-    m.emb = dalloc<bf16>(static_cast<size_t>(m.V) * m.d);
-    m.pos = dalloc<bf16>(static_cast<size_t>(w_max_seq) * m.d);
+    m.emb = dalloc<f16>(static_cast<size_t>(m.V) * m.d);
+    m.pos = dalloc<f16>(static_cast<size_t>(w_max_seq) * m.d);
     if (emb) HC_CUDA(cudaMemcpy(m.emb, emb, static_cast<size_t>(m.V) * m.d * 2, cudaMemcpyHostToDevice));
     if (pos) HC_CUDA(cudaMemcpy(m.pos, pos, static_cast<size_t>(w_max_seq) * m.d * 2, cudaMemcpyHostToDevice));
     if (m.opt()) {
         if (!lnf) throw InputError("Engine: opt arch needs the final LayerNorm");
-        m.lnf = dalloc<bf16>(2 * static_cast<size_t>(m.d));
+        m.lnf = dalloc<f16>(2 * static_cast<size_t>(m.d));
         HC_CUDA(cudaMemcpy(m.lnf, lnf, 2 * static_cast<size_t>(m.d) * 2, cudaMemcpyHostToDevice));
-        m.xn = dalloc<bf16>(static_cast<size_t>(m.B) * m.d);
+        m.xn = dalloc<f16>(static_cast<size_t>(m.B) * m.d);
     }
 
     // weights (fill_layer == nullptr: the caller draws them on the device);
     // fill_layer delivers the unsharded layer, cut to the rank's shard here
-    if (m.tpn > 1) m.wfull = dalloc<bf16>(m.LEF);
+    if (m.tpn > 1) m.wfull = dalloc<f16>(m.LEF);
     std::vector<uint16_t> tmp(fill_layer && m.tpn > 1 ? m.LEF : 0);
     auto place = [&](int l, void* dst, cudaMemcpyKind kind) {
         fill_layer(ctx, l, tmp.data());
@@ -507,10 +507,10 @@ void Engine::init(const ModelConfig& c, int w_max_seq, const uint16_t* emb, cons
         HC_CUDA(cudaStreamSynchronize(s_compute_));
     };
     if (opt_.weights_on_device) {
-        m.w_all = dalloc<bf16>(m.LE * m.L);
+        m.w_all = dalloc<f16>(m.LE * m.L);
         std::vector<uint16_t> t1(fill_layer && m.tpn == 1 ? m.LE : 0);
         for (int l = 0; fill_layer && l < m.L; ++l) {
-            bf16* dst = m.w_all + static_cast<size_t>(l) * m.LE;
+            f16* dst = m.w_all + static_cast<size_t>(l) * m.LE;
             if (m.tpn > 1) {
                 place(l, dst, cudaMemcpyDeviceToDevice);
             } else {
@@ -526,8 +526,8 @@ void Engine::init(const ModelConfig& c, int w_max_seq, const uint16_t* emb, cons
             else
                 fill_layer(ctx, l, m.h_w + static_cast<size_t>(l) * m.LE);
         }
-        m.wbuf[0] = dalloc<bf16>(m.wsn * m.wsS);  // >= LE (padded slices when the stream is shared)
-        m.wbuf[1] = dalloc<bf16>(m.wsn * m.wsS);
+        m.wbuf[0] = dalloc<f16>(m.wsn * m.wsS);  // >= LE (padded slices when the stream is shared)
+        m.wbuf[1] = dalloc<f16>(m.wsn * m.wsS);
     }
     if (fill_layer && m.wfull) {
         HC_CUDA(cudaFree(m.wfull));
@@ -535,12 +535,12 @@ void Engine::init(const ModelConfig& c, int w_max_seq, const uint16_t* emb, cons
     }
 
     // decode scratch
-    m.x[0] = dalloc<bf16>(static_cast<size_t>(m.B) * m.d);
-    m.x[1] = dalloc<bf16>(static_cast<size_t>(m.B) * m.d);
-    m.qkvb = dalloc<bf16>(static_cast<size_t>(m.B) * 3 * m.d);
-    m.att = dalloc<bf16>(static_cast<size_t>(m.B) * m.d);
-    m.proj = dalloc<bf16>(static_cast<size_t>(m.B) * m.d);
-    m.hbuf = dalloc<bf16>(static_cast<size_t>(m.B) * m.f);
+    m.x[0] = dalloc<f16>(static_cast<size_t>(m.B) * m.d);
+    m.x[1] = dalloc<f16>(static_cast<size_t>(m.B) * m.d);
+    m.qkvb = dalloc<f16>(static_cast<size_t>(m.B) * 3 * m.d);
+    m.att = dalloc<f16>(static_cast<size_t>(m.B) * m.d);
+    m.proj = dalloc<f16>(static_cast<size_t>(m.B) * m.d);
+    m.hbuf = dalloc<f16>(static_cast<size_t>(m.B) * m.f);
     m.logits = dalloc<float>(static_cast<size_t>(m.B) * m.V);
     m.amax = dalloc<int>(m.B);
     m.splitk_floats = static_cast<size_t>(16) * m.B * std::max(3 * m.d, m.f);
@@ -563,7 +563,7 @@ void Engine::configure_cache(const PoolCaps& caps, bool kv_on_gpu, CacheMode mod
     HC_CUDA(cudaDeviceSynchronize());
     m.configured = false;
     m.clear_graphs();
-    for (bf16** p : {&m.kv_gpu, &m.act_gpu, &m.kvr, &m.kv_stage[0], &m.kv_stage[1], &m.act_stage[0], &m.act_stage[1]}) {
+    for (f16** p : {&m.kv_gpu, &m.act_gpu, &m.kvr, &m.kv_stage[0], &m.kv_stage[1], &m.act_stage[0], &m.act_stage[1]}) {
         if (*p) cudaFree(*p);
         *p = nullptr;
     }
@@ -592,8 +592,8 @@ void Engine::configure_cache(const PoolCaps& caps, bool kv_on_gpu, CacheMode mod
     token_mode_ = mode == CacheMode::TokenRecompute;
     rc_ids_.clear();
     assigner_ = std::make_unique<BlockAssigner>(*cache_, token_mode_ ? CacheMode::KvOnly : mode, alloc, 0.0);
-    m.kv_gpu = dalloc<bf16>(static_cast<size_t>(m.L) * m.kv_gpu_cap * m.kvb);
-    m.act_gpu = dalloc<bf16>(static_cast<size_t>(m.L) * m.act_gpu_cap * m.actb);
+    m.kv_gpu = dalloc<f16>(static_cast<size_t>(m.L) * m.kv_gpu_cap * m.kvb);
+    m.act_gpu = dalloc<f16>(static_cast<size_t>(m.L) * m.act_gpu_cap * m.actb);
     m.act_cap_n = (m.act_host_cap + m.tpn - 1) / m.tpn;
     // pinned, mapped host pools: one arena, kept across configure_cache calls
     // while it is large enough (pinning tens of GB takes seconds per call)
@@ -606,17 +606,17 @@ void Engine::configure_cache(const PoolCaps& caps, bool kv_on_gpu, CacheMode mod
             if (m.h_arena) HC_CUDA(cudaFreeHost(m.h_arena));
             m.h_arena = nullptr;  // stays null if the new allocation fails
             m.h_arena_elems = 0;
-            m.h_arena = halloc<bf16>(need, true);
+            m.h_arena = halloc<f16>(need, true);
             m.h_arena_elems = need;
         }
         m.kv_host = kv_e ? m.h_arena : nullptr;
         m.act_host = act_e ? m.h_arena + kv_e_al : nullptr;
     }
     for (int s = 0; s < 2; ++s) {
-        m.kv_stage[s] = dalloc<bf16>(static_cast<size_t>(m.kv_host_cap) * m.kvb);
-        m.act_stage[s] = dalloc<bf16>(static_cast<size_t>(m.tpn) * m.act_cap_n * m.actb);
+        m.kv_stage[s] = dalloc<f16>(static_cast<size_t>(m.kv_host_cap) * m.kvb);
+        m.act_stage[s] = dalloc<f16>(static_cast<size_t>(m.tpn) * m.act_cap_n * m.actb);
     }
-    m.kvr = dalloc<bf16>(static_cast<size_t>(m.act_gpu_cap + m.tpn * m.act_cap_n) * m.kvb);
+    m.kvr = dalloc<f16>(static_cast<size_t>(m.act_gpu_cap + m.tpn * m.act_cap_n) * m.kvb);
     // staging slots start zeroed: whole-chunk copies (D2H runs, TP all-gathers)
     // never move uninitialised bytes, even for slots no block occupies yet
     for (int s = 0; s < 2; ++s) {
@@ -719,9 +719,9 @@ void Engine::run_layers(int T, int l0, int l1, const int* d_cu, uint16_t* layer_
             HC_CUDA(cudaMemcpy(m.wbuf[slot], m.h_w + static_cast<size_t>(l % m.Lw) * m.LE, m.LE * 2,
                                cudaMemcpyHostToDevice));
         }
-        const bf16* W = m.layer_w(l, slot);
-        bf16* xin = m.px[l & 1];
-        bf16* xout = m.px[(l + 1) & 1];
+        const f16* W = m.layer_w(l, slot);
+        f16* xin = m.px[l & 1];
+        f16* xout = m.px[(l + 1) & 1];
         if (layer_inputs)
             HC_CUDA(cudaMemcpyAsync(layer_inputs + per * li, xin, per * 2, cudaMemcpyDeviceToHost, s_compute_));
         m.qkv(W, m.ln(W, 1, xin, T, m.pxn, s_compute_), T, m.pqkv, s_compute_);
@@ -738,7 +738,7 @@ void Engine::run_layers(int T, int l0, int l1, const int* d_cu, uint16_t* layer_
                           opt_.scaled ? 1.0f / std::sqrt(static_cast<float>(m.hd)) : 1.0f, s_compute_, T);
         m.tail(W, m.patt, xin, T, m.pproj, m.patt, m.ph, xout, s_compute_);
     }
-    const bf16* y = final_ln ? m.final_norm(m.px[l1 & 1], T, m.pxn, s_compute_) : m.px[l1 & 1];
+    const f16* y = final_ln ? m.final_norm(m.px[l1 & 1], T, m.pxn, s_compute_) : m.px[l1 & 1];
     if (out) HC_CUDA(cudaMemcpyAsync(out, y, per * 2, cudaMemcpyDeviceToHost, s_compute_));
     HC_CUDA(cudaGetLastError());
     HC_CUDA(cudaStreamSynchronize(s_compute_));
@@ -746,8 +746,8 @@ void Engine::run_layers(int T, int l0, int l1, const int* d_cu, uint16_t* layer_
 
 // ---------------------------------------------------------------------------
 // GEMM helpers (weights transposed [out][in]; see model.hpp)
-void gemm_rows(int epi, const bf16* A, int M, int K, const bf16* W, int N, void* out, long long ldc, cudaStream_t st,
-               long long lda, float* ws, size_t ws_floats, const bf16* bias, const bf16* res, long long ldr) {
+void gemm_rows(int epi, const f16* A, int M, int K, const f16* W, int N, void* out, long long ldc, cudaStream_t st,
+               long long lda, float* ws, size_t ws_floats, const f16* bias, const f16* res, long long ldr) {
     GemmCall c;
     c.epi = epi;
     c.A = A;
@@ -896,13 +896,13 @@ void Engine::prefill(const std::vector<std::string>& ids, const std::vector<std:
         }
         // the staging slot is free once layer l-2's stores have left
         if (stores && l >= 2) HC_CUDA(cudaStreamWaitEvent(s_compute_, m.stored[slot]));
-        const bf16* W = m.layer_w(l, slot);
-        bf16* R[16];
+        const f16* W = m.layer_w(l, slot);
+        f16* R[16];
         m.regions(l, slot, R);
-        bf16* xin = m.px[l & 1];
-        bf16* xout = m.px[(l + 1) & 1];
+        f16* xin = m.px[l & 1];
+        f16* xout = m.px[(l + 1) & 1];
         // the layer's GEMM input: x (reference arch) or LN1(x) (kArchOpt)
-        const bf16* xa = m.ln(W, 1, xin, T, m.pxn, s_compute_);
+        const f16* xa = m.ln(W, 1, xin, T, m.pxn, s_compute_);
         st.launches += m.opt();
         // activation-cache writer: this layer's input rows of every ACT block
         BlockScatter sa;
@@ -920,8 +920,8 @@ void Engine::prefill(const std::vector<std::string>& ids, const std::vector<std:
         scatter_act_blocks(sa, s_compute_);
         st.launches += sa.n_blocks > 0;
         for (const Chunk& c : chunks) {
-            const bf16* cin = xin + static_cast<size_t>(c.row0) * m.d;
-            bf16* cout = xout + static_cast<size_t>(c.row0) * m.d;
+            const f16* cin = xin + static_cast<size_t>(c.row0) * m.d;
+            f16* cout = xout + static_cast<size_t>(c.row0) * m.d;
             m.span_begin(profile_, s_compute_, 2);
             m.qkv(W, xa + static_cast<size_t>(c.row0) * m.d, c.rows, m.pqkv, s_compute_);
             m.span_end(profile_, s_compute_);
@@ -948,7 +948,7 @@ void Engine::prefill(const std::vector<std::string>& ids, const std::vector<std:
             HC_CUDA(cudaStreamWaitEvent(s_store_, m.consumed[slot]));
             m.span_begin(profile_, s_store_, 4);
             const size_t lp = static_cast<size_t>(l % m.Lp);
-            const bf16* own = m.act_stage[slot] + static_cast<size_t>(m.tpr) * m.act_cap_n * m.actb;
+            const f16* own = m.act_stage[slot] + static_cast<size_t>(m.tpr) * m.act_cap_n * m.actb;
             for (const Run& r : act_runs) {
                 const size_t bytes = static_cast<size_t>(r.count) * m.actb * 2;
                 HC_CUDA(cudaMemcpyAsync(m.act_host + (lp * m.act_cap_n + r.start) * m.actb,
@@ -1010,7 +1010,7 @@ void Engine::admit_synthetic(const std::vector<std::string>& ids, const std::vec
     }
     if (m.pools_filled) return;
     // activations ~U(-0.1,0.1) like the embeddings; K,V of matching scale
-    auto fill = [&](bf16* p, size_t n, uint64_t s) {
+    auto fill = [&](f16* p, size_t n, uint64_t s) {
         if (p && n) fill_pattern(p, n, s, 0.1f, s_compute_);
     };
     fill(m.kv_gpu, static_cast<size_t>(m.L) * m.kv_gpu_cap * m.kvb, seed + 1);
@@ -1209,7 +1209,7 @@ void Engine::decode_step(const std::vector<std::string>& ids, const int* tokens,
                 if (!m.w_all && !(prefetched && l < 2))  // layers 0/1 may have come with the previous step
                     stream_weights(l, slot, st);
                 const size_t lp = static_cast<size_t>(l % m.Lp);
-                bf16* own = m.act_stage[slot] + static_cast<size_t>(m.tpr) * m.act_cap_n * m.actb;
+                f16* own = m.act_stage[slot] + static_cast<size_t>(m.tpr) * m.act_cap_n * m.actb;
                 for (const Run& r : act_runs) {
                     const size_t bytes = static_cast<size_t>(r.count) * m.actb * 2;
                     HC_CUDA(cudaMemcpyAsync(own + static_cast<size_t>(r.start) * m.actb,
@@ -1239,17 +1239,17 @@ void Engine::decode_step(const std::vector<std::string>& ids, const int* tokens,
                 HC_CUDA(cudaEventRecord(m.loaded[slot], s_copy_));
                 HC_CUDA(cudaStreamWaitEvent(s_compute_, m.loaded[slot]));
             }
-            const bf16* W = m.layer_w(l, slot);
-            bf16* R[16];
+            const f16* W = m.layer_w(l, slot);
+            f16* R[16];
             m.regions(l, slot, R);
-            bf16* xin = m.x[l & 1];
-            bf16* xout = m.x[(l + 1) & 1];
+            f16* xin = m.x[l & 1];
+            f16* xout = m.x[(l + 1) & 1];
             if (n_rc) {
                 // token recompute: full layer l over every prefix (FullLayer(rc) FLOPs,
                 // flops.cpp:20-22), its K|V written into the prefix blocks
                 m.span_begin(profile_, s_compute_, 0);
-                bf16* pin = m.px[l & 1];
-                bf16* pout = m.px[(l + 1) & 1];
+                f16* pin = m.px[l & 1];
+                f16* pout = m.px[(l + 1) & 1];
                 m.qkv(W, m.ln(W, 1, pin, n_rc, m.pxn, s_compute_), n_rc, m.pqkv, s_compute_);
                 st.launches += m.opt();
                 BlockScatter sk;
@@ -1278,7 +1278,7 @@ void Engine::decode_step(const std::vector<std::string>& ids, const int* tokens,
                 HC_CUDA(cudaMemcpyAsync(captured_.data() + static_cast<size_t>(l) * n * m.d, xin,
                                         static_cast<size_t>(n) * m.d * 2, cudaMemcpyDeviceToHost, s_compute_));
             // the layer's GEMM input (and ACT payload): x, or LN1(x) for kArchOpt
-            const bf16* xa = m.ln(W, 1, xin, n, m.xn, s_compute_);
+            const f16* xa = m.ln(W, 1, xin, n, m.xn, s_compute_);
             st.launches += m.opt();
             AppendCall ap;
             std::copy(R, R + 16, ap.region);
@@ -1366,7 +1366,7 @@ void Engine::decode_step(const std::vector<std::string>& ids, const int* tokens,
             else
                 HC_CUDA(cudaEventRecord(m.consumed[slot], s_compute_));
         }
-        const bf16* xf = m.final_norm(m.x[m.L & 1], n, m.xn, s_compute_);
+        const f16* xf = m.final_norm(m.x[m.L & 1], n, m.xn, s_compute_);
         st.launches += m.opt();
         if (lo || ao) {
             gemm_rows(gemm::kF32, xf, n, m.d, m.emb, m.V, m.logits, m.V, s_compute_);
@@ -1548,10 +1548,10 @@ void Engine::read_block(BlockKind kind, Location loc, int pbn, int layer, uint16
     const size_t be = kv ? m.kvb : m.actb;
     HC_CUDA(cudaStreamSynchronize(s_compute_));
     if (loc == Location::GpuMem) {
-        const bf16* base = kv ? m.kv_gpu : m.act_gpu;
+        const f16* base = kv ? m.kv_gpu : m.act_gpu;
         HC_CUDA(cudaMemcpy(out, base + (static_cast<size_t>(layer) * cap + pbn) * be, be * 2, cudaMemcpyDeviceToHost));
     } else {
-        const bf16* base = kv ? m.kv_host : m.act_host;
+        const f16* base = kv ? m.kv_host : m.act_host;
         const long hcap = kv ? cap : m.act_cap_n;
         const int idx = kv ? pbn : pbn / m.tpn;
         std::memcpy(out, base + (static_cast<size_t>(layer % m.Lp) * hcap + idx) * be, be * 2);
@@ -1567,11 +1567,11 @@ double Engine::time_kv_gen(int n_tokens, int reps) {
     const long stage_rows = static_cast<long>(m.tpn) * m.act_cap_n * m.tpb;
     const long cap_rows = std::max(stage_rows, m.act_gpu_cap * m.tpb);
     if (n_tokens > cap_rows) throw InputError("time_kv_gen: more tokens than the ACT pools hold");
-    const bf16* A = stage_rows >= n_tokens ? m.act_stage[0] : m.act_gpu;
+    const f16* A = stage_rows >= n_tokens ? m.act_stage[0] : m.act_gpu;
     m.w_prefetched = false;  // wbuf[0] is reloaded with layer 0 below
     if (!m.w_all)
         HC_CUDA(cudaMemcpy(m.wbuf[0], m.h_w, m.LE * 2, cudaMemcpyHostToDevice));
-    const bf16* W = m.layer_w(0, 0);
+    const f16* W = m.layer_w(0, 0);
     std::vector<int> tiles;
     for (int r = 0; r < n_tokens; r += gemm::BM) tiles.push_back(r);
     m.ensure_meta(tiles.size());

@@ -98,7 +98,7 @@ public:
 
     // One decode step for the listed requests (generation_step semantics,
     // decoder.cpp:159-174, batched). Outputs are optional (nullptr = skip):
-    // x_out [n x d] bf16 bits, logits [n x V] fp32 (tied head x.E^T),
+    // x_out [n x d] f16 bits, logits [n x V] fp32 (tied head x.E^T),
     // argmax [n].
     void decode_step(const std::vector<std::string>& ids, const int* tokens, uint16_t* x_out, float* logits,
                      int* argmax);
@@ -114,7 +114,7 @@ public:
 
     // forward_prompt (decoder.cpp:144-157) of one sequence on the GPU without
     // touching the cache: per-layer inputs X, K, V ([L][n][d]) and the output
-    // [n][d], bf16 bits. token_recompute_kv(ids, k) = (K, V)[k].
+    // [n][d], f16 bits. token_recompute_kv(ids, k) = (K, V)[k].
     void forward_trace(const std::vector<int>& ids, uint16_t* layer_inputs, uint16_t* k, uint16_t* v,
                        uint16_t* out);
     // One layer of forward_prompt on caller-given input rows x [T x d]
@@ -122,10 +122,10 @@ public:
     // K, V [T x d] and the layer output [T x d]. Teacher-forced parity.
     void layer_forward(int layer, const uint16_t* x, int T, uint16_t* k, uint16_t* v, uint16_t* out);
 
-    // Payload of one block at one layer (bf16 bits; KV: [2][H][tpb][hd],
+    // Payload of one block at one layer (f16 bits; KV: [2][H][tpb][hd],
     // ACT: [tpb][d]) — for parity tests of the cache writers.
     void read_block(BlockKind kind, Location loc, int pbn, int layer, uint16_t* out);
-    // Engine-held weights (bf16 bits): layer >= 0 packed layer (model.hpp
+    // Engine-held weights (f16 bits): layer >= 0 packed layer (model.hpp
     // layout), -1 embedding [V x d], -2 positional [max_seq x d], -3 final
     // LayerNorm gamma|beta [2d] (kArchOpt).
     void read_weights(int layer, uint16_t* out);

@@ -48,20 +48,39 @@ uint64_t mix_seed(uint64_t seed, uint64_t tag) {
     return r.next();
 }
 
-uint16_t to_bf16(double x) {
+uint16_t to_f16(double x) {
+    // fp64 -> fp32 (RNE, the C++ conversion) -> IEEE binary16 (RNE), with
+    // subnormals, overflow to inf and quiet NaNs — what __float2half_rn does
     const float f = static_cast<float>(x);
     uint32_t u;
     std::memcpy(&u, &f, 4);
-    if ((u & 0x7f800000u) == 0x7f800000u && (u & 0x007fffffu)) return static_cast<uint16_t>((u >> 16) | 0x40);
-    u += 0x7fffu + ((u >> 16) & 1u);
-    return static_cast<uint16_t>(u >> 16);
+    const uint32_t sign = (u >> 16) & 0x8000u;
+    const int exp = static_cast<int>((u >> 23) & 0xffu);
+    uint32_t mant = u & 0x7fffffu;
+    if (exp == 0xff) return static_cast<uint16_t>(sign | 0x7c00u | (mant ? 0x200u | (mant >> 13) : 0u));
+    const int e = exp - 127 + 15;
+    if (e >= 31) return static_cast<uint16_t>(sign | 0x7c00u);
+    if (e <= 0) {  // binary16 subnormal (or zero)
+        if (e < -10) return static_cast<uint16_t>(sign);
+        mant |= 0x800000u;
+        const int shift = 14 - e;
+        uint32_t h = mant >> shift;
+        const uint32_t rem = mant & ((1u << shift) - 1u), half = 1u << (shift - 1);
+        if (rem > half || (rem == half && (h & 1u))) ++h;
+        return static_cast<uint16_t>(sign | h);
+    }
+    uint32_t h = (static_cast<uint32_t>(e) << 10) | (mant >> 13);
+    const uint32_t rem = mant & 0x1fffu;
+    if (rem > 0x1000u || (rem == 0x1000u && (h & 1u))) ++h;  // a carry into the exponent is exact (up to inf)
+    return static_cast<uint16_t>(sign | h);
 }
 
-double from_bf16(uint16_t b) {
-    const uint32_t u = static_cast<uint32_t>(b) << 16;
-    float f;
-    std::memcpy(&f, &u, 4);
-    return f;
+double from_f16(uint16_t b) {
+    const int exp = (b >> 10) & 0x1f, mant = b & 0x3ff;
+    const double s = (b & 0x8000) ? -1.0 : 1.0;
+    if (exp == 0x1f) return mant ? std::nan("") : s * INFINITY;
+    if (exp == 0) return s * std::ldexp(static_cast<double>(mant), -24);
+    return s * std::ldexp(static_cast<double>(mant | 0x400), exp - 25);
 }
 
 void rescale_factors(const ModelConfig& c, double out[6]) {
@@ -102,7 +121,7 @@ size_t HostWeights::layer_elems() const { return LayerOffsets::of(config, arch).
 namespace {
 
 // Draw a rows x cols U(-0.1, 0.1) matrix from stream `seed` (model.cpp:82-87)
-// and store scale * value transposed into dst[cols x rows] as bf16. The
+// and store scale * value transposed into dst[cols x rows] as f16. The
 // counter-based generator lets threads split the draw sequence.
 void draw_transposed(uint16_t* dst, int rows, int cols, uint64_t seed, double scale) {
     const size_t n = static_cast<size_t>(rows) * cols;
@@ -115,7 +134,7 @@ void draw_transposed(uint16_t* dst, int rows, int cols, uint64_t seed, double sc
                 const uint64_t z = SplitMix64::mix(seed + (i + 1) * 0x9e3779b97f4a7c15ULL);
                 const double u = static_cast<double>(z >> 11) * 0x1.0p-53;
                 const double v = -0.1 + (0.1 - -0.1) * u;
-                dst[static_cast<size_t>(c) * rows + r] = to_bf16(v * scale);
+                dst[static_cast<size_t>(c) * rows + r] = to_f16(v * scale);
             }
         }
     };
@@ -138,7 +157,7 @@ void draw_plain(uint16_t* dst, int rows, int cols, uint64_t seed) {
         for (size_t i = i0; i < i1; ++i) {
             const uint64_t z = SplitMix64::mix(seed + (i + 1) * 0x9e3779b97f4a7c15ULL);
             const double u = static_cast<double>(z >> 11) * 0x1.0p-53;
-            dst[i] = to_bf16(-0.1 + (0.1 - -0.1) * u);
+            dst[i] = to_f16(-0.1 + (0.1 - -0.1) * u);
         }
     };
     std::vector<std::thread> ts;
@@ -176,7 +195,7 @@ void draw_vec(uint16_t* dst, size_t n, uint64_t seed, size_t blk) {
     for (size_t i = 0; i < n; ++i) {
         const uint64_t z = SplitMix64::mix(seed + (i + 1) * 0x9e3779b97f4a7c15ULL);
         const double u = -0.1 + (0.1 - -0.1) * (static_cast<double>(z >> 11) * 0x1.0p-53);
-        dst[i] = to_bf16(blk && (i / blk) % 2 == 0 ? 1.0 + u : u);
+        dst[i] = to_f16(blk && (i / blk) % 2 == 0 ? 1.0 + u : u);
     }
 }
 }  // namespace
@@ -218,13 +237,13 @@ HostWeights weights_from_f64(const ModelConfig& config, int max_seq, const doubl
     const int d = c.hidden_dim, f = c.ffn_dim;
     w.embedding.resize(static_cast<size_t>(c.vocab_size) * d);
     w.positional.resize(static_cast<size_t>(max_seq) * d);
-    for (size_t i = 0; i < w.embedding.size(); ++i) w.embedding[i] = to_bf16(emb[i]);
-    for (size_t i = 0; i < w.positional.size(); ++i) w.positional[i] = to_bf16(pos[i]);
+    for (size_t i = 0; i < w.embedding.size(); ++i) w.embedding[i] = to_f16(emb[i]);
+    for (size_t i = 0; i < w.positional.size(); ++i) w.positional[i] = to_f16(pos[i]);
     const LayerOffsets off = LayerOffsets::of(c);
     w.layers.resize(off.total * c.num_layers);
     auto put_t = [](uint16_t* dst, const double* src, int rows, int cols) {
         for (int r = 0; r < rows; ++r)
-            for (int k = 0; k < cols; ++k) dst[static_cast<size_t>(k) * rows + r] = to_bf16(src[static_cast<size_t>(r) * cols + k]);
+            for (int k = 0; k < cols; ++k) dst[static_cast<size_t>(k) * rows + r] = to_f16(src[static_cast<size_t>(r) * cols + k]);
     };
     for (int l = 0; l < c.num_layers; ++l) {
         uint16_t* L = w.layer(l);
@@ -258,11 +277,11 @@ HostWeights weights_from_f64_opt(const ModelConfig& config, int max_seq, const d
         const size_t dst[10] = {o.bqkv, o.bqkv + d, o.bqkv + 2 * d, o.bproj, o.b1, o.b2, o.ln1g, o.ln1b, o.ln2g, o.ln2b};
         for (int k = 0; k < 10; ++k) {
             const size_t n = k == 4 ? f : d;
-            for (size_t i = 0; i < n; ++i) L[dst[k] + i] = to_bf16(e[k][i]);
+            for (size_t i = 0; i < n; ++i) L[dst[k] + i] = to_f16(e[k][i]);
         }
     }
     w.final_ln.resize(2 * d);
-    for (size_t i = 0; i < 2 * d; ++i) w.final_ln[i] = to_bf16(final_ln[i]);
+    for (size_t i = 0; i < 2 * d; ++i) w.final_ln[i] = to_f16(final_ln[i]);
     return w;
 }
 

@@ -4,7 +4,7 @@
 // Weights are drawn exactly as the reference draws them (one SplitMix64
 // stream per tensor, U(-0.1, 0.1), identical tags), then rescaled per tensor
 // (the reference init has no LayerNorm / residual and blows
-// up ~10x per layer) and rounded to bf16. Device layout is transposed
+// up ~10x per layer) and rounded to f16. Device layout is transposed
 // ([out][in], K-major) for the tcgen05 GEMM:
 //   layer l: Wqkv^T [3d x d] | Wproj^T [d x d] | W1^T [f x d] | W2^T [d x f]
 // packed contiguously so one copy streams a whole layer.
@@ -47,9 +47,9 @@ struct SplitMix64 {
 
 uint64_t mix_seed(uint64_t seed, uint64_t tag);
 
-// fp64 -> fp32 (RNE) -> bf16 (RNE) bits.
-uint16_t to_bf16(double x);
-double from_bf16(uint16_t b);
+// fp64 -> fp32 (RNE) -> f16 (RNE) bits.
+uint16_t to_f16(double x);
+double from_f16(uint16_t b);
 
 // Per-tensor rescale factors (index: 0 q,1 k,2 v,3 proj,4 ffn1,5 ffn2).
 void rescale_factors(const ModelConfig& c, double out[6]);
@@ -65,14 +65,14 @@ void rescale_factors(const ModelConfig& c, double out[6]);
 //                   parity is pinned only by the oracle's restatement.
 enum Arch : int { kArchReference = 0, kArchOpt = 1 };
 
-// Extras of kArchOpt (bf16, drawn like the matrices: one SplitMix64 stream
+// Extras of kArchOpt (f16, drawn like the matrices: one SplitMix64 stream
 // per tag, U(-0.1, 0.1); tags the reference leaves unused):
 //   layer l, tag 100+8l+6: b_q | b_k | b_v | b_o | b_1 [f] | b_2   (raw draws)
 //   layer l, tag 100+8l+7: u -> gamma1 = 1+u | beta1 = u | gamma2 = 1+u | beta2 = u
 //   tag 2 (final LayerNorm): gamma_f = 1+u | beta_f = u
 constexpr double kLnEps = 1e-5;
 
-// Host copy of the bf16 weights in device layout.
+// Host copy of the f16 weights in device layout.
 struct HostWeights {
     ModelConfig config;
     int arch = kArchReference;
@@ -99,7 +99,7 @@ struct LayerOffsets {
     static LayerOffsets of(const ModelConfig& c, int arch = kArchReference, int tp = 1);
 };
 
-// DecoderWeights::generate (model.cpp:94-117) + rescale + bf16 + transpose.
+// DecoderWeights::generate (model.cpp:94-117) + rescale + f16 + transpose.
 // rescale=false keeps the raw U(-0.1, 0.1) draws (parity with the unmodified
 // reference init at toy depth).
 HostWeights generate_weights(const ModelConfig& config, uint64_t seed, int max_seq, bool rescale = true);

@@ -25,18 +25,18 @@ namespace {
 constexpr int kWarps = 4;
 constexpr float kLog2e = 1.4426950408889634f;
 
-__device__ __forceinline__ void load8(const bf16* p, float (&f)[8]) {
+__device__ __forceinline__ void load8(const f16* p, float (&f)[8]) {
     const uint4 u = __ldg(reinterpret_cast<const uint4*>(p));
-    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+    const __half2* h = reinterpret_cast<const __half2*>(&u);
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-        const float2 v = __bfloat1622float2(h[i]);
+        const float2 v = __half22float2(h[i]);
         f[2 * i] = v.x;
         f[2 * i + 1] = v.y;
     }
 }
 
-__device__ __forceinline__ uint4 ldg16(const bf16* p) {
+__device__ __forceinline__ uint4 ldg16(const f16* p) {
     uint4 r;
     asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
                  : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
@@ -45,10 +45,10 @@ __device__ __forceinline__ uint4 ldg16(const bf16* p) {
 }
 
 __device__ __forceinline__ void unpack8(const uint4& u, float (&f)[8]) {
-    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+    const __half2* h = reinterpret_cast<const __half2*>(&u);
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-        const float2 v = __bfloat1622float2(h[i]);
+        const float2 v = __half22float2(h[i]);
         f[2 * i] = v.x;
         f[2 * i + 1] = v.y;
     }
@@ -96,7 +96,7 @@ __global__ void __launch_bounds__(kWarps * 32)
     const int* refs = c.blk_ref + static_cast<long long>(b) * c.max_blocks;
     for (int blk = blk_begin + warp; blk < blk_end; blk += kWarps) {
         const int ref = refs[blk];
-        const bf16* base = c.region[ref >> 28] + static_cast<long long>(ref & 0x0FFFFFFF) * block_elems + head_off;
+        const f16* base = c.region[ref >> 28] + static_cast<long long>(ref & 0x0FFFFFFF) * block_elems + head_off;
         const int valid = (blk == nb - 1) ? ctx - (nb - 1) * TPB : TPB;
         uint4 kr[ITERS], vr[ITERS];
 #pragma unroll
@@ -175,7 +175,7 @@ __global__ void __launch_bounds__(kWarps * 32)
             O += sm_acc[w][threadIdx.x] * f;
         }
         if (c.splits == 1) {
-            c.out[static_cast<long long>(b) * d + h * HD + threadIdx.x] = __float2bfloat16(L > 0.f ? O / L : 0.f);
+            c.out[static_cast<long long>(b) * d + h * HD + threadIdx.x] = __float2half_rn(L > 0.f ? O / L : 0.f);
         } else {
             float* w = c.work + (static_cast<long long>(bh) * c.splits + split) * (HD + 2);
             w[threadIdx.x] = O;
@@ -206,7 +206,7 @@ __global__ void attn_combine_kernel(const AttnCall c) {
             L += ws[HD + 1] * f;
             O += ws[col] * f;
         }
-        c.out[static_cast<long long>(b) * d + h * HD + col] = __float2bfloat16(L > 0.f ? O / L : 0.f);
+        c.out[static_cast<long long>(b) * d + h * HD + col] = __float2half_rn(L > 0.f ? O / L : 0.f);
     }
 }
 

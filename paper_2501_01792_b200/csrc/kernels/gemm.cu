@@ -34,14 +34,14 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 
 }  // namespace
 
-// 2-D bf16 tensor [rows x cols] with row stride ld (elements); box = box_rows x 64.
+// 2-D f16 tensor [rows x cols] with row stride ld (elements); box = box_rows x 64.
 CUtensorMap make_map(const void* ptr, long long rows, long long cols, long long ld, int box_rows) {
     CUtensorMap m;
     cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
     cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * 2};
     cuuint32_t box[2] = {static_cast<cuuint32_t>(gemm::BK), static_cast<cuuint32_t>(box_rows)};
     cuuint32_t estr[2] = {1, 1};
-    const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims,
+    const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(ptr), dims,
                                    strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                                    CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -173,7 +173,7 @@ void run_gemm(const GemmCall& c, cudaStream_t st) {
     p.hd = c.hd;
     p.blk_off = c.blk_off;
     if ((c.bias || c.res) && (c.epi == gemm::kF32 || c.epi == gemm::kSplitF32))
-        throw std::invalid_argument("gemm: bias / residual apply to bf16 epilogues only");
+        throw std::invalid_argument("gemm: bias / residual apply to f16 epilogues only");
     if ((c.bias && reinterpret_cast<uintptr_t>(c.bias) % 16) ||
         (c.res && (reinterpret_cast<uintptr_t>(c.res) % 16 || (c.ldr * 2) % 16)))
         throw std::invalid_argument("gemm: bias / residual must be 16-byte aligned");
@@ -249,7 +249,7 @@ void run_gemm(const GemmCall& c, cudaStream_t st) {
     if (p.splits > 1 && c.epi == gemm::kF32)
         splitk_reduce_f32(c.ws, p.splits, c.M, c.N, static_cast<float*>(c.out), st);
     else if (p.splits > 1)
-        splitk_reduce(c.ws, p.splits, c.M, c.N, static_cast<bf16*>(c.out), c.epi == gemm::kRelu, st, c.bias, c.res,
+        splitk_reduce(c.ws, p.splits, c.M, c.N, static_cast<f16*>(c.out), c.epi == gemm::kRelu, st, c.bias, c.res,
                       c.ldr);
 }
 

@@ -1,6 +1,6 @@
 // Persistent warp-specialised tcgen05 GEMM for sm_100a.
 //
-//   C[M x N] = A[M x K] * B[N x K]^T     (bf16 in, fp32 accumulate in TMEM)
+//   C[M x N] = A[M x K] * B[N x K]^T     (f16 in, fp32 accumulate in TMEM)
 //
 // A: activations, row-major (K contiguous). B: weights stored transposed
 // ([out][in], K contiguous), so both operands are K-major and TMA loads
@@ -12,8 +12,8 @@
 // the MMAs of tile i+1; an S-stage smem ring overlaps TMA with MMA.
 //
 // Epilogues (one template instance each):
-//   kStore      bf16 row-major C
-//   kRelu       bf16 relu(C)                       (FFN1, decoder.cpp:118-119)
+//   kStore      f16 row-major C
+//   kRelu       f16 relu(C)                       (FFN1, decoder.cpp:118-119)
 //   kKvPaged    recompute K|V written straight into the paged KV block layout
 //               [blk][K|V][head][tok][hd]  (north-star (2), decoder.cpp:123-129)
 //   kF32        fp32 row-major (logits)
@@ -42,10 +42,10 @@ struct Params {
     // [s*kb_per_split, (s+1)*kb_per_split) and writes fp32 partials to
     // out + (s*M + row)*ldc
     int splits, kb_per_split;
-    // optional epilogue operands (bf16; applied before relu, not to fp32 outputs):
+    // optional epilogue operands (f16; applied before relu, not to fp32 outputs):
     // C[m][n] += bias[n] + res[m * ldr + n]
-    const __nv_bfloat16* bias;
-    const __nv_bfloat16* res;
+    const __half* bias;
+    const __half* res;
     long long ldr;
 };
 
@@ -85,16 +85,16 @@ __device__ __forceinline__ void tile_coords(int tile, const Params& p, int& m_id
     n_idx = within / gm;
 }
 
-// acc[0..16) += 16 consecutive bf16 at src (32-byte aligned run)
-__device__ __forceinline__ void add16(float (&acc)[16], const __nv_bfloat16* src) {
+// acc[0..16) += 16 consecutive f16 at src (32-byte aligned run)
+__device__ __forceinline__ void add16(float (&acc)[16], const __half* src) {
     const uint4* s4 = reinterpret_cast<const uint4*>(src);
 #pragma unroll
     for (int q = 0; q < 2; ++q) {
         const uint4 u = __ldg(s4 + q);
-        const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+        const __half2* h2 = reinterpret_cast<const __half2*>(&u);
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-            const float2 f = __bfloat1622float2(h2[i]);
+            const float2 f = __half22float2(h2[i]);
             acc[8 * q + 2 * i] += f.x;
             acc[8 * q + 2 * i + 1] += f.y;
         }
@@ -123,9 +123,9 @@ __device__ __forceinline__ void epilogue_chunk(const Params& p, int row, int col
                 a = fmaxf(a, 0.f);
                 b = fmaxf(b, 0.f);
             }
-            h[j] = ptx::pack_bf16x2(a, b);
+            h[j] = ptx::pack_f16x2(a, b);
         }
-        __nv_bfloat16* dst;
+        __half* dst;
         if constexpr (EPI == kKvPaged) {
             const int blk = row / p.tpb + p.blk_off;
             const int t = row - (row / p.tpb) * p.tpb;
@@ -134,11 +134,11 @@ __device__ __forceinline__ void epilogue_chunk(const Params& p, int row, int col
             const int head = rem / p.hd;
             const int c = rem - head * p.hd;
             const long long block_elems = 2LL * p.d * p.tpb;
-            dst = static_cast<__nv_bfloat16*>(p.out) + blk * block_elems +
+            dst = static_cast<__half*>(p.out) + blk * block_elems +
                   static_cast<long long>(part) * p.d * p.tpb + static_cast<long long>(head) * p.tpb * p.hd +
                   t * p.hd + c;
         } else {
-            dst = static_cast<__nv_bfloat16*>(p.out) + static_cast<long long>(row) * p.ldc + col;
+            dst = static_cast<__half*>(p.out) + static_cast<long long>(row) * p.ldc + col;
         }
         ptx::st_global_v4(dst, h[0], h[1], h[2], h[3]);
         ptx::st_global_v4(dst + 8, h[4], h[5], h[6], h[7]);
@@ -218,7 +218,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     } else if (warp == 1) {
         if (lane == 0) {
-            constexpr uint32_t idesc = ptx::idesc_bf16_f32(BM, BN);
+            constexpr uint32_t idesc = ptx::idesc_f16_f32(BM, BN);
             int stage = 0;
             uint32_t phase = 0;
             int as = 0;
@@ -237,7 +237,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                     for (int k = 0; k < BK / 16; ++k) {
                         // +32 B per 16-element K step inside the 128 B swizzle atom
-                        ptx::mma_bf16_ss(d_tmem, a_desc + 2 * k, b_desc + 2 * k, idesc, ((kb - kb0) | k) != 0);
+                        ptx::mma_f16_ss(d_tmem, a_desc + 2 * k, b_desc + 2 * k, idesc, ((kb - kb0) | k) != 0);
                     }
                     ptx::mma_commit(&empty[stage]);
                     if (++stage == S) {
@@ -410,7 +410,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         }
     } else if (warp == 1) {
         if (lane == 0 && rank == 0) {
-            constexpr uint32_t idesc = ptx::idesc_bf16_f32(2 * BM, BN);
+            constexpr uint32_t idesc = ptx::idesc_f16_f32(2 * BM, BN);
             int stage = 0;
             uint32_t phase = 0;
             int as = 0;
@@ -426,7 +426,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     const uint64_t b_desc = ptx::sw128_kmajor_desc(ptx::smem_u32(smem_b + stage * C::kBBytes));
 #pragma unroll
                     for (int k = 0; k < BK / 16; ++k)
-                        ptx::mma_bf16_ss_pair(d_tmem, a_desc + 2 * k, b_desc + 2 * k, idesc, (kb | k) != 0);
+                        ptx::mma_f16_ss_pair(d_tmem, a_desc + 2 * k, b_desc + 2 * k, idesc, (kb | k) != 0);
                     ptx::mma_commit_pair_mc(&empty[stage], 0x3);
                     if (++stage == S) {
                         stage = 0;

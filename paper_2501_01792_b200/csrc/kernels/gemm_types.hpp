@@ -7,6 +7,6 @@ namespace hc::gemm {
 enum Epi : int { kStore = 0, kRelu = 1, kKvPaged = 2, kF32 = 3, kSplitF32 = 4 };
 
 constexpr int BM = 128;  // rows per M tile (UMMA M)
-constexpr int BK = 64;   // K per pipeline stage (one 128-byte swizzle atom of bf16)
+constexpr int BK = 64;   // K per pipeline stage (one 128-byte swizzle atom of f16)
 
 }  // namespace hc::gemm

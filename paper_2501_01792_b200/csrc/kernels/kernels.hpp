@@ -1,22 +1,22 @@
 // Host-side launch API for every CUDA kernel of the hybrid-cache decode path.
 // No torch types; plain device pointers + a stream.
 #pragma once
-#include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
 
 namespace hc {
 
-using bf16 = __nv_bfloat16;
+using f16 = __half;
 
 // ---------------------------------------------------------------- GEMM ----
 struct GemmCall {
     int epi = 0;                 // gemm::Epi
-    const bf16* A = nullptr;     // [a_rows x K], row stride lda (elements)
+    const f16* A = nullptr;     // [a_rows x K], row stride lda (elements)
     long long lda = 0;
     int a_rows = 0;              // rows addressable by TMA (OOB rows read as 0)
-    const bf16* B = nullptr;     // [N x K] (weights transposed), row stride ldb
+    const f16* B = nullptr;     // [N x K] (weights transposed), row stride ldb
     long long ldb = 0;
     int M = 0, N = 0, K = 0;     // logical problem (rows >= M are not stored)
     const int* m_tile_rows = nullptr;  // device array of explicit tile first rows
@@ -30,16 +30,16 @@ struct GemmCall {
     float* ws = nullptr;         // split-K workspace (fp32); null disables split-K
     size_t ws_floats = 0;
     int splits = 0;              // 0 = planner (pick_split), else forced split count
-    // bf16 epilogue operands (kStore / kRelu / kKvPaged): C += bias[n] + res[m*ldr + n]
+    // f16 epilogue operands (kStore / kRelu / kKvPaged): C += bias[n] + res[m*ldr + n]
     // before relu (OPT linear biases and residual connections)
-    const bf16* bias = nullptr;
-    const bf16* res = nullptr;
+    const f16* bias = nullptr;
+    const f16* res = nullptr;
     long long ldr = 0;
 };
-// out[m][n] = bf16(epi(sum_s ws[s][m][n] + bias[n] + res[m*ldr + n])) — the
+// out[m][n] = f16(epi(sum_s ws[s][m][n] + bias[n] + res[m*ldr + n])) — the
 // split-K finish (relu, bias, res optional)
-void splitk_reduce(const float* ws, int splits, int M, int N, bf16* out, bool relu, cudaStream_t st,
-                   const bf16* bias = nullptr, const bf16* res = nullptr, long long ldr = 0);
+void splitk_reduce(const float* ws, int splits, int M, int N, f16* out, bool relu, cudaStream_t st,
+                   const f16* bias = nullptr, const f16* res = nullptr, long long ldr = 0);
 void run_gemm(const GemmCall& c, cudaStream_t st);
 int num_sms();
 
@@ -48,16 +48,16 @@ int num_sms();
 // For request b: blocks blk_ref[b*max_blocks + i], i < n_blocks[b], each a
 // packed (region << 28 | index) into one of 4 region base pointers; the last
 // block holds ctx_len[b] - (n_blocks[b]-1)*tpb tokens. Block layout:
-// [K|V][head][tpb][hd] bf16. q: [B x d] (row stride ldq), out: [B x d].
+// [K|V][head][tpb][hd] f16. q: [B x d] (row stride ldq), out: [B x d].
 struct AttnCall {
-    const bf16* q = nullptr;
+    const f16* q = nullptr;
     long long ldq = 0;
-    bf16* out = nullptr;
+    f16* out = nullptr;
     const int* blk_ref = nullptr;
     const int* n_blocks = nullptr;
     const int* ctx_len = nullptr;
     int max_blocks = 0;
-    const bf16* region[16] = {};
+    const f16* region[16] = {};
     int B = 0, H = 0, hd = 0, tpb = 0;
     float scale = 1.f;
     // split-K workspace (fp32): [B*H*splits*(hd+2)]; nullptr -> no split
@@ -75,12 +75,12 @@ int attention_splits(int B, int H, int max_ctx, int tpb);
 // rows = rows of qkv (bounds of the tcgen05 path's TMA map). head_dim 64 and 128
 // run on tcgen05/TMEM (prefill_attention_tc.cu); the mma.sync kernel
 // (prefill_attention.cu) only under HC_PREFILL_TC=0.
-void prefill_attention(const bf16* qkv, bf16* out, const int* cu, int n_req, int max_len, int H, int hd,
+void prefill_attention(const f16* qkv, f16* out, const int* cu, int n_req, int max_len, int H, int hd,
                        float scale, cudaStream_t st, long long rows);
 
 // --------------------------------------------------------------- misc ----
-// X[i] = E[ids[i]] + Pos[pos[i]]   (decoder.cpp:65-95), bf16 out
-void embed(const bf16* E, const bf16* Pos, const int* ids, const int* pos, int n, int d, bf16* X,
+// X[i] = E[ids[i]] + Pos[pos[i]]   (decoder.cpp:65-95), f16 out
+void embed(const f16* E, const f16* Pos, const int* ids, const int* pos, int n, int d, f16* X,
            long long ldx, cudaStream_t st);
 
 // Token-slot writes of the new decode token (activation-cache writer / KV
@@ -92,12 +92,12 @@ void embed(const bf16* E, const bf16* Pos, const int* ids, const int* pos, int n
 //   kv_append:  K|V columns of qkv[b] -> KV block token slot (layout
 //               [K|V][head][tpb][hd]) of dev_ref[b] / host_ref[b].
 struct AppendCall {
-    const bf16* src = nullptr;      // act: X [B x d]; kv: qkv [B x 3d] (K at +d, V at +2d)
+    const f16* src = nullptr;      // act: X [B x d]; kv: qkv [B x 3d] (K at +d, V at +2d)
     long long ld = 0;
     const int* dev_ref = nullptr;
     const int* host_ref = nullptr;
     const int* tok = nullptr;
-    bf16* region[16] = {};
+    f16* region[16] = {};
     int B = 0, d = 0, H = 0, hd = 0, tpb = 0;
 };
 void act_append(const AppendCall& c, cudaStream_t st);
@@ -106,27 +106,27 @@ void kv_append(const AppendCall& c, cudaStream_t st);
 // Prefill scatter of whole blocks: block i takes rows [src_row[i],
 // src_row[i] + n_tok[i]) of src and writes them to block dst_ref[i].
 struct BlockScatter {
-    const bf16* src = nullptr;      // act: X rows [d]; kv: qkv rows [3d]
+    const f16* src = nullptr;      // act: X rows [d]; kv: qkv rows [3d]
     long long ld = 0;
     const int* src_row = nullptr;
     const int* n_tok = nullptr;
     const int* dst_ref = nullptr;
-    bf16* region[16] = {};
+    f16* region[16] = {};
     int n_blocks = 0, d = 0, H = 0, hd = 0, tpb = 0;
 };
 void scatter_act_blocks(const BlockScatter& c, cudaStream_t st);
 void scatter_kv_blocks(const BlockScatter& c, cudaStream_t st);
 
 // y[r] = (x[r] - mean_r) / sqrt(var_r + eps) * gamma + beta over rows r < n of
-// width d (kArchOpt LayerNorms); bf16 in/out, fp32 statistics.
-void layernorm_rows(const bf16* x, long long ldx, const bf16* gamma, const bf16* beta, bf16* y, long long ldy, int n,
+// width d (kArchOpt LayerNorms); f16 in/out, fp32 statistics.
+void layernorm_rows(const f16* x, long long ldx, const f16* gamma, const f16* beta, f16* y, long long ldy, int n,
                     int d, float eps, cudaStream_t st);
 
 // out[i] = sum_j src[j*n + i] for i < n, j < parts (in-process all-reduce)
 void sum_rows_f32(const float* src, int parts, size_t n, float* out, cudaStream_t st);
-// out[m][n] = bf16(sum[m][n] + bias[n] + res[m*ldr + n]) (bias / res optional):
+// out[m][n] = f16(sum[m][n] + bias[n] + res[m*ldr + n]) (bias / res optional):
 // the finish of a tensor-parallel all-reduce (W_proj, W2 partial sums)
-void add_bias_residual(const float* sum, const bf16* bias, const bf16* res, long long ldr, int M, int N, bf16* out,
+void add_bias_residual(const float* sum, const f16* bias, const f16* res, long long ldr, int M, int N, f16* out,
                        cudaStream_t st);
 // fp32 split-K finish: out[m][n] = sum_s ws[s][m][n]
 void splitk_reduce_f32(const float* ws, int splits, int M, int N, float* out, cudaStream_t st);
@@ -135,14 +135,14 @@ void splitk_reduce_f32(const float* ws, int splits, int M, int N, float* out, cu
 void argmax_rows(const float* logits, int B, int V, int* out, cudaStream_t st);
 
 // DecoderWeights::generate draws on the GPU (bit-exact with host/model.cpp):
-// U(-0.1, 0.1) stream `seed`, times scale (if apply_scale), -> bf16 bits;
+// U(-0.1, 0.1) stream `seed`, times scale (if apply_scale), -> f16 bits;
 // transposed: dst[c*rows + r] = value(r, c) of the reference's [rows x cols].
 void gen_weights_transposed(uint16_t* dst, int rows, int cols, uint64_t seed, double scale, bool apply_scale,
                             cudaStream_t st);
 void gen_weights_plain(uint16_t* dst, size_t n, uint64_t seed, cudaStream_t st);
 
-// fill a bf16 buffer with a deterministic hash pattern in [-a, a]
-void fill_pattern(bf16* dst, size_t n, uint64_t seed, float amp, cudaStream_t st);
+// fill a f16 buffer with a deterministic hash pattern in [-a, a]
+void fill_pattern(f16* dst, size_t n, uint64_t seed, float amp, cudaStream_t st);
 
 inline int pack_ref(int region, int index) { return (region << 28) | index; }
 

@@ -12,28 +12,28 @@ namespace hc {
 
 namespace {
 
-__global__ void embed_kernel(const bf16* __restrict__ E, const bf16* __restrict__ Pos, const int* __restrict__ ids,
-                             const int* __restrict__ pos, int d, bf16* __restrict__ X, long long ldx) {
+__global__ void embed_kernel(const f16* __restrict__ E, const f16* __restrict__ Pos, const int* __restrict__ ids,
+                             const int* __restrict__ pos, int d, f16* __restrict__ X, long long ldx) {
     const int r = blockIdx.x;
-    const bf16* e = E + static_cast<long long>(ids[r]) * d;
-    const bf16* p = Pos + static_cast<long long>(pos[r]) * d;
-    bf16* x = X + r * ldx;
+    const f16* e = E + static_cast<long long>(ids[r]) * d;
+    const f16* p = Pos + static_cast<long long>(pos[r]) * d;
+    f16* x = X + r * ldx;
     for (int c = threadIdx.x * 8; c < d; c += blockDim.x * 8) {
         const uint4 a = *reinterpret_cast<const uint4*>(e + c);
         const uint4 b = *reinterpret_cast<const uint4*>(p + c);
-        const __nv_bfloat162* ha = reinterpret_cast<const __nv_bfloat162*>(&a);
-        const __nv_bfloat162* hb = reinterpret_cast<const __nv_bfloat162*>(&b);
+        const __half2* ha = reinterpret_cast<const __half2*>(&a);
+        const __half2* hb = reinterpret_cast<const __half2*>(&b);
         uint32_t o[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-            const float2 fa = __bfloat1622float2(ha[i]), fb = __bfloat1622float2(hb[i]);
-            o[i] = ptx::pack_bf16x2(fa.x + fb.x, fa.y + fb.y);
+            const float2 fa = __half22float2(ha[i]), fb = __half22float2(hb[i]);
+            o[i] = ptx::pack_f16x2(fa.x + fb.x, fa.y + fb.y);
         }
         *reinterpret_cast<uint4*>(x + c) = make_uint4(o[0], o[1], o[2], o[3]);
     }
 }
 
-__device__ __forceinline__ bf16* ref_ptr(bf16* const* region, int ref, long long block_elems) {
+__device__ __forceinline__ f16* ref_ptr(f16* const* region, int ref, long long block_elems) {
     return region[ref >> 28] + static_cast<long long>(ref & 0x0FFFFFFF) * block_elems;
 }
 
@@ -43,11 +43,11 @@ __global__ void act_append_kernel(const AppendCall c) {
     const int refs[2] = {c.dev_ref ? c.dev_ref[b] : -1, c.host_ref ? c.host_ref[b] : -1};
     const int t = c.tok[b];
     const long long block_elems = static_cast<long long>(c.tpb) * c.d;
-    const bf16* src = c.src + b * c.ld;
+    const f16* src = c.src + b * c.ld;
 #pragma unroll
     for (int k = 0; k < 2; ++k) {
         if (refs[k] < 0) continue;
-        bf16* dst = ref_ptr(c.region, refs[k], block_elems) + static_cast<long long>(t) * c.d;
+        f16* dst = ref_ptr(c.region, refs[k], block_elems) + static_cast<long long>(t) * c.d;
         for (int x = threadIdx.x * 8; x < c.d; x += blockDim.x * 8)
             *reinterpret_cast<uint4*>(dst + x) = *reinterpret_cast<const uint4*>(src + x);
     }
@@ -59,17 +59,17 @@ __global__ void kv_append_kernel(const AppendCall c) {
     const int refs[2] = {c.dev_ref ? c.dev_ref[b] : -1, c.host_ref ? c.host_ref[b] : -1};
     const int t = c.tok[b];
     const long long block_elems = 2LL * c.tpb * c.d;
-    const bf16* src = c.src + b * c.ld + c.d;  // K at +d, V at +2d
+    const f16* src = c.src + b * c.ld + c.d;  // K at +d, V at +2d
 #pragma unroll
     for (int k = 0; k < 2; ++k) {
         if (refs[k] < 0) continue;
-        bf16* blk = ref_ptr(c.region, refs[k], block_elems);
+        f16* blk = ref_ptr(c.region, refs[k], block_elems);
         for (int x = threadIdx.x * 8; x < 2 * c.d; x += blockDim.x * 8) {
             const int part = x / c.d;
             const int rem = x - part * c.d;
             const int h = rem / c.hd;
             const int cc = rem - h * c.hd;
-            bf16* dst = blk + static_cast<long long>(part) * c.d * c.tpb + static_cast<long long>(h) * c.tpb * c.hd +
+            f16* dst = blk + static_cast<long long>(part) * c.d * c.tpb + static_cast<long long>(h) * c.tpb * c.hd +
                         t * c.hd + cc;
             *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(src + x);
         }
@@ -81,8 +81,8 @@ __global__ void scatter_act_kernel(const BlockScatter c) {
     const int i = blockIdx.x;
     const int n = c.n_tok[i];
     const long long block_elems = static_cast<long long>(c.tpb) * c.d;
-    bf16* blk = ref_ptr(c.region, c.dst_ref[i], block_elems);
-    const bf16* src = c.src + static_cast<long long>(c.src_row[i]) * c.ld;
+    f16* blk = ref_ptr(c.region, c.dst_ref[i], block_elems);
+    const f16* src = c.src + static_cast<long long>(c.src_row[i]) * c.ld;
     const int per_row = c.d / 8;
     // rows past n_tok (a partial last block) are zeroed: the block's bytes
     // are deterministic wherever they are copied (HBM staging -> pinned host)
@@ -97,8 +97,8 @@ __global__ void scatter_kv_kernel(const BlockScatter c) {
     const int i = blockIdx.x;
     const int n = c.n_tok[i];
     const long long block_elems = 2LL * c.tpb * c.d;
-    bf16* blk = ref_ptr(c.region, c.dst_ref[i], block_elems);
-    const bf16* src = c.src + static_cast<long long>(c.src_row[i]) * c.ld + c.d;
+    f16* blk = ref_ptr(c.region, c.dst_ref[i], block_elems);
+    const f16* src = c.src + static_cast<long long>(c.src_row[i]) * c.ld + c.d;
     // destination-major walk: consecutive threads write consecutive 16 B of a
     // head's [tpb][hd] run
     const int chunks_per_head = c.tpb * c.hd / 8;
@@ -155,20 +155,20 @@ __global__ void argmax_kernel(const float* __restrict__ logits, int V, int* __re
 }
 
 // 8 columns per thread; partial s of element (m, n) at ws[(s*M + m)*N + n]
-// acc[0..8) += 8 consecutive bf16 at src (16-byte aligned)
-__device__ __forceinline__ void add8(float (&acc)[8], const bf16* src) {
+// acc[0..8) += 8 consecutive f16 at src (16-byte aligned)
+__device__ __forceinline__ void add8(float (&acc)[8], const f16* src) {
     const uint4 u = __ldg(reinterpret_cast<const uint4*>(src));
-    const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+    const __half2* h2 = reinterpret_cast<const __half2*>(&u);
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-        const float2 f = __bfloat1622float2(h2[i]);
+        const float2 f = __half22float2(h2[i]);
         acc[2 * i] += f.x;
         acc[2 * i + 1] += f.y;
     }
 }
 
-__global__ void splitk_reduce_kernel(const float* __restrict__ ws, int splits, int M, int N, bf16* __restrict__ out,
-                                     int relu, const bf16* __restrict__ bias, const bf16* __restrict__ res,
+__global__ void splitk_reduce_kernel(const float* __restrict__ ws, int splits, int M, int N, f16* __restrict__ out,
+                                     int relu, const f16* __restrict__ bias, const f16* __restrict__ res,
                                      long long ldr) {
     const size_t n8 = static_cast<size_t>(M) * N / 8;
     const size_t plane = static_cast<size_t>(M) * N;
@@ -193,13 +193,13 @@ __global__ void splitk_reduce_kernel(const float* __restrict__ ws, int splits, i
                 x = fmaxf(x, 0.f);
                 y = fmaxf(y, 0.f);
             }
-            o[j] = ptx::pack_bf16x2(x, y);
+            o[j] = ptx::pack_f16x2(x, y);
         }
         *reinterpret_cast<uint4*>(out + i * 8) = make_uint4(o[0], o[1], o[2], o[3]);
     }
 }
 
-__global__ void fill_pattern_kernel(bf16* dst, size_t n, uint64_t seed, float amp) {
+__global__ void fill_pattern_kernel(f16* dst, size_t n, uint64_t seed, float amp) {
     for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
          i += static_cast<size_t>(gridDim.x) * blockDim.x) {
         uint64_t z = seed + (i + 1) * 0x9E3779B97F4A7C15ull;
@@ -207,12 +207,12 @@ __global__ void fill_pattern_kernel(bf16* dst, size_t n, uint64_t seed, float am
         z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
         z ^= z >> 31;
         const float u = static_cast<float>(z >> 40) * (1.0f / 16777216.0f);
-        dst[i] = __float2bfloat16(amp * (2.f * u - 1.f));
+        dst[i] = __float2half_rn(amp * (2.f * u - 1.f));
     }
 }
 
 // LayerNorm of one row per CTA (256 threads): the row stays in registers
-// (8 bf16 per 16-byte chunk, <= kLnChunks chunks per thread), two-pass fp32
+// (8 f16 per 16-byte chunk, <= kLnChunks chunks per thread), two-pass fp32
 // mean / variance with warp-shuffle + smem block reductions.
 constexpr int kLnThreads = 256, kLnChunks = 8;  // d <= 16384
 
@@ -230,10 +230,10 @@ __device__ __forceinline__ float block_sum(float v, float* red) {
 }
 
 __global__ void __launch_bounds__(kLnThreads)
-    layernorm_kernel(const bf16* __restrict__ x, long long ldx, const bf16* __restrict__ g,
-                     const bf16* __restrict__ b, bf16* __restrict__ y, long long ldy, int d, float eps) {
+    layernorm_kernel(const f16* __restrict__ x, long long ldx, const f16* __restrict__ g,
+                     const f16* __restrict__ b, f16* __restrict__ y, long long ldy, int d, float eps) {
     __shared__ float red[kLnThreads / 32];
-    const bf16* xr = x + blockIdx.x * ldx;
+    const f16* xr = x + blockIdx.x * ldx;
     const int nch = d / 8;
     float v[kLnChunks][8];
     float s = 0.f;
@@ -242,10 +242,10 @@ __global__ void __launch_bounds__(kLnThreads)
         const int ch = threadIdx.x + k * kLnThreads;
         if (ch < nch) {
             const uint4 u = __ldg(reinterpret_cast<const uint4*>(xr) + ch);
-            const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+            const __half2* h = reinterpret_cast<const __half2*>(&u);
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
-                const float2 f = __bfloat1622float2(h[i]);
+                const float2 f = __half22float2(h[i]);
                 v[k][2 * i] = f.x;
                 v[k][2 * i + 1] = f.y;
                 s += f.x + f.y;
@@ -260,20 +260,20 @@ __global__ void __launch_bounds__(kLnThreads)
 #pragma unroll
             for (int i = 0; i < 8; ++i) q += (v[k][i] - mean) * (v[k][i] - mean);
     const float rstd = rsqrtf(block_sum(q, red) / d + eps);
-    bf16* yr = y + blockIdx.x * ldy;
+    f16* yr = y + blockIdx.x * ldy;
 #pragma unroll
     for (int k = 0; k < kLnChunks; ++k) {
         const int ch = threadIdx.x + k * kLnThreads;
         if (ch < nch) {
             const uint4 gu = __ldg(reinterpret_cast<const uint4*>(g) + ch);
             const uint4 bu = __ldg(reinterpret_cast<const uint4*>(b) + ch);
-            const __nv_bfloat162* gh = reinterpret_cast<const __nv_bfloat162*>(&gu);
-            const __nv_bfloat162* bh = reinterpret_cast<const __nv_bfloat162*>(&bu);
+            const __half2* gh = reinterpret_cast<const __half2*>(&gu);
+            const __half2* bh = reinterpret_cast<const __half2*>(&bu);
             uint32_t o[4];
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
-                const float2 gf = __bfloat1622float2(gh[i]), bf = __bfloat1622float2(bh[i]);
-                o[i] = ptx::pack_bf16x2((v[k][2 * i] - mean) * rstd * gf.x + bf.x,
+                const float2 gf = __half22float2(gh[i]), bf = __half22float2(bh[i]);
+                o[i] = ptx::pack_f16x2((v[k][2 * i] - mean) * rstd * gf.x + bf.x,
                                         (v[k][2 * i + 1] - mean) * rstd * gf.y + bf.y);
             }
             reinterpret_cast<uint4*>(yr)[ch] = make_uint4(o[0], o[1], o[2], o[3]);
@@ -291,9 +291,9 @@ __global__ void sum_rows_kernel(const float* __restrict__ src, int parts, size_t
 }
 
 // 8 columns per thread: 2 x float4 of the sum, 16 B of bias and residual
-__global__ void add_bias_residual_kernel(const float* __restrict__ sum, const bf16* __restrict__ bias,
-                                         const bf16* __restrict__ res, long long ldr, int M, int N,
-                                         bf16* __restrict__ out) {
+__global__ void add_bias_residual_kernel(const float* __restrict__ sum, const f16* __restrict__ bias,
+                                         const f16* __restrict__ res, long long ldr, int M, int N,
+                                         f16* __restrict__ out) {
     const size_t n8 = static_cast<size_t>(M) * N / 8;
     for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n8;
          i += static_cast<size_t>(gridDim.x) * blockDim.x) {
@@ -306,7 +306,7 @@ __global__ void add_bias_residual_kernel(const float* __restrict__ sum, const bf
         if (res) add8(acc, res + static_cast<long long>(row) * ldr + col);
         uint32_t o[4];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) o[j] = ptx::pack_bf16x2(acc[2 * j], acc[2 * j + 1]);
+        for (int j = 0; j < 4; ++j) o[j] = ptx::pack_f16x2(acc[2 * j], acc[2 * j + 1]);
         *reinterpret_cast<uint4*>(out + e0) = make_uint4(o[0], o[1], o[2], o[3]);
     }
 }
@@ -337,7 +337,7 @@ void sum_rows_f32(const float* src, int parts, size_t n, float* out, cudaStream_
     if (n) sum_rows_kernel<<<grid_for(n), 256, 0, st>>>(src, parts, n, out);
 }
 
-void add_bias_residual(const float* sum, const bf16* bias, const bf16* res, long long ldr, int M, int N, bf16* out,
+void add_bias_residual(const float* sum, const f16* bias, const f16* res, long long ldr, int M, int N, f16* out,
                        cudaStream_t st) {
     if (N % 8) throw std::invalid_argument("add_bias_residual: N must be a multiple of 8");
     const size_t n8 = static_cast<size_t>(M) * N / 8;
@@ -350,13 +350,13 @@ void splitk_reduce_f32(const float* ws, int splits, int M, int N, float* out, cu
     if (plane) splitk_reduce_f32_kernel<<<grid_for(plane / 4), 256, 0, st>>>(ws, splits, plane / 4, plane, out);
 }
 
-void layernorm_rows(const bf16* x, long long ldx, const bf16* gamma, const bf16* beta, bf16* y, long long ldy, int n,
+void layernorm_rows(const f16* x, long long ldx, const f16* gamma, const f16* beta, f16* y, long long ldy, int n,
                     int d, float eps, cudaStream_t st) {
     if (d % 8 || d > kLnThreads * kLnChunks * 8) throw std::invalid_argument("layernorm: d must be a multiple of 8, <= 16384");
     if (n > 0) layernorm_kernel<<<n, kLnThreads, 0, st>>>(x, ldx, gamma, beta, y, ldy, d, eps);
 }
 
-void embed(const bf16* E, const bf16* Pos, const int* ids, const int* pos, int n, int d, bf16* X,
+void embed(const f16* E, const f16* Pos, const int* ids, const int* pos, int n, int d, f16* X,
            long long ldx, cudaStream_t st) {
     if (n <= 0) return;
     if (d % 8) throw std::invalid_argument("embed: hidden_dim must be a multiple of 8");
@@ -383,15 +383,15 @@ void argmax_rows(const float* logits, int B, int V, int* out, cudaStream_t st) {
     if (B > 0) argmax_kernel<<<B, 256, 0, st>>>(logits, V, out);
 }
 
-void splitk_reduce(const float* ws, int splits, int M, int N, bf16* out, bool relu, cudaStream_t st,
-                   const bf16* bias, const bf16* res, long long ldr) {
+void splitk_reduce(const float* ws, int splits, int M, int N, f16* out, bool relu, cudaStream_t st,
+                   const f16* bias, const f16* res, long long ldr) {
     if (N % 8) throw std::invalid_argument("splitk_reduce: N must be a multiple of 8");
     const size_t n8 = static_cast<size_t>(M) * N / 8;
     const int blocks = static_cast<int>(std::min<size_t>((n8 + 255) / 256, 4 * static_cast<size_t>(num_sms())));
     if (n8) splitk_reduce_kernel<<<blocks, 256, 0, st>>>(ws, splits, M, N, out, relu ? 1 : 0, bias, res, ldr);
 }
 
-void fill_pattern(bf16* dst, size_t n, uint64_t seed, float amp, cudaStream_t st) {
+void fill_pattern(f16* dst, size_t n, uint64_t seed, float amp, cudaStream_t st) {
     if (n) fill_pattern_kernel<<<4 * num_sms(), 256, 0, st>>>(dst, n, seed, amp);
 }
 

@@ -8,7 +8,7 @@
 //
 // Tensor-core flash attention: one CTA (4 warps) per (64-query tile, head,
 // request); each warp owns 16 query rows. S = Q.K^T and O += P.V run on
-// mma.sync m16n8k16 bf16 (fp32 accumulate; P.V as hi+lo bf16 halves of P);
+// mma.sync m16n8k16 f16 (fp32 accumulate; P.V as hi+lo f16 halves of P);
 // the online softmax lives in the
 // accumulator registers (a thread owns 2 rows, quad shuffles reduce them) and
 // P is re-packed register-to-register as the A operand of P.V. K and V tiles
@@ -64,22 +64,22 @@ __device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t&
 
 __device__ __forceinline__ void mma16816(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
     asm volatile(
-        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
         "{%0,%1,%2,%3};\n"
         : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
         : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
 
-// (a, b) -> bf16x2 hi = rn(a, b) and lo = rn((a, b) - hi)
-__device__ __forceinline__ void split_bf16x2(float a, float b, uint32_t& hi, uint32_t& lo) {
-    const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
-    const float2 hf = __bfloat1622float2(h);
-    const __nv_bfloat162 l = __floats2bfloat162_rn(a - hf.x, b - hf.y);
+// (a, b) -> f16x2 hi = rn(a, b) and lo = rn((a, b) - hi)
+__device__ __forceinline__ void split_f16x2(float a, float b, uint32_t& hi, uint32_t& lo) {
+    const __half2 h = __floats2half2_rn(a, b);
+    const float2 hf = __half22float2(h);
+    const __half2 l = __floats2half2_rn(a - hf.x, b - hf.y);
     hi = *reinterpret_cast<const uint32_t*>(&h);
     lo = *reinterpret_cast<const uint32_t*>(&l);
 }
 
-// byte offset of 16-B chunk `ch` of row `row` in a [rows][HD] bf16 tile
+// byte offset of 16-B chunk `ch` of row `row` in a [rows][HD] f16 tile
 template <int HD>
 __device__ __forceinline__ uint32_t swz(int row, int ch) {
     constexpr int CH = HD / 8;  // chunks per row (16 or 8)
@@ -89,7 +89,7 @@ __device__ __forceinline__ uint32_t swz(int row, int ch) {
 // rows [0, min(n, 64)) of a 64 x HD tile at g (row stride ld elements) into
 // swizzled smem; rows >= n are zero-filled
 template <int HD>
-__device__ __forceinline__ void load_tile(uint32_t sbase, const bf16* g, long long ld, int n) {
+__device__ __forceinline__ void load_tile(uint32_t sbase, const f16* g, long long ld, int n) {
     constexpr int CH = HD / 8;
     for (int i = threadIdx.x; i < kKT * CH; i += blockDim.x) {
         const int r = i / CH, ch = i % CH;
@@ -100,7 +100,7 @@ __device__ __forceinline__ void load_tile(uint32_t sbase, const bf16* g, long lo
 
 template <int HD>
 __global__ void __launch_bounds__(128, 3)
-    prefill_flash_kernel(const bf16* __restrict__ qkv, bf16* __restrict__ out, const int* __restrict__ cu, int H,
+    prefill_flash_kernel(const f16* __restrict__ qkv, f16* __restrict__ out, const int* __restrict__ cu, int H,
                          float scale) {
     constexpr int NK = HD / 16;  // k16 steps over the head dim
     constexpr int NO = HD / 8;   // n8 tiles of O
@@ -113,7 +113,7 @@ __global__ void __launch_bounds__(128, 3)
     const int q0 = qt * kQT;
     const int d = H * HD;
     const long long ld = 3LL * d;
-    const bf16* base = qkv + static_cast<long long>(row0) * ld + h * HD;
+    const f16* base = qkv + static_cast<long long>(row0) * ld + h * HD;
 
     extern __shared__ __align__(128) unsigned char smem[];
     const uint32_t s0 = smem_u32(smem);
@@ -210,8 +210,8 @@ __global__ void __launch_bounds__(128, 3)
             o[j][3] *= alpha[1];
         }
         // P as the A operand (k16 chunk = keys 16kk..16kk+15), split into
-        // bf16 hi + lo parts: P.V = P_hi.V + P_lo.V keeps P to ~16 bits, so
-        // the prefill matches fp32 softmax weights (a single bf16 P costs ~2^-9
+        // f16 hi + lo parts: P.V = P_hi.V + P_lo.V keeps P to ~16 bits, so
+        // the prefill matches fp32 softmax weights (a single f16 P costs ~2^-9
         // relative per weight, visible after a dozen layers)
         uint32_t pa[4][4], pl[4][4];
 #pragma unroll
@@ -220,8 +220,8 @@ __global__ void __launch_bounds__(128, 3)
             const float p2 = exp2f(s[j][2] - m_r[1]), p3 = exp2f(s[j][3] - m_r[1]);
             l_r[0] += p0 + p1;
             l_r[1] += p2 + p3;
-            split_bf16x2(p0, p1, pa[j / 2][(j & 1) * 2 + 0], pl[j / 2][(j & 1) * 2 + 0]);
-            split_bf16x2(p2, p3, pa[j / 2][(j & 1) * 2 + 1], pl[j / 2][(j & 1) * 2 + 1]);
+            split_f16x2(p0, p1, pa[j / 2][(j & 1) * 2 + 0], pl[j / 2][(j & 1) * 2 + 0]);
+            split_f16x2(p2, p3, pa[j / 2][(j & 1) * 2 + 1], pl[j / 2][(j & 1) * 2 + 1]);
         }
         // O += P.V : V tile [key][hd] read transposed as the col-major B operand
 #pragma unroll
@@ -240,7 +240,7 @@ __global__ void __launch_bounds__(128, 3)
         }
         __syncthreads();  // tile `cur` is overwritten by the load issued next iteration
     }
-    // finish: full row sums across the quad, normalise, store bf16
+    // finish: full row sums across the quad, normalise, store f16
 #pragma unroll
     for (int i = 0; i < 2; ++i) {
         l_r[i] += __shfl_xor_sync(0xffffffffu, l_r[i], 1);
@@ -251,15 +251,15 @@ __global__ void __launch_bounds__(128, 3)
     for (int i = 0; i < 2; ++i) {
         const int row = qrow + i * 8;
         if (row >= P) continue;
-        bf16* op = out + static_cast<long long>(row0 + row) * d + h * HD + (lane % 4) * 2;
+        f16* op = out + static_cast<long long>(row0 + row) * d + h * HD + (lane % 4) * 2;
 #pragma unroll
         for (int j = 0; j < NO; ++j)
-            *reinterpret_cast<uint32_t*>(op + j * 8) = ptx::pack_bf16x2(o[j][2 * i] * l_r[i], o[j][2 * i + 1] * l_r[i]);
+            *reinterpret_cast<uint32_t*>(op + j * 8) = ptx::pack_f16x2(o[j][2 * i] * l_r[i], o[j][2 * i + 1] * l_r[i]);
     }
 }
 
 template <int HD>
-void launch_prefill(const bf16* qkv, bf16* out, const int* cu, int n_req, int max_len, int H, float scale,
+void launch_prefill(const f16* qkv, f16* out, const int* cu, int n_req, int max_len, int H, float scale,
                     cudaStream_t st) {
     constexpr size_t smem = static_cast<size_t>(4 * kKT) * HD * 2;
     static std::atomic<uint64_t> configured{0};
@@ -270,10 +270,10 @@ void launch_prefill(const bf16* qkv, bf16* out, const int* cu, int n_req, int ma
 
 }  // namespace
 
-bool prefill_attention_tc(const bf16* qkv, long long rows, bf16* out, const int* cu, int n_req, int max_len, int H,
+bool prefill_attention_tc(const f16* qkv, long long rows, f16* out, const int* cu, int n_req, int max_len, int H,
                           int hd, float scale, cudaStream_t st);
 
-void prefill_attention(const bf16* qkv, bf16* out, const int* cu, int n_req, int max_len, int H, int hd,
+void prefill_attention(const f16* qkv, f16* out, const int* cu, int n_req, int max_len, int H, int hd,
                        float scale, cudaStream_t st, long long rows) {
     if (n_req <= 0 || max_len <= 0) return;
     if (prefill_attention_tc(qkv, rows, out, cu, n_req, max_len, H, hd, scale, st)) return;

@@ -16,7 +16,7 @@
 //   warps 2..5  softmax: thread = query row = TMEM lane; S row via tcgen05.ld,
 //               causal / ragged mask, online max in the exp2 domain with a
 //               lazy O correction (only when the max grows by > 2^8, so P
-//               stays <= 256 and O is rescaled in TMEM rarely), P (bf16) into
+//               stays <= 256 and O is rescaled in TMEM rarely), P (f16) into
 //               a 128B-swizzled K-major smem tile for the P.V MMA; finally
 //               O / l from TMEM to HBM.
 // TMEM: S0 | S1 | O = 384 of 512 columns. smem: Q 32 KB, 2 x (K 32 + V 32) KB,
@@ -40,7 +40,7 @@ namespace {
 
 constexpr int kT = 128;        // queries per CTA = keys per tile
 constexpr int kHD = 128;       // head dim
-constexpr int kBox = kT * 64 * 2;           // one [128 rows][64 cols] bf16 box = 16 KB
+constexpr int kBox = kT * 64 * 2;           // one [128 rows][64 cols] f16 box = 16 KB
 constexpr int kTile = 2 * kBox;             // [128][128] = 32 KB
 constexpr int kStages = 2;
 constexpr int kThreads = 192;
@@ -113,7 +113,7 @@ __device__ __forceinline__ uint64_t sw128_mnmajor_desc(uint32_t smem_addr, uint3
 }
 
 __global__ void __launch_bounds__(kThreads, 1)
-    prefill_tc_kernel(const __grid_constant__ CUtensorMap tm, bf16* __restrict__ out, const int* __restrict__ cu,
+    prefill_tc_kernel(const __grid_constant__ CUtensorMap tm, f16* __restrict__ out, const int* __restrict__ cu,
                       int H, float scale, uint32_t v_lbo, uint32_t v_sbo) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -184,8 +184,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     } else if (warp == 1) {
         if (lane == 0) {  // ------------------------------------------ MMA issuer
-            constexpr uint32_t id_s = ptx::idesc_bf16_f32(kT, kT);               // A, B K-major
-            constexpr uint32_t id_o = ptx::idesc_bf16_f32(kT, kHD) | (1u << 16);  // B MN-major (V)
+            constexpr uint32_t id_s = ptx::idesc_f16_f32(kT, kT);               // A, B K-major
+            constexpr uint32_t id_o = ptx::idesc_f16_f32(kT, kHD) | (1u << 16);  // B MN-major (V)
             const uint32_t qa = ptx::smem_u32(smem + Smem::q);
             const uint32_t pa = ptx::smem_u32(smem + Smem::p);
             auto issue_s = [&](int j) {
@@ -197,7 +197,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                 for (int k = 0; k < kHD / 16; ++k) {  // hd in two 64-wide boxes, 4 k-steps each
                     const uint32_t off = (k / 4) * kBox;
-                    ptx::mma_bf16_ss(t_s(b), ptx::sw128_kmajor_desc(qa + off) + 2 * (k % 4),
+                    ptx::mma_f16_ss(t_s(b), ptx::sw128_kmajor_desc(qa + off) + 2 * (k % 4),
                                      ptx::sw128_kmajor_desc(kb + off) + 2 * (k % 4), id_s, k > 0);
                 }
                 ptx::mma_commit(&s_full[b]);
@@ -216,7 +216,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int k = 0; k < kT / 16; ++k) {  // keys: P in two 64-wide boxes; V rows 16 per step
                     const uint64_t a = ptx::sw128_kmajor_desc(pbuf + (k / 4) * kBox) + 2 * (k % 4);
                     const uint64_t bdesc = sw128_mnmajor_desc(vb + k * 16 * 128, v_lbo, v_sbo);
-                    ptx::mma_bf16_ss(t_o, a, bdesc, id_o, (j > 0 || k > 0) ? 1u : 0u);
+                    ptx::mma_f16_ss(t_o, a, bdesc, id_o, (j > 0 || k > 0) ? 1u : 0u);
                 }
                 ptx::mma_commit(&pv_done[pb]);
                 ptx::mma_commit(&kv_empty[s]);
@@ -266,14 +266,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                 m = mx;
                 l *= alpha;
             }
-            // P = exp2(s - m) as packed bf16, computed while P.V(j-1) still runs
+            // P = exp2(s - m) as packed f16, computed while P.V(j-1) still runs
             uint32_t pw[kT / 2];
             float l8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
             for (int i = 0; i < kT / 2; ++i) {
                 const float p0 = ex2(__uint_as_float(sraw[2 * i]) - m), p1 = ex2(__uint_as_float(sraw[2 * i + 1]) - m);
                 l8[i % 8] += p0 + p1;
-                pw[i] = ptx::pack_bf16x2(p0, p1);
+                pw[i] = ptx::pack_f16x2(p0, p1);
             }
             l += ((l8[0] + l8[1]) + (l8[2] + l8[3])) + ((l8[4] + l8[5]) + (l8[6] + l8[7]));
             // P buffer j%2 is free once P.V(j-2) has completed; O may be
@@ -312,7 +312,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         ptx::mbar_wait(&pv_done[(n_kt - 1) & 1], ((n_kt - 1) / 2) & 1);
         ptx::tc_fence_after();
         const float inv = l > 0.f ? 1.f / l : 0.f;
-        bf16* orow = out + static_cast<long long>(row0 + qrow) * d + h * kHD;
+        f16* orow = out + static_cast<long long>(row0 + qrow) * d + h * kHD;
 #pragma unroll 1
         for (int c = 0; c < kHD; c += 16) {
             uint32_t v[16];
@@ -321,7 +321,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             uint32_t o[8];
 #pragma unroll
             for (int i = 0; i < 8; ++i)
-                o[i] = ptx::pack_bf16x2(__uint_as_float(v[2 * i]) * inv, __uint_as_float(v[2 * i + 1]) * inv);
+                o[i] = ptx::pack_f16x2(__uint_as_float(v[2 * i]) * inv, __uint_as_float(v[2 * i + 1]) * inv);
             if (qrow < P) {
                 ptx::st_global_v4(orow + c, o[0], o[1], o[2], o[3]);
                 ptx::st_global_v4(orow + c + 8, o[4], o[5], o[6], o[7]);
@@ -362,7 +362,7 @@ constexpr int kSlots2 = 3;
 constexpr int kThreads2 = 320;
 
 // head_dim 64 has the smem for a second P buffer per tile: P = P_hi + P_lo (both
-// bf16, P_lo = bf16(p - P_hi)) and O += P_hi V + P_lo V keeps P to ~16 mantissa
+// f16, P_lo = f16(p - P_hi)) and O += P_hi V + P_lo V keeps P to ~16 mantissa
 // bits, as the mma.sync kernel's hi/lo split does — halving the head dim
 // doubles the weight of the P rounding per output (12-layer OPT-125M traces).
 template <int HD>
@@ -404,7 +404,7 @@ __device__ __forceinline__ bool item_of(int w, int n_pairs, int H, int n_req, co
 
 template <int HD>  // head_dim 64 or 128
 __global__ void __launch_bounds__(kThreads2, 1)
-    prefill_tc2_kernel(const __grid_constant__ CUtensorMap tm, bf16* __restrict__ out, const int* __restrict__ cu,
+    prefill_tc2_kernel(const __grid_constant__ CUtensorMap tm, f16* __restrict__ out, const int* __restrict__ cu,
                        int n_req, int n_pairs, int H, float scale, uint32_t v_lbo, uint32_t v_sbo) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -474,8 +474,8 @@ __global__ void __launch_bounds__(kThreads2, 1)
         }
     } else if (warp == 9) {
         if (lane == 0) {  // ------------------------------------------ MMA issuer
-            constexpr uint32_t id_s = ptx::idesc_bf16_f32(kT, kT);               // A, B K-major
-            constexpr uint32_t id_o = ptx::idesc_bf16_f32(kT, HD) | (1u << 16);  // B MN-major (V)
+            constexpr uint32_t id_s = ptx::idesc_f16_f32(kT, kT);               // A, B K-major
+            constexpr uint32_t id_o = ptx::idesc_f16_f32(kT, HD) | (1u << 16);  // B MN-major (V)
             uint32_t ring = 0, n_it = 0, pc[2] = {0, 0}, oc[2] = {0, 0};
             auto slot_addr = [&](uint32_t g) { return ptx::smem_u32(smem + Smem2<HD>::kv + (g % kSlots2) * Smem2<HD>::qkv); };
             auto s_mma = [&](int t, uint32_t g) {  // S_t = Q_t . K^T, K at ring entry g
@@ -485,7 +485,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
 #pragma unroll
                 for (int k = 0; k < HD / 16; ++k) {
                     const uint32_t off = (k / 4) * kBox;
-                    ptx::mma_bf16_ss(tmem + 128u * t, ptx::sw128_kmajor_desc(qa + off) + 2 * (k % 4),
+                    ptx::mma_f16_ss(tmem + 128u * t, ptx::sw128_kmajor_desc(qa + off) + 2 * (k % 4),
                                      ptx::sw128_kmajor_desc(kb + off) + 2 * (k % 4), id_s, k > 0);
                 }
                 ptx::mma_commit(&s_full[t]);
@@ -501,7 +501,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
                 for (int k = 0; k < kT / 16; ++k) {
                     const uint64_t a = ptx::sw128_kmajor_desc(pa + (k / 4) * kBox) + 2 * (k % 4);
                     const uint64_t bdesc = sw128_mnmajor_desc(vb + k * 16 * 128, v_lbo, v_sbo);
-                    ptx::mma_bf16_ss(tmem + 256u + static_cast<uint32_t>(HD) * t, a, bdesc, id_o, (!first || k > 0) ? 1u : 0u);
+                    ptx::mma_f16_ss(tmem + 256u + static_cast<uint32_t>(HD) * t, a, bdesc, id_o, (!first || k > 0) ? 1u : 0u);
                 }
                 if constexpr (Smem2<HD>::lo) {  // + P_lo . V
                     const uint32_t pl = ptx::smem_u32(smem + Smem2<HD>::plo + t * kTile);
@@ -509,7 +509,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
                     for (int k = 0; k < kT / 16; ++k) {
                         const uint64_t a = ptx::sw128_kmajor_desc(pl + (k / 4) * kBox) + 2 * (k % 4);
                         const uint64_t bdesc = sw128_mnmajor_desc(vb + k * 16 * 128, v_lbo, v_sbo);
-                        ptx::mma_bf16_ss(tmem + 256u + static_cast<uint32_t>(HD) * t, a, bdesc, id_o, 1u);
+                        ptx::mma_f16_ss(tmem + 256u + static_cast<uint32_t>(HD) * t, a, bdesc, id_o, 1u);
                     }
                 }
             };
@@ -609,10 +609,10 @@ __global__ void __launch_bounds__(kThreads2, 1)
                                                sl2, nm2);
                         const float2 pp = make_float2(ex2(y.x), ex2(y.y));
                         l4[u] = fadd2(l4[u], pp);
-                        pw[u] = ptx::pack_bf16x2(pp.x, pp.y);
-                        if constexpr (Smem2<HD>::lo) {  // the bf16 residual of each P entry
-                            const float h0 = __uint_as_float(pw[u] << 16), h1 = __uint_as_float(pw[u] & 0xFFFF0000u);
-                            plw[u] = ptx::pack_bf16x2(pp.x - h0, pp.y - h1);
+                        pw[u] = ptx::pack_f16x2(pp.x, pp.y);
+                        if constexpr (Smem2<HD>::lo) {  // the f16 residual of each P entry
+                            const float2 h = __half22float2(*reinterpret_cast<const __half2*>(&pw[u]));
+                            plw[u] = ptx::pack_f16x2(pp.x - h.x, pp.y - h.y);
                         }
                     }
                     const int box = c / 8, ch = c % 8;
@@ -643,7 +643,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
             ++oc;
             ptx::tc_fence_after();
             const float inv = l > 0.f ? 1.f / l : 0.f;
-            bf16* orow = out + static_cast<long long>(it.row0 + qrow) * d + it.h * HD;
+            f16* orow = out + static_cast<long long>(it.row0 + qrow) * d + it.h * HD;
 #pragma unroll 1
             for (int c = 0; c < HD; c += 16) {
                 uint32_t v[16];
@@ -652,7 +652,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
                 uint32_t o[8];
 #pragma unroll
                 for (int i = 0; i < 8; ++i)
-                    o[i] = ptx::pack_bf16x2(__uint_as_float(v[2 * i]) * inv, __uint_as_float(v[2 * i + 1]) * inv);
+                    o[i] = ptx::pack_f16x2(__uint_as_float(v[2 * i]) * inv, __uint_as_float(v[2 * i + 1]) * inv);
                 if (qrow < P) {
                     ptx::st_global_v4(orow + c, o[0], o[1], o[2], o[3]);
                     ptx::st_global_v4(orow + c + 8, o[4], o[5], o[6], o[7]);
@@ -673,7 +673,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
 
 // Tensor-core path for head_dim 128 (prefill_attention.cu dispatches here);
 // rows = total rows of qkv (the TMA map bounds).
-bool prefill_attention_tc(const bf16* qkv, long long rows, bf16* out, const int* cu, int n_req, int max_len, int H,
+bool prefill_attention_tc(const f16* qkv, long long rows, f16* out, const int* cu, int n_req, int max_len, int H,
                           int hd, float scale, cudaStream_t st) {
     static const int enabled = [] {
         const char* e = std::getenv("HC_PREFILL_TC");  // 0 mma.sync, 1 one tile per CTA, 2 tile pairs

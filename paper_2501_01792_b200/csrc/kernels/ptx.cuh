@@ -2,7 +2,7 @@
 // mbarrier, TMA (cp.async.bulk.tensor), tcgen05 (alloc / mma / commit / ld).
 #pragma once
 #include <cstdint>
-#include <cuda_bf16.h>
+#include <cuda_fp16.h>
 
 namespace hc::ptx {
 
@@ -97,8 +97,8 @@ __device__ __forceinline__ void tc_fence_after() {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 }
 
-// D[tmem] (+)= A[smem] * B[smem]^T, bf16 in, fp32 accumulate, both K-major.
-__device__ __forceinline__ void mma_bf16_ss(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
+// D[tmem] (+)= A[smem] * B[smem]^T, f16 in, fp32 accumulate, both K-major.
+__device__ __forceinline__ void mma_f16_ss(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
                                             uint32_t idesc, uint32_t accumulate) {
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
@@ -144,11 +144,11 @@ __device__ __forceinline__ uint64_t sw128_kmajor_desc(uint32_t smem_addr) {
     return d;
 }
 
-// Instruction descriptor, kind::f16: bf16 x bf16 -> fp32, A and B K-major.
-__host__ __device__ constexpr uint32_t idesc_bf16_f32(int m, int n) {
+// Instruction descriptor, kind::f16: f16 x f16 -> fp32, A and B K-major.
+__host__ __device__ constexpr uint32_t idesc_f16_f32(int m, int n) {
     return (1u << 4)                                   // D format f32
-           | (1u << 7)                                 // A bf16
-           | (1u << 10)                                // B bf16
+           | (0u << 7)                                 // A f16 (atype 0; bf16 would be 1)
+           | (0u << 10)                                // B f16
            | (static_cast<uint32_t>(n >> 3) << 17)     // N
            | (static_cast<uint32_t>(m >> 4) << 24);    // M
 }
@@ -188,7 +188,7 @@ __device__ __forceinline__ void tmem_dealloc_pair(uint32_t taddr) {
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "n"(kCols) : "memory");
 }
 
-__device__ __forceinline__ void mma_bf16_ss_pair(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+__device__ __forceinline__ void mma_f16_ss_pair(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
                                                  uint32_t accumulate) {
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
@@ -219,8 +219,8 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint64_t* bar, uint32_t cta)
 }
 
 // ---- misc ------------------------------------------------------------------
-__device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
-    const __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+__device__ __forceinline__ uint32_t pack_f16x2(float lo, float hi) {
+    const __half2 v = __floats2half2_rn(lo, hi);
     return *reinterpret_cast<const uint32_t*>(&v);
 }
 

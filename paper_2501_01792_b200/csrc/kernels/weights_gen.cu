@@ -1,5 +1,5 @@
 // DecoderWeights::generate on the GPU (model.cpp:82-117 + the rescale +
-// fp64 -> fp32 -> bf16 rounding of csrc/host/model.cpp), bit-exact with the
+// fp64 -> fp32 -> f16 rounding of csrc/host/model.cpp), bit-exact with the
 // host generator: SplitMix64 is counter based (draw i of stream s is
 // mix(s + (i+1)*golden)), so every output element is computed independently.
 // Each thread produces one element of the TRANSPOSED matrix ([cols][rows]),
@@ -17,12 +17,8 @@ __device__ __forceinline__ uint64_t splitmix_mix(uint64_t z) {
     return z ^ (z >> 31);
 }
 
-__device__ __forceinline__ uint16_t bf16_bits_rn(double v) {
-    const float f = __double2float_rn(v);
-    uint32_t u = __float_as_uint(f);
-    if ((u & 0x7f800000u) == 0x7f800000u && (u & 0x007fffffu)) return static_cast<uint16_t>((u >> 16) | 0x40);
-    u += 0x7fffu + ((u >> 16) & 1u);
-    return static_cast<uint16_t>(u >> 16);
+__device__ __forceinline__ uint16_t f16_bits_rn(double v) {
+    return __half_as_ushort(__float2half_rn(__double2float_rn(v)));
 }
 
 __device__ __forceinline__ double draw_u(uint64_t seed, uint64_t i) {
@@ -32,7 +28,7 @@ __device__ __forceinline__ double draw_u(uint64_t seed, uint64_t i) {
     return __dadd_rn(-0.1, __dmul_rn(__dadd_rn(0.1, 0.1), u));
 }
 
-// dst[c * rows + r] = bf16(scale * U_{r*cols + c})
+// dst[c * rows + r] = f16(scale * U_{r*cols + c})
 __global__ void gen_transposed_kernel(uint16_t* __restrict__ dst, int rows, int cols, uint64_t seed, double scale,
                                       int apply_scale) {
     const size_t n = static_cast<size_t>(rows) * cols;
@@ -41,14 +37,14 @@ __global__ void gen_transposed_kernel(uint16_t* __restrict__ dst, int rows, int 
         const size_t c = o / rows, r = o - c * rows;
         double v = draw_u(seed, r * static_cast<size_t>(cols) + c);
         if (apply_scale) v = __dmul_rn(v, scale);
-        dst[o] = bf16_bits_rn(v);
+        dst[o] = f16_bits_rn(v);
     }
 }
 
 __global__ void gen_plain_kernel(uint16_t* __restrict__ dst, size_t n, uint64_t seed) {
     for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
          i += static_cast<size_t>(gridDim.x) * blockDim.x)
-        dst[i] = bf16_bits_rn(draw_u(seed, i));
+        dst[i] = f16_bits_rn(draw_u(seed, i));
 }
 
 }  // namespace

@@ -22,7 +22,7 @@ using ncclComm_t = void*;
 struct ncclUniqueId {
     char internal[128];
 };
-enum { kNcclSum = 0, kNcclFloat32 = 7, kNcclBfloat16 = 9 };
+enum { kNcclSum = 0, kNcclFloat32 = 7, kNcclFloat16 = 6 };
 struct NcclApi {
     int (*get_unique_id)(ncclUniqueId*) = nullptr;
     int (*comm_init_rank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
@@ -84,13 +84,13 @@ public:
     void all_reduce_sum(float* buf, size_t n, cudaStream_t st) override {
         if (size_ > 1 && n) nccl_check(nccl().all_reduce(buf, buf, n, kNcclFloat32, kNcclSum, comm_, st), "ncclAllReduce");
     }
-    void all_gather(const bf16* send, bf16* recv, size_t n, cudaStream_t st) override {
+    void all_gather(const f16* send, f16* recv, size_t n, cudaStream_t st) override {
         if (!n) return;
         if (size_ == 1) {
             if (send != recv) HC_CUDA(cudaMemcpyAsync(recv, send, n * 2, cudaMemcpyDeviceToDevice, st));
             return;
         }
-        nccl_check(nccl().all_gather(send, recv, n, kNcclBfloat16, comm_, st), "ncclAllGather");
+        nccl_check(nccl().all_gather(send, recv, n, kNcclFloat16, comm_, st), "ncclAllGather");
     }
     TpGroup* copy_channel() override { return copy_ ? copy_ : this; }
 
@@ -107,7 +107,7 @@ public:
     int rank() const override { return compute_.rank(); }
     int size() const override { return compute_.size(); }
     void all_reduce_sum(float* buf, size_t n, cudaStream_t st) override { compute_.all_reduce_sum(buf, n, st); }
-    void all_gather(const bf16* s, bf16* r, size_t n, cudaStream_t st) override { compute_.all_gather(s, r, n, st); }
+    void all_gather(const f16* s, f16* r, size_t n, cudaStream_t st) override { compute_.all_gather(s, r, n, st); }
     TpGroup* copy_channel() override { return &copy_; }
 
 private:
@@ -138,7 +138,7 @@ public:
     int rank() const override { return rank_; }
     int size() const override { return size_; }
     void all_reduce_sum(float*, size_t, cudaStream_t) override {}
-    void all_gather(const bf16*, bf16*, size_t, cudaStream_t) override {}
+    void all_gather(const f16*, f16*, size_t, cudaStream_t) override {}
     TpGroup* copy_channel() override { return this; }
 
 private:
@@ -198,11 +198,11 @@ public:
         HC_CUDA(cudaStreamSynchronize(st));
         s_->barrier();
     }
-    void all_gather(const bf16* send, bf16* recv, size_t n, cudaStream_t st) override {
+    void all_gather(const f16* send, f16* recv, size_t n, cudaStream_t st) override {
         if (!n) return;
         post(send, st);
         for (int j = 0; j < s_->n; ++j) {
-            bf16* dst = recv + j * n;
+            f16* dst = recv + j * n;
             if (dst != s_->ptr[j] || s_->dev[j] != dev_)
                 HC_CUDA(cudaMemcpyPeerAsync(dst, dev_, s_->ptr[j], s_->dev[j], n * 2, st));
         }

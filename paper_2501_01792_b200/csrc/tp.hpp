@@ -36,7 +36,7 @@ public:
     // row-sharded W_proj / W2 GEMMs, reduced before bias + residual are added)
     virtual void all_reduce_sum(float* buf, size_t n, cudaStream_t st) = 0;
     // recv[r*n .. (r+1)*n) <- rank r's send[0..n)   (in-place when send == recv + rank*n)
-    virtual void all_gather(const bf16* send, bf16* recv, size_t n, cudaStream_t st) = 0;
+    virtual void all_gather(const f16* send, f16* recv, size_t n, cudaStream_t st) = 0;
     // distinct collective channel for the copy stream (same group, own ordering)
     virtual TpGroup* copy_channel() = 0;
 };

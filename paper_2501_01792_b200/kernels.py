@@ -1,6 +1,6 @@
 """Kernel-level calls through the C ABI (host numpy buffers in / out).
 
-bf16 tensors cross the boundary as uint16 bit patterns.
+fp16 (IEEE binary16) tensors cross the boundary as uint16 bit patterns.
 """
 from __future__ import annotations
 
@@ -12,16 +12,14 @@ import numpy as np
 from ._native import check, lib, ptr
 
 
-def f32_to_bf16_bits(x: np.ndarray) -> np.ndarray:
-    """Round-to-nearest-even fp32 -> bf16 bits (fp64 inputs go via fp32)."""
+def f32_to_f16_bits(x: np.ndarray) -> np.ndarray:
+    """Round-to-nearest-even fp32 -> IEEE binary16 bits (fp64 inputs go via fp32)."""
     f = np.ascontiguousarray(x, dtype=np.float32)
-    u = f.view(np.uint32).astype(np.uint64)
-    r = (u + ((u >> np.uint64(16)) & np.uint64(1)) + np.uint64(0x7FFF)) >> np.uint64(16)
-    return r.astype(np.uint16)
+    return f.astype(np.float16).view(np.uint16)
 
 
-def bf16_bits_to_f32(b: np.ndarray) -> np.ndarray:
-    return (np.ascontiguousarray(b, dtype=np.uint16).astype(np.uint32) << 16).view(np.float32)
+def f16_bits_to_f32(b: np.ndarray) -> np.ndarray:
+    return np.ascontiguousarray(b, dtype=np.uint16).view(np.float16).astype(np.float32)
 
 
 def _u16(a):
@@ -29,32 +27,32 @@ def _u16(a):
     return a, ptr(a, C.c_uint16)
 
 
-def gemm_bf16(a_bits: np.ndarray, wt_bits: np.ndarray, epi: int = 0, bn: int = 0) -> np.ndarray:
-    """C = A . W with W passed transposed (Wt [N x K]); epi 0 bf16, 1 relu, 3 f32."""
+def gemm_f16(a_bits: np.ndarray, wt_bits: np.ndarray, epi: int = 0, bn: int = 0) -> np.ndarray:
+    """C = A . W with W passed transposed (Wt [N x K]); epi 0 f16, 1 relu, 3 f32."""
     M, K = a_bits.shape
     N, K2 = wt_bits.shape
     assert K == K2
     a, ap = _u16(a_bits)
     w, wp = _u16(wt_bits)
     out = np.zeros((M, N), dtype=np.float32 if epi == 3 else np.uint16)
-    check(lib().hc_gemm_bf16(epi, M, N, K, ap, wp, out.ctypes.data_as(C.c_void_p), bn))
+    check(lib().hc_gemm_f16(epi, M, N, K, ap, wp, out.ctypes.data_as(C.c_void_p), bn))
     return out
 
 
-def gemm_bf16_splitk(a_bits: np.ndarray, wt_bits: np.ndarray, splits: int, epi: int = 0, bn: int = 128) -> np.ndarray:
-    """Split-K C = A . W (W transposed [N x K]); bf16 out (epi 0 store, 1 relu)."""
+def gemm_f16_splitk(a_bits: np.ndarray, wt_bits: np.ndarray, splits: int, epi: int = 0, bn: int = 128) -> np.ndarray:
+    """Split-K C = A . W (W transposed [N x K]); f16 out (epi 0 store, 1 relu)."""
     M, K = a_bits.shape
     N, _ = wt_bits.shape
     a, ap = _u16(a_bits)
     w, wp = _u16(wt_bits)
     out = np.zeros((M, N), np.uint16)
-    check(lib().hc_gemm_bf16_splitk(epi, M, N, K, ap, wp, ptr(out, C.c_uint16), bn, splits))
+    check(lib().hc_gemm_f16_splitk(epi, M, N, K, ap, wp, ptr(out, C.c_uint16), bn, splits))
     return out
 
 
 def recompute_kv_paged(act_pool_bits: np.ndarray, wkv_t_bits: np.ndarray, heads: int,
                        tiles: np.ndarray, bn: int = 0) -> np.ndarray:
-    """act_pool [n_blocks, tpb, d] -> kv [n_blocks, 2, H, tpb, hd] (bf16 bits)."""
+    """act_pool [n_blocks, tpb, d] -> kv [n_blocks, 2, H, tpb, hd] (f16 bits)."""
     nb, tpb, d = act_pool_bits.shape
     a, ap = _u16(act_pool_bits)
     w, wp = _u16(wkv_t_bits)

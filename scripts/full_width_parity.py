@@ -57,14 +57,14 @@ def main(argv=None):
         for b in range(2):
             seqs[b].append(toks[b])
             out = fwd(seqs[b], w).output[-1:]
-            errs.append({"step": step, "request": b, "x_rel": rel(O.bf16_bits_to_f64(res["x"][b]), out[0]),
+            errs.append({"step": step, "request": b, "x_rel": rel(O.f16_bits_to_f64(res["x"][b]), out[0]),
                          "logits_rel": rel(res["logits"][b], O.logits_tied(out, w)[0])})
     # recomputed K/V of the ACT blocks and stored KV blocks vs the oracle trace
     tr = fwd(seqs[1], w)
     row, blk_errs = 0, []
     for e in eng.cache.table("b").entries:
         n = e.filled_tokens
-        blk = O.bf16_bits_to_f64(eng.read_block(e.kind, e.location, e.pbn, 0))
+        blk = O.f16_bits_to_f64(eng.read_block(e.kind, e.location, e.pbn, 0))
         if int(e.kind) == 1:  # ACT blocks hold the layer input (OPT: LN1 of it)
             want = tr.act[0] if a.arch == "opt" else tr.layer_inputs[0]
             blk_errs.append(rel(blk[:n], want[row:row + n]))

@@ -6,7 +6,7 @@ g = np.load("tests/golden/golden.npz")
 cfg = api.ModelConfig(num_layers=12, hidden_dim=768, num_heads=12, ffn_dim=3072, vocab_size=50272)
 eng = api.Engine(cfg, seed=42, max_seq=160, rescale=True, max_batch=1)
 tr = eng.forward_trace(g["opt125m_shape/ids"].tolist())
-f = O.bf16_bits_to_f64
+f = O.f16_bits_to_f64
 for l in range(12):
     a = f(tr["layer_inputs"][l]); b = g["opt125m_shape/layer_inputs"][l]
     k = f(tr["k"][l]); kb = g["opt125m_shape/k"][l]

@@ -17,5 +17,5 @@ for mode in order:
     eng.configure_cache(api.PoolCaps(kv_host=8, act_host=8, act_gpu=2), mode=mode, allocation=api.HostAllocation(1, 1))
     eng.prefill(["q"], [ids])
     eng.set_profile(True)
-    x = O.bf16_bits_to_f64(eng.decode_step(["q"], [tok])["x"])
+    x = O.f16_bits_to_f64(eng.decode_step(["q"], [tok])["x"])
     print(mode, np.abs(x).max(), {k: round(v, 3) for k, v in eng.last_stats().items()})

@@ -30,16 +30,16 @@ def main():
     eng.prefill(["a"], [prompts[0]])
     eng.decode_step(["a"], [5])
     eng.close()
-    a = kernels.f32_to_bf16_bits(rng.uniform(-1, 1, (64, 1024)))
-    w = kernels.f32_to_bf16_bits(rng.uniform(-0.05, 0.05, (256, 1024)))
-    kernels.gemm_bf16_splitk(a, w, 4, 1, 128)
-    q = kernels.f32_to_bf16_bits(rng.uniform(-1, 1, (2, 256)))
-    pool = kernels.f32_to_bf16_bits(rng.uniform(-1, 1, (8, 2, 2, 16, 128)))
+    a = kernels.f32_to_f16_bits(rng.uniform(-1, 1, (64, 1024)))
+    w = kernels.f32_to_f16_bits(rng.uniform(-0.05, 0.05, (256, 1024)))
+    kernels.gemm_f16_splitk(a, w, 4, 1, 128)
+    q = kernels.f32_to_f16_bits(rng.uniform(-1, 1, (2, 256)))
+    pool = kernels.f32_to_f16_bits(rng.uniform(-1, 1, (8, 2, 2, 16, 128)))
     refs = np.array([[0, 1, 2, 3], [4, 5, 6, 7]], np.int32)
     kernels.decode_attention(q, pool, pool, refs, np.array([4, 3], np.int32), np.array([60, 40], np.int32), 2,
                              True, 2)
     # persistent two-tile prefill attention: several items per CTA, odd tile count
-    qkv = kernels.f32_to_bf16_bits(rng.uniform(-1, 1, (2 * 640, 3 * 256)))
+    qkv = kernels.f32_to_f16_bits(rng.uniform(-1, 1, (2 * 640, 3 * 256)))
     kernels.prefill_attention(qkv, 2, 640, 2)
     # session-2 paths: chunked offloaded prefill (store stream), OPT layers
     # (LayerNorm, bias / residual epilogues), head-sharded TP over the

@@ -42,7 +42,7 @@ def test_no_gpu_compute_fails_loudly():
     if kernels.device_count() > 0:
         pytest.skip("GPU present")
     with pytest.raises(HcError):
-        kernels.gemm_bf16(np.zeros((128, 64), np.uint16), np.zeros((64, 64), np.uint16))
+        kernels.gemm_f16(np.zeros((128, 64), np.uint16), np.zeros((64, 64), np.uint16))
 
 
 def test_tensor_parallel_handles_cpu():

@@ -220,12 +220,12 @@ def test_generate_weights_bit_exact_to_oracle():
     w = api.generate_weights(cfg, 42, 24, rescale=True)
     ocfg = O.ModelConfig(num_layers=2, hidden_dim=64, num_heads=2, ffn_dim=128, vocab_size=96).validate()
     ow = O.prepare_weights(O.generate_weights(ocfg, 42, 24))
-    assert np.array_equal(w["embedding"], O.to_bf16_bits(ow.embedding))
-    assert np.array_equal(w["positional"], O.to_bf16_bits(ow.positional))
+    assert np.array_equal(w["embedding"], O.to_f16_bits(ow.embedding))
+    assert np.array_equal(w["positional"], O.to_f16_bits(ow.positional))
     for l in range(2):
         lay = api.unpack_layer(cfg.validate(), w["layers"][l])
         for n in O.WEIGHT_NAMES:
-            assert np.array_equal(lay[n], O.to_bf16_bits(ow.layers[l][n])), n
+            assert np.array_equal(lay[n], O.to_f16_bits(ow.layers[l][n])), n
 
 
 def test_model_config_validation():

@@ -16,41 +16,41 @@ def rel(got, ref):
 
 
 def rand_bits(rng, shape, scale=1.0):
-    from paper_2501_01792_b200.kernels import f32_to_bf16_bits
-    return f32_to_bf16_bits(rng.uniform(-scale, scale, size=shape))
+    from paper_2501_01792_b200.kernels import f32_to_f16_bits
+    return f32_to_f16_bits(rng.uniform(-scale, scale, size=shape))
 
 
 def f64(bits):
-    from paper_2501_01792_b200.kernels import bf16_bits_to_f32
-    return bf16_bits_to_f32(bits).astype(np.float64)
+    from paper_2501_01792_b200.kernels import f16_bits_to_f32
+    return f16_bits_to_f32(bits).astype(np.float64)
 
 
 @pytest.mark.parametrize("M,N,K,bn", [
     (128, 128, 64, 0), (128, 256, 128, 256), (64, 768, 768, 0), (300, 512, 320, 128),
     (130, 96, 200, 32), (128, 7168 // 8, 1024, 64), (1024, 1024, 512, 256), (2048, 512, 7168 // 4, 0),
 ])
-def test_gemm_bf16_store(native, M, N, K, bn):
-    from paper_2501_01792_b200.kernels import gemm_bf16
+def test_gemm_f16_store(native, M, N, K, bn):
+    from paper_2501_01792_b200.kernels import gemm_f16
     rng = np.random.default_rng(M * 7 + N + K)
     a = rand_bits(rng, (M, K))
     wt = rand_bits(rng, (N, K), 1.0 / np.sqrt(K))
     ref = f64(a) @ f64(wt).T
-    got = f64(gemm_bf16(a, wt, 0, bn))
+    got = f64(gemm_f16(a, wt, 0, bn))
     assert rel(got, ref) <= TOL_BF16
 
 
 @pytest.mark.parametrize("bn", [32, 64, 128, 256])
 def test_gemm_relu_and_f32(native, bn):
-    from paper_2501_01792_b200.kernels import gemm_bf16
+    from paper_2501_01792_b200.kernels import gemm_f16
     rng = np.random.default_rng(bn)
     M, N, K = 200, 512, 384
     a = rand_bits(rng, (M, K))
     wt = rand_bits(rng, (N, K), 1.0 / np.sqrt(K))
     ref = f64(a) @ f64(wt).T
-    got = f64(gemm_bf16(a, wt, 1, bn))
+    got = f64(gemm_f16(a, wt, 1, bn))
     assert rel(got, np.maximum(ref, 0)) <= TOL_BF16
     assert (got >= 0).all()
-    got32 = gemm_bf16(a, wt, 3, bn).astype(np.float64)
+    got32 = gemm_f16(a, wt, 3, bn).astype(np.float64)
     assert rel(got32, ref) <= 1e-4
 
 
@@ -197,14 +197,14 @@ def test_prefill_attention_causal(native, n_req, P, H, hd):
 @pytest.mark.parametrize("epi", [0, 1, 3])
 def test_gemm_cta_pair(native, M, N, K, epi):
     """Large-M GEMMs run on the CTA-pair (cta_group::2, 256x256) kernel."""
-    from paper_2501_01792_b200.kernels import gemm_bf16
+    from paper_2501_01792_b200.kernels import gemm_f16
     rng = np.random.default_rng(M + N + epi)
     a = rand_bits(rng, (M, K))
     wt = rand_bits(rng, (N, K), 1.0 / np.sqrt(K))
     ref = f64(a) @ f64(wt).T
     if epi == 1:
         ref = np.maximum(ref, 0)
-    got = gemm_bf16(a, wt, epi, 0).astype(np.float64) if epi == 3 else f64(gemm_bf16(a, wt, epi, 0))
+    got = gemm_f16(a, wt, epi, 0).astype(np.float64) if epi == 3 else f64(gemm_f16(a, wt, epi, 0))
     assert rel(got, ref) <= (1e-4 if epi == 3 else TOL_BF16)
 
 
@@ -232,12 +232,12 @@ def test_recompute_kv_paged_cta_pair(native, nb, tpb, d, heads):
 ])
 def test_gemm_splitk(native, M, N, K, bn, splits, epi):
     """Split-K decode GEMM: fp32 partials over K ranges + reduce == the full GEMM."""
-    from paper_2501_01792_b200.kernels import gemm_bf16_splitk
+    from paper_2501_01792_b200.kernels import gemm_f16_splitk
     rng = np.random.default_rng(K + splits)
     a = rand_bits(rng, (M, K))
     wt = rand_bits(rng, (N, K), 1.0 / np.sqrt(K))
     ref = f64(a) @ f64(wt).T
     if epi == 1:
         ref = np.maximum(ref, 0)
-    got = f64(gemm_bf16_splitk(a, wt, splits, epi, bn))
+    got = f64(gemm_f16_splitk(a, wt, splits, epi, bn))
     assert rel(got, ref) <= TOL_BF16
