@@ -59,6 +59,60 @@ def weights_case(out, tag, L, d, H, f, V, tpb, seed, max_seq, rescale):
     out[f"{tag}/recompute_v"] = rv
 
 
+def config1_case(out, B=4, P=128, G=32, seed=42):
+    """BASELINE configs[0] on the reference: OPT-125M shape (rescaled, fp16
+    weights pushed in), B prompts of P tokens, G greedy tokens through the
+    tied head (x E^T; an extension — the reference has no LM head). Request
+    b: forward_prompt(prompt[:-1]) (decoder.cpp:144-157), then G
+    generation_steps (decoder.cpp:159-174) fed prompt[-1], t0, t1, ...; the
+    context of every step is assembled as in verify.cpp:62-73 at KV:ACT 0.5
+    (ACT, KV, ACT, ... blocks of 16): ACT-kind prompt blocks are rebuilt by
+    recompute_kv_from_activation from their layer inputs, KV-kind blocks and
+    decode-grown rows are the stored K,V. Saves per step the fed token, the
+    output x, the greedy token and its top-2 logit margin."""
+    L, d, H, f, V, tpb = 12, 768, 12, 3072, 50272, 16
+    cfg = O.ModelConfig(num_layers=L, hidden_dim=d, num_heads=H, ffn_dim=f, vocab_size=V,
+                        tokens_per_block=tpb).validate()
+    rw = R.RefWeights(L, d, H, f, V, tpb, seed, P + G + 1)
+    ow = O.prepare_weights(O.generate_weights(cfg, seed, P + G + 1))
+    rw.set(0, 0, ow.embedding)
+    rw.set(1, 0, ow.positional)
+    for l in range(L):
+        for i, n in enumerate(O.WEIGHT_NAMES):
+            rw.set(2 + i, l, ow.layers[l][n])
+    E = ow.embedding
+    rng = np.random.default_rng(3)
+    prompts = rng.integers(0, V, (B, P)).astype(np.int32)
+    fed = np.zeros((G, B), np.int32)
+    toks = np.zeros((G, B), np.int32)
+    xs = np.zeros((G, B, d), np.float32)
+    margin = np.zeros((G, B))
+    for b in range(B):
+        ins, k, v, _ = rw.forward_prompt(prompts[b, :-1])
+        n0 = P - 1
+        for blk in range(0, (n0 + tpb - 1) // tpb, 2):  # ACT-kind blocks (tie -> ACT first)
+            sl = slice(blk * tpb, min((blk + 1) * tpb, n0))
+            for l in range(L):
+                k[l, sl], v[l, sl] = rw.recompute_kv(l, ins[l, sl])
+        tok = int(prompts[b, -1])
+        for g in range(G):
+            o, nk, nv = rw.generation_step(tok, n0 + g, k, v)
+            k = np.concatenate([k, nk[:, None, :]], axis=1)
+            v = np.concatenate([v, nv[:, None, :]], axis=1)
+            lg = o[0] @ E.T
+            top = np.argsort(lg)[-2:]
+            fed[g, b] = tok
+            toks[g, b] = int(top[1])
+            xs[g, b] = o[0]
+            margin[g, b] = (lg[top[1]] - lg[top[0]]) / np.abs(lg).max()
+            tok = int(top[1])
+    out["config1/prompts"] = prompts
+    out["config1/fed"] = fed
+    out["config1/tokens"] = toks
+    out["config1/x"] = xs
+    out["config1/margin"] = margin
+
+
 def tables_case(tpb, lens, gens, mode, act_host, kv_host, act_gpu, frees=()):
     """Replay simulate()'s add_token order (sim.cpp:150-223, 308-310) on the
     reference HybridCache + next_block_kind."""
@@ -104,6 +158,7 @@ def main():
     weights_case(out, "toy", 2, 32, 4, 64, 50, 4, 42, 40, rescale=False)
     weights_case(out, "toy_rescaled", 3, 256, 2, 512, 512, 16, 7, 40, rescale=True)
     weights_case(out, "opt125m_shape", 12, 768, 12, 3072, 50272, 16, 42, 160, rescale=True)
+    config1_case(out)
     np.savez_compressed(os.path.join(HERE, "golden.npz"), **out)
 
     j = {"block_tables": [], "next_block_kind": [], "plan": [], "fit_linear": [], "equivalence": [],

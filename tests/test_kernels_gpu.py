@@ -241,3 +241,101 @@ def test_gemm_splitk(native, M, N, K, bn, splits, epi):
         ref = np.maximum(ref, 0)
     got = f64(gemm_f16_splitk(a, wt, splits, epi, bn))
     assert rel(got, ref) <= TOL_BF16
+
+
+@pytest.mark.parametrize("scaled", [True, False])
+def test_decode_attention_unscaled_matches_oracle(native, scaled):
+    """attention_step(q, kv, heads, scaled) with scaled=false (decoder.hpp:28,
+    test_decoder.cpp:124-135): the raw q.k scores, no 1/sqrt(hd)."""
+    from paper_2501_01792_b200.kernels import decode_attention
+    rng = np.random.default_rng(11)
+    B, H, hd, tpb = 3, 4, 64, 16
+    q, r0, r1, refs, nbk, cl, _ = _attention_case(rng, B, H, hd, tpb, [7, 40, 130])
+    q = f32_bits(f64(q) * 0.25)  # keep the unscaled scores in a sane range
+    want = np.zeros((B, H * hd))
+    pools = [f64(r0), f64(r1)]
+    for b, c in enumerate(cl):
+        ks, vs = [], []
+        for i in range(nbk[b]):
+            blk = pools[refs[b, i] >> 28][refs[b, i] & 0x0FFFFFFF]
+            ks.append(blk[0].transpose(1, 0, 2).reshape(tpb, -1))
+            vs.append(blk[1].transpose(1, 0, 2).reshape(tpb, -1))
+        want[b] = O.attention_rows(f64(q)[b:b + 1], np.concatenate(ks)[:c], np.concatenate(vs)[:c], [int(c)], H,
+                                   scaled)[0]
+    got = f64(decode_attention(q, r0, r1, refs, nbk, cl, H, scaled, 1))
+    assert rel(got, want) <= TOL_BF16
+
+
+def f32_bits(x):
+    from paper_2501_01792_b200.kernels import f32_to_f16_bits
+    return f32_to_f16_bits(x)
+
+
+@pytest.mark.parametrize("splits", [1, 3])
+def test_decode_attention_identical_rows_return_shared_v(native, splits):
+    """test_decoder.cpp:109-122: every context token with the same K row and the
+    same V row -> the output is that V row (softmax weights sum to 1; the fp32
+    result rounds back to the fp16 V value)."""
+    from paper_2501_01792_b200.kernels import decode_attention
+    rng = np.random.default_rng(12)
+    B, H, hd, tpb, nb = 2, 2, 128, 16, 5
+    q = rand_bits(rng, (B, H * hd))
+    krow, vrow = rand_bits(rng, (H, hd)), rand_bits(rng, (H, hd))
+    r0 = np.zeros((nb, 2, H, tpb, hd), np.uint16)
+    r0[:, 0] = krow[None, :, None, :]
+    r0[:, 1] = vrow[None, :, None, :]
+    r1 = r0[:1].copy()
+    refs = np.tile(np.arange(nb, dtype=np.int32), (B, 1))
+    refs[1, 2] = (1 << 28)  # a block of the second region
+    cl = np.array([nb * tpb, nb * tpb - 7], np.int32)
+    got = decode_attention(q, r0, r1, refs, np.full(B, nb, np.int32), cl, H, True, splits)
+    for b in range(B):
+        assert np.abs(f64(got[b]) - f64(vrow.reshape(-1))).max() <= 2 ** -10 * np.abs(f64(vrow)).max()
+
+
+@pytest.mark.parametrize("scaled", [True, False])
+def test_decode_attention_stays_in_v_envelope(native, scaled):
+    """test_decoder.cpp:140-162: each output column lies inside [min, max] of
+    that column of V over the context (a convex combination), up to one fp16
+    rounding of the output, over random heads / widths / context lengths."""
+    from paper_2501_01792_b200.kernels import decode_attention
+    rng = np.random.default_rng(13)
+    for trial in range(12):
+        H = int(rng.integers(1, 5))
+        hd = int(rng.choice([64, 128]))
+        tpb = int(rng.choice([8, 16, 32]))
+        ctxs = [int(c) for c in rng.integers(1, 200, 3)]
+        q, r0, r1, refs, nbk, cl, _ = _attention_case(rng, 3, H, hd, tpb, ctxs, n0=40, n1=40)
+        got = f64(decode_attention(q, r0, r1, refs, nbk, cl, H, scaled, int(rng.integers(0, 3))))
+        pools = [f64(r0), f64(r1)]
+        for b, c in enumerate(ctxs):
+            vs = [pools[refs[b, i] >> 28][refs[b, i] & 0x0FFFFFFF][1].transpose(1, 0, 2).reshape(tpb, -1)
+                  for i in range(nbk[b])]
+            V = np.concatenate(vs)[:c]
+            lo, hi = V.min(axis=0), V.max(axis=0)
+            ulp = 2.0 ** -10 * np.maximum(np.abs(lo), np.abs(hi))
+            assert (got[b] >= lo - ulp).all() and (got[b] <= hi + ulp).all(), (trial, b)
+
+
+def test_recompute_fault_injection_is_caught(native):
+    """Negative control (verify.cpp:49-50, test_decoder.cpp:299-302): W_K[0,0]
+    += 0.5 in the recompute path must make the recomputed-K comparison fail
+    the 1e-2 bar, while the clean weights pass it. (The reference checks the
+    end-to-end output at 1e-10 in fp64; through the decoder that fault moves
+    the output by 1e-10..7e-4 — below any 16-bit bar — so the control sits at
+    the recompute boundary the north star's K/V tolerance applies to.)"""
+    from paper_2501_01792_b200.kernels import recompute_kv_paged
+    rng = np.random.default_rng(14)
+    nb, tpb, d, H = 16, 16, 256, 2
+    act = rand_bits(rng, (nb, tpb, d), 0.1)
+    w_k = rng.uniform(-0.1, 0.1, (d, d)) * 10 * np.sqrt(3 / d)
+    w_v = rng.uniform(-0.1, 0.1, (d, d)) * 10 * np.sqrt(3 / d)
+    wkv_t = f32_bits(np.concatenate([w_k.T, w_v.T]))
+    X = f64(act).reshape(-1, d)
+    want_k = X @ f64(wkv_t[:d]).T
+    faulted = f64(wkv_t).copy()
+    faulted[0, 0] += 0.5  # W_K[0][0] (row 0 of W_K^T is output column 0)
+    for w, caught in ((wkv_t, False), (f32_bits(faulted), True)):
+        got = f64(recompute_kv_paged(act, w, H, np.array([0, 128], np.int32)))
+        k = got[:, 0].transpose(0, 2, 1, 3).reshape(-1, d)
+        assert (rel(k, want_k) > TOL_BF16) == caught

@@ -119,12 +119,15 @@ def test_token_recompute_kv_gpu():
         eng.token_recompute_kv(ids, 4)
 
 
-@pytest.mark.parametrize("seed", range(10))
-def test_equivalence_seeded_models(seed):
-    """run_equivalence_case (verify.cpp:26-95) on the GPU: a seeded random model,
-    its context held as stored KV, as ACT checkpoints (recomputed), and as a
-    block-wise mix; the decode output is the same for all (within bf16
-    tolerance) and equals the oracle."""
+@pytest.mark.parametrize("seed,scaled", [(s, True) for s in range(25)] + [(3, False), (11, False)])
+def test_equivalence_seeded_models(seed, scaled):
+    """run_equivalence_case (verify.cpp:26-95) on the GPU over the reference's 25
+    seeds (test_decoder.cpp:290-295) plus its unscaled-attention case
+    (:296-298): a seeded random model, its context held as stored KV, as ACT
+    checkpoints (recomputed), as token-recompute and as a block-wise mix; the
+    decode output is the same for all (within the 16-bit tolerance) and
+    equals the oracle. Shapes are the reference's draw mapped onto the
+    engine's supported widths (head_dim 64/128, tokens_per_block 8/16)."""
     from paper_2501_01792_b200 import api
     rng = O.SplitMix64(O.mix_seed(seed, 0x657175))
     L = rng.uniform_int(1, 4)
@@ -137,21 +140,24 @@ def test_equivalence_seeded_models(seed):
     wseed = O.mix_seed(seed, 0x77)
     ids = [rng.uniform_int(0, 63) for _ in range(P)]
     tok = rng.uniform_int(0, 63)
-    eng = api.Engine(cfg, seed=wseed, max_seq=P + 2, max_batch=1)
+    eng = api.Engine(cfg, seed=wseed, max_seq=P + 2, max_batch=1, scaled=scaled)
     outs, stats = {}, {}
-    for mode, alloc in (("kv_only", None), ("act_only", None), ("hybrid", api.HostAllocation(1, 1))):
-        eng.configure_cache(api.PoolCaps(kv_host=8, act_host=8, act_gpu=2), mode=mode, allocation=alloc)
+    for mode, alloc, rc in (("kv_only", None, 0.0), ("act_only", None, 0.0), ("hybrid", api.HostAllocation(1, 1), 0.0),
+                            ("token_recompute", None, 0.5)):
+        eng.configure_cache(api.PoolCaps(kv_host=8, act_host=8, act_gpu=2), mode=mode, allocation=alloc,
+                            recompute_ratio=rc)
         eng.prefill(["q"], [ids])
         eng.set_profile(True)
         outs[mode] = f64(eng.decode_step(["q"], [tok])["x"])
         stats[mode] = (eng.last_stats(), eng.cache.dump_json())
     ocfg = O.ModelConfig(num_layers=L, hidden_dim=d, num_heads=H, ffn_dim=2 * d, vocab_size=64).validate()
     w = O.prepare_weights(O.generate_weights(ocfg, wseed, P + 2))
-    ref = O.forward_prompt(ids + [tok], w).output[-1:]
+    ref = O.forward_prompt(ids + [tok], w, scaled).output[-1:]
     for m, o in outs.items():
         assert rel(o, ref) <= TOL, (m, stats[m], (L, H, d, tpb, P))
     assert rel(outs["act_only"], outs["kv_only"]) <= TOL
     assert rel(outs["hybrid"], outs["kv_only"]) <= TOL
+    assert rel(outs["token_recompute"], outs["kv_only"]) <= TOL
 
 
 @pytest.mark.parametrize("on_device", [True, False])
@@ -179,3 +185,49 @@ def test_full_width_opt30b_layer_parity():
     mod = importlib.util.module_from_spec(spec)
     spec.loader.exec_module(mod)
     mod.main([])
+
+
+@pytest.mark.parametrize("weights_on_device", [False, True])
+def test_config1_greedy_matches_reference(gold, weights_on_device):
+    """BASELINE configs[0] exactly: OPT-125M shape (12 layers, d 768, vocab
+    50272), 4 requests, prompt 128, 32 greedy tokens, KV:ACT 0.5
+    (HostAllocation{K, K}: ACT, KV, ACT, ... blocks in pinned host pools).
+    Against the golden run of the UNMODIFIED reference (make_golden.py
+    config1_case: forward_prompt + recompute_kv_from_activation +
+    generation_step, tied head): every step's output x and full-vocabulary
+    logits within 1e-2, every greedy token equal (the GPU's argmax is what is
+    fed back), block tables equal the oracle's add_token replay."""
+    from paper_2501_01792_b200 import api
+    B, P, G, tpb = 4, 128, 32, 16
+    prompts = gold["config1/prompts"]
+    fed, toks, xs, margin = gold["config1/fed"], gold["config1/tokens"], gold["config1/x"], gold["config1/margin"]
+    K = B * ((P + G + tpb - 1) // tpb)
+    cfg = api.ModelConfig(num_layers=12, hidden_dim=768, num_heads=12, ffn_dim=3072, vocab_size=50272)
+    eng = api.Engine(cfg, seed=42, max_seq=P + G + 1, rescale=True, max_batch=B, weights_on_device=weights_on_device,
+                     caps=api.PoolCaps(kv_host=K, act_host=K), allocation=api.HostAllocation(K, K), mode="hybrid")
+    E = f64(eng.read_weights(-1)).reshape(cfg.vocab_size, cfg.hidden_dim)
+    ids = [f"c1r{b}" for b in range(B)]
+    eng.prefill(ids, [p[:-1].tolist() for p in prompts])
+    cur = [int(p[-1]) for p in prompts]
+    worst = 0.0
+    for s in range(G):
+        assert cur == fed[s].tolist(), s  # the GPU's own greedy path is the reference's
+        res = eng.decode_step(ids, cur, want_x=True, want_logits=True, want_argmax=True)
+        for b in range(B):
+            worst = max(worst, rel(f64(res["x"][b]), xs[s, b]))
+            assert rel(f64(res["x"][b]), xs[s, b]) <= TOL, (s, b)
+            assert rel(res["logits"][b], xs[s, b].astype(np.float64) @ E.T) <= TOL, (s, b)
+        cur = [int(t) for t in res["argmax"]]
+        assert cur == toks[s].tolist(), (s, cur, toks[s].tolist(), margin[s].tolist())
+    # greedy path unambiguous: the smallest top-2 margin over the run is far above the error
+    assert margin.min() > 10 * worst
+    ba = O.BlockAssigner(tpb, O.HYBRID, O.HostAllocation(K, K), act_gpu=0)
+    for rid in ids:
+        ba.add_request(rid, P - 1)
+        for _ in range(P - 1):
+            ba.add_token(rid)
+    for _ in range(G):
+        for rid in ids:
+            ba.add_token(rid)
+    assert eng.cache.dump_json() == O.dumps(ba.cache.dump_json())
+    eng.close()
