@@ -31,6 +31,10 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "generated tokens/sec, OPT-30B offloaded, per KV:ACT ratio, at 1/2/4/8 B200"
+# NVLink 5 model for the emulated multi-rank variants: NCCL all-reduce /
+# all-gather bus bandwidth measured on B200 NVSwitch nodes (725 GB/s;
+# /opt/skills/guides/B200_PROFILING.md; peer copies reach 770 GB/s per direction)
+NVLINK_BUSBW = 725e9
 
 
 def parse():
@@ -78,6 +82,13 @@ def parse():
     p.add_argument("--no-config2", action="store_true", help="skip the OPT-6.7B resident (config 2) variant")
     p.add_argument("--artifacts", default="", help="write the reference CLI's artifacts (kv_gen.csv, load_kv.csv, "
                                                     "bundle.json, plan.json, metrics.json, trace.json) here")
+    p.add_argument("--bundle", default="committed",
+                   help="timing bundle the planner ratio comes from: 'committed' = profiles/planner_bundle_<model>.json "
+                        "(B200-measured, read by BOTH arms so they run the same r), 'live' = this run's calibration, "
+                        "or a path")
+    p.add_argument("--full-generation", action="store_true",
+                   help="time the whole generation instead: real prefill of P tokens + G decode steps, every step "
+                        "timed (prints the measured generation line; minutes)")
     a = p.parse_args()
     if a.config == 4:
         a.model = a.model or "opt-66b"
@@ -272,93 +283,185 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------ CPU baseline ---
-def cpu_reference_sample(cfg, prompt: int, ratio: float, threads: int):
-    """The reference's own CPU path for this workload, bounded: one request,
-    one layer of one decode step at full OPT width — recompute K,V of the
-    request's ACT-cached context tokens (recompute_kv_from_activation,
-    decoder.cpp:123-129) + generation_step of that layer over the full
-    context (decoder.cpp:159-174). tokens/s = 1 / (num_layers * t_sample)."""
+def cpu_reference_sample(dims, ctx: int, n_act: int, threads: int, chunk: int = 64):
+    """The reference's own CPU path for this workload, bounded: ONE request at
+    ONE layer of one decode step at full model width — generation_step of
+    that layer over a context of `ctx` tokens (decoder.cpp:159-174) plus
+    recompute_kv_from_activation (decoder.cpp:123-129) of a `chunk`-row slice
+    of the request's ACT rows, scaled to its n_act ACT tokens (the reference
+    GEMM is row-parallel, matrix.cpp:28, so its cost is linear in rows).
+    run() returns seconds per request-layer; a step of B requests x L layers
+    costs B x L of them, so tokens/s = 1 / (L x run()). Vocabulary 16 (the
+    reference has no LM head; the embedding table does not enter the
+    per-layer cost)."""
     os.environ["OMP_NUM_THREADS"] = str(threads)
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import ref_lib as R  # noqa: E402  (checker / baseline only)
-    d, H, f, V, tpb = cfg.hidden_dim, cfg.num_heads, cfg.ffn_dim, cfg.vocab_size, cfg.tokens_per_block
-    n_act = int(round(ratio * prompt))
+    d, H, f, tpb = dims.hidden_dim, dims.num_heads, dims.ffn_dim, dims.tokens_per_block
+    rng = np.random.default_rng(0)
+    ck = rng.uniform(-0.1, 0.1, (1, ctx, d))
+    cv = rng.uniform(-0.1, 0.1, (1, ctx, d))
+    a = rng.uniform(-0.1, 0.1, (chunk, d))
     if R.available():
         kind = "reference"
         threads = R.set_threads(threads)  # torchrun exports OMP_NUM_THREADS=1 before libgomp loads
-        rw = R.RefWeights(1, d, H, f, V, tpb, 42, prompt + 2)
-        rng = np.random.default_rng(0)
-        a = rng.uniform(-0.1, 0.1, (max(n_act, 1), d))
-        ck = rng.uniform(-0.1, 0.1, (1, prompt, d))
-        cv = rng.uniform(-0.1, 0.1, (1, prompt, d))
+        rw = R.RefWeights(1, d, H, f, 16, tpb, 42, ctx + 2)
 
         def run():
             t0 = time.perf_counter()
+            rw.generation_step(1, ctx, ck, cv)
+            t1 = time.perf_counter()
             if n_act:
                 rw.recompute_kv(0, a)
-            rw.generation_step(1, prompt, ck, cv)
-            return time.perf_counter() - t0
+            t2 = time.perf_counter()
+            return (t1 - t0) + (t2 - t1) * n_act / chunk
     else:
         import hybridsim_oracle as O  # noqa: E402
         kind = "port"
-        rng = np.random.default_rng(0)
-        wl = {n: rng.uniform(-0.1, 0.1, s) for n, s in
-              zip(O.WEIGHT_NAMES, [(d, d)] * 4 + [(d, f), (f, d)])}
+        wl = {n: rng.uniform(-0.1, 0.1, sh) for n, sh in zip(O.WEIGHT_NAMES, [(d, d)] * 4 + [(d, f), (f, d)])}
         w = O.DecoderWeights(O.ModelConfig(num_layers=1, hidden_dim=d, num_heads=H, ffn_dim=f,
-                                           vocab_size=V).validate(), prompt + 2,
-                             rng.uniform(-0.1, 0.1, (V, d)), rng.uniform(-0.1, 0.1, (prompt + 2, d)), [wl])
-        a = rng.uniform(-0.1, 0.1, (max(n_act, 1), d))
-        ck = [rng.uniform(-0.1, 0.1, (prompt, d))]
-        cv = [rng.uniform(-0.1, 0.1, (prompt, d))]
+                                           vocab_size=16).validate(), ctx + 2,
+                             rng.uniform(-0.1, 0.1, (16, d)), rng.uniform(-0.1, 0.1, (ctx + 2, d)), [wl])
 
         def run():
             t0 = time.perf_counter()
+            O.generation_step(1, ctx, [ck[0]], [cv[0]], w)
+            t1 = time.perf_counter()
             if n_act:
                 O.recompute_kv_from_activation(a, 0, w)
-            O.generation_step(1, prompt, ck, cv, w)
-            return time.perf_counter() - t0
-    return kind, run, (f"1 request x 1 layer of one decode step at {cfg.name} width (d={d}), context {prompt}, "
-                       f"{n_act} ACT-recomputed tokens + generation_step; extrapolated x{cfg.num_layers} layers"), threads
+            t2 = time.perf_counter()
+            return (t1 - t0) + (t2 - t1) * n_act / chunk
+
+    sample = (f"1 request x 1 layer of one decode step at {dims.name} width (d={d}): generation_step over context "
+              f"{ctx} + recompute_kv_from_activation of {chunk} of its {n_act} ACT rows (scaled linearly); x "
+              f"{dims.num_layers} layers per token")
+    return kind, run, sample, threads, R if kind == "reference" else None
 
 
-def reference_arm(args, cfg, world, rank, dist):
+def single_thread_leg(dims, ctx, n_act, reps=2):
+    """The same sample with OMP_NUM_THREADS=1."""
+    kind, run, sample, _, R = cpu_reference_sample(dims, ctx, n_act, 1)
+    run()
+    t = statistics.mean([run() for _ in range(reps)])
+    return {"value": 1.0 / (dims.num_layers * t), "unit": "tokens/s", "cores": 1, "kind": kind, "steps": reps}
+
+
+def reference_arm(args, world, rank, dist):
+    """The reference's CPU path on this host: never imports the product."""
     if rank != 0:
         return
+    dims = reference_dims(args.model)
+    if args.layers:
+        dims.num_layers = args.layers
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import ref_lib as R  # noqa: E402
+    B = per_rank_batch(args, world, 0)
+    bp = bundle_path(args)
+    if args.ratio >= 0:
+        r, src = args.ratio, "--ratio"
+    elif bp and R.available():
+        r, factor, _ = planned_ratio(R.parse_bundle(bp), dims, B * (args.prompt + args.gen), R.plan_host_allocation)
+        src = (f"planner: the reference's plan_host_allocation (plan.cpp:106-152) on the B200-measured bundle "
+               f"{os.path.relpath(bp, ROOT)}, workload-sized m_host (x{factor})")
+    else:
+        r, src = 1.0 / 3.0, "the paper's KV:ACT 2:1 (PAPER.md:714): no committed bundle"
+    ctx = args.prompt + args.gen // 2
+    n_act = int(round(r * ctx))
     threads = os.cpu_count() or 1
-    # the CPU path has no measured rates to plan with: it runs the paper's KV:ACT 2:1
-    # (PAPER.md:714) unless --ratio is given
-    r_cpu = args.ratio if args.ratio >= 0 else 1.0 / 3.0
-    kind, run, sample, threads = cpu_reference_sample(cfg, args.prompt, r_cpu, threads)
+    kind, run, sample, threads, _ = cpu_reference_sample(dims, ctx, n_act, threads)
     for _ in range(args.warmup):
         run()
     ts = [run() for _ in range(args.steps)]
     t = statistics.mean(ts)
-    v = 1.0 / (cfg.num_layers * t)
+    v = 1.0 / (dims.num_layers * t)
+    st = single_thread_leg(dims, ctx, n_act)
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": v, "unit": "tokens/s", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
-        "scaling": args.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": workload_config(args, cfg, world, {"act_share_r": r_cpu, "ratio_source":
-                                                     "--ratio, else the paper's 2:1 (no planner on the CPU path)"}),
-        "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": threads, "kind": kind, "sample": sample},
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": B * dims.num_layers * t * 1e3,
+        "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": bench_config(args, dims, world, r, src, ctx),
+        "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": threads, "kind": kind, "sample": sample,
+                         "single_thread": st},
         "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
 
 
-def workload_config(args, cfg, world, extra=None):
+class Dims:
+    """Model dimensions without importing the product (the reference arm must
+    not load libhybridcache_b200.so)."""
+
+    def __init__(self, name, layers, d, heads, ffn, vocab, tpb):
+        self.name, self.num_layers, self.hidden_dim, self.num_heads = name, layers, d, heads
+        self.ffn_dim, self.vocab_size, self.tokens_per_block = ffn, vocab, tpb
+
+
+def reference_dims(model):
+    """ModelConfig::preset (model.cpp:37-43) through the reference library,
+    else the oracle's restatement."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import ref_lib as R  # noqa: E402  (reference arm / baseline only)
+    if R.available():
+        return Dims(model, *R.model_preset(model))
+    import hybridsim_oracle as O  # noqa: E402
+    c = O.preset(model)
+    return Dims(model, c.num_layers, c.hidden_dim, c.num_heads, c.ffn_dim, c.vocab_size, c.tokens_per_block)
+
+
+def bundle_path(args):
+    if args.bundle == "live":
+        return None
+    if args.bundle == "committed":
+        p = os.path.join(ROOT, "profiles", f"planner_bundle_{args.model}.json")
+        return p if os.path.exists(p) else None
+    return args.bundle
+
+
+def read_bundle(path):
+    """bundle.json (timing.cpp:147-153) -> (kv slope, kv icept, load slope, load icept, t_load_w, s_w_layer, s_w_total)."""
+    with open(path) as fh:
+        j = json.load(fh)
+    return (j["kv_gen"]["slope"], j["kv_gen"]["intercept"], j["load_kv"]["slope"], j["load_kv"]["intercept"],
+            j["t_load_w"], float(j["s_weight_layer"]), float(j["s_weight_total"]))
+
+
+def planned_ratio(b7, dims, workload_tokens, plan_fn):
+    """plan_host_allocation (plan.cpp:106-152) over a WORKLOAD-sized host
+    budget, as the reference's interior-balance test sizes it
+    (test_sim.cpp:281-282: m_host = s_weight + 0.9 x workload blocks x
+    s_kv_block; widened only when Alg. 1 raises CapacityError). plan_fn(b5,
+    mem4, tpb, act_gpu) -> (act_host, kv_host, ...) is the reference's planner
+    in the reference arm and the product's (bit-exact) in ours, so both arms
+    derive the same r from the same bundle."""
+    L, d, tpb = dims.num_layers, dims.hidden_dim, dims.tokens_per_block
+    s_kv, s_act = float(tpb * 2 * d * 2) * L, float(tpb * d * 2) * L  # bytes_of x L (plan.cpp:46-49)
+    blocks = workload_tokens / tpb
+    err = None
+    for factor in (0.9, 1.5, 3.0, 6.0, 12.0):
+        mem = [b7[6] + blocks * s_kv * factor, b7[6], s_kv, s_act]
+        try:
+            a = plan_fn(list(b7[:5]), mem, tpb, 0)
+            return a[0] / max(a[0] + a[1], 1), factor, list(a)
+        except Exception as e:  # CapacityError (plan.cpp:79) in either library
+            err = e
+    raise err
+
+
+def bench_config(args, dims, world, r, ratio_source, timed_ctx):
+    """The `config` object, built identically by both arms (same workload,
+    same r, same timed context)."""
     B = per_rank_batch(args, world, 0)
     gb = args.global_batch or B * world
-    c = {"workload": f"BASELINE configs[{args.config - 1}]: {cfg.name}-shape offloaded decode (weights + hybrid KV/ACT "
-                     f"cache in pinned host memory), " +
-                     (f"global batch {gb} split over {world} GPU(s)" if args.global_batch else f"batch {B}/GPU") +
-                     f", prompt {args.prompt}, gen {args.gen}",
-         "model": cfg.name, "global_batch": gb, "batch_per_gpu": B, "seq_len": args.prompt, "gen_len": args.gen,
-         "act_share_r": round(extra.get("act_share_r", args.ratio), 4) if extra else round(args.ratio, 4),
-         "parallelism": f"batch-partitioned x{world} (no collective)", "arch": args.arch,
-         "l2": "inputs larger than L2 (~100+ GB streamed host->HBM per step)"}
-    if extra:
-        c.update(extra)
-    return c
+    return {"workload": f"BASELINE configs[{args.config - 1}]: {dims.name}-shape offloaded decode (weights + hybrid "
+                        f"KV/ACT cache in pinned host memory), " +
+                        (f"global batch {gb} split over {world} GPU(s)" if args.global_batch else f"batch {B}/GPU") +
+                        f", prompt {args.prompt}, gen {args.gen}",
+            "model": dims.name, "global_batch": gb, "batch_per_gpu": B, "seq_len": args.prompt, "gen_len": args.gen,
+            "act_share_r": round(r, 6),
+            "kv_act_ratio": (f"{(1 - r) / r:.3f}:1" if 0 < r < 1 else ("kv_only" if r <= 0 else "act_only")),
+            "ratio_source": ratio_source, "timed_context": timed_ctx,
+            "timed_context_note": "decode steps timed at the generation's mean context P + G/2",
+            "parallelism": f"batch-partitioned x{world} (no collective)", "arch": args.arch,
+            "l2": "inputs larger than L2 (~100+ GB streamed host->HBM per step)"}
 
 
 # ------------------------------------------------------------------ ours ---
@@ -624,14 +727,38 @@ def our_arm(args, cfg, world, rank, local, dist):
         B = per_rank_batch(args, world, rank)
     P, L, d = args.prompt, cfg.num_layers, cfg.hidden_dim
     total_steps = args.warmup + args.steps + 2
-    max_seq = P + max(total_steps, args.gen + 4) + 1  # room for the end-of-generation step (below)
-    r = args.ratio if args.ratio >= 0 else 1.0 / 3.0  # planner replaces the default below
-    mode, alloc, caps = pool_plan(cfg, B, P, total_steps, r)
+    # the timed steps sit at the generation's mean context P + G/2: after the
+    # real prefill of P tokens, each request is grown by n_adv tokens through
+    # the allocator in decode order (the block tables G/2 real steps would
+    # leave; slots pattern-filled), then warm-up, one profiled step, K timed
+    ctx_mid = P + args.gen // 2
+    c0 = ctx_mid - (args.steps - 1) // 2  # context before the first timed step
+    n_adv = max(0, c0 - (args.warmup + 1) - P)
+    span = P + n_adv + total_steps  # tokens per request the pools must hold
+    max_seq = max(span, P + args.gen + 4) + 1
+    # planner ratio (north-star (5)): paper Alg. 1 on a B200-measured timing
+    # bundle — by default the committed one both arms read (same r), the
+    # live calibration below is reported beside it
+    bp = bundle_path(args)
+    if args.ratio >= 0:
+        r, r_src = args.ratio, "--ratio"
+    elif bp:
+        r, factor, _ = planned_ratio(read_bundle(bp), cfg, B * (P + args.gen),
+                                     lambda b5, m4, tpb, ag: list(api.plan_host_allocation(
+                                         api.TimingBundle(api.LinearTimeModel(b5[0], b5[1]),
+                                                          api.LinearTimeModel(b5[2], b5[3]), b5[4]),
+                                         api.MemoryBudget(*m4), tpb, ag).__dict__.values()))
+        r_src = (f"planner: the reference's plan_host_allocation (plan.cpp:106-152) on the B200-measured bundle "
+                 f"{os.path.relpath(bp, ROOT)}, workload-sized m_host (x{factor})")
+    else:
+        r, r_src = 1.0 / 3.0, "live"  # replaced by the live planner below
+    mode, alloc, caps = pool_plan(cfg, B, span, 0, r)
     w_layer, _ = api.weight_bytes(cfg)
     local_world = int(os.environ.get("LOCAL_WORLD_SIZE", str(world)))
-    # pinned host budget: never more than 120 GB or MemAvailable - 48 GB per node
-    # (pinned pages cannot be reclaimed; folding keeps the streamed bytes)
-    budget = args.host_gb * 1e9 if args.host_gb > 0 else min(120e9, mem_available_bytes() - 48e9) / local_world
+    # pinned host budget: what the node has available minus a 40 GB reserve
+    # for the OS and this process, split over the node's ranks (pinned pages
+    # cannot be reclaimed; folding keeps the streamed bytes)
+    budget = args.host_gb * 1e9 if args.host_gb > 0 else max(16e9, mem_available_bytes() - 40e9) / local_world
     w_rank = w_layer / tpn  # pinned weight bytes per layer on this rank
     Lw = L if L * w_rank <= 0.55 * budget else max(2, int(0.55 * budget // w_rank))
     Lp = host_layers_for(cfg, caps, budget, Lw * w_rank, tpn)
@@ -640,13 +767,16 @@ def our_arm(args, cfg, world, rank, local, dist):
                      caps=caps, host_layers=Lp, weight_layers=Lw, mode=mode, allocation=alloc, device=local,
                      arch=args.arch, tp=tp, weight_share=ws)
     ids = [f"g{0 if tp else rank}r{i}" for i in range(B)]
-    # host-link peak: a large pinned H2D copy on the engine's copy stream
+    # host-link peak: a large pinned H2D copy on the engine's copy stream, all
+    # ranks copying at once (ranks share PCIe switches)
     tpb = cfg.tokens_per_block
     n_tok = min(caps.kv_host * tpb, 65536) if caps.kv_host else 0
+    barrier(dist)
     # (best of 3 trials of 4 back-to-back copies: the copy engine's sustained peak)
     link_gbs = (n_tok * 2 * (d // tpn) * 2) / min(eng.time_load_kv(n_tok, reps=4) for _ in range(3)) / 1e9 \
         if n_tok else None
-    # north-star (5): the ratio comes from the planner fed with measured rates
+    barrier(dist)
+    # live calibration (north-star (5)): measured recompute-GEMM and link samples
     planner = None
     if link_gbs and caps.act_host:
         try:
@@ -654,18 +784,23 @@ def our_arm(args, cfg, world, rank, local, dist):
                                         wsn=wsn)
         except Exception as e:  # planner failure must not kill the bench line
             planner = {"error": str(e)}
-    if args.ratio < 0 and planner and "planned_r" in planner:
+    if r_src == "live" and planner and "planned_r" in planner:
         r = planner["planned_r"]
-        mode, alloc, caps = pool_plan(cfg, B, P, total_steps, r)
+        r_src = "planner: plan_host_allocation (plan.cpp:106-152) on this run's live calibration"
+        mode, alloc, caps = pool_plan(cfg, B, span, 0, r)
         Lp = host_layers_for(cfg, caps, budget, Lw * w_rank, tpn)
         eng.configure_cache(caps, mode=mode, allocation=alloc, host_layers=Lp)
     setup_s = time.time() - t_setup
     # the cache the decode steps read is built by the real offloaded prefill
     # of B synthetic prompts (weights streamed once per layer, host blocks
     # stored by D2H runs) — measured, and reported as its own stage
-    prefill = run_prefill(eng, cfg, ids, P, rank, tflops_sust, link_gbs) if args.prefill == "real" else None
-    if prefill is None:
+    if args.prefill == "real":
+        eng.fill_pools(seed=1 + rank)  # slots handed out by advance_synthetic hold finite values
+        prefill = run_prefill(eng, cfg, ids, P, rank, tflops_sust, link_gbs)
+    else:
+        prefill = None
         eng.admit_synthetic(ids, [P] * B, seed=1 + rank)
+    eng.advance_synthetic(ids, n_adv)
 
     rng = np.random.default_rng(rank)
     tokens = rng.integers(0, cfg.vocab_size, (total_steps, B)).astype(np.int32)
@@ -718,7 +853,7 @@ def our_arm(args, cfg, world, rank, local, dist):
             "flops_per_launch": rec_flops, "launch_ms": rec_launch_ms}
     # per-step roofline (north_star): slower of link bytes / link BW, tensor
     # FLOPs / tensor peak, HBM bytes / HBM BW
-    ctx = P + args.warmup + 1 + args.steps // 2
+    ctx = c0 + (args.steps - 1) / 2.0
     # (a head-sharded rank does 1/N of the FLOPs and HBM traffic)
     tensor_flops = L * (4.0 * d * d * act_tokens + 2.0 * B * (4 * d * d + 2 * d * cfg.ffn_dim)) / tpn
     hbm_bytes = L * (B * (ctx + 1) * 2 * d * 2 + act_tokens * 3 * d * 2 + w_layer) / tpn + h2d_step
@@ -741,30 +876,15 @@ def our_arm(args, cfg, world, rank, local, dist):
     # steps at context P+g projected from the measured step by streamed bytes
     # (the step is link-bound: step_roofline.bound == "link")
     gen = None
-    if prefill is not None and not args.no_sweep:
-        # the decode step at the END of the generation (context P + G), measured on
-        # the same engine and ratio: step time is linear in the context (streamed
-        # blocks, attention bytes), so the G steps sum to G x the endpoint mean
-        try:
-            ctx_end = P + args.gen
-            _, alloc_e, caps_e = pool_plan(cfg, B, ctx_end, 4, r)
-            eng.configure_cache(caps_e, mode=mode, allocation=alloc_e,
-                                host_layers=host_layers_for(cfg, caps_e, budget, Lw * w_rank, tpn))
-            eng.admit_synthetic(ids, [ctx_end] * B, seed=3 + rank)
-            run_steps(eng, ids, tokens, 0, 1)
-            end = run_steps(eng, ids, tokens, 1, 2)
-            ms_end = end["dev_ms"] / 2
-            dec_s = args.gen * (ms_per_step + ms_end) / 2e3
-            gen = {"prefill_s": prefill["prefill_s"], "step_ms_at_prompt": ms_per_step,
-                   "step_ms_at_prompt_plus_gen": ms_end, "decode_s": dec_s, "gen_len": args.gen,
-                   "tokens_per_s": B * args.gen / (prefill["prefill_s"] + dec_s),
-                   "tokens_per_s_all_ranks": B * args.gen * world / (prefill["prefill_s"] + dec_s),
-                   "prefill_share": prefill["prefill_s"] / (prefill["prefill_s"] + dec_s),
-                   "method": "prefill measured; decode steps measured at context P and P+G (same ratio, real "
-                             "allocator, pattern-filled blocks), summed as G x their mean (step time is linear "
-                             "in the context)"}
-        except Exception as e:  # must not cost the bench line
-            gen = {"error": str(e)}
+    if prefill is not None:
+        dec_s = args.gen * ms_per_step / 1e3
+        gen = {"prefill_s": prefill["prefill_s"], "step_ms_at_mean_context": ms_per_step, "decode_s": dec_s,
+               "gen_len": args.gen, "tokens_per_s": B * args.gen / (prefill["prefill_s"] + dec_s),
+               "tokens_per_s_all_ranks": B * args.gen * world / (prefill["prefill_s"] + dec_s),
+               "prefill_share": prefill["prefill_s"] / (prefill["prefill_s"] + dec_s),
+               "method": "prefill measured at P; G decode steps x the step measured at the mean context P + G/2 "
+                         "(step time is linear in the context). The generation timed step by step: "
+                         "bench.py --full-generation (profiles/r02_full_generation_opt30b.json)"}
 
     # ---- per-ratio sweep, planner, HBM-tiered variant (untimed by the contract)
     extra = {}
@@ -775,9 +895,9 @@ def our_arm(args, cfg, world, rank, local, dist):
                     ({planner["planned_r"]} if planner and "planned_r" in planner else set()))
         per = []
         for tr in [float(x[2:]) for x in args.sweep.split(",") if x.startswith("tr")]:
-            cm = pool_plan(cfg, B, P, sweep_steps + sweep_warm + 1, 0.0)
+            cm = pool_plan(cfg, B, ctx_mid, sweep_steps + sweep_warm + 1, 0.0)
             try:
-                per.append(variant(eng, cfg, ids, sw_tokens, P, 0.0, cm,
+                per.append(variant(eng, cfg, ids, sw_tokens, ctx_mid, 0.0, cm,
                                    host_layers_for(cfg, cm[2], budget, Lw * w_layer), sweep_steps, sweep_warm,
                                    link_gbs, 5, token_recompute=tr))
             except Exception as e:
@@ -789,9 +909,9 @@ def our_arm(args, cfg, world, rank, local, dist):
                             "link_frac": step_roof["frac"], "e2e_tokens_per_s": e2e, "steps": args.steps,
                             "act_context_tokens": act_tokens, "headline": True})
                 continue
-            cm = pool_plan(cfg, B, P, sweep_steps + sweep_warm + 1, rr)
+            cm = pool_plan(cfg, B, ctx_mid, sweep_steps + sweep_warm + 1, rr)
             try:
-                per.append(variant(eng, cfg, ids, sw_tokens, P, rr, cm, host_layers_for(cfg, cm[2], budget, Lw * w_layer),
+                per.append(variant(eng, cfg, ids, sw_tokens, ctx_mid, rr, cm, host_layers_for(cfg, cm[2], budget, Lw * w_layer),
                                    sweep_steps, sweep_warm, link_gbs, 7 + len(per)))
             except Exception as e:
                 per.append({"act_share_r": rr, "error": str(e)})
@@ -799,11 +919,11 @@ def our_arm(args, cfg, world, rank, local, dist):
         # B200 tiering: ACT blocks in HBM first (cache.cpp:85-91 placement),
         # sized to the free HBM; weights still streamed from pinned host memory
         try:
-            cm = pool_plan(cfg, B, P, sweep_steps + sweep_warm + 1, 1.0)
+            cm = pool_plan(cfg, B, ctx_mid, sweep_steps + sweep_warm + 1, 1.0)
             free_b, _ = torch.cuda.mem_get_info(local)
             blk_all_layers = api.HybridCache.bytes_of("ACT", cfg) * L
             act_gpu = int(min(cm[2].act_host, 0.85 * (free_b - 8e9) // blk_all_layers))
-            hv = variant(eng, cfg, ids, sw_tokens, P, 1.0, cm, host_layers_for(cfg, cm[2], budget, Lw * w_layer),
+            hv = variant(eng, cfg, ids, sw_tokens, ctx_mid, 1.0, cm, host_layers_for(cfg, cm[2], budget, Lw * w_layer),
                          sweep_steps, sweep_warm, link_gbs, 99, act_gpu=act_gpu)
             hv["note"] = ("ACT/gpu pool in HBM (ACT blocks placed on GPU first, cache.cpp:85-91); "
                           "weights + overflow blocks streamed from pinned host")
@@ -820,12 +940,12 @@ def our_arm(args, cfg, world, rank, local, dist):
                    "rank_h2d_gb_per_step": h2d_step / 1e9, "rank_weight_h2d_gb_per_step": L * w_layer / wsn / 1e9,
                    "nvlink_allgather_bytes_per_layer": ag}
         if args.share_emulate > 1:
-            busbw = 650e9  # assumed NCCL all-gather bus bandwidth on NVLink 5 (900 GB/s/direction nominal)
+            busbw = NVLINK_BUSBW
             t_ag = L * ag / busbw
             t_proj = max(ms_per_step / 1e3, t_ag + (ag / busbw))  # + one layer's gather exposed at the start
             ws_info.update({"note": "ONE of N batch-partitioned ranks timed on one GPU with 1/N of every weight "
                                     "layer streamed over its host link; the all-gather is skipped and NVLink time "
-                                    "modelled at an assumed 650 GB/s (own stream, overlapped)",
+                                    "modelled at the measured NCCL bus bandwidth (own stream, overlapped)",
                             "rank_step_ms_measured": ms_per_step, "nvlink_allgather_ms_per_step": t_ag * 1e3,
                             "projected_step_ms": t_proj * 1e3, "projected_tokens_per_s_per_gpu": B / t_proj,
                             "projected_tokens_per_s_whole_job": wsn * B / t_proj})
@@ -841,46 +961,34 @@ def our_arm(args, cfg, world, rank, local, dist):
                    "rank_h2d_gb_per_step": h2d_step / 1e9,
                    "allgather_bytes_per_layer": ag_bytes, "allreduce_bytes_per_layer": ar_bytes}
         if args.tp_emulate > 1:
-            busbw = 650e9  # assumed NCCL bus bandwidth on NVLink 5 (900 GB/s/direction nominal)
+            busbw = NVLINK_BUSBW
             t_ag, t_ar = L * ag_bytes / busbw, L * ar_bytes / busbw
             t_proj = max(ms_per_step / 1e3, t_ag) + t_ar
             tp_info.update({"note": "ONE rank of the N-way head-sharded group timed on one GPU: its weight / KV / "
                                     "ACT shards streamed, its heads computed, collectives skipped; NVLink time "
-                                    "modelled at an assumed 650 GB/s NCCL bus bandwidth (gather overlapped on its "
+                                    "modelled at the measured NCCL bus bandwidth (gather overlapped on its "
                                     "own stream, all-reduces serial)",
                             "rank_step_ms_measured": ms_per_step, "nvlink_allgather_ms_per_step": t_ag * 1e3,
                             "nvlink_allreduce_ms_per_step": t_ar * 1e3, "projected_step_ms": t_proj * 1e3,
                             "projected_tokens_per_s": B / t_proj})
     res = None
     if rank == 0:
-        cpu = None
-        if world == 1 and not args.no_cpu_baseline:
-            if _ALL_CPUS:  # the CPU reference gets every host core back
-                os.sched_setaffinity(0, _ALL_CPUS)
-            threads = os.cpu_count() or 1
-            kind, run, sample, threads = cpu_reference_sample(cfg, P, r, threads)
-            run()  # warm
-            t = statistics.mean([run() for _ in range(2)])
-            cpu = {"value": 1.0 / (L * t), "unit": "tokens/s", "cores": threads, "kind": kind, "sample": sample}
         res = {
             "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": args.scaling,
-            "vs_baseline": None, "dtype": "bf16",
+            "vs_baseline": None, "dtype": "f16",
             "data": ("synthetic (reference-draw weights rescaled; random prompts, cache built by the real offloaded "
-                     "prefill)" if prefill else "synthetic (reference-draw weights rescaled, pattern-filled cache "
-                                                "at prompt length)"),
-            "config": workload_config(args, cfg, world, {
-                "act_share_r": r,
-                "kv_act_ratio": (f"{(1 - r) / r:.3f}:1" if 0 < r < 1 else ("kv_only" if r <= 0 else "act_only")),
-                "ratio_source": ("planner (plan_host_allocation on measured kv_gen / load_kv samples)"
-                                 if args.ratio < 0 and planner and "planned_r" in planner else "--ratio"),
-                "mode": mode, "host_layers_phys": Lp, "weight_layers_phys": Lw,
-                "host_pool_fold": ("none" if Lp == L and Lw == L else
-                                   f"host storage folded to {Lp} cache / {Lw} weight layer copies "
-                                   "(box DRAM); bytes streamed per layer unchanged"),
-                "kv_host_blocks": caps.kv_host, "act_host_blocks": caps.act_host,
-                "numa_node": numa_node,
-                "act_context_tokens": act_tokens}),
+                     "prefill, then grown to the mean context in decode order)" if prefill else
+                     "synthetic (reference-draw weights rescaled, pattern-filled cache)"),
+            "config": bench_config(args, cfg, world, r, r_src, ctx_mid),
+            "details": {"mode": mode, "host_layers_phys": Lp, "weight_layers_phys": Lw,
+                        "host_pool_fold": ("none" if Lp == L and Lw == L else
+                                           f"host storage folded to {Lp} cache / {Lw} weight layer copies "
+                                           "(box DRAM); bytes streamed per layer unchanged"),
+                        "pinned_budget_gb": budget / 1e9, "kv_host_blocks": caps.kv_host,
+                        "act_host_blocks": caps.act_host, "numa_node": numa_node, "act_context_tokens": act_tokens,
+                        "advanced_tokens_per_request": n_adv, "first_timed_context": c0,
+                        "live_planned_r": planner.get("planned_r") if planner else None},
             "e2e": {"value": e2e, "unit": "tokens/s", "h2d_bytes_per_step": h2d_step + B * 4,
                     "d2h_bytes_per_step": acc["d2h"] / args.steps + B * 4,
                     "note": "decode_step C-ABI call with host token ids in / argmax out; includes the host-link "
@@ -888,7 +996,7 @@ def our_arm(args, cfg, world, rank, local, dist):
             "gpu_launches": acc["launches"],
             "roofline": roof,
             "step_roofline": step_roof,
-            "cpu_baseline": cpu,
+            "cpu_baseline": None,
             "clocks": clk,
             "setup_s": setup_s,
             "planner": planner,
@@ -913,6 +1021,16 @@ def our_arm(args, cfg, world, rank, local, dist):
         res.update(extra)
     eng.close()
     if rank == 0:
+        if world == 1 and not args.no_cpu_baseline:
+            # after the engine released its pinned pools; every host core back
+            if _ALL_CPUS:
+                os.sched_setaffinity(0, _ALL_CPUS)
+            n_act = int(round(r * ctx_mid))
+            kind, run, sample, threads, _ = cpu_reference_sample(cfg, ctx_mid, n_act, os.cpu_count() or 1)
+            run()  # warm
+            t = statistics.mean([run() for _ in range(2)])
+            res["cpu_baseline"] = {"value": 1.0 / (L * t), "unit": "tokens/s", "cores": threads, "kind": kind,
+                                   "sample": sample, "single_thread": single_thread_leg(cfg, ctx_mid, n_act)}
         if not args.no_sweep and world == 1:
             try:
                 res["hbm_resident"] = resident_variants(local, cfg, B, P, args.arch)
@@ -1188,17 +1306,84 @@ def config2_resident(local, B=64, P=512, steps=3, warmup=2):
             "act_context_tokens": act, "launches_per_step": acc["launches"] / steps}
 
 
+def full_generation(args, cfg, local):
+    """The whole generation, timed: real prefill of B prompts of P tokens, then
+    G decode steps, every step timed with CUDA events (the paper's and the
+    sim's end-to-end definition, sim.cpp:618-628)."""
+    from paper_2501_01792_b200 import api, kernels
+    if kernels.device_count() == 0:
+        raise SystemExit("bench needs a CUDA device")
+    hbm_peak, tflops_sust, _, _ = measured_peaks()
+    bind_numa(local)
+    B, P, G, L = args.batch or 128, args.prompt, args.gen, cfg.num_layers
+    bp = bundle_path(args)
+    if args.ratio >= 0:
+        r, src = args.ratio, "--ratio"
+    else:
+        r, factor, _ = planned_ratio(read_bundle(bp), cfg, B * (P + G),
+                                     lambda b5, m4, tpb, ag: list(api.plan_host_allocation(
+                                         api.TimingBundle(api.LinearTimeModel(b5[0], b5[1]),
+                                                          api.LinearTimeModel(b5[2], b5[3]), b5[4]),
+                                         api.MemoryBudget(*m4), tpb, ag).__dict__.values()))
+        src = f"planner on {os.path.relpath(bp, ROOT)}"
+    mode, alloc, caps = pool_plan(cfg, B, P + G + 1, 0, r)
+    w_layer, _ = api.weight_bytes(cfg)
+    budget = args.host_gb * 1e9 if args.host_gb > 0 else max(16e9, mem_available_bytes() - 40e9)
+    Lw = L if L * w_layer <= 0.55 * budget else max(2, int(0.55 * budget // w_layer))
+    Lp = host_layers_for(cfg, caps, budget, Lw * w_layer)
+    eng = api.Engine(cfg, seed=42, max_seq=P + G + 2, rescale=True, max_batch=B, weights_on_device=False, caps=caps,
+                     host_layers=Lp, weight_layers=Lw, mode=mode, allocation=alloc, device=local, arch=args.arch)
+    ids = [f"f{i}" for i in range(B)]
+    rng = np.random.default_rng(100)
+    prompts = [rng.integers(0, cfg.vocab_size, P).tolist() for _ in ids]
+    import torch
+    torch.cuda.synchronize()
+    eng.set_profile(True)
+    w0 = time.perf_counter()
+    eng.prefill(ids, [p[:-1] for p in prompts])  # the last prompt token is the first decode step's input
+    eng.set_profile(False)
+    prefill_s = eng.last_stats()["step_ms"] / 1e3
+    out = {"argmax": np.zeros(B, np.int32)}
+    toks = [p[-1] for p in prompts]
+    step_ms = []
+    clocks = ClockSampler(local)
+    clocks.start()
+    for g in range(G):
+        eng.decode_step(ids, toks, want_x=False, want_argmax=True, out=out)
+        step_ms.append(eng.last_stats()["step_ms"])
+        toks = out["argmax"].tolist()
+    wall = time.perf_counter() - w0
+    clk = clocks.stop()
+    eng.close()
+    dec_s = sum(step_ms) / 1e3
+    print(json.dumps({
+        "metric": METRIC + " [whole generation: prefill + G greedy decode steps, every step timed]",
+        "value": B * G / (prefill_s + dec_s), "unit": "tokens/s", "n_gpus": 1, "dtype": "f16",
+        "config": {"workload": f"{cfg.name}, batch {B}, prompt {P}, gen {G}, weights + cache in pinned host",
+                   "act_share_r": r, "ratio_source": src, "mode": mode, "host_layers_phys": Lp,
+                   "weight_layers_phys": Lw},
+        "prefill_s": prefill_s, "decode_s": dec_s, "decode_tokens_per_s": B * G / dec_s,
+        "wall_s": wall, "e2e_tokens_per_s": B * G / wall,
+        "step_ms": {"first": step_ms[0], "mid": step_ms[len(step_ms) // 2], "last": step_ms[-1],
+                    "mean": statistics.mean(step_ms), "all": [round(x, 3) for x in step_ms]},
+        "clocks": clk}), flush=True)
+
+
 def main():
     args = parse()
     world, rank, local, dist = dist_setup(args)
-    from paper_2501_01792_b200 import api
-    cfg = api.ModelConfig.preset(args.model)
-    if args.layers:
-        cfg.num_layers = args.layers
-    if args.impl == "reference":
-        reference_arm(args, cfg, world, rank, dist)
+    if args.impl == "reference":  # the reference's CPU path: the product is never imported
+        reference_arm(args, world, rank, dist)
     else:
-        our_arm(args, cfg, world, rank, local, dist)
+        from paper_2501_01792_b200 import api
+        cfg = api.ModelConfig.preset(args.model)
+        if args.layers:
+            cfg.num_layers = args.layers
+        if args.full_generation:
+            if rank == 0:
+                full_generation(args, cfg, local)
+        else:
+            our_arm(args, cfg, world, rank, local, dist)
     if dist is not None:
         dist.destroy_process_group()
 

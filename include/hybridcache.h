@@ -190,6 +190,11 @@ int hc_engine_destroy(void* engine);
 int hc_engine_prefill(void* engine, int n, const char* const* ids, const int* offsets, const int* tokens);
 /* Bookkeeping-only admission + pattern-filled pools (benchmark setup). */
 int hc_engine_admit_synthetic(void* engine, int n, const char* const* ids, const int* prompt_lens, uint64_t seed);
+/* Pattern-fill every pool slot (benchmark setup, before a real prefill). */
+int hc_engine_fill_pools(void* engine, uint64_t seed);
+/* Grow each request by n_tokens through the allocator in decode order
+ * (sim.cpp:308-310), bookkeeping only (benchmark: timed steps at a later context). */
+int hc_engine_advance_synthetic(void* engine, int n, const char* const* ids, int n_tokens);
 /* One decode step; x_out [n x d] f16, logits [n x V] fp32, argmax [n]; any may be NULL. */
 int hc_engine_decode_step(void* engine, int n, const char* const* ids, const int* tokens, uint16_t* x_out,
                           float* logits, int* argmax);

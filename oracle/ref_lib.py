@@ -77,6 +77,8 @@ def lib():
         L.ref_alloc_remaining.argtypes = [_dp, _dp, C.c_int, C.c_long, C.c_long, _lp]
         L.ref_plan_host_allocation.argtypes = [_dp, _dp, C.c_int, C.c_long, _lp]
         L.ref_fit_linear.argtypes = [_dp, _dp, C.c_int, _dp]
+        L.ref_model_preset.argtypes = [C.c_char_p, _ip]
+        L.ref_parse_artifacts.argtypes = [C.c_char_p, C.c_char_p, _dp, _lp]
         _lib = L
     return _lib
 
@@ -98,6 +100,24 @@ def dptr(a: np.ndarray):
 
 def iptr(a: np.ndarray):
     return a.ctypes.data_as(_ip)
+
+
+def model_preset(name: str):
+    """ModelConfig::preset (model.cpp:37-43) -> (layers, d, heads, ffn, vocab, tpb)."""
+    out = (C.c_int * 6)()
+    _check(lib().ref_model_preset(name.encode(), out))
+    return tuple(out)
+
+
+def parse_bundle(path: str):
+    """TimingBundle::from_json (timing.cpp:155-163) of a bundle.json ->
+    (kv slope, kv intercept, load slope, load intercept, t_load_w, s_weight_layer, s_weight_total)."""
+    out = np.zeros(7)
+    alloc = (C.c_long * 6)()
+    with open(path) as fh:
+        text = fh.read().encode()
+    _check(lib().ref_parse_artifacts(text, None, dptr(out), alloc))
+    return tuple(out)
 
 
 class RefWeights:

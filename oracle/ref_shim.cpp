@@ -98,6 +98,19 @@ extern "C" {
 const char* ref_last_error() { return g_err.c_str(); }
 
 // ---- model + weights ------------------------------------------------------
+// ModelConfig::preset (model.cpp:37-43): out6 = {layers, d, heads, ffn, vocab, tpb}
+int ref_model_preset(const char* name, int* out6) {
+    return guarded([&] {
+        const ModelConfig c = ModelConfig::preset(name);
+        out6[0] = c.num_layers;
+        out6[1] = c.hidden_dim;
+        out6[2] = c.num_heads;
+        out6[3] = c.ffn_dim;
+        out6[4] = c.vocab_size;
+        out6[5] = c.tokens_per_block;
+    });
+}
+
 int ref_weights_new(int layers, int d, int heads, int ffn, int vocab, int tpb, uint64_t seed,
                     int max_seq, void** out) {
     return guarded([&] {

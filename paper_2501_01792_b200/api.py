@@ -81,7 +81,7 @@ class ModelConfig:
 
 
 def generate_weights(cfg: ModelConfig, seed: int, max_seq: int, rescale: bool = True) -> Dict[str, np.ndarray]:
-    """DecoderWeights::generate (+ rescale, bf16) in device layout (bf16 bits):
+    """DecoderWeights::generate (+ rescale, fp16) in device layout (fp16 bits):
     embedding [V,d], positional [S,d], layers [L, layer_elems] packed as
     Wqkv^T [3d,d] | Wproj^T [d,d] | W1^T [f,d] | W2^T [d,f]."""
     cfg = ModelConfig(**cfg.__dict__).validate()
@@ -617,6 +617,8 @@ class Engine:
         self.close()
 
     def prefill(self, ids: Sequence[str], prompts: Sequence[Sequence[int]]) -> None:
+        if len(ids) != len(prompts):
+            raise InputError("prefill: ids and prompts differ in length")
         offs = np.zeros(len(ids) + 1, np.int32)
         offs[1:] = np.cumsum([len(p) for p in prompts])
         toks = np.ascontiguousarray(np.concatenate([np.asarray(p, np.int32) for p in prompts])
@@ -627,17 +629,34 @@ class Engine:
         lens = np.ascontiguousarray(prompt_lens, np.int32)
         check(lib().hc_engine_admit_synthetic(self._h, len(ids), _ids(ids), ptr(lens, C.c_int), seed))
 
+    def fill_pools(self, seed: int = 1) -> None:
+        """Pattern-fill every pool slot (benchmark setup, before a real prefill)."""
+        check(lib().hc_engine_fill_pools(self._h, seed))
+
+    def advance_synthetic(self, ids: Sequence[str], n_tokens: int) -> None:
+        """Grow each request by n_tokens in decode order, bookkeeping only."""
+        check(lib().hc_engine_advance_synthetic(self._h, len(ids), _ids(ids), n_tokens))
+
     def decode_step(self, ids: Sequence[str], tokens: Sequence[int], *, want_x: bool = True,
                     want_logits: bool = False, want_argmax: bool = False, out: Optional[dict] = None) -> dict:
         n = len(ids)
         toks = np.ascontiguousarray(tokens, np.int32)
+        if toks.shape != (n,):
+            raise InputError(f"decode_step: {toks.size} tokens for {n} requests")
         res = out if out is not None else {}
-        if want_x and "x" not in res:
-            res["x"] = np.zeros((n, self.cfg.hidden_dim), np.uint16)
-        if want_logits and "logits" not in res:
-            res["logits"] = np.zeros((n, self.cfg.vocab_size), np.float32)
-        if want_argmax and "argmax" not in res:
-            res["argmax"] = np.zeros(n, np.int32)
+
+        def buf(key, shape, dtype):  # reuse the caller's array only when it fits exactly
+            a = res.get(key)
+            if not (isinstance(a, np.ndarray) and a.shape == shape and a.dtype == dtype and a.flags.c_contiguous
+                    and a.flags.writeable):
+                res[key] = np.zeros(shape, dtype)
+
+        if want_x:
+            buf("x", (n, self.cfg.hidden_dim), np.uint16)
+        if want_logits:
+            buf("logits", (n, self.cfg.vocab_size), np.float32)
+        if want_argmax:
+            buf("argmax", (n,), np.int32)
         check(lib().hc_engine_decode_step(
             self._h, n, _ids(ids), ptr(toks, C.c_int),
             ptr(res["x"], C.c_uint16) if want_x else None,
@@ -661,7 +680,7 @@ class Engine:
 
     def forward_trace(self, ids: Sequence[int]) -> dict:
         """GPU forward_prompt (decoder.cpp:144-157): layer inputs, K, V per layer
-        and the output, as bf16 bits."""
+        and the output, as fp16 bits."""
         n, L, d = len(ids), self.cfg.num_layers, self.cfg.hidden_dim
         t = np.ascontiguousarray(ids, np.int32)
         res = {k: np.zeros((L, n, d), np.uint16) for k in ("layer_inputs", "k", "v")}
@@ -672,7 +691,7 @@ class Engine:
         return res
 
     def layer_forward(self, layer: int, x_bits: np.ndarray) -> dict:
-        """One layer of forward_prompt on given bf16 input rows (teacher forcing)."""
+        """One layer of forward_prompt on given fp16 input rows (teacher forcing)."""
         x = np.ascontiguousarray(x_bits, np.uint16)
         n, d = x.shape
         res = {k: np.zeros((n, d), np.uint16) for k in ("k", "v", "output")}
@@ -697,7 +716,7 @@ class Engine:
         return out
 
     def read_weights(self, layer: int) -> np.ndarray:
-        """Engine-held bf16 weights: packed layer (layer >= 0), -1 embedding, -2 positional."""
+        """Engine-held fp16 weights: packed layer (layer >= 0), -1 embedding, -2 positional."""
         d, f = self.cfg.hidden_dim, self.cfg.ffn_dim
         if layer == -1:
             out = np.zeros((self.cfg.vocab_size, d), np.uint16)

@@ -432,6 +432,10 @@ int hc_engine_destroy(void* e) {
 }
 int hc_engine_prefill(void* e, int n, const char* const* ids, const int* offsets, const int* tokens) {
     return hc_guard([&] {
+        if (n < 0) throw InputError("prefill: negative request count");
+        if (n > 0 && (!ids || !offsets || (!tokens && offsets[n] > 0)))
+            throw InputError("prefill: null ids / offsets / tokens");
+        if (n > 0 && offsets[0] < 0) throw InputError("prefill: offsets[0] must be >= 0");
         std::vector<std::vector<int>> prompts(static_cast<size_t>(n));
         for (int r = 0; r < n; ++r) {
             if (offsets[r + 1] < offsets[r]) throw InputError("prefill: offsets must be non-decreasing");
@@ -443,9 +447,21 @@ int hc_engine_prefill(void* e, int n, const char* const* ids, const int* offsets
 int hc_engine_admit_synthetic(void* e, int n, const char* const* ids, const int* lens, uint64_t seed) {
     return hc_guard([&] { eng(e)->admit_synthetic(ids_of(n, ids), std::vector<int>(lens, lens + n), seed); });
 }
+
+int hc_engine_fill_pools(void* e, uint64_t seed) {
+    return hc_guard([&] { eng(e)->fill_pools(seed); });
+}
+
+int hc_engine_advance_synthetic(void* e, int n, const char* const* ids, int n_tokens) {
+    return hc_guard([&] { eng(e)->advance_synthetic(ids_of(n, ids), n_tokens); });
+}
 int hc_engine_decode_step(void* e, int n, const char* const* ids, const int* tokens, uint16_t* x_out, float* logits,
                           int* argmax) {
-    return hc_guard([&] { eng(e)->decode_step(ids_of(n, ids), tokens, x_out, logits, argmax); });
+    return hc_guard([&] {
+        if (n < 0) throw InputError("decode_step: negative request count");
+        if (n > 0 && (!ids || !tokens)) throw InputError("decode_step: null ids / tokens");
+        eng(e)->decode_step(ids_of(n, ids), tokens, x_out, logits, argmax);
+    });
 }
 int hc_engine_configure_cache(void* e, long kv_host, long kv_gpu, long act_host, long act_gpu, int kv_on_gpu, int mode,
                               long alloc_act_host, long alloc_kv_host, int host_layers, double recompute_ratio) {

@@ -1008,7 +1008,13 @@ void Engine::admit_synthetic(const std::vector<std::string>& ids, const std::vec
         }
         for (int t = rc; t < prompt_lens[r]; ++t) assigner_->add_token(ids[r]);
     }
-    if (m.pools_filled) return;
+    if (!m.pools_filled) fill_pools(seed);
+}
+
+void Engine::fill_pools(uint64_t seed) {
+    HC_CUDA(cudaSetDevice(opt_.device));
+    Impl& m = *impl_;
+    m.require_configured();
     // activations ~U(-0.1,0.1) like the embeddings; K,V of matching scale
     auto fill = [&](f16* p, size_t n, uint64_t s) {
         if (p && n) fill_pattern(p, n, s, 0.1f, s_compute_);
@@ -1020,6 +1026,19 @@ void Engine::admit_synthetic(const std::vector<std::string>& ids, const std::vec
     HC_CUDA(cudaGetLastError());
     HC_CUDA(cudaStreamSynchronize(s_compute_));
     m.pools_filled = true;
+}
+
+void Engine::advance_synthetic(const std::vector<std::string>& ids, int n_tokens) {
+    Impl& m = *impl_;
+    m.require_configured();
+    if (n_tokens < 0) throw InputError("advance_synthetic: negative token count");
+    for (const std::string& id : ids)
+        if (cache_->table(id).context_len() + recompute_prefix_len(id) + n_tokens > m.max_seq)
+            throw InputError("embed: sequence longer than max_seq");
+    // decode order: one token per request per iteration (sim.cpp:308-310), so
+    // the block tables are the ones n_tokens real decode steps would leave
+    for (int t = 0; t < n_tokens; ++t)
+        for (const std::string& id : ids) assigner_->add_token(id);
 }
 
 void Engine::free_request(const std::string& id) {
@@ -1563,11 +1582,13 @@ double Engine::time_kv_gen(int n_tokens, int reps) {
     HC_CUDA(cudaSetDevice(opt_.device));  // the calling thread may be on another device
     Impl& m = *impl_;
     if (n_tokens <= 0) throw InputError("time_kv_gen: n_tokens must be positive");
+    if (reps <= 0) throw InputError("time_kv_gen: reps must be positive");
     // recompute GEMM over n tokens of the ACT staging (or GPU) pool, layer 0
     const long stage_rows = static_cast<long>(m.tpn) * m.act_cap_n * m.tpb;
     const long cap_rows = std::max(stage_rows, m.act_gpu_cap * m.tpb);
     if (n_tokens > cap_rows) throw InputError("time_kv_gen: more tokens than the ACT pools hold");
-    const f16* A = stage_rows >= n_tokens ? m.act_stage[0] : m.act_gpu;
+    const bool from_stage = stage_rows >= n_tokens;
+    const f16* A = from_stage ? m.act_stage[0] : m.act_gpu;
     m.w_prefetched = false;  // wbuf[0] is reloaded with layer 0 below
     if (!m.w_all)
         HC_CUDA(cudaMemcpy(m.wbuf[0], m.h_w, m.LE * 2, cudaMemcpyHostToDevice));
@@ -1581,7 +1602,9 @@ double Engine::time_kv_gen(int n_tokens, int reps) {
     c.epi = gemm::kKvPaged;
     c.A = A;
     c.lda = m.d;
-    c.a_rows = static_cast<int>(cap_rows);
+    // the TMA map may not reach past the pool A points into (the last tile
+    // of a non-multiple-of-128 n reads up to 127 rows further)
+    c.a_rows = static_cast<int>(from_stage ? stage_rows : m.act_gpu_cap * m.tpb);
     c.B = W + m.off.wqkv + static_cast<size_t>(m.dg) * m.d;
     c.ldb = m.d;
     c.M = n_tokens;
@@ -1609,6 +1632,7 @@ double Engine::time_load_bytes(size_t bytes, int reps) {
     Impl& m = *impl_;
     const size_t cap = static_cast<size_t>(m.kv_host_cap) * m.kvb * 2;
     if (bytes == 0 || bytes > cap) throw InputError("time_load: byte count exceeds the KV host pool");
+    if (reps <= 0) throw InputError("time_load: reps must be positive");
     HC_CUDA(cudaMemcpyAsync(m.kv_stage[0], m.kv_host, bytes, cudaMemcpyHostToDevice, s_copy_));
     HC_CUDA(cudaEventRecord(m.ev0, s_copy_));
     for (int i = 0; i < reps; ++i)

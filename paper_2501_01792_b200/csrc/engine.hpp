@@ -95,6 +95,13 @@ public:
     // Admit requests with prompt_len tokens of bookkeeping only and fill their
     // blocks with a deterministic pattern (benchmark setup; no numerics).
     void admit_synthetic(const std::vector<std::string>& ids, const std::vector<int>& prompt_lens, uint64_t seed);
+    // Fill every pool slot with the deterministic pattern (benchmark setup:
+    // slots that advance_synthetic later hands out then hold finite values).
+    void fill_pools(uint64_t seed);
+    // Grow each listed request by n_tokens through the allocator in decode
+    // order (bookkeeping only; the slots keep the pool contents): places a
+    // benchmark's timed steps at a later context without running the steps.
+    void advance_synthetic(const std::vector<std::string>& ids, int n_tokens);
 
     // One decode step for the listed requests (generation_step semantics,
     // decoder.cpp:159-174, batched). Outputs are optional (nullptr = skip):
