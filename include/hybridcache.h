@@ -190,6 +190,12 @@ int hc_engine_destroy(void* engine);
 int hc_engine_prefill(void* engine, int n, const char* const* ids, const int* offsets, const int* tokens);
 /* Bookkeeping-only admission + pattern-filled pools (benchmark setup). */
 int hc_engine_admit_synthetic(void* engine, int n, const char* const* ids, const int* prompt_lens, uint64_t seed);
+/* Mini-batched decode (paper §4.3.3; sim.cpp:258-358; minibatch.cpp:36-83):
+ * staging slots of act_max ACT / kv_max KV blocks; each step is packed by
+ * form_minibatches on pre-growth block counts, priced by bundle5 = {kv_gen
+ * slope, intercept, load_kv slope, intercept, t_load_w}, and run as (layer,
+ * mini-batch) units. act_max = kv_max = 0: whole-batch steps. */
+int hc_engine_set_minibatching(void* engine, long act_max, long kv_max, const double* bundle5);
 /* Pattern-fill every pool slot (benchmark setup, before a real prefill). */
 int hc_engine_fill_pools(void* engine, uint64_t seed);
 /* Grow each request by n_tokens through the allocator in decode order
@@ -222,10 +228,10 @@ int hc_engine_read_weights(void* engine, int layer, uint16_t* out);  /* -3: fina
 int hc_engine_capture_inputs(void* engine, int on);
 /* Decode-time layer inputs of the last step, [L][n][d] f16 (n = last batch). */
 int hc_engine_captured_inputs(void* engine, uint16_t* out, long count);
-/* out11 = {step_ms, h2d_bytes, d2h_bytes, recompute_rows, recompute_ms, attn_ms, gemm_ms, launches,
- *          copy_ms, recompute_launches, store_ms} of the last decode step or prefill; the *_ms
- *          splits need hc_engine_set_profile(1). */
-int hc_engine_last_stats(void* engine, double* out11);
+/* out12 = {step_ms, h2d_bytes, d2h_bytes, recompute_rows, recompute_ms, attn_ms, gemm_ms, launches,
+ *          copy_ms, recompute_launches, store_ms, minibatches} of the last decode step or prefill;
+ *          the *_ms splits need hc_engine_set_profile(1). */
+int hc_engine_last_stats(void* engine, double* out12);
 /* Per-kernel CUDA-event timing of the next steps (small overhead). */
 int hc_engine_set_profile(void* engine, int on);
 /* Replay decode steps as CUDA graphs keyed by their launch structure (default on,

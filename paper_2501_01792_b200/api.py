@@ -629,6 +629,14 @@ class Engine:
         lens = np.ascontiguousarray(prompt_lens, np.int32)
         check(lib().hc_engine_admit_synthetic(self._h, len(ids), _ids(ids), ptr(lens, C.c_int), seed))
 
+    def set_minibatching(self, act_max: int, kv_max: int, bundle: Optional["TimingBundle"] = None) -> None:
+        """Mini-batched decode (paper §4.3.3; sim.cpp:258-358): staging slots of
+        act_max ACT / kv_max KV blocks, each step packed by form_minibatches
+        (minibatch.cpp:36-83) on pre-growth block counts priced by `bundle`.
+        act_max = kv_max = 0 returns to whole-batch steps."""
+        b, bp = (bundle.arr5() if bundle is not None else _darr(np.zeros(5)))
+        check(lib().hc_engine_set_minibatching(self._h, act_max, kv_max, bp))
+
     def fill_pools(self, seed: int = 1) -> None:
         """Pattern-fill every pool slot (benchmark setup, before a real prefill)."""
         check(lib().hc_engine_fill_pools(self._h, seed))
@@ -740,10 +748,10 @@ class Engine:
         return out
 
     def last_stats(self) -> dict:
-        out, op = _darr(np.zeros(11))
+        out, op = _darr(np.zeros(12))
         check(lib().hc_engine_last_stats(self._h, op))
         keys = ("step_ms", "h2d_bytes", "d2h_bytes", "recompute_rows", "recompute_ms", "attn_ms", "gemm_ms",
-                "launches", "copy_ms", "recompute_launches", "store_ms")
+                "launches", "copy_ms", "recompute_launches", "store_ms", "minibatches")
         return dict(zip(keys, out.tolist()))
 
     def set_profile(self, on: bool = True) -> None:

@@ -448,6 +448,14 @@ int hc_engine_admit_synthetic(void* e, int n, const char* const* ids, const int*
     return hc_guard([&] { eng(e)->admit_synthetic(ids_of(n, ids), std::vector<int>(lens, lens + n), seed); });
 }
 
+int hc_engine_set_minibatching(void* e, long act_max, long kv_max, const double* bundle5) {
+    return hc_guard([&] {
+        TimingBundle b{};
+        if (bundle5) b = bundle_of(bundle5);
+        eng(e)->set_minibatching(act_max, kv_max, b);
+    });
+}
+
 int hc_engine_fill_pools(void* e, uint64_t seed) {
     return hc_guard([&] { eng(e)->fill_pools(seed); });
 }
@@ -507,9 +515,10 @@ int hc_engine_captured_inputs(void* e, uint16_t* out, long count) {
 int hc_engine_last_stats(void* e, double* o) {
     return hc_guard([&] {
         const StepStats& s = eng(e)->last_stats();
-        const double v[11] = {s.step_ms, s.h2d_bytes, s.d2h_bytes, s.recompute_tokens, s.recompute_ms,
+        const double v[12] = {s.step_ms, s.h2d_bytes, s.d2h_bytes, s.recompute_tokens, s.recompute_ms,
                               s.attn_ms, s.gemm_ms, static_cast<double>(s.launches), s.copy_ms,
-                              static_cast<double>(s.recompute_launches), s.store_ms};
+                              static_cast<double>(s.recompute_launches), s.store_ms,
+                              static_cast<double>(s.minibatches)};
         std::memcpy(o, v, sizeof v);
     });
 }

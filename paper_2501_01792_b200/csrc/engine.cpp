@@ -29,6 +29,7 @@ enum Region : int {
 
 struct Run {
     int start, count;
+    int dst = 0;  // staging position of `start` (decode steps)
 };
 
 std::vector<Run> runs_of(std::vector<int> pbns) {
@@ -39,7 +40,7 @@ std::vector<Run> runs_of(std::vector<int> pbns) {
         if (!r.empty() && r.back().start + r.back().count == p)
             ++r.back().count;
         else
-            r.push_back({p, 1});
+            r.push_back({p, 1, 0});
     }
     return r;
 }
@@ -130,6 +131,27 @@ struct Engine::Impl {
     int wsn = 1, wsr = 0;
     size_t wsS = 0;
     cudaEvent_t w_h2d[2]{}, w_gath[2]{};
+    cudaEvent_t w_consumed[2]{};  // wbuf[slot] released: the last unit of the layer that used it ended
+    // mini-batched decode (set_minibatching): staging slots sized by the
+    // packer's capacities instead of the whole host pools
+    bool mb_on = false;
+    PackerConfig packer{};
+    TimingBundle packer_bundle{};
+    long stage_kv_cap = 0, stage_act_cap = 0;  // blocks one staging slot holds
+    float* agree_buf = nullptr;                // shared-weight-stream error agreement (1 float)
+    // ranks sharing a weight stream agree on a step's validation outcome
+    // before its first collective (an all-reduce of a failure flag)
+    void agree_or_throw(const std::string& local_error, cudaStream_t st) {
+        if (!agree_buf) agree_buf = dalloc<float>(1);
+        const float flag = local_error.empty() ? 0.f : 1.f;
+        HC_CUDA(cudaMemcpyAsync(agree_buf, &flag, 4, cudaMemcpyHostToDevice, st));
+        ws->all_reduce_sum(agree_buf, 1, st);
+        float sum = 0.f;
+        HC_CUDA(cudaMemcpyAsync(&sum, agree_buf, 4, cudaMemcpyDeviceToHost, st));
+        HC_CUDA(cudaStreamSynchronize(st));
+        if (!local_error.empty()) throw InputError(local_error);
+        if (sum > 0.f) throw InputError("decode_step: a rank sharing the weight stream rejected the step");
+    }
     bool pools_filled = false;
     bool configured = false;  // false while (or after a failed) configure_cache: pools may be missing
     void require_configured() const {
@@ -176,12 +198,13 @@ struct Engine::Impl {
         int kind;  // 0 recompute, 1 attention, 2 other gemm, 3 copy
         cudaEvent_t a, b;
         int layer;
+        int minibatch;
     };
     std::vector<Span> spans;
-    int cur_layer = -1;
+    int cur_layer = -1, cur_mb = 0;
     void span_begin(bool on, cudaStream_t s, int kind) {
         if (!on) return;
-        spans.push_back({kind, take_event(), nullptr, cur_layer});
+        spans.push_back({kind, take_event(), nullptr, cur_layer, cur_mb});
         HC_CUDA(cudaEventRecord(spans.back().a, s));
     }
     void span_end(bool on, cudaStream_t s) {
@@ -477,6 +500,7 @@ void Engine::init(const ModelConfig& c, int w_max_seq, const uint16_t* emb, cons
         HC_CUDA(cudaEventCreateWithFlags(&m.gathered[i], cudaEventDisableTiming));
         HC_CUDA(cudaEventCreateWithFlags(&m.w_h2d[i], cudaEventDisableTiming));
         HC_CUDA(cudaEventCreateWithFlags(&m.w_gath[i], cudaEventDisableTiming));
+        HC_CUDA(cudaEventCreateWithFlags(&m.w_consumed[i], cudaEventDisableTiming));
     }
     HC_CUDA(cudaEventCreate(&m.ev0));
     HC_CUDA(cudaEventCreate(&m.ev1));
@@ -612,19 +636,56 @@ void Engine::configure_cache(const PoolCaps& caps, bool kv_on_gpu, CacheMode mod
         m.kv_host = kv_e ? m.h_arena : nullptr;
         m.act_host = act_e ? m.h_arena + kv_e_al : nullptr;
     }
-    for (int s = 0; s < 2; ++s) {
-        m.kv_stage[s] = dalloc<f16>(static_cast<size_t>(m.kv_host_cap) * m.kvb);
-        m.act_stage[s] = dalloc<f16>(static_cast<size_t>(m.tpn) * m.act_cap_n * m.actb);
+    alloc_staging();
+    m.pools_filled = false;
+    HC_CUDA(cudaDeviceSynchronize());
+    m.configured = true;
+}
+
+// Staging slots (two, double-buffered) for the host blocks of one decode unit
+// and the recompute output: the whole host pools for whole-batch steps (the
+// slot mirrors the pool's pbn layout), the packer's capacities plus one
+// growth block per request for mini-batched steps.
+void Engine::alloc_staging() {
+    Impl& m = *impl_;
+    for (f16** p : {&m.kvr, &m.kv_stage[0], &m.kv_stage[1], &m.act_stage[0], &m.act_stage[1]}) {
+        if (*p) cudaFree(*p);
+        *p = nullptr;
     }
-    m.kvr = dalloc<f16>(static_cast<size_t>(m.act_gpu_cap + m.tpn * m.act_cap_n) * m.kvb);
+    m.stage_kv_cap = m.kv_host_cap;
+    m.stage_act_cap = static_cast<long>(m.tpn) * m.act_cap_n;
+    if (m.mb_on) {
+        m.stage_kv_cap = std::min(m.stage_kv_cap, m.packer.kv_max + m.B);
+        m.stage_act_cap = std::min(m.stage_act_cap, m.packer.act_max + m.B);
+    }
+    for (int s = 0; s < 2; ++s) {
+        m.kv_stage[s] = dalloc<f16>(static_cast<size_t>(m.stage_kv_cap) * m.kvb);
+        m.act_stage[s] = dalloc<f16>(static_cast<size_t>(m.stage_act_cap) * m.actb);
+    }
+    m.kvr = dalloc<f16>(static_cast<size_t>(m.act_gpu_cap + m.stage_act_cap) * m.kvb);
     // staging slots start zeroed: whole-chunk copies (D2H runs, TP all-gathers)
     // never move uninitialised bytes, even for slots no block occupies yet
     for (int s = 0; s < 2; ++s) {
-        if (m.kv_stage[s]) HC_CUDA(cudaMemset(m.kv_stage[s], 0, static_cast<size_t>(m.kv_host_cap) * m.kvb * 2));
-        if (m.act_stage[s])
-            HC_CUDA(cudaMemset(m.act_stage[s], 0, static_cast<size_t>(m.tpn) * m.act_cap_n * m.actb * 2));
+        if (m.kv_stage[s]) HC_CUDA(cudaMemset(m.kv_stage[s], 0, static_cast<size_t>(m.stage_kv_cap) * m.kvb * 2));
+        if (m.act_stage[s]) HC_CUDA(cudaMemset(m.act_stage[s], 0, static_cast<size_t>(m.stage_act_cap) * m.actb * 2));
     }
-    m.pools_filled = false;
+}
+
+void Engine::set_minibatching(long act_max, long kv_max, const TimingBundle& bundle) {
+    HC_CUDA(cudaSetDevice(opt_.device));
+    Impl& m = *impl_;
+    m.require_configured();
+    const bool on = act_max > 0 || kv_max > 0;
+    if (on && (act_max < 1 || kv_max < 1)) throw InputError("form_minibatches: capacities must be >= 1");
+    if (on && (m.tpn > 1 || m.wsn > 1))
+        throw ConfigError("Engine: mini-batched decode runs without tensor parallelism or a shared weight stream");
+    HC_CUDA(cudaDeviceSynchronize());
+    m.clear_graphs();
+    m.mb_on = on;
+    m.packer = PackerConfig{act_max, kv_max};
+    m.packer_bundle = bundle;
+    m.configured = false;
+    alloc_staging();
     HC_CUDA(cudaDeviceSynchronize());
     m.configured = true;
 }
@@ -675,7 +736,8 @@ Engine::~Engine() {
                     (void*)m.act_stage[1], (void*)m.x[0], (void*)m.x[1], (void*)m.qkvb, (void*)m.att, (void*)m.proj,
                     (void*)m.hbuf, (void*)m.logits, (void*)m.amax, (void*)m.attn_work, (void*)m.d_meta,
                     (void*)m.px[0], (void*)m.px[1], (void*)m.pqkv, (void*)m.patt, (void*)m.pproj, (void*)m.ph,
-                    (void*)m.tr_kv, (void*)m.splitk_ws, (void*)m.lnf, (void*)m.xn, (void*)m.pxn, (void*)m.red})
+                    (void*)m.tr_kv, (void*)m.splitk_ws, (void*)m.lnf, (void*)m.xn, (void*)m.pxn, (void*)m.red,
+                    (void*)m.agree_buf})
         if (p) cudaFree(p);
     for (auto& g : m.graphs) cudaGraphExecDestroy(g.second.exec);
     for (void* p : {(void*)m.h_w, (void*)m.h_arena, (void*)m.h_meta, (void*)m.h_x,
@@ -684,6 +746,7 @@ Engine::~Engine() {
     for (int i = 0; i < 2; ++i) {
         cudaEventDestroy(m.loaded[i]);
         cudaEventDestroy(m.consumed[i]);
+        cudaEventDestroy(m.w_consumed[i]);
         cudaEventDestroy(m.stored[i]);
         cudaEventDestroy(m.h2d_act[i]);
         cudaEventDestroy(m.gathered[i]);
@@ -827,14 +890,19 @@ void Engine::prefill(const std::vector<std::string>& ids, const std::vector<std:
                 if (gpu || m.owns(e.pbn)) {  // a host ACT block is written by its owning rank only
                     a_src.push_back(row);
                     a_n.push_back(e.filled_tokens);
-                    a_ref.push_back(pack_ref(gpu ? R_ACT_GPU : R_ACT_STAGE, gpu ? e.pbn : m.act_pos(e.pbn)));
-                    if (!gpu) acth.push_back(e.pbn / m.tpn);
+                    if (gpu)
+                        a_ref.push_back(pack_ref(R_ACT_GPU, e.pbn));
+                    else if (m.mb_on)  // staging smaller than the pool: straight into the mapped pool
+                        a_ref.push_back(pack_ref(R_ACT_HOST, e.pbn / m.tpn));
+                    else
+                        a_ref.push_back(pack_ref(R_ACT_STAGE, m.act_pos(e.pbn)));
+                    if (!gpu && !m.mb_on) acth.push_back(e.pbn / m.tpn);
                 }
             } else {
                 c.k_src.push_back(row - c.row0);
                 c.k_n.push_back(e.filled_tokens);
-                c.k_ref.push_back(pack_ref(gpu ? R_KV_GPU : R_KV_STAGE, e.pbn));
-                if (!gpu) kvh.push_back(e.pbn);
+                c.k_ref.push_back(pack_ref(gpu ? R_KV_GPU : (m.mb_on ? R_KV_HOST : R_KV_STAGE), e.pbn));
+                if (!gpu && !m.mb_on) kvh.push_back(e.pbn);
             }
             row += e.filled_tokens;
         }
@@ -1058,32 +1126,79 @@ long Engine::recompute_prefix_len(const std::string& id) const {
 }
 
 // ---------------------------------------------------------------------------
-void Engine::decode_step(const std::vector<std::string>& ids, const int* tokens, uint16_t* x_out, float* logits_out,
-                         int* argmax_out) {
+void Engine::decode_step(const std::vector<std::string>& ids_in, const int* tokens_in, uint16_t* x_out,
+                         float* logits_out, int* argmax_out) {
     Impl& m = *impl_;
     HC_CUDA(cudaSetDevice(opt_.device));  // the calling thread may differ from the constructing one
     m.require_configured();
-    const int n = static_cast<int>(ids.size());
-    if (n == 0) return;
-    if (n > m.B) throw InputError("decode_step: batch larger than max_batch");
-    std::vector<int> pos(n);
-    {
+    const int n = static_cast<int>(ids_in.size());
+    // ranks sharing one weight stream run the same collective sequence every
+    // step, so validation failures are agreed on before the first all-gather
+    // and an empty batch still streams (and gathers) every layer
+    std::string local_error;
+    std::vector<int> pos_in(n);
+    try {
+        if (n > m.B) throw InputError("decode_step: batch larger than max_batch");
         std::unordered_set<std::string> seen;
         for (int b = 0; b < n; ++b) {
-            if (!seen.insert(ids[b]).second) throw InputError("decode_step: duplicate request id " + ids[b]);
-            if (tokens[b] < 0 || tokens[b] >= m.V)
-                throw InputError("embed: token id out of range: " + std::to_string(tokens[b]));
-            pos[b] = cache_->table(ids[b]).context_len() + static_cast<int>(recompute_prefix_len(ids[b]));
-            if (pos[b] >= m.max_seq) throw InputError("embed: position exceeds max_seq: " + std::to_string(pos[b]));
+            if (!seen.insert(ids_in[b]).second) throw InputError("decode_step: duplicate request id " + ids_in[b]);
+            if (tokens_in[b] < 0 || tokens_in[b] >= m.V)
+                throw InputError("embed: token id out of range: " + std::to_string(tokens_in[b]));
+            pos_in[b] = cache_->table(ids_in[b]).context_len() + static_cast<int>(recompute_prefix_len(ids_in[b]));
+            if (pos_in[b] >= m.max_seq)
+                throw InputError("embed: position exceeds max_seq: " + std::to_string(pos_in[b]));
         }
+        if (n) assigner_->check_batch_capacity(ids_in);  // all contexts grow, or none (no half-applied step)
+    } catch (const std::exception& e) {
+        if (m.wsn == 1) throw;
+        local_error = e.what();
     }
-    // grow every context by this step's token (sim.cpp:308-310)
-    std::vector<int> act_dev(n, -1), act_host(n, -1), kv_dev(n, -1), kv_host(n, -1), tok(n, 0), nblk(n), ctx(n);
-    std::vector<int> refs(static_cast<size_t>(n) * m.max_blocks, 0);
-    // acth_pos: staging positions of every ACT/host block (recompute tiles);
-    // acth_own: host-pool indices of the ones this rank streams (pbn % tpn == tpr)
-    std::vector<int> kvh_pbns, acth_pos, acth_own, actg_pbns;
-    bool any_act = false, any_kv = false;
+    if (m.wsn > 1) {
+        m.agree_or_throw(local_error, s_compute_);
+    } else if (n == 0) {
+        return;
+    }
+
+    // ---- mini-batches (paper §4.3.3; sim.cpp:258-275): requests packed by
+    // form_minibatches (minibatch.cpp:36-83) on their PRE-growth block counts
+    // into units whose blocks fit one staging slot; a step is then the
+    // (layer, mini-batch) units of sim.cpp:324-358, double-buffered
+    std::vector<int> order(n);
+    std::iota(order.begin(), order.end(), 0);
+    std::vector<int> mb_row{0};
+    if (m.mb_on && n > 0) {
+        std::vector<RequestBlocks> reqs;
+        std::unordered_map<std::string, int> idx;
+        for (int b = 0; b < n; ++b) {
+            const auto ak = cache_->table(ids_in[b]).blocks_by_kind();
+            reqs.push_back(RequestBlocks{ids_in[b], ak.first, ak.second});
+            idx[ids_in[b]] = b;
+        }
+        std::vector<MiniBatch> mbs;
+        try {
+            mbs = form_minibatches(reqs, m.packer, m.packer_bundle, m.tpb);
+        } catch (const InputError& e) {
+            throw CapacityError(std::string("decode_step: request too large for the staging buffers: ") + e.what());
+        }
+        order.clear();
+        for (const MiniBatch& mb : mbs) {
+            for (const std::string& id : mb.ids) order.push_back(idx.at(id));
+            mb_row.push_back(static_cast<int>(order.size()));
+        }
+    } else {
+        mb_row.push_back(n);
+    }
+    const int M = static_cast<int>(mb_row.size()) - 1;
+    const bool permuted = M > 1;
+    // rows of the step in mini-batch order
+    std::vector<std::string> ids(n);
+    std::vector<int> tokv(n), pos(n);
+    for (int i = 0; i < n; ++i) {
+        ids[i] = ids_in[order[i]];
+        tokv[i] = tokens_in[order[i]];
+        pos[i] = pos_in[order[i]];
+    }
+
     // token-recompute prefixes: rows of a batched causal forward rebuilt
     // through every layer each step (the FlexGen-style baseline, sim.cpp:196-206)
     std::vector<int> rc_tok, rc_pos, rc_cu(1, 0), tr_src, tr_n, tr_ref;
@@ -1110,51 +1225,106 @@ void Engine::decode_step(const std::vector<std::string>& ids, const int* tokens,
     }
     const int n_rc = rc_cu.back();
     if (n_rc) m.ensure_prefill(n_rc);
-    assigner_->check_batch_capacity(ids);  // all contexts grow, or none (no half-applied step)
-    for (int b = 0; b < n; ++b) {
-        const int rcb = (rc_cu[b + 1] - rc_cu[b]) / m.tpb;
-        const TokenSlot s = assigner_->add_token(ids[b]);
-        const BlockTableEntry& e = s.entry;
-        const bool gpu = e.location == Location::GpuMem;
-        tok[b] = s.token_index;
-        if (e.kind == BlockKind::ACT) {
-            any_act = true;
-            act_dev[b] = pack_ref(gpu ? R_ACT_GPU : R_ACT_STAGE, gpu ? e.pbn : m.act_pos(e.pbn));
-            if (!gpu && m.owns(e.pbn)) act_host[b] = pack_ref(R_ACT_HOST, e.pbn / m.tpn);
-        } else {
-            any_kv = true;
-            kv_dev[b] = pack_ref(gpu ? R_KV_GPU : R_KV_STAGE, e.pbn);
-            if (!gpu) kv_host[b] = pack_ref(R_KV_HOST, e.pbn);
+
+    // grow every context by this step's token, in mini-batch order (the
+    // reference's add_token order, sim.cpp:294-310)
+    std::vector<TokenSlot> grown;
+    grown.reserve(n);
+    for (int b = 0; b < n; ++b) grown.push_back(assigner_->add_token(ids[b]));
+
+    // per mini-batch: the host blocks it stages (staging position = the host
+    // pool's own pbn layout for a whole-batch step; packed in pbn order for a
+    // mini-batch, so pbn runs stay contiguous DMA runs), recompute tiles and
+    // copy runs
+    struct Unit {
+        std::vector<Run> kv_runs, act_runs;  // start = host index, dst = staging position
+        std::vector<int> tiles_h, tiles_g;
+        int splits = 1;
+        bool any_act = false, any_kv = false;
+        size_t o_th = 0, o_tg = 0;
+    };
+    std::vector<Unit> units(M);
+    std::vector<int> act_dev(n, -1), act_host(n, -1), kv_dev(n, -1), kv_host(n, -1), tok(n, 0), nblk(n), ctx(n);
+    std::vector<int> refs(static_cast<size_t>(n) * m.max_blocks, 0);
+    bool gather_act = false;
+    long stage_kv_need = 0, stage_act_need = 0;
+    for (int u = 0; u < M; ++u) {
+        Unit& U = units[u];
+        std::vector<int> kvh, acth, actg;
+        for (int b = mb_row[u]; b < mb_row[u + 1]; ++b)
+            for (const auto& en : cache_->table(ids[b]).entries) {
+                if (en.location == Location::GpuMem) {
+                    if (en.kind == BlockKind::ACT) actg.push_back(en.pbn);
+                } else {
+                    (en.kind == BlockKind::KV ? kvh : acth).push_back(en.pbn);
+                }
+            }
+        for (auto* v : {&kvh, &acth}) {
+            std::sort(v->begin(), v->end());
+            v->erase(std::unique(v->begin(), v->end()), v->end());
         }
-        const BlockTable& t = cache_->table(ids[b]);
-        nblk[b] = rcb + static_cast<int>(t.entries.size());
-        ctx[b] = rcb * m.tpb + t.context_len();
-        int* rb = refs.data() + static_cast<size_t>(b) * m.max_blocks;
-        for (int i = 0; i < rcb; ++i) *rb++ = pack_ref(R_TOKREC, b * m.max_blocks + i);
-        for (size_t i = 0; i < t.entries.size(); ++i) {
-            const auto& en = t.entries[i];
-            const bool g = en.location == Location::GpuMem;
-            if (en.kind == BlockKind::KV) {
-                rb[i] = pack_ref(g ? R_KV_GPU : R_KV_STAGE, en.pbn);
-                if (!g) kvh_pbns.push_back(en.pbn);
-            } else if (g) {
-                rb[i] = pack_ref(R_KVR, en.pbn);
-                actg_pbns.push_back(en.pbn);
+        std::unordered_map<int, int> kvp, actp;  // pbn -> staging position
+        for (size_t i = 0; i < kvh.size(); ++i) kvp[kvh[i]] = permuted ? static_cast<int>(i) : kvh[i];
+        std::vector<int> apos;
+        for (size_t i = 0; i < acth.size(); ++i) {
+            const int p = permuted ? static_cast<int>(i) : m.act_pos(acth[i]);
+            actp[acth[i]] = p;
+            apos.push_back(p);
+        }
+        stage_kv_need = std::max(stage_kv_need, kvh.empty() ? 0L : static_cast<long>(kvp[kvh.back()]) + 1);
+        stage_act_need = std::max(stage_act_need, static_cast<long>(acth.size()));
+        for (const Run& r : runs_of(kvh)) U.kv_runs.push_back({r.start, r.count, kvp[r.start]});
+        std::vector<int> own;  // host indices of the ACT blocks this rank streams
+        for (int p : acth)
+            if (m.owns(p)) own.push_back(p);
+        for (const Run& r : runs_of(own))  // (tpn > 1: own pbns are g, g+N, ...; host index pbn / N)
+            U.act_runs.push_back({r.start / m.tpn, r.count, actp[r.start]});
+        if (m.tpn > 1) {
+            U.act_runs.clear();
+            std::vector<int> hidx;
+            for (int p : own) hidx.push_back(p / m.tpn);
+            for (const Run& r : runs_of(hidx))
+                U.act_runs.push_back({r.start, r.count, static_cast<int>(m.tpr * m.act_cap_n) + r.start});
+            gather_act = !acth.empty();
+        }
+        U.tiles_h = tiles_of(apos, m.tpb);
+        U.tiles_g = tiles_of(actg, m.tpb);
+        int max_ctx = 0;
+        for (int b = mb_row[u]; b < mb_row[u + 1]; ++b) {
+            const int rcb = (rc_cu[b + 1] - rc_cu[b]) / m.tpb;
+            const BlockTableEntry& e = grown[b].entry;
+            const bool gpu = e.location == Location::GpuMem;
+            tok[b] = grown[b].token_index;
+            if (e.kind == BlockKind::ACT) {
+                U.any_act = true;
+                act_dev[b] = pack_ref(gpu ? R_ACT_GPU : R_ACT_STAGE, gpu ? e.pbn : actp.at(e.pbn));
+                if (!gpu && m.owns(e.pbn)) act_host[b] = pack_ref(R_ACT_HOST, e.pbn / m.tpn);
             } else {
-                rb[i] = pack_ref(R_KVR, static_cast<int>(m.act_gpu_cap) + m.act_pos(en.pbn));
-                acth_pos.push_back(m.act_pos(en.pbn));
-                if (m.owns(en.pbn)) acth_own.push_back(en.pbn / m.tpn);
+                U.any_kv = true;
+                kv_dev[b] = pack_ref(gpu ? R_KV_GPU : R_KV_STAGE, gpu ? e.pbn : kvp.at(e.pbn));
+                if (!gpu) kv_host[b] = pack_ref(R_KV_HOST, e.pbn);
+            }
+            const BlockTable& t = cache_->table(ids[b]);
+            nblk[b] = rcb + static_cast<int>(t.entries.size());
+            ctx[b] = rcb * m.tpb + t.context_len();
+            max_ctx = std::max(max_ctx, ctx[b]);
+            int* rb = refs.data() + static_cast<size_t>(b) * m.max_blocks;
+            for (int i = 0; i < rcb; ++i) *rb++ = pack_ref(R_TOKREC, b * m.max_blocks + i);
+            for (size_t i = 0; i < t.entries.size(); ++i) {
+                const auto& en = t.entries[i];
+                const bool g = en.location == Location::GpuMem;
+                if (en.kind == BlockKind::KV)
+                    rb[i] = g ? pack_ref(R_KV_GPU, en.pbn) : pack_ref(R_KV_STAGE, kvp.at(en.pbn));
+                else
+                    rb[i] = pack_ref(R_KVR, g ? en.pbn : static_cast<int>(m.act_gpu_cap) + actp.at(en.pbn));
             }
         }
+        U.splits = attention_splits(mb_row[u + 1] - mb_row[u], m.Hg, max_ctx, m.tpb);
+        if (U.splits > 1)
+            m.ensure_attn_work(static_cast<size_t>(mb_row[u + 1] - mb_row[u]) * m.Hg * U.splits * (m.hd + 2));
     }
-    const std::vector<Run> kv_runs = runs_of(kvh_pbns);
-    const std::vector<Run> act_runs = runs_of(acth_own);
-    const std::vector<int> tiles_h = tiles_of(acth_pos, m.tpb);
-    const bool gather_act = m.tpn > 1 && !acth_pos.empty();
-    const std::vector<int> tiles_g = tiles_of(actg_pbns, m.tpb);
-    const int max_ctx = *std::max_element(ctx.begin(), ctx.end());
-    const int splits = attention_splits(n, m.Hg, max_ctx, m.tpb);
-    if (splits > 1) m.ensure_attn_work(static_cast<size_t>(n) * m.Hg * splits * (m.hd + 2));
+    if (stage_kv_need > m.stage_kv_cap || stage_act_need > m.stage_act_cap)
+        throw CapacityError("decode_step: a mini-batch's blocks exceed the staging buffers");
 
     // one upload of all step metadata
     std::vector<int> meta;
@@ -1163,21 +1333,28 @@ void Engine::decode_step(const std::vector<std::string>& ids, const int* tokens,
         meta.insert(meta.end(), v.begin(), v.end());
         return o;
     };
-    const size_t o_tok = put(std::vector<int>(tokens, tokens + n)), o_pos = put(pos), o_ad = put(act_dev),
-                 o_ah = put(act_host), o_kd = put(kv_dev), o_kh = put(kv_host), o_t = put(tok), o_nb = put(nblk),
-                 o_ctx = put(ctx), o_ref = put(refs), o_th = put(tiles_h), o_tg = put(tiles_g),
+    const size_t o_tok = put(tokv), o_pos = put(pos), o_ad = put(act_dev), o_ah = put(act_host), o_kd = put(kv_dev),
+                 o_kh = put(kv_host), o_t = put(tok), o_nb = put(nblk), o_ctx = put(ctx), o_ref = put(refs),
                  o_rtok = put(rc_tok), o_rpos = put(rc_pos), o_rcu = put(rc_cu), o_trs = put(tr_src),
                  o_trn = put(tr_n), o_trr = put(tr_ref);
-    m.ensure_meta(meta.size());
-    std::memcpy(m.h_meta, meta.data(), meta.size() * 4);
+    for (Unit& U : units) {
+        U.o_th = put(U.tiles_h);
+        U.o_tg = put(U.tiles_g);
+    }
+    m.ensure_meta(meta.size() + 1);
+    if (!meta.empty()) std::memcpy(m.h_meta, meta.data(), meta.size() * 4);
     const int* dm = m.d_meta;
 
     StepStats st{};
     m.pev_used = 0;
     m.spans.clear();
-    const bool stream_any = !m.w_all || !kv_runs.empty() || !act_runs.empty() || gather_act;
-    // layers 0/1 weights already in their slots (prefetched at the end of the previous step)
-    const bool prefetched = m.w_prefetched && !m.w_all;
+    bool stream_any = !m.w_all;
+    for (const Unit& U : units) stream_any = stream_any || !U.kv_runs.empty() || !U.act_runs.empty();
+    stream_any = stream_any || gather_act;
+    // layers 0/1 weights already in their slots (prefetched at the end of the
+    // previous step; never with a shared weight stream, whose ranks must issue
+    // the same gathers every step)
+    const bool prefetched = m.w_prefetched && !m.w_all && m.wsn == 1;
     m.w_prefetched = false;
     bool capturing = false;  // enqueue() runs under stream capture (graph mode)
     // one layer's weights into wbuf[slot] on the copy stream; with a shared
@@ -1205,9 +1382,12 @@ void Engine::decode_step(const std::vector<std::string>& ids, const int* tokens,
     // everything the step puts on the streams; outputs land in xo / lo / ao
     auto enqueue = [&](StepStats& st, uint16_t* xo, float* lo, int* ao) {
         HC_CUDA(cudaEventRecord(m.ev0, s_compute_));
-        HC_CUDA(cudaMemcpyAsync(m.d_meta, m.h_meta, meta.size() * 4, cudaMemcpyHostToDevice, s_compute_));
-        embed(m.emb, m.pos, dm + o_tok, dm + o_pos, n, m.d, m.x[0], m.d, s_compute_);
-        st.launches += 1;
+        if (!meta.empty())
+            HC_CUDA(cudaMemcpyAsync(m.d_meta, m.h_meta, meta.size() * 4, cudaMemcpyHostToDevice, s_compute_));
+        if (n) {
+            embed(m.emb, m.pos, dm + o_tok, dm + o_pos, n, m.d, m.x[0], m.d, s_compute_);
+            st.launches += 1;
+        }
         if (n_rc) {
             embed(m.emb, m.pos, dm + o_rtok, dm + o_rpos, n_rc, m.d, m.px[0], m.d, s_compute_);
             st.launches += 1;
@@ -1216,178 +1396,197 @@ void Engine::decode_step(const std::vector<std::string>& ids, const int* tokens,
         const float scale = opt_.scaled ? 1.0f / std::sqrt(static_cast<float>(m.hd)) : 1.0f;
 
         for (int l = 0; l < m.L; ++l) {
-            const int slot = l & 1;
+            const int wslot = l & 1;
             m.cur_layer = l;
-            if (stream_any) {
-                // copy stream: weights + this layer's host blocks into slot l%2,
-                // after compute released the slot (layer l-2; the previous step,
-                // fully synchronised, for the first two layers — so a captured
-                // graph only waits on events it records itself)
-                HC_CUDA(cudaStreamWaitEvent(s_copy_, l >= 2 ? m.consumed[slot] : m.ev0));
-                m.span_begin(profile_, s_copy_, 3);
-                if (!m.w_all && !(prefetched && l < 2))  // layers 0/1 may have come with the previous step
-                    stream_weights(l, slot, st);
-                const size_t lp = static_cast<size_t>(l % m.Lp);
-                f16* own = m.act_stage[slot] + static_cast<size_t>(m.tpr) * m.act_cap_n * m.actb;
-                for (const Run& r : act_runs) {
-                    const size_t bytes = static_cast<size_t>(r.count) * m.actb * 2;
-                    HC_CUDA(cudaMemcpyAsync(own + static_cast<size_t>(r.start) * m.actb,
-                                            m.act_host + (lp * m.act_cap_n + r.start) * m.actb, bytes,
-                                            cudaMemcpyHostToDevice, s_copy_));
-                    st.h2d_bytes += bytes;
+            const f16* W = m.layer_w(l, wslot);
+            for (int u = 0; u < M; ++u) {
+                const Unit& U = units[u];
+                const int j = l * M + u;  // unit index: staging slot j % 2 (sim.cpp:372-377)
+                m.cur_mb = u;
+                const int slot = j & 1;
+                const int r0 = mb_row[u], nb = mb_row[u + 1] - r0;
+                if (stream_any) {
+                    // copy stream: weights (first unit of the layer, once the layer
+                    // two back released wbuf[l%2]) then this unit's host blocks
+                    // into staging slot j%2 once unit j-2 released it; the first
+                    // two of the step wait for the step start only, so a captured
+                    // graph waits on events it records itself
+                    m.span_begin(profile_, s_copy_, 3);
+                    if (u == 0 && !m.w_all && !(prefetched && l < 2)) {  // layers 0/1 may have come with the previous step
+                        HC_CUDA(cudaStreamWaitEvent(s_copy_, l >= 2 ? m.w_consumed[wslot] : m.ev0));
+                        stream_weights(l, wslot, st);
+                    }
+                    HC_CUDA(cudaStreamWaitEvent(s_copy_, j >= 2 ? m.consumed[slot] : m.ev0));
+                    const size_t lp = static_cast<size_t>(l % m.Lp);
+                    for (const Run& r : U.act_runs) {
+                        const size_t bytes = static_cast<size_t>(r.count) * m.actb * 2;
+                        HC_CUDA(cudaMemcpyAsync(m.act_stage[slot] + static_cast<size_t>(r.dst) * m.actb,
+                                                m.act_host + (lp * m.act_cap_n + r.start) * m.actb, bytes,
+                                                cudaMemcpyHostToDevice, s_copy_));
+                        st.h2d_bytes += bytes;
+                    }
+                    // every rank streamed its 1/tpn of the ACT blocks; an NVLink all-gather
+                    // on the gather stream completes the staging (the recompute needs all
+                    // of X for its heads) while the copy stream moves on to the KV blocks
+                    // and the next layer
+                    if (gather_act) {
+                        f16* own = m.act_stage[slot] + static_cast<size_t>(m.tpr) * m.act_cap_n * m.actb;
+                        HC_CUDA(cudaEventRecord(m.h2d_act[slot], s_copy_));
+                        HC_CUDA(cudaStreamWaitEvent(s_gather_, m.h2d_act[slot]));
+                        m.tp->copy_channel()->all_gather(own, m.act_stage[slot], m.act_cap_n * m.actb, s_gather_);
+                        HC_CUDA(cudaEventRecord(m.gathered[slot], s_gather_));
+                        HC_CUDA(cudaStreamWaitEvent(s_compute_, m.gathered[slot]));
+                    }
+                    for (const Run& r : U.kv_runs) {
+                        const size_t bytes = static_cast<size_t>(r.count) * m.kvb * 2;
+                        HC_CUDA(cudaMemcpyAsync(m.kv_stage[slot] + static_cast<size_t>(r.dst) * m.kvb,
+                                                m.kv_host + (lp * m.kv_host_cap + r.start) * m.kvb, bytes,
+                                                cudaMemcpyHostToDevice, s_copy_));
+                        st.h2d_bytes += bytes;
+                    }
+                    m.span_end(profile_, s_copy_);
+                    HC_CUDA(cudaEventRecord(m.loaded[slot], s_copy_));
+                    HC_CUDA(cudaStreamWaitEvent(s_compute_, m.loaded[slot]));
                 }
-                // every rank streamed its 1/tpn of the ACT blocks; an NVLink all-gather
-                // on the gather stream completes the staging (the recompute needs all
-                // of X for its heads) while the copy stream moves on to the KV blocks
-                // and the next layer
-                if (gather_act) {
-                    HC_CUDA(cudaEventRecord(m.h2d_act[slot], s_copy_));
-                    HC_CUDA(cudaStreamWaitEvent(s_gather_, m.h2d_act[slot]));
-                    m.tp->copy_channel()->all_gather(own, m.act_stage[slot], m.act_cap_n * m.actb, s_gather_);
-                    HC_CUDA(cudaEventRecord(m.gathered[slot], s_gather_));
-                    HC_CUDA(cudaStreamWaitEvent(s_compute_, m.gathered[slot]));
+                f16* R[16];
+                m.regions(l, slot, R);
+                f16* xin = m.x[l & 1];
+                f16* xout = m.x[(l + 1) & 1];
+                if (n_rc && u == 0) {
+                    // token recompute: full layer l over every prefix (FullLayer(rc) FLOPs,
+                    // flops.cpp:20-22), its K|V written into the prefix blocks
+                    m.span_begin(profile_, s_compute_, 0);
+                    f16* pin = m.px[l & 1];
+                    f16* pout = m.px[(l + 1) & 1];
+                    m.qkv(W, m.ln(W, 1, pin, n_rc, m.pxn, s_compute_), n_rc, m.pqkv, s_compute_);
+                    st.launches += m.opt();
+                    BlockScatter sk;
+                    sk.src = m.pqkv;
+                    sk.ld = 3 * m.d;
+                    sk.src_row = dm + o_trs;
+                    sk.n_tok = dm + o_trn;
+                    sk.dst_ref = dm + o_trr;
+                    std::copy(R, R + 16, sk.region);
+                    sk.n_blocks = static_cast<int>(tr_src.size());
+                    sk.d = m.d;
+                    sk.H = m.H;
+                    sk.hd = m.hd;
+                    sk.tpb = m.tpb;
+                    scatter_kv_blocks(sk, s_compute_);
+                    if (l + 1 < m.L) {  // the last layer's prefix output is never needed
+                        prefill_attention(m.pqkv, m.patt, dm + o_rcu, n, rc_max, m.H, m.hd, scale, s_compute_, n_rc);
+                        m.tail(W, m.patt, pin, n_rc, m.pproj, m.patt, m.ph, pout, s_compute_);
+                        st.launches += 1 + m.tail_launches();
+                    }
+                    st.launches += 2;
+                    st.recompute_tokens += n_rc;
+                    m.span_end(profile_, s_compute_);
                 }
-                for (const Run& r : kv_runs) {
-                    const size_t bytes = static_cast<size_t>(r.count) * m.kvb * 2;
-                    HC_CUDA(cudaMemcpyAsync(m.kv_stage[slot] + static_cast<size_t>(r.start) * m.kvb,
-                                            m.kv_host + (lp * m.kv_host_cap + r.start) * m.kvb, bytes,
-                                            cudaMemcpyHostToDevice, s_copy_));
-                    st.h2d_bytes += bytes;
+                if (capture_inputs_ && u == 0)
+                    HC_CUDA(cudaMemcpyAsync(captured_.data() + static_cast<size_t>(l) * n * m.d, xin,
+                                            static_cast<size_t>(n) * m.d * 2, cudaMemcpyDeviceToHost, s_compute_));
+                if (nb > 0) {
+                    const size_t rd = static_cast<size_t>(r0) * m.d;
+                    // the layer's GEMM input (and ACT payload): x, or LN1(x) for kArchOpt
+                    const f16* xa = m.ln(W, 1, xin + rd, nb, m.xn + (m.xn ? rd : 0), s_compute_);
+                    st.launches += m.opt();
+                    AppendCall ap;
+                    std::copy(R, R + 16, ap.region);
+                    ap.B = nb;
+                    ap.d = m.d;  // ACT rows are full width; K|V slots below are this rank's heads
+                    ap.H = m.H;
+                    ap.hd = m.hd;
+                    ap.tpb = m.tpb;
+                    ap.tok = dm + o_t + r0;
+                    if (U.any_act) {  // ACT writer: X of the new token -> its ACT slot (device + host)
+                        ap.src = xa;
+                        ap.ld = m.d;
+                        ap.dev_ref = dm + o_ad + r0;
+                        ap.host_ref = dm + o_ah + r0;
+                        act_append(ap, s_compute_);
+                        st.launches += 1;
+                    }
+                    // recompute K|V of the unit's ACT blocks (streamed and resident) into R_KVR
+                    for (int which = 0; which < 2; ++which) {
+                        const std::vector<int>& tl = which == 0 ? U.tiles_h : U.tiles_g;
+                        if (tl.empty()) continue;
+                        GemmCall c;
+                        c.epi = gemm::kKvPaged;
+                        c.A = which == 0 ? m.act_stage[slot] : R[R_ACT_GPU];
+                        c.lda = m.d;
+                        c.a_rows = static_cast<int>((which == 0 ? m.stage_act_cap : m.act_gpu_cap) * m.tpb);
+                        c.B = W + m.off.wqkv + static_cast<size_t>(m.dg) * m.d;  // rows dg..3dg of Wqkv^T = [Wk|Wv]^T (own heads)
+                        c.ldb = m.d;
+                        c.M = c.a_rows;
+                        c.N = 2 * m.dg;
+                        c.K = m.d;
+                        c.m_tile_rows = dm + (which == 0 ? U.o_th : U.o_tg);
+                        c.num_m_tiles = static_cast<int>(tl.size());
+                        c.out = m.kvr;
+                        c.tpb = m.tpb;
+                        c.d = m.dg;
+                        c.hd = m.hd;
+                        c.blk_off = which == 0 ? static_cast<int>(m.act_gpu_cap) : 0;
+                        c.bias = m.bias(W, m.off.bqkv + m.dg);  // [b_k | b_v] of the own heads
+                        m.span_begin(profile_, s_compute_, 0);
+                        run_gemm(c, s_compute_);
+                        m.span_end(profile_, s_compute_);
+                        st.launches += 1;
+                        st.recompute_tokens += static_cast<double>(tl.size()) * gemm::BM;
+                    }
+                    f16* qkvb = m.qkvb + static_cast<size_t>(r0) * 3 * m.dg;
+                    f16* att = m.att + static_cast<size_t>(r0) * m.dg;
+                    m.span_begin(profile_, s_compute_, 2);
+                    m.qkv(W, xa, nb, qkvb, s_compute_, m.splitk_ws, m.splitk_floats);
+                    m.span_end(profile_, s_compute_);
+                    if (U.any_kv) {  // new token's K|V -> its KV slot (device + host)
+                        ap.src = qkvb;
+                        ap.ld = 3 * m.dg;
+                        ap.d = m.dg;
+                        ap.H = m.Hg;
+                        ap.dev_ref = dm + o_kd + r0;
+                        ap.host_ref = dm + o_kh + r0;
+                        kv_append(ap, s_compute_);
+                        st.launches += 1;
+                    }
+                    AttnCall a;
+                    a.q = qkvb;
+                    a.ldq = 3 * m.dg;
+                    a.out = att;
+                    a.blk_ref = dm + o_ref + static_cast<size_t>(r0) * m.max_blocks;
+                    a.n_blocks = dm + o_nb + r0;
+                    a.ctx_len = dm + o_ctx + r0;
+                    a.max_blocks = m.max_blocks;
+                    for (int i = 0; i < 16; ++i) a.region[i] = R[i];
+                    a.B = nb;
+                    a.H = m.Hg;
+                    a.hd = m.hd;
+                    a.tpb = m.tpb;
+                    a.scale = scale;
+                    a.work = m.attn_work;
+                    a.splits = U.splits;
+                    m.span_begin(profile_, s_compute_, 1);
+                    decode_attention(a, s_compute_);
+                    m.span_end(profile_, s_compute_);
+                    m.span_begin(profile_, s_compute_, 2);
+                    m.tail(W, att, xin + rd, nb, m.proj + rd, att, m.hbuf + static_cast<size_t>(r0) * m.fg,
+                           xout + rd, s_compute_, m.splitk_ws, m.splitk_floats);
+                    m.span_end(profile_, s_compute_);
+                    st.launches += 1 + m.tail_launches() + (U.splits > 1 ? 2 : 1);
                 }
-                m.span_end(profile_, s_copy_);
-                HC_CUDA(cudaEventRecord(m.loaded[slot], s_copy_));
-                HC_CUDA(cudaStreamWaitEvent(s_compute_, m.loaded[slot]));
-            }
-            const f16* W = m.layer_w(l, slot);
-            f16* R[16];
-            m.regions(l, slot, R);
-            f16* xin = m.x[l & 1];
-            f16* xout = m.x[(l + 1) & 1];
-            if (n_rc) {
-                // token recompute: full layer l over every prefix (FullLayer(rc) FLOPs,
-                // flops.cpp:20-22), its K|V written into the prefix blocks
-                m.span_begin(profile_, s_compute_, 0);
-                f16* pin = m.px[l & 1];
-                f16* pout = m.px[(l + 1) & 1];
-                m.qkv(W, m.ln(W, 1, pin, n_rc, m.pxn, s_compute_), n_rc, m.pqkv, s_compute_);
-                st.launches += m.opt();
-                BlockScatter sk;
-                sk.src = m.pqkv;
-                sk.ld = 3 * m.d;
-                sk.src_row = dm + o_trs;
-                sk.n_tok = dm + o_trn;
-                sk.dst_ref = dm + o_trr;
-                std::copy(R, R + 16, sk.region);
-                sk.n_blocks = static_cast<int>(tr_src.size());
-                sk.d = m.d;
-                sk.H = m.H;
-                sk.hd = m.hd;
-                sk.tpb = m.tpb;
-                scatter_kv_blocks(sk, s_compute_);
-                if (l + 1 < m.L) {  // the last layer's prefix output is never needed
-                    prefill_attention(m.pqkv, m.patt, dm + o_rcu, n, rc_max, m.H, m.hd, scale, s_compute_, n_rc);
-                    m.tail(W, m.patt, pin, n_rc, m.pproj, m.patt, m.ph, pout, s_compute_);
-                    st.launches += 1 + m.tail_launches();
-                }
-                st.launches += 2;
-                st.recompute_tokens += n_rc;
-                m.span_end(profile_, s_compute_);
-            }
-            if (capture_inputs_)
-                HC_CUDA(cudaMemcpyAsync(captured_.data() + static_cast<size_t>(l) * n * m.d, xin,
-                                        static_cast<size_t>(n) * m.d * 2, cudaMemcpyDeviceToHost, s_compute_));
-            // the layer's GEMM input (and ACT payload): x, or LN1(x) for kArchOpt
-            const f16* xa = m.ln(W, 1, xin, n, m.xn, s_compute_);
-            st.launches += m.opt();
-            AppendCall ap;
-            std::copy(R, R + 16, ap.region);
-            ap.B = n;
-            ap.d = m.d;  // ACT rows are full width; K|V slots below are this rank's heads
-            ap.H = m.H;
-            ap.hd = m.hd;
-            ap.tpb = m.tpb;
-            ap.tok = dm + o_t;
-            if (any_act) {  // ACT writer: X of the new token -> its ACT slot (device + host)
-                ap.src = xa;
-                ap.ld = m.d;
-                ap.dev_ref = dm + o_ad;
-                ap.host_ref = dm + o_ah;
-                act_append(ap, s_compute_);
-                st.launches += 1;
-                st.d2h_bytes += 0;  // counted below from the slot lists
-            }
-            // recompute K|V of every ACT block (streamed and resident) into R_KVR
-            for (int which = 0; which < 2; ++which) {
-                const std::vector<int>& tl = which == 0 ? tiles_h : tiles_g;
-                if (tl.empty()) continue;
-                GemmCall c;
-                c.epi = gemm::kKvPaged;
-                c.A = which == 0 ? m.act_stage[slot] : R[R_ACT_GPU];
-                c.lda = m.d;
-                c.a_rows = static_cast<int>((which == 0 ? m.tpn * m.act_cap_n : m.act_gpu_cap) * m.tpb);
-                c.B = W + m.off.wqkv + static_cast<size_t>(m.dg) * m.d;  // rows dg..3dg of Wqkv^T = [Wk|Wv]^T (own heads)
-                c.ldb = m.d;
-                c.M = c.a_rows;
-                c.N = 2 * m.dg;
-                c.K = m.d;
-                c.m_tile_rows = dm + (which == 0 ? o_th : o_tg);
-                c.num_m_tiles = static_cast<int>(tl.size());
-                c.out = m.kvr;
-                c.tpb = m.tpb;
-                c.d = m.dg;
-                c.hd = m.hd;
-                c.blk_off = which == 0 ? static_cast<int>(m.act_gpu_cap) : 0;
-                c.bias = m.bias(W, m.off.bqkv + m.dg);  // [b_k | b_v] of the own heads
-                m.span_begin(profile_, s_compute_, 0);
-                run_gemm(c, s_compute_);
-                m.span_end(profile_, s_compute_);
-                st.launches += 1;
-                st.recompute_tokens += static_cast<double>(tl.size()) * gemm::BM;
-            }
-            m.span_begin(profile_, s_compute_, 2);
-            m.qkv(W, xa, n, m.qkvb, s_compute_, m.splitk_ws, m.splitk_floats);
-            m.span_end(profile_, s_compute_);
-            if (any_kv) {  // new token's K|V -> its KV slot (device + host)
-                ap.src = m.qkvb;
-                ap.ld = 3 * m.dg;
-                ap.d = m.dg;
-                ap.H = m.Hg;
-                ap.dev_ref = dm + o_kd;
-                ap.host_ref = dm + o_kh;
-                kv_append(ap, s_compute_);
-                st.launches += 1;
-            }
-            AttnCall a;
-            a.q = m.qkvb;
-            a.ldq = 3 * m.dg;
-            a.out = m.att;
-            a.blk_ref = dm + o_ref;
-            a.n_blocks = dm + o_nb;
-            a.ctx_len = dm + o_ctx;
-            a.max_blocks = m.max_blocks;
-            for (int i = 0; i < 16; ++i) a.region[i] = R[i];
-            a.B = n;
-            a.H = m.Hg;
-            a.hd = m.hd;
-            a.tpb = m.tpb;
-            a.scale = scale;
-            a.work = m.attn_work;
-            a.splits = splits;
-            m.span_begin(profile_, s_compute_, 1);
-            decode_attention(a, s_compute_);
-            m.span_end(profile_, s_compute_);
-            m.span_begin(profile_, s_compute_, 2);
-            m.tail(W, m.att, xin, n, m.proj, m.att, m.hbuf, xout, s_compute_, m.splitk_ws, m.splitk_floats);
-            m.span_end(profile_, s_compute_);
-            st.launches += 1 + m.tail_launches() + (splits > 1 ? 2 : 1);
-            if (capturing && l >= m.L - 2)  // the weight prefetch waits on these from outside the graph
-                HC_CUDA(cudaEventRecordWithFlags(m.consumed[slot], s_compute_, cudaEventRecordExternal));
-            else
+                const bool external = capturing && l >= m.L - 2;  // the weight prefetch waits from outside the graph
                 HC_CUDA(cudaEventRecord(m.consumed[slot], s_compute_));
+                if (u == M - 1) {
+                    if (external)
+                        HC_CUDA(cudaEventRecordWithFlags(m.w_consumed[wslot], s_compute_, cudaEventRecordExternal));
+                    else
+                        HC_CUDA(cudaEventRecord(m.w_consumed[wslot], s_compute_));
+                }
+            }
         }
-        const f16* xf = m.final_norm(m.x[m.L & 1], n, m.xn, s_compute_);
-        st.launches += m.opt();
-        if (lo || ao) {
+        const f16* xf = n ? m.final_norm(m.x[m.L & 1], n, m.xn, s_compute_) : m.x[m.L & 1];
+        st.launches += n ? m.opt() : 0;
+        if ((lo || ao) && n) {
             gemm_rows(gemm::kF32, xf, n, m.d, m.emb, m.V, m.logits, m.V, s_compute_);
             st.launches += 1;
             if (ao) {
@@ -1397,35 +1596,55 @@ void Engine::decode_step(const std::vector<std::string>& ids, const int* tokens,
         }
         HC_CUDA(cudaEventRecord(m.ev1, s_compute_));
         HC_CUDA(cudaGetLastError());
-        if (xo) HC_CUDA(cudaMemcpyAsync(xo, xf, static_cast<size_t>(n) * m.d * 2, cudaMemcpyDeviceToHost, s_compute_));
-        if (lo)
+        if (xo && n)
+            HC_CUDA(cudaMemcpyAsync(xo, xf, static_cast<size_t>(n) * m.d * 2, cudaMemcpyDeviceToHost, s_compute_));
+        if (lo && n)
             HC_CUDA(cudaMemcpyAsync(lo, m.logits, static_cast<size_t>(n) * m.V * 4, cudaMemcpyDeviceToHost, s_compute_));
-        if (ao) HC_CUDA(cudaMemcpyAsync(ao, m.amax, static_cast<size_t>(n) * 4, cudaMemcpyDeviceToHost, s_compute_));
+        if (ao && n) HC_CUDA(cudaMemcpyAsync(ao, m.amax, static_cast<size_t>(n) * 4, cudaMemcpyDeviceToHost, s_compute_));
     };
 
-    // CUDA graph of the step: its launch structure (sizes, copy runs, splits,
-    // outputs) is the key; the data rides in the metadata block
-    const bool use_graph = graphs_ && !profile_ && !capture_inputs_ && m.tpn == 1 && m.wsn == 1;
-    if (!use_graph) {
-        enqueue(st, x_out, logits_out, argmax_out);
-    } else {
+    // outputs of a permuted (mini-batched) step land in the pinned staging
+    // buffers and are put back in the caller's order on the host
+    auto ensure_host_out = [&] {
         if (!m.h_x) {
             m.h_x = halloc<uint16_t>(static_cast<size_t>(m.B) * m.d, false);
             m.h_logits = halloc<float>(static_cast<size_t>(m.B) * m.V, false);
             m.h_amax = halloc<int>(m.B, false);
         }
+    };
+    // CUDA graph of the step: its launch structure (sizes, copy runs, splits,
+    // outputs) is the key; the data rides in the metadata block
+    const bool use_graph = graphs_ && !profile_ && !capture_inputs_ && m.tpn == 1 && m.wsn == 1 && n > 0;
+    const bool via_host = use_graph || permuted;
+    if (via_host) ensure_host_out();
+    uint16_t* xo = x_out ? (via_host ? m.h_x : x_out) : nullptr;
+    float* lo = logits_out ? (via_host ? m.h_logits : logits_out) : nullptr;
+    int* ao = argmax_out ? (via_host ? m.h_amax : argmax_out) : nullptr;
+    if (!use_graph) {
+        enqueue(st, xo, lo, ao);
+    } else {
         std::string key;
         auto add = [&](long v) { key.append(reinterpret_cast<const char*>(&v), sizeof v); };
         for (long v : {static_cast<long>(n), static_cast<long>(n_rc), static_cast<long>(rc_max),
-                       static_cast<long>(meta.size()), static_cast<long>(tiles_h.size()),
-                       static_cast<long>(tiles_g.size()), static_cast<long>(tr_src.size()), static_cast<long>(splits),
-                       static_cast<long>(any_act), static_cast<long>(any_kv), static_cast<long>(stream_any),
-                       static_cast<long>(x_out != nullptr), static_cast<long>(logits_out != nullptr),
-                       static_cast<long>(argmax_out != nullptr), static_cast<long>(prefetched), m.graph_gen})
+                       static_cast<long>(meta.size()), static_cast<long>(tr_src.size()), static_cast<long>(M),
+                       static_cast<long>(stream_any), static_cast<long>(x_out != nullptr),
+                       static_cast<long>(logits_out != nullptr), static_cast<long>(argmax_out != nullptr),
+                       static_cast<long>(prefetched), m.graph_gen})
             add(v);
-        for (const auto* runs : {&kv_runs, &act_runs}) {
-            add(static_cast<long>(runs->size()));
-            for (const Run& r : *runs) add((static_cast<long>(r.start) << 32) | r.count);
+        for (int u = 0; u < M; ++u) {
+            const Unit& U = units[u];
+            for (long v : {static_cast<long>(mb_row[u + 1]), static_cast<long>(U.tiles_h.size()),
+                           static_cast<long>(U.tiles_g.size()), static_cast<long>(U.splits),
+                           static_cast<long>(U.any_act), static_cast<long>(U.any_kv), static_cast<long>(U.o_th),
+                           static_cast<long>(U.o_tg)})
+                add(v);
+            for (const auto* runs : {&U.kv_runs, &U.act_runs}) {
+                add(static_cast<long>(runs->size()));
+                for (const Run& r : *runs) {
+                    add((static_cast<long>(r.start) << 32) | r.count);
+                    add(r.dst);
+                }
+            }
         }
         auto it = m.graphs.find(key);
         if (it == m.graphs.end()) {
@@ -1441,8 +1660,7 @@ void Engine::decode_step(const std::vector<std::string>& ids, const int* tokens,
             HC_CUDA(cudaStreamBeginCapture(s_compute_, cudaStreamCaptureModeThreadLocal));
             capturing = true;
             try {
-                enqueue(sg.stats, x_out ? m.h_x : nullptr, logits_out ? m.h_logits : nullptr,
-                        argmax_out ? m.h_amax : nullptr);
+                enqueue(sg.stats, xo, lo, ao);
             } catch (...) {
                 capturing = false;
                 cudaStreamEndCapture(s_compute_, &g);
@@ -1466,9 +1684,9 @@ void Engine::decode_step(const std::vector<std::string>& ids, const int* tokens,
     // next step's layer 0/1 weights (step-independent) over the link while the
     // last two layers compute — the reference arms weight(step+1) before the
     // step's tail too (sim.cpp:534-537); the step ends when they have landed
-    if (!m.w_all && stream_any) {
+    if (!m.w_all && stream_any && m.wsn == 1) {
         for (int l = 0; l < std::min(2, m.L); ++l) {
-            HC_CUDA(cudaStreamWaitEvent(s_copy_, m.consumed[l & 1]));
+            HC_CUDA(cudaStreamWaitEvent(s_copy_, m.w_consumed[l & 1]));
             stream_weights(l, l & 1, st);
         }
         HC_CUDA(cudaEventRecord(m.wpre, s_copy_));
@@ -1477,14 +1695,27 @@ void Engine::decode_step(const std::vector<std::string>& ids, const int* tokens,
     }
     HC_CUDA(cudaEventRecord(use_graph ? m.tg1 : m.ev1, s_compute_));
     HC_CUDA(cudaStreamSynchronize(s_compute_));
-    if (use_graph) {
-        if (x_out) std::memcpy(x_out, m.h_x, static_cast<size_t>(n) * m.d * 2);
-        if (logits_out) std::memcpy(logits_out, m.h_logits, static_cast<size_t>(n) * m.V * 4);
-        if (argmax_out) std::memcpy(argmax_out, m.h_amax, static_cast<size_t>(n) * 4);
+    if (via_host) {  // back to the caller's request order
+        for (int i = 0; i < n; ++i) {
+            const int b = order[i];
+            if (x_out) std::memcpy(x_out + static_cast<size_t>(b) * m.d, m.h_x + static_cast<size_t>(i) * m.d, m.d * 2);
+            if (logits_out)
+                std::memcpy(logits_out + static_cast<size_t>(b) * m.V, m.h_logits + static_cast<size_t>(i) * m.V,
+                            static_cast<size_t>(m.V) * 4);
+            if (argmax_out) argmax_out[b] = m.h_amax[i];
+        }
+    }
+    if (capture_inputs_ && permuted) {  // captured rows back to the caller's order too
+        std::vector<uint16_t> c(captured_);
+        for (int l = 0; l < m.L; ++l)
+            for (int i = 0; i < n; ++i)
+                std::memcpy(captured_.data() + (static_cast<size_t>(l) * n + order[i]) * m.d,
+                            c.data() + (static_cast<size_t>(l) * n + i) * m.d, static_cast<size_t>(m.d) * 2);
     }
     float ms = 0;
     HC_CUDA(cudaEventElapsedTime(&ms, use_graph ? m.tg0 : m.ev0, use_graph ? m.tg1 : m.ev1));
     st.step_ms = ms;
+    st.minibatches = M;
     // trace of the profiled step: the reference's SimEvent schema
     // (sim.hpp:50-58; trace.json main.cpp:263-275) from CUDA events
     std::string trace;
@@ -1499,10 +1730,10 @@ void Engine::decode_step(const std::vector<std::string>& ids, const int* tokens,
             char buf[256];
             std::snprintf(buf, sizeof buf,
                           "%s{\"name\":\"%s\",\"track\":\"%s\",\"start_us\":%.3f,\"end_us\":%.3f,\"iteration\":%ld,"
-                          "\"layer\":%d,\"minibatch\":0}",
+                          "\"layer\":%d,\"minibatch\":%d}",
                           first ? "" : ",", (sp.kind == 0 && token_mode_) ? "token_recompute" : names[sp.kind],
                           sp.kind == 3 ? "PCIe" : "GPU", t0 * 1e3, t1 * 1e3, static_cast<long>(step_counter_),
-                          sp.layer);
+                          sp.layer, sp.minibatch);
             trace += buf;
             first = false;
         }
@@ -1584,7 +1815,7 @@ double Engine::time_kv_gen(int n_tokens, int reps) {
     if (n_tokens <= 0) throw InputError("time_kv_gen: n_tokens must be positive");
     if (reps <= 0) throw InputError("time_kv_gen: reps must be positive");
     // recompute GEMM over n tokens of the ACT staging (or GPU) pool, layer 0
-    const long stage_rows = static_cast<long>(m.tpn) * m.act_cap_n * m.tpb;
+    const long stage_rows = m.stage_act_cap * m.tpb;
     const long cap_rows = std::max(stage_rows, m.act_gpu_cap * m.tpb);
     if (n_tokens > cap_rows) throw InputError("time_kv_gen: more tokens than the ACT pools hold");
     const bool from_stage = stage_rows >= n_tokens;

@@ -32,6 +32,7 @@
 #include <vector>
 
 #include "host/cache.hpp"
+#include "host/minibatch.hpp"
 #include "host/model.hpp"
 #include "kernels/kernels.hpp"
 #include "tp.hpp"
@@ -74,6 +75,7 @@ struct StepStats {
     double copy_ms = 0;           // summed copy-stream time of the H2D streams (profiled)
     int recompute_launches = 0;
     double store_ms = 0;          // summed store-stream (D2H) time (profiled prefill)
+    int minibatches = 1;          // (layer, mini-batch) units per layer of the last decode step
 };
 
 class Engine {
@@ -95,6 +97,13 @@ public:
     // Admit requests with prompt_len tokens of bookkeeping only and fill their
     // blocks with a deterministic pattern (benchmark setup; no numerics).
     void admit_synthetic(const std::vector<std::string>& ids, const std::vector<int>& prompt_lens, uint64_t seed);
+    // Mini-batched decode (paper §4.3.3; sim.cpp:258-358): staging slots hold
+    // act_max ACT / kv_max KV blocks (+ one growth block per request); every
+    // step packs its requests with form_minibatches (minibatch.cpp:36-83) on
+    // pre-growth block counts, priced by `bundle`, and runs (layer,
+    // mini-batch) units double-buffered. act_max = kv_max = 0 turns it off
+    // (whole-batch steps, staging = the host pools).
+    void set_minibatching(long act_max, long kv_max, const TimingBundle& bundle);
     // Fill every pool slot with the deterministic pattern (benchmark setup:
     // slots that advance_synthetic later hands out then hold finite values).
     void fill_pools(uint64_t seed);
@@ -171,6 +180,7 @@ private:
     std::unique_ptr<HybridCache> cache_;
     std::unique_ptr<BlockAssigner> assigner_;
     cudaStream_t s_compute_ = nullptr, s_copy_ = nullptr, s_store_ = nullptr, s_gather_ = nullptr;
+    void alloc_staging();
     StepStats stats_{};
     bool profile_ = false;
     bool graphs_ = true;

@@ -1,6 +1,7 @@
 """N>1 host path on CPU: world_size-2 gloo process group exercising bench.py's
 rank plumbing (barrier, max-over-ranks timing, summed tokens) and the
 batch partition (each rank its own requests / cache, no data collective)."""
+import json
 import os
 import socket
 import subprocess
@@ -68,22 +69,69 @@ def test_two_rank_gloo_bench_plumbing(tmp_path):
 
 
 def test_reference_arm_nonzero_ranks_exit_silently(tmp_path):
-    """--impl reference under N>1: rank 0 alone prints; others exit 0 (tested
-    with a stubbed sample to stay fast)."""
+    """--impl reference under N>1: rank 0 alone prints; others exit 0."""
     code = f"""
 import sys, json
 sys.path.insert(0, {ROOT!r})
 import bench
 class A: pass
 a = A(); a.gpus = 2; a.steps = 1; a.warmup = 0; a.prompt = 8; a.ratio = 0.5; a.batch = 2; a.gen = 4
-from paper_2501_01792_b200 import api
-cfg = api.ModelConfig(num_layers=2, hidden_dim=64, num_heads=1, ffn_dim=128, vocab_size=64, name="tiny")
-bench.reference_arm(a, cfg, 2, 1, None)
+bench.reference_arm(a, 2, 1, None)
 print("done")
 """
     out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=120)
     assert out.returncode == 0, out.stderr
     assert out.stdout.strip() == "done"
+
+
+def test_reference_arm_never_loads_the_product():
+    """bench.py --impl reference runs the reference library only: the product
+    package is never imported and libhybridcache_b200.so never mapped; its
+    config equals the one our arm builds (same r from the same bundle)."""
+    import importlib.util
+    if importlib.util.find_spec("ref_lib") is None:
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import ref_lib as R
+    if not R.available():
+        pytest.skip("oracle/_ref not built")
+    code = f"""
+import sys, json
+sys.path.insert(0, {ROOT!r})
+sys.argv = ["bench.py", "--impl", "reference", "--model", "opt-6.7b", "--layers", "1", "--steps", "1",
+            "--warmup", "0", "--batch", "4", "--prompt", "64", "--gen", "16"]
+import bench
+bench.main()
+assert not any(m.startswith("paper_2501_01792_b200") for m in sys.modules), "product imported"
+maps = open("/proc/self/maps").read()
+assert "libhybridcache_b200" not in maps, "product library mapped"
+assert "libhybridsim_ref" in maps
+"""
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stderr
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    assert line["impl"] == "reference" and line["cpu_baseline"]["single_thread"]["cores"] == 1
+    assert line["config"]["timed_context"] == 64 + 8
+
+
+def test_both_arms_plan_the_same_ratio():
+    """The reference arm's planner (the reference's plan_host_allocation) and
+    ours (bit-exact restatement) pick the same r from the committed bundle."""
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import bench
+    import ref_lib as R
+    from paper_2501_01792_b200 import api
+    if not R.available():
+        pytest.skip("oracle/_ref not built")
+    path = os.path.join(ROOT, "profiles", "planner_bundle_opt-30b.json")
+    cfg = api.ModelConfig.preset("opt-30b")
+    ref = bench.planned_ratio(R.parse_bundle(path), cfg, 128 * (1024 + 256), R.plan_host_allocation)
+    ours = bench.planned_ratio(bench.read_bundle(path), cfg, 128 * (1024 + 256),
+                               lambda b5, m4, tpb, ag: list(api.plan_host_allocation(
+                                   api.TimingBundle(api.LinearTimeModel(b5[0], b5[1]),
+                                                    api.LinearTimeModel(b5[2], b5[3]), b5[4]),
+                                   api.MemoryBudget(*m4), tpb, ag).__dict__.values()))
+    assert ref == ours and 0.0 < ref[0] < 1.0
 
 
 def test_config4_strong_split_covers_global_batch():

@@ -1000,3 +1000,64 @@ def test_engine_reconfigure_across_modes(native):
                     continue  # folded host pools (a benchmark device): payloads alias across layers
                 ref = O.forward_prompt(seqs[b], w).output[-1]
                 assert rel(f64(res["x"][b]), ref) <= TOL, (i, mode, step, b)
+
+
+@pytest.mark.parametrize("weights_on_device,graphs", [(False, True), (True, False)])
+def test_engine_minibatched_decode_matches_oracle(native, weights_on_device, graphs):
+    """Mini-batched decode (paper §4.3.3; sim.cpp:258-358): staging slots capped
+    so every step splits into >= 2 (layer, mini-batch) units packed by
+    form_minibatches on PRE-growth block counts (minibatch.cpp:36-83). Outputs
+    equal the oracle; the block tables equal the oracle's add_token replay in
+    the reference's mini-batch order (sim.cpp:294-310); the prefill writes its
+    host blocks straight into the pinned pools (the staging is smaller)."""
+    from paper_2501_01792_b200.api import HostAllocation, LinearTimeModel, PoolCaps, TimingBundle
+    cfg = small_cfg(L=3, d=256, H=2, f=512, tpb=8)
+    w = oracle_weights(cfg, seed=21, max_seq=96)
+    rng = np.random.default_rng(77)
+    lens = [23, 40, 9, 31, 17]
+    prompts = [rng.integers(0, cfg.vocab_size, n).tolist() for n in lens]
+    ids = [f"m{i}" for i in range(len(lens))]
+    alloc = HostAllocation(3, 2)
+    caps = PoolCaps(kv_host=40, act_host=40, act_gpu=2)
+    eng = make_engine(cfg, w, max_batch=len(ids), caps=caps, allocation=alloc, mode="hybrid",
+                      weights_on_device=weights_on_device)
+    eng.set_graphs(graphs)
+    bundle = TimingBundle(LinearTimeModel(1e-7, 1e-5), LinearTimeModel(5e-7, 0.0), 0.02)
+    act_max, kv_max = 6, 5
+    eng.set_minibatching(act_max, kv_max, bundle)
+    eng.prefill(ids, prompts)
+    ba = O.BlockAssigner(cfg.tokens_per_block, O.HYBRID, O.HostAllocation(3, 2), act_gpu=2)
+    for rid, n in zip(ids, lens):
+        ba.add_request(rid, n)
+        for _ in range(n):
+            ba.add_token(rid)
+    ob = O.TimingBundle(O.LinearTimeModel(1e-7, 1e-5), O.LinearTimeModel(5e-7, 0.0), 0.02)
+    seqs = [list(p) for p in prompts]
+    n_mb = []
+    for step in range(5):
+        toks = [int(t) for t in rng.integers(0, cfg.vocab_size, len(ids))]
+        # the reference's order: pack on pre-growth counts, grow mini-batch by mini-batch
+        reqs = [(rid, *ba.cache.table(rid).blocks_by_kind()) for rid in ids]
+        for mb in O.form_minibatches(reqs, act_max, kv_max, ob, cfg.tokens_per_block):
+            for rid in mb:
+                ba.add_token(rid)
+        res = eng.decode_step(ids, toks, want_x=True, want_logits=True, want_argmax=True)
+        n_mb.append(eng.last_stats()["minibatches"])
+        for b in range(len(ids)):
+            seqs[b].append(toks[b])
+            x = O.forward_prompt(seqs[b], w).output[-1:]
+            assert rel(f64(res["x"][b]), x[0]) <= TOL, (step, b)
+            assert rel(res["logits"][b], O.logits_tied(x, w)[0]) <= TOL, (step, b)
+        assert eng.cache.dump_json() == O.dumps(ba.cache.dump_json()), step
+    assert min(n_mb) >= 2, n_mb
+    # a request larger than the staging: CapacityError, tables untouched
+    from paper_2501_01792_b200 import CapacityError
+    before = eng.cache.dump_json()
+    eng.set_minibatching(1, 1, bundle)
+    with pytest.raises(CapacityError):
+        eng.decode_step(ids, toks)
+    assert eng.cache.dump_json() == before
+    eng.set_minibatching(0, 0)
+    res = eng.decode_step(ids, toks, want_x=True)
+    assert eng.last_stats()["minibatches"] == 1
+    eng.close()
