@@ -626,7 +626,7 @@ def run_prefill(eng, cfg, ids, P, rank, tflops_sust, link_gbs):
             "launches": int(st["launches"])}
 
 
-def calibrate_planner(eng, cfg, link_gbs, caps_act_rows, workload_tokens, act_gpu=0, tpn=1, wsn=1):
+def calibrate_planner(eng, cfg, link_gbs, caps_act_rows, workload_tokens, act_gpu=0, tpn=1, wsn=1, caps_kv_blocks=0):
     """North-star (5): measured recompute-GEMM and host-link samples ->
     bundle_from_samples (timing.cpp:172-183) -> plan_host_allocation
     (plan.cpp:106-152) over a WORKLOAD-sized host budget, as the reference's
@@ -639,7 +639,11 @@ def calibrate_planner(eng, cfg, link_gbs, caps_act_rows, workload_tokens, act_gp
     if len(ns) < 2:  # small per-rank batches (config 4 split 8 ways): smaller samples, still >= 2
         ns = [n for n in (512, 1024, 2048, 4096, 8192) if n <= caps_act_rows][-3:]
     kv = [(float(n), eng.time_kv_gen(n, reps=3)) for n in ns]
-    ld = [(float(n), eng.time_load_kv(n, reps=2)) for n in ns]
+    # link samples: KV-token byte counts the pinned pools and a staging slot hold
+    kv_tok = 2 * cfg.hidden_dim * 2 // tpn
+    room = max(caps_kv_blocks * api.HybridCache.bytes_of("KV", cfg), caps_act_rows * cfg.hidden_dim * 2)
+    ln = [n for n in (4096, 16384, 32768, 65536) if n * kv_tok <= room] or [n for n in (256, 1024, 2048)]
+    ld = [(float(n), eng.time_load_kv(n, reps=2)) for n in ln]
     bundle = api.bundle_from_samples(kv, ld, link_gbs * 1e9, cfg)
     if tpn > 1:  # a head-sharded rank streams and stores 1/N of every weight and block
         bundle.t_load_w /= tpn
@@ -770,7 +774,7 @@ def our_arm(args, cfg, world, rank, local, dist):
     # host-link peak: a large pinned H2D copy on the engine's copy stream, all
     # ranks copying at once (ranks share PCIe switches)
     tpb = cfg.tokens_per_block
-    n_tok = min(caps.kv_host * tpb, 65536) if caps.kv_host else 0
+    n_tok = min(max(caps.kv_host * tpb, caps.act_host * tpb // 2), 65536)
     barrier(dist)
     # (best of 3 trials of 4 back-to-back copies: the copy engine's sustained peak)
     link_gbs = (n_tok * 2 * (d // tpn) * 2) / min(eng.time_load_kv(n_tok, reps=4) for _ in range(3)) / 1e9 \
@@ -781,7 +785,7 @@ def our_arm(args, cfg, world, rank, local, dist):
     if link_gbs and caps.act_host:
         try:
             planner = calibrate_planner(eng, cfg, link_gbs, caps.act_host * tpb, B * (P + args.gen), tpn=tpn,
-                                        wsn=wsn)
+                                        wsn=wsn, caps_kv_blocks=caps.kv_host)
         except Exception as e:  # planner failure must not kill the bench line
             planner = {"error": str(e)}
     if r_src == "live" and planner and "planned_r" in planner:

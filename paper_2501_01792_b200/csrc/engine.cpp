@@ -1861,13 +1861,16 @@ double Engine::time_kv_gen(int n_tokens, int reps) {
 double Engine::time_load_bytes(size_t bytes, int reps) {
     HC_CUDA(cudaSetDevice(opt_.device));  // the calling thread may be on another device
     Impl& m = *impl_;
-    const size_t cap = static_cast<size_t>(m.kv_host_cap) * m.kvb * 2;
-    if (bytes == 0 || bytes > cap) throw InputError("time_load: byte count exceeds the KV host pool");
+    // pinned arena (KV then ACT host pools) -> the larger staging slot pair
+    const bool kv_dst = m.stage_kv_cap * m.kvb >= m.stage_act_cap * m.actb;
+    f16* dst[2] = {kv_dst ? m.kv_stage[0] : m.act_stage[0], kv_dst ? m.kv_stage[1] : m.act_stage[1]};
+    const size_t cap = std::min(m.h_arena_elems, kv_dst ? m.stage_kv_cap * m.kvb : m.stage_act_cap * m.actb) * 2;
+    if (bytes == 0 || bytes > cap) throw InputError("time_load: byte count exceeds the host pools / staging");
     if (reps <= 0) throw InputError("time_load: reps must be positive");
-    HC_CUDA(cudaMemcpyAsync(m.kv_stage[0], m.kv_host, bytes, cudaMemcpyHostToDevice, s_copy_));
+    HC_CUDA(cudaMemcpyAsync(dst[0], m.h_arena, bytes, cudaMemcpyHostToDevice, s_copy_));
     HC_CUDA(cudaEventRecord(m.ev0, s_copy_));
     for (int i = 0; i < reps; ++i)
-        HC_CUDA(cudaMemcpyAsync(m.kv_stage[i & 1], m.kv_host, bytes, cudaMemcpyHostToDevice, s_copy_));
+        HC_CUDA(cudaMemcpyAsync(dst[i & 1], m.h_arena, bytes, cudaMemcpyHostToDevice, s_copy_));
     HC_CUDA(cudaEventRecord(m.ev1, s_copy_));
     HC_CUDA(cudaEventSynchronize(m.ev1));
     float ms = 0;
