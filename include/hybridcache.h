@@ -122,6 +122,10 @@ int hc_weight_bytes(const hc_model_config* cfg, uint64_t* out2);
  * order, batch_of[i] = mini-batch of request i. */
 int hc_form_minibatches(int n, const char* const* ids, const long* act_blocks, const long* kv_blocks, long act_max,
                         long kv_max, const double* bundle5, int tpb, int* order, int* batch_of, int* n_batches);
+/* brute_force_pack (minibatch.hpp:43-47; <= 10 requests): exhaustive search,
+ * fewest mini-batches then smallest mean F_b; outputs as hc_form_minibatches. */
+int hc_brute_force_pack(int n, const char* const* ids, const long* act_blocks, const long* kv_blocks, long act_max,
+                        long kv_max, const double* bundle5, int tpb, int* order, int* batch_of, int* n_batches);
 /* balance / cost_fb (minibatch.cpp:10-23): out2 = {balance, F_b} */
 int hc_cost_fb(long act_mb, long kv_mb, const double* bundle5, int tpb, double* out2);
 /* default_packer (sim.cpp:122-132): out2 = {act_max, kv_max} */

@@ -70,6 +70,7 @@ SIGNATURES = {
     "hc_weight_bytes": (i, [cfgp, u64p]),
     # mini-batch packer
     "hc_form_minibatches": (i, [i, cpp, lp, lp, l, l, dp, i, ip, ip, ip]),
+    "hc_brute_force_pack": (i, [i, cpp, lp, lp, l, l, dp, i, ip, ip, ip]),
     "hc_cost_fb": (i, [l, l, dp, i, dp]),
     "hc_default_packer": (i, [d, cfgp, lp]),
     # engine

@@ -317,15 +317,13 @@ int hc_budget_for(double host_mem, const hc_model_config* cfg, double s_weight_t
 }
 int hc_flop_count(int kind, const hc_model_config* cfg, long n, int k, double* out) {
     return hc_guard([&] {
-        ModelConfig c = to_cfg(cfg);
-        c.validate();
+        const ModelConfig c = to_cfg(cfg);  // pure arithmetic: no validation (flops.cpp:7-33)
         *out = flop_count(kind, c, n, k);
     });
 }
 int hc_weight_bytes(const hc_model_config* cfg, uint64_t* out2) {
     return hc_guard([&] {
-        ModelConfig c = to_cfg(cfg);
-        c.validate();
+        const ModelConfig c = to_cfg(cfg);  // pure arithmetic: no validation (timing.cpp:118-127)
         const WeightBytes w = weight_bytes(c);
         out2[0] = w.per_layer;
         out2[1] = w.total;
@@ -333,12 +331,14 @@ int hc_weight_bytes(const hc_model_config* cfg, uint64_t* out2) {
 }
 
 // ---- mini-batch packer ----------------------------------------------------
-int hc_form_minibatches(int n, const char* const* ids, const long* act_blocks, const long* kv_blocks, long act_max,
-                        long kv_max, const double* b5, int tpb, int* order, int* batch_of, int* n_batches) {
+namespace {
+int pack_into(decltype(&form_minibatches) fn, int n, const char* const* ids, const long* act_blocks,
+              const long* kv_blocks, long act_max, long kv_max, const double* b5, int tpb, int* order, int* batch_of,
+              int* n_batches) {
     return hc_guard([&] {
         std::vector<RequestBlocks> reqs;
         for (int i = 0; i < n; ++i) reqs.push_back(RequestBlocks{sid(ids[i]), act_blocks[i], kv_blocks[i]});
-        const auto mbs = form_minibatches(reqs, PackerConfig{act_max, kv_max}, bundle_of(b5), tpb);
+        const auto mbs = fn(reqs, PackerConfig{act_max, kv_max}, bundle_of(b5), tpb);
         std::unordered_map<std::string, int> pos;
         for (int i = 0; i < n; ++i) pos[reqs[i].id] = i;
         int k = 0;
@@ -349,6 +349,18 @@ int hc_form_minibatches(int n, const char* const* ids, const long* act_blocks, c
             }
         *n_batches = static_cast<int>(mbs.size());
     });
+}
+}  // namespace
+
+int hc_form_minibatches(int n, const char* const* ids, const long* act_blocks, const long* kv_blocks, long act_max,
+                        long kv_max, const double* b5, int tpb, int* order, int* batch_of, int* n_batches) {
+    return pack_into(&form_minibatches, n, ids, act_blocks, kv_blocks, act_max, kv_max, b5, tpb, order, batch_of,
+                     n_batches);
+}
+int hc_brute_force_pack(int n, const char* const* ids, const long* act_blocks, const long* kv_blocks, long act_max,
+                        long kv_max, const double* b5, int tpb, int* order, int* batch_of, int* n_batches) {
+    return pack_into(&brute_force_pack, n, ids, act_blocks, kv_blocks, act_max, kv_max, b5, tpb, order, batch_of,
+                     n_batches);
 }
 int hc_cost_fb(long act_mb, long kv_mb, const double* b5, int tpb, double* out2) {
     return hc_guard([&] {

@@ -70,6 +70,68 @@ std::vector<MiniBatch> form_minibatches(const std::vector<RequestBlocks>& reques
     return out;
 }
 
+// Exhaustive partition search (the quality oracle for the greedy packer,
+// minibatch.hpp:43-47): every assignment of requests to groups that respect
+// the capacities, fewest groups first, then the smallest mean F_b. Groups are
+// grown request by request; a branch is cut once it has more groups than the
+// best complete partition.
+std::vector<MiniBatch> brute_force_pack(const std::vector<RequestBlocks>& requests, const PackerConfig& cfg,
+                                        const TimingBundle& b, int tpb) {
+    if (requests.size() > 10) throw InputError("brute_force_pack: refusing more than 10 requests");
+    for (const RequestBlocks& r : requests)
+        if (r.act_blocks < 0 || r.kv_blocks < 0 || r.act_blocks > cfg.act_max || r.kv_blocks > cfg.kv_max)
+            throw InputError("request too large for GPU buffer capacities: " + r.id);
+    if (requests.empty()) return {};
+    const size_t n = requests.size();
+    std::vector<int> group(n, -1), best;
+    std::vector<long> ga, gk;  // per open group: ACT / KV blocks
+    size_t best_groups = n + 1;
+    double best_mean = std::numeric_limits<double>::infinity();
+    auto mean_fb = [&] {
+        double s = 0;
+        for (size_t g = 0; g < ga.size(); ++g) s += cost_fb(ga[g], gk[g], b, tpb);
+        return s / static_cast<double>(ga.size());
+    };
+    auto dfs = [&](auto&& self, size_t i) -> void {
+        if (ga.size() > best_groups) return;
+        if (i == n) {
+            const double m = mean_fb();
+            if (ga.size() < best_groups || m < best_mean) {
+                best_groups = ga.size();
+                best_mean = m;
+                best = group;
+            }
+            return;
+        }
+        const RequestBlocks& r = requests[i];
+        for (size_t g = 0; g < ga.size(); ++g) {
+            if (ga[g] + r.act_blocks > cfg.act_max || gk[g] + r.kv_blocks > cfg.kv_max) continue;
+            ga[g] += r.act_blocks;
+            gk[g] += r.kv_blocks;
+            group[i] = static_cast<int>(g);
+            self(self, i + 1);
+            ga[g] -= r.act_blocks;
+            gk[g] -= r.kv_blocks;
+        }
+        ga.push_back(r.act_blocks);
+        gk.push_back(r.kv_blocks);
+        group[i] = static_cast<int>(ga.size()) - 1;
+        self(self, i + 1);
+        ga.pop_back();
+        gk.pop_back();
+        group[i] = -1;
+    };
+    dfs(dfs, 0);
+    std::vector<MiniBatch> out(best_groups);
+    for (size_t i = 0; i < n; ++i) {
+        MiniBatch& mb = out[static_cast<size_t>(best[i])];
+        mb.ids.push_back(requests[i].id);
+        mb.act_mb += requests[i].act_blocks;
+        mb.kv_mb += requests[i].kv_blocks;
+    }
+    return out;
+}
+
 PackerConfig default_packer(double gpu_mem_bytes, const ModelConfig& c) {
     const double kv = static_cast<double>(HybridCache::bytes_of(BlockKind::KV, c));
     const double act = static_cast<double>(HybridCache::bytes_of(BlockKind::ACT, c));

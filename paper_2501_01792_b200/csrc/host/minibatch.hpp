@@ -32,6 +32,10 @@ double balance(long act_mb, long kv_mb, const TimingBundle& b, int tpb);
 double cost_fb(long act_mb, long kv_mb, const TimingBundle& b, int tpb);
 std::vector<MiniBatch> form_minibatches(const std::vector<RequestBlocks>& requests, const PackerConfig& cfg,
                                         const TimingBundle& b, int tpb);
+// Exhaustive search (<= 10 requests): fewest mini-batches, then the smallest
+// mean F_b — the packer's quality oracle.
+std::vector<MiniBatch> brute_force_pack(const std::vector<RequestBlocks>& requests, const PackerConfig& cfg,
+                                        const TimingBundle& b, int tpb);
 // Staging capacities from a GPU memory size: 1/4 for KV, 1/8 for ACT, halved
 // for double buffering (sim.cpp:122-132).
 PackerConfig default_packer(double gpu_mem_bytes, const ModelConfig& c);
