@@ -1037,9 +1037,18 @@ def our_arm(args, cfg, world, rank, local, dist):
                                    "sample": sample, "single_thread": single_thread_leg(cfg, ctx_mid, n_act)}
         if not args.no_sweep and world == 1:
             try:
-                res["hbm_resident"] = resident_variants(local, cfg, B, P, args.arch)
+                res["hbm_resident"] = resident_variants(local, cfg, B, ctx_mid, args.arch)
             except Exception as e:
                 res["hbm_resident"] = {"error": str(e)}
+            # the offloaded workload itself (weights still streamed from pinned
+            # host every layer) with an HBM cache tier planned by the reference's
+            # own act_gpu / kv_on_gpu placement (cache.cpp:79-107): hybrid vs
+            # pure KV vs pure ACT
+            try:
+                res["hbm_tiers_streamed_weights"] = resident_variants(local, cfg, B, ctx_mid, args.arch,
+                                                                      weights_on_device=False)
+            except Exception as e:
+                res["hbm_tiers_streamed_weights"] = {"error": str(e)}
         if not args.no_sweep and world == 1 and args.config == 3:
             try:
                 res["config1_e2e"] = config1_e2e(local, None if args.no_cpu_baseline else os.cpu_count() or 1)
@@ -1066,7 +1075,8 @@ def _host_mem_available():
     return 0.0
 
 
-def resident_variants(local, cfg, B, P, arch, steps=2, warmup=1, reserve=3e9, only_planned=False):
+def resident_variants(local, cfg, B, P, arch, steps=2, warmup=1, reserve=3e9, only_planned=False,
+                      weights_on_device=True):
     """The same workload with the weights AND the cache in HBM (B200 has 180 GB):
     KV and ACT blocks both placed on the GPU first (kv_on_gpu / ACT-first,
     cache.cpp:64-91). Pure KV does not fit, so its overflow blocks stream from
@@ -1088,8 +1098,8 @@ def resident_variants(local, cfg, B, P, arch, steps=2, warmup=1, reserve=3e9, on
     kv_all = api.HybridCache.bytes_of("KV", cfg) * L
     act_all = api.HybridCache.bytes_of("ACT", cfg) * L
     kv_one = api.HybridCache.bytes_of("KV", cfg)  # recompute output buffer per ACT block (one layer)
-    eng = api.Engine(cfg, seed=42, max_seq=P + total + 1, rescale=True, max_batch=B, weights_on_device=True,
-                     caps=api.PoolCaps(), mode="act_only", device=local, arch=arch)
+    eng = api.Engine(cfg, seed=42, max_seq=P + total + 1, rescale=True, max_batch=B,
+                     weights_on_device=weights_on_device, caps=api.PoolCaps(), mode="act_only", device=local, arch=arch)
     # measured rates on this engine (north-star (5)): recompute GEMM vs ACT
     # tokens, host link vs KV tokens, through small calibration pools
     eng.configure_cache(api.PoolCaps(kv_host=1024, act_host=4096), mode="hybrid", host_layers=1)
@@ -1106,7 +1116,8 @@ def resident_variants(local, cfg, B, P, arch, steps=2, warmup=1, reserve=3e9, on
     # host, max(t_kv_gen, t_load_kv) minimised on the measured bundle)
     r_fit, caps_fit = api.plan_hbm_residency(cfg, B, nb, free)
     try:
-        r_bal, caps_bal, t_bal = api.plan_hbm_tiers(cfg, B, nb, free, bundle, host_bytes=host_budget)
+        r_bal, caps_bal, t_bal = api.plan_hbm_tiers(cfg, B, nb, free, bundle, host_bytes=host_budget,
+                                                    weights_streamed=not weights_on_device)
     except api.CapacityError as e:  # e.g. OPT-66B: 130 GB of weights leave too little HBM for this cache
         eng.close()
         return {"workload": f"{cfg.name}-shape, batch {B}, prompt {P}: weights + cache in HBM",
@@ -1114,8 +1125,11 @@ def resident_variants(local, cfg, B, P, arch, steps=2, warmup=1, reserve=3e9, on
                 "cache_gb": {"all_kv": N * kv_all / 1e9, "all_act": N * act_all / 1e9}}
     ids = [f"h{i}" for i in range(B)]
     tokens = np.random.default_rng(9).integers(0, cfg.vocab_size, (total, B)).astype(np.int32)
-    out = {"workload": f"{cfg.name}-shape, batch {B}, prompt {P}: weights + cache in HBM (KV and ACT placed on "
-                       "the GPU first); overflow blocks in pinned host memory",
+    out = {"workload": (f"{cfg.name}-shape, batch {B}, context {P}: " +
+                        ("weights + cache in HBM" if weights_on_device else
+                         "weights streamed from pinned host every layer, cache in HBM") +
+                        " (KV and ACT placed on the GPU first); overflow blocks in pinned host memory"),
+           "weights": "HBM" if weights_on_device else "pinned host, streamed per layer",
            "free_hbm_gb": free / 1e9, "host_budget_gb": host_budget / 1e9, "blocks": N, "r_fit": r_fit, "r_planned": r_bal,
            "planned_tiers": {"act_gpu": caps_bal.act_gpu, "kv_gpu": caps_bal.kv_gpu, "kv_host": caps_bal.kv_host,
                              "act_host": caps_bal.act_host, "predicted_t_comp_ms_per_layer": t_bal[0] * 1e3,
@@ -1181,7 +1195,8 @@ def resident_variants(local, cfg, B, P, arch, steps=2, warmup=1, reserve=3e9, on
                 slope = prof["recompute_ms"] / 1e3 / prof["recompute_rows"]
                 b2 = api.TimingBundle(api.LinearTimeModel(slope, 0.0, 1.0, False), bundle.t_load_kv,
                                       bundle.t_load_w, bundle.s_weight_layer, bundle.s_weight_total)
-                r2, caps2, t2 = api.plan_hbm_tiers(cfg, B, nb, free, b2, host_bytes=host_budget)
+                r2, caps2, t2 = api.plan_hbm_tiers(cfg, B, nb, free, b2, host_bytes=host_budget,
+                                                   weights_streamed=not weights_on_device)
                 out["replanned"] = {"insitu_kv_gen_slope": slope, "r": r2,
                                     "tiers": {"act_gpu": caps2.act_gpu, "kv_gpu": caps2.kv_gpu,
                                               "kv_host": caps2.kv_host, "act_host": caps2.act_host},

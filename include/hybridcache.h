@@ -98,10 +98,11 @@ int hc_plan_hbm_residency(const hc_model_config* cfg, long requests, long blocks
                           double* out_share, long* out4);
 /* Balanced three tiers (ACT in HBM, KV in HBM, KV streamed from pinned host)
  * minimising max(t_kv_gen, t_load_kv) per layer from a measured bundle5;
- * host_bytes bounds the pinned host tiers (0 = unbounded); out4 as above,
- * out_times2 = predicted per-layer {t_comp, t_link} seconds. */
+ * host_bytes bounds the pinned host tiers (0 = unbounded); weights_streamed:
+ * the link also carries t_load_w per layer (weights left in pinned host);
+ * out4 as above, out_times2 = predicted per-layer {t_comp, t_link} seconds. */
 int hc_plan_hbm_tiers(const hc_model_config* cfg, long requests, long blocks_per_request, double hbm_bytes,
-                      double host_bytes, const double* bundle5, double* out_share, long* out4,
+                      double host_bytes, const double* bundle5, int weights_streamed, double* out_share, long* out4,
                       double* out_times2);
 /* bundle_from_samples (timing.cpp:172-183) from MEASURED samples; out =
  * {kv slope, kv icept, kv r2, kv clamped, load slope, load icept, load r2,

@@ -62,7 +62,7 @@ SIGNATURES = {
     "hc_alloc_remaining": (i, [dp, dp, i, l, l, lp]),
     "hc_plan_host_allocation": (i, [dp, dp, i, l, lp]),
     "hc_plan_hbm_residency": (i, [cfgp, l, l, d, dp, lp]),
-    "hc_plan_hbm_tiers": (i, [cfgp, l, l, d, d, dp, dp, lp, dp]),
+    "hc_plan_hbm_tiers": (i, [cfgp, l, l, d, d, dp, i, dp, lp, dp]),
     "hc_planned_times": (i, [dp, i, l, l, l, dp]),
     "hc_bundle_from_samples": (i, [dp, dp, i, dp, dp, i, d, cfgp, dp]),
     "hc_budget_for": (i, [d, cfgp, d, dp]),

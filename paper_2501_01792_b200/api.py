@@ -343,15 +343,17 @@ def plan_hbm_residency(cfg: ModelConfig, requests: int, blocks_per_request: int,
 
 
 def plan_hbm_tiers(cfg: ModelConfig, requests: int, blocks_per_request: int, hbm_bytes: float,
-                   bundle: TimingBundle, host_bytes: float = 0.0):
+                   bundle: TimingBundle, host_bytes: float = 0.0, weights_streamed: bool = False):
     """Balanced three-tier plan (csrc/host/plan.hpp): (r, PoolCaps, (t_comp, t_link) per layer).
-    host_bytes bounds the pinned host tiers (0 = unbounded)."""
+    host_bytes bounds the pinned host tiers (0 = unbounded); weights_streamed adds
+    the per-layer weight stream (bundle.t_load_w) to the link side."""
     c = cfg.to_c()
     b, bp = bundle.arr5()
     r = C.c_double()
     out = (C.c_long * 4)()
     t, tp = _darr(np.zeros(2))
-    check(lib().hc_plan_hbm_tiers(C.byref(c), requests, blocks_per_request, float(hbm_bytes), float(host_bytes), bp, C.byref(r), out, tp))
+    check(lib().hc_plan_hbm_tiers(C.byref(c), requests, blocks_per_request, float(hbm_bytes), float(host_bytes), bp,
+                                  int(weights_streamed), C.byref(r), out, tp))
     return r.value, PoolCaps(kv_host=out[3], kv_gpu=out[1], act_host=out[2], act_gpu=out[0]), tuple(t.tolist())
 
 

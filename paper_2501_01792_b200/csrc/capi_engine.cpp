@@ -263,11 +263,11 @@ int hc_plan_hbm_residency(const hc_model_config* cfg, long requests, long bpr, d
     });
 }
 int hc_plan_hbm_tiers(const hc_model_config* cfg, long requests, long bpr, double hbm_bytes, double host_bytes,
-                      const double* b, double* share, long* out4, double* times2) {
+                      const double* b, int weights_streamed, double* share, long* out4, double* times2) {
     return hc_guard([&] {
         ModelConfig c = to_cfg(cfg);
         c.validate();
-        const HbmTierPlan p = plan_hbm_tiers(c, requests, bpr, hbm_bytes, bundle_of(b), host_bytes);
+        const HbmTierPlan p = plan_hbm_tiers(c, requests, bpr, hbm_bytes, bundle_of(b), host_bytes, weights_streamed != 0);
         *share = p.act_share;
         const long v[4] = {p.act_gpu, p.kv_gpu, p.act_host, p.kv_host};
         std::memcpy(out4, v, sizeof v);

@@ -1574,8 +1574,13 @@ void Engine::decode_step(const std::vector<std::string>& ids_in, const int* toke
                     m.span_end(profile_, s_compute_);
                     st.launches += 1 + m.tail_launches() + (U.splits > 1 ? 2 : 1);
                 }
-                const bool external = capturing && l >= m.L - 2;  // the weight prefetch waits from outside the graph
-                HC_CUDA(cudaEventRecord(m.consumed[slot], s_compute_));
+                // events the next step / prefill waits on from outside the graph: the
+                // last two units' staging slots and the last two layers' weight slots
+                const bool external = capturing && l >= m.L - 2;
+                if (capturing && j >= m.L * M - 2)
+                    HC_CUDA(cudaEventRecordWithFlags(m.consumed[slot], s_compute_, cudaEventRecordExternal));
+                else
+                    HC_CUDA(cudaEventRecord(m.consumed[slot], s_compute_));
                 if (u == M - 1) {
                     if (external)
                         HC_CUDA(cudaEventRecordWithFlags(m.w_consumed[wslot], s_compute_, cudaEventRecordExternal));

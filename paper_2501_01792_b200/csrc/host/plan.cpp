@@ -230,7 +230,7 @@ HbmPlan plan_hbm_residency(const ModelConfig& c, long requests, long blocks_per_
 }
 
 HbmTierPlan plan_hbm_tiers(const ModelConfig& c, long requests, long blocks_per_request, double hbm_bytes,
-                           const TimingBundle& b, double host_bytes) {
+                           const TimingBundle& b, double host_bytes, bool weights_streamed) {
     if (requests < 1 || blocks_per_request < 1) throw InputError("plan_hbm_tiers: empty workload");
     if (hbm_bytes <= 0) throw InputError("plan_hbm_tiers: no device memory");
     if (host_bytes < 0) throw InputError("plan_hbm_tiers: negative host budget");
@@ -240,7 +240,8 @@ HbmTierPlan plan_hbm_tiers(const ModelConfig& c, long requests, long blocks_per_
     const double kv_all = kv_one * L, act_all = act_one * L;
     const long N = requests * blocks_per_request;
     auto t_comp = [&](long x) { return x > 0 ? eval(b.t_kv_gen, static_cast<double>(x) * tpb) : 0.0; };
-    auto t_link = [&](long z) { return z > 0 ? eval(b.t_load_kv, static_cast<double>(z) * tpb) : 0.0; };
+    const double t_w = weights_streamed ? b.t_load_w : 0.0;
+    auto t_link = [&](long z) { return t_w + (z > 0 ? eval(b.t_load_kv, static_cast<double>(z) * tpb) : 0.0); };
     HbmTierPlan best;
     double best_t = -1;
     for (long x = 0; x <= N; ++x) {

@@ -91,11 +91,15 @@ HbmPlan plan_hbm_residency(const ModelConfig& c, long requests, long blocks_per_
 // rounding of the ratio. t_comp / t_link are the predicted per-layer times.
 // host_bytes (> 0) bounds the pinned host memory of the host tiers (KV host
 // blocks, all layers, plus the ACT spill blocks); 0 = unbounded.
+// weights_streamed: the weights stay in pinned host memory and cross the link
+// every layer (hbm_bytes then excludes only their two streaming slots), so the
+// link side of the critical path is t_load_w + t_load_kv(z tpb): recompute is
+// free up to the weight stream's time, KV blocks fill the remaining HBM.
 struct HbmTierPlan : HbmPlan {
     double t_comp = 0, t_link = 0;
 };
 HbmTierPlan plan_hbm_tiers(const ModelConfig& c, long requests, long blocks_per_request, double hbm_bytes,
-                           const TimingBundle& b, double host_bytes = 0);
+                           const TimingBundle& b, double host_bytes = 0, bool weights_streamed = false);
 
 // FLOP model (flops.cpp:7-37); kinds: 0 KvGen, 1 QkvGen, 2 Attention,
 // 3 ProjFfn, 4 TokenRecomputeToLayerK, 5 FullLayer.

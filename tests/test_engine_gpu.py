@@ -1027,6 +1027,7 @@ def test_engine_minibatched_decode_matches_oracle(native, weights_on_device, gra
     eng.set_minibatching(act_max, kv_max, bundle)
     eng.prefill(ids, prompts)
     ba = O.BlockAssigner(cfg.tokens_per_block, O.HYBRID, O.HostAllocation(3, 2), act_gpu=2)
+    ba.cache = O.HybridCache(cfg.tokens_per_block, 40, 0, 40, 2)  # the engine's pools; (3, 2) is only the target
     for rid, n in zip(ids, lens):
         ba.add_request(rid, n)
         for _ in range(n):

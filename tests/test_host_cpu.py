@@ -280,7 +280,7 @@ def test_plan_hbm_residency(model, B, nb, hbm_gb):
         api.plan_hbm_residency(cfg, 0, nb, 1e9)
 
 
-def _hbm_tiers_restated(cfg, B, nb, hbm, slope_gen, slope_load, host=0.0):
+def _hbm_tiers_restated(cfg, B, nb, hbm, slope_gen, slope_load, host=0.0, t_w=0.0):
     """Python restatement of plan_hbm_tiers (csrc/host/plan.hpp), zero intercepts."""
     import math
     from paper_2501_01792_b200 import api
@@ -298,7 +298,7 @@ def _hbm_tiers_restated(cfg, B, nb, hbm, slope_gen, slope_load, host=0.0):
         slack = B if 0 < x < N else 0
         if host > 0 and (z + slack) * kv_all + slack * act_all > host:
             continue
-        t = max(slope_gen * x * tpb, slope_load * z * tpb)
+        t = max(slope_gen * x * tpb, t_w + slope_load * z * tpb)
         if best is None or t < best[0]:
             best = (t, x, max(y, 0), z)
     if best is None:
@@ -328,6 +328,26 @@ def test_plan_hbm_tiers(model, B, nb, hbm_gb, gen, load):
     elif gen < 1e-6:
         assert caps.act_gpu > 0 and caps.kv_host > B            # both channels busy ...
         assert abs(tc - tl) <= max(tc, tl) * 0.02               # ... and balanced
+
+
+@pytest.mark.parametrize("hbm_gb", [170.0, 120.0, 60.0])
+def test_plan_hbm_tiers_streamed_weights(hbm_gb):
+    """Weights left in pinned host memory (streamed every layer): the link side
+    carries t_load_w too, so recompute is free up to the weight stream's time
+    and the plan matches the restatement with that term."""
+    from paper_2501_01792_b200 import api
+    cfg = api.ModelConfig.preset("opt-30b")
+    B, nb = 128, 73
+    kv = [(1024.0, 1024 * 1.2e-7), (4096.0, 4096 * 1.2e-7)]
+    ld = [(1024.0, 1024 * 5.2e-7), (4096.0, 4096 * 5.2e-7)]
+    bundle = api.bundle_from_samples(kv, ld, 55e9, cfg)
+    r, caps, (tc, tl) = api.plan_hbm_tiers(cfg, B, nb, hbm_gb * 1e9, bundle, weights_streamed=True)
+    r2, c2 = _hbm_tiers_restated(cfg, B, nb, hbm_gb * 1e9, bundle.t_kv_gen.slope, bundle.t_load_kv.slope,
+                                 t_w=bundle.t_load_w)
+    assert r == pytest.approx(r2) and (caps.act_gpu, caps.kv_gpu, caps.act_host, caps.kv_host) == c2
+    assert tl >= bundle.t_load_w
+    r0, _, _ = api.plan_hbm_tiers(cfg, B, nb, hbm_gb * 1e9, bundle)
+    assert r >= r0 - 1e-12  # a busier link shifts blocks to recompute: never less ACT
 
 
 
