@@ -739,6 +739,58 @@ def test_engine_shared_weight_stream_matches_oracle(native, n):
         assert -full_w * 0.05 <= kv_act < full_w, (r, st["h2d_bytes"], full_w / n)  # weights ~ 1/N of a stream
 
 
+def test_engine_shared_weight_stream_uneven_and_failing_ranks(native):
+    """Ranks sharing a weight stream issue the same collectives every step even
+    when their own work differs: a rank with an empty batch still streams and
+    gathers every layer, a rank admitting requests in between (prefill) keeps
+    the sequence, and a step one rank rejects (bad token id) fails on every
+    rank before the first all-gather — after which all ranks keep decoding."""
+    from paper_2501_01792_b200 import InputError
+    from paper_2501_01792_b200.api import HostAllocation, PoolCaps, TensorParallel
+    cfg = small_cfg(L=3, d=256, H=2, f=512, tpb=8)
+    w = oracle_weights(cfg)
+    group = TensorParallel.local_group(2)
+    kw = dict(max_batch=2, caps=PoolCaps(kv_host=16, act_host=16, act_gpu=1), allocation=HostAllocation(1, 1),
+              mode="hybrid", weights_on_device=False)
+    engs = [make_engine(cfg, w, weight_share=group[r], **kw) for r in range(2)]
+    rng = np.random.default_rng(5)
+    prompt = rng.integers(0, cfg.vocab_size, 13).tolist()
+
+    def rank_fn(r):
+        def run():
+            e, got, errs = engs[r], [], []
+            if r == 0:
+                e.prefill(["a"], [prompt])
+            for step in range(4):
+                if r == 1 and step == 2:
+                    e.prefill(["b"], [prompt])  # admits between steps: no collectives, sequence intact
+                ids = ["a"] if r == 0 else (["b"] if step >= 2 else [])
+                toks = [7] if ids else []
+                if step == 1:
+                    toks = [7] if r == 0 else []
+                    if r == 0:
+                        toks = [cfg.vocab_size + 5]  # rank 0 rejects this step ...
+                try:
+                    got.append(e.decode_step(ids, toks, want_x=True)["x"].copy() if ids else None)
+                except InputError as ex:
+                    errs.append((step, str(ex)))
+            return got, errs
+        return run
+
+    outs = _run_ranks([rank_fn(r) for r in range(2)])
+    for r in range(2):
+        assert [s for s, _ in outs[r][1]] == [1], outs[r][1]  # ... and every rank raised at step 1
+    assert "token id out of range" in outs[0][1][0][1] and "rejected" in outs[1][1][0][1]
+    seq = list(prompt)
+    for x in outs[0][0]:
+        seq.append(7)
+        assert rel(f64(x[0]), O.forward_prompt(seq, w).output[-1]) <= TOL
+    seq = list(prompt)
+    for x in outs[1][0][2:]:
+        seq.append(7)
+        assert rel(f64(x[0]), O.forward_prompt(seq, w).output[-1]) <= TOL
+
+
 def test_engine_shared_weight_stream_rejects_tp_and_resident(native):
     from paper_2501_01792_b200 import ConfigError
     from paper_2501_01792_b200.api import TensorParallel
