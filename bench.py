@@ -35,6 +35,10 @@ METRIC = "generated tokens/sec, OPT-30B offloaded, per KV:ACT ratio, at 1/2/4/8 
 # all-gather bus bandwidth measured on B200 NVSwitch nodes (725 GB/s;
 # /opt/skills/guides/B200_PROFILING.md; peer copies reach 770 GB/s per direction)
 NVLINK_BUSBW = 725e9
+# best host->device rate of the standalone link probe on this pool's B200 boxes
+# (scripts/link_probe.py -> profiles/r01_link_probe.json: one copy stream,
+# >= 64 MB chunks; more streams or SM zero-copy reads add nothing)
+LINK_PROBE_GBS = 55.59
 
 
 def parse():
@@ -870,6 +874,11 @@ def our_arm(args, cfg, world, rank, local, dist):
                  "roofline_tokens_per_s_per_gpu": B / t_roof if t_roof else None,
                  "frac": (t_roof * 1e3) / ms_per_step if ms_per_step else None,
                  "link_peak_gbs": link_gbs, "link_peak_source": "measured: pinned H2D cudaMemcpyAsync on this box",
+                 # the same step against independent link ceilings: the standalone probe's best
+                 # (1-4 copy streams, 8-256 MB chunks, SM zero-copy; profiles/r01_link_probe.json)
+                 # and PCIe Gen5 x16's nominal 64 GB/s per direction
+                 "frac_vs_probe_ceiling": (h2d_step / (LINK_PROBE_GBS * 1e9)) / (ms_per_step / 1e3),
+                 "frac_vs_pcie5_nominal": (h2d_step / 64e9) / (ms_per_step / 1e3),
                  "achieved_link_gbs": h2d_step / (ms_per_step / 1e3) / 1e9,
                  "copy_stream_gbs": prof["h2d_bytes"] / (prof["copy_ms"] / 1e3) / 1e9 if prof["copy_ms"] else None,
                  "profile_split_ms": {"recompute": prof["recompute_ms"], "attention": prof["attn_ms"],
@@ -1336,10 +1345,11 @@ def full_generation(args, cfg, local):
     bind_numa(local)
     B, P, G, L = args.batch or 128, args.prompt, args.gen, cfg.num_layers
     bp = bundle_path(args)
+    alloc6 = None
     if args.ratio >= 0:
         r, src = args.ratio, "--ratio"
     else:
-        r, factor, _ = planned_ratio(read_bundle(bp), cfg, B * (P + G),
+        r, factor, alloc6 = planned_ratio(read_bundle(bp), cfg, B * (P + G),
                                      lambda b5, m4, tpb, ag: list(api.plan_host_allocation(
                                          api.TimingBundle(api.LinearTimeModel(b5[0], b5[1]),
                                                           api.LinearTimeModel(b5[2], b5[3]), b5[4]),
@@ -1362,22 +1372,41 @@ def full_generation(args, cfg, local):
     eng.prefill(ids, [p[:-1] for p in prompts])  # the last prompt token is the first decode step's input
     eng.set_profile(False)
     prefill_s = eng.last_stats()["step_ms"] / 1e3
+    pre = eng.last_stats()
     out = {"argmax": np.zeros(B, np.int32)}
     toks = [p[-1] for p in prompts]
-    step_ms = []
+    step_ms, traffic = [], {k: pre[k] for k in ("h2d_weights", "h2d_kv", "h2d_act", "d2h_kv", "d2h_act")}
+    busy = []  # (compute busy, copy busy) fractions of the profiled steps
+    trace = None
     clocks = ClockSampler(local)
     clocks.start()
     for g in range(G):
+        prof = g % 32 == 16  # every 32nd step profiled (CUDA events per kernel, eager)
+        eng.set_profile(prof)
         eng.decode_step(ids, toks, want_x=False, want_argmax=True, out=out)
-        step_ms.append(eng.last_stats()["step_ms"])
+        st = eng.last_stats()
+        step_ms.append(st["step_ms"])
+        for k in traffic:
+            traffic[k] += st[k]
+        if prof:
+            busy.append(((st["recompute_ms"] + st["attn_ms"] + st["gemm_ms"]) / st["step_ms"],
+                         st["copy_ms"] / st["step_ms"]))
+            if trace is None:
+                trace = eng.trace()
         toks = out["argmax"].tolist()
+    eng.set_profile(False)
     wall = time.perf_counter() - w0
     clk = clocks.stop()
     eng.close()
     dec_s = sum(step_ms) / 1e3
-    print(json.dumps({
+    makespan = prefill_s + dec_s
+    gpu_dec = statistics.mean(b for b, _ in busy) if busy else None
+    pcie_dec = statistics.mean(c for _, c in busy) if busy else None
+    pre_busy = (pre["gemm_ms"] + pre["attn_ms"]) / pre["step_ms"] if pre["step_ms"] else 0.0
+    pre_copy = pre["copy_ms"] / pre["step_ms"] if pre["step_ms"] else 0.0
+    res = {
         "metric": METRIC + " [whole generation: prefill + G greedy decode steps, every step timed]",
-        "value": B * G / (prefill_s + dec_s), "unit": "tokens/s", "n_gpus": 1, "dtype": "f16",
+        "value": B * G / makespan, "unit": "tokens/s", "n_gpus": 1, "dtype": "f16",
         "config": {"workload": f"{cfg.name}, batch {B}, prompt {P}, gen {G}, weights + cache in pinned host",
                    "act_share_r": r, "ratio_source": src, "mode": mode, "host_layers_phys": Lp,
                    "weight_layers_phys": Lw},
@@ -1385,7 +1414,45 @@ def full_generation(args, cfg, local):
         "wall_s": wall, "e2e_tokens_per_s": B * G / wall,
         "step_ms": {"first": step_ms[0], "mid": step_ms[len(step_ms) // 2], "last": step_ms[-1],
                     "mean": statistics.mean(step_ms), "all": [round(x, 3) for x in step_ms]},
-        "clocks": clk}), flush=True)
+        "clocks": clk}
+    if args.artifacts:
+        # the reference CLI's metrics.json (main.cpp:101-115, 255-261) for the MEASURED run:
+        # busy fractions from the profiled steps (every 32nd) and the profiled prefill
+        tb = {"weights": traffic["h2d_weights"], "kv_load": traffic["h2d_kv"], "act_load": traffic["h2d_act"],
+              "kv_store": traffic["d2h_kv"], "act_store": traffic["d2h_act"]}
+        tot = sum(tb.values())
+        metrics = {"tokens_generated": B * G, "makespan_s": makespan, "throughput_tok_s": B * G / makespan,
+                   "pcie_busy": (pre_copy * prefill_s + (pcie_dec or 0.0) * dec_s) / makespan,
+                   "gpu_busy": (pre_busy * prefill_s + (gpu_dec or 0.0) * dec_s) / makespan,
+                   "prefill_s": prefill_s, "gen_s": dec_s, "traffic": {k: int(v) for k, v in tb.items()},
+                   "mode": mode, "batch": B, "prompt_len": P, "gen_len": G,
+                   "traffic_report": dict({k: int(v) for k, v in tb.items()}, total=int(tot),
+                                          context_load=int(tb["kv_load"] + tb["act_load"]),
+                                          **{f"frac_{k}": v / tot for k, v in tb.items()}),
+                   "measured_on": "B200, bench.py --full-generation (every step timed)",
+                   "meta": {"version": "b200-measured", "seed": 42, "inputs": {}}}
+        os.makedirs(args.artifacts, exist_ok=True)
+        with open(os.path.join(args.artifacts, "metrics.json"), "w") as fh:
+            json.dump(metrics, fh, indent=2)
+        if trace is not None:
+            trace["meta"] = metrics["meta"]
+            with open(os.path.join(args.artifacts, "trace.json"), "w") as fh:
+                json.dump(trace, fh)
+        if bp and alloc6:  # the bundle the ratio came from and the plan Alg. 1 made of it
+            import shutil
+            shutil.copy(bp, os.path.join(args.artifacts, "bundle.json"))
+            b7 = read_bundle(bp)
+            tb5 = api.TimingBundle(api.LinearTimeModel(b7[0], b7[1]), api.LinearTimeModel(b7[2], b7[3]), b7[4])
+            ha = api.HostAllocation(*alloc6)
+            plan = dict(ha.__dict__, predicted={"t_pcie": api.planned_t_pcie(tb5, cfg.tokens_per_block, ha),
+                                                "t_computation": api.planned_t_computation(tb5, cfg.tokens_per_block,
+                                                                                           ha, 0)},
+                        meta=metrics["meta"])
+            with open(os.path.join(args.artifacts, "plan.json"), "w") as fh:
+                json.dump(plan, fh, indent=2)
+        res["artifacts"] = {"dir": args.artifacts, "metrics": {k: metrics[k] for k in
+                                                               ("pcie_busy", "gpu_busy", "prefill_s", "gen_s")}}
+    print(json.dumps(res), flush=True)
 
 
 def main():

@@ -233,10 +233,11 @@ int hc_engine_read_weights(void* engine, int layer, uint16_t* out);  /* -3: fina
 int hc_engine_capture_inputs(void* engine, int on);
 /* Decode-time layer inputs of the last step, [L][n][d] f16 (n = last batch). */
 int hc_engine_captured_inputs(void* engine, uint16_t* out, long count);
-/* out12 = {step_ms, h2d_bytes, d2h_bytes, recompute_rows, recompute_ms, attn_ms, gemm_ms, launches,
- *          copy_ms, recompute_launches, store_ms, minibatches} of the last decode step or prefill;
- *          the *_ms splits need hc_engine_set_profile(1). */
-int hc_engine_last_stats(void* engine, double* out12);
+/* out17 = {step_ms, h2d_bytes, d2h_bytes, recompute_rows, recompute_ms, attn_ms, gemm_ms, launches,
+ *          copy_ms, recompute_launches, store_ms, minibatches, h2d_weights, h2d_kv, h2d_act, d2h_kv,
+ *          d2h_act} of the last decode step or prefill (bytes by the reference's traffic classes,
+ *          sim.hpp:60-66); the *_ms splits need hc_engine_set_profile(1). */
+int hc_engine_last_stats(void* engine, double* out17);
 /* Per-kernel CUDA-event timing of the next steps (small overhead). */
 int hc_engine_set_profile(void* engine, int on);
 /* Replay decode steps as CUDA graphs keyed by their launch structure (default on,

@@ -750,10 +750,11 @@ class Engine:
         return out
 
     def last_stats(self) -> dict:
-        out, op = _darr(np.zeros(12))
+        out, op = _darr(np.zeros(17))
         check(lib().hc_engine_last_stats(self._h, op))
         keys = ("step_ms", "h2d_bytes", "d2h_bytes", "recompute_rows", "recompute_ms", "attn_ms", "gemm_ms",
-                "launches", "copy_ms", "recompute_launches", "store_ms", "minibatches")
+                "launches", "copy_ms", "recompute_launches", "store_ms", "minibatches", "h2d_weights", "h2d_kv",
+                "h2d_act", "d2h_kv", "d2h_act")
         return dict(zip(keys, out.tolist()))
 
     def set_profile(self, on: bool = True) -> None:

@@ -527,10 +527,11 @@ int hc_engine_captured_inputs(void* e, uint16_t* out, long count) {
 int hc_engine_last_stats(void* e, double* o) {
     return hc_guard([&] {
         const StepStats& s = eng(e)->last_stats();
-        const double v[12] = {s.step_ms, s.h2d_bytes, s.d2h_bytes, s.recompute_tokens, s.recompute_ms,
+        const double v[17] = {s.step_ms, s.h2d_bytes, s.d2h_bytes, s.recompute_tokens, s.recompute_ms,
                               s.attn_ms, s.gemm_ms, static_cast<double>(s.launches), s.copy_ms,
                               static_cast<double>(s.recompute_launches), s.store_ms,
-                              static_cast<double>(s.minibatches)};
+                              static_cast<double>(s.minibatches), s.h2d_weights, s.h2d_kv, s.h2d_act,
+                              s.d2h_kv, s.d2h_act};
         std::memcpy(o, v, sizeof v);
     });
 }

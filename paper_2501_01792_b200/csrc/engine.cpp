@@ -865,6 +865,7 @@ void Engine::prefill(const std::vector<std::string>& ids, const std::vector<std:
     };
     std::vector<Chunk> chunks;
     std::vector<int> tokens, positions, a_src, a_n, a_ref, acth, kvh;
+    long direct_act = 0, direct_kv = 0;  // host blocks written through mapped stores (mini-batched staging)
     try {  // none of ids existed before this call (checked above): on failure all are released again
     for (size_t r = 0; r < ids.size(); ++r) {
         const int P = static_cast<int>(prompts[r].size());
@@ -892,8 +893,10 @@ void Engine::prefill(const std::vector<std::string>& ids, const std::vector<std:
                     a_n.push_back(e.filled_tokens);
                     if (gpu)
                         a_ref.push_back(pack_ref(R_ACT_GPU, e.pbn));
-                    else if (m.mb_on)  // staging smaller than the pool: straight into the mapped pool
+                    else if (m.mb_on) {  // staging smaller than the pool: straight into the mapped pool
                         a_ref.push_back(pack_ref(R_ACT_HOST, e.pbn / m.tpn));
+                        direct_act += 1;
+                    }
                     else
                         a_ref.push_back(pack_ref(R_ACT_STAGE, m.act_pos(e.pbn)));
                     if (!gpu && !m.mb_on) acth.push_back(e.pbn / m.tpn);
@@ -902,6 +905,7 @@ void Engine::prefill(const std::vector<std::string>& ids, const std::vector<std:
                 c.k_src.push_back(row - c.row0);
                 c.k_n.push_back(e.filled_tokens);
                 c.k_ref.push_back(pack_ref(gpu ? R_KV_GPU : (m.mb_on ? R_KV_HOST : R_KV_STAGE), e.pbn));
+                if (!gpu && m.mb_on) direct_kv += 1;
                 if (!gpu && !m.mb_on) kvh.push_back(e.pbn);
             }
             row += e.filled_tokens;
@@ -959,6 +963,7 @@ void Engine::prefill(const std::vector<std::string>& ids, const std::vector<std:
                                     cudaMemcpyHostToDevice, s_copy_));
             m.span_end(profile_, s_copy_);
             st.h2d_bytes += m.LE * 2.0;
+            st.h2d_weights += m.LE * 2.0;
             HC_CUDA(cudaEventRecord(m.loaded[slot], s_copy_));
             HC_CUDA(cudaStreamWaitEvent(s_compute_, m.loaded[slot]));
         }
@@ -1023,6 +1028,7 @@ void Engine::prefill(const std::vector<std::string>& ids, const std::vector<std:
                                         own + static_cast<size_t>(r.start) * m.actb, bytes, cudaMemcpyDeviceToHost,
                                         s_store_));
                 st.d2h_bytes += bytes;
+                st.d2h_act += bytes;
             }
             for (const Run& r : kv_runs) {
                 const size_t bytes = static_cast<size_t>(r.count) * m.kvb * 2;
@@ -1030,6 +1036,7 @@ void Engine::prefill(const std::vector<std::string>& ids, const std::vector<std:
                                         m.kv_stage[slot] + static_cast<size_t>(r.start) * m.kvb, bytes,
                                         cudaMemcpyDeviceToHost, s_store_));
                 st.d2h_bytes += bytes;
+                st.d2h_kv += bytes;
             }
             m.span_end(profile_, s_store_);
             HC_CUDA(cudaEventRecord(m.stored[slot], s_store_));
@@ -1045,6 +1052,9 @@ void Engine::prefill(const std::vector<std::string>& ids, const std::vector<std:
     float ms = 0;
     HC_CUDA(cudaEventElapsedTime(&ms, m.ev0, m.ev1));
     st.step_ms = ms;
+    st.d2h_act += static_cast<double>(direct_act) * m.actb * 2 * m.L;
+    st.d2h_kv += static_cast<double>(direct_kv) * m.kvb * 2 * m.L;
+    st.d2h_bytes += static_cast<double>(direct_act) * m.actb * 2 * m.L + static_cast<double>(direct_kv) * m.kvb * 2 * m.L;
     for (const auto& sp : m.spans) {
         float t = 0;
         HC_CUDA(cudaEventElapsedTime(&t, sp.a, sp.b));
@@ -1366,6 +1376,7 @@ void Engine::decode_step(const std::vector<std::string>& ids_in, const int* toke
         if (m.wsn == 1) {
             HC_CUDA(cudaMemcpyAsync(m.wbuf[slot], src, m.LE * 2, cudaMemcpyHostToDevice, s_copy_));
             st.h2d_bytes += m.LE * 2.0;
+            st.h2d_weights += m.LE * 2.0;
             return;
         }
         const size_t s0 = static_cast<size_t>(m.wsr) * m.wsS;
@@ -1373,6 +1384,7 @@ void Engine::decode_step(const std::vector<std::string>& ids_in, const int* toke
         if (cnt)
             HC_CUDA(cudaMemcpyAsync(m.wbuf[slot] + s0, src + s0, cnt * 2, cudaMemcpyHostToDevice, s_copy_));
         st.h2d_bytes += cnt * 2.0;
+        st.h2d_weights += cnt * 2.0;
         HC_CUDA(cudaEventRecord(m.w_h2d[slot], s_copy_));
         HC_CUDA(cudaStreamWaitEvent(s_gather_, m.w_h2d[slot]));
         m.ws->copy_channel()->all_gather(m.wbuf[slot] + s0, m.wbuf[slot], m.wsS, s_gather_);
@@ -1424,6 +1436,7 @@ void Engine::decode_step(const std::vector<std::string>& ids_in, const int* toke
                                                 m.act_host + (lp * m.act_cap_n + r.start) * m.actb, bytes,
                                                 cudaMemcpyHostToDevice, s_copy_));
                         st.h2d_bytes += bytes;
+                        st.h2d_act += bytes;
                     }
                     // every rank streamed its 1/tpn of the ACT blocks; an NVLink all-gather
                     // on the gather stream completes the staging (the recompute needs all
@@ -1443,6 +1456,7 @@ void Engine::decode_step(const std::vector<std::string>& ids_in, const int* toke
                                                 m.kv_host + (lp * m.kv_host_cap + r.start) * m.kvb, bytes,
                                                 cudaMemcpyHostToDevice, s_copy_));
                         st.h2d_bytes += bytes;
+                        st.h2d_kv += bytes;
                     }
                     m.span_end(profile_, s_copy_);
                     HC_CUDA(cudaEventRecord(m.loaded[slot], s_copy_));
@@ -1761,8 +1775,14 @@ void Engine::decode_step(const std::vector<std::string>& ids_in, const int* toke
         }
     }
     for (int b = 0; b < n; ++b) {
-        if (act_host[b] >= 0) st.d2h_bytes += static_cast<double>(m.d) * 2 * m.L;
-        if (kv_host[b] >= 0) st.d2h_bytes += static_cast<double>(m.dg) * 4 * m.L;
+        if (act_host[b] >= 0) {
+            st.d2h_bytes += static_cast<double>(m.d) * 2 * m.L;
+            st.d2h_act += static_cast<double>(m.d) * 2 * m.L;
+        }
+        if (kv_host[b] >= 0) {
+            st.d2h_bytes += static_cast<double>(m.dg) * 4 * m.L;
+            st.d2h_kv += static_cast<double>(m.dg) * 4 * m.L;
+        }
     }
     stats_ = st;
 }

@@ -76,6 +76,8 @@ struct StepStats {
     int recompute_launches = 0;
     double store_ms = 0;          // summed store-stream (D2H) time (profiled prefill)
     int minibatches = 1;          // (layer, mini-batch) units per layer of the last decode step
+    // the h2d / d2h bytes by kind (the reference's traffic classes, sim.hpp:60-66)
+    double h2d_weights = 0, h2d_kv = 0, h2d_act = 0, d2h_kv = 0, d2h_act = 0;
 };
 
 class Engine {
