@@ -35,6 +35,11 @@ METRIC = "generated tokens/sec, OPT-30B offloaded, per KV:ACT ratio, at 1/2/4/8 
 # all-gather bus bandwidth measured on B200 NVSwitch nodes (725 GB/s;
 # /opt/skills/guides/B200_PROFILING.md; peer copies reach 770 GB/s per direction)
 NVLINK_BUSBW = 725e9
+# recompute GEMM DRAM bytes per ACT row from ncu captures at OPT-30B width (scaled by rows in
+# the bench's roofline.traffic); kKvPaged: profiles/r02_ncu_recompute.txt (18.17 GB / 122880)
+RECOMPUTE_NCU_BYTES_PER_ROW = 18.17e9 / 122880
+RECOMPUTE_NCU_BYTES_PER_ROW_FUSED = 18.17e9 / 122880
+RECOMPUTE_NCU_NOTE = "kKvPaged 18.17 GB at 122880 rows, profiles/r02_ncu_recompute.txt"
 # best host->device rate of the standalone link probe on this pool's B200 boxes
 # (scripts/link_probe.py -> profiles/r01_link_probe.json: one copy stream,
 # >= 64 MB chunks; more streams or SM zero-copy reads add nothing)
@@ -544,7 +549,7 @@ def _np_default(o):
     return o.item() if hasattr(o, "item") else str(o)
 
 
-def write_artifacts(out_dir, eng, cfg, ids, planner, prof, mode, r):
+def write_artifacts(out_dir, eng, cfg, ids, planner, prof, mode, r, prefill=None):
     """The reference CLI's artifacts from MEASURED B200 data, in its schemas
     (main.cpp:75-115, 146-166, 255-275; timing.cpp:147-153; plan.cpp:22-28):
     the unmodified `hybridsim plan --bundle` / `simulate --plan` can consume them."""
@@ -585,11 +590,17 @@ def write_artifacts(out_dir, eng, cfg, ids, planner, prof, mode, r):
                 act_host_blocks += 1
     w_layer, _ = api.weight_bytes(cfg)
     step_s = prof["step_ms"] / 1e3
+    busy = (prof["recompute_ms"] + prof["attn_ms"] + prof["gemm_ms"]) / prof["step_ms"]
     metrics = {"tokens_generated": len(ids), "makespan_s": step_s, "throughput_tok_s": len(ids) / step_s,
-               "pcie_busy": prof["copy_ms"] / prof["step_ms"], "gpu_busy": None, "prefill_s": 0.0, "gen_s": step_s,
+               "pcie_busy": prof["copy_ms"] / prof["step_ms"], "gpu_busy": min(busy, 1.0),
+               "prefill_s": prefill["prefill_s"] if prefill else 0.0, "gen_s": step_s,
                "traffic": {"weights": w_layer * L, "kv_load": kv_blocks * kvb * L, "act_load": act_host_blocks * actb * L,
-                           "kv_store": None, "act_store": None},
-               "mode": mode, "act_share_r": r, "batch": len(ids), "measured_on": "B200 (one profiled decode step)",
+                           # the new token's cache rows, stored by mapped writes from the append kernels
+                           "kv_store": prof["d2h_kv"], "act_store": prof["d2h_act"]},
+               "mode": mode, "act_share_r": r, "batch": len(ids),
+               "measured_on": "B200: one profiled decode step at the mean context (prefill_s: the measured prefill "
+                              "of the same run, not part of makespan_s; the whole generation is "
+                              "metrics_full_generation.json)",
                "meta": meta}
     with open(os.path.join(out_dir, "metrics.json"), "w") as fh:
         json.dump(metrics, fh, indent=2, default=_np_default)
@@ -817,7 +828,7 @@ def our_arm(args, cfg, world, rank, local, dist):
     prof = run_steps(eng, ids, tokens, args.warmup, 1, prof=True)["last"]
     act_tokens = act_context_tokens(eng, ids)
     if args.artifacts and rank == 0:
-        write_artifacts(args.artifacts, eng, cfg, ids, planner, prof, mode, r)
+        write_artifacts(args.artifacts, eng, cfg, ids, planner, prof, mode, r, prefill)
 
     clocks = ClockSampler(local)
     barrier(dist)
@@ -844,15 +855,21 @@ def our_arm(args, cfg, world, rank, local, dist):
     rec_flops = 4.0 * d * d * act_tokens / max(prof["recompute_launches"] / L, 1)
     rec_rows = act_tokens / max(prof["recompute_launches"] / L, 1)  # ACT rows per launch
     achieved = rec_flops / (rec_launch_ms / 1e3) / 1e12 if rec_launch_ms > 0 else 0.0
-    roof = {"kernel": "gemm_tn_kernel<256,kKvPaged> (ACT->K|V recompute)", "bound": "tensor",
+    fused = eng.fused_recompute()
+    if fused:  # recompute fused with the attention: partial records instead of K|V
+        rec_kernel = "gemm_tn_kernel<256,kAttnPart> (ACT->K|V recompute fused with decode attention)"
+        rec_alg = rec_rows * d * 2 + 2 * d * d * 2 + rec_rows / tpb * cfg.num_heads * (cfg.head_dim + 4) * 4
+        rec_alg_note = "A + [Wk|Wv] read once, one partial record per block and head written"
+    else:
+        rec_kernel = "gemm_tn_kernel<256,kKvPaged> (ACT->K|V recompute)"
+        rec_alg = rec_rows * (3 * d * 2) + 2 * d * d * 2
+        rec_alg_note = "A + [Wk|Wv] read once, K|V written once"
+    roof = {"kernel": rec_kernel, "bound": "tensor",
             "achieved": achieved, "peak": tflops_sust, "unit": "TFLOP/s",
             "frac": achieved / tflops_sust if tflops_sust else None,
-            "traffic": rec_rows * 1.525e5,
-            "traffic_note": ("ncu dram__bytes_read+write per launch scaled by ACT rows: 18.73e9 B at 122880 rows "
-                             "(1.525e5 B/row, OPT-30B width; profiles/r01_ncu_recompute.csv). Algorithmic "
-                             f"{rec_rows * (3 * d * 2) + 2 * d * d * 2:.3e} B (A + [Wk|Wv] read once, K|V written "
-                             "once); the excess is [Wk|Wv] (205 MB > the 126 MB L2) re-read once per 16-tile M "
-                             "group — the L2-capacity floor for this shape, DESIGN.md §3"),
+            "traffic": rec_rows * (RECOMPUTE_NCU_BYTES_PER_ROW_FUSED if fused else RECOMPUTE_NCU_BYTES_PER_ROW),
+            "traffic_note": (f"ncu dram__bytes_read+write per launch scaled by ACT rows ({RECOMPUTE_NCU_NOTE}); "
+                             f"algorithmic {rec_alg:.3e} B ({rec_alg_note}). DESIGN.md §3"),
             "peak_source": f"{peak_src} bf16_tflops_sustained (MEASURED_PEAKS.json); burst {tflops_burst}",
             "frac_vs_burst": achieved / tflops_burst if tflops_burst else None,
             "frac_note": ("the kernel is timed inside a long step, so the peak is the sustained figure (cuBLAS "
@@ -864,7 +881,11 @@ def our_arm(args, cfg, world, rank, local, dist):
     ctx = c0 + (args.steps - 1) / 2.0
     # (a head-sharded rank does 1/N of the FLOPs and HBM traffic)
     tensor_flops = L * (4.0 * d * d * act_tokens + 2.0 * B * (4 * d * d + 2 * d * cfg.ffn_dim)) / tpn
-    hbm_bytes = L * (B * (ctx + 1) * 2 * d * 2 + act_tokens * 3 * d * 2 + w_layer) / tpn + h2d_step
+    # HBM: KV-cached context read by the attention, ACT rows read by the recompute (+ K|V written
+    # and read back unless the recompute is fused with the attention), the layer weights
+    kv_ctx_tokens = max(B * (ctx + 1) - act_tokens, 0.0)
+    hbm_bytes = L * (kv_ctx_tokens * 2 * d * 2 + act_tokens * (d * 2 if fused else 5 * d * 2) + w_layer) / tpn \
+        + h2d_step
     t_link = h2d_step / (link_gbs * 1e9) if link_gbs else 0.0
     t_tensor = tensor_flops / (tflops_sust * 1e12)
     t_hbm = hbm_bytes / (hbm_peak * 1e9)
