@@ -1335,6 +1335,7 @@ def config2_resident(local, B=64, P=512, steps=3, warmup=2):
     run_steps(eng, ids, tokens, 0, warmup)
     prof = run_steps(eng, ids, tokens, warmup, 1, prof=True)["last"]
     act = act_context_tokens(eng, ids)
+    fused = eng.fused_recompute()
     acc = run_steps(eng, ids, tokens, warmup + 1, steps)
     eng.close()
     ms = acc["dev_ms"] / steps
@@ -1342,7 +1343,9 @@ def config2_resident(local, B=64, P=512, steps=3, warmup=2):
     rec_tflops = 4.0 * d * d * act / (rec_ms / 1e3) / 1e12 if rec_ms else None
     flops = L * (4.0 * d * d * act + 2.0 * B * (4 * d * d + 2 * d * f))
     ctx = P + warmup + 2
-    hbm = L * (B * (ctx + 1) * 2 * d * 2 + act * 3 * d * 2 + (4 * d * d + 2 * d * f) * 2)
+    # ACT rows read by the recompute (+ its K|V written and read back by the attention
+    # unless the recompute is fused with it) and the layer weights
+    hbm = L * (act * (d * 2 if fused else 5 * d * 2) + (4 * d * d + 2 * d * f) * 2)
     t_roof = max(flops / (tflops_sust * 1e12), hbm / (hbm_peak * 1e9))
     return {"workload": "opt-6.7b-shape, batch 64, prompt 512, ACT-only cache + weights resident in HBM",
             "tokens_per_s": B * 1e3 / ms, "ms_per_step": ms, "e2e_tokens_per_s": B * steps / acc["wall"],
@@ -1352,7 +1355,8 @@ def config2_resident(local, B=64, P=512, steps=3, warmup=2):
                               "roofline_tokens_per_s": B / t_roof},
             "profile_split_ms": {"recompute": prof["recompute_ms"], "attention": prof["attn_ms"],
                                  "qkv_proj_ffn": prof["gemm_ms"]},
-            "act_context_tokens": act, "launches_per_step": acc["launches"] / steps}
+            "act_context_tokens": act, "recompute_rows": prof["recompute_rows"],
+            "recompute_fused_with_attention": fused, "launches_per_step": acc["launches"] / steps}
 
 
 def full_generation(args, cfg, local):

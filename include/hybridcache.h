@@ -201,6 +201,13 @@ int hc_engine_admit_synthetic(void* engine, int n, const char* const* ids, const
  * slope, intercept, load_kv slope, intercept, t_load_w}, and run as (layer,
  * mini-batch) units. act_max = kv_max = 0: whole-batch steps. */
 int hc_engine_set_minibatching(void* engine, long act_max, long kv_max, const double* bundle5);
+/* Recompute fused with decode attention (default on when the heads' width is a
+ * multiple of 128): the recompute GEMM (recompute_kv_from_activation,
+ * decoder.cpp:123-129) reduces each recomputed block to flash-decoding partials
+ * against the step's queries (attention_row, decoder.cpp:15-43) instead of
+ * storing K|V in the paged layout. on = 0: K|V written (kKvPaged) and read back
+ * by the attention; on < 0: query only. *active (may be NULL) = the path now in use. */
+int hc_engine_set_fused_recompute(void* engine, int on, int* active);
 /* Pattern-fill every pool slot (benchmark setup, before a real prefill). */
 int hc_engine_fill_pools(void* engine, uint64_t seed);
 /* Grow each request by n_tokens through the allocator in decode order

@@ -88,6 +88,7 @@ SIGNATURES = {
     "hc_engine_admit_synthetic": (i, [vp, i, cpp, ip, u64]),
     "hc_engine_fill_pools": (i, [vp, u64]),
     "hc_engine_set_minibatching": (i, [vp, l, l, dp]),
+    "hc_engine_set_fused_recompute": (i, [vp, i, ip]),
     "hc_engine_advance_synthetic": (i, [vp, i, cpp, i]),
     "hc_engine_decode_step": (i, [vp, i, cpp, ip, u16p, fp, ip]),
     "hc_engine_free_request": (i, [vp, cp]),

@@ -639,6 +639,20 @@ class Engine:
         b, bp = (bundle.arr5() if bundle is not None else _darr(np.zeros(5)))
         check(lib().hc_engine_set_minibatching(self._h, act_max, kv_max, bp))
 
+    def set_fused_recompute(self, on: bool) -> bool:
+        """Recompute fused with decode attention (default on where the heads'
+        width is a multiple of 128): the recompute GEMM's epilogue reduces each
+        recomputed block to flash-decoding partials against the step's queries
+        instead of writing K|V into the paged layout. Returns the path in use."""
+        a = C.c_int(0)
+        check(lib().hc_engine_set_fused_recompute(self._h, int(bool(on)), C.byref(a)))
+        return bool(a.value)
+
+    def fused_recompute(self) -> bool:
+        a = C.c_int(0)
+        check(lib().hc_engine_set_fused_recompute(self._h, -1, C.byref(a)))
+        return bool(a.value)
+
     def fill_pools(self, seed: int = 1) -> None:
         """Pattern-fill every pool slot (benchmark setup, before a real prefill)."""
         check(lib().hc_engine_fill_pools(self._h, seed))

@@ -468,6 +468,13 @@ int hc_engine_set_minibatching(void* e, long act_max, long kv_max, const double*
     });
 }
 
+int hc_engine_set_fused_recompute(void* e, int on, int* active) {
+    return hc_guard([&] {
+        const bool a = on < 0 ? eng(e)->fused_recompute() : eng(e)->set_fused_recompute(on != 0);
+        if (active) *active = a ? 1 : 0;
+    });
+}
+
 int hc_engine_fill_pools(void* e, uint64_t seed) {
     return hc_guard([&] { eng(e)->fill_pools(seed); });
 }

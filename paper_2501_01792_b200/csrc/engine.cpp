@@ -104,6 +104,13 @@ struct Engine::Impl {
     f16* wbuf[2] = {nullptr, nullptr};
     uint16_t* h_w = nullptr;
     f16 *kv_gpu = nullptr, *act_gpu = nullptr, *kvr = nullptr;
+    // fused recompute + attention (Engine::set_fused_recompute): partial
+    // records [(act_gpu_cap + stage_act_cap) blocks][nseg][Hg][hd + 4] fp32
+    // take the place of kvr
+    float* part = nullptr;
+    bool fused = false;
+    int nseg = 1;  // records per block: tpb / min(tpb, 32)
+    bool fused_supported() const { return dg % 128 == 0 && (hd == 64 || hd == 128) && tpb >= 4 && tpb <= 64; }
     f16 *kv_stage[2] = {nullptr, nullptr}, *act_stage[2] = {nullptr, nullptr};
     f16 *kv_host = nullptr, *act_host = nullptr;  // pinned, mapped (views into h_arena)
     f16* h_arena = nullptr;
@@ -479,6 +486,10 @@ void Engine::init(const ModelConfig& c, int w_max_seq, const uint16_t* emb, cons
     m.dg = m.d / m.tpn;
     m.fg = m.f / m.tpn;
     if (m.dg % 64 || m.fg % 64) throw InputError("tensor parallel: per-rank hidden / ffn slices must be multiples of 64");
+    {
+        const char* e = std::getenv("HC_FUSED_RECOMPUTE");  // 0: recompute writes K|V (kKvPaged) by default
+        m.fused = m.fused_supported() && !(e && e[0] == '0');
+    }
     m.off = LayerOffsets::of(cfg_, m.arch, m.tpn);
     m.offF = LayerOffsets::of(cfg_, m.arch, 1);
     m.LE = m.off.total;
@@ -618,6 +629,10 @@ void Engine::configure_cache(const PoolCaps& caps, bool kv_on_gpu, CacheMode mod
     assigner_ = std::make_unique<BlockAssigner>(*cache_, token_mode_ ? CacheMode::KvOnly : mode, alloc, 0.0);
     m.kv_gpu = dalloc<f16>(static_cast<size_t>(m.L) * m.kv_gpu_cap * m.kvb);
     m.act_gpu = dalloc<f16>(static_cast<size_t>(m.L) * m.act_gpu_cap * m.actb);
+    if (std::getenv("HC_POISON")) {  // debug: NaN in every slot no writer has filled yet
+        if (m.kv_gpu) HC_CUDA(cudaMemset(m.kv_gpu, 0xFF, static_cast<size_t>(m.L) * m.kv_gpu_cap * m.kvb * 2));
+        if (m.act_gpu) HC_CUDA(cudaMemset(m.act_gpu, 0xFF, static_cast<size_t>(m.L) * m.act_gpu_cap * m.actb * 2));
+    }
     m.act_cap_n = (m.act_host_cap + m.tpn - 1) / m.tpn;
     // pinned, mapped host pools: one arena, kept across configure_cache calls
     // while it is large enough (pinning tens of GB takes seconds per call)
@@ -652,6 +667,8 @@ void Engine::alloc_staging() {
         if (*p) cudaFree(*p);
         *p = nullptr;
     }
+    if (m.part) cudaFree(m.part);
+    m.part = nullptr;
     m.stage_kv_cap = m.kv_host_cap;
     m.stage_act_cap = static_cast<long>(m.tpn) * m.act_cap_n;
     if (m.mb_on) {
@@ -662,14 +679,42 @@ void Engine::alloc_staging() {
         m.kv_stage[s] = dalloc<f16>(static_cast<size_t>(m.stage_kv_cap) * m.kvb);
         m.act_stage[s] = dalloc<f16>(static_cast<size_t>(m.stage_act_cap) * m.actb);
     }
-    m.kvr = dalloc<f16>(static_cast<size_t>(m.act_gpu_cap + m.stage_act_cap) * m.kvb);
+    m.nseg = m.tpb / std::min(m.tpb, 32);
+    if (m.fused) {  // partial records instead of recomputed K|V blocks
+        const size_t n = static_cast<size_t>(m.act_gpu_cap + m.stage_act_cap) * m.nseg * m.Hg * (m.hd + 4);
+        m.part = dalloc<float>(n);
+        if (std::getenv("HC_POISON"))  // debug: NaN records expose any record read before it is written
+            HC_CUDA(cudaMemset(m.part, 0xFF, n * sizeof(float)));
+    }
+    else
+        m.kvr = dalloc<f16>(static_cast<size_t>(m.act_gpu_cap + m.stage_act_cap) * m.kvb);
     // staging slots start zeroed: whole-chunk copies (D2H runs, TP all-gathers)
     // never move uninitialised bytes, even for slots no block occupies yet
     for (int s = 0; s < 2; ++s) {
-        if (m.kv_stage[s]) HC_CUDA(cudaMemset(m.kv_stage[s], 0, static_cast<size_t>(m.stage_kv_cap) * m.kvb * 2));
-        if (m.act_stage[s]) HC_CUDA(cudaMemset(m.act_stage[s], 0, static_cast<size_t>(m.stage_act_cap) * m.actb * 2));
+        const int fill = std::getenv("HC_POISON") ? 0xFF : 0;  // debug: NaN staging
+        if (m.kv_stage[s]) HC_CUDA(cudaMemset(m.kv_stage[s], fill, static_cast<size_t>(m.stage_kv_cap) * m.kvb * 2));
+        if (m.act_stage[s]) HC_CUDA(cudaMemset(m.act_stage[s], fill, static_cast<size_t>(m.stage_act_cap) * m.actb * 2));
     }
 }
+
+bool Engine::set_fused_recompute(bool on) {
+    HC_CUDA(cudaSetDevice(opt_.device));
+    Impl& m = *impl_;
+    on = on && m.fused_supported();
+    if (on == m.fused) return on;
+    HC_CUDA(cudaDeviceSynchronize());
+    m.clear_graphs();
+    m.fused = on;
+    if (m.configured) {
+        m.configured = false;
+        alloc_staging();
+        HC_CUDA(cudaDeviceSynchronize());
+        m.configured = true;
+    }
+    return on;
+}
+
+bool Engine::fused_recompute() const { return impl_->fused; }
 
 void Engine::set_minibatching(long act_max, long kv_max, const TimingBundle& bundle) {
     HC_CUDA(cudaSetDevice(opt_.device));
@@ -737,7 +782,7 @@ Engine::~Engine() {
                     (void*)m.hbuf, (void*)m.logits, (void*)m.amax, (void*)m.attn_work, (void*)m.d_meta,
                     (void*)m.px[0], (void*)m.px[1], (void*)m.pqkv, (void*)m.patt, (void*)m.pproj, (void*)m.ph,
                     (void*)m.tr_kv, (void*)m.splitk_ws, (void*)m.lnf, (void*)m.xn, (void*)m.pxn, (void*)m.red,
-                    (void*)m.agree_buf})
+                    (void*)m.agree_buf, (void*)m.part})
         if (p) cudaFree(p);
     for (auto& g : m.graphs) cudaGraphExecDestroy(g.second.exec);
     for (void* p : {(void*)m.h_w, (void*)m.h_arena, (void*)m.h_meta, (void*)m.h_x,
@@ -1249,9 +1294,11 @@ void Engine::decode_step(const std::vector<std::string>& ids_in, const int* toke
     struct Unit {
         std::vector<Run> kv_runs, act_runs;  // start = host index, dst = staging position
         std::vector<int> tiles_h, tiles_g;
+        // fused recompute: per (tile, block slot) request << 8 | valid tokens, -1 = not in the unit
+        std::vector<int> info_h, info_g;
         int splits = 1;
         bool any_act = false, any_kv = false;
-        size_t o_th = 0, o_tg = 0;
+        size_t o_th = 0, o_tg = 0, o_ih = 0, o_ig = 0;
     };
     std::vector<Unit> units(M);
     std::vector<int> act_dev(n, -1), act_host(n, -1), kv_dev(n, -1), kv_host(n, -1), tok(n, 0), nblk(n), ctx(n);
@@ -1300,6 +1347,7 @@ void Engine::decode_step(const std::vector<std::string>& ids_in, const int* toke
         U.tiles_h = tiles_of(apos, m.tpb);
         U.tiles_g = tiles_of(actg, m.tpb);
         int max_ctx = 0;
+        std::unordered_map<int, int> binfo_h, binfo_g;  // fused: block position -> request << 8 | valid
         for (int b = mb_row[u]; b < mb_row[u + 1]; ++b) {
             const int rcb = (rc_cu[b + 1] - rc_cu[b]) / m.tpb;
             const BlockTableEntry& e = grown[b].entry;
@@ -1323,10 +1371,31 @@ void Engine::decode_step(const std::vector<std::string>& ids_in, const int* toke
             for (size_t i = 0; i < t.entries.size(); ++i) {
                 const auto& en = t.entries[i];
                 const bool g = en.location == Location::GpuMem;
-                if (en.kind == BlockKind::KV)
+                if (en.kind == BlockKind::KV) {
                     rb[i] = g ? pack_ref(R_KV_GPU, en.pbn) : pack_ref(R_KV_STAGE, kvp.at(en.pbn));
-                else
-                    rb[i] = pack_ref(R_KVR, g ? en.pbn : static_cast<int>(m.act_gpu_cap) + actp.at(en.pbn));
+                } else {
+                    const int pos = g ? en.pbn : actp.at(en.pbn);
+                    rb[i] = pack_ref(R_KVR, g ? pos : static_cast<int>(m.act_gpu_cap) + pos);
+                    if (m.fused) {
+                        const int valid = std::min(m.tpb, static_cast<int>(t.context_len() - static_cast<long>(i) * m.tpb));
+                        if (!(g ? binfo_g : binfo_h).emplace(pos, b << 8 | valid).second)
+                            throw std::logic_error("decode_step: an ACT block is listed by two requests");
+                    }
+                }
+            }
+        }
+        if (m.fused) {  // per (tile, block slot) of the recompute tiles
+            const int bpt = gemm::BM / m.tpb;
+            for (int which = 0; which < 2; ++which) {
+                const std::vector<int>& tl = which == 0 ? U.tiles_h : U.tiles_g;
+                const auto& mp = which == 0 ? binfo_h : binfo_g;
+                std::vector<int>& info = which == 0 ? U.info_h : U.info_g;
+                info.assign(tl.size() * bpt, -1);
+                for (size_t ti = 0; ti < tl.size(); ++ti)
+                    for (int k = 0; k < bpt; ++k) {
+                        const auto it = mp.find(tl[ti] / m.tpb + k);
+                        if (it != mp.end()) info[ti * bpt + k] = it->second;
+                    }
             }
         }
         U.splits = attention_splits(mb_row[u + 1] - mb_row[u], m.Hg, max_ctx, m.tpb);
@@ -1350,6 +1419,8 @@ void Engine::decode_step(const std::vector<std::string>& ids_in, const int* toke
     for (Unit& U : units) {
         U.o_th = put(U.tiles_h);
         U.o_tg = put(U.tiles_g);
+        U.o_ih = put(U.info_h);
+        U.o_ig = put(U.info_g);
     }
     m.ensure_meta(meta.size() + 1);
     if (!meta.empty()) std::memcpy(m.h_meta, meta.data(), meta.size() * 4);
@@ -1520,39 +1591,52 @@ void Engine::decode_step(const std::vector<std::string>& ids_in, const int* toke
                         act_append(ap, s_compute_);
                         st.launches += 1;
                     }
-                    // recompute K|V of the unit's ACT blocks (streamed and resident) into R_KVR
-                    for (int which = 0; which < 2; ++which) {
-                        const std::vector<int>& tl = which == 0 ? U.tiles_h : U.tiles_g;
-                        if (tl.empty()) continue;
-                        GemmCall c;
-                        c.epi = gemm::kKvPaged;
-                        c.A = which == 0 ? m.act_stage[slot] : R[R_ACT_GPU];
-                        c.lda = m.d;
-                        c.a_rows = static_cast<int>((which == 0 ? m.stage_act_cap : m.act_gpu_cap) * m.tpb);
-                        c.B = W + m.off.wqkv + static_cast<size_t>(m.dg) * m.d;  // rows dg..3dg of Wqkv^T = [Wk|Wv]^T (own heads)
-                        c.ldb = m.d;
-                        c.M = c.a_rows;
-                        c.N = 2 * m.dg;
-                        c.K = m.d;
-                        c.m_tile_rows = dm + (which == 0 ? U.o_th : U.o_tg);
-                        c.num_m_tiles = static_cast<int>(tl.size());
-                        c.out = m.kvr;
-                        c.tpb = m.tpb;
-                        c.d = m.dg;
-                        c.hd = m.hd;
-                        c.blk_off = which == 0 ? static_cast<int>(m.act_gpu_cap) : 0;
-                        c.bias = m.bias(W, m.off.bqkv + m.dg);  // [b_k | b_v] of the own heads
-                        m.span_begin(profile_, s_compute_, 0);
-                        run_gemm(c, s_compute_);
-                        m.span_end(profile_, s_compute_);
-                        st.launches += 1;
-                        st.recompute_tokens += static_cast<double>(tl.size()) * gemm::BM;
-                    }
+                    // recompute K|V of the unit's ACT blocks (streamed and resident): into
+                    // R_KVR (kKvPaged), or fused with the attention (kAttnPart: partial
+                    // records against the unit's queries, so the QKV GEMM runs first)
                     f16* qkvb = m.qkvb + static_cast<size_t>(r0) * 3 * m.dg;
                     f16* att = m.att + static_cast<size_t>(r0) * m.dg;
+                    auto recompute = [&] {
+                        for (int which = 0; which < 2; ++which) {
+                            const std::vector<int>& tl = which == 0 ? U.tiles_h : U.tiles_g;
+                            if (tl.empty()) continue;
+                            GemmCall c;
+                            c.epi = m.fused ? gemm::kAttnPart : gemm::kKvPaged;
+                            c.A = which == 0 ? m.act_stage[slot] : R[R_ACT_GPU];
+                            c.lda = m.d;
+                            c.a_rows = static_cast<int>((which == 0 ? m.stage_act_cap : m.act_gpu_cap) * m.tpb);
+                            c.B = W + m.off.wqkv + static_cast<size_t>(m.dg) * m.d;  // rows dg..3dg of Wqkv^T = [Wk|Wv]^T (own heads)
+                            c.ldb = m.d;
+                            c.M = c.a_rows;
+                            c.N = 2 * m.dg;
+                            c.K = m.d;
+                            c.m_tile_rows = dm + (which == 0 ? U.o_th : U.o_tg);
+                            c.num_m_tiles = static_cast<int>(tl.size());
+                            c.out = m.kvr;
+                            c.tpb = m.tpb;
+                            c.d = m.dg;
+                            c.hd = m.hd;
+                            c.blk_off = which == 0 ? static_cast<int>(m.act_gpu_cap) : 0;
+                            c.bias = m.bias(W, m.off.bqkv + m.dg);  // [b_k | b_v] of the own heads
+                            if (m.fused) {
+                                c.blk_info = dm + (which == 0 ? U.o_ih : U.o_ig);
+                                c.q = m.qkvb;  // request rows of the step (own heads' Q at column 0)
+                                c.ldq = 3 * m.dg;
+                                c.qscale = scale * 1.4426950408889634f;
+                                c.part = m.part;
+                            }
+                            m.span_begin(profile_, s_compute_, 0);
+                            run_gemm(c, s_compute_);
+                            m.span_end(profile_, s_compute_);
+                            st.launches += 1;
+                            st.recompute_tokens += static_cast<double>(tl.size()) * gemm::BM;
+                        }
+                    };
+                    if (!m.fused) recompute();
                     m.span_begin(profile_, s_compute_, 2);
                     m.qkv(W, xa, nb, qkvb, s_compute_, m.splitk_ws, m.splitk_floats);
                     m.span_end(profile_, s_compute_);
+                    if (m.fused) recompute();
                     if (U.any_kv) {  // new token's K|V -> its KV slot (device + host)
                         ap.src = qkvb;
                         ap.ld = 3 * m.dg;
@@ -1579,6 +1663,10 @@ void Engine::decode_step(const std::vector<std::string>& ids_in, const int* toke
                     a.scale = scale;
                     a.work = m.attn_work;
                     a.splits = U.splits;
+                    if (m.fused) {
+                        a.part = m.part;
+                        a.part_region = R_KVR;
+                    }
                     m.span_begin(profile_, s_compute_, 1);
                     decode_attention(a, s_compute_);
                     m.span_end(profile_, s_compute_);
@@ -1851,9 +1939,13 @@ double Engine::time_kv_gen(int n_tokens, int reps) {
     const f16* W = m.layer_w(0, 0);
     std::vector<int> tiles;
     for (int r = 0; r < n_tokens; r += gemm::BM) tiles.push_back(r);
+    const size_t n_tiles = tiles.size();
+    if (m.fused)  // every block full, all rows one request (query row 0)
+        tiles.resize(n_tiles + n_tiles * (gemm::BM / m.tpb), m.tpb);
     m.ensure_meta(tiles.size());
     std::memcpy(m.h_meta, tiles.data(), tiles.size() * 4);
     HC_CUDA(cudaMemcpy(m.d_meta, m.h_meta, tiles.size() * 4, cudaMemcpyHostToDevice));
+    if (m.fused) HC_CUDA(cudaMemset(m.qkvb, 0, static_cast<size_t>(3) * m.dg * 2));
     GemmCall c;
     c.epi = gemm::kKvPaged;
     c.A = A;
@@ -1867,12 +1959,20 @@ double Engine::time_kv_gen(int n_tokens, int reps) {
     c.N = 2 * m.dg;
     c.K = m.d;
     c.m_tile_rows = m.d_meta;
-    c.num_m_tiles = static_cast<int>(tiles.size());
+    c.num_m_tiles = static_cast<int>(n_tiles);
     c.out = m.kvr;
     c.tpb = m.tpb;
     c.d = m.dg;
     c.hd = m.hd;
     c.bias = m.bias(W, m.off.bqkv + m.dg);
+    if (m.fused) {  // the kernel the decode step runs: recompute fused with attention
+        c.epi = gemm::kAttnPart;
+        c.blk_info = m.d_meta + n_tiles;
+        c.q = m.qkvb;
+        c.ldq = 3 * m.dg;
+        c.qscale = 1.f;
+        c.part = m.part;
+    }
     run_gemm(c, s_compute_);  // warm-up
     HC_CUDA(cudaEventRecord(m.ev0, s_compute_));
     for (int i = 0; i < reps; ++i) run_gemm(c, s_compute_);

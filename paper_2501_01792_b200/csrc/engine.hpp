@@ -106,6 +106,14 @@ public:
     // mini-batch) units double-buffered. act_max = kv_max = 0 turns it off
     // (whole-batch steps, staging = the host pools).
     void set_minibatching(long act_max, long kv_max, const TimingBundle& bundle);
+    // Recompute fused with decode attention (default on where supported: own
+    // heads' width a multiple of 128): the recompute GEMM's epilogue reduces
+    // each recomputed block to flash-decoding partials against the step's
+    // queries instead of writing its K|V into the paged KV layout, so the
+    // recomputed K|V never touch HBM. Off: the kKvPaged path (K|V stored,
+    // attention reads them). Returns whether the fused path is in use.
+    bool set_fused_recompute(bool on);
+    bool fused_recompute() const;
     // Fill every pool slot with the deterministic pattern (benchmark setup:
     // slots that advance_synthetic later hands out then hold finite values).
     void fill_pools(uint64_t seed);

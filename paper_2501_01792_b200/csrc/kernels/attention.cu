@@ -94,8 +94,46 @@ __global__ void __launch_bounds__(kWarps * 32)
     float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 
     const int* refs = c.blk_ref + static_cast<long long>(b) * c.max_blocks;
+    constexpr int SEG = TPB < 32 ? TPB : 32;  // rows per partial record (gemm.cuh attn_part_tile)
+    // the next block's ref is loaded one iteration ahead, so a block's K|V (or
+    // partial record) loads never wait on its ref
+    int ref_next = blk_begin + warp < blk_end ? __ldg(refs + blk_begin + warp) : 0;
     for (int blk = blk_begin + warp; blk < blk_end; blk += kWarps) {
-        const int ref = refs[blk];
+        const int ref = ref_next;
+        if (blk + kWarps < blk_end) ref_next = __ldg(refs + blk + kWarps);
+        if ((ref >> 28) == c.part_region) {
+            // partials of a recomputed block: o, m (log2 domain, scale folded in), l;
+            // every load of the block's records is issued before any math
+            float4 o0[TPB / SEG], o1[TPB / SEG];
+            float mp[TPB / SEG], lp[TPB / SEG];
+#pragma unroll
+            for (int sg = 0; sg < TPB / SEG; ++sg) {
+                const float* rec =
+                    c.part + ((static_cast<long long>(ref & 0x0FFFFFFF) * (TPB / SEG) + sg) * c.H + h) * (HD + 4);
+                o0[sg] = __ldg(reinterpret_cast<const float4*>(rec + col));
+                o1[sg] = __ldg(reinterpret_cast<const float4*>(rec + col + 4));
+                mp[sg] = __ldg(rec + HD);
+                lp[sg] = __ldg(rec + HD + 1);
+            }
+#pragma unroll
+            for (int sg = 0; sg < TPB / SEG; ++sg) {
+                const float m_new = fmaxf(m, mp[sg]);
+                const float corr = exp2f(m - m_new);
+                // one token group adds the record (the fold below sums the groups)
+                const float f = grp == 0 ? exp2f(mp[sg] - m_new) : 0.f;
+                l = l * corr + lp[sg] * f;
+                acc[0] = acc[0] * corr + o0[sg].x * f;
+                acc[1] = acc[1] * corr + o0[sg].y * f;
+                acc[2] = acc[2] * corr + o0[sg].z * f;
+                acc[3] = acc[3] * corr + o0[sg].w * f;
+                acc[4] = acc[4] * corr + o1[sg].x * f;
+                acc[5] = acc[5] * corr + o1[sg].y * f;
+                acc[6] = acc[6] * corr + o1[sg].z * f;
+                acc[7] = acc[7] * corr + o1[sg].w * f;
+                m = m_new;
+            }
+            continue;
+        }
         const f16* base = c.region[ref >> 28] + static_cast<long long>(ref & 0x0FFFFFFF) * block_elems + head_off;
         const int valid = (blk == nb - 1) ? ctx - (nb - 1) * TPB : TPB;
         uint4 kr[ITERS], vr[ITERS];

@@ -54,24 +54,24 @@ CUtensorMap make_map(const void* ptr, long long rows, long long cols, long long 
 
 namespace {
 
-template <int BN, int EPI>
+template <int BN, int EPI, int HD = 0, int SEG = 0>
 void launch(const GemmCall& c, const gemm::Params& p, cudaStream_t st) {
     using Cf = gemm::Cfg<BN>;
-    auto kern = gemm::gemm_tn_kernel<BN, EPI>;
+    auto kern = gemm::gemm_tn_kernel<BN, EPI, HD, SEG>;
     static std::atomic<uint64_t> attr_set{0};  // per instantiation, per device
     max_dynamic_smem_once(kern, Cf::kSmemBytes, attr_set);
     const CUtensorMap ta = make_map(c.A, c.a_rows, c.K, c.lda, gemm::BM);
-    const CUtensorMap tb = make_map(c.B, c.N, c.K, c.ldb, BN);
+    const CUtensorMap tb = make_map(c.B, c.N, c.K, c.ldb, EPI == gemm::kAttnPart ? 128 : BN);
     const int tiles = p.num_m_tiles * p.num_n_tiles * p.splits;
     int grid = tiles < num_sms() ? tiles : num_sms();
     if (c.max_ctas > 0 && grid > c.max_ctas) grid = c.max_ctas;
     kern<<<grid, gemm::kThreads, Cf::kSmemBytes, st>>>(ta, tb, p);
 }
 
-template <int EPI>
+template <int EPI, int HD = 0, int SEG = 0>
 void launch_pair(const GemmCall& c, const gemm::Params& p, cudaStream_t st) {
     using Cf = gemm::Cfg2;
-    auto kern = gemm::gemm2_tn_kernel<EPI>;
+    auto kern = gemm::gemm2_tn_kernel<EPI, HD, SEG>;
     static std::atomic<uint64_t> attr_set{0};
     max_dynamic_smem_once(kern, Cf::kSmemBytes, attr_set);
     const CUtensorMap ta = make_map(c.A, c.a_rows, c.K, c.lda, gemm::BM);
@@ -91,6 +91,33 @@ void dispatch_epi(const GemmCall& c, const gemm::Params& p, cudaStream_t st) {
         case gemm::kSplitF32: return launch<BN, gemm::kSplitF32>(c, p, st);
     }
     throw std::invalid_argument("gemm: unknown epilogue");
+}
+
+// recompute fused with decode attention: template on (head_dim, segment rows)
+template <bool kPair, int HD>
+void dispatch_attn_seg(const GemmCall& c, const gemm::Params& p, cudaStream_t st) {
+    const int seg = c.tpb < 32 ? c.tpb : 32;
+#define HC_SEG(S_)                                                           \
+    if (seg == S_) {                                                         \
+        if constexpr (kPair)                                                 \
+            launch_pair<gemm::kAttnPart, HD, S_>(c, p, st);                  \
+        else                                                                 \
+            launch<256, gemm::kAttnPart, HD, S_>(c, p, st);                  \
+        return;                                                              \
+    }
+    HC_SEG(4)
+    HC_SEG(8)
+    HC_SEG(16)
+    HC_SEG(32)
+#undef HC_SEG
+    throw std::invalid_argument("gemm: kAttnPart needs tokens_per_block 4..64");
+}
+
+template <bool kPair>
+void dispatch_attn(const GemmCall& c, const gemm::Params& p, cudaStream_t st) {
+    if (c.hd == 128) return dispatch_attn_seg<kPair, 128>(c, p, st);
+    if (c.hd == 64) return dispatch_attn_seg<kPair, 64>(c, p, st);
+    throw std::invalid_argument("gemm: kAttnPart needs head_dim 64 or 128");
 }
 
 int pick_bn(int num_m_tiles, int N) {
@@ -180,6 +207,18 @@ void run_gemm(const GemmCall& c, cudaStream_t st) {
     p.bias = c.bias;
     p.res = c.res;
     p.ldr = c.ldr;
+    if (c.epi == gemm::kAttnPart) {
+        if (c.d % 128 || c.N != 2 * c.d || !c.blk_info || !c.q || !c.part || c.res || !c.m_tile_rows ||
+            c.tpb <= 0 || gemm::BM % c.tpb || (c.ldq * 2) % 16 || reinterpret_cast<uintptr_t>(c.q) % 16)
+            throw std::invalid_argument("gemm: kAttnPart needs d % 128 == 0, N = 2d, tile rows, blk_info, q, part");
+        p.v_row = c.d;
+        p.blk_info = c.blk_info;
+        p.q = c.q;
+        p.ldq = c.ldq;
+        p.qscale = c.qscale;
+        p.heads = c.d / c.hd;
+        p.part = c.part;
+    }
     p.group_m = c.group_m > 0 ? c.group_m : (c.K <= 4096 ? 32 : 16);
     if (const char* g = std::getenv("HC_GEMM_GROUP_M")) p.group_m = std::max(1, std::atoi(g));  // tuning knob
     static const int group_n_env = [] {
@@ -187,6 +226,16 @@ void run_gemm(const GemmCall& c, cudaStream_t st) {
         return g ? std::atoi(g) : 0;
     }();
     p.group_n = group_n_env;
+    static const int l2_env = [] {
+        const char* e = std::getenv("HC_GEMM_L2HINT");  // tuning knob: gemm::kL2* bits
+        return e ? std::atoi(e) : -1;
+    }();
+    // by shape: the recompute GEMM keeps its A group in L2 and streams its K|V
+    // out (scripts/gemm_sustained.py: +8 % sustained for the pair kernel)
+    p.l2_hint = c.l2_hint >= 0 ? c.l2_hint
+                : c.epi == gemm::kKvPaged ? (gemm::kL2KeepA | gemm::kL2StreamC)
+                : c.epi == gemm::kAttnPart ? gemm::kL2KeepA : 0;
+    if (l2_env >= 0) p.l2_hint = l2_env;
     p.splits = 1;
     p.kb_per_split = (c.K + gemm::BK - 1) / gemm::BK;
     GemmCall cc = c;
@@ -219,24 +268,30 @@ void run_gemm(const GemmCall& c, cudaStream_t st) {
         const char* e = std::getenv("HC_GEMM_PAIR");
         return !(e && e[0] == '0');
     }();
-    // Measured on B200 (profiles/r01_gemm_pair.txt): the pair kernel reaches
-    // 99.7 % tensor-pipe activity but, under the 1 kW cap, its extra DRAM
-    // traffic at K = 7168 costs clock (1.17 vs 1.36 GHz in situ), so it only
-    // wins for K <= 4096 (OPT-6.7B recompute: +10 % in situ).
+    // Sustained under the 1 kW cap (scripts/gemm_sustained.py, profiles/r02_gemm_sustained.txt):
+    // at K = 7168 the pair kernel runs 1.43-1.58 PFLOP/s against the 1-SM
+    // kernel's 1.15-1.21 (the 256 x 256 tile halves the smem / L2 feed per MAC),
+    // group_m 32 rows-of-128 (16 pair tiles) with the L2 hints
     static const int pair_max_k = [] {
         const char* e = std::getenv("HC_GEMM_PAIR_MAX_K");  // tuning knob
-        return e ? std::atoi(e) : 4096;
+        return e ? std::atoi(e) : 1 << 30;
     }();
     if (pair_ok && p.splits == 1 && !c.bn && p.num_m_tiles >= 8 && c.K <= pair_max_k && cc.epi != gemm::kSplitF32) {
         p.num_n_tiles = (c.N + gemm::Cfg2::BN - 1) / gemm::Cfg2::BN;
-        p.group_m = c.group_m > 0 ? std::max(1, c.group_m / 2) : 8;
+        p.group_m = c.group_m > 0 ? std::max(1, c.group_m / 2) : 16;
         if (const char* g = std::getenv("HC_GEMM_GROUP_M")) p.group_m = std::max(1, std::atoi(g) / 2);
         switch (cc.epi) {
+            case gemm::kAttnPart: dispatch_attn<true>(cc, p, st); return;
             case gemm::kStore: launch_pair<gemm::kStore>(cc, p, st); return;
             case gemm::kRelu: launch_pair<gemm::kRelu>(cc, p, st); return;
             case gemm::kKvPaged: launch_pair<gemm::kKvPaged>(cc, p, st); return;
             case gemm::kF32: launch_pair<gemm::kF32>(cc, p, st); return;
         }
+    }
+    if (cc.epi == gemm::kAttnPart) {
+        p.num_n_tiles = c.N / 256;
+        dispatch_attn<false>(cc, p, st);
+        return;
     }
     p.num_n_tiles = (c.N + bn - 1) / bn;
     switch (bn) {

@@ -17,8 +17,14 @@
 //   kKvPaged    recompute K|V written straight into the paged KV block layout
 //               [blk][K|V][head][tok][hd]  (north-star (2), decoder.cpp:123-129)
 //   kF32        fp32 row-major (logits)
+//   kAttnPart   recompute fused with decode attention: the N tile is [K_h | V_h]
+//               of 128/hd heads, and instead of storing K|V the epilogue turns
+//               each segment of tokens into a flash-decoding partial (m, l, o)
+//               for its request's query (decoder.cpp:15-43 over the recomputed
+//               rows), which decode_attention merges with the KV-cached blocks
 #pragma once
 #include <cuda.h>
+#include <cfloat>
 #include <cuda_runtime.h>
 
 #include "gemm_types.hpp"
@@ -47,7 +53,28 @@ struct Params {
     const __half* bias;
     const __half* res;
     long long ldr;
+    // L2 policy bits (kL2*): which operand the raster wants kept in L2
+    int l2_hint;
+    // kAttnPart: N tile ni = heads [ni*128/hd, (ni+1)*128/hd); B rows of the V
+    // half start at v_row (= d); blk_info[mi * (BM/tpb) + slot] = request << 8 |
+    // valid tokens of the block at that slot of M tile mi (-1: not in this
+    // step); q rows by request (f16, ld ldq, own heads from column 0), scaled
+    // by qscale (= softmax scale * log2 e); partial records (fp32, hd + 4 for
+    // 16-byte rows: o[hd], m, l, pad) at part[((blk * (tpb/seg) + seg) * heads + h) * (hd + 4)]
+    int v_row;
+    const int* blk_info;
+    const __half* q;
+    long long ldq;
+    float qscale;
+    int heads;
+    float* part;
 };
+
+// L2 policy bits (Params::l2_hint)
+constexpr int kL2KeepA = 1;    // A tiles evict_last (the group's A slab is reused across the N sweep),
+                               // evict_first on an A tile's last use (its last N tile)
+constexpr int kL2StreamB = 2;  // B tiles evict_first
+constexpr int kL2StreamC = 4;  // C stores streaming (st.global.cs: the output is not re-read from L2)
 
 template <int BN>
 struct Cfg {
@@ -101,6 +128,131 @@ __device__ __forceinline__ void add16(float (&acc)[16], const __half* src) {
     }
 }
 
+// ---- kAttnPart epilogue ----------------------------------------------------
+// 16 consecutive f16 at src -> fp32 (32-byte aligned run)
+__device__ __forceinline__ void load16(float (&f)[16], const __half* src) {
+    const uint4* s4 = reinterpret_cast<const uint4*>(src);
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+        const uint4 u = __ldg(s4 + q);
+        const __half2* h2 = reinterpret_cast<const __half2*>(&u);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const float2 v = __half22float2(h2[i]);
+            f[8 * q + 2 * i] = v.x;
+            f[8 * q + 2 * i + 1] = v.y;
+        }
+    }
+}
+
+// the f16 value the unfused path would have stored (K|V are cached as f16)
+__device__ __forceinline__ float round_f16(float x) { return __half2float(__float2half_rn(x)); }
+
+// Sum v[0..16) over the SEG lanes of a segment (lanes that differ in their
+// low log2(SEG) bits) and scatter the sums: on return this lane holds
+// n = max(1, 16/SEG) column sums in v[0..n), for columns [*col0, *col0 + n)
+// of the 16 (lanes whose low bits differ only above bit log2(16)... hold copies
+// when SEG = 32: lane pairs (i, i^1) agree).
+template <int SEG>
+__device__ __forceinline__ void seg_reduce_scatter16(float (&v)[16], int lane, int* col0) {
+    int base = 0;
+    int n = 16;
+#pragma unroll
+    for (int off = SEG / 2; off >= 1; off >>= 1) {
+        if (n > 1) {
+            const bool up = (lane & off) != 0;
+            const int half = n / 2;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                if (k < half) {
+                    const float send = up ? v[k] : v[k + half];
+                    const float keep = up ? v[k + half] : v[k];
+                    v[k] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+                }
+            }
+            if (up) base += half;
+            n = half;
+        } else {
+            v[0] += __shfl_xor_sync(0xffffffffu, v[0], off);
+        }
+    }
+    *col0 = base;
+}
+
+// One TMEM lane (= one recomputed token row) of a finished [K_h | V_h] tile:
+// s = q_b,h . K_row (K rounded to f16 as the cache stores it), then per
+// segment of SEG rows (one block, one request) m = max s, p = 2^(s - m),
+// l = sum p, o = sum p V_row -> partial record. Rows outside the step
+// (blk_info -1) and unfilled slots of a request's last block get p = 0.
+template <int HD, int SEG>
+__device__ __forceinline__ void attn_part_tile(const Params& p, uint32_t t_row, int mi, int r_in_tile, int row,
+                                               int ni, int lane) {
+    constexpr int HPT = 128 / HD;  // heads per tile
+    const int bpt = BM / p.tpb;
+    const int slot = r_in_tile / p.tpb;
+    const int info = row < p.M ? __ldg(p.blk_info + mi * bpt + slot) : -1;
+    const int tok = r_in_tile - slot * p.tpb;
+    const bool valid = info >= 0 && tok < (info & 0xFF);
+    const int req = info >= 0 ? (info >> 8) : 0;
+    const int nseg = p.tpb / SEG;
+    const int seg = tok / SEG;
+    const long long blk = row / p.tpb + p.blk_off;
+#pragma unroll 1
+    for (int j = 0; j < HPT; ++j) {
+        const int h = ni * HPT + j;
+        const __half* qp = p.q + static_cast<long long>(req) * p.ldq + h * HD;
+        float sc = 0.f;
+#pragma unroll 1
+        for (int c = 0; c < HD; c += 16) {
+            uint32_t v[16];
+            ptx::tmem_ld_x16(t_row + j * HD + c, v);
+            float qf[16], bk[16];
+            load16(qf, qp + c);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) bk[i] = 0.f;
+            if (p.bias) add16(bk, p.bias + h * HD + c);
+            ptx::tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 16; ++i) sc = fmaf(qf[i] * p.qscale, round_f16(__uint_as_float(v[i]) + bk[i]), sc);
+        }
+        if (!valid) sc = -FLT_MAX;
+        float m = sc;
+#pragma unroll
+        for (int off = SEG / 2; off >= 1; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
+        const float pr = valid ? exp2f(sc - m) : 0.f;
+        float l = pr;
+#pragma unroll
+        for (int off = SEG / 2; off >= 1; off >>= 1) l += __shfl_xor_sync(0xffffffffu, l, off);
+        float* rec = p.part + ((blk * nseg + seg) * p.heads + h) * (HD + 4);
+        const bool write = info >= 0 && row < p.M;
+        constexpr int NV = 16 / SEG > 1 ? 16 / SEG : 1;
+        const bool writer = SEG <= 16 || (lane & (SEG / 16 - 1)) == 0;
+#pragma unroll 1
+        for (int c = 0; c < HD; c += 16) {
+            uint32_t v[16];
+            ptx::tmem_ld_x16(t_row + 128 + j * HD + c, v);
+            float bv[16], o[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) bv[i] = 0.f;
+            if (p.bias) add16(bv, p.bias + p.d + h * HD + c);
+            ptx::tmem_ld_wait();
+#pragma unroll
+            // rows outside the step / unfilled slots may hold any bits (even NaN): 0 * NaN != 0
+            for (int i = 0; i < 16; ++i) o[i] = valid ? pr * round_f16(__uint_as_float(v[i]) + bv[i]) : 0.f;
+            int col0;
+            seg_reduce_scatter16<SEG>(o, lane, &col0);
+            if (write && writer) {
+#pragma unroll
+                for (int i = 0; i < NV; ++i) rec[c + col0 + i] = o[i];
+            }
+        }
+        if (write && (lane & (SEG - 1)) == 0) {
+            rec[HD] = m;
+            rec[HD + 1] = l;
+        }
+    }
+}
+
 template <int BN, int EPI>
 __device__ __forceinline__ void epilogue_chunk(const Params& p, int row, int col, int split, const uint32_t (&v)[16]) {
     if (row >= p.M || col >= p.N) return;
@@ -140,12 +292,17 @@ __device__ __forceinline__ void epilogue_chunk(const Params& p, int row, int col
         } else {
             dst = static_cast<__half*>(p.out) + static_cast<long long>(row) * p.ldc + col;
         }
-        ptx::st_global_v4(dst, h[0], h[1], h[2], h[3]);
-        ptx::st_global_v4(dst + 8, h[4], h[5], h[6], h[7]);
+        if (p.l2_hint & kL2StreamC) {
+            ptx::st_global_cs_v4(dst, h[0], h[1], h[2], h[3]);
+            ptx::st_global_cs_v4(dst + 8, h[4], h[5], h[6], h[7]);
+        } else {
+            ptx::st_global_v4(dst, h[0], h[1], h[2], h[3]);
+            ptx::st_global_v4(dst + 8, h[4], h[5], h[6], h[7]);
+        }
     }
 }
 
-template <int BN, int EPI>
+template <int BN, int EPI, int HD = 0, int SEG = 0>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tn_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const Params p) {
@@ -198,17 +355,37 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) {
             int stage = 0;
             uint32_t phase = 0;
+            const uint64_t pol_last = ptx::policy_evict_last(), pol_first = ptx::policy_evict_first();
+            // operands without a policy bit take plain loads (no cache hint at all)
+            auto load_a = [&](void* dst, uint64_t* bar, int k, int row, uint64_t pol) {
+                if (p.l2_hint & kL2KeepA)
+                    ptx::tma_load_2d_hint(dst, &tmA, bar, k, row, pol);
+                else
+                    ptx::tma_load_2d(dst, &tmA, bar, k, row);
+            };
+            auto load_b = [&](void* dst, uint64_t* bar, int k, int row) {
+                if (p.l2_hint & kL2StreamB)
+                    ptx::tma_load_2d_hint(dst, &tmB, bar, k, row, pol_first);
+                else
+                    ptx::tma_load_2d(dst, &tmB, bar, k, row);
+            };
             for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
                 int mi, ni, kb0, kb1;
                 tile_coords(tile, p, mi, ni);
                 kb_range(tile, kb0, kb1);
                 const int m_row = p.m_tile_rows ? p.m_tile_rows[mi] : mi * BM;
                 const int n_row = ni * BN;
+                const uint64_t pol_a = ni == p.num_n_tiles - 1 ? pol_first : pol_last;
                 for (int kb = kb0; kb < kb1; ++kb) {
                     ptx::mbar_wait(&empty[stage], phase ^ 1);
                     ptx::mbar_arrive_expect_tx(&full[stage], C::kStageBytes);
-                    ptx::tma_load_2d(smem_a + stage * C::kABytes, &tmA, &full[stage], kb * BK, m_row);
-                    ptx::tma_load_2d(smem_b + stage * C::kBBytes, &tmB, &full[stage], kb * BK, n_row);
+                    load_a(smem_a + stage * C::kABytes, &full[stage], kb * BK, m_row, pol_a);
+                    if constexpr (EPI == kAttnPart) {  // [K_h | V_h]: two 128-row boxes
+                        load_b(smem_b + stage * C::kBBytes, &full[stage], kb * BK, ni * 128);
+                        load_b(smem_b + stage * C::kBBytes + 128 * BK * 2, &full[stage], kb * BK, p.v_row + ni * 128);
+                    } else {
+                        load_b(smem_b + stage * C::kBBytes, &full[stage], kb * BK, n_row);
+                    }
                     if (++stage == S) {
                         stage = 0;
                         phase ^= 1;
@@ -267,12 +444,17 @@ __global__ void __launch_bounds__(kThreads, 1)
             ptx::mbar_wait(&tfull[as], aphase);
             ptx::tc_fence_after();
             const uint32_t t_row = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + as * BN;
+            if constexpr (EPI == kAttnPart) {
+                static_assert(BN == 256, "kAttnPart tiles are [K_h | V_h], 128 + 128 columns");
+                attn_part_tile<HD, SEG>(p, t_row, mi, r_in_tile, row, ni, lane);
+            } else {
 #pragma unroll 1
-            for (int c = 0; c < BN; c += 16) {
-                uint32_t v[16];
-                ptx::tmem_ld_x16(t_row + c, v);
-                ptx::tmem_ld_wait();
-                epilogue_chunk<BN, EPI>(p, row, n0 + c, split, v);
+                for (int c = 0; c < BN; c += 16) {
+                    uint32_t v[16];
+                    ptx::tmem_ld_x16(t_row + c, v);
+                    ptx::tmem_ld_wait();
+                    epilogue_chunk<BN, EPI>(p, row, n0 + c, split, v);
+                }
             }
             ptx::tc_fence_before();
             ptx::mbar_arrive(&tempty[as]);
@@ -332,7 +514,7 @@ __device__ __forceinline__ void pair_tile_coords(int tile, int num_pm, int num_n
     ni = within / gm;
 }
 
-template <int EPI>
+template <int EPI, int HD = 0, int SEG = 0>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     gemm2_tn_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     const Params p) {
@@ -391,16 +573,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         if (lane == 0) {
             int stage = 0;
             uint32_t phase = 0;
+            const uint64_t pol_last = ptx::policy_evict_last(), pol_first = ptx::policy_evict_first();
             for (int tile = pair; tile < num_tiles; tile += num_pairs) {
                 int pm, ni;
                 pair_tile_coords(tile, num_pm, p.num_n_tiles, p.group_m, p.group_n, pm, ni);
                 const int m_row = m_row_of(pm, rank);
-                const int n_row = ni * BN + static_cast<int>(rank) * (BN / 2);
+                // kAttnPart: rank 0 loads K_h rows, rank 1 the V_h rows of the heads
+                const int n_row = EPI == kAttnPart ? (rank ? p.v_row : 0) + ni * 128
+                                                   : ni * BN + static_cast<int>(rank) * (BN / 2);
+                const uint64_t pol_a = ni == p.num_n_tiles - 1 ? pol_first : pol_last;
                 for (int kb = 0; kb < num_kb; ++kb) {
                     ptx::mbar_wait(&empty[stage], phase ^ 1);
                     if (rank == 0) ptx::mbar_arrive_expect_tx(&full[stage], 2 * C::kStageBytes);
-                    ptx::tma_load_2d_pair(smem_a + stage * C::kABytes, &tmA, &full[stage], kb * BK, m_row);
-                    ptx::tma_load_2d_pair(smem_b + stage * C::kBBytes, &tmB, &full[stage], kb * BK, n_row);
+                    if (p.l2_hint & kL2KeepA)
+                        ptx::tma_load_2d_pair_hint(smem_a + stage * C::kABytes, &tmA, &full[stage], kb * BK, m_row,
+                                                   pol_a);
+                    else
+                        ptx::tma_load_2d_pair(smem_a + stage * C::kABytes, &tmA, &full[stage], kb * BK, m_row);
+                    if (p.l2_hint & kL2StreamB)
+                        ptx::tma_load_2d_pair_hint(smem_b + stage * C::kBBytes, &tmB, &full[stage], kb * BK, n_row,
+                                                   pol_first);
+                    else
+                        ptx::tma_load_2d_pair(smem_b + stage * C::kBBytes, &tmB, &full[stage], kb * BK, n_row);
                     if (++stage == S) {
                         stage = 0;
                         phase ^= 1;
@@ -452,12 +646,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             ptx::mbar_wait(&tfull[as], aphase);
             ptx::tc_fence_after();
             const uint32_t t_row = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + as * BN;
+            if constexpr (EPI == kAttnPart) {
+                int mt = 2 * pm + static_cast<int>(rank);  // this CTA's 128-row M tile (odd tail repeats the last)
+                if (mt >= p.num_m_tiles) mt = p.num_m_tiles - 1;
+                const bool dup = 2 * pm + static_cast<int>(rank) >= p.num_m_tiles;
+                if (!dup) attn_part_tile<HD, SEG>(p, t_row, mt, q * 32 + lane, row, ni, lane);
+            } else {
 #pragma unroll 1
-            for (int c = 0; c < BN; c += 16) {
-                uint32_t v[16];
-                ptx::tmem_ld_x16(t_row + c, v);
-                ptx::tmem_ld_wait();
-                epilogue_chunk<BN, EPI>(p, row, n0 + c, 0, v);
+                for (int c = 0; c < BN; c += 16) {
+                    uint32_t v[16];
+                    ptx::tmem_ld_x16(t_row + c, v);
+                    ptx::tmem_ld_wait();
+                    epilogue_chunk<BN, EPI>(p, row, n0 + c, 0, v);
+                }
             }
             ptx::tc_fence_before();
             ptx::mbar_arrive_cluster(&tempty[as], 0);

@@ -27,6 +27,7 @@ struct GemmCall {
     int bn = 0;                  // 0 = heuristic
     int max_ctas = 0;            // 0 = all SMs
     int group_m = 0;             // rasterisation group (0 = default 16)
+    int l2_hint = -1;            // gemm::kL2* bits; -1 = by shape (large-M GEMMs keep the A slab in L2)
     float* ws = nullptr;         // split-K workspace (fp32); null disables split-K
     size_t ws_floats = 0;
     int splits = 0;              // 0 = planner (pick_split), else forced split count
@@ -35,6 +36,15 @@ struct GemmCall {
     const f16* bias = nullptr;
     const f16* res = nullptr;
     long long ldr = 0;
+    // kAttnPart (recompute fused with decode attention; gemm.cuh attn_part_tile):
+    // B = [Wk | Wv]^T with the V rows from v_row; N = 2 * heads * hd; blk_info
+    // per (M tile, block slot) = request << 8 | valid tokens (-1: skip); q rows
+    // by request (ld ldq, head h at column h * hd); partial records into part
+    const int* blk_info = nullptr;
+    const f16* q = nullptr;
+    long long ldq = 0;
+    float qscale = 1.f;
+    float* part = nullptr;
 };
 // out[m][n] = f16(epi(sum_s ws[s][m][n] + bias[n] + res[m*ldr + n])) — the
 // split-K finish (relu, bias, res optional)
@@ -63,6 +73,11 @@ struct AttnCall {
     // split-K workspace (fp32): [B*H*splits*(hd+2)]; nullptr -> no split
     float* work = nullptr;
     int splits = 1;
+    // refs of region part_region are blocks whose K|V the fused recompute
+    // (GemmCall kAttnPart) already reduced to flash-decoding partials: the
+    // block's tpb / min(tpb, 32) records per head are merged instead of K|V
+    const float* part = nullptr;
+    int part_region = -1;
 };
 void decode_attention(const AttnCall& c, cudaStream_t st);
 // the (head_dim, tokens_per_block) pairs decode_attention is instantiated for

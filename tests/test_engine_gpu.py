@@ -42,11 +42,16 @@ def as_engine_weights(w):
     return {"embedding": w.embedding, "positional": w.positional, "layers": w.layers}
 
 
-def make_engine(cfg, w, **kw):
+def make_engine(cfg, w, fused=None, **kw):
+    """fused: None = the engine's default (recompute fused with attention where
+    the heads' width is a multiple of 128), True / False = force the path."""
     from paper_2501_01792_b200.api import Engine, ModelConfig
     mc = ModelConfig(num_layers=cfg.num_layers, hidden_dim=cfg.hidden_dim, num_heads=cfg.num_heads,
                      ffn_dim=cfg.ffn_dim, vocab_size=cfg.vocab_size, tokens_per_block=cfg.tokens_per_block)
-    return Engine(mc, weights=as_engine_weights(w), **kw)
+    eng = Engine(mc, weights=as_engine_weights(w), **kw)
+    if fused is not None:
+        assert eng.set_fused_recompute(fused) == fused
+    return eng
 
 
 def run_case(cfg, w, prompts, decode_tokens, **engine_kw):
@@ -98,10 +103,11 @@ def test_engine_resident_act_only_matches_oracle(native):
     assert st["h2d_bytes"] == 0 and st["launches"] > 0
 
 
-@pytest.mark.parametrize("weights_on_device", [True, False])
-def test_engine_hybrid_offloaded_matches_oracle(native, weights_on_device):
+@pytest.mark.parametrize("weights_on_device,fused", [(True, True), (False, True), (True, False), (False, False)])
+def test_engine_hybrid_offloaded_matches_oracle(native, weights_on_device, fused):
     """Hybrid 1:1 ratio, ACT blocks split GPU/host, KV on host, weights streamed
-    or resident: outputs match the oracle and block tables match bit-exactly."""
+    or resident, recompute fused with the attention or writing K|V: outputs
+    match the oracle and block tables match bit-exactly."""
     from paper_2501_01792_b200.api import HostAllocation, PoolCaps
     cfg = small_cfg(L=4, d=256, H=4, f=768)
     w = oracle_weights(cfg)
@@ -112,7 +118,8 @@ def test_engine_hybrid_offloaded_matches_oracle(native, weights_on_device):
     alloc = HostAllocation(20, 20)
     caps = PoolCaps(kv_host=20, act_host=20, act_gpu=3)
     eng, ids, got, want = run_case(cfg, w, prompts, dec, caps=caps, allocation=alloc, mode="hybrid",
-                                   weights_on_device=weights_on_device)
+                                   weights_on_device=weights_on_device, fused=fused)
+    assert eng.fused_recompute() == fused
     check_outputs(got, want)
     # block tables: the oracle's add_token replay in the same call order
     ba = O.BlockAssigner(cfg.tokens_per_block, O.HYBRID, O.HostAllocation(20, 20), act_gpu=3)
@@ -983,9 +990,11 @@ def test_engine_tensor_parallel_fuzz(native, tpn, seed):
             assert rel(x, O.forward_prompt(seq, w).output[-1]) <= TOL, (rid, len(seq))
 
 
-@pytest.mark.parametrize("B,tpb,mode", [(200, 16, "hybrid"), (64, 32, "act_only"), (96, 4, "kv_only"),
-                                        (48, 64, "hybrid")])
-def test_engine_large_batches_and_block_sizes(native, B, tpb, mode):
+@pytest.mark.parametrize("B,tpb,mode,fused", [(200, 16, "hybrid", True), (64, 32, "act_only", True),
+                                              (96, 4, "kv_only", True), (48, 64, "hybrid", True),
+                                              (40, 4, "act_only", True), (40, 8, "hybrid", True),
+                                              (200, 16, "hybrid", False), (48, 64, "hybrid", False)])
+def test_engine_large_batches_and_block_sizes(native, B, tpb, mode, fused):
     """Edge sizes the reference allows: hundreds of requests in one decode
     step (grid = B x heads, staging sized for every host block) and block
     sizes other than 16 (tokens_per_block is a model parameter, model.hpp:22):
@@ -998,7 +1007,7 @@ def test_engine_large_batches_and_block_sizes(native, B, tpb, mode):
     per = max(-(-(n + 3) // tpb) for n in lens) + 1
     caps = PoolCaps(kv_host=B * per, act_host=B * per, act_gpu=B // 2)
     eng = make_engine(cfg, w, max_batch=B, max_seq=64, caps=caps, mode=mode, allocation=HostAllocation(1, 1),
-                      weights_on_device=False)
+                      weights_on_device=False, fused=fused)
     ids = [f"b{i}" for i in range(B)]
     prompts = [rng.integers(0, cfg.vocab_size, n).tolist() for n in lens]
     eng.prefill(ids, prompts)
@@ -1013,6 +1022,44 @@ def test_engine_large_batches_and_block_sizes(native, B, tpb, mode):
         for b in range(B):
             if b % (7 if B > 100 else 3):
                 seqs[b].append(toks[b])
+
+
+@pytest.mark.parametrize("hd,tpb,scaled", [(128, 16, True), (64, 16, True), (128, 4, True), (64, 8, False),
+                                           (128, 32, False), (64, 64, True)])
+def test_fused_recompute_attention_agrees_with_kv_paged_path(native, hd, tpb, scaled):
+    """The fused recompute + attention path (kAttnPart partial records merged by
+    decode_attention) against the kKvPaged path (K|V written to the paged
+    layout, attention reads them): two engines, same weights, prompts and
+    tokens, ACT blocks resident and streamed, ragged contexts (partially filled
+    last blocks, 128-row tiles shared by several requests). The same f16 K|V
+    meet the same queries, so the outputs agree to accumulation order, and both
+    match the oracle."""
+    from paper_2501_01792_b200.api import HostAllocation, PoolCaps
+    H = 4
+    cfg = small_cfg(L=2, d=H * hd, H=H, f=512, tpb=tpb)
+    w = oracle_weights(cfg, max_seq=160)
+    rng = np.random.default_rng(hd + tpb)
+    B = 9
+    lens = rng.integers(1, 120, B).tolist()
+    per = max(-(-(n + 4) // tpb) for n in lens) + 1
+    caps = PoolCaps(kv_host=B * per, act_host=B * per, act_gpu=B * per // 3)
+    engs = [make_engine(cfg, w, max_batch=B, max_seq=160, caps=caps, mode="hybrid", allocation=HostAllocation(3, 1),
+                        weights_on_device=False, scaled=scaled, fused=f) for f in (True, False)]
+    ids = [f"f{i}" for i in range(B)]
+    prompts = [rng.integers(0, cfg.vocab_size, n).tolist() for n in lens]
+    for e in engs:
+        e.prefill(ids, prompts)
+    seqs = [list(p) for p in prompts]
+    for step in range(3):
+        toks = rng.integers(0, cfg.vocab_size, B).tolist()
+        fused, paged = (e.decode_step(ids, toks, want_x=True, want_logits=True) for e in engs)
+        assert rel(f64(fused["x"]), f64(paged["x"])) <= 2e-3, step
+        assert rel(fused["logits"], paged["logits"]) <= 2e-3, step
+        for b in range(B):
+            seqs[b].append(toks[b])
+            ref = O.forward_prompt(seqs[b], w, scaled=scaled).output[-1]
+            assert rel(f64(fused["x"][b]), ref) <= TOL, (step, b)
+    assert engs[0].last_stats()["recompute_rows"] > 0
 
 
 def test_engine_rejects_unsupported_block_size(native):
