@@ -265,6 +265,14 @@ int hc_gemm_f16(int epi, int M, int N, int K, const uint16_t* A, const uint16_t*
 /* Split-K weight-streaming GEMM (epi 0 / 1), fp32 partials reduced in a second kernel. */
 int hc_gemm_f16_splitk(int epi, int M, int N, int K, const uint16_t* A, const uint16_t* Wt, uint16_t* out, int bn,
                         int splits);
+/* Weight-streaming decode GEMM (swap-AB, stream-K over `ctas` CTAs, 0 = one per SM; M <= 256):
+ * C = A . W (+ bias) (+ res), relu for epi 1, fp32 for epi 3 — the M = batch projections of
+ * qkv_generate / project_ffn (decoder.cpp:97-121); cut units are summed by a second, dependent kernel. */
+int hc_gemm_f16_wstream(int epi, int M, int N, int K, const uint16_t* A, const uint16_t* Wt, const uint16_t* bias,
+                        const uint16_t* res, void* out, int ctas);
+/* Device microseconds per launch of one decode GEMM (M x N x K, epi 0/1/3) over `reps` back-to-back
+ * launches with W streamed from HBM; mode 0 tile kernel + split-K, 1 weight-streaming kernel. */
+int hc_gemm_bench(int M, int N, int K, int epi, int mode, int reps, double* us_per_call);
 /* recompute_kv_from_activation (decoder.cpp:123-129) into the paged layout. */
 int hc_recompute_kv_paged(int n_blocks, int tpb, int d, int heads, const uint16_t* act_pool, const uint16_t* wkv_t,
                           const int* tiles, int n_tiles, uint16_t* kv_out, int bn);

@@ -109,6 +109,8 @@ SIGNATURES = {
     # kernels (host buffers in / out)
     "hc_gemm_f16": (i, [i, i, i, i, u16p, u16p, vp, i]),
     "hc_gemm_f16_splitk": (i, [i, i, i, i, u16p, u16p, u16p, i, i]),
+    "hc_gemm_f16_wstream": (i, [i, i, i, i, u16p, u16p, u16p, u16p, vp, i]),
+    "hc_gemm_bench": (i, [i, i, i, i, i, i, dp]),
     "hc_recompute_kv_paged": (i, [i, i, i, i, u16p, u16p, ip, i, u16p, i]),
     "hc_decode_attention": (i, [i, i, i, i, u16p, u16p, l, u16p, l, ip, i, ip, ip, i, i, u16p]),
     "hc_prefill_attention": (i, [i, i, i, i, u16p, i, u16p]),

@@ -3,6 +3,7 @@
 // path and copies the result back — the boundary the parity tests drive.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstring>
 #include <stdexcept>
 #include <string>
@@ -99,6 +100,104 @@ int hc_gemm_f16_splitk(int epi, int M, int N, int K, const uint16_t* A, const ui
         HC_CUDA(cudaGetLastError());
         HC_CUDA(cudaDeviceSynchronize());
         o.to_host(out);
+    });
+}
+
+// The weight-streaming decode GEMM (wstream.cuh: swap-AB, stream-K over
+// `ctas` CTAs, 0 = one per SM) with the f16 epilogue operands of the OPT
+// projections: C = A . W (+ bias[n]) (+ res[m][n]) (relu for epi 1); epi 3 fp32.
+int hc_gemm_f16_wstream(int epi, int M, int N, int K, const uint16_t* A, const uint16_t* Wt, const uint16_t* bias,
+                        const uint16_t* res, void* out, int ctas) {
+    return hc_guard([&] {
+        if (epi != gemm::kStore && epi != gemm::kRelu && epi != gemm::kF32)
+            throw hc_input_error("hc_gemm_f16_wstream: epi must be 0, 1 or 3");
+        if (M < 1 || M > 256 || N < 16 || N % 16 || K < 8 || K % 8)
+            throw hc_input_error("hc_gemm_f16_wstream: needs 1 <= M <= 256, N % 16 == 0, K % 8 == 0");
+        if (epi == gemm::kF32 && (bias || res)) throw hc_input_error("hc_gemm_f16_wstream: fp32 output takes no bias / res");
+        DevBuf<uint16_t> a(A, size_t(M) * K), w(Wt, size_t(N) * K);
+        DevBuf<uint16_t> b(bias, bias ? size_t(N) : 0), r(res, res ? size_t(M) * N : 0);
+        const size_t out_bytes = size_t(M) * N * (epi == gemm::kF32 ? 4 : 2);
+        DevBuf<uint8_t> o(out_bytes);
+        DevBuf<float> ws(wstream_ws_floats(M));
+        GemmCall c;
+        c.epi = epi;
+        c.A = reinterpret_cast<const f16*>(a.p);
+        c.lda = K;
+        c.a_rows = M;
+        c.B = reinterpret_cast<const f16*>(w.p);
+        c.ldb = K;
+        c.M = M;
+        c.N = N;
+        c.K = K;
+        c.out = o.p;
+        c.ldc = N;
+        c.bias = bias ? reinterpret_cast<const f16*>(b.p) : nullptr;
+        c.res = res ? reinterpret_cast<const f16*>(r.p) : nullptr;
+        c.ldr = N;
+        c.ws = ws.p;
+        c.ws_floats = ws.n;
+        c.max_ctas = ctas;
+        if (!run_wstream(c, nullptr)) throw hc_input_error("hc_gemm_f16_wstream: shape not supported (or HC_WSTREAM=0)");
+        HC_CUDA(cudaGetLastError());
+        HC_CUDA(cudaDeviceSynchronize());
+        o.to_host(static_cast<uint8_t*>(out));
+    });
+}
+
+// Device time of one decode GEMM C[M x N] = A . W (W [N x K]) per launch, over
+// `reps` back-to-back launches cycling through enough copies of W that none is
+// L2-resident (weights stream from HBM as in a decode step). mode 0: the tile
+// kernel with split-K + reduce (the planner's pick), 1: the weight-streaming
+// kernel (wstream.cuh), 2: the same launched programmatically dependent (its
+// weight prefetch overlaps the previous launch's tail). Measurement helper (scripts/decode_gemm_bench.py).
+int hc_gemm_bench(int M, int N, int K, int epi, int mode, int reps, double* us_per_call) {
+    return hc_guard([&] {
+        if (M < 1 || N < 16 || K < 64 || reps < 1 || !us_per_call) throw hc_input_error("hc_gemm_bench: bad shape");
+        const size_t wbytes = size_t(N) * K * 2;
+        const int copies = std::max<int>(2, static_cast<int>((512ull << 20) / wbytes) + 1);
+        DevBuf<uint16_t> a(size_t(M) * K), w(size_t(N) * K * copies), o(size_t(M) * N * 2);
+        HC_CUDA(cudaMemset(a.p, 0x11, a.n * 2));
+        HC_CUDA(cudaMemset(w.p, 0x11, w.n * 2));
+        const size_t wsf = std::max(size_t(16) * M * N, wstream_ws_floats(M));
+        DevBuf<float> ws(wsf);
+        GemmCall c;
+        c.epi = epi;
+        c.A = reinterpret_cast<const f16*>(a.p);
+        c.lda = K;
+        c.a_rows = M;
+        c.ldb = K;
+        c.M = M;
+        c.N = N;
+        c.K = K;
+        c.out = o.p;
+        c.ldc = N;
+        c.ws = ws.p;
+        c.ws_floats = ws.n;
+        auto launch = [&](int i) {
+            c.B = reinterpret_cast<const f16*>(w.p) + size_t(i % copies) * N * K;
+            c.pdl = mode == 2;
+            if (mode >= 1) {
+                if (!run_wstream(c, nullptr)) throw hc_input_error("hc_gemm_bench: wstream does not take this shape");
+            } else {
+                GemmCall t = c;
+                t.splits = 0;
+                run_gemm_tiled(t, nullptr);
+            }
+        };
+        for (int i = 0; i < 3; ++i) launch(i);
+        cudaEvent_t e0, e1;
+        HC_CUDA(cudaEventCreate(&e0));
+        HC_CUDA(cudaEventCreate(&e1));
+        HC_CUDA(cudaEventRecord(e0, nullptr));
+        for (int i = 0; i < reps; ++i) launch(i);
+        HC_CUDA(cudaEventRecord(e1, nullptr));
+        HC_CUDA(cudaEventSynchronize(e1));
+        float ms = 0.f;
+        HC_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        HC_CUDA(cudaGetLastError());
+        *us_per_call = ms * 1e3 / reps;
     });
 }
 

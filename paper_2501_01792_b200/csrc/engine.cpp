@@ -76,7 +76,7 @@ T* halloc(size_t n, bool mapped) {
 }  // namespace
 
 void gemm_rows(int epi, const f16* A, int M, int K, const f16* W, int N, void* out, long long ldc, cudaStream_t st,
-               long long lda = 0, float* ws = nullptr, size_t ws_floats = 0, const f16* bias = nullptr,
+               long long lda = 0, const GemmScratch& sc = GemmScratch{}, const f16* bias = nullptr,
                const f16* res = nullptr, long long ldr = 0);
 
 struct Engine::Impl {
@@ -120,8 +120,12 @@ struct Engine::Impl {
     float* logits = nullptr;
     int* amax = nullptr;
     float* attn_work = nullptr;
-    float* splitk_ws = nullptr;  // split-K partials of the weight-streaming decode GEMMs
+    float* splitk_ws = nullptr;  // split-K / stream-K partials of the weight-streaming decode GEMMs
     size_t splitk_floats = 0;
+    // pdl: the tail GEMMs (proj / FFN1 / FFN2) always follow a kernel of this
+    // stream, so they may launch programmatically (weight prefetch under the
+    // predecessor's tail); off while profiling (span events sit between them)
+    GemmScratch scratch(bool pdl = false) const { return GemmScratch{splitk_ws, splitk_floats, pdl ? 1 : 0}; }
     size_t attn_work_elems = 0;
     int* d_meta = nullptr;
     int* h_meta = nullptr;
@@ -271,9 +275,11 @@ struct Engine::Impl {
     }
     // qkv [T x 3dg] = LN1(x) . Wqkv (+ b_qkv) for this rank's heads
     // (qkv_generate, decoder.cpp:97-103)
-    void qkv(const f16* W, const f16* xa, int T, f16* out, cudaStream_t st, float* ws = nullptr,
-             size_t wsf = 0) const {
-        gemm_rows(gemm::kStore, xa, T, d, W + off.wqkv, 3 * dg, out, 3 * dg, st, 0, ws, wsf, bias(W, off.bqkv));
+    void qkv(const f16* W, const f16* xa, int T, f16* out, cudaStream_t st,
+             const GemmScratch& sc = GemmScratch{}) const {
+        // no programmatic launch: QKV may follow a cross-stream event wait
+        const GemmScratch s{sc.ws, sc.floats, 0};
+        gemm_rows(gemm::kStore, xa, T, d, W + off.wqkv, 3 * dg, out, 3 * dg, st, 0, s, bias(W, off.bqkv));
     }
     // project_ffn (decoder.cpp:113-121) of T attention rows [T x dg]; kArchOpt
     // adds the biases, the two residuals (x, then x') and LN2. Head-sharded:
@@ -281,24 +287,24 @@ struct Engine::Impl {
     // all-reduce each completes (bias and residual enter once, on rank 0).
     // lnbuf may alias att.
     void tail(const f16* W, const f16* att, const f16* x, int T, f16* proj, f16* lnbuf, f16* h, f16* out,
-              cudaStream_t st, float* ws = nullptr, size_t wsf = 0) {
+              cudaStream_t st, const GemmScratch& sc = GemmScratch{}) {
         if (tpn == 1) {  // bias + residual fused into the GEMM epilogues
-            gemm_rows(gemm::kStore, att, T, d, W + off.wproj, d, proj, d, st, 0, ws, wsf, bias(W, off.bproj),
+            gemm_rows(gemm::kStore, att, T, d, W + off.wproj, d, proj, d, st, 0, sc, bias(W, off.bproj),
                       opt() ? x : nullptr, d);
             const f16* p2 = ln(W, 2, proj, T, lnbuf, st);
-            gemm_rows(gemm::kRelu, p2, T, d, W + off.w1, f, h, f, st, 0, ws, wsf, bias(W, off.b1));
-            gemm_rows(gemm::kStore, h, T, f, W + off.w2, d, out, d, st, 0, ws, wsf, bias(W, off.b2),
+            gemm_rows(gemm::kRelu, p2, T, d, W + off.w1, f, h, f, st, 0, sc, bias(W, off.b1));
+            gemm_rows(gemm::kStore, h, T, f, W + off.w2, d, out, d, st, 0, sc, bias(W, off.b2),
                       opt() ? proj : nullptr, d);
             return;
         }
         // head-sharded: fp32 partial sums -> all-reduce -> + bias + residual
         float* r = ensure_red(static_cast<size_t>(T) * d);
-        gemm_rows(gemm::kF32, att, T, dg, W + off.wproj, d, r, d, st, 0, ws, wsf);
+        gemm_rows(gemm::kF32, att, T, dg, W + off.wproj, d, r, d, st, 0, sc);
         tp->all_reduce_sum(r, static_cast<size_t>(T) * d, st);
         add_bias_residual(r, bias(W, off.bproj), opt() ? x : nullptr, d, T, d, proj, st);
         const f16* p2 = ln(W, 2, proj, T, lnbuf, st);
-        gemm_rows(gemm::kRelu, p2, T, d, W + off.w1, fg, h, fg, st, 0, ws, wsf, bias(W, off.b1));
-        gemm_rows(gemm::kF32, h, T, fg, W + off.w2, d, r, d, st, 0, ws, wsf);
+        gemm_rows(gemm::kRelu, p2, T, d, W + off.w1, fg, h, fg, st, 0, sc, bias(W, off.b1));
+        gemm_rows(gemm::kF32, h, T, fg, W + off.w2, d, r, d, st, 0, sc);
         tp->all_reduce_sum(r, static_cast<size_t>(T) * d, st);
         add_bias_residual(r, bias(W, off.b2), opt() ? proj : nullptr, d, T, d, out, st);
     }
@@ -578,7 +584,7 @@ void Engine::init(const ModelConfig& c, int w_max_seq, const uint16_t* emb, cons
     m.hbuf = dalloc<f16>(static_cast<size_t>(m.B) * m.f);
     m.logits = dalloc<float>(static_cast<size_t>(m.B) * m.V);
     m.amax = dalloc<int>(m.B);
-    m.splitk_floats = static_cast<size_t>(16) * m.B * std::max(3 * m.d, m.f);
+    m.splitk_floats = std::max(static_cast<size_t>(16) * m.B * std::max(3 * m.d, m.f), wstream_ws_floats(m.B));
     m.splitk_ws = dalloc<float>(m.splitk_floats);
     configure_cache(PoolCaps{opt_.kv_host_cap, opt_.kv_gpu_cap, opt_.act_host_cap, opt_.act_gpu_cap}, opt_.kv_on_gpu != 0,
                     opt_.mode, opt_.alloc, opt_.host_layers, opt_.recompute_ratio);
@@ -855,7 +861,7 @@ void Engine::run_layers(int T, int l0, int l1, const int* d_cu, uint16_t* layer_
 // ---------------------------------------------------------------------------
 // GEMM helpers (weights transposed [out][in]; see model.hpp)
 void gemm_rows(int epi, const f16* A, int M, int K, const f16* W, int N, void* out, long long ldc, cudaStream_t st,
-               long long lda, float* ws, size_t ws_floats, const f16* bias, const f16* res, long long ldr) {
+               long long lda, const GemmScratch& sc, const f16* bias, const f16* res, long long ldr) {
     GemmCall c;
     c.epi = epi;
     c.A = A;
@@ -868,8 +874,9 @@ void gemm_rows(int epi, const f16* A, int M, int K, const f16* W, int N, void* o
     c.K = K;
     c.out = out;
     c.ldc = ldc;
-    c.ws = ws;
-    c.ws_floats = ws_floats;
+    c.ws = sc.ws;
+    c.ws_floats = sc.floats;
+    c.pdl = sc.pdl;
     c.bias = bias;
     c.res = res;
     c.ldr = ldr;
@@ -1634,7 +1641,7 @@ void Engine::decode_step(const std::vector<std::string>& ids_in, const int* toke
                     };
                     if (!m.fused) recompute();
                     m.span_begin(profile_, s_compute_, 2);
-                    m.qkv(W, xa, nb, qkvb, s_compute_, m.splitk_ws, m.splitk_floats);
+                    m.qkv(W, xa, nb, qkvb, s_compute_, m.scratch());
                     m.span_end(profile_, s_compute_);
                     if (m.fused) recompute();
                     if (U.any_kv) {  // new token's K|V -> its KV slot (device + host)
@@ -1672,7 +1679,7 @@ void Engine::decode_step(const std::vector<std::string>& ids_in, const int* toke
                     m.span_end(profile_, s_compute_);
                     m.span_begin(profile_, s_compute_, 2);
                     m.tail(W, att, xin + rd, nb, m.proj + rd, att, m.hbuf + static_cast<size_t>(r0) * m.fg,
-                           xout + rd, s_compute_, m.splitk_ws, m.splitk_floats);
+                           xout + rd, s_compute_, m.scratch(!profile_));
                     m.span_end(profile_, s_compute_);
                     st.launches += 1 + m.tail_launches() + (U.splits > 1 ? 2 : 1);
                 }
@@ -1694,7 +1701,7 @@ void Engine::decode_step(const std::vector<std::string>& ids_in, const int* toke
         const f16* xf = n ? m.final_norm(m.x[m.L & 1], n, m.xn, s_compute_) : m.x[m.L & 1];
         st.launches += n ? m.opt() : 0;
         if ((lo || ao) && n) {
-            gemm_rows(gemm::kF32, xf, n, m.d, m.emb, m.V, m.logits, m.V, s_compute_);
+            gemm_rows(gemm::kF32, xf, n, m.d, m.emb, m.V, m.logits, m.V, s_compute_, 0, m.scratch());
             st.launches += 1;
             if (ao) {
                 argmax_rows(m.logits, n, m.V, m.amax, s_compute_);

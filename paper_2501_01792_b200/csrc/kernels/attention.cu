@@ -58,6 +58,7 @@ __device__ __forceinline__ void unpack8(const uint4& u, float (&f)[8]) {
 template <int HD, int TPB>
 __global__ void __launch_bounds__(kWarps * 32)
     decode_attn_kernel(const AttnCall c) {
+    ptx::pdl_trigger();  // the projection GEMM after it may start streaming its weights
     constexpr int LPT = HD / 8;        // lanes per token row
     constexpr int TPW = 32 / LPT;      // token rows per warp-wide load
     constexpr int ITERS = TPB / TPW;   // loads per block per lane (K and V each)
@@ -227,6 +228,7 @@ __global__ void __launch_bounds__(kWarps * 32)
 
 template <int HD>
 __global__ void attn_combine_kernel(const AttnCall c) {
+    ptx::pdl_trigger();
     const int bh = blockIdx.x;
     const int b = bh / c.H;
     const int h = bh - b * c.H;

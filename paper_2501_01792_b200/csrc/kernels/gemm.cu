@@ -179,13 +179,26 @@ int num_sms() {
     return n;
 }
 
-void run_gemm(const GemmCall& c, cudaStream_t st) {
-    if (c.M <= 0 || c.N <= 0 || c.K <= 0) return;
+namespace {
+bool validate(const GemmCall& c) {  // false: an empty problem
+    if (c.M <= 0 || c.N <= 0 || c.K <= 0) return false;
     if (c.N % 16 != 0) throw std::invalid_argument("gemm: N must be a multiple of 16");
     if ((c.lda * 2) % 16 || (c.ldb * 2) % 16 || (c.K * 2) % 16)
         throw std::invalid_argument("gemm: row strides must be 16-byte multiples");
     if (reinterpret_cast<uintptr_t>(c.A) % 16 || reinterpret_cast<uintptr_t>(c.B) % 16)
         throw std::invalid_argument("gemm: operands must be 16-byte aligned");
+    return true;
+}
+}  // namespace
+
+void run_gemm(const GemmCall& c, cudaStream_t st) {
+    if (!validate(c)) return;
+    if (run_wstream(c, st)) return;  // decode-batch GEMMs: swap-AB stream-K weight streaming (wstream.cuh)
+    run_gemm_tiled(c, st);
+}
+
+void run_gemm_tiled(const GemmCall& c, cudaStream_t st) {
+    if (!validate(c)) return;
     gemm::Params p{};
     p.M = c.M;
     p.N = c.N;

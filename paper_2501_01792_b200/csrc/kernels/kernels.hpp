@@ -45,12 +45,28 @@ struct GemmCall {
     long long ldq = 0;
     float qscale = 1.f;
     float* part = nullptr;
+    // weight-streaming kernel: launch with programmatic stream serialisation
+    // (only when the previous operation on the stream is a kernel)
+    int pdl = 0;
 };
+// the decode GEMMs' workspace (split-K / stream-K fp32 partials): with ws and
+// neither splits nor bn forced, M <= 256 kStore / kRelu / kF32 GEMMs run the
+// weight-streaming kernel (wstream.cuh), which needs wstream_ws_floats(M)
+struct GemmScratch {
+    float* ws = nullptr;
+    size_t floats = 0;
+    int pdl = 0;  // GemmCall::pdl for the weight-streaming kernel
+};
+// fp32 partial slots the weight-streaming GEMM uses at batch M (0: M > 256)
+size_t wstream_ws_floats(int M);
+// the weight-streaming GEMM when c qualifies (returns false otherwise)
+bool run_wstream(const GemmCall& c, cudaStream_t st);
 // out[m][n] = f16(epi(sum_s ws[s][m][n] + bias[n] + res[m*ldr + n])) — the
 // split-K finish (relu, bias, res optional)
 void splitk_reduce(const float* ws, int splits, int M, int N, f16* out, bool relu, cudaStream_t st,
                    const f16* bias = nullptr, const f16* res = nullptr, long long ldr = 0);
 void run_gemm(const GemmCall& c, cudaStream_t st);
+void run_gemm_tiled(const GemmCall& c, cudaStream_t st);  // run_gemm without the weight-streaming dispatch
 int num_sms();
 
 // ----------------------------------------------------------- attention ----

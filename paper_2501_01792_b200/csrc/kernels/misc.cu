@@ -232,6 +232,7 @@ __device__ __forceinline__ float block_sum(float v, float* red) {
 __global__ void __launch_bounds__(kLnThreads)
     layernorm_kernel(const f16* __restrict__ x, long long ldx, const f16* __restrict__ g,
                      const f16* __restrict__ b, f16* __restrict__ y, long long ldy, int d, float eps) {
+    ptx::pdl_trigger();  // the FFN1 GEMM after LN2 may start streaming its weights
     __shared__ float red[kLnThreads / 32];
     const f16* xr = x + blockIdx.x * ldx;
     const int nch = d / 8;
@@ -294,6 +295,7 @@ __global__ void sum_rows_kernel(const float* __restrict__ src, int parts, size_t
 __global__ void add_bias_residual_kernel(const float* __restrict__ sum, const f16* __restrict__ bias,
                                          const f16* __restrict__ res, long long ldr, int M, int N,
                                          f16* __restrict__ out) {
+    ptx::pdl_trigger();
     const size_t n8 = static_cast<size_t>(M) * N / 8;
     for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n8;
          i += static_cast<size_t>(gridDim.x) * blockDim.x) {

@@ -234,6 +234,14 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint64_t* bar, uint32_t cta)
         : "memory");
 }
 
+// ---- programmatic dependent launch -------------------------------------------
+// let the next kernel of the stream launch now if it was launched with
+// programmatic stream serialisation (it must griddepcontrol.wait before
+// touching this kernel's outputs); a no-op for ordinary launches
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+// wait for the predecessor grid (complete, memory visible); a no-op without one
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // ---- misc ------------------------------------------------------------------
 __device__ __forceinline__ uint32_t pack_f16x2(float lo, float hi) {
     const __half2 v = __floats2half2_rn(lo, hi);

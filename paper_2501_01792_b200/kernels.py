@@ -50,6 +50,25 @@ def gemm_f16_splitk(a_bits: np.ndarray, wt_bits: np.ndarray, splits: int, epi: i
     return out
 
 
+def gemm_f16_wstream(a_bits: np.ndarray, wt_bits: np.ndarray, epi: int = 0, bias_bits=None, res_bits=None,
+                     ctas: int = 0) -> np.ndarray:
+    """Weight-streaming decode GEMM (swap-AB stream-K, M <= 256): C = A . W
+    (+ bias[n]) (+ res[m][n]), relu for epi 1, fp32 for epi 3; `ctas` CTAs
+    share the k-block iterations (0 = one per SM)."""
+    M, K = a_bits.shape
+    N, _ = wt_bits.shape
+    a, ap = _u16(a_bits)
+    w, wp = _u16(wt_bits)
+    bp = rp = None
+    if bias_bits is not None:
+        b, bp = _u16(bias_bits)
+    if res_bits is not None:
+        r, rp = _u16(res_bits)
+    out = np.zeros((M, N), dtype=np.float32 if epi == 3 else np.uint16)
+    check(lib().hc_gemm_f16_wstream(epi, M, N, K, ap, wp, bp, rp, out.ctypes.data_as(C.c_void_p), ctas))
+    return out
+
+
 def recompute_kv_paged(act_pool_bits: np.ndarray, wkv_t_bits: np.ndarray, heads: int,
                        tiles: np.ndarray, bn: int = 0) -> np.ndarray:
     """act_pool [n_blocks, tpb, d] -> kv [n_blocks, 2, H, tpb, hd] (f16 bits)."""

@@ -339,3 +339,45 @@ def test_recompute_fault_injection_is_caught(native):
         got = f64(recompute_kv_paged(act, w, H, np.array([0, 128], np.int32)))
         k = got[:, 0].transpose(0, 2, 1, 3).reshape(-1, d)
         assert (rel(k, want_k) > TOL_BF16) == caught
+
+
+@pytest.mark.parametrize("M,N,K,epi,ctas", [
+    (1, 256, 64, 0, 0), (4, 768, 256, 0, 0), (16, 512, 1000, 1, 0), (33, 1536, 4096, 0, 0),
+    (64, 12288, 4096, 0, 0), (64, 4096, 16384, 0, 0), (100, 2048, 2048, 1, 0), (128, 21504, 7168, 0, 0),
+    (128, 7168, 28672, 0, 0), (200, 1024, 512, 0, 0), (256, 640, 1088, 1, 0), (128, 50272, 1024, 3, 0),
+    (64, 2048, 4096, 0, 7), (48, 1024, 8192, 1, 3), (128, 1280, 640, 0, 148), (8, 272, 136, 3, 5),
+])
+def test_gemm_wstream(native, M, N, K, epi, ctas):
+    """Weight-streaming decode GEMM (swap-AB, stream-K, cut units summed by
+    the dependent reduce kernel): equals the fp64 product for every batch width
+    MP 16..256, ragged N / K (OOB boxes), units cut across 1..148 CTAs, relu /
+    fp32 epilogues."""
+    from paper_2501_01792_b200.kernels import gemm_f16_wstream
+    rng = np.random.default_rng(M * 31 + N + K + ctas)
+    a = rand_bits(rng, (M, K))
+    wt = rand_bits(rng, (N, K), 1.0 / np.sqrt(K))
+    ref = f64(a) @ f64(wt).T
+    if epi == 3:
+        got = gemm_f16_wstream(a, wt, 3, ctas=ctas).astype(np.float64)
+        assert rel(got, ref) <= 1e-4
+        return
+    if epi == 1:
+        ref = np.maximum(ref, 0)
+    got = f64(gemm_f16_wstream(a, wt, epi, ctas=ctas))
+    assert rel(got, ref) <= TOL_BF16
+
+
+@pytest.mark.parametrize("M,N,K,relu", [(64, 768, 512, False), (128, 1024, 3000, True), (5, 4096, 256, False)])
+def test_gemm_wstream_bias_residual(native, M, N, K, relu):
+    """The OPT projections' epilogue: C = relu?(A . W + bias[n] + res[m][n])."""
+    from paper_2501_01792_b200.kernels import gemm_f16_wstream
+    rng = np.random.default_rng(N + K)
+    a = rand_bits(rng, (M, K))
+    wt = rand_bits(rng, (N, K), 1.0 / np.sqrt(K))
+    bias = rand_bits(rng, (N,), 0.5)
+    res = rand_bits(rng, (M, N))
+    ref = f64(a) @ f64(wt).T + f64(bias)[None, :] + f64(res)
+    if relu:
+        ref = np.maximum(ref, 0)
+    got = f64(gemm_f16_wstream(a, wt, 1 if relu else 0, bias, res, ctas=37))
+    assert rel(got, ref) <= TOL_BF16
