@@ -35,11 +35,13 @@ METRIC = "generated tokens/sec, OPT-30B offloaded, per KV:ACT ratio, at 1/2/4/8 
 # all-gather bus bandwidth measured on B200 NVSwitch nodes (725 GB/s;
 # /opt/skills/guides/B200_PROFILING.md; peer copies reach 770 GB/s per direction)
 NVLINK_BUSBW = 725e9
-# recompute GEMM DRAM bytes per ACT row from ncu captures at OPT-30B width (scaled by rows in
-# the bench's roofline.traffic); kKvPaged: profiles/r02_ncu_recompute.txt (18.17 GB / 122880)
-RECOMPUTE_NCU_BYTES_PER_ROW = 18.17e9 / 122880
-RECOMPUTE_NCU_BYTES_PER_ROW_FUSED = 18.17e9 / 122880
-RECOMPUTE_NCU_NOTE = "kKvPaged 18.17 GB at 122880 rows, profiles/r02_ncu_recompute.txt"
+# recompute GEMM DRAM bytes per ACT row from ncu captures at OPT-30B width, default raster
+# (1-SM kernel, group_m 16, A kept in L2), scaled by rows in the bench's roofline.traffic:
+# profiles/r02_recompute_dram_sweep.txt and r02_ncu_recompute_fused.txt
+RECOMPUTE_NCU_BYTES_PER_ROW = (15.37e9 + 3.51e9) / 122880
+RECOMPUTE_NCU_BYTES_PER_ROW_FUSED = (14.22e9 + 0.23e9) / 122880
+RECOMPUTE_NCU_NOTE = ("fused (kAttnPart) 14.45 GB, kKvPaged 18.88 GB at 122880 rows; [Wk|Wv] (205 MB > L2) "
+                      "re-read once per 16-tile M group, profiles/r02_recompute_dram_sweep.txt")
 # best host->device rate of the standalone link probe on this pool's B200 boxes
 # (scripts/link_probe.py -> profiles/r01_link_probe.json: one copy stream,
 # >= 64 MB chunks; more streams or SM zero-copy reads add nothing)

@@ -281,17 +281,24 @@ void run_gemm_tiled(const GemmCall& c, cudaStream_t st) {
         const char* e = std::getenv("HC_GEMM_PAIR");
         return !(e && e[0] == '0');
     }();
-    // Sustained under the 1 kW cap (scripts/gemm_sustained.py, profiles/r02_gemm_sustained.txt):
-    // at K = 7168 the pair kernel runs 1.43-1.58 PFLOP/s against the 1-SM
-    // kernel's 1.15-1.21 (the 256 x 256 tile halves the smem / L2 feed per MAC),
-    // group_m 32 rows-of-128 (16 pair tiles) with the L2 hints
+    // Sustained under the 1 kW cap (scripts/gemm_sustained.py, 3 s back to back,
+    // profiles/r02_gemm_sustained.txt): at K = 4096 the pair kernel runs 1.75
+    // PFLOP/s against the 1-SM kernel's 1.61 (the 256 x 256 tile halves the
+    // smem / L2 feed per MAC); at K = 7168 [Wk|Wv] (205 MB) outgrows L2, the
+    // pair kernel's rasters re-read it to 26-40 GB of DRAM per 122880-row launch
+    // (1-SM: 14 GB, profiles/r02_recompute_dram_sweep.txt), and the extra HBM
+    // power costs it the clock: 1.58 vs 1.62 PFLOP/s (1432 vs 1560 MHz)
     static const int pair_max_k = [] {
         const char* e = std::getenv("HC_GEMM_PAIR_MAX_K");  // tuning knob
-        return e ? std::atoi(e) : 1 << 30;
+        return e ? std::atoi(e) : 4096;
     }();
     if (pair_ok && p.splits == 1 && !c.bn && p.num_m_tiles >= 8 && c.K <= pair_max_k && cc.epi != gemm::kSplitF32) {
         p.num_n_tiles = (c.N + gemm::Cfg2::BN - 1) / gemm::Cfg2::BN;
         p.group_m = c.group_m > 0 ? std::max(1, c.group_m / 2) : 16;
+        // weight-stationary by default: 16 N tiles (16 x 256 rows of B, 33.5 MB at
+        // K = 4096) stay in L2 while M is swept — 0.70 GB of DRAM per 33792-row
+        // recompute vs 1.06 GB for the M-grouped raster (r02_recompute_dram_sweep.txt)
+        if (!group_n_env && c.group_m <= 0) p.group_n = 16;
         if (const char* g = std::getenv("HC_GEMM_GROUP_M")) p.group_m = std::max(1, std::atoi(g) / 2);
         switch (cc.epi) {
             case gemm::kAttnPart: dispatch_attn<true>(cc, p, st); return;

@@ -7,7 +7,7 @@ back to back for ~`secs` seconds twice and reports the second window, with the
 median SM clock and power nvidia-smi saw during it.
 
     python scripts/gemm_sustained.py [--n 122880] [--width 7168] [--secs 3]
-        [--grid "pair=0,1;group=16,32;l2=0,5;fused=0,1"]
+        [--grid "pair=0,1;group=16,32;gn=0,16;l2=0,5;fused=0,1"]   (gn: weight-stationary raster)
 """
 import argparse
 import itertools
@@ -97,7 +97,7 @@ def main():
         st = dict(zip(keys, combo))
         env = {"HC_GEMM_PAIR": st.get("pair", "0"), "HC_GEMM_PAIR_MAX_K": "100000",
                "HC_GEMM_GROUP_M": st.get("group", "16"), "HC_GEMM_L2HINT": st.get("l2", "0"),
-               "HC_FUSED_RECOMPUTE": st.get("fused", "1")}
+               "HC_FUSED_RECOMPUTE": st.get("fused", "1"), "HC_GEMM_GROUP_N": st.get("gn", "0")}
         res = run(a.n, a.width, a.secs, env)
         print(json.dumps({"n": a.n, "width": a.width, **st, **res}), flush=True)
 
