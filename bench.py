@@ -927,8 +927,24 @@ def our_arm(args, cfg, world, rank, local, dist):
     if not args.no_sweep and world == 1:
         sweep_steps, sweep_warm = 2, 1
         sw_tokens = rng.integers(0, cfg.vocab_size, (sweep_steps + sweep_warm + 1, B)).astype(np.int32)
+        # B200 extension: the host-only min-step planner (csrc/host/plan.hpp) on the same bundle,
+        # Alg. 1's cost model plus the ACT blocks' own link time
+        min_step = None
+        if bp:
+            b7m = read_bundle(bp)
+            tbm = api.TimingBundle(api.LinearTimeModel(b7m[0], b7m[1]), api.LinearTimeModel(b7m[2], b7m[3]), b7m[4])
+            try:
+                r_ms, caps_ms, (tc_ms, tl_ms) = api.plan_host_min_step(cfg, B, math.ceil(ctx_mid / cfg.tokens_per_block),
+                                                                       tbm)
+                min_step = {"r": r_ms, "predicted_t_comp_ms_per_layer": tc_ms * 1e3,
+                            "predicted_t_link_ms_per_layer": tl_ms * 1e3, "bundle": os.path.relpath(bp, ROOT),
+                            "note": "plan_host_min_step: Alg. 1's cost model plus the ACT blocks' link time; "
+                                    "min over r of max(t_link, t_comp) per layer"}
+            except Exception as e:
+                min_step = {"error": str(e)}
         rs = sorted(set(float(x) for x in args.sweep.split(",") if x and not x.startswith("tr")) | {r} |
-                    ({planner["planned_r"]} if planner and "planned_r" in planner else set()))
+                    ({planner["planned_r"]} if planner and "planned_r" in planner else set()) |
+                    ({round(min_step["r"], 4)} if min_step and "r" in min_step else set()))
         per = []
         for tr in [float(x[2:]) for x in args.sweep.split(",") if x.startswith("tr")]:
             cm = pool_plan(cfg, B, ctx_mid, sweep_steps + sweep_warm + 1, 0.0)
@@ -952,6 +968,12 @@ def our_arm(args, cfg, world, rank, local, dist):
             except Exception as e:
                 per.append({"act_share_r": rr, "error": str(e)})
         extra["per_ratio"] = per
+        if min_step and "r" in min_step:
+            hit = [x for x in per if abs(x.get("act_share_r", -1) - round(min_step["r"], 4)) < 1e-4 and "tokens_per_s" in x]
+            if hit:
+                min_step["tokens_per_s"] = hit[0]["tokens_per_s"]
+                min_step["vs_alg1"] = hit[0]["tokens_per_s"] / value
+        extra["planner_min_step"] = min_step
         # B200 tiering: ACT blocks in HBM first (cache.cpp:85-91 placement),
         # sized to the free HBM; weights still streamed from pinned host memory
         try:

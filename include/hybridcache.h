@@ -104,6 +104,14 @@ int hc_plan_hbm_residency(const hc_model_config* cfg, long requests, long blocks
 int hc_plan_hbm_tiers(const hc_model_config* cfg, long requests, long blocks_per_request, double hbm_bytes,
                       double host_bytes, const double* bundle5, int weights_streamed, double* out_share, long* out4,
                       double* out_times2);
+/* Host-only plan minimising the predicted step (B200 extension of Alg. 1, whose
+ * planned_t_pcie, plan.cpp:166-168, leaves the ACT blocks' own link time out):
+ * x of N = requests * blocks_per_request host blocks as ACT minimising
+ * max(t_load_w + t_load_kv(KV + ACT-equivalent tokens), t_kv_gen(x tpb)) per layer
+ * within host_bytes (0 = unbounded). out2 = {act_host, kv_host} capacities
+ * (+ one block per request of rounding slack), out_times2 = {t_comp, t_link}. */
+int hc_plan_host_min_step(const hc_model_config* cfg, long requests, long blocks_per_request, double host_bytes,
+                          const double* bundle5, double* out_share, long* out2, double* out_times2);
 /* bundle_from_samples (timing.cpp:172-183) from MEASURED samples; out =
  * {kv slope, kv icept, kv r2, kv clamped, load slope, load icept, load r2,
  *  load clamped, t_load_w, s_weight_layer, s_weight_total} */

@@ -64,6 +64,7 @@ SIGNATURES = {
     "hc_plan_hbm_residency": (i, [cfgp, l, l, d, dp, lp]),
     "hc_plan_hbm_tiers": (i, [cfgp, l, l, d, d, dp, i, dp, lp, dp]),
     "hc_planned_times": (i, [dp, i, l, l, l, dp]),
+    "hc_plan_host_min_step": (i, [cfgp, l, l, d, dp, dp, lp, dp]),
     "hc_bundle_from_samples": (i, [dp, dp, i, dp, dp, i, d, cfgp, dp]),
     "hc_budget_for": (i, [d, cfgp, d, dp]),
     "hc_flop_count": (i, [i, cfgp, l, i, dp]),

@@ -357,6 +357,21 @@ def plan_hbm_tiers(cfg: ModelConfig, requests: int, blocks_per_request: int, hbm
     return r.value, PoolCaps(kv_host=out[3], kv_gpu=out[1], act_host=out[2], act_gpu=out[0]), tuple(t.tolist())
 
 
+def plan_host_min_step(cfg: ModelConfig, requests: int, blocks_per_request: int, bundle: TimingBundle,
+                       host_bytes: float = 0.0):
+    """Host-only plan minimising the predicted step (csrc/host/plan.hpp): Alg. 1's
+    cost model plus the ACT blocks' own link time. Returns (r, PoolCaps with the
+    host tiers, (t_comp, t_link) per layer)."""
+    c = cfg.to_c()
+    b, bp = bundle.arr5()
+    r = C.c_double()
+    out = (C.c_long * 2)()
+    t, tp = _darr(np.zeros(2))
+    check(lib().hc_plan_host_min_step(C.byref(c), requests, blocks_per_request, float(host_bytes), bp, C.byref(r),
+                                      out, tp))
+    return r.value, PoolCaps(act_host=out[0], kv_host=out[1]), tuple(t.tolist())
+
+
 def plan_host_allocation(bundle: TimingBundle, mem: MemoryBudget, tpb: int, act_gpu: int) -> HostAllocation:
     """plan.cpp:106-152 (paper Alg. 1 + frontier polish)."""
     b, bp = bundle.arr5()

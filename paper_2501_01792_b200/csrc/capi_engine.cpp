@@ -275,6 +275,19 @@ int hc_plan_hbm_tiers(const hc_model_config* cfg, long requests, long bpr, doubl
         times2[1] = p.t_link;
     });
 }
+int hc_plan_host_min_step(const hc_model_config* cfg, long requests, long bpr, double host_bytes, const double* b,
+                          double* share, long* out2, double* times2) {
+    return hc_guard([&] {
+        ModelConfig c = to_cfg(cfg);
+        c.validate();
+        const HostStepPlan p = plan_host_min_step(c, requests, bpr, bundle_of(b), host_bytes);
+        *share = p.act_share;
+        out2[0] = p.act_host;
+        out2[1] = p.kv_host;
+        times2[0] = p.t_comp;
+        times2[1] = p.t_link;
+    });
+}
 int hc_planned_times(const double* b, int tpb, long act_host, long kv_host, long act_gpu, double* out2) {
     return hc_guard([&] {
         HostAllocation a;

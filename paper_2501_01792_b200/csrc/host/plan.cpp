@@ -273,4 +273,34 @@ HbmTierPlan plan_hbm_tiers(const ModelConfig& c, long requests, long blocks_per_
     return best;
 }
 
+HostStepPlan plan_host_min_step(const ModelConfig& c, long requests, long blocks_per_request, const TimingBundle& b,
+                                double host_bytes) {
+    if (requests < 1 || blocks_per_request < 1) throw InputError("plan_host_min_step: empty workload");
+    if (host_bytes < 0) throw InputError("plan_host_min_step: negative host budget");
+    const double L = c.num_layers, tpb = c.tokens_per_block, B = static_cast<double>(requests);
+    const double kv_one = static_cast<double>(HybridCache::bytes_of(BlockKind::KV, c));
+    const double act_one = static_cast<double>(HybridCache::bytes_of(BlockKind::ACT, c));
+    const double ratio = act_one / kv_one;  // link cost of an ACT token in KV tokens
+    const long N = requests * blocks_per_request;
+    HostStepPlan best;
+    double best_t = -1;
+    for (long x = 0; x <= N; ++x) {
+        const double slack = x > 0 && x < N ? B : 0.0;
+        if (host_bytes > 0 && ((N - x + slack) * kv_one + (x + slack) * act_one) * L > host_bytes) continue;
+        const double tc = x > 0 ? eval(b.t_kv_gen, static_cast<double>(x) * tpb) : 0.0;
+        const double tl = b.t_load_w + eval(b.t_load_kv, (static_cast<double>(N - x) + x * ratio) * tpb);
+        const double t = std::max(tc, tl);
+        if (best_t < 0 || t < best_t) {
+            best_t = t;
+            best.act_share = static_cast<double>(x) / N;
+            best.act_host = x + static_cast<long>(slack);
+            best.kv_host = N - x + static_cast<long>(slack);
+            best.t_comp = tc;
+            best.t_link = tl;
+        }
+    }
+    if (best_t < 0) throw CapacityError("plan_host_min_step: pinned host memory cannot hold the workload");
+    return best;
+}
+
 }  // namespace hc

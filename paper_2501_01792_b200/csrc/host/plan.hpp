@@ -101,6 +101,26 @@ struct HbmTierPlan : HbmPlan {
 HbmTierPlan plan_hbm_tiers(const ModelConfig& c, long requests, long blocks_per_request, double hbm_bytes,
                            const TimingBundle& b, double host_bytes = 0, bool weights_streamed = false);
 
+// Host-only plan minimising the predicted step (B200 extension of Alg. 1).
+// Alg. 1's t_pcie (planned_t_pcie, plan.cpp:166-168) prices the weights and
+// the KV host blocks only, but an ACT host block crosses the link too (d*2
+// bytes per token against the KV block's 2*d*2). While recompute is cheap
+// against the link — the B200 case: the recompute GEMM of a whole OPT-30B
+// context takes a quarter of its ACT transfer — that term decides the ratio.
+// Over x ACT blocks of the N = requests * blocks_per_request host blocks:
+//   t_link(x) = t_load_w + t_load_kv((N - x) tpb + x tpb s_act / s_kv)
+//   t_comp(x) = t_kv_gen(x tpb)
+// minimise max(t_link, t_comp) per layer with the pinned host tiers
+// ((N - x) KV + x ACT blocks, all layers, + one block of rounding slack per
+// request of each kind for 0 < x < N) inside host_bytes (0 = unbounded).
+struct HostStepPlan {
+    double act_share = 0;  // r = x / N
+    long act_host = 0, kv_host = 0;  // pool capacities (blocks)
+    double t_comp = 0, t_link = 0;   // predicted per-layer seconds
+};
+HostStepPlan plan_host_min_step(const ModelConfig& c, long requests, long blocks_per_request, const TimingBundle& b,
+                                double host_bytes = 0);
+
 // FLOP model (flops.cpp:7-37); kinds: 0 KvGen, 1 QkvGen, 2 Attention,
 // 3 ProjFfn, 4 TokenRecomputeToLayerK, 5 FullLayer.
 double flop_count(int kind, const ModelConfig& c, long n_tokens, int k = 0);

@@ -376,3 +376,58 @@ def test_plan_hbm_tiers_host_budget(host_gb):
     assert caps.kv_host * kv_all + caps.act_host * act_all <= host_gb * 1e9
     r_free, _, _ = api.plan_hbm_tiers(cfg, B, nb, 56e9, bundle)
     assert r >= r_free
+
+
+def _host_min_step_restated(cfg, B, nb, b, host=0.0):
+    """Python restatement of plan_host_min_step (csrc/host/plan.hpp)."""
+    from paper_2501_01792_b200 import api
+    L, tpb = cfg.num_layers, cfg.tokens_per_block
+    kv_one, act_one = api.HybridCache.bytes_of("KV", cfg), api.HybridCache.bytes_of("ACT", cfg)
+    N = B * nb
+    ev = lambda m, n: m.intercept + m.slope * n  # noqa: E731  (eval, timing.cpp:75-77)
+    best = None
+    for x in range(N + 1):
+        slack = B if 0 < x < N else 0
+        if host > 0 and ((N - x + slack) * kv_one + (x + slack) * act_one) * L > host:
+            continue
+        tc = ev(b.t_kv_gen, x * tpb) if x > 0 else 0.0
+        tl = b.t_load_w + ev(b.t_load_kv, ((N - x) + x * act_one / kv_one) * tpb)
+        if best is None or max(tc, tl) < best[0]:
+            best = (max(tc, tl), x, slack, tc, tl)
+    _, x, slack, tc, tl = best
+    return x / N, x + slack, N - x + slack, tc, tl
+
+
+@pytest.mark.parametrize("gen,host_gb", [(None, 0.0), (None, 140.0), (2.5e-6, 0.0), (1e-4, 0.0)])
+def test_plan_host_min_step(gen, host_gb):
+    """Host-only min-step planner (B200 extension): equals its restatement; on the
+    committed B200 bundle at config 3 (OPT-30B, B 128, context 1152) the link
+    dominates even at r = 1, so it picks pure ACT (the measured per-ratio sweep's
+    fastest, 43.8 vs Alg. 1's 42.5 tok/s); with costly recompute it balances the
+    two channels; with prohibitive recompute it keeps nearly all KV; a host budget that
+    cannot hold all-KV pushes it towards ACT."""
+    import json
+    import os
+    from paper_2501_01792_b200 import api
+    bj = json.load(open(os.path.join(os.path.dirname(os.path.dirname(__file__)), "profiles",
+                                     "planner_bundle_opt-30b.json")))
+    cfg = api.ModelConfig.preset("opt-30b")
+    b = api.TimingBundle(api.LinearTimeModel(gen if gen else bj["kv_gen"]["slope"], bj["kv_gen"]["intercept"]),
+                         api.LinearTimeModel(bj["load_kv"]["slope"], bj["load_kv"]["intercept"]), bj["t_load_w"])
+    B, nb = 128, 72  # 1152 tokens of context per request
+    r, caps, (tc, tl) = api.plan_host_min_step(cfg, B, nb, b, host_gb * 1e9)
+    r2, ah, kh, tc2, tl2 = _host_min_step_restated(cfg, B, nb, b, host_gb * 1e9)
+    assert r == pytest.approx(r2) and (caps.act_host, caps.kv_host) == (ah, kh)
+    assert (tc, tl) == pytest.approx((tc2, tl2))
+    if gen is None and host_gb == 0:
+        assert r == 1.0 and tc < tl
+    elif gen == 2.5e-6:
+        assert 0 < r < 1 and abs(tc - tl) <= max(tc, tl) * 0.01
+    elif gen == 1e-4:  # recompute 190x dearer than streaming: only a sliver of ACT pays
+        assert 0 < r < 0.01 and abs(tc - tl) <= 16 * gen * 1.01
+    else:  # 140 GB cannot hold all-KV (194 GB): the budget binds
+        kv_all = api.HybridCache.bytes_of("KV", cfg) * cfg.num_layers
+        act_all = api.HybridCache.bytes_of("ACT", cfg) * cfg.num_layers
+        assert caps.kv_host * kv_all + caps.act_host * act_all <= 140e9
+    with pytest.raises(api.InputError):
+        api.plan_host_min_step(cfg, 0, nb, b)
