@@ -33,6 +33,11 @@ def main():
     a = kernels.f32_to_f16_bits(rng.uniform(-1, 1, (64, 1024)))
     w = kernels.f32_to_f16_bits(rng.uniform(-0.05, 0.05, (256, 1024)))
     kernels.gemm_f16_splitk(a, w, 4, 1, 128)
+    # weight-streaming decode GEMM: units cut over 7 CTAs (partials + reduce), whole units, bias + residual
+    bias = kernels.f32_to_f16_bits(rng.uniform(-1, 1, (256,)))
+    kernels.gemm_f16_wstream(a, w, 0, bias, kernels.f32_to_f16_bits(rng.uniform(-1, 1, (64, 256))), ctas=7)
+    kernels.gemm_f16_wstream(a[:5], w, 1, ctas=0)
+    kernels.gemm_f16_wstream(a, w, 3, ctas=3)
     q = kernels.f32_to_f16_bits(rng.uniform(-1, 1, (2, 256)))
     pool = kernels.f32_to_f16_bits(rng.uniform(-1, 1, (8, 2, 2, 16, 128)))
     refs = np.array([[0, 1, 2, 3], [4, 5, 6, 7]], np.int32)
