@@ -54,10 +54,11 @@ def parse():
     p.add_argument("--steps", type=int, default=5)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    p.add_argument("--config", type=int, default=3, choices=[3, 4],
+    p.add_argument("--config", type=int, default=3, choices=[3, 4, 5],
                    help="BASELINE configs[] entry (1-based): 3 = OPT-30B, 128 requests per GPU (weak scaling); "
                         "4 = OPT-66B fully offloaded, global batch 128 split across the ranks (strong scaling), "
-                        "planner-chosen ratio")
+                        "planner-chosen ratio; 5 = OPT-13B, prompt 2048, ratio sweep 0 -> 1 beside pure KV and the "
+                        "token-recompute baseline")
     p.add_argument("--model", default="")
     p.add_argument("--batch", type=int, default=0, help="requests per GPU (config 3 default 128)")
     p.add_argument("--global-batch", type=int, default=0, help="total requests split across ranks (config 4: 128)")
@@ -101,6 +102,12 @@ def parse():
                    help="time the whole generation instead: real prefill of P tokens + G decode steps, every step "
                         "timed (prints the measured generation line; minutes)")
     a = p.parse_args()
+    if a.config == 5:  # BASELINE configs[4]: the OPT-13B ratio sweep (batch 64 as SURVEY.md §8(d) sizes it)
+        a.model = a.model or "opt-13b"
+        a.prompt = 2048 if a.prompt == 1024 else a.prompt
+        a.batch = a.batch or 64
+        if a.sweep == "0,0.3333333333333333,0.5,1,tr0.5":
+            a.sweep = "0,0.25,0.5,0.75,1,tr0.5"
     if a.config == 4:
         a.model = a.model or "opt-66b"
         a.global_batch = a.global_batch or 128
@@ -929,15 +936,23 @@ def our_arm(args, cfg, world, rank, local, dist):
         sw_tokens = rng.integers(0, cfg.vocab_size, (sweep_steps + sweep_warm + 1, B)).astype(np.int32)
         # B200 extension: the host-only min-step planner (csrc/host/plan.hpp) on the same bundle,
         # Alg. 1's cost model plus the ACT blocks' own link time
-        min_step = None
+        min_step, tbm, src_ms = None, None, None
         if bp:
             b7m = read_bundle(bp)
             tbm = api.TimingBundle(api.LinearTimeModel(b7m[0], b7m[1]), api.LinearTimeModel(b7m[2], b7m[3]), b7m[4])
+            src_ms = os.path.relpath(bp, ROOT)
+        elif planner and "t_kv_gen" in planner:  # no committed bundle for this model: this run's calibration
+            tbm = api.TimingBundle(api.LinearTimeModel(planner["t_kv_gen"]["slope_s_per_token"],
+                                                       planner["t_kv_gen"]["intercept_s"]),
+                                   api.LinearTimeModel(planner["t_load_kv"]["slope_s_per_token"],
+                                                       planner["t_load_kv"]["intercept_s"]), planner["t_load_w_s"])
+            src_ms = "live calibration of this run"
+        if tbm is not None:
             try:
                 r_ms, caps_ms, (tc_ms, tl_ms) = api.plan_host_min_step(cfg, B, math.ceil(ctx_mid / cfg.tokens_per_block),
                                                                        tbm)
                 min_step = {"r": r_ms, "predicted_t_comp_ms_per_layer": tc_ms * 1e3,
-                            "predicted_t_link_ms_per_layer": tl_ms * 1e3, "bundle": os.path.relpath(bp, ROOT),
+                            "predicted_t_link_ms_per_layer": tl_ms * 1e3, "bundle": src_ms,
                             "note": "plan_host_min_step: Alg. 1's cost model plus the ACT blocks' link time; "
                                     "min over r of max(t_link, t_comp) per layer"}
             except Exception as e:

@@ -149,6 +149,11 @@ def test_config4_strong_split_covers_global_batch():
     b = bench.parse()
     assert b.model == "opt-30b" and b.scaling == "weak" and b.ratio == -1.0  # planner-chosen by default
     assert bench.per_rank_batch(b, 8, 7) == 128
+    sys.argv = ["bench.py", "--config", "5"]  # the OPT-13B ratio sweep
+    c = bench.parse()
+    assert (c.model, c.prompt, c.batch, c.scaling) == ("opt-13b", 2048, 64, "weak")
+    assert c.sweep.split(",")[:5] == ["0", "0.25", "0.5", "0.75", "1"] and "tr0.5" in c.sweep
+    sys.argv = ["bench.py"]
 
 
 def test_weight_share_group_selection(monkeypatch):
