@@ -77,6 +77,26 @@ def test_recompute_kv_paged(native, d, heads, nb, tpb):
     assert rel(got, ref) <= TOL_BF16
 
 
+@pytest.mark.parametrize("nb,d,heads", [(300, 512, 4), (560, 256, 2), (1100, 256, 2)])
+def test_recompute_kv_paged_many_groups(native, nb, d, heads):
+    """The 1-SM recompute over 38 / 70 / 138 M tiles: several rasterisation
+    groups including a partial last one, every tile exactly once."""
+    from paper_2501_01792_b200.kernels import recompute_kv_paged
+    rng = np.random.default_rng(nb + d)
+    tpb = 16
+    hd = d // heads
+    act = rand_bits(rng, (nb, tpb, d))
+    wkv = rand_bits(rng, (2 * d, d), 1.0 / np.sqrt(d))
+    tiles = np.arange(0, nb * tpb, 128, dtype=np.int32)
+    got = f64(recompute_kv_paged(act, wkv, heads, tiles, bn=256))
+    x = f64(act).reshape(nb * tpb, d)
+    kv = x @ f64(wkv).T
+    k, v = kv[:, :d], kv[:, d:]
+    ref = np.stack([k.reshape(nb, tpb, heads, hd).transpose(0, 2, 1, 3),
+                    v.reshape(nb, tpb, heads, hd).transpose(0, 2, 1, 3)], axis=1)
+    assert rel(got, ref) <= TOL_BF16
+
+
 def test_recompute_kv_paged_tile_subset(native):
     """Only listed 128-row tiles are recomputed; other blocks stay untouched."""
     from paper_2501_01792_b200.kernels import recompute_kv_paged
