@@ -1305,6 +1305,7 @@ void Engine::decode_step(const std::vector<std::string>& ids_in, const int* toke
         std::vector<int> info_h, info_g;
         int splits = 1;
         bool any_act = false, any_kv = false;
+        bool records_only = false;  // fused and every context block recomputed: the records-only attention
         size_t o_th = 0, o_tg = 0, o_ih = 0, o_ig = 0;
     };
     std::vector<Unit> units(M);
@@ -1355,6 +1356,7 @@ void Engine::decode_step(const std::vector<std::string>& ids_in, const int* toke
         U.tiles_g = tiles_of(actg, m.tpb);
         int max_ctx = 0;
         std::unordered_map<int, int> binfo_h, binfo_g;  // fused: block position -> request << 8 | valid
+        U.records_only = m.fused;
         for (int b = mb_row[u]; b < mb_row[u + 1]; ++b) {
             const int rcb = (rc_cu[b + 1] - rc_cu[b]) / m.tpb;
             const BlockTableEntry& e = grown[b].entry;
@@ -1374,11 +1376,13 @@ void Engine::decode_step(const std::vector<std::string>& ids_in, const int* toke
             ctx[b] = rcb * m.tpb + t.context_len();
             max_ctx = std::max(max_ctx, ctx[b]);
             int* rb = refs.data() + static_cast<size_t>(b) * m.max_blocks;
+            if (rcb > 0) U.records_only = false;
             for (int i = 0; i < rcb; ++i) *rb++ = pack_ref(R_TOKREC, b * m.max_blocks + i);
             for (size_t i = 0; i < t.entries.size(); ++i) {
                 const auto& en = t.entries[i];
                 const bool g = en.location == Location::GpuMem;
                 if (en.kind == BlockKind::KV) {
+                    U.records_only = false;
                     rb[i] = g ? pack_ref(R_KV_GPU, en.pbn) : pack_ref(R_KV_STAGE, kvp.at(en.pbn));
                 } else {
                     const int pos = g ? en.pbn : actp.at(en.pbn);
@@ -1673,6 +1677,7 @@ void Engine::decode_step(const std::vector<std::string>& ids_in, const int* toke
                     if (m.fused) {
                         a.part = m.part;
                         a.part_region = R_KVR;
+                        a.records_only = U.records_only ? 1 : 0;
                     }
                     m.span_begin(profile_, s_compute_, 1);
                     decode_attention(a, s_compute_);

@@ -55,7 +55,10 @@ __device__ __forceinline__ void unpack8(const uint4& u, float (&f)[8]) {
 }
 
 // grid: (B*H, splits); block: 128 threads (4 warps)
-template <int HD, int TPB>
+// REC: every block of the call is a fused-recompute block (c.records_only):
+// the K|V path compiles out, so the kernel holds few registers, runs more CTAs
+// per SM and keeps 8 records per warp in flight
+template <int HD, int TPB, bool REC = false>
 __global__ void __launch_bounds__(kWarps * 32)
     decode_attn_kernel(const AttnCall c) {
     ptx::pdl_trigger();  // the projection GEMM after it may start streaming its weights
@@ -99,90 +102,125 @@ __global__ void __launch_bounds__(kWarps * 32)
     // the next block's ref is loaded one iteration ahead, so a block's K|V (or
     // partial record) loads never wait on its ref
     int ref_next = blk_begin + warp < blk_end ? __ldg(refs + blk_begin + warp) : 0;
-    for (int blk = blk_begin + warp; blk < blk_end; blk += kWarps) {
+    constexpr int SEGS = TPB / SEG;
+    constexpr int RB = REC ? (SEGS >= 2 ? 2 : 4) : 1;  // records in flight per warp (the mixed kernel keeps its registers for K|V)
+    for (int blk = blk_begin + warp; blk < blk_end;) {
         const int ref = ref_next;
-        if (blk + kWarps < blk_end) ref_next = __ldg(refs + blk + kWarps);
-        if ((ref >> 28) == c.part_region) {
-            // partials of a recomputed block: o, m (log2 domain, scale folded in), l;
-            // every load of the block's records is issued before any math
-            float4 o0[TPB / SEG], o1[TPB / SEG];
-            float mp[TPB / SEG], lp[TPB / SEG];
+        if (REC || (ref >> 28) == c.part_region) {
+            // partials of recomputed blocks: o, m (log2 domain, scale folded in), l.
+            // Up to RB of this warp's next blocks that are recomputed ones go
+            // together: every record load is issued before any math (a record is
+            // 0.5 KB, so one per warp would leave the loads latency-bound)
+            int rr[RB];
+            rr[0] = ref;
+            int n = 1;
 #pragma unroll
-            for (int sg = 0; sg < TPB / SEG; ++sg) {
-                const float* rec =
-                    c.part + ((static_cast<long long>(ref & 0x0FFFFFFF) * (TPB / SEG) + sg) * c.H + h) * (HD + 4);
-                o0[sg] = __ldg(reinterpret_cast<const float4*>(rec + col));
-                o1[sg] = __ldg(reinterpret_cast<const float4*>(rec + col + 4));
-                mp[sg] = __ldg(rec + HD);
-                lp[sg] = __ldg(rec + HD + 1);
+            for (int k = 1; k < RB; ++k) {
+                const int bk = blk + k * kWarps;
+                if (n == k && bk < blk_end) {
+                    const int rk = __ldg(refs + bk);
+                    if (REC || (rk >> 28) == c.part_region) {
+                        rr[k] = rk;
+                        ++n;
+                    }
+                }
             }
+            float4 o0[RB][SEGS], o1[RB][SEGS];
+            float mp[RB][SEGS], lp[RB][SEGS];
 #pragma unroll
-            for (int sg = 0; sg < TPB / SEG; ++sg) {
-                const float m_new = fmaxf(m, mp[sg]);
-                const float corr = exp2f(m - m_new);
-                // one token group adds the record (the fold below sums the groups)
-                const float f = grp == 0 ? exp2f(mp[sg] - m_new) : 0.f;
-                l = l * corr + lp[sg] * f;
-                acc[0] = acc[0] * corr + o0[sg].x * f;
-                acc[1] = acc[1] * corr + o0[sg].y * f;
-                acc[2] = acc[2] * corr + o0[sg].z * f;
-                acc[3] = acc[3] * corr + o0[sg].w * f;
-                acc[4] = acc[4] * corr + o1[sg].x * f;
-                acc[5] = acc[5] * corr + o1[sg].y * f;
-                acc[6] = acc[6] * corr + o1[sg].z * f;
-                acc[7] = acc[7] * corr + o1[sg].w * f;
-                m = m_new;
+            for (int k = 0; k < RB; ++k) {
+                if (k < n) {
+#pragma unroll
+                    for (int sg = 0; sg < SEGS; ++sg) {
+                        const float* rec =
+                            c.part + ((static_cast<long long>(rr[k] & 0x0FFFFFFF) * SEGS + sg) * c.H + h) * (HD + 4);
+                        o0[k][sg] = __ldg(reinterpret_cast<const float4*>(rec + col));
+                        o1[k][sg] = __ldg(reinterpret_cast<const float4*>(rec + col + 4));
+                        mp[k][sg] = __ldg(rec + HD);
+                        lp[k][sg] = __ldg(rec + HD + 1);
+                    }
+                }
+            }
+            blk += n * kWarps;
+            if (blk < blk_end) ref_next = __ldg(refs + blk);
+#pragma unroll
+            for (int k = 0; k < RB; ++k) {
+                if (k < n) {
+#pragma unroll
+                    for (int sg = 0; sg < SEGS; ++sg) {
+                        const float m_new = fmaxf(m, mp[k][sg]);
+                        const float corr = exp2f(m - m_new);
+                        // one token group adds the record (the fold below sums the groups)
+                        const float f = grp == 0 ? exp2f(mp[k][sg] - m_new) : 0.f;
+                        l = l * corr + lp[k][sg] * f;
+                        acc[0] = acc[0] * corr + o0[k][sg].x * f;
+                        acc[1] = acc[1] * corr + o0[k][sg].y * f;
+                        acc[2] = acc[2] * corr + o0[k][sg].z * f;
+                        acc[3] = acc[3] * corr + o0[k][sg].w * f;
+                        acc[4] = acc[4] * corr + o1[k][sg].x * f;
+                        acc[5] = acc[5] * corr + o1[k][sg].y * f;
+                        acc[6] = acc[6] * corr + o1[k][sg].z * f;
+                        acc[7] = acc[7] * corr + o1[k][sg].w * f;
+                        m = m_new;
+                    }
+                }
             }
             continue;
         }
-        const f16* base = c.region[ref >> 28] + static_cast<long long>(ref & 0x0FFFFFFF) * block_elems + head_off;
-        const int valid = (blk == nb - 1) ? ctx - (nb - 1) * TPB : TPB;
-        uint4 kr[ITERS], vr[ITERS];
+        if constexpr (!REC) {
+            blk += kWarps;
+            if (blk < blk_end) ref_next = __ldg(refs + blk);
+            const int blk_cur = blk - kWarps;
+            const f16* base = c.region[ref >> 28] + static_cast<long long>(ref & 0x0FFFFFFF) * block_elems + head_off;
+            const int valid = (blk_cur == nb - 1) ? ctx - (nb - 1) * TPB : TPB;
+            uint4 kr[ITERS], vr[ITERS];
 #pragma unroll
-        for (int i = 0; i < ITERS; ++i) {
-            const int t = i * TPW + grp;
-            kr[i] = ldg16(base + t * HD + col);
-            vr[i] = ldg16(base + v_off + t * HD + col);
-        }
-        if (valid < TPB) {  // unfilled slots of the last block may hold any bits (even NaN): 0 * NaN != 0
+            for (int i = 0; i < ITERS; ++i) {
+                const int t = i * TPW + grp;
+                kr[i] = ldg16(base + t * HD + col);
+                vr[i] = ldg16(base + v_off + t * HD + col);
+            }
+            if (valid < TPB) {  // unfilled slots of the last block may hold any bits (even NaN): 0 * NaN != 0
 #pragma unroll
-            for (int i = 0; i < ITERS; ++i)
-                if (i * TPW + grp >= valid) vr[i] = make_uint4(0, 0, 0, 0);
-        }
-        float s[ITERS];
-        float bmax = -FLT_MAX;
+                for (int i = 0; i < ITERS; ++i)
+                    if (i * TPW + grp >= valid) vr[i] = make_uint4(0, 0, 0, 0);
+            }
+            float s[ITERS];
+            float bmax = -FLT_MAX;
 #pragma unroll
-        for (int i = 0; i < ITERS; ++i) {
-            float kf[8];
-            unpack8(kr[i], kf);
-            float dot = 0.f;
+            for (int i = 0; i < ITERS; ++i) {
+                float kf[8];
+                unpack8(kr[i], kf);
+                float dot = 0.f;
 #pragma unroll
-            for (int j = 0; j < 8; ++j) dot = fmaf(q[j], kf[j], dot);
+                for (int j = 0; j < 8; ++j) dot = fmaf(q[j], kf[j], dot);
 #pragma unroll
-            for (int o = LPT / 2; o >= 1; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
-            const int t = i * TPW + grp;
-            s[i] = t < valid ? dot : -FLT_MAX;
-            bmax = fmaxf(bmax, s[i]);
-        }
+                for (int o = LPT / 2; o >= 1; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+                const int t = i * TPW + grp;
+                s[i] = t < valid ? dot : -FLT_MAX;
+                bmax = fmaxf(bmax, s[i]);
+            }
 #pragma unroll
-        for (int o = LPT; o < 32; o <<= 1) bmax = fmaxf(bmax, __shfl_xor_sync(0xffffffffu, bmax, o));
-        const float m_new = fmaxf(m, bmax);
-        const float corr = exp2f(m - m_new);
-        l *= corr;
+            for (int o = LPT; o < 32; o <<= 1) bmax = fmaxf(bmax, __shfl_xor_sync(0xffffffffu, bmax, o));
+            const float m_new = fmaxf(m, bmax);
+            const float corr = exp2f(m - m_new);
+            l *= corr;
 #pragma unroll
-        for (int j = 0; j < 8; ++j) acc[j] *= corr;
-        m = m_new;
+            for (int j = 0; j < 8; ++j) acc[j] *= corr;
+            m = m_new;
 #pragma unroll
-        for (int i = 0; i < ITERS; ++i) {
-            const int t = i * TPW + grp;
-            const float pr = t < valid ? exp2f(s[i] - m) : 0.f;
-            l += pr;
-            float vf[8];
-            unpack8(vr[i], vf);
+            for (int i = 0; i < ITERS; ++i) {
+                const int t = i * TPW + grp;
+                const float pr = t < valid ? exp2f(s[i] - m) : 0.f;
+                l += pr;
+                float vf[8];
+                unpack8(vr[i], vf);
 #pragma unroll
-            for (int j = 0; j < 8; ++j) acc[j] = fmaf(pr, vf[j], acc[j]);
-        }
+                for (int j = 0; j < 8; ++j) acc[j] = fmaf(pr, vf[j], acc[j]);
+            }
+            }
     }
+
     // fold token groups of the warp (all share m)
 #pragma unroll
     for (int o = LPT; o < 32; o <<= 1) {
@@ -267,7 +305,10 @@ void decode_attention(const AttnCall& c, cudaStream_t st) {
     const dim3 grid(c.B * c.H, c.splits);
 #define HC_ATTN(HD_, TPB_)                                                       \
     if (c.hd == HD_ && c.tpb == TPB_) {                                          \
-        decode_attn_kernel<HD_, TPB_><<<grid, kWarps * 32, 0, st>>>(c);          \
+        if (c.records_only && c.part)                                            \
+            decode_attn_kernel<HD_, TPB_, true><<<grid, kWarps * 32, 0, st>>>(c);  \
+        else                                                                     \
+            decode_attn_kernel<HD_, TPB_><<<grid, kWarps * 32, 0, st>>>(c);      \
         if (c.splits > 1) attn_combine_kernel<HD_><<<c.B * c.H, HD_, 0, st>>>(c); \
         return;                                                                  \
     }

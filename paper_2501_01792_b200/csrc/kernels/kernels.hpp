@@ -94,6 +94,9 @@ struct AttnCall {
     // block's tpb / min(tpb, 32) records per head are merged instead of K|V
     const float* part = nullptr;
     int part_region = -1;
+    // every block ref of the call is in part_region (no K|V-cached block, no
+    // token-recompute block): the records-only kernel runs
+    int records_only = 0;
 };
 void decode_attention(const AttnCall& c, cudaStream_t st);
 // the (head_dim, tokens_per_block) pairs decode_attention is instantiated for
