@@ -3,6 +3,7 @@
 #include <atomic>
 #include <cstdlib>
 #include <stdexcept>
+#include <string>
 
 #include "kernels.hpp"
 #include "launch.hpp"
@@ -40,7 +41,8 @@ void launch_ws(const GemmCall& c, wstream::Params p, cudaStream_t st) {
         cfg.stream = st;
         cfg.attrs = attr;
         cfg.numAttrs = c.pdl ? 1 : 0;
-        cudaLaunchKernelEx(&cfg, kern, tw, tx, p);
+        const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, tw, tx, p);
+        if (e != cudaSuccess) throw std::runtime_error(std::string("wstream launch: ") + cudaGetErrorString(e));
     }
     // any CTA boundary inside a unit leaves partials to reduce
     bool cut = false;
@@ -53,7 +55,8 @@ void launch_ws(const GemmCall& c, wstream::Params p, cudaStream_t st) {
     cfg.stream = st;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, wstream::wstream_reduce_kernel<MP, EPI>, p);
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, wstream::wstream_reduce_kernel<MP, EPI>, p);
+    if (e != cudaSuccess) throw std::runtime_error(std::string("wstream reduce launch: ") + cudaGetErrorString(e));
 }
 
 template <int MP>
