@@ -1227,6 +1227,8 @@ def resident_variants(local, cfg, B, P, arch, steps=2, warmup=1, reserve=3e9, on
                          "capacity_only" if r == r_fit else ""))
     while jobs:
         r, caps, alloc, tag = jobs.pop(0)
+        retried = tag.startswith("retry:")
+        tag = tag[len("retry:"):] if retried else tag
         act_cap, kv_gpu = caps.act_gpu, caps.kv_gpu
         mode = "kv_only" if r <= 0 else ("act_only" if r >= 1 else "hybrid")
         host_need = caps.kv_host * kv_all + caps.act_host * act_all
@@ -1256,7 +1258,7 @@ def resident_variants(local, cfg, B, P, arch, steps=2, warmup=1, reserve=3e9, on
                                      "ms_per_step": ms, "kv_gpu_blocks": kv_gpu, "kv_host_blocks": caps.kv_host,
                                      "act_gpu_blocks": act_cap, "h2d_gb_per_step": acc["h2d"] / steps / 1e9,
                                      "planned": tag == "planned", "capacity_only": tag == "capacity_only",
-                                     "replanned": tag == "replanned"})
+                                     "replanned": tag == "replanned", "retried_host_alloc": retried})
             if tag == "planned" and prof["recompute_rows"] > 0 and prof["recompute_ms"] > 0:
                 # closed loop (north-star (5)): the recompute rate measured IN the step
                 # (power cap, concurrent DMA) replaces the isolated calibration slope,
@@ -1274,6 +1276,18 @@ def resident_variants(local, cfg, B, P, arch, steps=2, warmup=1, reserve=3e9, on
                 if caps2.act_gpu != caps_bal.act_gpu:
                     jobs.insert(0, (r2, caps2, tiered_alloc(caps2), "replanned"))
         except Exception as e:
+            if "cudaHostAlloc" in str(e) and not retried:
+                # page-locking the host tier can fail transiently while the OS
+                # reclaims the previous tier's pages: release every pool and retry once
+                try:
+                    eng.configure_cache(api.PoolCaps(), mode="act_only")
+                except Exception:
+                    pass
+                import gc
+                gc.collect()
+                time.sleep(5)
+                jobs.insert(0, (r, caps, alloc, "retry:" + tag))
+                continue
             out["per_ratio"].append({"act_share_r": round(r, 4), "error": str(e)})
     eng.close()
     return out
