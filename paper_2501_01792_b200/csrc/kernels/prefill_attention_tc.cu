@@ -402,7 +402,12 @@ __device__ __forceinline__ bool item_of(int w, int n_pairs, int H, int n_req, co
     return true;
 }
 
-template <int HD>  // head_dim 64 or 128
+// PT: P_t is written into TMEM over S_t's first columns (packed f16 pairs;
+// P_lo after it at head_dim 64) and O += P V reads it from there (tcgen05.mma
+// with A in TMEM) instead of a swizzled smem tile: no smem stores, no async-proxy
+// fence, no smem reads of P by the tensor core. S_t is in registers by then, and
+// S_t(j+1) is issued after PV_t(j) by the same thread (in-order completion).
+template <int HD, bool PT = false>  // head_dim 64 or 128
 __global__ void __launch_bounds__(kThreads2, 1)
     prefill_tc2_kernel(const __grid_constant__ CUtensorMap tm, f16* __restrict__ out, const int* __restrict__ cu,
                        int n_req, int n_pairs, int H, float scale, uint32_t v_lbo, uint32_t v_sbo) {
@@ -497,19 +502,28 @@ __global__ void __launch_bounds__(kThreads2, 1)
                 ++pc[t];
                 ptx::tc_fence_after();
                 const uint32_t pa = ptx::smem_u32(smem + Smem2<HD>::p + t * kTile), vb = slot_addr(g);
+                const uint32_t d_o = tmem + 256u + static_cast<uint32_t>(HD) * t;
 #pragma unroll
                 for (int k = 0; k < kT / 16; ++k) {
-                    const uint64_t a = ptx::sw128_kmajor_desc(pa + (k / 4) * kBox) + 2 * (k % 4);
                     const uint64_t bdesc = sw128_mnmajor_desc(vb + k * 16 * 128, v_lbo, v_sbo);
-                    ptx::mma_f16_ss(tmem + 256u + static_cast<uint32_t>(HD) * t, a, bdesc, id_o, (!first || k > 0) ? 1u : 0u);
+                    if constexpr (PT) {
+                        ptx::mma_f16_ts(d_o, tmem + 128u * t + 8u * k, bdesc, id_o, (!first || k > 0) ? 1u : 0u);
+                    } else {
+                        const uint64_t a = ptx::sw128_kmajor_desc(pa + (k / 4) * kBox) + 2 * (k % 4);
+                        ptx::mma_f16_ss(d_o, a, bdesc, id_o, (!first || k > 0) ? 1u : 0u);
+                    }
                 }
                 if constexpr (Smem2<HD>::lo) {  // + P_lo . V
                     const uint32_t pl = ptx::smem_u32(smem + Smem2<HD>::plo + t * kTile);
 #pragma unroll
                     for (int k = 0; k < kT / 16; ++k) {
-                        const uint64_t a = ptx::sw128_kmajor_desc(pl + (k / 4) * kBox) + 2 * (k % 4);
                         const uint64_t bdesc = sw128_mnmajor_desc(vb + k * 16 * 128, v_lbo, v_sbo);
-                        ptx::mma_f16_ss(tmem + 256u + static_cast<uint32_t>(HD) * t, a, bdesc, id_o, 1u);
+                        if constexpr (PT) {
+                            ptx::mma_f16_ts(d_o, tmem + 128u * t + 64u + 8u * k, bdesc, id_o, 1u);
+                        } else {
+                            const uint64_t a = ptx::sw128_kmajor_desc(pl + (k / 4) * kBox) + 2 * (k % 4);
+                            ptx::mma_f16_ss(d_o, a, bdesc, id_o, 1u);
+                        }
                     }
                 }
             };
@@ -599,6 +613,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
                 // of packed words is live at a time.
                 float2 l4[4] = {{0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}};
                 const float2 sl2 = make_float2(sl, sl), nm2 = make_float2(-m, -m);
+                uint32_t pt16[16], plt16[16];  // PT: 32 keys of packed P (and P_lo) per tcgen05.st
 #pragma unroll
                 for (int c = 0; c < kT / 8; ++c) {
                     uint32_t pw[4], plw[4];
@@ -615,11 +630,23 @@ __global__ void __launch_bounds__(kThreads2, 1)
                             plw[u] = ptx::pack_f16x2(pp.x - h.x, pp.y - h.y);
                         }
                     }
-                    const int box = c / 8, ch = c % 8;
-                    const uint32_t dst = pbase + box * kBox + ((ch ^ (r % 8)) * 16);
-                    sts128(dst, pw[0], pw[1], pw[2], pw[3]);
-                    if constexpr (Smem2<HD>::lo)
-                        sts128(dst + (Smem2<HD>::plo - Smem2<HD>::p), plw[0], plw[1], plw[2], plw[3]);
+                    if constexpr (PT) {  // P over S_t's columns [0, 64), P_lo over [64, 128)
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            pt16[(c % 4) * 4 + u] = pw[u];
+                            if constexpr (Smem2<HD>::lo) plt16[(c % 4) * 4 + u] = plw[u];
+                        }
+                        if (c % 4 == 3) {
+                            tmem_st_x16(t_s + lane_off + 16u * (c / 4), pt16);
+                            if constexpr (Smem2<HD>::lo) tmem_st_x16(t_s + lane_off + 64u + 16u * (c / 4), plt16);
+                        }
+                    } else {
+                        const int box = c / 8, ch = c % 8;
+                        const uint32_t dst = pbase + box * kBox + ((ch ^ (r % 8)) * 16);
+                        sts128(dst, pw[0], pw[1], pw[2], pw[3]);
+                        if constexpr (Smem2<HD>::lo)
+                            sts128(dst + (Smem2<HD>::plo - Smem2<HD>::p), plw[0], plw[1], plw[2], plw[3]);
+                    }
                 }
                 const float2 ls = fadd2(fadd2(l4[0], l4[1]), fadd2(l4[2], l4[3]));
                 l += ls.x + ls.y;
@@ -635,7 +662,10 @@ __global__ void __launch_bounds__(kThreads2, 1)
                     }
                     tmem_st_wait();
                 }
-                fence_async_smem();
+                if constexpr (PT)
+                    tmem_st_wait();  // P is in TMEM before the MMA lane is told
+                else
+                    fence_async_smem();
                 ptx::tc_fence_before();
                 ptx::mbar_arrive(&p_full[t]);
             }
@@ -683,8 +713,11 @@ bool prefill_attention_tc(const f16* qkv, long long rows, f16* out, const int* c
     static std::atomic<uint64_t> configured1{0}, configured2{0};
     max_dynamic_smem_once(prefill_tc_kernel, Smem::bytes, configured1);
     static std::atomic<uint64_t> configured3{0};
+    static std::atomic<uint64_t> configured4{0}, configured5{0};
     max_dynamic_smem_once(prefill_tc2_kernel<128>, Smem2<128>::bytes, configured2);
     max_dynamic_smem_once(prefill_tc2_kernel<64>, Smem2<64>::bytes, configured3);
+    max_dynamic_smem_once(prefill_tc2_kernel<128, true>, Smem2<128>::bytes, configured4);
+    max_dynamic_smem_once(prefill_tc2_kernel<64, true>, Smem2<64>::bytes, configured5);
     const long long d3 = 3LL * H * hd;
     const CUtensorMap tm = make_map(qkv, rows, d3, d3, kT);
     static const uint32_t lbo = [] {
@@ -708,9 +741,21 @@ bool prefill_attention_tc(const f16* qkv, long long rows, f16* out, const int* c
         const int n_pairs = (n_qt + 1) / 2;
         const long long items = static_cast<long long>(n_pairs) * H * n_req;
         const int grid = static_cast<int>(std::min<long long>(items, sms));
-        if (hd == 128)
+        // P kept in TMEM (TS-form P.V MMA): 1.4-2.2 % faster at head_dim 128 (P = 1024 / 2048),
+        // 6 % slower at 64 (its hi/lo split doubles the tcgen05.st traffic) — so 128 only by default
+        static const int p_tmem = [] {
+            const char* e = std::getenv("HC_PREFILL_PTMEM");  // 0: never, 1: head_dim 128 (default), 2: both
+            return e ? std::atoi(e) : 1;
+        }();
+        if (hd == 128 && p_tmem >= 1)
+            prefill_tc2_kernel<128, true><<<grid, kThreads2, Smem2<128>::bytes, st>>>(tm, out, cu, n_req, n_pairs, H,
+                                                                                       scale, lbo, sbo);
+        else if (hd == 128)
             prefill_tc2_kernel<128><<<grid, kThreads2, Smem2<128>::bytes, st>>>(tm, out, cu, n_req, n_pairs, H, scale,
                                                                                  lbo, sbo);
+        else if (p_tmem >= 2)
+            prefill_tc2_kernel<64, true><<<grid, kThreads2, Smem2<64>::bytes, st>>>(tm, out, cu, n_req, n_pairs, H,
+                                                                                     scale, lbo, sbo);
         else
             prefill_tc2_kernel<64><<<grid, kThreads2, Smem2<64>::bytes, st>>>(tm, out, cu, n_req, n_pairs, H, scale,
                                                                                lbo, sbo);
