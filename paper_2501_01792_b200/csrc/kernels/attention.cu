@@ -103,64 +103,68 @@ __global__ void __launch_bounds__(kWarps * 32)
     // partial record) loads never wait on its ref
     int ref_next = blk_begin + warp < blk_end ? __ldg(refs + blk_begin + warp) : 0;
     constexpr int SEGS = TPB / SEG;
-    constexpr int RB = REC ? (SEGS >= 2 ? 2 : 4) : 1;  // records in flight per warp (the mixed kernel keeps its registers for K|V)
+    constexpr int G = 32 / LPT;  // token groups per warp: each takes its own record
+    constexpr int RB = REC ? (SEGS >= 2 ? 2 : 4) : (SEGS >= 2 ? 1 : 2);  // records per group in flight (the mixed kernel keeps its registers for K|V)
     for (int blk = blk_begin + warp; blk < blk_end;) {
         const int ref = ref_next;
         if (REC || (ref >> 28) == c.part_region) {
             // partials of recomputed blocks: o, m (log2 domain, scale folded in), l.
-            // Up to RB of this warp's next blocks that are recomputed ones go
-            // together: every record load is issued before any math (a record is
-            // 0.5 KB, so one per warp would leave the loads latency-bound)
-            int rr[RB];
-            rr[0] = ref;
+            // The next n <= RB x G blocks of this warp that are recomputed ones go
+            // together, one per token group and slot (a record is 0.5 KB: one per
+            // warp would leave the loads latency-bound); every record load is issued
+            // before any math. Each lane keeps its own running (m, l, acc); the fold
+            // after the loop rescales the groups to a common max.
+            constexpr int NC = RB * G;
+            int rk[NC];
+            rk[0] = ref;
+#pragma unroll
+            for (int k = 1; k < NC; ++k) {
+                const int bk = blk + k * kWarps;
+                rk[k] = bk < blk_end ? __ldg(refs + bk) : -1;  // same address on every lane
+            }
             int n = 1;
 #pragma unroll
-            for (int k = 1; k < RB; ++k) {
-                const int bk = blk + k * kWarps;
-                if (n == k && bk < blk_end) {
-                    const int rk = __ldg(refs + bk);
-                    if (REC || (rk >> 28) == c.part_region) {
-                        rr[k] = rk;
-                        ++n;
-                    }
-                }
-            }
+            for (int k = 1; k < NC; ++k)
+                if (n == k && rk[k] >= 0 && (REC || (rk[k] >> 28) == c.part_region)) ++n;
             float4 o0[RB][SEGS], o1[RB][SEGS];
             float mp[RB][SEGS], lp[RB][SEGS];
 #pragma unroll
-            for (int k = 0; k < RB; ++k) {
-                if (k < n) {
+            for (int kk = 0; kk < RB; ++kk) {
+                int mine = rk[kk * G];
+#pragma unroll
+                for (int g = 1; g < G; ++g)
+                    if (grp == g) mine = rk[kk * G + g];
+                if (kk * G + grp < n) {
 #pragma unroll
                     for (int sg = 0; sg < SEGS; ++sg) {
                         const float* rec =
-                            c.part + ((static_cast<long long>(rr[k] & 0x0FFFFFFF) * SEGS + sg) * c.H + h) * (HD + 4);
-                        o0[k][sg] = __ldg(reinterpret_cast<const float4*>(rec + col));
-                        o1[k][sg] = __ldg(reinterpret_cast<const float4*>(rec + col + 4));
-                        mp[k][sg] = __ldg(rec + HD);
-                        lp[k][sg] = __ldg(rec + HD + 1);
+                            c.part + ((static_cast<long long>(mine & 0x0FFFFFFF) * SEGS + sg) * c.H + h) * (HD + 4);
+                        o0[kk][sg] = __ldg(reinterpret_cast<const float4*>(rec + col));
+                        o1[kk][sg] = __ldg(reinterpret_cast<const float4*>(rec + col + 4));
+                        mp[kk][sg] = __ldg(rec + HD);
+                        lp[kk][sg] = __ldg(rec + HD + 1);
                     }
                 }
             }
             blk += n * kWarps;
             if (blk < blk_end) ref_next = __ldg(refs + blk);
 #pragma unroll
-            for (int k = 0; k < RB; ++k) {
-                if (k < n) {
+            for (int kk = 0; kk < RB; ++kk) {
+                if (kk * G + grp < n) {
 #pragma unroll
                     for (int sg = 0; sg < SEGS; ++sg) {
-                        const float m_new = fmaxf(m, mp[k][sg]);
+                        const float m_new = fmaxf(m, mp[kk][sg]);
                         const float corr = exp2f(m - m_new);
-                        // one token group adds the record (the fold below sums the groups)
-                        const float f = grp == 0 ? exp2f(mp[k][sg] - m_new) : 0.f;
-                        l = l * corr + lp[k][sg] * f;
-                        acc[0] = acc[0] * corr + o0[k][sg].x * f;
-                        acc[1] = acc[1] * corr + o0[k][sg].y * f;
-                        acc[2] = acc[2] * corr + o0[k][sg].z * f;
-                        acc[3] = acc[3] * corr + o0[k][sg].w * f;
-                        acc[4] = acc[4] * corr + o1[k][sg].x * f;
-                        acc[5] = acc[5] * corr + o1[k][sg].y * f;
-                        acc[6] = acc[6] * corr + o1[k][sg].z * f;
-                        acc[7] = acc[7] * corr + o1[k][sg].w * f;
+                        const float f = exp2f(mp[kk][sg] - m_new);
+                        l = l * corr + lp[kk][sg] * f;
+                        acc[0] = acc[0] * corr + o0[kk][sg].x * f;
+                        acc[1] = acc[1] * corr + o0[kk][sg].y * f;
+                        acc[2] = acc[2] * corr + o0[kk][sg].z * f;
+                        acc[3] = acc[3] * corr + o0[kk][sg].w * f;
+                        acc[4] = acc[4] * corr + o1[kk][sg].x * f;
+                        acc[5] = acc[5] * corr + o1[kk][sg].y * f;
+                        acc[6] = acc[6] * corr + o1[kk][sg].z * f;
+                        acc[7] = acc[7] * corr + o1[kk][sg].w * f;
                         m = m_new;
                     }
                 }
@@ -221,7 +225,18 @@ __global__ void __launch_bounds__(kWarps * 32)
             }
     }
 
-    // fold token groups of the warp (all share m)
+    // fold the token groups of the warp: each lane's (m, l, acc) is self-consistent
+    // (records give the groups different maxima), so rescale to the warp max first
+    {
+        float M = m;
+#pragma unroll
+        for (int o = LPT; o < 32; o <<= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+        const float f = exp2f(m - M);  // m = -FLT_MAX (nothing merged) -> 0, or 1 when M is too
+        l *= f;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[j] *= f;
+        m = M;
+    }
 #pragma unroll
     for (int o = LPT; o < 32; o <<= 1) {
         l += __shfl_xor_sync(0xffffffffu, l, o);
