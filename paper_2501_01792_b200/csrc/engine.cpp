@@ -275,11 +275,15 @@ struct Engine::Impl {
     }
     // qkv [T x 3dg] = LN1(x) . Wqkv (+ b_qkv) for this rank's heads
     // (qkv_generate, decoder.cpp:97-103)
+    // q_only: the Q columns alone (rows 0..dg of Wqkv^T) into the same [T x 3dg]
+    // layout — a fused decode step whose new tokens all land in ACT blocks gets
+    // their K|V from the recompute, so the K|V thirds of the weights need not stream
     void qkv(const f16* W, const f16* xa, int T, f16* out, cudaStream_t st,
-             const GemmScratch& sc = GemmScratch{}) const {
+             const GemmScratch& sc = GemmScratch{}, bool q_only = false) const {
         // no programmatic launch: QKV may follow a cross-stream event wait
         const GemmScratch s{sc.ws, sc.floats, 0};
-        gemm_rows(gemm::kStore, xa, T, d, W + off.wqkv, 3 * dg, out, 3 * dg, st, 0, s, bias(W, off.bqkv));
+        gemm_rows(gemm::kStore, xa, T, d, W + off.wqkv, (q_only ? 1 : 3) * dg, out, 3 * dg, st, 0, s,
+                  bias(W, off.bqkv));
     }
     // project_ffn (decoder.cpp:113-121) of T attention rows [T x dg]; kArchOpt
     // adds the biases, the two residuals (x, then x') and LN2. Head-sharded:
@@ -1645,7 +1649,9 @@ void Engine::decode_step(const std::vector<std::string>& ids_in, const int* toke
                     };
                     if (!m.fused) recompute();
                     m.span_begin(profile_, s_compute_, 2);
-                    m.qkv(W, xa, nb, qkvb, s_compute_, m.scratch());
+                    // every new token of the unit goes to an ACT block: the fused recompute
+                    // produces its K|V from the appended X row, QKV needs only Q
+                    m.qkv(W, xa, nb, qkvb, s_compute_, m.scratch(), m.fused && !U.any_kv && U.any_act);
                     m.span_end(profile_, s_compute_);
                     if (m.fused) recompute();
                     if (U.any_kv) {  // new token's K|V -> its KV slot (device + host)
