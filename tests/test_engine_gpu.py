@@ -1165,3 +1165,21 @@ def test_engine_minibatched_decode_matches_oracle(native, weights_on_device, gra
     res = eng.decode_step(ids, toks, want_x=True)
     assert eng.last_stats()["minibatches"] == 1
     eng.close()
+
+
+@pytest.mark.parametrize("env", [{"HC_WSTREAM": "0"}, {"HC_PREFILL_PTMEM": "0"}, {"HC_PREFILL_PTMEM": "2"}])
+def test_engine_kernel_alternatives_match_oracle(native, env):
+    """The A/B knobs' alternative kernels stay correct: decode-batch GEMMs on the
+    tile kernel + split-K instead of wstream, prefill attention with P in smem
+    (or in TMEM at head_dim 64 too). The knobs are read once per process, so the
+    engine parity tests run again in a child process with the knob set."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
+                        os.path.join(root, "tests", "test_engine_gpu.py"),
+                        "-k", "resident_act_only or hybrid_offloaded or opt_arch or large_batches"],
+                       env=dict(os.environ, **env), capture_output=True, text=True, timeout=900, cwd=root)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+    assert " passed" in r.stdout and "failed" not in r.stdout
