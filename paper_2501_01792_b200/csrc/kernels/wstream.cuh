@@ -20,7 +20,11 @@
 //   * a unit cut between CTAs leaves one fp32 partial per segment; a small
 //     reduce kernel (launched programmatically dependent, so its launch hides
 //     under the GEMM's tail) sums them in a fixed order — deterministic, and
-//     spread over every SM instead of serialised on one contributor.
+//     spread over every SM instead of serialised on one contributor;
+//   * launched with programmatic stream serialisation (GemmCall::pdl) the GEMM
+//     requests its first S stages of W before griddepcontrol.wait — weights
+//     never depend on the predecessor — so the weight stream starts under the
+//     previous kernel's tail; the batch operand, residual and stores wait.
 //
 // Roles (192 threads) as in gemm.cuh: warp 0 TMA producer, warp 1 TMEM
 // allocator + MMA issuer, warps 2..5 epilogue (TMEM lane quarter = warp % 4,
